@@ -1,0 +1,156 @@
+// build_csr.cu — row a1: CSR of the undirected simple graph.
+//
+// Edge pairs -> 64-bit keys (u<<32 | v) for both directions (self loops become a
+// sentinel row n) -> CUB radix sort -> unique -> rowptr by per-row binary search.
+// Deterministic and bit-exact (integer work only).
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace netmfp {
+
+__global__ void k_make_keys(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
+                            int64_t m, uint64_t n, uint64_t *__restrict__ keys, int *bad) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  int32_t s = src[e], t = dst[e];
+  if (s < 0 || t < 0 || (uint64_t)s >= n || (uint64_t)t >= n) {
+    atomicExch(bad, 1);
+    keys[2 * e] = keys[2 * e + 1] = n << 32;
+    return;
+  }
+  if (s == t) {  // self loop: dropped (sentinel row n sorts last)
+    keys[2 * e] = keys[2 * e + 1] = n << 32;
+  } else {
+    keys[2 * e] = ((uint64_t)s << 32) | (uint32_t)t;
+    keys[2 * e + 1] = ((uint64_t)t << 32) | (uint32_t)s;
+  }
+}
+
+// rowptr[u] = first key index with row >= u (lower bound), u in [0, n]
+__global__ void k_rowptr(const uint64_t *__restrict__ keys, int64_t nnz, int64_t n,
+                         int64_t *__restrict__ rowptr) {
+  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u > n) return;
+  uint64_t target = (uint64_t)u << 32;
+  int64_t lo = 0, hi = nnz;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  rowptr[u] = lo;
+}
+
+__global__ void k_col_deg(const uint64_t *__restrict__ keys, int64_t nnz,
+                          const int64_t *__restrict__ rowptr, int64_t n, int32_t *__restrict__ col,
+                          int32_t *__restrict__ deg, uint8_t *__restrict__ heavy_flag) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < nnz) col[i] = (int32_t)(keys[i] & 0xFFFFFFFFu);
+  if (i < n) {
+    int64_t dg = rowptr[i + 1] - rowptr[i];
+    deg[i] = (int32_t)dg;
+    heavy_flag[i] = dg > kLightCap ? 1 : 0;
+  }
+}
+
+__global__ void k_heavy_segs(const int32_t *__restrict__ heavy, int64_t nh,
+                             const int32_t *__restrict__ deg, int64_t *__restrict__ nseg) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < nh) nseg[i] = (deg[heavy[i]] + kHeavySeg - 1) / kHeavySeg;
+  if (i == nh) nseg[i] = 0;
+}
+
+static int bits_for(uint64_t v) {
+  int b = 0;
+  while ((1ull << b) <= v && b < 63) ++b;
+  return b;
+}
+
+Graph *build_csr_device(Ctx &c, int64_t n, const int32_t *src, const int32_t *dst, int64_t m) {
+  NM_REQUIRE(n > 0 && n < (1ll << 31), "build_csr: need 0 < n < 2^31");
+  NM_REQUIRE(m >= 0, "build_csr: m_in < 0");
+  cudaStream_t s = c.stream;
+  auto g = new Graph();
+  g->n = n;
+  g->device = c.device;
+  try {
+    int64_t nk = 2 * m;
+    DBuf<uint64_t> keys(nk > 0 ? nk : 1, s), keys2(nk > 0 ? nk : 1, s);
+    DBuf<int> bad(1, s);
+    bad.zero();
+    if (m > 0) {
+      NM_LAUNCH(c, "make_keys", k_make_keys<<<ceil_div(m, 256), 256, 0, s>>>(src, dst, m, (uint64_t)n, keys, bad));
+    }
+    int end_bit = 32 + bits_for((uint64_t)n);
+    size_t tmp_bytes = 0, tmp2 = 0;
+    DBuf<int64_t> nsel(1, s);
+    if (nk > 0) {
+      NM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys.p, keys2.p, nk, 0, end_bit, s));
+      NM_CUDA(cub::DeviceSelect::Unique(nullptr, tmp2, keys2.p, keys.p, nsel.p, nk, s));
+      DBuf<char> tmp(std::max(tmp_bytes, tmp2), s);
+      NM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, keys.p, keys2.p, nk, 0, end_bit, s));
+      c.launches += 4;
+      NM_CUDA(cub::DeviceSelect::Unique(tmp.p, tmp2, keys2.p, keys.p, nsel.p, nk, s));
+      c.launches += 2;
+    } else {
+      nsel.zero();
+    }
+    int64_t nuniq = 0;
+    int hbad = 0;
+    NM_CUDA(cudaMemcpyAsync(&nuniq, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    NM_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    NM_CUDA(cudaStreamSynchronize(s));
+    NM_REQUIRE(!hbad, "build_csr: vertex id out of [0, n)");
+    // drop the sentinel (row n) if present: it is the last unique key
+    int64_t nnz = nuniq;
+    if (nnz > 0) {
+      uint64_t last = 0;
+      NM_CUDA(cudaMemcpyAsync(&last, keys.p + nnz - 1, 8, cudaMemcpyDeviceToHost, s));
+      NM_CUDA(cudaStreamSynchronize(s));
+      if ((last >> 32) == (uint64_t)n) --nnz;
+    }
+    g->nnz = nnz;
+    g->rowptr.alloc(n + 1, s);
+    g->col.alloc(nnz > 0 ? nnz : 1, s);
+    g->deg.alloc(n, s);
+    DBuf<uint8_t> hflag(n, s);
+    NM_LAUNCH(c, "rowptr", k_rowptr<<<ceil_div(n + 1, 256), 256, 0, s>>>(keys, nnz, n, g->rowptr));
+    int64_t mx = std::max(nnz, n);
+    NM_LAUNCH(c, "col_deg", k_col_deg<<<ceil_div(mx, 256), 256, 0, s>>>(keys, nnz, g->rowptr, n, g->col, g->deg, hflag));
+    // heavy rows (degree > kLightCap) for the split SpMM path
+    {
+      DBuf<int32_t> hv(n, s);
+      size_t tb = 0;
+      cub::CountingInputIterator<int32_t> it(0);
+      NM_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, hflag.p, hv.p, nsel.p, n, s));
+      DBuf<char> tmp(tb, s);
+      NM_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, it, hflag.p, hv.p, nsel.p, n, s));
+      c.launches += 2;
+      int64_t nh = 0;
+      NM_CUDA(cudaMemcpyAsync(&nh, nsel.p, 8, cudaMemcpyDeviceToHost, s));
+      NM_CUDA(cudaStreamSynchronize(s));
+      g->n_heavy = nh;
+      g->heavy.alloc(nh > 0 ? nh : 1, s);
+      if (nh > 0)
+        NM_CUDA(cudaMemcpyAsync(g->heavy.p, hv.p, nh * 4, cudaMemcpyDeviceToDevice, s));
+      g->heavy_seg_ptr.alloc(nh + 1, s);
+      DBuf<int64_t> nseg(nh + 1, s);
+      NM_LAUNCH(c, "heavy_segs", k_heavy_segs<<<ceil_div(nh + 1, 256), 256, 0, s>>>(g->heavy, nh, g->deg, nseg));
+      size_t tb2 = 0;
+      NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, nseg.p, g->heavy_seg_ptr.p, nh + 1, s));
+      DBuf<char> tmp2b(tb2, s);
+      NM_CUDA(cub::DeviceScan::ExclusiveSum(tmp2b.p, tb2, nseg.p, g->heavy_seg_ptr.p, nh + 1, s));
+      c.launches += 1;
+      int64_t nsegs = 0;
+      NM_CUDA(cudaMemcpyAsync(&nsegs, g->heavy_seg_ptr.p + nh, 8, cudaMemcpyDeviceToHost, s));
+      NM_CUDA(cudaStreamSynchronize(s));
+      g->n_heavy_segs = nsegs;
+    }
+  } catch (...) {
+    delete g;
+    throw;
+  }
+  return g;
+}
+
+}  // namespace netmfp

@@ -1,0 +1,259 @@
+// common.cuh — shared plumbing of libnetmfp (context, errors, buffers, RNG).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/netmfp.h"
+
+namespace netmfp {
+
+// ----------------------------------------------------------------------------
+// errors: internal code throws netmfp::Error; the C ABI converts to codes.
+// ----------------------------------------------------------------------------
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string &msg);
+
+#define NM_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t _e = (call);                                                           \
+    if (_e != cudaSuccess) {                                                           \
+      throw ::netmfp::Error(_e == cudaErrorMemoryAllocation ? NETMFP_ERR_OOM           \
+                                                            : NETMFP_ERR_CUDA,         \
+                            std::string(#call) + ": " + cudaGetErrorString(_e) +       \
+                                " (" __FILE__ ":" + std::to_string(__LINE__) + ")");  \
+    }                                                                                  \
+  } while (0)
+
+#define NM_REQUIRE(cond, msg)                                        \
+  do {                                                               \
+    if (!(cond)) throw ::netmfp::Error(NETMFP_ERR_ARG, (msg));       \
+  } while (0)
+
+// ----------------------------------------------------------------------------
+// context
+// ----------------------------------------------------------------------------
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  int64_t launches = 0;
+  int *d_flags = nullptr;  // device status flags (numeric breakdown counters)
+  // per-kernel CUDA-event profiling (netmfp_ctx_profile): events around each
+  // launch whose name matches one of the comma-separated filter prefixes
+  bool prof = false;
+  std::string prof_filter;
+  struct PEv {
+    cudaEvent_t a, b;
+    const char *name;
+  };
+  std::vector<PEv> pending;
+  std::vector<cudaEvent_t> evpool;
+  cudaEvent_t cur_a = nullptr;
+  const char *cur_name = nullptr;
+  std::vector<std::pair<std::string, std::pair<int64_t, double>>> stats;
+};
+
+inline bool prof_match(const Ctx &c, const char *name) {
+  if (c.prof_filter.empty()) return true;
+  size_t st = 0;
+  const std::string n(name);
+  while (st <= c.prof_filter.size()) {
+    size_t e = c.prof_filter.find(',', st);
+    if (e == std::string::npos) e = c.prof_filter.size();
+    std::string tok = c.prof_filter.substr(st, e - st);
+    if (!tok.empty() && n.compare(0, tok.size(), tok) == 0) return true;
+    st = e + 1;
+  }
+  return false;
+}
+
+inline cudaEvent_t prof_event(Ctx &c) {
+  if (c.evpool.empty()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = c.evpool.back();
+  c.evpool.pop_back();
+  return e;
+}
+
+inline void prof_begin(Ctx &c, const char *name) {
+  c.cur_name = nullptr;
+  if (!c.prof || !prof_match(c, name)) return;
+  c.cur_a = prof_event(c);
+  cudaEventRecord(c.cur_a, c.stream);
+  c.cur_name = name;
+}
+
+// count + check a kernel launch (and close its profiling interval)
+inline void launched(Ctx &c, const char *what) {
+  c.launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    throw Error(NETMFP_ERR_CUDA, std::string("launch ") + what + ": " + cudaGetErrorString(e));
+  if (c.cur_name) {
+    cudaEvent_t b = prof_event(c);
+    cudaEventRecord(b, c.stream);
+    c.pending.push_back({c.cur_a, b, c.cur_name});
+    c.cur_name = nullptr;
+  }
+}
+
+// fold finished intervals into per-kernel (count, total ms); stream must be idle
+inline void prof_collect(Ctx &c) {
+  for (auto &pe : c.pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, pe.a, pe.b);
+    bool found = false;
+    for (auto &s : c.stats)
+      if (s.first == pe.name) {
+        s.second.first += 1;
+        s.second.second += ms;
+        found = true;
+        break;
+      }
+    if (!found) c.stats.push_back({pe.name, {1, (double)ms}});
+    c.evpool.push_back(pe.a);
+    c.evpool.push_back(pe.b);
+  }
+  c.pending.clear();
+}
+
+#define NM_LAUNCH(c, name, ...)   \
+  do {                            \
+    ::netmfp::prof_begin(c, name); \
+    __VA_ARGS__;                  \
+    ::netmfp::launched(c, name);  \
+  } while (0)
+
+// stream-ordered device buffer (cudaMallocAsync pool; freed on scope exit)
+template <class T>
+struct DBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count) NM_CUDA(cudaMallocAsync((void **)&p, count * sizeof(T), st));
+  }
+  void zero() {
+    if (n) NM_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  T *get() const { return p; }
+  operator T *() const { return p; }
+  DBuf(const DBuf &) = delete;
+  DBuf &operator=(const DBuf &) = delete;
+  DBuf(DBuf &&o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf &operator=(DBuf &&o) noexcept {
+    release();
+    p = o.p; n = o.n; s = o.s;
+    o.p = nullptr; o.n = 0;
+    return *this;
+  }
+  ~DBuf() { release(); }
+};
+
+// Dense fp32 block view: rows × cols, row-major, leading dimension ld.
+struct Mat {
+  float *p = nullptr;
+  int64_t rows = 0, cols = 0, ld = 0;
+  float *row(int64_t i) const { return p + i * ld; }
+};
+
+inline int64_t pad4(int64_t c) { return (c + 3) / 4 * 4; }
+inline int64_t pad32(int64_t c) { return (c + 31) / 32 * 32; }
+
+// Owned dense fp32 block with ld padded to a multiple of 32 floats (128 B rows
+// segments) and zeroed padding.
+struct Block {
+  DBuf<float> buf;
+  Mat m;
+  Block() = default;
+  Block(int64_t rows, int64_t cols, cudaStream_t s) { alloc(rows, cols, s); }
+  void alloc(int64_t rows, int64_t cols, cudaStream_t s) {
+    int64_t ld = pad32(cols);
+    buf.alloc((size_t)rows * ld, s);
+    buf.zero();
+    m.p = buf.p;
+    m.rows = rows;
+    m.cols = cols;
+    m.ld = ld;
+  }
+  operator Mat() const { return m; }
+};
+
+// ----------------------------------------------------------------------------
+// graph (device CSR)
+// ----------------------------------------------------------------------------
+struct Graph {
+  int64_t n = 0, nnz = 0;
+  DBuf<int64_t> rowptr;   // n+1
+  DBuf<int32_t> col;      // nnz
+  DBuf<int32_t> deg;      // n
+  DBuf<int32_t> heavy;    // rows with degree > kLightCap, ascending
+  int64_t n_heavy = 0;
+  int64_t heavy_nnz = 0;
+  DBuf<int64_t> heavy_seg_ptr;  // per heavy row: first segment index (n_heavy+1)
+  int64_t n_heavy_segs = 0;
+  int device = 0;
+};
+
+// rows with more neighbours than this are split across warps (spmm.cu)
+constexpr int kLightCap = 512;
+constexpr int kHeavySeg = 512;
+
+// ----------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al. SC'11) — the CUDA side's own implementation of
+// the counter-based generator named in DESIGN.md [R1].
+// ----------------------------------------------------------------------------
+struct U4 {
+  uint32_t x, y, z, w;
+};
+
+__host__ __device__ inline U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * c.x;
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    U4 o;
+    o.x = hi1 ^ c.y ^ k0;
+    o.y = lo1;
+    o.z = hi0 ^ c.w ^ k1;
+    o.w = lo0;
+    c = o;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+constexpr uint32_t kTagOmega = 0x4F4D4547u;
+constexpr uint32_t kTagPsi = 0x50534931u;
+constexpr uint32_t kTagPi = 0x50493132u;
+
+inline unsigned ceil_div(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+
+}  // namespace netmfp

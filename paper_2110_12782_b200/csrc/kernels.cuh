@@ -1,0 +1,92 @@
+// kernels.cuh — internal interfaces between the .cu translation units.
+#pragma once
+#include "common.cuh"
+
+namespace netmfp {
+
+// ---- build_csr.cu
+Graph *build_csr_device(Ctx &c, int64_t n, const int32_t *src, const int32_t *dst, int64_t m);
+
+// ---- spmm.cu
+struct SpmmArgs {
+  const float *X = nullptr;
+  int64_t ldx = 0;
+  float *Y = nullptr;  // may be null (only acc_out written)
+  int64_t ldy = 0;
+  int64_t cols = 0;
+  float a = 0.f;                 // row scale d_u^-a (computed from rowptr)
+  const float *s_col = nullptr;  // optional column scale vector (n), e.g. d_v^-b
+  float coef = 1.f;              // y = coef * rs * sum + beta * prev
+  const float *prev = nullptr;
+  int64_t ldp = 0;
+  float beta = 0.f;
+  const float *acc_in = nullptr;  // acc_out = acc_scale * acc_in + gamma * y
+  int64_t ldai = 0;
+  float *acc_out = nullptr;
+  int64_t ldacc = 0;
+  float acc_scale = 0.f;
+  float gamma = 0.f;
+};
+void spmm(Ctx &c, const Graph &g, const SpmmArgs &p);
+void deg_pow(Ctx &c, const Graph &g, float e, float *out);  // out[i] = d_i^-e (0 if d_i = 0)
+
+// ---- dense.cu (tall-skinny fp32 blocks, fp64 small results)
+// G[a×b] (fp64, row-major ldg) = Σ_i w_i A[i,:a]ᵀ B[i,:b]; w optional (row weight
+// d_i^-e when wexp != 0, computed from deg).  If A == B and a == b only the
+// upper triangle is computed and mirrored.
+void gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg);
+// C[n×b] = rs_i · (A[n×a] · Bs[a×b]) with Bs fp64 small (converted to fp32),
+// rs_i = d_i^-e (e = rexp, deg != null) else 1.
+void gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcols, const int32_t *deg,
+               float rexp, const Mat &C);
+// Ω = randn(n, l) from Philox [R1], row-scaled by d_i^-e (deg != null)
+void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, float rexp);
+// Y[i, :] *= d_i^-e
+void row_scale_block(Ctx &c, const Mat &Y, const int32_t *deg, float rexp);
+// copy with ld conversion (device-to-device)
+void copy_block(Ctx &c, const float *src, int64_t lds, float *dst, int64_t ldd, int64_t rows,
+                int64_t cols);
+
+// ---- small.cu (fp64 small dense, row-major, single-CTA or few-CTA kernels)
+// In place upper Cholesky: G = Rᵀ R (R in the upper triangle, lower zeroed).
+// On breakdown retries with a diagonal shift (shifted CholeskyQR); increments
+// *flag when a shift was needed and sets *flag |= 1<<30 on failure.
+void cholesky_upper(Ctx &c, double *G, int64_t l, int64_t ld, int *flag);
+// Rinv = R^-1 for upper triangular R (l×l)
+void tri_inv_upper(Ctx &c, const double *R, int64_t ld, double *Rinv, int64_t l);
+// symmetric eigendecomposition (cyclic Jacobi), S overwritten; V (l×l) gets
+// eigenvectors as columns, lam the eigenvalues, both sorted by desc |λ| when
+// abs_order, else by desc λ.
+void sym_eig(Ctx &c, double *S, int64_t l, double *lam, double *V, bool abs_order);
+// C = alpha op(A) op(B) + beta C (fp64 small), op = transpose if flag
+void gemm64(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+            int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc);
+void symmetrize64(Ctx &c, double *S, int64_t l, int64_t ld);
+void scale_cols64(Ctx &c, double *A, int64_t rows, int64_t cols, int64_t ld, const double *s, int mode);
+void set_identity64(Ctx &c, double *A, int64_t l, int64_t ld);
+void axpy64(Ctx &c, int64_t n, double alpha, const double *x, double *y);
+
+// ---- sketch.cu
+struct SparseSign {
+  int64_t n = 0, h = 0, z = 0;
+  DBuf<int32_t> rows;     // h*z (column-major by column j: rows[j*z + t])
+  DBuf<float> signs;      // h*z
+  // CSR over unique coordinates p (ascending): entries (column, sign)
+  int64_t v = 0;
+  DBuf<int32_t> p;        // v
+  DBuf<int32_t> pptr;     // v+1
+  DBuf<int32_t> pcol;     // h*z
+  DBuf<float> psign;      // h*z
+};
+void gen_sparse_sign(Ctx &c, int64_t n, int64_t h, int64_t z, uint64_t seed, uint32_t tag, SparseSign &S);
+// Y[n×h] = f(scale · A Bpᵀ) Ψp   (A: n×k, Bp = rows p of B, both fp32 row-major)
+void sketch_apply(Ctx &c, const Mat &A, const Mat &B, const SparseSign &S, float scale, int logmode,
+                  const Mat &Y);
+// Out[h×cols] (fp64) = Ψᵀ X  (sign-gather of rows of X; X fp32 n×cols)
+void sign_gather_T(Ctx &c, const SparseSign &S, const Mat &X, double *Out, int64_t ldo);
+// Out[h×cols] (fp64) = Ψᵀ X restricted: X row i <-> coordinate p[i] (X has v rows, fp32)
+void sign_gather_T_p(Ctx &c, const SparseSign &S, const Mat &Xp, double *Out, int64_t ldo);
+// gather rows p of X into Xp (v × cols)
+void gather_rows(Ctx &c, const Mat &X, const int32_t *idx, int64_t cnt, const Mat &Out);
+
+}  // namespace netmfp

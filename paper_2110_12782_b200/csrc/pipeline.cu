@@ -1,0 +1,245 @@
+// pipeline.cu — the NetMF+ stages of Alg. 5 on device blocks.
+#include <cmath>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "pipeline.cuh"
+
+namespace netmfp {
+
+static void check_flag(Ctx &c, const char *what) {
+  int h = 0;
+  NM_CUDA(cudaMemcpyAsync(&h, c.d_flags, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  NM_CUDA(cudaStreamSynchronize(c.stream));
+  if (h & (1 << 30)) {
+    NM_CUDA(cudaMemsetAsync(c.d_flags, 0, sizeof(int), c.stream));
+    throw Error(NETMFP_ERR_NUMERIC, std::string(what) +
+                                        ": Gram matrix not positive definite even after shifting "
+                                        "(input not of full column rank, PAPER.md:215)");
+  }
+}
+
+// CholeskyQR (north_star; [R7]): Gram G = YᵀY (fp64), G = RᵀR, out = rs · Y R⁻¹.
+// passes = 2 gives CholeskyQR2 (second pass on the materialised Y R1⁻¹ in tmp).
+void cholqr(Ctx &c, const Mat &Y, const Mat &out, const int32_t *deg, float rexp, int passes,
+            const Mat *tmp) {
+  const int64_t l = Y.cols;
+  cudaStream_t s = c.stream;
+  DBuf<double> G((size_t)l * l, s), Rinv((size_t)l * l, s);
+  Mat cur = Y;
+  for (int ps = 0; ps < passes; ++ps) {
+    gram(c, cur, cur, nullptr, 0.f, G, l);
+    cholesky_upper(c, G, l, l, c.d_flags);
+    tri_inv_upper(c, G, l, Rinv, l);
+    const bool last = (ps + 1 == passes);
+    if (last) {
+      gemm_tall(c, cur, Rinv, l, l, deg, rexp, out);
+    } else {
+      NM_REQUIRE(tmp && tmp->p != cur.p, "cholqr2: needs a scratch block");
+      gemm_tall(c, cur, Rinv, l, l, nullptr, 0.f, *tmp);
+      cur = *tmp;
+    }
+  }
+}
+
+// Alg. 2 freigs(D^-α A D^-α, k, s1, q) with the basis kept pre-scaled
+// (P = D^-α Q) so that every SpMM is an unweighted gather with a row scale:
+//   X Q = D^-α A P;  X X Q = D^-α A (D^-2α A P);  S = Qᵀ X Q = Pᵀ (A P);  U = D^α P Û.
+void freigs(Ctx &c, const Graph &g, double alpha, int k, int s1, int q, uint64_t seed, const Mat &U,
+            double *lam_dev) {
+  const int64_t n = g.n, l = (int64_t)k + s1;
+  NM_REQUIRE(k >= 1 && s1 >= 0 && q >= 0, "eig: need k >= 1, s1 >= 0, q >= 0");
+  NM_REQUIRE(l <= n, "eig: k + s1 must not exceed n (Alg. 2)");
+  NM_REQUIRE(alpha > 0.0 && alpha <= 0.5, "eig: alpha in (0, 0.5] (PAPER.md:217)");
+  cudaStream_t s = c.stream;
+  const float a = (float)alpha;
+  Block P(n, l, s), T(n, l, s), Y(n, l, s);
+  // step 2: Ω = randn(n, l), Y = X Ω
+  gaussian_block(c, P.m, seed, g.deg, a);  // P = D^-α Ω
+  SpmmArgs sp;
+  sp.cols = l;
+  sp.X = P.m.p; sp.ldx = P.m.ld; sp.Y = Y.m.p; sp.ldy = Y.m.ld; sp.a = a;
+  spmm(c, g, sp);
+  // step 3: Q = orth(Y)
+  cholqr(c, Y.m, P.m, g.deg, a, q == 0 ? 2 : 1, &T.m);
+  // steps 4-6: Q = orth(X X Q)
+  for (int it = 0; it < q; ++it) {
+    SpmmArgs s1a;
+    s1a.cols = l;
+    s1a.X = P.m.p; s1a.ldx = P.m.ld; s1a.Y = T.m.p; s1a.ldy = T.m.ld; s1a.a = 2.f * a;
+    spmm(c, g, s1a);  // T = D^-2α A P = D^-α (X Q)
+    SpmmArgs s2a;
+    s2a.cols = l;
+    s2a.X = T.m.p; s2a.ldx = T.m.ld; s2a.Y = Y.m.p; s2a.ldy = Y.m.ld; s2a.a = a;
+    spmm(c, g, s2a);  // Y = D^-α A T = X X Q
+    cholqr(c, Y.m, P.m, g.deg, a, it + 1 == q ? 2 : 1, &T.m);
+  }
+  check_flag(c, "freigs orthonormalisation");
+  // step 7: S = Qᵀ X Q = Pᵀ A P
+  SpmmArgs s3;
+  s3.cols = l;
+  s3.X = P.m.p; s3.ldx = P.m.ld; s3.Y = T.m.p; s3.ldy = T.m.ld; s3.a = 0.f;
+  spmm(c, g, s3);
+  DBuf<double> S((size_t)l * l, s), lam(l, s), V((size_t)l * l, s);
+  gram(c, P.m, T.m, nullptr, 0.f, S, l);
+  symmetrize64(c, S, l, l);
+  // step 8: [Û, Λ] = eig(S), ordered by |λ| [R3]
+  sym_eig(c, S, l, lam, V, true);
+  // step 9-10: U = Q Û(:, 1:k) = D^α P Û(:, 1:k)
+  gemm_tall(c, P.m, V, l, k, g.deg, -a, U);
+  NM_CUDA(cudaMemcpyAsync(lam_dev, lam.p, (size_t)k * 8, cudaMemcpyDeviceToDevice, s));
+}
+
+// Eq. 3 / Alg. 5 steps 2-3
+void factor_pair(Ctx &c, const Graph &g, double alpha, int T, const Mat &U, const double *lam, int k,
+                 const Mat &F, double *C) {
+  NM_REQUIRE(T >= 1, "factor_pair: T >= 1");
+  cudaStream_t s = c.stream;
+  DBuf<double> K((size_t)k * k, s), Pw((size_t)k * k, s), Pn((size_t)k * k, s), acc((size_t)k * k, s);
+  // K = Uᵀ D^(-1+2α) U Λ
+  gram(c, U, U, g.deg, (float)(1.0 - 2.0 * alpha), K, k);
+  scale_cols64(c, K, k, k, k, lam, 0);
+  // Σ_{r=1}^T K^(r-1)
+  set_identity64(c, acc, k, k);
+  set_identity64(c, Pw, k, k);
+  for (int r = 2; r <= T; ++r) {
+    gemm64(c, false, false, k, k, k, 1.0, Pw, k, K, k, 0.0, Pn, k);
+    std::swap(Pw.p, Pn.p);
+    axpy64(c, (int64_t)k * k, 1.0, Pw, acc);
+  }
+  // C = Λ · acc
+  NM_CUDA(cudaMemcpyAsync(C, acc.p, (size_t)k * k * 8, cudaMemcpyDeviceToDevice, s));
+  scale_cols64(c, C, k, k, k, lam, 1);
+  // F = D^(-1+α) U
+  copy_block(c, U.p, U.ld, F.p, F.ld, U.rows, U.cols);
+  row_scale_block(c, F, g.deg, (float)(1.0 - alpha));
+}
+
+__global__ void k_sqrt_abs(const double *lam, int d, double *out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < d) out[i] = sqrt(fabs(lam[i]));
+}
+__global__ void k_abs(const double *lam, int d, double *out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < d) out[i] = fabs(lam[i]);
+}
+
+// Alg. 4
+void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int d, int s2, int s3, int z,
+                uint64_t seed, int logmode, const Mat *Uout, double *sigma_dev, const Mat *Eout,
+                const Mat *Yout, double *Zout) {
+  const int64_t n = F.rows;
+  const int64_t h2 = (int64_t)d + s2, h3 = (int64_t)d + s3;
+  NM_REQUIRE(d >= 1 && s2 >= 0 && s3 >= 0, "sketch_svd: need d >= 1, s2, s3 >= 0");
+  NM_REQUIRE(h2 <= n && h3 <= n * (int64_t)z, "sketch_svd: d + s2 must not exceed n");
+  NM_REQUIRE(h3 >= h2, "sketch_svd: need s3 >= s2 (PAPER.md:413)");
+  cudaStream_t s = c.stream;
+  const float fs = (float)scale;
+  // step 2: Ψ
+  SparseSign Psi;
+  gen_sparse_sign(c, n, h2, z, seed, kTagPsi, Psi);
+  // FC = F · C
+  Block FC(n, k, s);
+  gemm_tall(c, F, C, k, k, nullptr, 0.f, FC.m);
+  // step 3: Y = f(scale F C F(p,:)ᵀ) Ψ
+  Block Y(n, h2, s), Qb(n, h2, s), Tb(n, h2, s);
+  sketch_apply(c, FC.m, F, Psi, fs, logmode, Y.m);
+  if (Yout) copy_block(c, Y.m.p, Y.m.ld, Yout->p, Yout->ld, n, h2);
+  // step 4: Q = orth(Y)   (CholeskyQR2 [R7])
+  cholqr(c, Y.m, Qb.m, nullptr, 0.f, 2, &Tb.m);
+  check_flag(c, "single-pass SVD orth(Y)");
+  // step 5: Π
+  SparseSign Pi;
+  gen_sparse_sign(c, n, h3, z, seed, kTagPi, Pi);
+  // step 6: Z = Πᵀ f(scale F(p,:) C F(p,:)ᵀ) Π
+  Block FpC(Pi.v, k, s), H(Pi.v, h3, s);
+  gather_rows(c, FC.m, Pi.p, Pi.v, FpC.m);
+  sketch_apply(c, FpC.m, F, Pi, fs, logmode, H.m);
+  DBuf<double> Z((size_t)h3 * h3, s), PtQ((size_t)h3 * h2, s);
+  sign_gather_T_p(c, Pi, H.m, Z, h3);
+  if (Zout) NM_CUDA(cudaMemcpyAsync(Zout, Z.p, (size_t)h3 * h3 * 8, cudaMemcpyDeviceToDevice, s));
+  // step 7: S = (ΠᵀQ)† Z (QᵀΠ)†  via the normal equations in fp64
+  sign_gather_T(c, Pi, Qb.m, PtQ, h2);
+  DBuf<double> N((size_t)h2 * h2, s), Ninv((size_t)h2 * h2, s), Rinv((size_t)h2 * h2, s);
+  DBuf<double> W((size_t)h2 * h3, s), WZ((size_t)h2 * h3, s), S((size_t)h2 * h2, s);
+  gemm64(c, true, false, h2, h2, h3, 1.0, PtQ, h2, PtQ, h2, 0.0, N, h2);  // N = AᵀA
+  cholesky_upper(c, N, h2, h2, c.d_flags);
+  tri_inv_upper(c, N, h2, Rinv, h2);
+  gemm64(c, false, true, h2, h2, h2, 1.0, Rinv, h2, Rinv, h2, 0.0, Ninv, h2);  // (AᵀA)⁻¹
+  gemm64(c, false, true, h2, h3, h2, 1.0, Ninv, h2, PtQ, h2, 0.0, W, h3);      // A† = (AᵀA)⁻¹Aᵀ
+  gemm64(c, false, false, h2, h3, h3, 1.0, W, h3, Z, h3, 0.0, WZ, h3);
+  gemm64(c, false, true, h2, h2, h3, 1.0, WZ, h3, W, h3, 0.0, S, h2);
+  symmetrize64(c, S, h2, h2);
+  check_flag(c, "single-pass SVD core solve");
+  // step 8: svd(S) of the symmetric core = eig with |λ| ordering
+  DBuf<double> lam(h2, s), V((size_t)h2 * h2, s), sq(d, s);
+  sym_eig(c, S, h2, lam, V, true);
+  if (sigma_dev) {
+    NM_LAUNCH(c, "abs", k_abs<<<ceil_div(d, 128), 128, 0, s>>>(lam, d, sigma_dev));
+  }
+  // step 9: U = Q Û(:, 1:d);  Alg. 5 step 5: E = U √Σ
+  if (Uout) gemm_tall(c, Qb.m, V, h2, d, nullptr, 0.f, *Uout);
+  if (Eout) {
+    NM_LAUNCH(c, "sqrt_abs", k_sqrt_abs<<<ceil_div(d, 128), 128, 0, s>>>(lam, d, sq));
+    DBuf<double> Vs((size_t)h2 * d, s);
+    NM_CUDA(cudaMemcpy2DAsync(Vs.p, d * 8, V.p, h2 * 8, d * 8, h2, cudaMemcpyDeviceToDevice, s));
+    scale_cols64(c, Vs, h2, d, d, sq, 0);
+    gemm_tall(c, Qb.m, Vs, d, d, nullptr, 0.f, *Eout);
+  }
+}
+
+// Chebyshev coefficients of the band-pass kernel [R6] (host, fp64)
+void cheb_coeffs(int order, double mu, double theta, double *c) {
+  const int N = 256;
+  const double PI = 3.14159265358979323846;
+  for (int r = 0; r <= order; ++r) {
+    double sacc = 0.0;
+    for (int j = 0; j < N; ++j) {
+      double t = PI * (j + 0.5) / N;
+      double x = std::cos(t);
+      double lam = x + 1.0;
+      double g = std::exp(-0.5 * ((lam - mu) * (lam - mu) - 1.0) * theta);
+      sacc += g * std::cos(r * t);
+    }
+    c[r] = 2.0 / N * sacc;
+  }
+  c[0] *= 0.5;
+  const double c0 = c[0];
+  for (int r = 0; r <= order; ++r) c[r] /= c0;
+}
+
+// E <- Σ_r c_r T_r(L~) E, L~ = -D^-1 A; Z_{r+1} = 2 L~ Z_r - Z_{r-1} fused in the SpMM
+// epilogue together with Acc += c_{r+1} Z_{r+1}.  E is used as Z_0 storage.
+void propagate(Ctx &c, const Graph &g, const Mat &E, int order, double mu, double theta) {
+  if (order <= 0) return;
+  NM_REQUIRE(order <= 64, "propagate: order <= 64");
+  std::vector<double> cf(order + 1);
+  cheb_coeffs(order, mu, theta, cf.data());
+  cudaStream_t s = c.stream;
+  const int64_t n = E.rows, d = E.cols;
+  Block Z1(n, d, s), Acc(n, d, s);
+  // Z_1 = L~ E = -D^-1 A E ;  Acc = c0 E + c1 Z_1
+  SpmmArgs a;
+  a.cols = d;
+  a.X = E.p; a.ldx = E.ld; a.Y = Z1.m.p; a.ldy = Z1.m.ld; a.a = 1.f; a.coef = -1.f;
+  a.acc_in = E.p; a.ldai = E.ld; a.acc_out = Acc.m.p; a.ldacc = Acc.m.ld;
+  a.acc_scale = (float)cf[0]; a.gamma = (float)cf[1];
+  spmm(c, g, a);
+  // Z_0 lives in E, Z_1 in Z1; Z_{r} overwrites Z_{r-2} in place
+  Mat zprev = E, zcur = Z1.m;
+  for (int r = 2; r <= order; ++r) {
+    SpmmArgs b;
+    b.cols = d;
+    b.X = zcur.p; b.ldx = zcur.ld;
+    b.Y = zprev.p; b.ldy = zprev.ld;
+    b.prev = zprev.p; b.ldp = zprev.ld; b.beta = -1.f;
+    b.a = 1.f; b.coef = -2.f;
+    b.acc_in = Acc.m.p; b.ldai = Acc.m.ld; b.acc_out = Acc.m.p; b.ldacc = Acc.m.ld; b.acc_scale = 1.f;
+    b.gamma = (float)cf[r];
+    spmm(c, g, b);
+    std::swap(zprev, zcur);
+  }
+  copy_block(c, Acc.m.p, Acc.m.ld, E.p, E.ld, n, d);
+}
+
+}  // namespace netmfp

@@ -1,0 +1,16 @@
+// pipeline.cuh — NetMF+ stages on device blocks (pipeline.cu).
+#pragma once
+#include "common.cuh"
+
+namespace netmfp {
+void cholqr(Ctx &c, const Mat &Y, const Mat &out, const int32_t *deg, float rexp, int passes, const Mat *tmp);
+void freigs(Ctx &c, const Graph &g, double alpha, int k, int s1, int q, uint64_t seed, const Mat &U,
+            double *lam_dev);
+void factor_pair(Ctx &c, const Graph &g, double alpha, int T, const Mat &U, const double *lam, int k,
+                 const Mat &F, double *C);
+void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int d, int s2, int s3, int z,
+                uint64_t seed, int logmode, const Mat *Uout, double *sigma_dev, const Mat *Eout,
+                const Mat *Yout, double *Zout);
+void cheb_coeffs(int order, double mu, double theta, double *c);
+void propagate(Ctx &c, const Graph &g, const Mat &E, int order, double mu, double theta);
+}  // namespace netmfp

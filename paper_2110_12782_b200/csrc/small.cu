@@ -1,0 +1,651 @@
+// small.cu — fp64 dense kernels for the l×l problems of Alg. 2/4 (l <= ~460):
+//   * cholesky_upper  — CholeskyQR's R (north_star; [R7]); left-looking blocked,
+//                       one CTA, 32-column panels in shared memory, device-side
+//                       shifted retry on breakdown
+//   * tri_inv_upper   — R^-1, one warp per column
+//   * sym_eig         — eig(S) of Alg. 2 step 8 / svd(S) of Alg. 4 step 8:
+//                       Householder tridiagonalisation on an 8-CTA cluster with
+//                       the matrix resident in distributed shared memory,
+//                       bisection (Sturm counts) for eigenvalues, inverse
+//                       iteration with in-cluster modified Gram–Schmidt for
+//                       eigenvectors, reflector back-transformation
+//   * gemm64 and small helpers
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace netmfp {
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int NT>
+__device__ double block_sum(double v, double *red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x / 32, ln = threadIdx.x % 32;
+  __syncthreads();
+  if (ln == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = (threadIdx.x < NT / 32) ? red[threadIdx.x] : 0.0;
+    s = warp_sum(s);
+    if (threadIdx.x == 0) red[32] = s;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// ---------------------------------------------------------------------------
+// gemm64: C = alpha op(A) op(B) + beta C
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_gemm64(bool ta, bool tb, int64_t M, int64_t N, int64_t K,
+                                                double alpha, const double *__restrict__ A, int64_t lda,
+                                                const double *__restrict__ B, int64_t ldb, double beta,
+                                                double *__restrict__ C, int64_t ldc) {
+  __shared__ double As[16][65];
+  __shared__ double Bs[16][65];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int64_t m0 = (int64_t)blockIdx.y * 64, n0 = (int64_t)blockIdx.x * 64;
+  double acc[4][4] = {};
+  for (int64_t k0 = 0; k0 < K; k0 += 16) {
+    for (int idx = threadIdx.x; idx < 16 * 64; idx += 256) {
+      int kk = idx / 64, mm = idx % 64;
+      int64_t gm = m0 + mm, gk = k0 + kk;
+      double a = 0.0;
+      if (gm < M && gk < K) a = ta ? A[gk * lda + gm] : A[gm * lda + gk];
+      As[kk][mm] = a;
+      int64_t gn = n0 + mm;
+      double b = 0.0;
+      if (gn < N && gk < K) b = tb ? B[gn * ldb + gk] : B[gk * ldb + gn];
+      Bs[kk][mm] = b;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int64_t gm = m0 + ty + 16 * i, gn = n0 + tx + 16 * j;
+      if (gm < M && gn < N) {
+        double *c = C + gm * ldc + gn;
+        *c = alpha * acc[i][j] + (beta != 0.0 ? beta * *c : 0.0);
+      }
+    }
+}
+
+void gemm64(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
+            int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc) {
+  if (M <= 0 || N <= 0) return;
+  dim3 grid(ceil_div(N, 64), ceil_div(M, 64));
+  NM_LAUNCH(c, "gemm64", k_gemm64<<<grid, 256, 0, c.stream>>>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc));
+}
+
+__global__ void k_symmetrize(double *S, int64_t l, int64_t ld) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t i = idx / l, j = idx % l;
+  if (i >= l || j <= i) return;
+  double v = 0.5 * (S[i * ld + j] + S[j * ld + i]);
+  S[i * ld + j] = v;
+  S[j * ld + i] = v;
+}
+void symmetrize64(Ctx &c, double *S, int64_t l, int64_t ld) {
+  NM_LAUNCH(c, "symmetrize", k_symmetrize<<<ceil_div(l * l, 256), 256, 0, c.stream>>>(S, l, ld));
+}
+
+// mode 0: A[:, j] *= s[j]; mode 1: A[i, :] *= s[i]
+__global__ void k_scale64(double *A, int64_t rows, int64_t cols, int64_t ld, const double *s, int mode) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= rows * cols) return;
+  int64_t i = idx / cols, j = idx % cols;
+  A[i * ld + j] *= (mode == 0 ? s[j] : s[i]);
+}
+void scale_cols64(Ctx &c, double *A, int64_t rows, int64_t cols, int64_t ld, const double *s, int mode) {
+  NM_LAUNCH(c, "scale64", k_scale64<<<ceil_div(rows * cols, 256), 256, 0, c.stream>>>(A, rows, cols, ld, s, mode));
+}
+
+__global__ void k_identity(double *A, int64_t l, int64_t ld) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= l * l) return;
+  int64_t i = idx / l, j = idx % l;
+  A[i * ld + j] = (i == j) ? 1.0 : 0.0;
+}
+void set_identity64(Ctx &c, double *A, int64_t l, int64_t ld) {
+  NM_LAUNCH(c, "identity", k_identity<<<ceil_div(l * l, 256), 256, 0, c.stream>>>(A, l, ld));
+}
+
+__global__ void k_axpy64(int64_t n, double a, const double *x, double *y) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) y[i] += a * x[i];
+}
+void axpy64(Ctx &c, int64_t n, double alpha, const double *x, double *y) {
+  NM_LAUNCH(c, "axpy64", k_axpy64<<<ceil_div(n, 256), 256, 0, c.stream>>>(n, alpha, x, y));
+}
+
+// ---------------------------------------------------------------------------
+// Cholesky  G = Rᵀ R  (one CTA, left-looking, 32-column panels in smem)
+// ---------------------------------------------------------------------------
+constexpr int CHP = 32;
+
+__global__ void __launch_bounds__(1024) k_cholesky(double *G, int l, int64_t ld, double *G0, int *flag) {
+  extern __shared__ double P[];  // (l) x CHP panel
+  __shared__ int fail;
+  __shared__ double maxdiag;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // keep the original for shifted retries
+  for (int64_t idx = tid; idx < (int64_t)l * l; idx += nt) G0[idx] = G[(idx / l) * ld + idx % l];
+  if (tid == 0) {
+    double m = 0.0;
+    for (int i = 0; i < l; ++i) m = fmax(m, G0[(int64_t)i * l + i]);
+    maxdiag = m;
+  }
+  __syncthreads();
+  for (int attempt = 0; attempt < 6; ++attempt) {
+    const double shift = attempt == 0 ? 0.0 : maxdiag * 1e-7 * pow(100.0, (double)(attempt - 1));
+    if (attempt > 0) {
+      for (int64_t idx = tid; idx < (int64_t)l * l; idx += nt) {
+        int64_t i = idx / l, j = idx % l;
+        G[i * ld + j] = G0[idx] + (i == j ? shift : 0.0);
+      }
+    }
+    if (tid == 0) fail = 0;
+    __syncthreads();
+    for (int J = 0; J < l && !fail; J += CHP) {
+      const int jb = min(CHP, l - J), rows = l - J;
+      // panel = G[J:, J:J+jb] - L[J:, :J] L[J:J+jb, :J]^T   (lower part r >= c)
+      for (int idx = tid; idx < rows * jb; idx += nt) {
+        int r = idx / jb, cc = idx % jb;
+        double s = 0.0;
+        if (r >= cc) {
+          s = G[(int64_t)(J + r) * ld + J + cc];
+          const double *Lr = G + (int64_t)(J + r) * ld;
+          const double *Lc = G + (int64_t)(J + cc) * ld;
+          for (int t = 0; t < J; ++t) s -= Lr[t] * Lc[t];
+        }
+        P[r * CHP + cc] = s;
+      }
+      __syncthreads();
+      for (int j = 0; j < jb; ++j) {
+        if (tid == 0) {
+          double piv = P[j * CHP + j];
+          double ref = G0[(int64_t)(J + j) * l + J + j] + shift;
+          if (!(piv > 1e-12 * ref) || !isfinite(piv)) fail = 1;
+          else P[j * CHP + j] = sqrt(piv);
+        }
+        __syncthreads();
+        if (fail) break;
+        const double pj = P[j * CHP + j];
+        for (int r = j + 1 + tid; r < rows; r += nt) P[r * CHP + j] /= pj;
+        __syncthreads();
+        const int w = jb - j - 1;
+        for (int idx = tid; idx < (rows - j - 1) * w; idx += nt) {
+          int r = j + 1 + idx / w, cc = j + 1 + idx % w;
+          if (r >= cc) P[r * CHP + cc] -= P[r * CHP + j] * P[cc * CHP + j];
+        }
+        __syncthreads();
+      }
+      if (fail) break;
+      for (int idx = tid; idx < rows * jb; idx += nt) {
+        int r = idx / jb, cc = idx % jb;
+        if (r >= cc) G[(int64_t)(J + r) * ld + J + cc] = P[r * CHP + cc];
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (!fail) {
+      if (attempt > 0 && tid == 0) atomicAdd(flag, 1);
+      // R = L^T in the upper triangle, zero the strict lower
+      for (int64_t idx = tid; idx < (int64_t)l * l; idx += nt) {
+        int64_t i = idx / l, j = idx % l;
+        if (j > i) G[i * ld + j] = G[j * ld + i];
+      }
+      __syncthreads();
+      for (int64_t idx = tid; idx < (int64_t)l * l; idx += nt) {
+        int64_t i = idx / l, j = idx % l;
+        if (j < i) G[i * ld + j] = 0.0;
+      }
+      return;
+    }
+  }
+  if (tid == 0) atomicOr(flag, 1 << 30);
+}
+
+void cholesky_upper(Ctx &c, double *G, int64_t l, int64_t ld, int *flag) {
+  NM_REQUIRE(l > 0 && l <= 4096, "cholesky: l out of range");
+  DBuf<double> G0((size_t)l * l, c.stream);
+  size_t smem = (size_t)l * CHP * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    NM_CUDA(cudaFuncSetAttribute(k_cholesky, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  NM_REQUIRE(smem <= 200 * 1024, "cholesky: l too large for one CTA panel");
+  NM_LAUNCH(c, "cholesky", k_cholesky<<<1, 1024, smem, c.stream>>>(G, (int)l, ld, G0, flag));
+}
+
+// ---------------------------------------------------------------------------
+// Rinv = R^-1 (upper), one warp per column, x in shared memory
+// ---------------------------------------------------------------------------
+__global__ void k_trinv(const double *__restrict__ R, int64_t ld, double *__restrict__ Rinv, int l) {
+  extern __shared__ double xs[];
+  const int w = threadIdx.x / 32, ln = threadIdx.x % 32;
+  const int j = blockIdx.x * (blockDim.x / 32) + w;
+  if (j >= l) return;
+  double *x = xs + (int64_t)w * l;
+  for (int i = j; i >= 0; --i) {
+    double s = 0.0;
+    for (int k = i + 1 + ln; k <= j; k += 32) s += R[(int64_t)i * ld + k] * x[k];
+    s = warp_sum(s);
+    if (ln == 0) x[i] = ((i == j ? 1.0 : 0.0) - s) / R[(int64_t)i * ld + i];
+    __syncwarp();
+  }
+  for (int i = ln; i < l; i += 32) Rinv[(int64_t)i * l + j] = (i <= j) ? x[i] : 0.0;
+}
+
+void tri_inv_upper(Ctx &c, const double *R, int64_t ld, double *Rinv, int64_t l) {
+  const int wpb = 8;
+  size_t smem = (size_t)wpb * l * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    NM_CUDA(cudaFuncSetAttribute(k_trinv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  NM_REQUIRE(smem <= 200 * 1024, "tri_inv: l too large");
+  NM_LAUNCH(c, "trinv", k_trinv<<<ceil_div(l, wpb), wpb * 32, smem, c.stream>>>(R, ld, Rinv, (int)l));
+}
+
+// ---------------------------------------------------------------------------
+// symmetric eigensolver
+// ---------------------------------------------------------------------------
+constexpr int TDC = 8;     // cluster size (CTAs) for the tridiagonalisation
+constexpr int TDT = 512;   // threads per CTA
+
+// Householder tridiagonalisation Qᵀ S Q = T, Q = H_0 … H_{l-3}, H_j = I - beta_j v_j v_jᵀ
+// (v_j non-zero on indices j+1..l-1, stored in row j of Hv).  Row i of S lives in
+// CTA i % TDC of the cluster (local row i / TDC).
+__global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
+    k_tridiag(const double *__restrict__ S, int l, double *__restrict__ dd, double *__restrict__ ee,
+              double *__restrict__ Hv, double *__restrict__ hbeta) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int wid = tid / 32, ln = tid % 32;
+  const int nloc = (l - rank + TDC - 1) / TDC;
+  // identical shared-memory layout in every CTA (DSMEM addresses are mapped
+  // rank to rank), sized for the largest per-rank row count
+  const int nmax = (l + TDC - 1) / TDC;
+  extern __shared__ double sm[];
+  double *A = sm;                         // nmax × l (first nloc rows used)
+  double *vfull = A + (int64_t)nmax * l;  // l
+  double *wfull = vfull + l;              // l  (own rows' w at their global index)
+  double *pl = wfull + l;                 // nmax
+  double *red = pl + nmax;                // 33
+  double *xchg = red + 40;                // [0] partial vᵀp, [1] beta
+  for (int64_t idx = tid; idx < (int64_t)nloc * l; idx += nt) {
+    int li = (int)(idx / l), k = (int)(idx % l);
+    A[idx] = S[(int64_t)(li * TDC + rank) * l + k];
+  }
+  cl.sync();
+  for (int j = 0; j + 2 < l; ++j) {
+    const int owner = j % TDC;
+    // (1) owner: reflector from row j, entries j+1..l-1
+    if (rank == owner) {
+      const double *x = A + (int64_t)(j / TDC) * l;
+      double ss = 0.0;
+      for (int k = j + 2 + tid; k < l; k += nt) ss += x[k] * x[k];
+      ss = block_sum<TDT>(ss, red);
+      const double x0 = x[j + 1];
+      double beta = 0.0, alpha = x0;
+      if (ss > 0.0) {
+        double nrm = sqrt(ss + x0 * x0);
+        alpha = x0 >= 0 ? -nrm : nrm;
+        double v0 = x0 - alpha;
+        beta = 2.0 / (ss + v0 * v0);
+        for (int k = j + 1 + tid; k < l; k += nt) vfull[k] = (k == j + 1) ? v0 : x[k];
+      } else {
+        for (int k = j + 1 + tid; k < l; k += nt) vfull[k] = 0.0;
+      }
+      if (tid == 0) {
+        xchg[1] = beta;
+        dd[j] = x[j];
+        ee[j] = alpha;
+        hbeta[j] = beta;
+      }
+      __syncthreads();
+      for (int k = j + 1 + tid; k < l; k += nt) Hv[(int64_t)j * l + k] = vfull[k];
+    }
+    cl.sync();  // S1
+    double beta;
+    if (rank != owner) {
+      double *rv = cl.map_shared_rank(vfull, owner);
+      double *rx = cl.map_shared_rank(xchg, owner);
+      for (int k = j + 1 + tid; k < l; k += nt) vfull[k] = rv[k];
+      beta = rx[1];
+    } else {
+      beta = xchg[1];
+    }
+    __syncthreads();
+    // (2) p_i = beta * A[i, j+1:] · v for own rows i > j; partial vᵀp
+    double part = 0.0;
+    for (int li = wid; li < nloc; li += nt / 32) {
+      const int i = li * TDC + rank;
+      if (i <= j) continue;
+      const double *Ai = A + (int64_t)li * l;
+      double s = 0.0;
+      for (int k = j + 1 + ln; k < l; k += 32) s += Ai[k] * vfull[k];
+      s = warp_sum(s) * beta;
+      if (ln == 0) {
+        pl[li] = s;
+        part += s * vfull[i];
+      }
+    }
+    part = block_sum<TDT>(part, red);
+    if (tid == 0) xchg[0] = part;
+    cl.sync();  // S2
+    double K = 0.0;
+    for (int r = 0; r < TDC; ++r) K += *cl.map_shared_rank(xchg, r);
+    K *= 0.5 * beta;
+    // (3) w_i = p_i - K v_i (own rows)
+    for (int li = tid; li < nloc; li += nt) {
+      const int i = li * TDC + rank;
+      if (i > j) wfull[i] = pl[li] - K * vfull[i];
+    }
+    cl.sync();  // S3
+    // (4) gather w for k > j from the owners, then A_i -= v_i w + w_i v
+    for (int k = j + 1 + tid; k < l; k += nt) {
+      const int r = k % TDC;
+      if (r != rank) wfull[k] = cl.map_shared_rank(wfull, r)[k];
+    }
+    __syncthreads();
+    for (int li = wid; li < nloc; li += nt / 32) {
+      const int i = li * TDC + rank;
+      if (i <= j) continue;
+      double *Ai = A + (int64_t)li * l;
+      const double vi = vfull[i], wi = wfull[i];
+      for (int k = j + 1 + ln; k < l; k += 32) Ai[k] -= vi * wfull[k] + wi * vfull[k];
+    }
+    // CTA barrier: the next owner reads its freshly updated row and rewrites
+    // vfull; remote wfull reads are ordered by the next step's S1/S2
+    __syncthreads();
+  }
+  // trailing 2×2 (or 1×1)
+  if (l >= 2) {
+    const int i0 = l - 2, i1 = l - 1;
+    if (rank == i0 % TDC && tid == 0) {
+      dd[i0] = A[(int64_t)(i0 / TDC) * l + i0];
+      ee[i0] = A[(int64_t)(i0 / TDC) * l + i1];
+    }
+    if (rank == i1 % TDC && tid == 0) dd[i1] = A[(int64_t)(i1 / TDC) * l + i1];
+  } else if (rank == 0 && tid == 0) {
+    dd[0] = A[0];
+  }
+  cl.sync();  // no CTA may exit while others still read its shared memory
+}
+
+// Sturm count: number of eigenvalues of T strictly less than x
+__device__ int sturm_count(const double *d, const double *e, int l, double x, double pivmin) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  cnt += q < 0;
+  for (int i = 1; i < l; ++i) {
+    q = d[i] - x - e[i - 1] * e[i - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0;
+  }
+  return cnt;
+}
+
+// eigenvalue m (ascending) by bisection; also computes the 1-norm bound
+__global__ void k_bisect(const double *__restrict__ d, const double *__restrict__ e, int l,
+                         double *__restrict__ w) {
+  int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= l) return;
+  double lo = 1e300, hi = -1e300, emax = 0.0;
+  for (int i = 0; i < l; ++i) {
+    double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < l ? fabs(e[i]) : 0.0);
+    lo = fmin(lo, d[i] - r);
+    hi = fmax(hi, d[i] + r);
+    if (i + 1 < l) emax = fmax(emax, e[i] * e[i]);
+  }
+  const double tnorm = fmax(fabs(lo), fabs(hi));
+  const double eps = 2.220446049250313e-16;
+  const double pivmin = fmax(1e-300, 4.0 * 2.2250738585072014e-308 * fmax(1.0, emax));
+  lo -= 2.0 * eps * tnorm + pivmin;
+  hi += 2.0 * eps * tnorm + pivmin;
+  for (int it = 0; it < 200; ++it) {
+    double mid = 0.5 * (lo + hi);
+    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin) break;
+    if (mid <= lo || mid >= hi) break;
+    if (sturm_count(d, e, l, mid, pivmin) > m) hi = mid; else lo = mid;
+  }
+  w[m] = 0.5 * (lo + hi);
+}
+
+// Inverse iteration (dstein-style): one warp per cluster of (near-)degenerate
+// eigenvalues, gap <= 1e-9 ||T|| (isolated eigenvalues converge to vectors whose
+// mutual angle is ~eps ||T|| / gap).  The LU of T - sigma I (dgttrf with partial
+// pivoting) lives in shared memory; the c right-hand sides of a cluster are
+// solved in parallel, one lane each, then orthonormalised together (MGS).
+constexpr int IVW = 4;  // warps per block
+
+__global__ void __launch_bounds__(IVW * 32) k_invit(const double *__restrict__ d, const double *__restrict__ e,
+                                                    int l, const double *__restrict__ w,
+                                                    const int *__restrict__ cstart, int ncl,
+                                                    double *__restrict__ Zt, uint32_t seed) {
+  extern __shared__ double ivs[];
+  const int wib = threadIdx.x / 32, ln = threadIdx.x % 32;
+  const int gw = blockIdx.x * IVW + wib;
+  if (gw >= ncl) return;
+  double *dl = ivs + (int64_t)wib * 4 * l;
+  double *dg = dl + l, *du = dg + l, *du2 = du + l;
+  int8_t *piv = reinterpret_cast<int8_t *>(ivs + (int64_t)IVW * 4 * l) + wib * l;
+  double tnorm = 0.0;
+  for (int i = ln; i < l; i += 32) {
+    double r = fabs(d[i]) + (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < l ? fabs(e[i]) : 0.0);
+    tnorm = fmax(tnorm, r);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tnorm = fmax(tnorm, __shfl_xor_sync(0xffffffffu, tnorm, o));
+  const double eps = 2.220446049250313e-16;
+  const double tiny = eps * fmax(tnorm, 1e-300);
+  const int m0 = cstart[gw], m1 = cstart[gw + 1];
+  double sigma = 0.0;
+  for (int m = m0; m < m1; ++m) sigma += w[m];
+  sigma /= (m1 - m0);
+  if (ln == 0) {
+    for (int i = 0; i < l; ++i) {
+      dg[i] = d[i] - sigma;
+      if (i + 1 < l) { dl[i] = e[i]; du[i] = e[i]; }
+      du2[i] = 0.0;
+      piv[i] = 0;
+    }
+    for (int i = 0; i + 1 < l; ++i) {
+      if (fabs(dg[i]) >= fabs(dl[i])) {
+        if (dg[i] != 0.0) {
+          double f = dl[i] / dg[i];
+          dl[i] = f;
+          dg[i + 1] -= f * du[i];
+        }
+      } else {
+        double f = dg[i] / dl[i];
+        dg[i] = dl[i];
+        dl[i] = f;
+        double t = du[i];
+        du[i] = dg[i + 1];
+        dg[i + 1] = t - f * dg[i + 1];
+        if (i + 2 < l) {
+          du2[i] = du[i + 1];
+          du[i + 1] = -f * du[i + 1];
+        }
+        piv[i] = 1;
+      }
+    }
+    for (int i = 0; i < l; ++i)
+      if (fabs(dg[i]) < tiny) dg[i] = dg[i] < 0 ? -tiny : tiny;
+  }
+  // deterministic random starts in the output rows
+  for (int m = m0; m < m1; ++m)
+    for (int i = ln; i < l; i += 32) {
+      U4 r = philox4x32_10(U4{(uint32_t)i, (uint32_t)m, 0x494E5649u, 0u}, seed, 0x5EEDu);
+      Zt[(int64_t)m * l + i] = ((double)r.x + 0.5) * 2.3283064365386963e-10 - 0.5;
+    }
+  __syncwarp();
+  for (int it = 0; it < 3; ++it) {
+    // solve (T - sigma I) x = x for every vector of the cluster, one lane each
+    for (int m = m0 + ln; m < m1; m += 32) {
+      double *x = Zt + (int64_t)m * l;
+      for (int i = 0; i + 1 < l; ++i) {
+        if (!piv[i]) {
+          x[i + 1] -= dl[i] * x[i];
+        } else {
+          double t = x[i];
+          x[i] = x[i + 1];
+          x[i + 1] = t - dl[i] * x[i];
+        }
+      }
+      x[l - 1] /= dg[l - 1];
+      if (l > 1) x[l - 2] = (x[l - 2] - du[l - 2] * x[l - 1]) / dg[l - 2];
+      for (int i = l - 3; i >= 0; --i) x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) / dg[i];
+    }
+    __syncwarp();
+    // modified Gram-Schmidt over the cluster
+    for (int m = m0; m < m1; ++m) {
+      double *x = Zt + (int64_t)m * l;
+      for (int q = m0; q < m; ++q) {
+        const double *zq = Zt + (int64_t)q * l;
+        double s = 0.0;
+        for (int i = ln; i < l; i += 32) s += zq[i] * x[i];
+        s = warp_sum(s);
+        for (int i = ln; i < l; i += 32) x[i] -= s * zq[i];
+        __syncwarp();
+      }
+      double nrm = 0.0;
+      for (int i = ln; i < l; i += 32) nrm += x[i] * x[i];
+      nrm = sqrt(warp_sum(nrm));
+      const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+      for (int i = ln; i < l; i += 32) x[i] *= inv;
+      __syncwarp();
+    }
+  }
+}
+
+// cluster starts: consecutive eigenvalues closer than ortol = 1e-9 ||T||
+__global__ void k_clusters(const double *__restrict__ w, const double *__restrict__ d,
+                           const double *__restrict__ e, int l, int *__restrict__ cstart, int *ncl) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double tnorm = 0.0;
+  for (int i = 0; i < l; ++i)
+    tnorm = fmax(tnorm, fabs(d[i]) + (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < l ? fabs(e[i]) : 0.0));
+  const double ortol = 1e-9 * tnorm;
+  int c = 0;
+  cstart[c++] = 0;
+  for (int m = 1; m < l; ++m)
+    if (w[m] - w[m - 1] > ortol) cstart[c++] = m;
+  cstart[c] = l;
+  *ncl = c;
+}
+
+// eigenvectors of S: x <- H_0 (H_1 (… H_{l-3} z)); one warp per eigenvector
+__global__ void k_backtransform(const double *__restrict__ Hv, const double *__restrict__ hbeta, int l,
+                                double *__restrict__ Zt) {
+  const int m = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int ln = threadIdx.x % 32;
+  if (m >= l) return;
+  double *x = Zt + (int64_t)m * l;
+  for (int j = l - 3; j >= 0; --j) {
+    const double b = hbeta[j];
+    if (b == 0.0) continue;
+    const double *v = Hv + (int64_t)j * l;
+    double s = 0.0;
+    for (int k = j + 1 + ln; k < l; k += 32) s += v[k] * x[k];
+    s = warp_sum(s) * b;
+    for (int k = j + 1 + ln; k < l; k += 32) x[k] -= s * v[k];
+    __syncwarp();
+  }
+}
+
+// order by desc |λ| (ties: desc λ) or desc λ; V[r][c] = Zt[perm[c]][r]
+__global__ void k_eig_sort(const double *__restrict__ w, const double *__restrict__ Zt, int l,
+                           bool abs_order, double *__restrict__ lam, double *__restrict__ V) {
+  const int i = blockIdx.x;  // one block per eigenpair
+  const double wi = w[i];
+  __shared__ int rank_s;
+  if (threadIdx.x == 0) rank_s = 0;
+  __syncthreads();
+  int cnt = 0;
+  for (int j = threadIdx.x; j < l; j += blockDim.x) {
+    const double wj = w[j];
+    bool before;
+    if (abs_order) {
+      const double ai = fabs(wi), aj = fabs(wj);
+      before = (aj > ai) || (aj == ai && (wj > wi || (wj == wi && j < i)));
+    } else {
+      before = (wj > wi) || (wj == wi && j < i);
+    }
+    cnt += before;
+  }
+  atomicAdd(&rank_s, cnt);
+  __syncthreads();
+  const int r = rank_s;
+  if (threadIdx.x == 0) lam[r] = wi;
+  for (int k = threadIdx.x; k < l; k += blockDim.x) V[(int64_t)k * l + r] = Zt[(int64_t)i * l + k];
+}
+
+void sym_eig(Ctx &c, double *S, int64_t l64, double *lam, double *V, bool abs_order) {
+  const int l = (int)l64;
+  NM_REQUIRE(l >= 1, "sym_eig: l >= 1");
+  cudaStream_t s = c.stream;
+  DBuf<double> d(l, s), e(l, s), Hv((size_t)l * l, s), hb(l, s), w(l, s), Zt((size_t)l * l, s);
+  NM_CUDA(cudaMemsetAsync(Hv.p, 0, (size_t)l * l * 8, s));
+  NM_CUDA(cudaMemsetAsync(hb.p, 0, (size_t)l * 8, s));
+  NM_CUDA(cudaMemsetAsync(e.p, 0, (size_t)l * 8, s));
+  const int nloc = (l + TDC - 1) / TDC;
+  size_t smem = ((size_t)nloc * l + 2 * l + nloc + 48) * sizeof(double);
+  NM_REQUIRE(smem <= 220 * 1024, "sym_eig: l too large for the 8-CTA cluster (l <= ~460)");
+  static bool attr = false;
+  if (!attr) {
+    NM_CUDA(cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    attr = true;
+  }
+  NM_LAUNCH(c, "tridiag", k_tridiag<<<TDC, TDT, smem, s>>>(S, l, d, e, Hv, hb));
+  NM_LAUNCH(c, "bisect", k_bisect<<<ceil_div(l, 64), 64, 0, s>>>(d, e, l, w));
+  DBuf<int> cst(l + 1, s), ncl(1, s);
+  NM_LAUNCH(c, "clusters", k_clusters<<<1, 32, 0, s>>>(w, d, e, l, cst, ncl));
+  int hncl = 0;
+  NM_CUDA(cudaMemcpyAsync(&hncl, ncl.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NM_CUDA(cudaStreamSynchronize(s));
+  const size_t ivsm = (size_t)IVW * 4 * l * sizeof(double) + (size_t)IVW * l + 16;
+  static bool attr_iv = false;
+  if (!attr_iv) {
+    NM_CUDA(cudaFuncSetAttribute(k_invit, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_iv = true;
+  }
+  NM_LAUNCH(c, "invit", k_invit<<<ceil_div(hncl, IVW), IVW * 32, ivsm, s>>>(d, e, l, w, cst, hncl, Zt, 0x1234567u));
+  NM_LAUNCH(c, "backtransform", k_backtransform<<<ceil_div((int64_t)l * 32, 256), 256, 0, s>>>(Hv, hb, l, Zt));
+  NM_LAUNCH(c, "eig_sort", k_eig_sort<<<l, 128, 0, s>>>(w, Zt, l, abs_order, lam, V));
+}
+
+}  // namespace netmfp

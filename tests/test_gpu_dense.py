@@ -1,0 +1,104 @@
+"""GPU parity of the dense steps of Alg. 2 / Alg. 4 exposed through the ABI:
+Gram (eigSVD's YᵀY), orth (CholeskyQR [R7]) and the symmetric eigensolver
+(Alg. 2 step 8, Alg. 4 step 8) against numpy / the oracle."""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def L():
+    import __graft_entry__ as ge
+    ge.build()
+    from paper_2110_12782_b200 import _lib
+    return _lib
+
+
+@pytest.fixture(scope="module")
+def ctx(L):
+    return L.Context(0)
+
+
+def padded(n, c):
+    ld = (c + 31) // 32 * 32
+    return torch.zeros(n, ld, dtype=torch.float32, device=DEV)[:, :c]
+
+
+@pytest.mark.parametrize("n,a,b", [(1000, 7, 7), (5000, 158, 158), (3000, 64, 37), (70000, 286, 286)])
+def test_gram(L, ctx, n, a, b):
+    rng = np.random.default_rng(a)
+    A = rng.standard_normal((n, a)).astype(np.float32)
+    B = A if a == b else rng.standard_normal((n, b)).astype(np.float32)
+    Ad = padded(n, a); Ad.copy_(torch.from_numpy(A))
+    Bd = Ad if a == b else padded(n, b)
+    if a != b:
+        Bd.copy_(torch.from_numpy(B))
+    G = torch.zeros(a, b, dtype=torch.float64, device=DEV)
+    L.netmfp_gram(ctx, Ad, Bd, G)
+    ref = A.astype(np.float64).T @ B.astype(np.float64)
+    assert np.abs(G.cpu().numpy() - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("passes", [1, 2])
+@pytest.mark.parametrize("n,c", [(2000, 5), (20000, 158), (50000, 286)])
+def test_orthonormalize(L, ctx, n, c, passes):
+    rng = np.random.default_rng(c)
+    Y = (rng.standard_normal((n, c)) * np.logspace(0, 2, c)[None, :]).astype(np.float32)
+    Yd = padded(n, c); Yd.copy_(torch.from_numpy(Y))
+    Qd = padded(n, c)
+    L.netmfp_orthonormalize(ctx, Yd, Qd, passes)
+    Q = Qd.cpu().numpy().astype(np.float64)
+    assert np.abs(Q.T @ Q - np.eye(c)).max() <= (1e-5 if passes == 2 else 1e-3)
+    Qo, _, _ = O.eig_svd(Y.astype(np.float64))          # span(Q) == span(eigSVD Q)  [R7]
+    assert np.abs(Q.T @ Qo).sum(0).min() > 0            # not degenerate
+    assert np.linalg.norm(Q @ (Q.T @ Qo) - Qo) <= 1e-4 * np.sqrt(c)
+
+
+def _check_eig(L, ctx, S, abs_order=True):
+    l = S.shape[0]
+    lam = torch.zeros(l, dtype=torch.float64, device=DEV)
+    V = torch.zeros(l, l, dtype=torch.float64, device=DEV)
+    L.netmfp_sym_eig(ctx, torch.from_numpy(S).to(DEV), lam, V, abs_order)
+    lg, Vg = lam.cpu().numpy(), V.cpu().numpy()
+    ev = np.linalg.eigvalsh(S)
+    nrm = np.abs(ev).max()
+    # same multiset of eigenvalues; order non-increasing in |λ| (or λ) up to
+    # rounding (exact ties such as +1 / -1 may come in either order)
+    assert np.abs(np.sort(lg) - np.sort(ev)).max() <= 1e-10 * nrm
+    key = np.abs(lg) if abs_order else lg
+    assert np.all(np.diff(key) <= 1e-10 * nrm)
+    assert np.abs(Vg.T @ Vg - np.eye(l)).max() <= 1e-9
+    assert np.abs(S @ Vg - Vg * lg[None, :]).max() <= 1e-9 * nrm
+
+
+@pytest.mark.parametrize("l", [1, 2, 3, 5, 42, 158, 286, 460])
+def test_sym_eig_random(L, ctx, l):
+    A = np.random.default_rng(l).standard_normal((l, l))
+    _check_eig(L, ctx, (A + A.T) / 2)
+
+
+@pytest.mark.parametrize("l", [40, 228])
+def test_sym_eig_degenerate(L, ctx, l):
+    """Exactly repeated eigenvalues (twin vertices give such spectra)."""
+    rng = np.random.default_rng(1)
+    Q = np.linalg.qr(rng.standard_normal((l, l)))[0]
+    ev = np.resize(np.repeat(np.linspace(-1, 1, l // 8), 8), l)
+    ev[: l // 4] = 0.5
+    _check_eig(L, ctx, (Q * ev) @ Q.T)
+    _check_eig(L, ctx, (Q * ev) @ Q.T, abs_order=False)
+
+
+def test_sym_eig_graph_ritz(L, ctx):
+    """A Rayleigh-quotient matrix of a power-law graph operator (the Alg. 2 step 8 input)."""
+    from paper_2110_12782_b200 import inputs
+    n, s, t = inputs.small_graph("rmat", 4096, 2, edge_factor=8)
+    rp, col, deg = O.build_csr(n, s, t)
+    Y = O.normalized_spmm(rp, col, deg, np.random.default_rng(0).standard_normal((n, 120)), 0.45)
+    Q = np.linalg.qr(Y)[0]
+    S = Q.T @ O.normalized_spmm(rp, col, deg, Q, 0.45)
+    _check_eig(L, ctx, (S + S.T) / 2)
