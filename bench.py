@@ -141,10 +141,10 @@ def oracle_sample(w, n, src, dst, budget_s=20.0):
     # Eq. 5 on a row sample of F (random F of the right shape)
     F = rng.standard_normal((n, w.k)) * 1e-3
     Cm = np.eye(w.k)
-    rows_psi, sg_psi, p_psi = O.gen_sparse_sign(n, w.d + w.s2, w.z, 0, O.TAG_PSI)
     ns = min(n, 8192)
+    rows_psi, sg_psi, p_psi = O.gen_sparse_sign(ns, w.d + w.s2, w.z, 0, O.TAG_PSI)
     t0 = time.perf_counter()
-    O.sketch_y(F[:ns], Cm, 1.0, rows_psi, sg_psi, np.minimum(p_psi, ns - 1), 0)
+    O.sketch_y(F[:ns], Cm, 1.0, rows_psi, sg_psi, p_psi, 0)
     t_sky = (time.perf_counter() - t0) * n / ns
     rows_pi, sg_pi, p_pi = O.gen_sparse_sign(n, w.d + w.s3, w.z, 0, O.TAG_PI)
     v = p_pi.size

@@ -17,6 +17,8 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <cstdlib>
+
 namespace netmfp {
 
 __device__ __forceinline__ float row_scale(int64_t dg, float a) {
@@ -39,29 +41,38 @@ __device__ __forceinline__ float4 f4_add(float4 x, float4 a) {
   return a;
 }
 
-// Partial sum over neighbours e in [e0, e1) of one row for this lane's float4.
-template <int LPR, bool SCOL>
+// Partial sum over neighbours e in [e0, e1) of one row for this lane's float4
+// (Xc = X + this lane's column offset).  Every lane of the row's group reads
+// the same column index (an L1 broadcast) and its own 16 B of the neighbour's
+// row, so a group moves one full 128-B segment per neighbour; 4 neighbours are
+// in flight per iteration.  No shuffles: lanes never wait on each other.
+template <bool SCOL>
 __device__ __forceinline__ float4 gather_sum(const int32_t *__restrict__ col, int64_t e0, int64_t e1,
-                                             const float *__restrict__ X, int64_t ldx, int c,
-                                             bool active, const float *__restrict__ s_col,
-                                             int li, unsigned gmask) {
+                                             const float *__restrict__ Xc, uint32_t ldx,
+                                             const float *__restrict__ s_col) {
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int64_t e = e0; e < e1; e += LPR) {
-    int64_t my = e + li;
-    int vidx = my < e1 ? __ldg(col + my) : -1;
-    float sc = 1.f;
-    if (SCOL && vidx >= 0) sc = __ldg(s_col + vidx);
-    float4 xs[LPR];
-    float ss[LPR];
-#pragma unroll
-    for (int t = 0; t < LPR; ++t) {
-      int v = __shfl_sync(gmask, vidx, t, LPR);
-      ss[t] = SCOL ? __shfl_sync(gmask, sc, t, LPR) : 1.f;
-      xs[t] = (v >= 0 && active) ? __ldg(reinterpret_cast<const float4 *>(X + (int64_t)v * ldx + c))
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+  const int32_t *cp = col + e0;
+  int cnt = (int)(e1 - e0);
+  for (; cnt >= 4; cnt -= 4, cp += 4) {
+    const uint32_t v0 = __ldg(cp), v1 = __ldg(cp + 1), v2 = __ldg(cp + 2), v3 = __ldg(cp + 3);
+    const float4 x0 = __ldg(reinterpret_cast<const float4 *>(Xc + (uint64_t)v0 * ldx));
+    const float4 x1 = __ldg(reinterpret_cast<const float4 *>(Xc + (uint64_t)v1 * ldx));
+    const float4 x2 = __ldg(reinterpret_cast<const float4 *>(Xc + (uint64_t)v2 * ldx));
+    const float4 x3 = __ldg(reinterpret_cast<const float4 *>(Xc + (uint64_t)v3 * ldx));
+    if (SCOL) {
+      acc = f4_fma(__ldg(s_col + v0), x0, acc);
+      acc = f4_fma(__ldg(s_col + v1), x1, acc);
+      acc = f4_fma(__ldg(s_col + v2), x2, acc);
+      acc = f4_fma(__ldg(s_col + v3), x3, acc);
+    } else {
+      acc = f4_add(f4_add(x0, x1), acc);
+      acc = f4_add(f4_add(x2, x3), acc);
     }
-#pragma unroll
-    for (int t = 0; t < LPR; ++t) acc = SCOL ? f4_fma(ss[t], xs[t], acc) : f4_add(xs[t], acc);
+  }
+  for (; cnt > 0; --cnt, ++cp) {
+    const uint32_t v = __ldg(cp);
+    const float4 x = __ldg(reinterpret_cast<const float4 *>(Xc + (uint64_t)v * ldx));
+    acc = SCOL ? f4_fma(__ldg(s_col + v), x, acc) : f4_add(x, acc);
   }
   return acc;
 }
@@ -93,15 +104,15 @@ __global__ void __launch_bounds__(256) k_spmm_heavy(SpmmArgs p, const int64_t *_
   int64_t rb = rowptr[u], re = rowptr[u + 1];
   int64_t e0 = rb + (sidx - seg_ptr[h]) * kHeavySeg;
   int64_t e1 = min(e0 + (int64_t)kHeavySeg, re);
-  float4 acc = gather_sum<LPR, SCOL>(col, e0, e1, p.X, p.ldx, c, active, p.s_col, li, gmask);
   if (active) {
+    float4 acc = gather_sum<SCOL>(col, e0, e1, p.X + c, (uint32_t)p.ldx, p.s_col);
     float *dst = hsum + h * ldh + c;
     atomicAdd(reinterpret_cast<float4 *>(dst), acc);
   }
 }
 
-template <int LPR, bool SCOL>
-__global__ void __launch_bounds__(256) k_spmm_rows(SpmmArgs p, const int64_t *__restrict__ rowptr,
+template <int LPR, bool SCOL, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_spmm_rows(SpmmArgs p, const int64_t *__restrict__ rowptr,
                                                    const int32_t *__restrict__ col, int64_t n,
                                                    const int32_t *__restrict__ heavy, int64_t nh,
                                                    const float *__restrict__ hsum, int64_t ldh) {
@@ -116,6 +127,11 @@ __global__ void __launch_bounds__(256) k_spmm_rows(SpmmArgs p, const int64_t *__
   for (int64_t u = (int64_t)blockIdx.x * GPB + gi; u < n; u += stride) {
     int64_t e0 = __ldg(rowptr + u), e1 = __ldg(rowptr + u + 1);
     int64_t dg = e1 - e0;
+    // epilogue operands do not depend on the gather: issue their loads first
+    float4 pv = make_float4(0.f, 0.f, 0.f, 0.f), a0 = pv;
+    if (active && p.prev) pv = *reinterpret_cast<const float4 *>(p.prev + u * p.ldp + c);
+    if (active && p.acc_out && p.acc_in && p.acc_scale != 0.f)
+      a0 = *reinterpret_cast<const float4 *>(p.acc_in + u * p.ldai + c);
     float4 acc;
     if (dg > kLightCap) {
       // heavy row: partial sums were reduced by k_spmm_heavy
@@ -126,16 +142,13 @@ __global__ void __launch_bounds__(256) k_spmm_rows(SpmmArgs p, const int64_t *__
       }
       acc = active ? *reinterpret_cast<const float4 *>(hsum + lo * ldh + c)
                    : make_float4(0.f, 0.f, 0.f, 0.f);
-    } else {
-      acc = gather_sum<LPR, SCOL>(col, e0, e1, p.X, p.ldx, c, active, p.s_col, li, gmask);
+    } else if (active) {
+      acc = gather_sum<SCOL>(col, e0, e1, p.X + c, (uint32_t)p.ldx, p.s_col);
     }
     if (!active) continue;
     const float s = p.coef * row_scale(dg, p.a);
     float4 y = make_float4(s * acc.x, s * acc.y, s * acc.z, s * acc.w);
-    if (p.prev) {
-      float4 pv = *reinterpret_cast<const float4 *>(p.prev + u * p.ldp + c);
-      y = f4_fma(p.beta, pv, y);
-    }
+    if (p.prev) y = f4_fma(p.beta, pv, y);
     const int nv = p.cols - c;  // valid floats in this float4 (>= 1)
     if (p.Y) {
       float *dst = p.Y + u * p.ldy + c;
@@ -148,9 +161,6 @@ __global__ void __launch_bounds__(256) k_spmm_rows(SpmmArgs p, const int64_t *__
       }
     }
     if (p.acc_out) {
-      float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (p.acc_in && p.acc_scale != 0.f)
-        a0 = *reinterpret_cast<const float4 *>(p.acc_in + u * p.ldai + c);
       float4 r;
       r.x = p.acc_scale * a0.x + p.gamma * y.x;
       r.y = p.acc_scale * a0.y + p.gamma * y.y;
@@ -168,7 +178,155 @@ __global__ void __launch_bounds__(256) k_spmm_rows(SpmmArgs p, const int64_t *__
   }
 }
 
+// Fused epilogue for row u: y = coef·d_u^-a·acc (+ β·prev); Y = y; Acc = σ·Acc + γ·y.
+__device__ __forceinline__ void row_epilogue(const SpmmArgs &p, int64_t u, int64_t dg, float4 acc, int c) {
+  const float s = p.coef * row_scale(dg, p.a);
+  float4 y = make_float4(s * acc.x, s * acc.y, s * acc.z, s * acc.w);
+  if (p.prev) y = f4_fma(p.beta, *reinterpret_cast<const float4 *>(p.prev + u * p.ldp + c), y);
+  const int nv = (int)p.cols - c;
+  if (p.Y) {
+    float *dst = p.Y + u * p.ldy + c;
+    if (nv >= 4) {
+      *reinterpret_cast<float4 *>(dst) = y;
+    } else {
+      dst[0] = y.x;
+      if (nv > 1) dst[1] = y.y;
+      if (nv > 2) dst[2] = y.z;
+    }
+  }
+  if (p.acc_out) {
+    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (p.acc_in && p.acc_scale != 0.f) a0 = *reinterpret_cast<const float4 *>(p.acc_in + u * p.ldai + c);
+    float4 r;
+    r.x = p.acc_scale * a0.x + p.gamma * y.x;
+    r.y = p.acc_scale * a0.y + p.gamma * y.y;
+    r.z = p.acc_scale * a0.z + p.gamma * y.z;
+    r.w = p.acc_scale * a0.w + p.gamma * y.w;
+    float *dst = p.acc_out + u * p.ldacc + c;
+    if (nv >= 4) {
+      *reinterpret_cast<float4 *>(dst) = r;
+    } else {
+      dst[0] = r.x;
+      if (nv > 1) dst[1] = r.y;
+      if (nv > 2) dst[2] = r.z;
+    }
+  }
+}
+
+// Flattened row-block SpMM: each warp owns blocks of 32 consecutive rows whose
+// rowptr it stages in shared memory once; each LPR-lane group streams the
+// neighbours of its 32/GPW rows in batches of 4 that cross row boundaries
+// (segmented accumulation), so short rows never serialise memory latency.
+// Heavy rows (a ballot mask per block) are skipped and finalised from hsum.
 template <int LPR, bool SCOL>
+__global__ void __launch_bounds__(256) k_spmm_flat(SpmmArgs p, const int64_t *__restrict__ rowptr,
+                                                   const int32_t *__restrict__ col, int64_t n,
+                                                   const int32_t *__restrict__ heavy, int64_t nh,
+                                                   const float *__restrict__ hsum, int64_t ldh) {
+  constexpr int GPW = 32 / LPR;  // groups per warp
+  constexpr int RPG = 32 / GPW;  // rows per group in a 32-row block
+  __shared__ int64_t srp_all[8][33];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int64_t *srp = srp_all[wib];
+  const int gi = lane / LPR, li = lane % LPR;
+  const int c = blockIdx.y * (LPR * 4) + li * 4;
+  const bool active = c < p.cols;
+  const float *Xc = p.X + c;
+  const uint32_t ldx = (uint32_t)p.ldx;
+  const int64_t wstride = (int64_t)gridDim.x * 8 * 32;
+  for (int64_t r0 = ((int64_t)blockIdx.x * 8 + wib) * 32; r0 < n; r0 += wstride) {
+    srp[lane] = __ldg(rowptr + min(r0 + lane, n));
+    if (lane == 31) srp[32] = __ldg(rowptr + min(r0 + 32, n));
+    __syncwarp();
+    const unsigned hmask = __ballot_sync(0xffffffffu, srp[lane + 1] - srp[lane] > kLightCap);
+    const int rb = gi * RPG, re = rb + RPG;
+    const unsigned range = (re == 32 ? 0xffffffffu : ((1u << re) - 1u));
+    const int64_t gend = srp[re];
+    int row = rb;
+    int64_t e = srp[rb];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto finalize = [&](int ri) {
+      const int64_t u = r0 + ri;
+      if (u >= n || !active) return;
+      const int64_t dg = srp[ri + 1] - srp[ri];
+      if (dg > kLightCap) {
+        int64_t lo = 0, hi = nh - 1;
+        while (lo < hi) {
+          int64_t mid = (lo + hi) >> 1;
+          if (heavy[mid] < u) lo = mid + 1; else hi = mid;
+        }
+        acc = *reinterpret_cast<const float4 *>(hsum + lo * ldh + c);
+      }
+      row_epilogue(p, u, dg, acc, c);
+    };
+    while (true) {
+      while (row < re && srp[row + 1] <= e) {
+        finalize(row);
+        acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        ++row;
+      }
+      if (row >= re) break;
+      if ((hmask >> row) & 1u) {
+        finalize(row);
+        acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        e = srp[row + 1];
+        ++row;
+        continue;
+      }
+      const unsigned hm = hmask & range & (row == 31 ? 0u : ~((2u << row) - 1u));
+      const int64_t run_end = hm ? srp[__ffs(hm) - 1] : gend;
+      const int nb = (int)min((int64_t)4, run_end - e);
+      uint32_t v[4];
+      float4 x[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) v[t] = t < nb ? (uint32_t)__ldg(col + e + t) : 0u;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        x[t] = (t < nb && active) ? __ldg(reinterpret_cast<const float4 *>(Xc + (uint64_t)v[t] * ldx))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (SCOL && t < nb && active) {
+          const float sc = __ldg(p.s_col + v[t]);
+          x[t].x *= sc; x[t].y *= sc; x[t].z *= sc; x[t].w *= sc;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (t < nb) {
+          while (srp[row + 1] <= e + t) {
+            finalize(row);
+            acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            ++row;
+          }
+          acc = f4_add(x[t], acc);
+        }
+      }
+      e += nb;
+    }
+    __syncwarp();
+  }
+}
+
+template <int LPR, bool SCOL>
+static void spmm_flat_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
+  constexpr int GPB = 256 / LPR;
+  constexpr int CW = LPR * 4;
+  const unsigned chunks = ceil_div(p.cols, CW);
+  DBuf<float> hsum;
+  int64_t ldh = pad4(p.cols);
+  if (g.n_heavy > 0) {
+    hsum.alloc((size_t)g.n_heavy * ldh, c.stream);
+    hsum.zero();
+    dim3 gh(ceil_div(g.n_heavy_segs, GPB), chunks);
+    NM_LAUNCH(c, "spmm_heavy", k_spmm_heavy<LPR, SCOL><<<gh, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.heavy, g.heavy_seg_ptr,
+                                                      g.n_heavy, g.n_heavy_segs, hsum, ldh));
+  }
+  const int64_t blocks = ceil_div(g.n, 256);  // 8 warps × 32 rows
+  dim3 grid((unsigned)std::min<int64_t>(blocks, (int64_t)c.num_sms * 32), chunks);
+  NM_LAUNCH(c, "spmm_flat", k_spmm_flat<LPR, SCOL><<<grid, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.n, g.heavy,
+                                                                             g.n_heavy, hsum.p, ldh));
+}
+
+template <int LPR, bool SCOL, int MINB>
 static void spmm_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
   constexpr int GPB = 256 / LPR;
   constexpr int CW = LPR * 4;
@@ -186,17 +344,39 @@ static void spmm_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
   int64_t row_blocks = ceil_div(g.n, GPB);
   int64_t cap = (int64_t)c.num_sms * 64;
   dim3 grid((unsigned)std::min<int64_t>(row_blocks, cap), chunks);
-  NM_LAUNCH(c, "spmm_rows", k_spmm_rows<LPR, SCOL><<<grid, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.n, g.heavy, g.n_heavy,
+  NM_LAUNCH(c, "spmm_rows", k_spmm_rows<LPR, SCOL, MINB><<<grid, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.n, g.heavy, g.n_heavy,
                                                      hsum.p, ldh));
 }
 
 void spmm(Ctx &c, const Graph &g, const SpmmArgs &p) {
   NM_REQUIRE(p.cols > 0 && p.ldx % 4 == 0 && p.ldy % 4 == 0, "spmm: ld must be a multiple of 4");
+  NM_REQUIRE(p.ldx < (int64_t)1 << 32, "spmm: ldx must fit 32 bits");
   NM_REQUIRE(((uintptr_t)p.X & 15) == 0 && (!p.Y || ((uintptr_t)p.Y & 15) == 0),
              "spmm: buffers must be 16-byte aligned");
   if (g.n == 0) return;
-  if (p.s_col) spmm_impl<8, true>(c, g, p);
-  else spmm_impl<8, false>(c, g, p);
+  // tuning variants (NETMFP_SPMM env var, default 0): lanes per row x min blocks/SM
+  static int variant = [] {
+    const char *v = getenv("NETMFP_SPMM");
+    return v ? atoi(v) : 9;
+  }();
+  if (p.s_col) {
+    spmm_impl<32, true, 4>(c, g, p);
+    return;
+  }
+  switch (variant) {
+    case 0: spmm_impl<8, false, 4>(c, g, p); break;
+    case 1: spmm_impl<8, false, 5>(c, g, p); break;
+    case 8: spmm_impl<16, false, 5>(c, g, p); break;
+    case 9: spmm_impl<32, false, 4>(c, g, p); break;
+    case 10: spmm_impl<16, false, 3>(c, g, p); break;
+    case 2: spmm_impl<4, false, 4>(c, g, p); break;
+    case 3: spmm_impl<16, false, 4>(c, g, p); break;
+    case 4: spmm_impl<4, false, 6>(c, g, p); break;
+    case 5: spmm_flat_impl<8, false>(c, g, p); break;
+    case 6: spmm_flat_impl<16, false>(c, g, p); break;
+    case 7: spmm_flat_impl<32, false>(c, g, p); break;
+    default: spmm_impl<16, false, 4>(c, g, p); break;  // variant 3: 64-column chunks
+  }
 }
 
 // d^-e (0 for d = 0) as fp32 — column scaling vector for general (a, b)
