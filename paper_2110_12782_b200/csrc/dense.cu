@@ -7,6 +7,8 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <cstdlib>
+
 namespace netmfp {
 
 __device__ __forceinline__ float dpow_scale(const int32_t *deg, int64_t i, float e) {
@@ -105,8 +107,20 @@ __global__ void k_gram_reduce(const float *__restrict__ part, int nslab, int64_t
   G[i * ldg + j] = s;
 }
 
+bool tc_enabled() {
+  static int on = [] {
+    const char *v = getenv("NETMFP_TC");
+    return v ? atoi(v) : 1;
+  }();
+  return on != 0;
+}
+
 void gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg) {
   NM_REQUIRE(A.rows == B.rows, "gram: row mismatch");
+  if (tc_enabled() && A.rows >= 128) {
+    tc_gram(c, A, B, deg, wexp, G, ldg);
+    return;
+  }
   const int64_t n = A.rows;
   const bool sym = (A.p == B.p && A.cols == B.cols && A.ld == B.ld);
   const int ta = (int)ceil_div(A.cols, GT), tb = (int)ceil_div(B.cols, GT);
@@ -204,6 +218,10 @@ void gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcol
                float rexp, const Mat &C) {
   NM_REQUIRE(A.rows == C.rows && C.cols == bcols, "gemm_tall: shape mismatch");
   NM_REQUIRE(C.p != A.p, "gemm_tall: in-place not supported");
+  if (tc_enabled() && bcols <= 288 && A.rows >= 128) {
+    tc_gemm_tall(c, A, Bs, ldb, bcols, deg, rexp, C);
+    return;
+  }
   dim3 grid(ceil_div(A.rows, TM), ceil_div(bcols, TN));
   NM_LAUNCH(c, "gemm_tall", k_gemm_tall<<<grid, 256, 0, c.stream>>>(A, Bs, ldb, bcols, deg, rexp, C));
 }
