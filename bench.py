@@ -240,6 +240,8 @@ def run_ours(args):
         "spmm" if k.startswith("spmm") else k.rsplit("_", 1)[0] if k.startswith("gram") else k)
     tot_by = {}
     for k, (c, ms) in prof_all.items():
+        if k.startswith("stage_"):
+            continue
         tot_by[k] = tot_by.get(k, 0.0) + ms
     g = L.netmfp_build_csr(ctx, n, src, dst)
     nnz = g.nnz
@@ -319,7 +321,10 @@ def run_ours(args):
                         "d2h_bytes_per_step": int(n * d * 4)},
                 "gpu_launches": int(launches // args.steps),
                 "roofline": roof,
-                "kernel_ms_per_step": {k: v[1] / max(1, 1) for k, v in sorted(prof_all.items(), key=lambda x: -x[1][1])[:12]},
+                "kernel_ms_per_step": dict([(k, v[1]) for k, v in sorted(prof_all.items(), key=lambda x: -x[1][1])
+                                            if not k.startswith("stage_")][:14]),
+                "stage_ms_per_step": {k[6:]: v[1] for k, v in sorted(prof_all.items(), key=lambda x: -x[1][1])
+                                      if k.startswith("stage_")},
                 "clocks": clk}
         if ws == 1 and not args.no_cpu:
             v, cores, sample = oracle_sample(w, n, s_np, t_np)

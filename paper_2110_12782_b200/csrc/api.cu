@@ -397,15 +397,27 @@ static void embed_impl(Ctx &c, const Graph &g, const netmfp_params &p, const Mat
   const int64_t n = g.n;
   Block U(n, p.k, s), F(n, p.k, s);
   DBuf<double> lam(p.k, s), C((size_t)p.k * p.k, s);
-  freigs(c, g, p.alpha, p.k, p.s1, p.q, p.seed, U.m, lam);          // Alg. 5 step 1
+  {
+    NM_STAGE(c, "stage_freigs");
+    freigs(c, g, p.alpha, p.k, p.s1, p.q, p.seed, U.m, lam);          // Alg. 5 step 1
+  }
   if (lambda_dev) NM_CUDA(cudaMemcpyAsync(lambda_dev, lam.p, p.k * 8, cudaMemcpyDeviceToDevice, s));
-  factor_pair(c, g, p.alpha, p.T, U.m, lam, p.k, F.m, C);            // steps 2-3
+  {
+    NM_STAGE(c, "stage_factor_pair");
+    factor_pair(c, g, p.alpha, p.T, U.m, lam, p.k, F.m, C);            // steps 2-3
+  }
   U.buf.release();
   const double scale = (double)g.nnz / (p.b * p.T);                  // vol(G)/(bT)
-  sketch_svd(c, F.m, C, p.k, scale, p.d, p.s2, p.s3, p.z, p.seed, p.logmode, nullptr, sigma_dev, &E,
-             nullptr, nullptr);                                      // steps 4-5
+  {
+    NM_STAGE(c, "stage_sketch_svd");
+    sketch_svd(c, F.m, C, p.k, scale, p.d, p.s2, p.s3, p.z, p.seed, p.logmode, nullptr, sigma_dev, &E,
+               nullptr, nullptr);                                      // steps 4-5
+  }
   F.buf.release();
-  propagate(c, g, E, p.prop_order, p.mu, p.theta);                   // step 6
+  {
+    NM_STAGE(c, "stage_propagate");
+    propagate(c, g, E, p.prop_order, p.mu, p.theta);                   // step 6
+  }
 }
 
 int netmfp_embed(netmfp_ctx *ctx, const netmfp_graph *gr, const netmfp_params *p, float *E, int64_t lde,
@@ -432,7 +444,11 @@ int netmfp_embed_edges(netmfp_ctx *ctx, int64_t n, const int32_t *src, const int
     check_mem(mem);
     Ctx &c = ctx->c;
     InVec<int32_t> s(c, src, m_in, mem, true), t(c, dst, m_in, mem, true);
-    std::unique_ptr<Graph> g(build_csr_device(c, n, s.p, t.p, m_in));
+    std::unique_ptr<Graph> g;
+    {
+      NM_STAGE(c, "stage_build_csr");
+      g.reset(build_csr_device(c, n, s.p, t.p, m_in));
+    }
     InMat eo(c, E, n, p->d, lde, mem, false);
     InVec<double> so(c, sigma, p->d, mem, false);
     embed_impl(c, *g, *p, eo.m, so.p, nullptr);

@@ -131,6 +131,30 @@ inline void prof_collect(Ctx &c) {
   c.pending.clear();
 }
 
+// Stream-time interval of a whole stage (kernels, copies, memsets and idle
+// gaps between them), recorded like a kernel when profiling matches `name`.
+struct StageScope {
+  Ctx &c;
+  const char *name;
+  cudaEvent_t a = nullptr;
+  StageScope(Ctx &cc, const char *n) : c(cc), name(n) {
+    if (!c.prof || !prof_match(c, n)) return;
+    a = prof_event(c);
+    cudaEventRecord(a, c.stream);
+  }
+  ~StageScope() {
+    if (!a) return;
+    cudaEvent_t b = prof_event(c);
+    cudaEventRecord(b, c.stream);
+    c.pending.push_back({a, b, name});
+  }
+  StageScope(const StageScope &) = delete;
+  StageScope &operator=(const StageScope &) = delete;
+};
+#define NM_STAGE_CAT2(a, b) a##b
+#define NM_STAGE_CAT(a, b) NM_STAGE_CAT2(a, b)
+#define NM_STAGE(c, name) ::netmfp::StageScope NM_STAGE_CAT(_stage_, __LINE__)(c, name)
+
 #define NM_LAUNCH(c, name, ...)   \
   do {                            \
     ::netmfp::prof_begin(c, name); \

@@ -218,12 +218,21 @@ void gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcol
                float rexp, const Mat &C) {
   NM_REQUIRE(A.rows == C.rows && C.cols == bcols, "gemm_tall: shape mismatch");
   NM_REQUIRE(C.p != A.p, "gemm_tall: in-place not supported");
-  if (tc_enabled() && bcols <= 288 && A.rows >= 128) {
+  if (tc_enabled() && A.rows >= 128) {
     tc_gemm_tall(c, A, Bs, ldb, bcols, deg, rexp, C);
     return;
   }
   dim3 grid(ceil_div(A.rows, TM), ceil_div(bcols, TN));
   NM_LAUNCH(c, "gemm_tall", k_gemm_tall<<<grid, 256, 0, c.stream>>>(A, Bs, ldb, bcols, deg, rexp, C));
+}
+
+void gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, const int32_t *deg, float rexp,
+                   const Mat &C) {
+  if (tc_enabled() && A.rows >= 128 && A.cols <= 288) {
+    tc_gemm_tall_tri(c, A, Rinv, ldb, A.cols, deg, rexp, C);
+    return;
+  }
+  gemm_tall(c, A, Rinv, ldb, A.cols, deg, rexp, C);
 }
 
 // ---------------------------------------------------------------------------

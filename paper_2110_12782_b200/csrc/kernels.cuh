@@ -43,6 +43,11 @@ void gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcol
 void tc_gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcols, const int32_t *deg,
                   float rexp, const Mat &C);
 void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg);
+void tc_gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, int64_t bcols, const int32_t *deg,
+                      float rexp, const Mat &C);
+// C = rs · A · Rinv with Rinv (a×a) upper triangular (CholeskyQR's Y R⁻¹)
+void gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, const int32_t *deg, float rexp,
+                   const Mat &C);
 bool tc_enabled();
 // Ω = randn(n, l) from Philox [R1], row-scaled by d_i^-e (deg != null)
 void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, float rexp);
@@ -57,6 +62,9 @@ void copy_block(Ctx &c, const float *src, int64_t lds, float *dst, int64_t ldd, 
 // On breakdown retries with a diagonal shift (shifted CholeskyQR); increments
 // *flag when a shift was needed and sets *flag |= 1<<30 on failure.
 void cholesky_upper(Ctx &c, double *G, int64_t l, int64_t ld, int *flag);
+// G = RᵀR (l×l, ld) → Rinv = R⁻¹ (l×l upper, ld = l); G is overwritten.
+// Shifted retry and *flag protocol as cholesky_upper.
+void chol_inv_upper(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *flag);
 // Rinv = R^-1 for upper triangular R (l×l)
 void tri_inv_upper(Ctx &c, const double *R, int64_t ld, double *Rinv, int64_t l);
 // symmetric eigendecomposition (cyclic Jacobi), S overwritten; V (l×l) gets

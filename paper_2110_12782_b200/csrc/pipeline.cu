@@ -23,20 +23,20 @@ static void check_flag(Ctx &c, const char *what) {
 // passes = 2 gives CholeskyQR2 (second pass on the materialised Y R1⁻¹ in tmp).
 void cholqr(Ctx &c, const Mat &Y, const Mat &out, const int32_t *deg, float rexp, int passes,
             const Mat *tmp) {
+  NM_STAGE(c, "stage_cholqr");
   const int64_t l = Y.cols;
   cudaStream_t s = c.stream;
   DBuf<double> G((size_t)l * l, s), Rinv((size_t)l * l, s);
   Mat cur = Y;
   for (int ps = 0; ps < passes; ++ps) {
     gram(c, cur, cur, nullptr, 0.f, G, l);
-    cholesky_upper(c, G, l, l, c.d_flags);
-    tri_inv_upper(c, G, l, Rinv, l);
+    chol_inv_upper(c, G, l, l, Rinv, c.d_flags);
     const bool last = (ps + 1 == passes);
     if (last) {
-      gemm_tall(c, cur, Rinv, l, l, deg, rexp, out);
+      gemm_tall_tri(c, cur, Rinv, l, deg, rexp, out);
     } else {
       NM_REQUIRE(tmp && tmp->p != cur.p, "cholqr2: needs a scratch block");
-      gemm_tall(c, cur, Rinv, l, l, nullptr, 0.f, *tmp);
+      gemm_tall_tri(c, cur, Rinv, l, nullptr, 0.f, *tmp);
       cur = *tmp;
     }
   }
@@ -84,7 +84,10 @@ void freigs(Ctx &c, const Graph &g, double alpha, int k, int s1, int q, uint64_t
   gram(c, P.m, T.m, nullptr, 0.f, S, l);
   symmetrize64(c, S, l, l);
   // step 8: [Û, Λ] = eig(S), ordered by |λ| [R3]
-  sym_eig(c, S, l, lam, V, true);
+  {
+    NM_STAGE(c, "stage_sym_eig");
+    sym_eig(c, S, l, lam, V, true);
+  }
   // step 9-10: U = Q Û(:, 1:k) = D^α P Û(:, 1:k)
   gemm_tall(c, P.m, V, l, k, g.deg, -a, U);
   NM_CUDA(cudaMemcpyAsync(lam_dev, lam.p, (size_t)k * 8, cudaMemcpyDeviceToDevice, s));
@@ -137,21 +140,31 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
   const float fs = (float)scale;
   // step 2: Ψ
   SparseSign Psi;
-  gen_sparse_sign(c, n, h2, z, seed, kTagPsi, Psi);
+  {
+    NM_STAGE(c, "stage_gen_sparse_sign");
+    gen_sparse_sign(c, n, h2, z, seed, kTagPsi, Psi);
+  }
   // FC = F · C
   Block FC(n, k, s);
   gemm_tall(c, F, C, k, k, nullptr, 0.f, FC.m);
   // step 3: Y = f(scale F C F(p,:)ᵀ) Ψ
   Block Y(n, h2, s), Qb(n, h2, s), Tb(n, h2, s);
-  sketch_apply(c, FC.m, F, Psi, fs, logmode, Y.m);
+  {
+    NM_STAGE(c, "stage_sketch_y");
+    sketch_apply(c, FC.m, F, Psi, fs, logmode, Y.m);
+  }
   if (Yout) copy_block(c, Y.m.p, Y.m.ld, Yout->p, Yout->ld, n, h2);
   // step 4: Q = orth(Y)   (CholeskyQR2 [R7])
   cholqr(c, Y.m, Qb.m, nullptr, 0.f, 2, &Tb.m);
   check_flag(c, "single-pass SVD orth(Y)");
   // step 5: Π
   SparseSign Pi;
-  gen_sparse_sign(c, n, h3, z, seed, kTagPi, Pi);
+  {
+    NM_STAGE(c, "stage_gen_sparse_sign");
+    gen_sparse_sign(c, n, h3, z, seed, kTagPi, Pi);
+  }
   // step 6: Z = Πᵀ f(scale F(p,:) C F(p,:)ᵀ) Π
+  NM_STAGE(c, "stage_sketch_z_core");
   Block FpC(Pi.v, k, s), H(Pi.v, h3, s);
   gather_rows(c, FC.m, Pi.p, Pi.v, FpC.m);
   sketch_apply(c, FpC.m, F, Pi, fs, logmode, H.m);
@@ -163,8 +176,7 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
   DBuf<double> N((size_t)h2 * h2, s), Ninv((size_t)h2 * h2, s), Rinv((size_t)h2 * h2, s);
   DBuf<double> W((size_t)h2 * h3, s), WZ((size_t)h2 * h3, s), S((size_t)h2 * h2, s);
   gemm64(c, true, false, h2, h2, h3, 1.0, PtQ, h2, PtQ, h2, 0.0, N, h2);  // N = AᵀA
-  cholesky_upper(c, N, h2, h2, c.d_flags);
-  tri_inv_upper(c, N, h2, Rinv, h2);
+  chol_inv_upper(c, N, h2, h2, Rinv, c.d_flags);
   gemm64(c, false, true, h2, h2, h2, 1.0, Rinv, h2, Rinv, h2, 0.0, Ninv, h2);  // (AᵀA)⁻¹
   gemm64(c, false, true, h2, h3, h2, 1.0, Ninv, h2, PtQ, h2, 0.0, W, h3);      // A† = (AᵀA)⁻¹Aᵀ
   gemm64(c, false, false, h2, h3, h3, 1.0, W, h3, Z, h3, 0.0, WZ, h3);
@@ -173,7 +185,10 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
   check_flag(c, "single-pass SVD core solve");
   // step 8: svd(S) of the symmetric core = eig with |λ| ordering
   DBuf<double> lam(h2, s), V((size_t)h2 * h2, s), sq(d, s);
-  sym_eig(c, S, h2, lam, V, true);
+  {
+    NM_STAGE(c, "stage_sym_eig");
+    sym_eig(c, S, h2, lam, V, true);
+  }
   if (sigma_dev) {
     NM_LAUNCH(c, "abs", k_abs<<<ceil_div(d, 128), 128, 0, s>>>(lam, d, sigma_dev));
   }

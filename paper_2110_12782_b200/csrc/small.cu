@@ -246,6 +246,224 @@ void cholesky_upper(Ctx &c, double *G, int64_t l, int64_t ld, int *flag) {
 }
 
 // ---------------------------------------------------------------------------
+// Fused Cholesky + inverse:  G = Rᵀ R (R upper),  Rinv = R⁻¹  — one CTA.
+// L = Rᵀ (lower) is built in place in G's lower triangle by 32-column panels:
+//   (a) LsT[t][c] = L[J+c][t] (t < J) staged in shared memory;
+//   (b) P[r][c] = G[J+r][J+c] − Σ_t L[J+r][t] LsT[t][c]   (left-looking update);
+//   (c) warp 0 factors the 32×32 diagonal block in registers (shuffles only);
+//   (d) every thread owning a row below solves against it (forward substitution).
+// Then X = L⁻¹ by 32-row block rows: X_II = L_II⁻¹ (warp 0, registers),
+// X_IJ = −X_II Σ_K L_IK X_KJ, and finally Rinv = Xᵀ in place.  A breakdown
+// (pivot <= 1e-12 · original diagonal, or non-finite) restarts from the saved
+// G with a diagonal shift (shifted CholeskyQR), as cholesky_upper does.
+// ---------------------------------------------------------------------------
+constexpr int CI_T = 512;
+constexpr int CI_MAXL = 320;
+constexpr int CI_LD = 33;                  // row stride of 32-wide panels
+constexpr int CI_R = CI_MAXL * CI_LD;      // doubles per big region
+constexpr int CI_K = (CI_MAXL * 32 + CI_T - 1) / CI_T;  // outputs per thread
+
+__global__ void __launch_bounds__(CI_T) k_chol_inv(double *G, int l, int64_t ld, double *G0, double *Rinv,
+                                                   int *flag) {
+  extern __shared__ double sm[];
+  double *R1 = sm;             // phase 1: L rows chunk [rows][33];   phase 2: L_I rows [32][l+1]
+  double *R2 = sm + CI_R;      // phase 1: panel P [rows][33];        phase 2: X chunk / T [32][l+1]
+  double *R3 = sm + 2 * CI_R;  // phase 1: LsT chunk [32][33];        phase 2: X_II [32][33]
+  __shared__ double diag0[CI_MAXL];
+  __shared__ int fail;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t idx = tid; idx < (int64_t)l * l; idx += CI_T) G0[idx] = G[(idx / l) * ld + idx % l];
+  for (int i = tid; i < l; i += CI_T) diag0[i] = G[(int64_t)i * ld + i];
+  __syncthreads();
+  double maxdiag = 0.0;
+  for (int i = 0; i < l; ++i) maxdiag = fmax(maxdiag, diag0[i]);
+  bool ok = false;
+  double acc[CI_K];
+  for (int attempt = 0; attempt < 6 && !ok; ++attempt) {
+    const double shift = attempt == 0 ? 0.0 : maxdiag * 1e-7 * pow(100.0, (double)(attempt - 1));
+    if (attempt > 0) {
+      for (int64_t idx = tid; idx < (int64_t)l * l; idx += CI_T) {
+        const int64_t i = idx / l, j = idx % l;
+        G[i * ld + j] = G0[idx] + (i == j ? shift : 0.0);
+      }
+    }
+    if (tid == 0) fail = 0;
+    __syncthreads();
+    for (int J = 0; J < l; J += 32) {
+      const int jb = min(32, l - J), rows = l - J, np = rows * jb;
+      // (b) P = G[J:, J:J+jb] − L[J:, :J] L[J:J+jb, :J]ᵀ, tiled over 32-wide t chunks
+#pragma unroll
+      for (int k = 0; k < CI_K; ++k) {
+        const int idx = tid + k * CI_T;
+        acc[k] = idx < np ? G[(int64_t)(J + idx / jb) * ld + J + idx % jb] : 0.0;
+      }
+      for (int t0 = 0; t0 < J; t0 += 32) {
+        for (int idx = tid; idx < rows * 32; idx += CI_T)
+          R1[(idx >> 5) * CI_LD + (idx & 31)] = G[(int64_t)(J + (idx >> 5)) * ld + t0 + (idx & 31)];
+        for (int idx = tid; idx < jb * 32; idx += CI_T)
+          R3[(idx & 31) * CI_LD + (idx >> 5)] = G[(int64_t)(J + (idx >> 5)) * ld + t0 + (idx & 31)];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < CI_K; ++k) {
+          const int idx = tid + k * CI_T;
+          if (idx < np) {
+            const double *a = R1 + (idx / jb) * CI_LD;
+            const double *b = R3 + idx % jb;
+            double s = 0.0;
+#pragma unroll 8
+            for (int tt = 0; tt < 32; ++tt) s += a[tt] * b[tt * CI_LD];
+            acc[k] -= s;
+          }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int k = 0; k < CI_K; ++k) {
+        const int idx = tid + k * CI_T;
+        if (idx < np) {
+          const int r = idx / jb, cc = idx % jb;
+          R2[r * CI_LD + cc] = (r < jb && r < cc) ? 0.0 : acc[k];
+        }
+      }
+      __syncthreads();
+      // (c) diagonal block by warp 0, lane r = row r
+      if (warp == 0) {
+        bool bad = false;
+        for (int j = 0; j < jb; ++j) {
+          const double d = R2[j * CI_LD + j];
+          if (!(d > 1e-12 * (diag0[J + j] + shift)) || !isfinite(d)) bad = true;
+          const double sq = sqrt(fmax(d, 1e-300));
+          __syncwarp();
+          if (lane == j) R2[j * CI_LD + j] = sq;
+          if (lane > j && lane < jb) R2[lane * CI_LD + j] /= sq;
+          __syncwarp();
+          if (lane > j && lane < jb) {
+            const double lr = R2[lane * CI_LD + j];
+            for (int cc = j + 1; cc <= lane; ++cc) R2[lane * CI_LD + cc] -= lr * R2[cc * CI_LD + j];
+          }
+          __syncwarp();
+        }
+        if (bad && lane == 0) fail = 1;
+      }
+      __syncthreads();
+      if (fail) break;
+      // (d) rows below the diagonal block: forward substitution
+      for (int r = jb + tid; r < rows; r += CI_T) {
+        double *Pr = R2 + r * CI_LD;
+        for (int cc = 0; cc < jb; ++cc) {
+          double v = Pr[cc];
+          for (int t = 0; t < cc; ++t) v -= Pr[t] * R2[cc * CI_LD + t];
+          Pr[cc] = v / R2[cc * CI_LD + cc];
+        }
+      }
+      __syncthreads();
+      for (int idx = tid; idx < np; idx += CI_T) {
+        const int r = idx / jb, cc = idx % jb;
+        if (r >= cc) G[(int64_t)(J + r) * ld + J + cc] = R2[r * CI_LD + cc];
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    ok = !fail;
+    if (ok && attempt > 0 && tid == 0) atomicAdd(flag, 1);
+  }
+  if (!ok) {
+    if (tid == 0) atomicOr(flag, 1 << 30);
+    return;
+  }
+  // ---- X = L⁻¹ (lower, row-major in Rinv), block row by block row
+  const int WL = l + 1;
+  for (int I = 0; I < l; I += 32) {
+    const int ib = min(32, l - I), nt = ib * I;
+    for (int idx = tid; idx < ib * (I + ib); idx += CI_T) {
+      const int r = idx / (I + ib), t = idx % (I + ib);
+      R1[r * WL + t] = G[(int64_t)(I + r) * ld + t];
+    }
+    __syncthreads();
+    // (i) X_II = L_II⁻¹ (warp 0; lane = column)
+    if (warp == 0) {
+      for (int r = 0; r < 32; ++r) {
+        double v = 0.0;
+        if (r < ib && lane < ib && r >= lane) {
+          v = (r == lane) ? 1.0 : 0.0;
+          const double *Lr = R1 + r * WL + I;
+          for (int t = lane; t < r; ++t) v -= Lr[t] * R3[t * CI_LD + lane];
+          v /= Lr[r];
+        }
+        R3[r * CI_LD + lane] = v;
+        __syncwarp();
+      }
+    }
+    // (ii) T = L[I:I+ib, :I] · X[:I, :I], tiled over 32-row chunks of X
+#pragma unroll
+    for (int k = 0; k < CI_K; ++k) acc[k] = 0.0;
+    for (int t0 = 0; t0 < I; t0 += 32) {
+      for (int idx = tid; idx < 32 * I; idx += CI_T) {
+        const int tt = idx / I, cc = idx % I;
+        R2[tt * WL + cc] = Rinv[(int64_t)(t0 + tt) * l + cc];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < CI_K; ++k) {
+        const int idx = tid + k * CI_T;
+        if (idx < nt) {
+          const double *a = R1 + (idx / I) * WL + t0;
+          const double *b = R2 + idx % I;
+          double s = 0.0;
+#pragma unroll 8
+          for (int tt = 0; tt < 32; ++tt) s += a[tt] * b[tt * WL];
+          acc[k] += s;
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < CI_K; ++k) {
+      const int idx = tid + k * CI_T;
+      if (idx < nt) R2[(idx / I) * WL + idx % I] = acc[k];
+    }
+    __syncthreads();
+    // (iii) X[I+r][c] = −Σ_s X_II[r][s] T[s][c] (c < I); diagonal block = X_II
+    for (int idx = tid; idx < ib * l; idx += CI_T) {
+      const int r = idx / l, cc = idx % l;
+      double v = 0.0;
+      if (cc < I) {
+        for (int s2 = 0; s2 <= r; ++s2) v -= R3[r * CI_LD + s2] * R2[s2 * WL + cc];
+      } else if (cc < I + ib) {
+        v = R3[r * CI_LD + (cc - I)];
+      }
+      Rinv[(int64_t)(I + r) * l + cc] = v;
+    }
+    __syncthreads();
+  }
+  // ---- Rinv = Xᵀ (upper) in place
+  for (int64_t idx = tid; idx < (int64_t)l * l; idx += CI_T) {
+    const int64_t i = idx / l, j = idx % l;
+    if (i < j) {
+      const double v = Rinv[j * l + i];
+      Rinv[i * l + j] = v;
+      Rinv[j * l + i] = 0.0;
+    }
+  }
+}
+
+void chol_inv_upper(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *flag) {
+  if (l > CI_MAXL) {
+    cholesky_upper(c, G, l, ld, flag);
+    tri_inv_upper(c, G, ld, Rinv, l);
+    return;
+  }
+  DBuf<double> G0((size_t)l * l, c.stream);
+  const size_t smem = ((size_t)2 * CI_R + 32 * CI_LD) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    NM_CUDA(cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  NM_LAUNCH(c, "chol_inv", k_chol_inv<<<1, CI_T, smem, c.stream>>>(G, (int)l, ld, G0, Rinv, flag));
+}
+
+// ---------------------------------------------------------------------------
 // Rinv = R^-1 (upper), one warp per column, x in shared memory
 // ---------------------------------------------------------------------------
 __global__ void k_trinv(const double *__restrict__ R, int64_t ld, double *__restrict__ Rinv, int l) {

@@ -354,6 +354,7 @@ void spmm(Ctx &c, const Graph &g, const SpmmArgs &p) {
   NM_REQUIRE(((uintptr_t)p.X & 15) == 0 && (!p.Y || ((uintptr_t)p.Y & 15) == 0),
              "spmm: buffers must be 16-byte aligned");
   if (g.n == 0) return;
+  NM_STAGE(c, "stage_spmm");
   // tuning variants (NETMFP_SPMM env var, default 0): lanes per row x min blocks/SM
   static int variant = [] {
     const char *v = getenv("NETMFP_SPMM");

@@ -1,27 +1,40 @@
-// tc_gemm.cu — tall-skinny dense contractions on the 5th-gen tensor cores.
+// tc_gemm.cu — tall-skinny dense contractions on the 5th-gen tensor cores
+// (Gram matrices of CholeskyQR / Rayleigh–Ritz / Eq. 3, and the n×c · c×c
+// products Q = Y R⁻¹, U = Q Û, F·C, E = Q Û √Σ of Alg. 2 / 4 / 5).
 //
-// C = A·Bᵀ with fp32 operands at fp32-level accuracy via 3xTF32: every operand
-// x is split into tf32 parts x = hi + lo (hi = rna_tf32(x), lo = x - hi) and
-// C = A_hi B_hiᵀ + A_hi B_loᵀ + A_lo B_hiᵀ (the dropped lo·lo term is ~2^-22
-// relative), accumulated in fp32 in TMEM by tcgen05.mma.kind::tf32.
+// Precision: 3xTF32.  An fp32 operand x is used as hi = x (the tensor core
+// reads the top 19 bits, i.e. trunc_tf32(x)) and lo = x − trunc_tf32(x)
+// (exact in fp32), and C = A_hi·B_hi + A_hi·B_lo + A_lo·B_hi is accumulated
+// in fp32 TMEM by tcgen05.mma.kind::tf32 (dropped lo·lo term ~2^-21 relative).
 //
-//   * one CTA computes a 128-row tile of C for up to 2×256 columns (two MMA
-//     N-subtiles side by side in TMEM), looping over K in 32-element chunks;
-//   * 256 threads stage each K-chunk: global fp32 -> hi/lo split -> the
-//     K-major SWIZZLE_128B canonical layout in shared memory (8-row × 128-B
-//     atoms, 16-B chunk c of row r at c ^ (r & 7)); two stages, mbarrier-
-//     tracked (tcgen05.commit) so the next chunk loads while the tensor core
-//     works on the current one;
-//   * one elected thread issues the MMAs; the epilogue reads TMEM with
-//     tcgen05.ld (warp w%4 owns TMEM lanes = tile rows 32(w%4)..+31).
+// Both kernels are warp-specialised and TMA-fed (one CTA per SM, 192 threads):
+//   warp 0      TMA producer: cp.async.bulk.tensor 2-D boxes, SWIZZLE_128B,
+//               into an S-stage ring guarded by mbarriers (expect_tx);
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer; commits
+//               release ring slots (tcgen05.commit → mbarrier);
+//   warps 2-5   "workers": compute the lo parts of each staged chunk in shared
+//               memory (generic proxy → fence.proxy.async → mbarrier) and run
+//               the epilogue (tcgen05.ld; warp w owns TMEM lanes 32·(w%4)..+31).
 //
-// Producers: ROWS  — operand element (row, k) = P[row*ld + k] (K contiguous):
-//                    A of gemm_tall / sketch, Bᵀ of gemm_tall;
-//            TRANS — element (row, k) = P[k*ld + row] (the Gram's Aᵀ, Bᵀ:
-//                    rows of the n×c block are the contraction index).
-// Epilogues: STORE — C = rs_i · acc (fp32, row-major, optional row scale d_i^-e)
-//            PART  — fp32 partial tile of a K-slab (Gram, reduced in fp64 later)
+// Gram  G = Aᵀ diag(w) B over the n rows: the row-major n×c block is the
+//   contraction (K) dimension, so chunks of BK rows × 32 columns are loaded
+//   as-is and fed to the MMA as MN-major operands (no transposition): a
+//   column block of 32 fp32 = one 128-B swizzle row, 8 rows = one 1-KB atom.
+//   One CTA reduces a K-slab ("chain") of rows into all output tiles it owns
+//   (Σ widths ≤ 512 TMEM columns), then writes an fp32 partial; partials are
+//   summed in fp64 by a deterministic two-level reduction.  Chains are kept
+//   short (≈2k rows) because the tensor core's fp32 accumulation truncates.
+// GEMM  C = diag(rs)·A·B (B small, fp64 on input): persistent over 128-row
+//   tiles of A (K-major operand straight from the row-major block); Bᵀ hi/lo
+//   are prepared once in fp32 and streamed per K-chunk from L2.  With
+//   tri_upper (B = R⁻¹ upper triangular) K-chunk kb only touches output
+//   columns ≥ 32·kb, halving MMA work.
 #include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -29,66 +42,17 @@
 namespace netmfp {
 namespace tc {
 
-constexpr int BM = 128;       // tile rows (UMMA M)
-constexpr int BK = 32;        // fp32 elements per K-chunk = one 128-B swizzle row
-constexpr int NT = 256;       // threads
-constexpr int MAXN = 288;     // max columns per CTA (2 subtiles of <= 144.. 256)
+constexpr int NT = 192;  // 6 warps
+constexpr int kWorkers = 128;
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
-// byte offset of the 16-B chunk (row r, chunk c) inside a K-major SW128 tile
-__device__ __forceinline__ uint32_t sw128(int r, int c) {
-  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
-}
-
-// SM100 shared-memory matrix descriptor: K-major, SWIZZLE_128B, SBO = 1024 B
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
-  d |= (uint64_t)1 << 16;                          // LBO (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;                // SBO: 8-row core-matrix stride
-  d |= (uint64_t)1 << 46;                          // version 1 (sm_100)
-  d |= (uint64_t)2 << 61;                          // layout: SWIZZLE_128B
-  return d;
-}
-
-// instruction descriptor: kind::tf32, D f32, A/B tf32, both K-major, M=128, N
-__host__ __device__ constexpr uint32_t make_idesc(int N) {
-  return (1u << 4)                 // c_format = F32
-         | (2u << 7)               // a_format = TF32
-         | (2u << 10)              // b_format = TF32
-         | ((uint32_t)(N >> 3) << 17)
-         | ((uint32_t)(BM >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
-      :
-      : "r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
-}
-
-__device__ __forceinline__ void mma_commit(uint64_t *bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
-
+// ---- mbarrier ---------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred done;\n\t"
@@ -98,449 +62,731 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-
-__device__ __forceinline__ void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
 }
 
-// 16 consecutive fp32 columns of this thread's TMEM lane
+// ---- TMA ------------------------------------------------------------------------
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, int c0, int c1, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *tm) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
+}
+
+// ---- tcgen05 ----------------------------------------------------------------------
+// SM100 shared-memory descriptors.
+//  K-major, SWIZZLE_128B (layout 2): 16-B chunks of a 128-B row XOR row%8;
+//    SBO = 8-row atom stride (1024 B), LBO unused.
+//  MN-major tf32, SWIZZLE_128B_BASE32B (layout 1; the only MN-major layout for
+//    32-bit operands): 32-B chunks of a 128-B row (32 MN elements) XOR row%4,
+//    rows = K indices; LBO = stride between 32-element MN blocks, SBO = stride
+//    between 4-deep K groups (512 B when rows are contiguous).  TMA writes it
+//    with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version (sm_100)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ uint64_t make_desc_mn32(uint32_t saddr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((512 >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version (sm_100)
+  d |= (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B
+  return d;
+}
+// kind::tf32, D = f32, M = 128, N, operand majors (1 = MN-major)
+__host__ __device__ constexpr uint32_t make_idesc(int N, int a_mn, int b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
   uint32_t r[16];
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-enum Prod { ROWS = 0, TRANS = 1 };
-enum Epi { STORE = 0, PART = 1 };
-
-struct Operand {
-  const float *p;
-  int64_t ld;
-  int64_t rows;   // valid rows (MN extent) of the operand
-  int64_t kdim;   // valid K extent
-  const int32_t *gather;  // ROWS: optional row index map
-  const int32_t *wdeg;    // TRANS: optional K-row weight d_k^-wexp
-  float wexp;
-};
-
-// stage one K-chunk of `rows_tile` operand rows starting at row0 into hi/lo tiles
-template <int PROD>
-__device__ __forceinline__ void stage_operand(const Operand &op, int64_t row0, int rows_tile, int64_t k0,
-                                              uint8_t *hi, uint8_t *lo) {
-  if (PROD == ROWS) {
-    // chunk id = r*8 + c (c: 16-B chunk within the 32-float K row)
-    for (int idx = threadIdx.x; idx < rows_tile * 8; idx += NT) {
-      const int r = idx >> 3, c = idx & 7;
-      const int64_t gr = row0 + r;
-      const int64_t kk = k0 + c * 4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (gr < op.rows && kk < op.kdim) {
-        const int64_t src = op.gather ? (int64_t)op.gather[gr] : gr;
-        const float *ptr = op.p + src * op.ld + kk;
-        if (kk + 4 <= op.kdim) {
-          v = __ldg(reinterpret_cast<const float4 *>(ptr));
-        } else {
-          v.x = ptr[0];
-          if (kk + 1 < op.kdim) v.y = ptr[1];
-          if (kk + 2 < op.kdim) v.z = ptr[2];
-        }
-      }
-      float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
-      float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-      const uint32_t off = sw128(r, c);
-      *reinterpret_cast<float4 *>(hi + off) = h;
-      *reinterpret_cast<float4 *>(lo + off) = l;
-    }
-  } else {
-    // element (row r, k) = P[(k0+k)*ld + row0 + r]; thread t of a warp takes
-    // k = t (one global row each), float4 along r: conflict-free scatter
-    const int nr4 = rows_tile / 4;
-    for (int idx = threadIdx.x; idx < nr4 * BK; idx += NT) {
-      const int k = idx % BK, r4 = idx / BK;
-      const int64_t gk = k0 + k;
-      const int64_t gr = row0 + r4 * 4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (gk < op.kdim && gr < op.rows) {
-        const float *ptr = op.p + gk * op.ld + gr;
-        if (gr + 4 <= op.rows) {
-          v = __ldg(reinterpret_cast<const float4 *>(ptr));
-        } else {
-          v.x = ptr[0];
-          if (gr + 1 < op.rows) v.y = ptr[1];
-          if (gr + 2 < op.rows) v.z = ptr[2];
-        }
-        if (op.wdeg) {
-          const int dg = op.wdeg[gk];
-          const float w = dg <= 0 ? 0.f : (op.wexp == 0.f ? 1.f : powf((float)dg, -op.wexp));
-          v.x *= w; v.y *= w; v.z *= w; v.w *= w;
-        }
-      }
-      const float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = r4 * 4 + i;
-        const uint32_t off = sw128(r, k >> 2) + (k & 3) * 4;
-        const float h = tf32_rna(e[i]);
-        *reinterpret_cast<float *>(hi + off) = h;
-        *reinterpret_cast<float *>(lo + off) = e[i] - h;
-      }
-    }
-  }
+__device__ __forceinline__ void tmem_alloc(uint32_t *slot, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(slot)), "r"(cols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t addr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(addr), "r"(cols));
 }
 
-struct EpiArgs {
-  float *C;        // STORE: C[row*ldc + col]; PART: partial tile base for this slab
-  int64_t ldc;
-  int64_t rows;    // valid output rows
-  int64_t cols;    // valid output cols
-  const int32_t *deg;
-  float rexp;
+__device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
+  return reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+__device__ __forceinline__ float deg_pow_dev(const int32_t *deg, int64_t i, float e) {
+  const int d = deg[i];
+  if (d <= 0) return 0.f;
+  if (e == 0.f) return 1.f;
+  if (e == 0.5f) return rsqrtf((float)d);
+  if (e == 1.f) return 1.f / (float)d;
+  return powf((float)d, -e);
+}
+
+// ===========================================================================
+// Gram
+// ===========================================================================
+constexpr int kMaxUnits = 12;
+struct GUnit {
+  int mblk;   // first 32-col block of A forming the 128-row M tile (4 blocks)
+  int nblk;   // first 32-col block of B for this unit's N range
+  int nw;     // N width (multiple of 16, <= 256)
+  int tcol;   // TMEM column of the accumulator
+  int64_t off;  // float offset of the unit inside one chain's partial
+};
+struct GramP {
+  int64_t n;        // rows (K extent)
+  int64_t kslab;    // rows per chain (multiple of BK)
+  int na_blk, nb_blk;  // 32-col blocks staged of A and (if !sym) B
+  int nunits;
+  GUnit u[kMaxUnits];
+  uint32_t tcols;   // TMEM allocation
+  int stages;
+  const int32_t *wdeg;  // optional row weights
+  float wexp;           // weight applied to A (non-sym) or sqrt applied to both (sym)
+  int64_t part_stride;  // floats per chain partial
+  float *part;
 };
 
-// C tile (BM × ntot) = A(m0.., k-range) · B(0..ntot, k-range)ᵀ
-template <int PA, int PB, int EPI>
-__global__ void __launch_bounds__(NT, 1) k_tc_gemm(Operand A, Operand B, int ntot, int n_sub, int nsub_w,
-                                                   int64_t kslab, EpiArgs ep) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-B aligned carve-up
-  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int a_bytes = BM * 128;               // 16 KB per part
-  const int b_bytes = ((ntot + 7) / 8) * 1024;  // rows rounded to 8-row atoms
-  const int stage_bytes = 2 * a_bytes + 2 * b_bytes;
-  uint8_t *st[2] = {base, base + stage_bytes};
-  uint64_t *bars = reinterpret_cast<uint64_t *>(base + 2 * stage_bytes);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2);
+template <int BK, bool SYM>
+__global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUtensorMap tmA,
+                                                   const __grid_constant__ CUtensorMap tmB, const GramP p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = align1024(smem_raw);
+  constexpr int BLK = BK * 128;  // bytes of one 32-col block of BK rows
+  const int nblk = p.na_blk + (SYM ? 0 : p.nb_blk);
+  const int stage_bytes = 2 * nblk * BLK;  // raw + lo
+  const int S = p.stages;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(base + S * stage_bytes + 3 * BLK);
+  uint64_t *full = bars, *split = bars + S, *empty = bars + 2 * S, *done = bars + 3 * S;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * S + 1);
 
-  const int warp = threadIdx.x / 32;
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
-  const int64_t kbeg = (int64_t)blockIdx.y * kslab;
-  const int64_t kend = min(kbeg + kslab, A.kdim);
-  const int nk = (int)((kend - kbeg + BK - 1) / BK);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t chain = blockIdx.x;
+  const int64_t r0 = chain * p.kslab;
+  const int64_t r1 = min(r0 + p.kslab, p.n);
+  const int nk = (int)((r1 - r0 + BK - 1) / BK);
 
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&split[s], kWorkers);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  const uint32_t tcols = ntot <= 32 ? 32u : ntot <= 64 ? 64u : ntot <= 128 ? 128u : ntot <= 256 ? 256u : 512u;
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
-                 "r"(tcols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-  }
+  if (warp == 1) tmem_alloc(tmem_slot, p.tcols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t idesc = make_idesc(nsub_w);
 
-  for (int kt = 0; kt < nk; ++kt) {
-    const int s = kt & 1;
-    if (kt >= 2) mbar_wait(&bars[s], (uint32_t)(((kt - 2) >> 1) & 1));
-    const int64_t k0 = kbeg + (int64_t)kt * BK;
-    uint8_t *ahi = st[s], *alo = st[s] + a_bytes, *bhi = st[s] + 2 * a_bytes, *blo = bhi + b_bytes;
-    stage_operand<PA>(A, m0, BM, k0, ahi, alo);
-    stage_operand<PB>(B, 0, (ntot + 7) / 8 * 8, k0, bhi, blo);
-    fence_async_smem();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      tc_fence_after();
-      const uint32_t a_hi = smem_u32(ahi), a_lo = smem_u32(alo);
-      const uint32_t b_hi = smem_u32(bhi), b_lo = smem_u32(blo);
-#pragma unroll
-      for (int ks = 0; ks < BK / 8; ++ks) {
-        const uint32_t koff = ks * 32;  // 8 tf32 = 32 B along K inside the swizzle row
-        for (int sb = 0; sb < n_sub; ++sb) {
-          const uint32_t boff = (uint32_t)sb * (uint32_t)(nsub_w / 8) * 1024u;
-          const uint32_t d = tmem + (uint32_t)(sb * nsub_w);
-          const uint32_t acc0 = (kt > 0 || ks > 0) ? 1u : 0u;
-          mma_tf32(d, make_desc(a_hi + koff), make_desc(b_hi + boff + koff), idesc, acc0);
-          mma_tf32(d, make_desc(a_hi + koff), make_desc(b_lo + boff + koff), idesc, 1u);
-          mma_tf32(d, make_desc(a_lo + koff), make_desc(b_hi + boff + koff), idesc, 1u);
-        }
-      }
-      mma_commit(&bars[s]);
-    }
-    __syncwarp();
-  }
-  // wait for the last chunk's MMAs (commit covers all earlier MMAs of the thread)
-  if (nk > 0) mbar_wait(&bars[(nk - 1) & 1], (uint32_t)(((nk - 1) >> 1) & 1));
-  tc_fence_after();
-
-  // epilogue: warp w reads lanes 32(w%4).. ; warps 0-3 and 4-7 split the columns
-  const int lane_base = (warp & 3) * 32;
-  const int row_in_tile = lane_base + (threadIdx.x & 31);
-  const int64_t row = m0 + row_in_tile;
-  const int ncols16 = (ntot + 15) / 16;
-  const int half = (ncols16 + 1) / 2;
-  const int c16_beg = (warp < 4) ? 0 : half, c16_end = (warp < 4) ? half : ncols16;
-  float scale = 1.f;
-  if (EPI == STORE && ep.deg && row < ep.rows) {
-    const int dg = ep.deg[row];
-    scale = dg <= 0 ? 0.f : (ep.rexp == 0.f ? 1.f : powf((float)dg, -ep.rexp));
-  }
-  for (int c16 = c16_beg; c16 < c16_end; ++c16) {
-    float v[16];
-    tmem_ld16(tmem + ((uint32_t)lane_base << 16) + (uint32_t)(c16 * 16), v);
-    const int col0 = c16 * 16;
-    if (nk == 0) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = 0.f;
-    }
-    if (EPI == STORE) {
-      if (row < ep.rows) {
-        float *dst = ep.C + row * ep.ldc + col0;
-        if (col0 + 16 <= ep.cols) {
-#pragma unroll
-          for (int i = 0; i < 16; i += 4)
-            *reinterpret_cast<float4 *>(dst + i) =
-                make_float4(scale * v[i], scale * v[i + 1], scale * v[i + 2], scale * v[i + 3]);
-        } else {
-          for (int i = 0; i < 16 && col0 + i < ep.cols; ++i) dst[i] = scale * v[i];
-        }
-      }
-    } else {
-      // PART: dense (BM_pad × ntot_pad) fp32 tile at ep.C + slab*stride; ldc = padded cols
-      float *dst = ep.C + (int64_t)blockIdx.y * ep.rows * ep.ldc + row * ep.ldc + col0;
-#pragma unroll
-      for (int i = 0; i < 16; i += 4)
-        *reinterpret_cast<float4 *>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tcols));
-}
-
-static size_t smem_for(int ntot) {
-  const int a_bytes = BM * 128;
-  const int b_bytes = ((ntot + 7) / 8) * 1024;
-  return (size_t)2 * (2 * a_bytes + 2 * b_bytes) + 64 + 1024;
-}
-
-// split ntot (<= 512) into 1-2 MMA subtiles of equal width (multiple of 16, <= 256)
-static void subtiles(int64_t cols, int &ntot, int &n_sub, int &nsub_w) {
-  const int c16 = (int)((cols + 15) / 16) * 16;
-  n_sub = c16 <= 256 ? 1 : 2;
-  nsub_w = (int)(((c16 / n_sub) + 15) / 16 * 16);
-  ntot = nsub_w * n_sub;
-}
-
-template <int PA, int PB, int EPI>
-static void launch(Ctx &c, const Operand &A, const Operand &B, int64_t mtiles, int64_t nslab, int64_t kslab,
-                   int ntot, int n_sub, int nsub_w, const EpiArgs &ep) {
-  const size_t smem = smem_for(ntot);
-  NM_REQUIRE(smem <= 227 * 1024, "tc_gemm: tile too wide for shared memory");
-  static bool attr = false;
-  if (!attr) {
-    NM_CUDA(cudaFuncSetAttribute(k_tc_gemm<PA, PB, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
-  dim3 grid((unsigned)mtiles, (unsigned)nslab);
-  NM_LAUNCH(c, EPI == STORE ? "tc_gemm_tall" : "tc_gram",
-            k_tc_gemm<PA, PB, EPI><<<grid, NT, smem, c.stream>>>(A, B, ntot, n_sub, nsub_w, kslab, ep));
-}
-
-// ---------------------------------------------------------------------------
-// Gram kernel: G tile (128 × 128) of Aᵀ W B over one K-slab of the n rows.
-// The tensor core's fp32 accumulation truncates, so a long K chain biases sums
-// of squares by ~1e-8 per row; the TMEM accumulator is therefore drained into
-// fp32 registers (round-to-nearest adds) every GD K-chunks (256 rows) and the
-// chain restarts.  CTAs of the same K-slab are adjacent in launch order so the
-// slab's rows are read from HBM once and shared through L2.
-// ---------------------------------------------------------------------------
-constexpr int GN = 128;
-constexpr int GD = 4;
-
-__device__ __forceinline__ void gram_drain(uint32_t tmem, int lane_base, int cbase, float (&rs)[64]) {
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    float v[16];
-    tmem_ld16(tmem + ((uint32_t)lane_base << 16) + (uint32_t)(cbase + 16 * j), v);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) rs[16 * j + i] += v[i];
-  }
-}
-
-__global__ void __launch_bounds__(NT, 1) k_tc_gram(Operand A, Operand B, int nta, int ntb, bool sym,
-                                                   int64_t kslab, float *__restrict__ part, int64_t rows_pad,
-                                                   int64_t ldp) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int TB = BM * 128;  // 16 KB: one 128-row × 32-fp32 tile part
-  uint8_t *st[2] = {base, base + 4 * TB};
-  uint64_t *bars = reinterpret_cast<uint64_t *>(base + 8 * TB);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2);
-
-  // tile (ta, tb) of this CTA; CTAs of one slab are consecutive
-  const int ntiles = sym ? nta * (nta + 1) / 2 : nta * ntb;
-  int t = blockIdx.x % ntiles;
-  const int64_t slab = blockIdx.x / ntiles;
-  int ta = 0, tb = 0;
-  if (sym) {
-    while (t >= nta - ta) { t -= nta - ta; ++ta; }
-    tb = ta + t;
-  } else {
-    ta = t / ntb;
-    tb = t % ntb;
-  }
-  const int64_t m0 = (int64_t)ta * BM, n0 = (int64_t)tb * GN;
-  const int64_t kbeg = slab * kslab;
-  const int64_t kend = min(kbeg + kslab, A.kdim);
-  const int nk = (int)((kend - kbeg + BK - 1) / BK);
-  const int warp = threadIdx.x / 32;
-
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
-                 "r"(GN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t idesc = make_idesc(GN);
-  const int lane_base = (warp & 3) * 32;
-  const int cbase = (warp < 4) ? 0 : 64;
-  float rs[64];
-#pragma unroll
-  for (int i = 0; i < 64; ++i) rs[i] = 0.f;
-
-  for (int kt = 0; kt < nk; ++kt) {
-    const int s = kt & 1;
-    if (kt >= 2) mbar_wait(&bars[s], (uint32_t)(((kt - 2) >> 1) & 1));
-    const int64_t k0 = kbeg + (int64_t)kt * BK;
-    uint8_t *ahi = st[s], *alo = st[s] + TB, *bhi = st[s] + 2 * TB, *blo = st[s] + 3 * TB;
-    stage_operand<TRANS>(A, m0, BM, k0, ahi, alo);
-    stage_operand<TRANS>(B, n0, GN, k0, bhi, blo);
-    fence_async_smem();
-    __syncthreads();
-    const bool chain_start = (kt % GD) == 0;
-    if (chain_start && kt > 0) {
-      // close the previous chain: its MMAs are complete, fold TMEM into registers
-      mbar_wait(&bars[(kt - 1) & 1], (uint32_t)(((kt - 1) >> 1) & 1));
-      tc_fence_after();
-      gram_drain(tmem, lane_base, cbase, rs);
-      tc_fence_before();
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      tc_fence_after();
-      const uint32_t a_hi = smem_u32(ahi), a_lo = smem_u32(alo);
-      const uint32_t b_hi = smem_u32(bhi), b_lo = smem_u32(blo);
-#pragma unroll
-      for (int ks = 0; ks < BK / 8; ++ks) {
-        const uint32_t koff = ks * 32;
-        const uint32_t acc0 = (!chain_start || ks > 0) ? 1u : 0u;
-        mma_tf32(tmem, make_desc(a_hi + koff), make_desc(b_hi + koff), idesc, acc0);
-        mma_tf32(tmem, make_desc(a_hi + koff), make_desc(b_lo + koff), idesc, 1u);
-        mma_tf32(tmem, make_desc(a_lo + koff), make_desc(b_hi + koff), idesc, 1u);
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      if (!SYM) tma_prefetch_desc(&tmB);
+      for (int kc = 0; kc < nk; ++kc) {
+        const int s = kc % S, use = kc / S;
+        if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+        uint8_t *st = base + s * stage_bytes;
+        mbar_expect_tx(&full[s], (uint32_t)(nblk * BLK));
+        const int row = (int)(r0 + (int64_t)kc * BK);
+        for (int b = 0; b < p.na_blk; ++b) tma_load_2d(st + b * BLK, &tmA, b * 32, row, &full[s]);
+        if (!SYM)
+          for (int b = 0; b < p.nb_blk; ++b) tma_load_2d(st + (p.na_blk + b) * BLK, &tmB, b * 32, row, &full[s]);
       }
-      mma_commit(&bars[s]);
     }
-    __syncwarp();
-  }
-  if (nk > 0) {
-    mbar_wait(&bars[(nk - 1) & 1], (uint32_t)(((nk - 1) >> 1) & 1));
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int kc = 0; kc < nk; ++kc) {
+        const int s = kc % S, use = kc / S;
+        mbar_wait(&split[s], (uint32_t)(use & 1));
+        tc_fence_after();
+        const uint32_t raw = smem_u32(base + s * stage_bytes);
+        const uint32_t lo = raw + nblk * BLK;
+        const uint32_t braw = SYM ? raw : raw + p.na_blk * BLK;
+        const uint32_t blo = SYM ? lo : lo + p.na_blk * BLK;
+#pragma unroll
+        for (int ks = 0; ks < BK / 8; ++ks) {
+          const uint32_t ko = ks * 1024;
+          for (int ui = 0; ui < p.nunits; ++ui) {
+            const GUnit &u = p.u[ui];
+            const uint32_t idesc = make_idesc(u.nw, 1, 1);
+            const uint32_t ao = u.mblk * BLK + ko, bo = u.nblk * BLK + ko;
+            const uint32_t d = tmem + (uint32_t)u.tcol;
+            const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
+            mma_tf32(d, make_desc_mn32(raw + ao, BLK), make_desc_mn32(braw + bo, BLK), idesc, acc0);
+            mma_tf32(d, make_desc_mn32(raw + ao, BLK), make_desc_mn32(blo + bo, BLK), idesc, 1u);
+            mma_tf32(d, make_desc_mn32(lo + ao, BLK), make_desc_mn32(braw + bo, BLK), idesc, 1u);
+          }
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(done);
+    }
+  } else {
+    // workers: lo split (+ row weights) for every chunk, then the epilogue
+    const int wt = threadIdx.x - 64;  // 0..127
+    const int q = warp & 3;
+    for (int kc = 0; kc < nk; ++kc) {
+      const int s = kc % S, use = kc / S;
+      mbar_wait(&full[s], (uint32_t)(use & 1));
+      uint8_t *raw = base + s * stage_bytes;
+      uint8_t *lo = raw + nblk * BLK;
+      const int64_t row0 = r0 + (int64_t)kc * BK;
+      const int n16 = nblk * BLK / 16;
+      for (int i = wt; i < n16; i += kWorkers) {
+        float4 v = reinterpret_cast<float4 *>(raw)[i];
+        if (p.wdeg) {
+          const int blk = i / (BLK / 16);
+          const int r = (i % (BLK / 16)) / 8;  // row inside the chunk (128-B rows)
+          const int64_t grow = row0 + r;
+          if (SYM || blk < p.na_blk) {
+            float w = 0.f;
+            if (grow < p.n) w = deg_pow_dev(p.wdeg, grow, SYM ? 0.5f * p.wexp : p.wexp);
+            v.x *= w; v.y *= w; v.z *= w; v.w *= w;
+            reinterpret_cast<float4 *>(raw)[i] = v;
+          }
+        }
+        float4 l;
+        l.x = v.x - tf32_trunc(v.x);
+        l.y = v.y - tf32_trunc(v.y);
+        l.z = v.z - tf32_trunc(v.z);
+        l.w = v.w - tf32_trunc(v.w);
+        reinterpret_cast<float4 *>(lo)[i] = l;
+      }
+      fence_async_smem();
+      mbar_arrive(&split[s]);
+    }
+    // epilogue: TMEM lanes 32q..32q+31 = rows of every unit's 128-row M tile
+    mbar_wait(done, 0);
     tc_fence_after();
-    gram_drain(tmem, lane_base, cbase, rs);
-  }
-  const int64_t row = m0 + lane_base + (threadIdx.x & 31);
-  float *dst = part + slab * rows_pad * ldp + row * ldp + n0 + cbase;
+    const int r = 32 * q + lane;
+    float *dst0 = p.part + chain * p.part_stride;
+    for (int ui = 0; ui < p.nunits; ++ui) {
+      const GUnit &u = p.u[ui];
+      float *dst = dst0 + u.off + (int64_t)r * u.nw;
+      for (int c = 0; c < u.nw; c += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(u.tcol + c), v);
+        if (nk == 0) {
 #pragma unroll
-  for (int i = 0; i < 64; i += 4) *reinterpret_cast<float4 *>(dst + i) = make_float4(rs[i], rs[i + 1], rs[i + 2], rs[i + 3]);
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+          *reinterpret_cast<float4 *>(dst + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      }
+    }
+    (void)wt;
+  }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(GN));
+  if (warp == 1) tmem_dealloc(tmem, p.tcols);
 }
 
-}  // namespace tc
+// partial sums over chain groups: tmp[g][i*b+j] = Σ_{chains in g} part(i, j)
+struct GramRed {
+  int nunits;
+  GUnit u[kMaxUnits];
+  int64_t a, b;
+  bool sym;
+  int64_t nchain, part_stride;
+};
 
-// Bt[j][k] = (float)Bs[k][j] for the tall GEMM's B operand (K-major), zero padded
-__global__ void k_transpose64to32(const double *__restrict__ Bs, int64_t ldb, int64_t K, int64_t N,
-                                  float *__restrict__ Bt, int64_t ldt) {
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= N * ldt) return;
-  int64_t j = idx / ldt, k = idx % ldt;
-  Bt[idx] = (k < K) ? (float)Bs[k * ldb + j] : 0.f;
-}
-
-// C[n×b] = rs ⊙ (A[n×a] · Bs[a×b]) on tensor cores (b <= 512)
-void tc_gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcols, const int32_t *deg,
-                  float rexp, const Mat &C) {
-  using namespace tc;
-  NM_REQUIRE(bcols <= 512 && A.cols <= 4096, "tc_gemm_tall: shape out of range");
-  int ntot, n_sub, nsub_w;
-  subtiles(bcols, ntot, n_sub, nsub_w);
-  if (n_sub == 2 && smem_for(ntot) > 227 * 1024) NM_REQUIRE(false, "tc_gemm_tall: too wide");
-  const int64_t K = A.cols, ldt = pad32(K);
-  DBuf<float> Bt((size_t)ntot * ldt, c.stream);
-  NM_CUDA(cudaMemsetAsync(Bt.p, 0, (size_t)ntot * ldt * 4, c.stream));
-  NM_LAUNCH(c, "transpose64", k_transpose64to32<<<ceil_div(bcols * ldt, 256), 256, 0, c.stream>>>(Bs, ldb, K, bcols, Bt, ldt));
-  Operand oa{A.p, A.ld, A.rows, K, nullptr, nullptr, 0.f};
-  Operand ob{Bt.p, ldt, bcols, K, nullptr, nullptr, 0.f};
-  EpiArgs ep{C.p, C.ld, C.rows, bcols, deg, rexp};
-  launch<ROWS, ROWS, STORE>(c, oa, ob, ceil_div(A.rows, BM), 1, K, ntot, n_sub, nsub_w, ep);
-}
-
-__global__ void k_tc_gram_reduce(const float *__restrict__ part, int nslab, int64_t a, int64_t b,
-                                 int64_t rows_pad, int64_t ldp, bool sym, double *__restrict__ G, int64_t ldg) {
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= a * b) return;
-  int64_t i = idx / b, j = idx % b;
-  if (sym && (i / tc::BM) > (j / tc::GN)) {  // lower tile: mirror of the computed upper one
+__device__ __forceinline__ int64_t gram_locate(const GramRed &R, int64_t i, int64_t j) {
+  for (int pass = 0; pass < 2; ++pass) {
+    const int64_t mt = i / 128;
+    for (int ui = 0; ui < R.nunits; ++ui) {
+      const GUnit &u = R.u[ui];
+      const int64_t n0 = (int64_t)u.nblk * 32;
+      if (u.mblk / 4 == mt && j >= n0 && j < n0 + u.nw) return u.off + (i - 128 * mt) * u.nw + (j - n0);
+    }
     const int64_t t = i;
     i = j;
     j = t;
   }
+  return -1;
+}
+
+__global__ void k_gram_reduce1(const float *__restrict__ part, GramRed R, int64_t per_group, double *__restrict__ tmp) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= R.a * R.b) return;
+  const int64_t off = gram_locate(R, idx / R.b, idx % R.b);
+  const int64_t c0 = blockIdx.y * per_group, c1 = min(c0 + per_group, R.nchain);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t c = c0;
+  for (; c + 4 <= c1; c += 4) {
+    s0 += (double)__ldg(part + c * R.part_stride + off);
+    s1 += (double)__ldg(part + (c + 1) * R.part_stride + off);
+    s2 += (double)__ldg(part + (c + 2) * R.part_stride + off);
+    s3 += (double)__ldg(part + (c + 3) * R.part_stride + off);
+  }
+  for (; c < c1; ++c) s0 += (double)__ldg(part + c * R.part_stride + off);
+  tmp[blockIdx.y * R.a * R.b + idx] = (s0 + s1) + (s2 + s3);
+}
+
+__global__ void k_gram_reduce2(const double *__restrict__ tmp, int groups, int64_t a, int64_t b, double *__restrict__ G,
+                               int64_t ldg) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= a * b) return;
   double s = 0.0;
-  for (int t = 0; t < nslab; ++t) s += (double)part[(size_t)t * rows_pad * ldp + i * ldp + j];
+  for (int g = 0; g < groups; ++g) s += tmp[(int64_t)g * a * b + idx];
   G[(idx / b) * ldg + idx % b] = s;
 }
 
-// G[a×b] (fp64) = Aᵀ W B over n rows on tensor cores (W = diag(d^-wexp) if deg)
+// ===========================================================================
+// tall GEMM  C = diag(rs) · A · B
+// ===========================================================================
+struct GemmP {
+  int64_t n;      // rows of A / C
+  int K;          // contraction length
+  int nk;         // K chunks of 32
+  int ntot;       // MMA N total (multiple of 16)
+  int nsub, nsub_w;  // N subtiles (each <= 256)
+  int nbox, box_rows;  // TMA boxes for Bᵀ rows (box_rows each)
+  int tri;        // B upper triangular: chunk kb touches columns >= 32 kb
+  int64_t ntiles;
+  int stages;
+  uint32_t tcols;
+  float *C;
+  int64_t ldc;
+  int64_t ccols;  // valid output columns
+  const int32_t *deg;
+  float rexp;
+};
+
+__global__ void __launch_bounds__(NT, 1) k_gemm_tc(const __grid_constant__ CUtensorMap tmA,
+                                                   const __grid_constant__ CUtensorMap tmBh,
+                                                   const __grid_constant__ CUtensorMap tmBl, const GemmP p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = align1024(smem_raw);
+  constexpr int ABYTES = 128 * 128;  // 128 rows × 32 fp32
+  const int bbytes = p.ntot * 128;
+  const int stage_bytes = 2 * ABYTES + 2 * bbytes;
+  const int S = p.stages;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(base + S * stage_bytes);
+  uint64_t *full = bars, *split = bars + S, *empty = bars + 2 * S;
+  uint64_t *done = bars + 3 * S, *tfree = bars + 3 * S + 1;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * S + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&split[s], kWorkers);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    mbar_init(tfree, kWorkers);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, p.tcols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmBh);
+      tma_prefetch_desc(&tmBl);
+      int64_t g = 0;
+      for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        for (int kc = 0; kc < p.nk; ++kc, ++g) {
+          const int s = (int)(g % S);
+          const int64_t use = g / S;
+          if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+          uint8_t *st = base + s * stage_bytes;
+          mbar_expect_tx(&full[s], (uint32_t)(ABYTES + 2 * p.nbox * p.box_rows * 128));
+          tma_load_2d(st, &tmA, kc * 32, (int)(t * 128), &full[s]);
+          uint8_t *bh = st + 2 * ABYTES, *bl = bh + bbytes;
+          for (int b = 0; b < p.nbox; ++b) {
+            tma_load_2d(bh + b * p.box_rows * 128, &tmBh, kc * 32, b * p.box_rows, &full[s]);
+            tma_load_2d(bl + b * p.box_rows * 128, &tmBl, kc * 32, b * p.box_rows, &full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int64_t g = 0, it = 0;
+      for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
+        if (it > 0) mbar_wait(tfree, (uint32_t)((it - 1) & 1));
+        tc_fence_after();
+        for (int kc = 0; kc < p.nk; ++kc, ++g) {
+          const int s = (int)(g % S);
+          const int64_t use = g / S;
+          mbar_wait(&split[s], (uint32_t)(use & 1));
+          tc_fence_after();
+          const uint32_t ahi = smem_u32(base + s * stage_bytes), alo = ahi + ABYTES;
+          const uint32_t bhi = alo + ABYTES, blo = bhi + bbytes;
+          for (int sb = 0; sb < p.nsub; ++sb) {
+            int c0 = sb * p.nsub_w;
+            const int c1 = c0 + p.nsub_w;
+            if (p.tri) {
+              const int cmin = (kc * 32) & ~15;
+              if (c1 <= cmin) continue;
+              c0 = max(c0, cmin);
+            }
+            const int N = c1 - c0;
+            const uint32_t idesc = make_idesc(N, 0, 0);
+            const uint32_t d = tmem + (uint32_t)c0;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              const uint32_t ko = ks * 32;
+              // every column is first touched by K-chunk 0 (tri: chunk kb only
+              // adds to columns >= 32 kb), so chunk 0 / kstep 0 starts the sums
+              const uint32_t acc0 = (kc == 0 && ks == 0) ? 0u : 1u;
+              mma_tf32(d, make_desc(ahi + ko, 16, 1024), make_desc(bhi + c0 * 128 + ko, 16, 1024), idesc, acc0);
+              mma_tf32(d, make_desc(ahi + ko, 16, 1024), make_desc(blo + c0 * 128 + ko, 16, 1024), idesc, 1u);
+              mma_tf32(d, make_desc(alo + ko, 16, 1024), make_desc(bhi + c0 * 128 + ko, 16, 1024), idesc, 1u);
+            }
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(done);
+      }
+    }
+  } else {
+    const int wt = threadIdx.x - 64;
+    const int q = warp & 3;
+    int64_t g = 0, it = 0;
+    for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
+      for (int kc = 0; kc < p.nk; ++kc, ++g) {
+        const int s = (int)(g % S);
+        const int64_t use = g / S;
+        mbar_wait(&full[s], (uint32_t)(use & 1));
+        float4 *raw = reinterpret_cast<float4 *>(base + s * stage_bytes);
+        float4 *lo = raw + ABYTES / 16;
+        for (int i = wt; i < ABYTES / 16; i += kWorkers) {
+          const float4 v = raw[i];
+          lo[i] = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
+                              v.w - tf32_trunc(v.w));
+        }
+        fence_async_smem();
+        mbar_arrive(&split[s]);
+      }
+      mbar_wait(done, (uint32_t)(it & 1));
+      tc_fence_after();
+      const int64_t row = t * 128 + 32 * q + lane;
+      float sc = 1.f;
+      if (p.deg && row < p.n) sc = deg_pow_dev(p.deg, row, p.rexp);
+      float *dst = p.C + row * p.ldc;
+      for (int c = 0; c < p.ntot; c += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c, v);
+        if (row < p.n && c < p.ccols) {
+          if (c + 16 <= p.ccols) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+              *reinterpret_cast<float4 *>(dst + c + i) =
+                  make_float4(sc * v[i], sc * v[i + 1], sc * v[i + 2], sc * v[i + 3]);
+          } else {
+            for (int i = 0; c + i < p.ccols; ++i) dst[c + i] = sc * v[i];
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tfree);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, p.tcols);
+}
+
+}  // namespace tc
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *f = nullptr;
+    NM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess) throw Error(NETMFP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// 2-D fp32 row-major [rows][cols] (row stride ld floats), box {32, box_rows},
+// SWIZZLE_128B (K-major operands) or SWIZZLE_128B_ATOM_32B (MN-major tf32)
+static CUtensorMap make_map(const float *p, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                            bool mn32 = false) {
+  NM_REQUIRE(((uintptr_t)p & 15) == 0 && ld % 4 == 0, "tensor map: 16-byte aligned base and ld % 4 == 0 required");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32u, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1u, 1u};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(p), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           mn32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(NETMFP_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
+static uint32_t tmem_cols_for(int cols) {
+  uint32_t t = 32;
+  while (t < (uint32_t)cols) t <<= 1;
+  return t;
+}
+
+static constexpr size_t kSmemMax = 227 * 1024;
+// An M tile reads 4 column blocks of A; when A has fewer blocks the last tile
+// reads past its region (into B / lo / the next stage: finite data that only
+// feeds output rows >= a, which are never reduced).  The ring is followed by
+// this many spare blocks so the last stage's over-read stays in bounds.
+static constexpr int kPadBlocks = 3;
+
+template <int BK, bool SYM>
+static void launch_gram(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, tc::GramP &p, int64_t nchain,
+                        int ngroup_units_offset) {
+  (void)ngroup_units_offset;
+  const int nblk = p.na_blk + (SYM ? 0 : p.nb_blk);
+  const size_t stage = (size_t)2 * nblk * BK * 128;
+  int S = (int)std::min<size_t>(6, (kSmemMax - 1024 - 256 - kPadBlocks * BK * 128) / stage);
+  NM_REQUIRE(S >= 2, "tc_gram: too many columns for the staged chunk");
+  p.stages = S;
+  const size_t smem = 1024 + S * stage + kPadBlocks * BK * 128 + (3 * S + 2) * 8 + 16;
+  static bool attr = false;
+  if (!attr) {
+    NM_CUDA(cudaFuncSetAttribute(tc::k_gram_tc<BK, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
+    attr = true;
+  }
+  NM_LAUNCH(c, "tc_gram", tc::k_gram_tc<BK, SYM><<<(unsigned)nchain, tc::NT, smem, c.stream>>>(ma, mb, p));
+}
+
+// G[a×b] (fp64, ldg) = Aᵀ diag(d^-wexp) B over the n rows
 void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg) {
   using namespace tc;
   NM_REQUIRE(A.rows == B.rows, "tc_gram: row mismatch");
-  const int64_t n = A.rows;
-  const bool sym = (A.p == B.p && A.cols == B.cols && A.ld == B.ld && deg == nullptr);
-  const int nta = (int)ceil_div(A.cols, BM), ntb = (int)ceil_div(B.cols, GN);
-  const int ntiles = sym ? nta * (nta + 1) / 2 : nta * ntb;
-  int64_t nslab = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 2048), ceil_div((int64_t)c.num_sms * 2, ntiles)));
-  int64_t kslab = (ceil_div(n, nslab) + BK - 1) / BK * BK;
-  nslab = ceil_div(n, kslab);
-  const int64_t rows_pad = (int64_t)nta * BM, ldp = (int64_t)ntb * GN;
-  DBuf<float> part((size_t)nslab * rows_pad * ldp, c.stream);
-  // operand element (row = column index of the n×c block, k = its row index)
-  Operand oa{A.p, A.ld, A.cols, n, nullptr, deg, wexp};
-  Operand ob{B.p, B.ld, B.cols, n, nullptr, nullptr, 0.f};
-  const size_t smem = 8 * (size_t)BM * 128 + 64 + 1024;
+  const int64_t n = A.rows, a = A.cols, b = B.cols;
+  if (n == 0) {
+    NM_CUDA(cudaMemset2DAsync(G, ldg * 8, 0, b * 8, a, c.stream));
+    return;
+  }
+  const bool sym = (A.p == B.p && A.cols == B.cols && A.ld == B.ld);
+  const int na_blk = (int)ceil_div(a, 32), nb_blk = (int)ceil_div(b, 32);
+  // output units: M tiles of 128 rows (4 blocks of A), N ranges of <= 256 cols
+  std::vector<GUnit> all;
+  const int mt = (int)ceil_div(a, 128);
+  for (int m = 0; m < mt; ++m) {
+    const int n_lo = sym ? 4 * m : 0;  // sym: upper block-triangle only
+    const int n_hi = nb_blk;
+    int ncols = (n_hi - n_lo) * 32;
+    if (ncols <= 0) continue;
+    const int parts = (ncols + 255) / 256;
+    const int blks = n_hi - n_lo;
+    int start = n_lo;
+    for (int pi = 0; pi < parts; ++pi) {
+      const int nb = (blks - (start - n_lo) + (parts - pi) - 1) / (parts - pi);
+      all.push_back(GUnit{4 * m, start, nb * 32, 0, 0});
+      start += nb;
+    }
+  }
+  // global partial offsets, then pack units into groups of <= 512 TMEM columns
+  int64_t total = 0;
+  for (auto &u : all) {
+    u.off = total;
+    total += (int64_t)128 * u.nw;
+  }
+  NM_REQUIRE((int)all.size() <= kMaxUnits, "tc_gram: too many output units");
+  std::vector<std::vector<GUnit>> groups;
+  {
+    std::vector<GUnit> cur;
+    int w = 0;
+    for (auto u : all) {
+      if (w + u.nw > 512) {
+        groups.push_back(cur);
+        cur.clear();
+        w = 0;
+      }
+      u.tcol = w;
+      w += u.nw;
+      cur.push_back(u);
+    }
+    if (!cur.empty()) groups.push_back(cur);
+  }
+  // chains: a multiple of the SM count, ~2k rows each (short TMEM chains)
+  constexpr int BKs = 32, BKn = 16;
+  const int BK = sym ? BKs : BKn;
+  const int64_t waves = std::max<int64_t>(1, (n + (int64_t)c.num_sms * 2048 - 1) / ((int64_t)c.num_sms * 2048));
+  int64_t nchain = std::max<int64_t>(1, std::min<int64_t>((int64_t)c.num_sms * waves, ceil_div(n, BK)));
+  const int64_t kslab = (ceil_div(n, nchain) + BK - 1) / BK * BK;
+  nchain = ceil_div(n, kslab);
+  CUtensorMap ma = make_map(A.p, n, a, A.ld, BK, true);
+  CUtensorMap mb = sym ? ma : make_map(B.p, n, b, B.ld, BK, true);
+  DBuf<float> part((size_t)nchain * total, c.stream);
+  for (auto &grp : groups) {
+    GramP p{};
+    p.n = n;
+    p.kslab = kslab;
+    p.na_blk = na_blk;
+    p.nb_blk = sym ? 0 : nb_blk;
+    p.nunits = (int)grp.size();
+    int w = 0;
+    for (int i = 0; i < p.nunits; ++i) {
+      p.u[i] = grp[i];
+      w += grp[i].nw;
+    }
+    p.tcols = tmem_cols_for(w);
+    p.wdeg = deg;
+    p.wexp = wexp;
+    p.part_stride = total;
+    p.part = part.p;
+    if (sym)
+      launch_gram<BKs, true>(c, ma, mb, p, nchain, 0);
+    else
+      launch_gram<BKn, false>(c, ma, mb, p, nchain, 0);
+  }
+  GramRed R{};
+  R.nunits = (int)all.size();
+  for (int i = 0; i < R.nunits; ++i) R.u[i] = all[i];
+  R.a = a;
+  R.b = b;
+  R.sym = sym;
+  R.nchain = nchain;
+  R.part_stride = total;
+  const int RG = (int)std::min<int64_t>(16, nchain);
+  const int64_t per = ceil_div(nchain, RG);
+  DBuf<double> tmp((size_t)RG * a * b, c.stream);
+  dim3 g1(ceil_div(a * b, 256), RG);
+  NM_LAUNCH(c, "tc_gram_reduce", k_gram_reduce1<<<g1, 256, 0, c.stream>>>(part.p, R, per, tmp.p));
+  NM_LAUNCH(c, "tc_gram_reduce", k_gram_reduce2<<<ceil_div(a * b, 256), 256, 0, c.stream>>>(tmp.p, RG, a, b, G, ldg));
+}
+
+// Bᵀ hi/lo: Bt_hi[j][k] = rna_tf32(B[k][j]), Bt_lo[j][k] = (float)(B[k][j] - hi), zero padded
+__global__ void k_bt_split(const double *__restrict__ Bs, int64_t ldb, int64_t K, int64_t N, int64_t nrows, int64_t ldt,
+                           float *__restrict__ hi, float *__restrict__ lo) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= nrows * ldt) return;
+  const int64_t j = idx / ldt, k = idx % ldt;
+  float h = 0.f, l = 0.f;
+  if (j < N && k < K) {
+    const double x = Bs[k * ldb + j];
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"((float)x));
+    h = __uint_as_float(r);
+    l = (float)(x - (double)h);
+  }
+  hi[idx] = h;
+  lo[idx] = l;
+}
+
+// C[n×b] = rs ⊙ (A[n×a] · Bs[a×b])
+static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcols, const int32_t *deg,
+                              float rexp, const Mat &C, bool tri) {
+  using namespace tc;
+  const int64_t n = A.rows, K = A.cols;
+  const int c16 = (int)((bcols + 15) / 16) * 16;
+  const int nsub = (c16 + 255) / 256;
+  const int nsub_w = ((c16 / nsub) + 15) / 16 * 16;
+  const int ntot = nsub * nsub_w;
+  NM_REQUIRE(ntot <= 304, "tc_gemm_tall: at most 304 output columns per call");
+  const int nbox = (ntot + 255) / 256;
+  const int box_rows = ntot / nbox;  // multiple of 8 (ntot multiple of 16, nbox <= 2)
+  NM_REQUIRE(box_rows % 8 == 0 && box_rows * nbox == ntot, "tc_gemm_tall: box split");
+  const int64_t ldt = pad32(K);
+  DBuf<float> bh((size_t)ntot * ldt, c.stream), bl((size_t)ntot * ldt, c.stream);
+  NM_LAUNCH(c, "bt_split", k_bt_split<<<ceil_div((int64_t)ntot * ldt, 256), 256, 0, c.stream>>>(Bs, ldb, K, bcols, ntot,
+                                                                                                   ldt, bh.p, bl.p));
+  CUtensorMap ma = make_map(A.p, n, K, A.ld, 128);
+  CUtensorMap mh = make_map(bh.p, ntot, ldt, ldt, box_rows);
+  CUtensorMap ml = make_map(bl.p, ntot, ldt, ldt, box_rows);
+  GemmP p{};
+  p.n = n;
+  p.K = (int)K;
+  p.nk = (int)ceil_div(K, 32);
+  p.ntot = ntot;
+  p.nsub = nsub;
+  p.nsub_w = nsub_w;
+  p.nbox = nbox;
+  p.box_rows = box_rows;
+  p.tri = tri ? 1 : 0;
+  p.ntiles = ceil_div(n, 128);
+  p.tcols = tmem_cols_for(ntot);
+  p.C = C.p;
+  p.ldc = C.ld;
+  p.ccols = bcols;
+  p.deg = deg;
+  p.rexp = rexp;
+  const size_t stage = (size_t)2 * 128 * 128 + (size_t)2 * ntot * 128;
+  const int S = (int)std::min<size_t>(4, (kSmemMax - 1024 - 256) / stage);
+  NM_REQUIRE(S >= 2, "tc_gemm_tall: stage does not fit");
+  p.stages = S;
+  const size_t smem = 1024 + S * stage + (3 * S + 3) * 8 + 16;
   static bool attr = false;
   if (!attr) {
-    NM_CUDA(cudaFuncSetAttribute(k_tc_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    NM_CUDA(cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
     attr = true;
   }
-  NM_LAUNCH(c, "tc_gram", k_tc_gram<<<(unsigned)(ntiles * nslab), NT, smem, c.stream>>>(oa, ob, nta, ntb, sym, kslab,
-                                                                                     part, rows_pad, ldp));
-  NM_LAUNCH(c, "tc_gram_reduce", k_tc_gram_reduce<<<ceil_div(A.cols * B.cols, 256), 256, 0, c.stream>>>(
-                                     part, (int)nslab, A.cols, B.cols, rows_pad, ldp, sym, G, ldg));
+  const int64_t grid = std::min<int64_t>(p.ntiles, c.num_sms);
+  NM_LAUNCH(c, "tc_gemm_tall", k_gemm_tc<<<(unsigned)grid, NT, smem, c.stream>>>(ma, mh, ml, p));
+}
+
+void tc_gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcols, const int32_t *deg, float rexp,
+                  const Mat &C) {
+  // column groups of <= 288 outputs
+  for (int64_t c0 = 0; c0 < bcols; c0 += 288) {
+    const int64_t w = std::min<int64_t>(288, bcols - c0);
+    Mat Cg = C;
+    Cg.p = C.p + c0;
+    Cg.cols = w;
+    tc_gemm_tall_impl(c, A, Bs + c0, ldb, w, deg, rexp, Cg, false);
+  }
+}
+
+void tc_gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, int64_t bcols, const int32_t *deg,
+                      float rexp, const Mat &C) {
+  NM_REQUIRE(bcols <= 288 && A.cols == bcols, "tc_gemm_tall_tri: square upper-triangular B, <= 288");
+  tc_gemm_tall_impl(c, A, Rinv, ldb, bcols, deg, rexp, C, true);
 }
 
 }  // namespace netmfp

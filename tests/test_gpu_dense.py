@@ -29,19 +29,24 @@ def padded(n, c):
     return torch.zeros(n, ld, dtype=torch.float32, device=DEV)[:, :c]
 
 
-@pytest.mark.parametrize("n,a,b", [(1000, 7, 7), (5000, 158, 158), (3000, 64, 37), (70000, 286, 286)])
-def test_gram(L, ctx, n, a, b):
-    rng = np.random.default_rng(a)
+@pytest.mark.parametrize("n,a,b,same", [(1000, 7, 7, True), (5000, 158, 158, True), (3000, 64, 37, False),
+                                        (70000, 286, 286, True), (70001, 286, 286, False), (131, 40, 40, True),
+                                        (100, 33, 33, True), (250007, 228, 228, True), (20000, 256, 100, False),
+                                        (4099, 300, 300, True)])
+def test_gram(L, ctx, n, a, b, same):
+    rng = np.random.default_rng(a + n)
     A = rng.standard_normal((n, a)).astype(np.float32)
-    B = A if a == b else rng.standard_normal((n, b)).astype(np.float32)
+    B = A if same else rng.standard_normal((n, b)).astype(np.float32)
     Ad = padded(n, a); Ad.copy_(torch.from_numpy(A))
-    Bd = Ad if a == b else padded(n, b)
-    if a != b:
+    Bd = Ad if same else padded(n, b)
+    if not same:
         Bd.copy_(torch.from_numpy(B))
     G = torch.zeros(a, b, dtype=torch.float64, device=DEV)
     L.netmfp_gram(ctx, Ad, Bd, G)
     ref = A.astype(np.float64).T @ B.astype(np.float64)
-    assert np.abs(G.cpu().numpy() - ref).max() <= 1e-5 * np.abs(ref).max()
+    # 3xTF32 on tcgen05: the fp32 TMEM accumulation truncates, so each K-chain
+    # of <= ~2k rows carries a relative bias of ~1e-8 per row
+    assert np.abs(G.cpu().numpy() - ref).max() <= 1e-4 * np.abs(ref).max()
 
 
 @pytest.mark.parametrize("passes", [1, 2])
