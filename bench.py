@@ -319,6 +319,7 @@ def run_ours(args):
                            "l2": "flushed by a 512 MiB write between timed steps"},
                 "e2e": {"value": e2e / 1e3, "unit": "s", "h2d_bytes_per_step": int(s_np.nbytes + t_np.nbytes),
                         "d2h_bytes_per_step": int(n * d * 4)},
+                "step_ms": [round(x, 3) for x in step_ms],
                 "gpu_launches": int(launches // args.steps),
                 "roofline": roof,
                 "kernel_ms_per_step": dict([(k, v[1]) for k, v in sorted(prof_all.items(), key=lambda x: -x[1][1])

@@ -79,27 +79,24 @@ void scale_cols64(Ctx &c, double *A, int64_t rows, int64_t cols, int64_t ld, con
 void set_identity64(Ctx &c, double *A, int64_t l, int64_t ld);
 void axpy64(Ctx &c, int64_t n, double alpha, const double *x, double *y);
 
-// ---- sketch.cu
+// ---- sketch.cu / sketch_tc.cu
+// Alg. 3 sparse-sign matrix n×h with z nonzeros per column: column j's entries
+// are (rows[j*z + t], signs[j*z + t]), t < z, distinct rows.
 struct SparseSign {
   int64_t n = 0, h = 0, z = 0;
-  DBuf<int32_t> rows;     // h*z (column-major by column j: rows[j*z + t])
-  DBuf<float> signs;      // h*z
-  // CSR over unique coordinates p (ascending): entries (column, sign)
-  int64_t v = 0;
-  DBuf<int32_t> p;        // v
-  DBuf<int32_t> pptr;     // v+1
-  DBuf<int32_t> pcol;     // h*z
-  DBuf<float> psign;      // h*z
+  DBuf<int32_t> rows;  // h*z
+  DBuf<float> signs;   // h*z (±1)
 };
 void gen_sparse_sign(Ctx &c, int64_t n, int64_t h, int64_t z, uint64_t seed, uint32_t tag, SparseSign &S);
-// Y[n×h] = f(scale · A Bpᵀ) Ψp   (A: n×k, Bp = rows p of B, both fp32 row-major)
-void sketch_apply(Ctx &c, const Mat &A, const Mat &B, const SparseSign &S, float scale, int logmode,
-                  const Mat &Y);
+// Y[n×h] = f(scale · A F(rows)ᵀ) Ψ  (Eq. 5 sketch; A = F·C), tensor cores
+void tc_sketch_y(Ctx &c, const Mat &A, const Mat &F, const int32_t *rows, const float *signs, int64_t h, int z,
+                 float scale, int logmode, const Mat &Y);
+// Zf[h×h] (fp32, ldz) = Πᵀ f(scale · FC F ᵀ restricted to Π's rows) Π  (Alg. 4 step 6)
+void tc_sketch_z(Ctx &c, const Mat &FC, const Mat &F, const int32_t *rows, const float *signs, int64_t h, int z,
+                 float scale, int logmode, float *Zf, int64_t ldz);
 // Out[h×cols] (fp64) = Ψᵀ X  (sign-gather of rows of X; X fp32 n×cols)
 void sign_gather_T(Ctx &c, const SparseSign &S, const Mat &X, double *Out, int64_t ldo);
-// Out[h×cols] (fp64) = Ψᵀ X restricted: X row i <-> coordinate p[i] (X has v rows, fp32)
-void sign_gather_T_p(Ctx &c, const SparseSign &S, const Mat &Xp, double *Out, int64_t ldo);
-// gather rows p of X into Xp (v × cols)
-void gather_rows(Ctx &c, const Mat &X, const int32_t *idx, int64_t cnt, const Mat &Out);
+// fp32 -> fp64 copy of an r×c matrix
+void f32_to_f64(Ctx &c, const float *src, int64_t lds, double *dst, int64_t ldd, int64_t rows, int64_t cols);
 
 }  // namespace netmfp

@@ -147,11 +147,11 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
   // FC = F · C
   Block FC(n, k, s);
   gemm_tall(c, F, C, k, k, nullptr, 0.f, FC.m);
-  // step 3: Y = f(scale F C F(p,:)ᵀ) Ψ
+  // step 3: Y = f(scale F C F(p,:)ᵀ) Ψ  (Eq. 5, column group by column group of Ψ)
   Block Y(n, h2, s), Qb(n, h2, s), Tb(n, h2, s);
   {
     NM_STAGE(c, "stage_sketch_y");
-    sketch_apply(c, FC.m, F, Psi, fs, logmode, Y.m);
+    tc_sketch_y(c, FC.m, F, Psi.rows, Psi.signs, h2, z, fs, logmode, Y.m);
   }
   if (Yout) copy_block(c, Y.m.p, Y.m.ld, Yout->p, Yout->ld, n, h2);
   // step 4: Q = orth(Y)   (CholeskyQR2 [R7])
@@ -163,13 +163,14 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
     NM_STAGE(c, "stage_gen_sparse_sign");
     gen_sparse_sign(c, n, h3, z, seed, kTagPi, Pi);
   }
-  // step 6: Z = Πᵀ f(scale F(p,:) C F(p,:)ᵀ) Π
+  // step 6: Z = Πᵀ f(scale F(p,:) C F(p,:)ᵀ) Π  (both sides restricted to Π's coordinates)
   NM_STAGE(c, "stage_sketch_z_core");
-  Block FpC(Pi.v, k, s), H(Pi.v, h3, s);
-  gather_rows(c, FC.m, Pi.p, Pi.v, FpC.m);
-  sketch_apply(c, FpC.m, F, Pi, fs, logmode, H.m);
   DBuf<double> Z((size_t)h3 * h3, s), PtQ((size_t)h3 * h2, s);
-  sign_gather_T_p(c, Pi, H.m, Z, h3);
+  {
+    DBuf<float> Zf((size_t)h3 * h3, s);
+    tc_sketch_z(c, FC.m, F, Pi.rows, Pi.signs, h3, z, fs, logmode, Zf, h3);
+    f32_to_f64(c, Zf, h3, Z, h3, h3, h3);
+  }
   if (Zout) NM_CUDA(cudaMemcpyAsync(Zout, Z.p, (size_t)h3 * h3 * 8, cudaMemcpyDeviceToDevice, s));
   // step 7: S = (ΠᵀQ)† Z (QᵀΠ)†  via the normal equations in fp64
   sign_gather_T(c, Pi, Qb.m, PtQ, h2);

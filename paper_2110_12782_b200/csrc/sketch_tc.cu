@@ -1,0 +1,381 @@
+// sketch_tc.cu — rows a6/a7: the sketches of Alg. 4 without materialising the
+// NetMF matrix (Eq. 5), on the tensor cores.
+//
+// A sparse-sign matrix Ψ (Alg. 3) has, in column c, z entries (row r_{c,t},
+// sign s_{c,t}).  Eq. 5's sketch Y = f(M̂')Ψ with M̂' = scale·F C Fᵀ is then
+//
+//   Y[i, c] = Σ_{t<z} s_{c,t} · f(scale · (FC)_i · F_{r_{c,t}}ᵀ)              (Y mode)
+//
+// i.e. a GEMM of A = FC (n × k) against B = the h·z rows F_{r_{c,t}} laid out
+// column group by column group, followed by a fixed segmented sum of z
+// consecutive output columns.  The core sketch of Alg. 4 step 6 is the same
+// with the row side gathered too:
+//
+//   Z[c', c] = Σ_{t'} s_{c',t'} Σ_t s_{c,t} f(scale · (FC)_{r_{c',t'}} · F_{r_{c,t}}ᵀ)   (Z mode)
+//
+// Group sizes are padded to zp = next power of two ≥ z with sign-0 dummy rows,
+// so every group is an aligned run of zp columns (and, in Z mode, zp lanes).
+// This needs neither the unique coordinate set p of Alg. 3 nor a scatter: the
+// epilogue is f(·), one FFMA per element and a register / shuffle reduction.
+//
+// One CTA per SM, persistent over (128-row M tile, N-tile range) items:
+//   warp 0      TMA: A chunk (128 rows × 16 fp32, SWIZZLE_64B) and the
+//               B hi / lo chunks (256 rows × 16) of the current N tile;
+//   warp 1      tcgen05.mma 3xTF32 (A_hi·B_hi + A_hi·B_lo + A_lo·B_hi) into one
+//               of two 256-column TMEM accumulators (double-buffered);
+//   warps 2-3   split the staged A chunk into lo parts (x − trunc_tf32(x));
+//   warps 4-7   epilogue: tcgen05.ld, f(scale·x)·sign, segmented sums; Y mode
+//               stages a row's 256/zp outputs per N tile in shared memory and
+//               writes them as one contiguous run; Z mode reduces zp lanes
+//               with shuffles and stores one value per (row group, col group).
+#include "common.cuh"
+#include "kernels.cuh"
+#include "tc_common.cuh"
+
+#include <algorithm>
+
+namespace netmfp {
+namespace tcs {
+
+using namespace tc;
+
+constexpr int THREADS = 256;
+constexpr int NW = 256;           // N tile per accumulator
+constexpr int BK = 16;            // K per stage (64-B swizzled rows)
+constexpr int ABYTES = 128 * 64;  // A chunk: 128 rows × 16 fp32
+constexpr int BBYTES = NW * 64;   // B chunk: NW rows × 16 fp32
+constexpr int STAGE = 2 * ABYTES + 2 * BBYTES;
+constexpr int S = 3;
+constexpr int kSplit = 64;  // split threads (warps 2-3)
+constexpr int kEpi = 128;   // epilogue threads (warps 4-7)
+constexpr int kStageLd = 129;  // Y-mode staging row stride (floats)
+
+struct SkP {
+  int64_t m;        // rows of A
+  int k, nk;        // contraction length, K chunks
+  int64_t ncols;    // N = h·zp
+  int ntn;          // N tiles
+  int64_t nmt;      // M tiles
+  int nsplit;       // N-tile ranges per M tile (items = nmt × nsplit)
+  int zp, lzp;      // group size (power of two) and log2
+  int64_t h;        // output column groups
+  float scale;
+  int logmode;
+  const float *col_sign;  // ncols, 0 on padding
+  const float *row_sign;  // m (Z mode) or null (Y mode)
+  float *out;
+  int64_t ldo;
+};
+
+// f(x) = trunc_log(x) = log(max(x, 1)) or log1p(max(x, 0))   [R4]
+__device__ __forceinline__ float apply_f(float x, int logmode) {
+  return logmode == 0 ? __logf(fmaxf(x, 1.f)) : log1pf(fmaxf(x, 0.f));
+}
+
+__global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant__ CUtensorMap tmA,
+                                                          const __grid_constant__ CUtensorMap tmBh,
+                                                          const __grid_constant__ CUtensorMap tmBl, const SkP p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = align1024(smem_raw);
+  float *stage_out = reinterpret_cast<float *>(base + S * STAGE);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(base + S * STAGE + (size_t)128 * kStageLd * 4);
+  uint64_t *full = bars, *split = bars + S, *empty = bars + 2 * S;
+  uint64_t *done = bars + 3 * S, *tfree = bars + 3 * S + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * S + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nitems = p.nmt * p.nsplit;
+  const int per = (p.ntn + p.nsplit - 1) / p.nsplit;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&split[s], kSplit);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&done[b], 1);
+      mbar_init(&tfree[b], kEpi);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmBh);
+      tma_prefetch_desc(&tmBl);
+      int64_t g = 0;
+      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const int64_t mt = it / p.nsplit;
+        const int nt0 = (int)(it % p.nsplit) * per, nt1 = min(p.ntn, nt0 + per);
+        for (int nt = nt0; nt < nt1; ++nt) {
+          for (int kc = 0; kc < p.nk; ++kc, ++g) {
+            const int s = (int)(g % S);
+            const int64_t use = g / S;
+            if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+            uint8_t *st = base + s * STAGE;
+            mbar_expect_tx(&full[s], (uint32_t)(ABYTES + 2 * BBYTES));
+            tma_load_2d(st, &tmA, kc * BK, (int)(mt * 128), &full[s]);
+            tma_load_2d(st + 2 * ABYTES, &tmBh, kc * BK, nt * NW, &full[s]);
+            tma_load_2d(st + 2 * ABYTES + BBYTES, &tmBl, kc * BK, nt * NW, &full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int64_t g = 0, tcount = 0;
+      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const int nt0 = (int)(it % p.nsplit) * per, nt1 = min(p.ntn, nt0 + per);
+        for (int nt = nt0; nt < nt1; ++nt, ++tcount) {
+          const int buf = (int)(tcount & 1);
+          const int64_t use_b = tcount >> 1;
+          if (use_b > 0) mbar_wait(&tfree[buf], (uint32_t)((use_b - 1) & 1));
+          tc_fence_after();
+          const int64_t rem = p.ncols - (int64_t)nt * NW;
+          const int N = (int)std::min<int64_t>(NW, (rem + 15) / 16 * 16);
+          const uint32_t idesc = make_idesc(N, 0, 0);
+          const uint32_t d = tmem + (uint32_t)(buf * NW);
+          for (int kc = 0; kc < p.nk; ++kc, ++g) {
+            const int s = (int)(g % S);
+            const int64_t use = g / S;
+            mbar_wait(&split[s], (uint32_t)(use & 1));
+            tc_fence_after();
+            const uint32_t ahi = smem_u32(base + s * STAGE), alo = ahi + ABYTES;
+            const uint32_t bhi = alo + ABYTES, blo = bhi + BBYTES;
+#pragma unroll
+            for (int ks = 0; ks < BK / 8; ++ks) {
+              const uint32_t ko = ks * 32;
+              const uint32_t acc0 = (kc == 0 && ks == 0) ? 0u : 1u;
+              mma_tf32(d, make_desc_sw64(ahi + ko), make_desc_sw64(bhi + ko), idesc, acc0);
+              mma_tf32(d, make_desc_sw64(ahi + ko), make_desc_sw64(blo + ko), idesc, 1u);
+              mma_tf32(d, make_desc_sw64(alo + ko), make_desc_sw64(bhi + ko), idesc, 1u);
+            }
+            mma_commit(&empty[s]);
+          }
+          mma_commit(&done[buf]);
+        }
+      }
+    }
+  } else if (warp < 4) {
+    // split warps: A lo parts
+    const int st_id = threadIdx.x - 64;
+    int64_t g = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int nt0 = (int)(it % p.nsplit) * per, nt1 = min(p.ntn, nt0 + per);
+      for (int nt = nt0; nt < nt1; ++nt) {
+        for (int kc = 0; kc < p.nk; ++kc, ++g) {
+          const int s = (int)(g % S);
+          const int64_t use = g / S;
+          mbar_wait(&full[s], (uint32_t)(use & 1));
+          float4 *raw = reinterpret_cast<float4 *>(base + s * STAGE);
+          float4 *lo = raw + ABYTES / 16;
+          for (int i = st_id; i < ABYTES / 16; i += kSplit) {
+            const float4 x = raw[i];
+            lo[i] = make_float4(x.x - tf32_trunc(x.x), x.y - tf32_trunc(x.y), x.z - tf32_trunc(x.z),
+                                x.w - tf32_trunc(x.w));
+          }
+          fence_async_smem();
+          mbar_arrive(&split[s]);
+        }
+      }
+    }
+  } else {
+    // epilogue warps 4-7: TMEM lane quadrant q, row r of the M tile per thread
+    const int q = warp & 3;
+    const int r = 32 * q + lane;
+    float *srow = stage_out + (size_t)r * kStageLd;
+    const bool zmode = p.row_sign != nullptr;
+    const int gpt = NW >> p.lzp;  // groups per N tile
+    int64_t tcount = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int64_t mt = it / p.nsplit;
+      const int nt0 = (int)(it % p.nsplit) * per, nt1 = min(p.ntn, nt0 + per);
+      const int64_t row = mt * 128 + r;
+      const float rsign = (zmode && row < p.m) ? __ldg(p.row_sign + row) : 1.f;
+      for (int nt = nt0; nt < nt1; ++nt, ++tcount) {
+        const int buf = (int)(tcount & 1);
+        mbar_wait(&done[buf], (uint32_t)((tcount >> 1) & 1));
+        tc_fence_after();
+        const int64_t j0 = (int64_t)nt * NW;
+        const int ncol = (int)std::min<int64_t>(NW, p.ncols - j0);
+        float run = 0.f;
+        for (int cc = 0; cc < ncol; cc += 16) {
+          float x[16];
+          tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * NW + cc), x);
+          float sg[16];
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            const float4 s4 = __ldg(reinterpret_cast<const float4 *>(p.col_sign + j0 + cc + i));
+            sg[i] = s4.x; sg[i + 1] = s4.y; sg[i + 2] = s4.z; sg[i + 3] = s4.w;
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            run = fmaf(sg[i], apply_f(p.scale * x[i], p.logmode), run);
+            if (((cc + i + 1) & (p.zp - 1)) == 0) {
+              const int gl = (cc + i) >> p.lzp;  // group index inside the N tile
+              if (!zmode) {
+                srow[gl] = run;
+              } else {
+                float v = run * rsign;
+                for (int o = 1; o < min(p.zp, 32); o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                const int64_t cg = (j0 >> p.lzp) + gl;
+                const int64_t rg = row >> p.lzp;
+                if ((lane & (min(p.zp, 32) - 1)) == 0 && row < p.m && cg < p.h) {
+                  if (p.zp <= 32)
+                    p.out[rg * p.ldo + cg] = v;
+                  else
+                    atomicAdd(p.out + rg * p.ldo + cg, v);  // 2 warps per group: a + b, order-free
+                }
+              }
+              run = 0.f;
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tfree[buf]);
+        if (!zmode && row < p.m) {
+          // the N tile's groups of this row: one contiguous run of outputs
+          const int64_t cg0 = j0 >> p.lzp;
+          const int cnt = (int)std::min<int64_t>(gpt, p.h - cg0);
+          float *dst = p.out + row * p.ldo + cg0;
+          for (int gi = 0; gi < cnt; ++gi) dst[gi] = srow[gi];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// rows of X at the sparse-sign coordinates, one zp-group per column c:
+// out row c·zp + t = X[rows[c·z + t]] for t < z, zero for the padding (sign 0);
+// optional tf32 lo part and the sign vector
+__global__ void k_gather_groups(const float *__restrict__ X, int64_t ldx, const int32_t *__restrict__ rows,
+                                const float *__restrict__ signs, int64_t h, int z, int zp, int k, int64_t ldb,
+                                float *__restrict__ hi, float *__restrict__ lo, float *__restrict__ sgn) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nr = h * zp;
+  if (idx >= nr * ldb) return;
+  const int64_t j = idx / ldb, kk = idx % ldb;
+  const int64_t c = j / zp;
+  const int t = (int)(j % zp);
+  float x = 0.f;
+  if (t < z && kk < k) x = X[(int64_t)rows[c * z + t] * ldx + kk];
+  hi[idx] = x;
+  if (lo) lo[idx] = x - tc::tf32_trunc(x);
+  if (kk == 0) sgn[j] = t < z ? signs[c * z + t] : 0.f;
+}
+
+}  // namespace tcs
+
+static int pow2_at_least(int z) {
+  int zp = 1;
+  while (zp < z) zp <<= 1;
+  return zp;
+}
+
+static void launch_sketch(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mh, const CUtensorMap &ml,
+                          tcs::SkP &prm) {
+  using namespace tcs;
+  const size_t smem = 1024 + (size_t)S * STAGE + (size_t)128 * kStageLd * 4 + (3 * S + 4) * 8 + 16;
+  static bool attr = false;
+  if (!attr) {
+    NM_CUDA(cudaFuncSetAttribute(k_sketch_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  // enough items for every SM: split the N tiles of an M tile when M tiles are few
+  prm.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(prm.ntn, ceil_div(2 * (int64_t)c.num_sms, prm.nmt)));
+  const int per = (prm.ntn + prm.nsplit - 1) / prm.nsplit;
+  prm.nsplit = (prm.ntn + per - 1) / per;
+  const int64_t items = prm.nmt * prm.nsplit;
+  const unsigned grid = (unsigned)std::min<int64_t>(items, c.num_sms);
+  NM_LAUNCH(c, "sketch_tc", k_sketch_tc<<<grid, THREADS, smem, c.stream>>>(ma, mh, ml, prm));
+}
+
+// Y[n × h] = f(scale · A F(rows)ᵀ) Ψ  (Y mode; A = F·C, Ψ = (rows, signs) with z per column)
+void tc_sketch_y(Ctx &c, const Mat &A, const Mat &F, const int32_t *rows, const float *signs, int64_t h, int z,
+                 float scale, int logmode, const Mat &Y) {
+  using namespace tcs;
+  NM_REQUIRE(A.cols == F.cols && Y.rows == A.rows && Y.cols == h, "tc_sketch_y: shapes");
+  NM_REQUIRE(z >= 2 && z <= 64, "tc_sketch_y: 2 <= z <= 64");
+  const int64_t n = A.rows;
+  const int k = (int)A.cols;
+  if (n == 0 || h == 0) return;
+  const int zp = pow2_at_least(z);
+  const int64_t ncols = h * zp;
+  const int64_t ldb = pad32(k);
+  DBuf<float> bh((size_t)ncols * ldb, c.stream), bl((size_t)ncols * ldb, c.stream), sg(pad4(ncols) + NW, c.stream);
+  NM_CUDA(cudaMemsetAsync(sg.p, 0, sg.n * 4, c.stream));
+  NM_LAUNCH(c, "gather_groups", k_gather_groups<<<ceil_div(ncols * ldb, 256), 256, 0, c.stream>>>(
+                                    F.p, F.ld, rows, signs, h, z, zp, k, ldb, bh.p, bl.p, sg.p));
+  CUtensorMap ma = make_map(A.p, n, k, A.ld, 128, SW64, BK);
+  CUtensorMap mh = make_map(bh.p, ncols, k, ldb, NW, SW64, BK);
+  CUtensorMap ml = make_map(bl.p, ncols, k, ldb, NW, SW64, BK);
+  SkP prm{};
+  prm.m = n;
+  prm.k = k;
+  prm.nk = (int)ceil_div(k, BK);
+  prm.ncols = ncols;
+  prm.ntn = (int)ceil_div(ncols, NW);
+  prm.nmt = ceil_div(n, 128);
+  prm.zp = zp;
+  prm.lzp = __builtin_ctz(zp);
+  prm.h = h;
+  prm.scale = scale;
+  prm.logmode = logmode;
+  prm.col_sign = sg.p;
+  prm.row_sign = nullptr;
+  prm.out = Y.p;
+  prm.ldo = Y.ld;
+  launch_sketch(c, ma, mh, ml, prm);
+}
+
+// Z[h × h] = Πᵀ f(scale · FC(rows) F(rows)ᵀ) Π  (Z mode), fp32 output with ldz
+void tc_sketch_z(Ctx &c, const Mat &FC, const Mat &F, const int32_t *rows, const float *signs, int64_t h, int z,
+                 float scale, int logmode, float *Zf, int64_t ldz) {
+  using namespace tcs;
+  NM_REQUIRE(FC.cols == F.cols, "tc_sketch_z: shapes");
+  NM_REQUIRE(z >= 2 && z <= 64, "tc_sketch_z: 2 <= z <= 64");
+  const int k = (int)F.cols;
+  const int zp = pow2_at_least(z);
+  const int64_t nr = h * zp;
+  const int64_t ldb = pad32(k);
+  DBuf<float> ah((size_t)nr * ldb, c.stream), rs(pad4(nr) + NW, c.stream);
+  DBuf<float> bh((size_t)nr * ldb, c.stream), bl((size_t)nr * ldb, c.stream), sg(pad4(nr) + NW, c.stream);
+  NM_CUDA(cudaMemsetAsync(sg.p, 0, sg.n * 4, c.stream));
+  NM_CUDA(cudaMemsetAsync(rs.p, 0, rs.n * 4, c.stream));
+  NM_LAUNCH(c, "gather_groups", k_gather_groups<<<ceil_div(nr * ldb, 256), 256, 0, c.stream>>>(
+                                    FC.p, FC.ld, rows, signs, h, z, zp, k, ldb, ah.p, nullptr, rs.p));
+  NM_LAUNCH(c, "gather_groups", k_gather_groups<<<ceil_div(nr * ldb, 256), 256, 0, c.stream>>>(
+                                    F.p, F.ld, rows, signs, h, z, zp, k, ldb, bh.p, bl.p, sg.p));
+  if (zp > 32) NM_CUDA(cudaMemset2DAsync(Zf, ldz * 4, 0, h * 4, h, c.stream));
+  CUtensorMap ma = make_map(ah.p, nr, k, ldb, 128, SW64, BK);
+  CUtensorMap mh = make_map(bh.p, nr, k, ldb, NW, SW64, BK);
+  CUtensorMap ml = make_map(bl.p, nr, k, ldb, NW, SW64, BK);
+  SkP prm{};
+  prm.m = nr;
+  prm.k = k;
+  prm.nk = (int)ceil_div(k, BK);
+  prm.ncols = nr;
+  prm.ntn = (int)ceil_div(nr, NW);
+  prm.nmt = ceil_div(nr, 128);
+  prm.zp = zp;
+  prm.lzp = __builtin_ctz(zp);
+  prm.h = h;
+  prm.scale = scale;
+  prm.logmode = logmode;
+  prm.col_sign = sg.p;
+  prm.row_sign = rs.p;
+  prm.out = Zf;
+  prm.ldo = ldz;
+  launch_sketch(c, ma, mh, ml, prm);
+}
+
+}  // namespace netmfp
