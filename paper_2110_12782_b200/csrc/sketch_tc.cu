@@ -19,8 +19,9 @@
 // epilogue is f(·), one FFMA per element and a register / shuffle reduction.
 //
 // One CTA per SM, persistent over (128-row M tile, N-tile range) items:
-//   warp 0      TMA: A chunk (128 rows × 16 fp32, SWIZZLE_64B) and the
-//               B hi / lo chunks (256 rows × 16) of the current N tile;
+//   warp 0      TMA: A chunk (128 rows × 32 fp32, SWIZZLE_128B) and the
+//               B hi / lo chunks (256 rows × 32) of the current N tile, one
+//               box each, issued by three lanes in parallel;
 //   warp 1      tcgen05.mma 3xTF32 (A_hi·B_hi + A_hi·B_lo + A_lo·B_hi) into one
 //               of two 256-column TMEM accumulators (double-buffered);
 //   warps 2-3   split the staged A chunk into lo parts (x − trunc_tf32(x));
@@ -34,6 +35,14 @@
 
 #include <algorithm>
 
+#ifdef SK_PROF
+__device__ unsigned long long g_skprof[148 * 8];
+#define SKP_T0() const unsigned long long _t0 = clock64()
+#define SKP_ADD(slot) atomicAdd(&g_skprof[blockIdx.x * 8 + (slot)], clock64() - _t0)
+#else
+#define SKP_T0()
+#define SKP_ADD(slot)
+#endif
 namespace netmfp {
 namespace tcs {
 
@@ -41,14 +50,13 @@ using namespace tc;
 
 constexpr int THREADS = 256;
 constexpr int NW = 256;           // N tile per accumulator
-constexpr int BK = 16;            // K per stage (64-B swizzled rows)
-constexpr int ABYTES = 128 * 64;  // A chunk: 128 rows × 16 fp32
-constexpr int BBYTES = NW * 64;   // B chunk: NW rows × 16 fp32
+constexpr int BK = 32;             // K per stage (128-B swizzled rows)
+constexpr int ABYTES = 128 * 128;  // A chunk: 128 rows × 32 fp32
+constexpr int BBYTES = NW * 128;   // B chunk: NW rows × 32 fp32
 constexpr int STAGE = 2 * ABYTES + 2 * BBYTES;
-constexpr int S = 3;
+constexpr int S = 2;
 constexpr int kSplit = 64;  // split threads (warps 2-3)
 constexpr int kEpi = 128;   // epilogue threads (warps 4-7)
-constexpr int kStageLd = 129;  // Y-mode staging row stride (floats)
 
 struct SkP {
   int64_t m;        // rows of A
@@ -61,7 +69,9 @@ struct SkP {
   int64_t h;        // output column groups
   float scale;
   int logmode;
-  const float *col_sign;  // ncols, 0 on padding
+  const uint32_t *neg_bits;  // per 32 columns: 1 = sign −1
+  const uint32_t *val_bits;  // per 32 columns: 0 = padding (sign 0)
+  int epi;                   // epilogue variant: zp·4 + zmode·2 + log1p
   const float *row_sign;  // m (Z mode) or null (Y mode)
   float *out;
   int64_t ldo;
@@ -72,13 +82,88 @@ __device__ __forceinline__ float apply_f(float x, int logmode) {
   return logmode == 0 ? __logf(fmaxf(x, 1.f)) : log1pf(fmaxf(x, 0.f));
 }
 
+// One 128 × NW accumulator tile → f, signs, segmented sums (see file header).
+// f is evaluated as ln2 · log2(max(scale x, 1)) (trunc_log) or log1p(max(scale x, 0)).
+// Column signs come as bit masks (neg, valid) of the N tile, 32 columns a word.
+template <int ZP, bool ZM, bool L1P>
+__device__ __forceinline__ void epi_tile(const SkP &p, uint32_t tb, int nt, int64_t row, float rsign, int lane) {
+  const int64_t j0 = (int64_t)nt * NW;
+  const int ncol = (int)min((int64_t)NW, p.ncols - j0);
+  uint32_t neg[NW / 32], val[NW / 32];
+#pragma unroll
+  for (int w = 0; w < NW / 32; ++w) {
+    neg[w] = __ldg(p.neg_bits + nt * (NW / 32) + w);
+    val[w] = __ldg(p.val_bits + nt * (NW / 32) + w);
+  }
+  const float sc = p.scale;
+  constexpr float kLn2 = 0.69314718055994531f;
+  float run = 0.f;
+  float outs[16 / ZP > 0 ? 16 / ZP : 1];
+#pragma unroll
+  for (int cc = 0; cc < NW; cc += 16) {
+    if (cc < ncol) {
+      float x[16];
+      tmem_ld16(tb + (uint32_t)cc, x);
+      const uint32_t nb = (neg[cc >> 5] >> (cc & 16)) & 0xFFFFu;
+      const uint32_t vb = (val[cc >> 5] >> (cc & 16)) & 0xFFFFu;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float v = L1P ? log1pf(fmaxf(sc * x[i], 0.f)) : __log2f(fmaxf(sc * x[i], 1.f));
+        v = ((vb >> i) & 1u) ? v : 0.f;
+        run += ((nb >> i) & 1u) ? -v : v;
+        if (((i + 1) % ZP) == 0 || (ZP > 16 && i == 15 && ((cc + 16) % ZP) == 0)) {
+          const float res = L1P ? run : run * kLn2;
+          run = 0.f;
+          if (ZP <= 16) {
+            outs[i / ZP] = res;
+          } else {
+            outs[0] = res;
+          }
+          if (ZM) {
+            float w = outs[ZP <= 16 ? i / ZP : 0] * rsign;
+#pragma unroll
+            for (int o = 1; o < (ZP < 32 ? ZP : 32); o <<= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+            const int64_t cg = (j0 + cc + i) / ZP;
+            const int64_t rg = row / ZP;
+            if ((lane & ((ZP < 32 ? ZP : 32) - 1)) == 0 && row < p.m && cg < p.h) {
+              if (ZP <= 32)
+                p.out[rg * p.ldo + cg] = w;
+              else
+                atomicAdd(p.out + rg * p.ldo + cg, w);  // 2 warps per group: a + b, order-free
+            }
+          }
+        }
+      }
+      if (!ZM && row < p.m) {
+        // this chunk's outputs: contiguous in the row
+        if (ZP <= 16 || ((cc + 16) % ZP) == 0) {
+          const int64_t cg0 = (j0 + cc + 16) / ZP - (ZP <= 16 ? 16 / ZP : 1);
+          float *dst = p.out + row * p.ldo + cg0;
+          const int nval = (int)min((int64_t)(ZP <= 16 ? 16 / ZP : 1), p.h - cg0);
+          if (ZP <= 4 && nval == 16 / ZP) {
+#pragma unroll
+            for (int o = 0; o < 16 / ZP; o += 4)
+              *reinterpret_cast<float4 *>(dst + o) = make_float4(outs[o], outs[o + 1], outs[o + 2], outs[o + 3]);
+          } else if (ZP == 8 && nval == 2) {
+            *reinterpret_cast<float2 *>(dst) = make_float2(outs[0], outs[1]);
+          } else {
+#pragma unroll
+            for (int o = 0; o < (ZP <= 16 ? 16 / ZP : 1); ++o)
+              if (o < nval) dst[o] = outs[o];
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int ZP, bool ZM, bool L1P>
 __global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant__ CUtensorMap tmA,
                                                           const __grid_constant__ CUtensorMap tmBh,
                                                           const __grid_constant__ CUtensorMap tmBl, const SkP p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = align1024(smem_raw);
-  float *stage_out = reinterpret_cast<float *>(base + S * STAGE);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(base + S * STAGE + (size_t)128 * kStageLd * 4);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(base + S * STAGE);
   uint64_t *full = bars, *split = bars + S, *empty = bars + 2 * S;
   uint64_t *done = bars + 3 * S, *tfree = bars + 3 * S + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * S + 4);
@@ -105,25 +190,32 @@ __global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant_
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
+    // lanes 0-2 issue the stage's three boxes in parallel (a TMA issue blocks
+    // the issuing thread for ~150-300 cycles regardless of the box size)
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmBh);
       tma_prefetch_desc(&tmBl);
-      int64_t g = 0;
-      for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const int64_t mt = it / p.nsplit;
-        const int nt0 = (int)(it % p.nsplit) * per, nt1 = min(p.ntn, nt0 + per);
-        for (int nt = nt0; nt < nt1; ++nt) {
-          for (int kc = 0; kc < p.nk; ++kc, ++g) {
-            const int s = (int)(g % S);
-            const int64_t use = g / S;
-            if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
-            uint8_t *st = base + s * STAGE;
-            mbar_expect_tx(&full[s], (uint32_t)(ABYTES + 2 * BBYTES));
-            tma_load_2d(st, &tmA, kc * BK, (int)(mt * 128), &full[s]);
-            tma_load_2d(st + 2 * ABYTES, &tmBh, kc * BK, nt * NW, &full[s]);
-            tma_load_2d(st + 2 * ABYTES + BBYTES, &tmBl, kc * BK, nt * NW, &full[s]);
+    }
+    int64_t g = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int64_t mt = it / p.nsplit;
+      const int nt0 = (int)(it % p.nsplit) * per, nt1 = min(p.ntn, nt0 + per);
+      for (int nt = nt0; nt < nt1; ++nt) {
+        for (int kc = 0; kc < p.nk; ++kc, ++g) {
+          const int s = (int)(g % S);
+          const int64_t use = g / S;
+          if (use > 0) {
+            SKP_T0();
+            mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+            if (lane == 0) SKP_ADD(0);
           }
+          uint8_t *st = base + s * STAGE;
+          if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)(ABYTES + 2 * BBYTES));
+          __syncwarp();
+          if (lane == 0) tma_load_2d(st, &tmA, kc * BK, (int)(mt * 128), &full[s]);
+          if (lane == 1) tma_load_2d(st + 2 * ABYTES, &tmBh, kc * BK, nt * NW, &full[s]);
+          if (lane == 2) tma_load_2d(st + 2 * ABYTES + BBYTES, &tmBl, kc * BK, nt * NW, &full[s]);
         }
       }
     }
@@ -135,7 +227,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant_
         for (int nt = nt0; nt < nt1; ++nt, ++tcount) {
           const int buf = (int)(tcount & 1);
           const int64_t use_b = tcount >> 1;
-          if (use_b > 0) mbar_wait(&tfree[buf], (uint32_t)((use_b - 1) & 1));
+          if (use_b > 0) {
+            SKP_T0();
+            mbar_wait(&tfree[buf], (uint32_t)((use_b - 1) & 1));
+            SKP_ADD(1);
+          }
           tc_fence_after();
           const int64_t rem = p.ncols - (int64_t)nt * NW;
           const int N = (int)std::min<int64_t>(NW, (rem + 15) / 16 * 16);
@@ -144,7 +240,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant_
           for (int kc = 0; kc < p.nk; ++kc, ++g) {
             const int s = (int)(g % S);
             const int64_t use = g / S;
-            mbar_wait(&split[s], (uint32_t)(use & 1));
+            {
+              SKP_T0();
+              mbar_wait(&split[s], (uint32_t)(use & 1));
+              SKP_ADD(2);
+            }
             tc_fence_after();
             const uint32_t ahi = smem_u32(base + s * STAGE), alo = ahi + ABYTES;
             const uint32_t bhi = alo + ABYTES, blo = bhi + BBYTES;
@@ -152,9 +252,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant_
             for (int ks = 0; ks < BK / 8; ++ks) {
               const uint32_t ko = ks * 32;
               const uint32_t acc0 = (kc == 0 && ks == 0) ? 0u : 1u;
-              mma_tf32(d, make_desc_sw64(ahi + ko), make_desc_sw64(bhi + ko), idesc, acc0);
-              mma_tf32(d, make_desc_sw64(ahi + ko), make_desc_sw64(blo + ko), idesc, 1u);
-              mma_tf32(d, make_desc_sw64(alo + ko), make_desc_sw64(bhi + ko), idesc, 1u);
+              mma_tf32(d, make_desc(ahi + ko, 16, 1024), make_desc(bhi + ko, 16, 1024), idesc, acc0);
+              mma_tf32(d, make_desc(ahi + ko, 16, 1024), make_desc(blo + ko, 16, 1024), idesc, 1u);
+              mma_tf32(d, make_desc(alo + ko, 16, 1024), make_desc(bhi + ko, 16, 1024), idesc, 1u);
             }
             mma_commit(&empty[s]);
           }
@@ -172,7 +272,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant_
         for (int kc = 0; kc < p.nk; ++kc, ++g) {
           const int s = (int)(g % S);
           const int64_t use = g / S;
-          mbar_wait(&full[s], (uint32_t)(use & 1));
+          {
+            SKP_T0();
+            mbar_wait(&full[s], (uint32_t)(use & 1));
+            if (st_id == 0) SKP_ADD(3);
+          }
           float4 *raw = reinterpret_cast<float4 *>(base + s * STAGE);
           float4 *lo = raw + ABYTES / 16;
           for (int i = st_id; i < ABYTES / 16; i += kSplit) {
@@ -189,9 +293,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant_
     // epilogue warps 4-7: TMEM lane quadrant q, row r of the M tile per thread
     const int q = warp & 3;
     const int r = 32 * q + lane;
-    float *srow = stage_out + (size_t)r * kStageLd;
     const bool zmode = p.row_sign != nullptr;
-    const int gpt = NW >> p.lzp;  // groups per N tile
     int64_t tcount = 0;
     for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
       const int64_t mt = it / p.nsplit;
@@ -200,52 +302,18 @@ __global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant_
       const float rsign = (zmode && row < p.m) ? __ldg(p.row_sign + row) : 1.f;
       for (int nt = nt0; nt < nt1; ++nt, ++tcount) {
         const int buf = (int)(tcount & 1);
-        mbar_wait(&done[buf], (uint32_t)((tcount >> 1) & 1));
-        tc_fence_after();
-        const int64_t j0 = (int64_t)nt * NW;
-        const int ncol = (int)std::min<int64_t>(NW, p.ncols - j0);
-        float run = 0.f;
-        for (int cc = 0; cc < ncol; cc += 16) {
-          float x[16];
-          tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * NW + cc), x);
-          float sg[16];
-#pragma unroll
-          for (int i = 0; i < 16; i += 4) {
-            const float4 s4 = __ldg(reinterpret_cast<const float4 *>(p.col_sign + j0 + cc + i));
-            sg[i] = s4.x; sg[i + 1] = s4.y; sg[i + 2] = s4.z; sg[i + 3] = s4.w;
-          }
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            run = fmaf(sg[i], apply_f(p.scale * x[i], p.logmode), run);
-            if (((cc + i + 1) & (p.zp - 1)) == 0) {
-              const int gl = (cc + i) >> p.lzp;  // group index inside the N tile
-              if (!zmode) {
-                srow[gl] = run;
-              } else {
-                float v = run * rsign;
-                for (int o = 1; o < min(p.zp, 32); o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                const int64_t cg = (j0 >> p.lzp) + gl;
-                const int64_t rg = row >> p.lzp;
-                if ((lane & (min(p.zp, 32) - 1)) == 0 && row < p.m && cg < p.h) {
-                  if (p.zp <= 32)
-                    p.out[rg * p.ldo + cg] = v;
-                  else
-                    atomicAdd(p.out + rg * p.ldo + cg, v);  // 2 warps per group: a + b, order-free
-                }
-              }
-              run = 0.f;
-            }
-          }
+        {
+          SKP_T0();
+          mbar_wait(&done[buf], (uint32_t)((tcount >> 1) & 1));
+          if (r == 0) SKP_ADD(4);
         }
+        tc_fence_after();
+        SKP_T0();
+        const uint32_t tb = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * NW);
+        epi_tile<ZP, ZM, L1P>(p, tb, nt, row, rsign, lane);
         tc_fence_before();
         mbar_arrive(&tfree[buf]);
-        if (!zmode && row < p.m) {
-          // the N tile's groups of this row: one contiguous run of outputs
-          const int64_t cg0 = j0 >> p.lzp;
-          const int cnt = (int)std::min<int64_t>(gpt, p.h - cg0);
-          float *dst = p.out + row * p.ldo + cg0;
-          for (int gi = 0; gi < cnt; ++gi) dst[gi] = srow[gi];
-        }
+        if (r == 0) SKP_ADD(5);
       }
     }
   }
@@ -273,6 +341,22 @@ __global__ void k_gather_groups(const float *__restrict__ X, int64_t ldx, const 
   if (kk == 0) sgn[j] = t < z ? signs[c * z + t] : 0.f;
 }
 
+// sign → bit masks, 32 columns per word (NW/32 words per N tile, zero padded)
+__global__ void k_sign_bits(const float *__restrict__ sg, int64_t ncols, int64_t nwords, uint32_t *__restrict__ neg,
+                            uint32_t *__restrict__ val) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w >= nwords) return;
+  uint32_t nb = 0, vb = 0;
+  for (int i = 0; i < 32; ++i) {
+    const int64_t j = w * 32 + i;
+    const float v = j < ncols ? sg[j] : 0.f;
+    if (v < 0.f) nb |= 1u << i;
+    if (v != 0.f) vb |= 1u << i;
+  }
+  neg[w] = nb;
+  val[w] = vb;
+}
+
 }  // namespace tcs
 
 static int pow2_at_least(int z) {
@@ -282,13 +366,31 @@ static int pow2_at_least(int z) {
 }
 
 static void launch_sketch(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mh, const CUtensorMap &ml,
-                          tcs::SkP &prm) {
+                          tcs::SkP &prm, const float *col_sign) {
   using namespace tcs;
-  const size_t smem = 1024 + (size_t)S * STAGE + (size_t)128 * kStageLd * 4 + (3 * S + 4) * 8 + 16;
-  static bool attr = false;
-  if (!attr) {
-    NM_CUDA(cudaFuncSetAttribute(k_sketch_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+  const int64_t nwords = (int64_t)prm.ntn * (NW / 32);
+  DBuf<uint32_t> bits((size_t)2 * nwords, c.stream);
+  NM_LAUNCH(c, "sign_bits", k_sign_bits<<<ceil_div(nwords, 128), 128, 0, c.stream>>>(col_sign, prm.ncols, nwords, bits.p,
+                                                                                    bits.p + nwords));
+  prm.neg_bits = bits.p;
+  prm.val_bits = bits.p + nwords;
+  prm.epi = prm.zp * 4 + (prm.row_sign ? 2 : 0) + (prm.logmode ? 1 : 0);
+  const size_t smem = 1024 + (size_t)S * STAGE + (3 * S + 4) * 8 + 16;
+  auto kern = k_sketch_tc<8, false, false>;
+  switch (prm.epi) {
+#define SK_CASE(ZP, ZM, L1P) \
+  case (ZP) * 4 + (ZM) * 2 + (L1P): kern = k_sketch_tc<ZP, ZM, L1P>; break;
+    SK_CASE(2, 0, 0) SK_CASE(4, 0, 0) SK_CASE(8, 0, 0) SK_CASE(16, 0, 0) SK_CASE(32, 0, 0) SK_CASE(64, 0, 0)
+    SK_CASE(2, 1, 0) SK_CASE(4, 1, 0) SK_CASE(8, 1, 0) SK_CASE(16, 1, 0) SK_CASE(32, 1, 0) SK_CASE(64, 1, 0)
+    SK_CASE(2, 0, 1) SK_CASE(4, 0, 1) SK_CASE(8, 0, 1) SK_CASE(16, 0, 1) SK_CASE(32, 0, 1) SK_CASE(64, 0, 1)
+    SK_CASE(2, 1, 1) SK_CASE(4, 1, 1) SK_CASE(8, 1, 1) SK_CASE(16, 1, 1) SK_CASE(32, 1, 1) SK_CASE(64, 1, 1)
+#undef SK_CASE
+    default: NM_REQUIRE(false, "tc_sketch: unsupported group size");
+  }
+  static bool attr_set[64 * 4] = {};
+  if (!attr_set[prm.epi]) {
+    NM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set[prm.epi] = true;
   }
   // enough items for every SM: split the N tiles of an M tile when M tiles are few
   prm.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(prm.ntn, ceil_div(2 * (int64_t)c.num_sms, prm.nmt)));
@@ -296,7 +398,7 @@ static void launch_sketch(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mh, 
   prm.nsplit = (prm.ntn + per - 1) / per;
   const int64_t items = prm.nmt * prm.nsplit;
   const unsigned grid = (unsigned)std::min<int64_t>(items, c.num_sms);
-  NM_LAUNCH(c, "sketch_tc", k_sketch_tc<<<grid, THREADS, smem, c.stream>>>(ma, mh, ml, prm));
+  NM_LAUNCH(c, "sketch_tc", kern<<<grid, THREADS, smem, c.stream>>>(ma, mh, ml, prm));
 }
 
 // Y[n × h] = f(scale · A F(rows)ᵀ) Ψ  (Y mode; A = F·C, Ψ = (rows, signs) with z per column)
@@ -315,9 +417,9 @@ void tc_sketch_y(Ctx &c, const Mat &A, const Mat &F, const int32_t *rows, const 
   NM_CUDA(cudaMemsetAsync(sg.p, 0, sg.n * 4, c.stream));
   NM_LAUNCH(c, "gather_groups", k_gather_groups<<<ceil_div(ncols * ldb, 256), 256, 0, c.stream>>>(
                                     F.p, F.ld, rows, signs, h, z, zp, k, ldb, bh.p, bl.p, sg.p));
-  CUtensorMap ma = make_map(A.p, n, k, A.ld, 128, SW64, BK);
-  CUtensorMap mh = make_map(bh.p, ncols, k, ldb, NW, SW64, BK);
-  CUtensorMap ml = make_map(bl.p, ncols, k, ldb, NW, SW64, BK);
+  CUtensorMap ma = make_map(A.p, n, k, A.ld, 128, SW128, BK);
+  CUtensorMap mh = make_map(bh.p, ncols, k, ldb, NW, SW128, BK);
+  CUtensorMap ml = make_map(bl.p, ncols, k, ldb, NW, SW128, BK);
   SkP prm{};
   prm.m = n;
   prm.k = k;
@@ -330,11 +432,10 @@ void tc_sketch_y(Ctx &c, const Mat &A, const Mat &F, const int32_t *rows, const 
   prm.h = h;
   prm.scale = scale;
   prm.logmode = logmode;
-  prm.col_sign = sg.p;
   prm.row_sign = nullptr;
   prm.out = Y.p;
   prm.ldo = Y.ld;
-  launch_sketch(c, ma, mh, ml, prm);
+  launch_sketch(c, ma, mh, ml, prm, sg.p);
 }
 
 // Z[h × h] = Πᵀ f(scale · FC(rows) F(rows)ᵀ) Π  (Z mode), fp32 output with ldz
@@ -356,9 +457,9 @@ void tc_sketch_z(Ctx &c, const Mat &FC, const Mat &F, const int32_t *rows, const
   NM_LAUNCH(c, "gather_groups", k_gather_groups<<<ceil_div(nr * ldb, 256), 256, 0, c.stream>>>(
                                     F.p, F.ld, rows, signs, h, z, zp, k, ldb, bh.p, bl.p, sg.p));
   if (zp > 32) NM_CUDA(cudaMemset2DAsync(Zf, ldz * 4, 0, h * 4, h, c.stream));
-  CUtensorMap ma = make_map(ah.p, nr, k, ldb, 128, SW64, BK);
-  CUtensorMap mh = make_map(bh.p, nr, k, ldb, NW, SW64, BK);
-  CUtensorMap ml = make_map(bl.p, nr, k, ldb, NW, SW64, BK);
+  CUtensorMap ma = make_map(ah.p, nr, k, ldb, 128, SW128, BK);
+  CUtensorMap mh = make_map(bh.p, nr, k, ldb, NW, SW128, BK);
+  CUtensorMap ml = make_map(bl.p, nr, k, ldb, NW, SW128, BK);
   SkP prm{};
   prm.m = nr;
   prm.k = k;
@@ -371,11 +472,10 @@ void tc_sketch_z(Ctx &c, const Mat &FC, const Mat &F, const int32_t *rows, const
   prm.h = h;
   prm.scale = scale;
   prm.logmode = logmode;
-  prm.col_sign = sg.p;
   prm.row_sign = rs.p;
   prm.out = Zf;
   prm.ldo = ldz;
-  launch_sketch(c, ma, mh, ml, prm);
+  launch_sketch(c, ma, mh, ml, prm, sg.p);
 }
 
 }  // namespace netmfp
