@@ -18,7 +18,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["api.cu", "build_csr.cu", "spmm.cu", "dense.cu", "small.cu", "sketch.cu", "pipeline.cu", "tc_gemm.cu", "sketch_tc.cu"]
+SOURCES = ["api.cu", "build_csr.cu", "spmm.cu", "dense.cu", "small.cu", "sketch.cu", "pipeline.cu", "tc_gemm.cu", "sketch_tc.cu", "chol_df.cu"]
 
 
 def _deps():

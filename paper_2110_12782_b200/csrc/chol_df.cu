@@ -1,0 +1,353 @@
+// chol_df.cu — CholeskyQR's small factorisation on many SMs:
+//   G = Rᵀ R (R upper, G l×l SPD fp64),  Rinv = R⁻¹.
+// The lower triangle is cut into 32×32 tiles; one CTA owns one tile (I, J),
+// I >= J, and the tiles run as a dataflow graph synchronised through
+// per-tile ready flags in global memory (release/acquire at gpu scope), so
+// the critical path is ~2·nb tile steps instead of l column steps on one SM:
+//   Cholesky (L = Rᵀ, right-looking by dependencies):
+//     S_IJ = G_IJ − Σ_{K<J} L_IK L_JKᵀ      (waits for L_IK, L_JK)
+//     L_JJ = chol(S_JJ)                      (warp 0, shared memory)
+//     L_IJ = S_IJ L_JJ⁻ᵀ                     (waits for L_JJ; one row per thread)
+//   inverse X = L⁻¹ (lower):
+//     X_II = L_II⁻¹ ;  X_IJ = −X_II Σ_{K=J}^{I−1} L_IK X_KJ   (waits for X_KJ, X_II)
+//   Rinv = Xᵀ.
+// A breakdown (pivot <= 1e-12 × original diagonal, or non-finite) raises a
+// global fail word; every CTA notices it, the grid synchronises and all tiles
+// restart from the saved G with a diagonal shift (shifted CholeskyQR), as the
+// single-CTA kernels in small.cu do.  Launched cooperatively (co-residency of
+// the ≤ nb(nb+1)/2 CTAs is required by the spin waits).
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+#ifdef CDF_PROF
+__device__ unsigned long long g_cdf_t[64 * 16];
+#define CDF_MARK(i)                                                                 \
+  do {                                                                              \
+    if (threadIdx.x == 0) {                                                         \
+      unsigned long long _t;                                                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                        \
+      g_cdf_t[blockIdx.x * 16 + (i)] = _t;                                           \
+    }                                                                               \
+  } while (0)
+#else
+#define CDF_MARK(i)
+#endif
+namespace netmfp {
+namespace cdf {
+
+constexpr int T = 256;
+constexpr int TL = 33;  // smem tile row stride (doubles)
+
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int *p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+struct DfP {
+  double *G;   // l×l (ld), overwritten: L in the lower tiles
+  int64_t ld;
+  int l, nb;
+  double *G0;  // saved copy of G (l×l, ld = l)
+  double *Rinv;  // l×l (ld = l); holds X = L⁻¹ (lower) before the final transpose
+  int *lflag, *xflag;  // nb×nb ready flags (value = attempt + 1)
+  int *fail;           // 0 = ok, else attempt+1 of the failing attempt
+  int *flag;           // caller's status word (shift counter, 1<<30 on failure)
+};
+
+// wait until *f >= want (or the attempt failed); returns false on failure
+__device__ bool wait_flag(const DfP &p, const int *f, int want, int attempt) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    int r = 1;
+    while (ld_acquire(f) < want) {
+      if (ld_acquire(p.fail) == attempt + 1) {
+        r = 0;
+        break;
+      }
+      __nanosleep(64);
+    }
+    ok = r;
+  }
+  __syncthreads();
+  const bool r = ok != 0;
+  __syncthreads();
+  return r;
+}
+
+__device__ void publish(int *f, int v) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(f, v);
+  }
+}
+
+// load a 32×32 tile (rows r0.., cols c0.., valid ib×jb, zero padded) bypassing L1
+__device__ void load_tile(double *dst, const double *src, int64_t ld, int r0, int c0, int ib, int jb) {
+  for (int i = threadIdx.x; i < 32 * 32; i += T) {
+    const int r = i >> 5, c = i & 31;
+    dst[r * TL + c] = (r < ib && c < jb) ? __ldcg(src + (int64_t)(r0 + r) * ld + c0 + c) : 0.0;
+  }
+}
+__device__ void store_tile(double *dst, int64_t ld, const double *src, int r0, int c0, int ib, int jb) {
+  for (int i = threadIdx.x; i < 32 * 32; i += T) {
+    const int r = i >> 5, c = i & 31;
+    if (r < ib && c < jb) __stcg(dst + (int64_t)(r0 + r) * ld + c0 + c, src[r * TL + c]);
+  }
+}
+
+// S -= A · Bᵀ  (32×32 tiles in smem); thread owns 4 outputs (rows r, r+8, r+16, r+24)
+__device__ void tile_sub_abt(double *S, const double *A, const double *B) {
+  const int c = threadIdx.x & 31, r0 = threadIdx.x >> 5;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+  for (int t = 0; t < 32; ++t) {
+    const double b = B[c * TL + t];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] += A[(r0 + 8 * i) * TL + t] * b;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) S[(r0 + 8 * i) * TL + c] -= acc[i];
+}
+// S += A · B  (A, B, S 32×32 smem)
+__device__ void tile_add_ab(double *S, const double *A, const double *B) {
+  const int c = threadIdx.x & 31, r0 = threadIdx.x >> 5;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+  for (int t = 0; t < 32; ++t) {
+    const double b = B[t * TL + c];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] += A[(r0 + 8 * i) * TL + t] * b;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) S[(r0 + 8 * i) * TL + c] += acc[i];
+}
+
+__global__ void __launch_bounds__(T) k_chol_df(DfP p) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double S[32 * TL], A[32 * TL], B[32 * TL], D[32 * TL];
+  __shared__ int bad;
+  __shared__ double piv[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // tile of this CTA: t -> (I, J), I >= J, column-major over the lower triangle
+  int t = blockIdx.x, J = 0;
+  while (t >= p.nb - J) {
+    t -= p.nb - J;
+    ++J;
+  }
+  const int I = J + t;
+  const int ib = min(32, p.l - 32 * I), jb = min(32, p.l - 32 * J);
+  CDF_MARK(0);
+  // save G (for shifted retries) and the original diagonal
+  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < (int64_t)p.l * p.l; i += (int64_t)gridDim.x * T)
+    p.G0[i] = p.G[(i / p.l) * p.ld + i % p.l];
+  grid.sync();
+  CDF_MARK(1);
+  __shared__ double red[T / 32];
+  double maxdiag = 0.0;
+  for (int i = threadIdx.x; i < p.l; i += T) maxdiag = fmax(maxdiag, __ldcg(p.G0 + (int64_t)i * p.l + i));
+  for (int o = 16; o > 0; o >>= 1) maxdiag = fmax(maxdiag, __shfl_xor_sync(0xffffffffu, maxdiag, o));
+  if (lane == 0) red[warp] = maxdiag;
+  __syncthreads();
+  maxdiag = 0.0;
+  for (int w = 0; w < T / 32; ++w) maxdiag = fmax(maxdiag, red[w]);
+  int attempt = 0;
+  for (; attempt < 6; ++attempt) {
+    const double shift = attempt == 0 ? 0.0 : maxdiag * 1e-7 * pow(100.0, (double)(attempt - 1));
+    const int want = attempt + 1;
+    bool alive = true;
+    // S = G_IJ (+ shift on the diagonal)
+    CDF_MARK(8);
+    load_tile(S, p.G0, p.l, 32 * I, 32 * J, ib, jb);
+    __syncthreads();
+    CDF_MARK(9);
+    if (I == J)
+      for (int i = threadIdx.x; i < ib; i += T) S[i * TL + i] += shift;
+    // left-looking updates
+    for (int K = 0; K < J && alive; ++K) {
+      alive = wait_flag(p, p.lflag + I * p.nb + K, want, attempt) &&
+              wait_flag(p, p.lflag + J * p.nb + K, want, attempt);
+      if (!alive) break;
+      load_tile(A, p.G, p.ld, 32 * I, 32 * K, ib, 32);
+      load_tile(B, p.G, p.ld, 32 * J, 32 * K, jb, 32);
+      __syncthreads();
+      tile_sub_abt(S, A, B);
+      __syncthreads();
+    }
+    CDF_MARK(4);
+    if (alive && I == J) {
+      // factor the diagonal tile (warp 0), rows beyond ib are identity padding
+      if (threadIdx.x == 0) bad = 0;
+      __syncthreads();
+      CDF_MARK(10);
+      // unnormalised right-looking elimination, all threads, one barrier per pivot:
+      // after step j column j holds s_rj and L_rj = s_rj / sqrt(s_jj)
+      if (threadIdx.x < 32 && threadIdx.x >= ib)
+        for (int cc = 0; cc < 32; ++cc) S[threadIdx.x * TL + cc] = (cc == (int)threadIdx.x) ? 1.0 : 0.0;
+      if (threadIdx.x < 32)
+        piv[threadIdx.x] = (int)threadIdx.x < ib
+                               ? __ldcg(p.G0 + (int64_t)(32 * I + threadIdx.x) * p.l + 32 * I + threadIdx.x) + shift
+                               : 1.0;
+      __syncthreads();
+      for (int j = 0; j < 32; ++j) {
+        const double d = S[j * TL + j];
+        if (threadIdx.x == 0 && j < ib && (!(d > 1e-12 * piv[j]) || !isfinite(d))) bad = 1;
+        const double inv = 1.0 / fmax(d, 1e-300);
+        for (int e = threadIdx.x; e < 32 * 32; e += T) {
+          const int r = e >> 5, cc = e & 31;
+          if (cc > j && r >= cc) S[r * TL + cc] -= S[r * TL + j] * S[cc * TL + j] * inv;
+        }
+        __syncthreads();
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) piv[threadIdx.x] = rsqrt(fmax(S[threadIdx.x * TL + threadIdx.x], 1e-300));
+      __syncthreads();
+      for (int e = threadIdx.x; e < 32 * 32; e += T) {
+        const int r = e >> 5, cc = e & 31;
+        S[r * TL + cc] = (r >= cc) ? S[r * TL + cc] * piv[cc] : 0.0;  // diagonal: s_cc/sqrt(s_cc)
+      }
+      CDF_MARK(11);
+      __syncthreads();
+      CDF_MARK(12);
+      if (bad) {
+        if (threadIdx.x == 0) atomicMax(p.fail, want);
+        alive = false;
+      } else {
+        store_tile(p.G, p.ld, S, 32 * I, 32 * I, ib, ib);
+        CDF_MARK(13);
+        publish(p.lflag + I * p.nb + I, want);
+        CDF_MARK(7);
+      }
+    } else if (alive) {
+      alive = wait_flag(p, p.lflag + J * p.nb + J, want, attempt);
+      if (alive) {
+        load_tile(D, p.G, p.ld, 32 * J, 32 * J, jb, jb);
+        __syncthreads();
+        // L_IJ = S L_JJ⁻ᵀ by column elimination, one barrier per column
+        for (int cc = 0; cc < jb; ++cc) {
+          if (threadIdx.x < 32) S[threadIdx.x * TL + cc] /= D[cc * TL + cc];
+          __syncthreads();
+          for (int e = threadIdx.x; e < 32 * 32; e += T) {
+            const int r = e >> 5, c2 = e & 31;
+            if (c2 > cc && c2 < jb) S[r * TL + c2] -= S[r * TL + cc] * D[c2 * TL + cc];
+          }
+          __syncthreads();
+        }
+        __syncthreads();
+        store_tile(p.G, p.ld, S, 32 * I, 32 * J, ib, jb);
+        publish(p.lflag + I * p.nb + J, want);
+        CDF_MARK(7);
+      }
+    }
+    CDF_MARK(2);
+    grid.sync();
+    CDF_MARK(3);
+    if (__ldcg(p.fail) != want) break;  // this attempt succeeded
+  }
+  if (attempt >= 6) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(p.flag, 1 << 30);
+    return;
+  }
+  if (attempt > 0 && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(p.flag, 1);
+  // ---- inverse: X = L⁻¹
+  const int want = 1;
+  if (I == J) {
+    load_tile(A, p.G, p.ld, 32 * I, 32 * I, ib, ib);
+    __syncthreads();
+    // X_II = L_II⁻¹ by forward elimination on the identity, one barrier per row
+    for (int e = threadIdx.x; e < 32 * 32; e += T) D[(e >> 5) * TL + (e & 31)] = ((e >> 5) == (e & 31)) ? 1.0 : 0.0;
+    __syncthreads();
+    for (int rr = 0; rr < ib; ++rr) {
+      if (threadIdx.x < 32) D[rr * TL + threadIdx.x] /= A[rr * TL + rr];
+      __syncthreads();
+      for (int e = threadIdx.x; e < 32 * 32; e += T) {
+        const int r = e >> 5, c2 = e & 31;
+        if (r > rr && r < ib) D[r * TL + c2] -= A[r * TL + rr] * D[rr * TL + c2];
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < 32 * 32; e += T)
+      if ((e >> 5) >= ib || (e & 31) >= ib) D[(e >> 5) * TL + (e & 31)] = 0.0;
+    __syncthreads();
+    store_tile(p.Rinv, p.l, D, 32 * I, 32 * I, ib, ib);
+    publish(p.xflag + I * p.nb + I, want);
+  } else {
+    for (int i = threadIdx.x; i < 32 * TL; i += T) S[i] = 0.0;
+    __syncthreads();
+    for (int K = J; K < I; ++K) {
+      wait_flag(p, p.xflag + K * p.nb + J, want, -100);
+      load_tile(A, p.G, p.ld, 32 * I, 32 * K, ib, 32);          // L_IK
+      load_tile(B, p.Rinv, p.l, 32 * K, 32 * J, 32, jb);        // X_KJ
+      __syncthreads();
+      tile_add_ab(S, A, B);
+      __syncthreads();
+    }
+    wait_flag(p, p.xflag + I * p.nb + I, want, -100);
+    load_tile(A, p.Rinv, p.l, 32 * I, 32 * I, ib, ib);          // X_II
+    for (int i = threadIdx.x; i < 32 * TL; i += T) D[i] = 0.0;
+    __syncthreads();
+    tile_add_ab(D, A, S);  // D = X_II · S
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * TL; i += T) D[i] = -D[i];
+    __syncthreads();
+    store_tile(p.Rinv, p.l, D, 32 * I, 32 * J, ib, jb);
+    publish(p.xflag + I * p.nb + J, want);
+  }
+  CDF_MARK(4);
+  grid.sync();
+  CDF_MARK(5);
+  // ---- Rinv = Xᵀ: this CTA transposes its own tile pair
+  if (I == J) {
+    load_tile(A, p.Rinv, p.l, 32 * I, 32 * I, ib, ib);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * 32; i += T) {
+      const int r = i >> 5, c = i & 31;
+      if (r < ib && c < ib) p.Rinv[(int64_t)(32 * I + r) * p.l + 32 * I + c] = (c >= r) ? A[c * TL + r] : 0.0;
+    }
+  } else {
+    load_tile(A, p.Rinv, p.l, 32 * I, 32 * J, ib, jb);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * 32; i += T) {
+      const int r = i >> 5, c = i & 31;
+      if (r < jb && c < ib) p.Rinv[(int64_t)(32 * J + r) * p.l + 32 * I + c] = A[c * TL + r];
+      if (r < ib && c < jb) p.Rinv[(int64_t)(32 * I + r) * p.l + 32 * J + c] = 0.0;
+    }
+  }
+  CDF_MARK(6);
+}
+
+}  // namespace cdf
+
+// G = RᵀR → Rinv = R⁻¹ on nb(nb+1)/2 co-resident CTAs (cooperative launch)
+void chol_inv_df(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *flag) {
+  using namespace cdf;
+  const int nb = (int)ceil_div(l, 32);
+  const int tiles = nb * (nb + 1) / 2;
+  DBuf<double> G0((size_t)l * l, c.stream);
+  DBuf<int> flags((size_t)2 * nb * nb + 1, c.stream);
+  NM_CUDA(cudaMemsetAsync(flags.p, 0, flags.n * sizeof(int), c.stream));
+  DfP p{};
+  p.G = G;
+  p.ld = ld;
+  p.l = (int)l;
+  p.nb = nb;
+  p.G0 = G0.p;
+  p.Rinv = Rinv;
+  p.lflag = flags.p;
+  p.xflag = flags.p + nb * nb;
+  p.fail = flags.p + 2 * nb * nb;
+  p.flag = flag;
+  void *args[] = {&p};
+  NM_LAUNCH(c, "chol_df", NM_CUDA(cudaLaunchCooperativeKernel((void *)k_chol_df, dim3(tiles), dim3(T), args, 0,
+                                                                c.stream)));
+}
+
+}  // namespace netmfp

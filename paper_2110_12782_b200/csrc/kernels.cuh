@@ -65,6 +65,8 @@ void cholesky_upper(Ctx &c, double *G, int64_t l, int64_t ld, int *flag);
 // G = RᵀR (l×l, ld) → Rinv = R⁻¹ (l×l upper, ld = l); G is overwritten.
 // Shifted retry and *flag protocol as cholesky_upper.
 void chol_inv_upper(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *flag);
+// the same on nb(nb+1)/2 cooperative CTAs (chol_df.cu), nb = ceil(l/32)
+void chol_inv_df(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *flag);
 // Rinv = R^-1 for upper triangular R (l×l)
 void tri_inv_upper(Ctx &c, const double *R, int64_t ld, double *Rinv, int64_t l);
 // symmetric eigendecomposition (cyclic Jacobi), S overwritten; V (l×l) gets

@@ -448,6 +448,11 @@ __global__ void __launch_bounds__(CI_T) k_chol_inv(double *G, int l, int64_t ld,
 }
 
 void chol_inv_upper(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *flag) {
+  // tile dataflow on many SMs while the lower triangle fits in co-resident CTAs
+  if (l > 64 && (l + 31) / 32 * ((l + 31) / 32 + 1) / 2 <= c.num_sms) {
+    chol_inv_df(c, G, l, ld, Rinv, flag);
+    return;
+  }
   if (l > CI_MAXL) {
     cholesky_upper(c, G, l, ld, flag);
     tri_inv_upper(c, G, ld, Rinv, l);
