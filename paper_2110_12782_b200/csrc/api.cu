@@ -207,6 +207,8 @@ int netmfp_graph_free(netmfp_graph *g) {
     // stream) may already be gone
     Graph *gg = g->g;
     gg->rowptr.s = gg->col.s = gg->deg.s = gg->heavy.s = gg->heavy_seg_ptr.s = nullptr;
+    gg->seg_e0.s = nullptr;
+    gg->seg_h.s = nullptr;
     delete gg;
     delete g;
   });

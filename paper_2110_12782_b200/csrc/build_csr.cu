@@ -53,6 +53,18 @@ __global__ void k_col_deg(const uint64_t *__restrict__ keys, int64_t nnz,
   }
 }
 
+__global__ void k_heavy_seg_map(const int32_t *__restrict__ heavy, int64_t nh, const int64_t *__restrict__ seg_ptr,
+                                const int64_t *__restrict__ rowptr, int64_t *__restrict__ seg_e0,
+                                int32_t *__restrict__ seg_h) {
+  const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (h >= nh) return;
+  const int64_t b = rowptr[heavy[h]];
+  for (int64_t sg = seg_ptr[h]; sg < seg_ptr[h + 1]; ++sg) {
+    seg_e0[sg] = b + (sg - seg_ptr[h]) * kHeavySeg;
+    seg_h[sg] = (int32_t)h;
+  }
+}
+
 __global__ void k_heavy_segs(const int32_t *__restrict__ heavy, int64_t nh,
                              const int32_t *__restrict__ deg, int64_t *__restrict__ nseg) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -145,6 +157,12 @@ Graph *build_csr_device(Ctx &c, int64_t n, const int32_t *src, const int32_t *ds
       NM_CUDA(cudaMemcpyAsync(&nsegs, g->heavy_seg_ptr.p + nh, 8, cudaMemcpyDeviceToHost, s));
       NM_CUDA(cudaStreamSynchronize(s));
       g->n_heavy_segs = nsegs;
+      // per segment: first entry and heavy-row index (no search in the SpMM)
+      g->seg_e0.alloc(nsegs > 0 ? nsegs : 1, s);
+      g->seg_h.alloc(nsegs > 0 ? nsegs : 1, s);
+      if (nh > 0)
+        NM_LAUNCH(c, "heavy_seg_map", k_heavy_seg_map<<<ceil_div(nh, 128), 128, 0, s>>>(
+                                          g->heavy, nh, g->heavy_seg_ptr, g->rowptr, g->seg_e0, g->seg_h));
     }
   } catch (...) {
     delete g;

@@ -240,12 +240,14 @@ struct Graph {
   int64_t heavy_nnz = 0;
   DBuf<int64_t> heavy_seg_ptr;  // per heavy row: first segment index (n_heavy+1)
   int64_t n_heavy_segs = 0;
+  DBuf<int64_t> seg_e0;  // per heavy segment: first entry
+  DBuf<int32_t> seg_h;   // per heavy segment: index into heavy
   int device = 0;
 };
 
 // rows with more neighbours than this are split across warps (spmm.cu)
-constexpr int kLightCap = 512;
-constexpr int kHeavySeg = 512;
+constexpr int kLightCap = 64;
+constexpr int kHeavySeg = 64;
 
 // ----------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al. SC'11) — the CUDA side's own implementation of

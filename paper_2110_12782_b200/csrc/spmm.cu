@@ -81,29 +81,20 @@ template <int LPR, bool SCOL>
 __global__ void __launch_bounds__(256) k_spmm_heavy(SpmmArgs p, const int64_t *__restrict__ rowptr,
                                                     const int32_t *__restrict__ col,
                                                     const int32_t *__restrict__ heavy,
-                                                    const int64_t *__restrict__ seg_ptr, int64_t nh,
-                                                    int64_t nsegs, float *__restrict__ hsum,
-                                                    int64_t ldh) {
+                                                    const int64_t *__restrict__ seg_e0,
+                                                    const int32_t *__restrict__ seg_h, int64_t nsegs,
+                                                    float *__restrict__ hsum, int64_t ldh) {
   constexpr int GPB = 256 / LPR;
   const int li = threadIdx.x % LPR;
   const int gi = threadIdx.x / LPR;
-  const unsigned gmask = (LPR == 32) ? 0xffffffffu
-                                     : (((1u << LPR) - 1u) << ((threadIdx.x % 32) / LPR * LPR));
   const int c = blockIdx.y * (LPR * 4) + li * 4;
   const bool active = c < p.cols;
-  int64_t sidx = (int64_t)blockIdx.x * GPB + gi;
+  const int64_t sidx = (int64_t)blockIdx.x * GPB + gi;
   if (sidx >= nsegs) return;
-  // heavy row owning this segment: largest h with seg_ptr[h] <= sidx
-  int64_t lo = 0, hi = nh - 1;
-  while (lo < hi) {
-    int64_t mid = (lo + hi + 1) >> 1;
-    if (seg_ptr[mid] <= sidx) lo = mid; else hi = mid - 1;
-  }
-  int64_t h = lo;
-  int u = heavy[h];
-  int64_t rb = rowptr[u], re = rowptr[u + 1];
-  int64_t e0 = rb + (sidx - seg_ptr[h]) * kHeavySeg;
-  int64_t e1 = min(e0 + (int64_t)kHeavySeg, re);
+  const int64_t h = __ldg(seg_h + sidx);
+  const int64_t e0 = __ldg(seg_e0 + sidx);
+  const int64_t re = __ldg(rowptr + __ldg(heavy + h) + 1);
+  const int64_t e1 = min(e0 + (int64_t)kHeavySeg, re);
   if (active) {
     float4 acc = gather_sum<SCOL>(col, e0, e1, p.X + c, (uint32_t)p.ldx, p.s_col);
     float *dst = hsum + h * ldh + c;
@@ -306,6 +297,234 @@ __global__ void __launch_bounds__(256) k_spmm_flat(SpmmArgs p, const int64_t *__
   }
 }
 
+// Segmented warp-per-32-rows SpMM.  A warp owns 32 consecutive rows and a
+// column pass of 128·NV columns (lane = NV float4 slices).  Their neighbour
+// lists are walked as one flat run: each 32-entry chunk loads its column
+// indices coalesced (one per lane), lanes find their row by a shuffle binary
+// search, and the X gathers of 8 entries are issued back to back (8·NV
+// independent 16-B loads per lane in flight) before the accumulation, which
+// flushes a row through the fused epilogue whenever the (warp-uniform) row
+// index advances.  Entries of heavy rows are skipped (their partial sums come
+// from k_spmm_heavy) and whole heavy ranges are jumped over.
+template <int NV, bool SCOL>
+__global__ void __launch_bounds__(256) k_spmm_seg(SpmmArgs p, const int64_t *__restrict__ rowptr,
+                                                  const int32_t *__restrict__ col, int64_t n,
+                                                  const int32_t *__restrict__ heavy, int64_t nh,
+                                                  const float *__restrict__ hsum, int64_t ldh) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  int cq[NV];
+  bool aq[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    cq[q] = blockIdx.y * (128 * NV) + (q * 32 + lane) * 4;
+    aq[q] = cq[q] < p.cols;
+  }
+  const uint32_t ldx = (uint32_t)p.ldx;
+  for (int64_t r0 = wid * 32; r0 < n; r0 += nwarps * 32) {
+    const int rows = (int)min((int64_t)32, n - r0);
+    const int64_t rs = __ldg(rowptr + r0 + min(lane, rows));
+    const int64_t re = __ldg(rowptr + r0 + min(lane + 1, rows));
+    const unsigned hmask = __ballot_sync(FULL, lane < rows && re - rs > kLightCap);
+    const int64_t E0 = __shfl_sync(FULL, rs, 0), E1 = __shfl_sync(FULL, re, rows - 1);
+    float4 acc[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int cur = 0;
+    // flush rows [cur, upto): row cur gets acc, later ones are empty (or heavy)
+    auto flush_to = [&](int upto) {
+      for (; cur < upto; ++cur) {
+        const int64_t u = r0 + cur;
+        const int64_t dg = __shfl_sync(FULL, re, cur) - __shfl_sync(FULL, rs, cur);
+        if ((hmask >> cur) & 1u) {
+          int64_t lo = 0, hi = nh - 1;
+          while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (__ldg(heavy + mid) < u) lo = mid + 1; else hi = mid;
+          }
+#pragma unroll
+          for (int q = 0; q < NV; ++q)
+            if (aq[q]) acc[q] = *reinterpret_cast<const float4 *>(hsum + lo * ldh + cq[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          if (aq[q]) row_epilogue(p, u, dg, acc[q], cq[q]);
+          acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+    };
+    int64_t e = E0;
+    while (e < E1) {
+      const int64_t idx = e + lane;
+      // row of this lane's entry: largest r with rs_r <= idx (shuffle binary search)
+      int lo = 0, hi = rows - 1;
+#pragma unroll
+      for (int it = 0; it < 5; ++it) {
+        const int mid = (lo + hi + 1) >> 1;
+        const int64_t v = __shfl_sync(FULL, rs, mid);
+        if (v <= idx) lo = mid; else hi = mid - 1;
+      }
+      const int myrow = idx < E1 ? lo : 32;
+      const int row0 = __shfl_sync(FULL, myrow, 0);
+      if ((hmask >> row0) & 1u) {  // chunk starts inside a heavy row: jump over it
+        e = __shfl_sync(FULL, re, row0);
+        continue;
+      }
+      const bool valid = idx < E1 && !((hmask >> myrow) & 1u);
+      const int32_t cv = valid ? __ldg(col + idx) : -1;
+#pragma unroll 1
+      for (int j = 0; j < 32; j += 8) {
+        float4 x[8][NV];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int32_t v = __shfl_sync(FULL, cv, j + t);
+          float sc = 1.f;
+          if (SCOL && v >= 0) sc = __ldg(p.s_col + v);
+#pragma unroll
+          for (int q = 0; q < NV; ++q) {
+            x[t][q] = (v >= 0 && aq[q]) ? __ldg(reinterpret_cast<const float4 *>(p.X + (uint64_t)(uint32_t)v * ldx + cq[q]))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (SCOL) { x[t][q].x *= sc; x[t][q].y *= sc; x[t][q].z *= sc; x[t][q].w *= sc; }
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int r = __shfl_sync(FULL, myrow, j + t);
+          if (r >= 32) break;
+          if (r != cur) flush_to(r);
+#pragma unroll
+          for (int q = 0; q < NV; ++q) acc[q] = f4_add(x[t][q], acc[q]);
+        }
+      }
+      e += 32;
+    }
+    flush_to(rows);
+  }
+}
+
+// Warp-per-row SpMM with a column pass of 128·NV columns (lane = NV float4
+// slices).  Per row: the row's column indices are loaded coalesced (one per
+// lane, 32 at a time) and broadcast by shuffles, and the X gathers of 8
+// neighbours are issued back to back (8·NV independent 16-B loads per lane)
+// before they are summed; the next row's rowptr pair is prefetched while the
+// current row is gathered.  Heavy rows take their sums from k_spmm_heavy.
+template <int NV, bool SCOL>
+__global__ void __launch_bounds__(256) k_spmm_wr(SpmmArgs p, const int64_t *__restrict__ rowptr,
+                                                 const int32_t *__restrict__ col, int64_t n,
+                                                 const int32_t *__restrict__ heavy, int64_t nh,
+                                                 const float *__restrict__ hsum, int64_t ldh) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  int cq[NV];
+  bool aq[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    cq[q] = blockIdx.y * (128 * NV) + (q * 32 + lane) * 4;
+    aq[q] = cq[q] < p.cols;
+  }
+  const uint32_t ldx = (uint32_t)p.ldx;
+  int64_t u = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  int64_t e0 = 0, e1 = 0;
+  if (u < n) {
+    e0 = __ldg(rowptr + u);
+    e1 = __ldg(rowptr + u + 1);
+  }
+  for (; u < n; u += nwarps) {
+    // prefetch the next row's range
+    const int64_t un = u + nwarps;
+    int64_t f0 = 0, f1 = 0;
+    if (un < n) {
+      f0 = __ldg(rowptr + un);
+      f1 = __ldg(rowptr + un + 1);
+    }
+    const int64_t dg = e1 - e0;
+    float4 acc[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (dg > kLightCap) {
+      int64_t lo = 0, hi = nh - 1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(heavy + mid) < u) lo = mid + 1; else hi = mid;
+      }
+#pragma unroll
+      for (int q = 0; q < NV; ++q)
+        if (aq[q]) acc[q] = *reinterpret_cast<const float4 *>(hsum + lo * ldh + cq[q]);
+    } else {
+      for (int64_t b = e0; b < e1; b += 32) {
+        const int cnt = (int)min((int64_t)32, e1 - b);
+        const int32_t cv = lane < cnt ? __ldg(col + b + lane) : 0;
+        for (int j = 0; j < cnt; j += 8) {
+          float4 x[8][NV];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int32_t v = __shfl_sync(FULL, cv, j + t);
+            const bool ok = j + t < cnt;
+            float sc = 1.f;
+            if (SCOL && ok) sc = __ldg(p.s_col + v);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+              x[t][q] = (ok && aq[q]) ? __ldg(reinterpret_cast<const float4 *>(p.X + (uint64_t)(uint32_t)v * ldx + cq[q]))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+              if (SCOL) { x[t][q].x *= sc; x[t][q].y *= sc; x[t][q].z *= sc; x[t][q].w *= sc; }
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+#pragma unroll
+            for (int q = 0; q < NV; ++q) acc[q] = f4_add(x[t][q], acc[q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+      if (aq[q]) row_epilogue(p, u, dg, acc[q], cq[q]);
+    e0 = f0;
+    e1 = f1;
+  }
+}
+
+template <int NV, bool SCOL>
+static void spmm_wr_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
+  constexpr int CW = 128 * NV;
+  const unsigned chunks = ceil_div(p.cols, CW);
+  DBuf<float> hsum;
+  int64_t ldh = pad4(p.cols);
+  if (g.n_heavy > 0) {
+    hsum.alloc((size_t)g.n_heavy * ldh, c.stream);
+    hsum.zero();
+    dim3 gh(ceil_div(g.n_heavy_segs, 8), ceil_div(p.cols, 128));
+    NM_LAUNCH(c, "spmm_heavy", k_spmm_heavy<32, SCOL><<<gh, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.heavy, g.seg_e0,
+                                                                                 g.seg_h, g.n_heavy_segs, hsum, ldh));
+  }
+  const int64_t blocks = ceil_div(g.n, 8);  // 8 warps, one row each per iteration
+  dim3 grid((unsigned)std::min<int64_t>(blocks, (int64_t)c.num_sms * 64), chunks);
+  NM_LAUNCH(c, "spmm_wr", k_spmm_wr<NV, SCOL><<<grid, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.n, g.heavy,
+                                                                            g.n_heavy, hsum.p, ldh));
+}
+
+template <int NV, bool SCOL>
+static void spmm_seg_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
+  constexpr int CW = 128 * NV;
+  const unsigned chunks = ceil_div(p.cols, CW);
+  DBuf<float> hsum;
+  int64_t ldh = pad4(p.cols);
+  if (g.n_heavy > 0) {
+    hsum.alloc((size_t)g.n_heavy * ldh, c.stream);
+    hsum.zero();
+    dim3 gh(ceil_div(g.n_heavy_segs, 8), chunks * NV);
+    NM_LAUNCH(c, "spmm_heavy", k_spmm_heavy<32, SCOL><<<gh, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.heavy, g.seg_e0,
+                                                                                 g.seg_h, g.n_heavy_segs, hsum, ldh));
+  }
+  const int64_t blocks = ceil_div(g.n, 256);  // 8 warps × 32 rows
+  dim3 grid((unsigned)std::min<int64_t>(blocks, (int64_t)c.num_sms * 16), chunks);
+  NM_LAUNCH(c, "spmm_seg", k_spmm_seg<NV, SCOL><<<grid, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.n, g.heavy,
+                                                                              g.n_heavy, hsum.p, ldh));
+}
+
 template <int LPR, bool SCOL>
 static void spmm_flat_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
   constexpr int GPB = 256 / LPR;
@@ -317,8 +536,8 @@ static void spmm_flat_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
     hsum.alloc((size_t)g.n_heavy * ldh, c.stream);
     hsum.zero();
     dim3 gh(ceil_div(g.n_heavy_segs, GPB), chunks);
-    NM_LAUNCH(c, "spmm_heavy", k_spmm_heavy<LPR, SCOL><<<gh, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.heavy, g.heavy_seg_ptr,
-                                                      g.n_heavy, g.n_heavy_segs, hsum, ldh));
+    NM_LAUNCH(c, "spmm_heavy", k_spmm_heavy<LPR, SCOL><<<gh, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.heavy, g.seg_e0, g.seg_h,
+                                                      g.n_heavy_segs, hsum, ldh));
   }
   const int64_t blocks = ceil_div(g.n, 256);  // 8 warps × 32 rows
   dim3 grid((unsigned)std::min<int64_t>(blocks, (int64_t)c.num_sms * 32), chunks);
@@ -337,8 +556,8 @@ static void spmm_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
     hsum.alloc((size_t)g.n_heavy * ldh, c.stream);
     hsum.zero();
     dim3 gh(ceil_div(g.n_heavy_segs, GPB), chunks);
-    NM_LAUNCH(c, "spmm_heavy", k_spmm_heavy<LPR, SCOL><<<gh, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.heavy, g.heavy_seg_ptr,
-                                                      g.n_heavy, g.n_heavy_segs, hsum, ldh));
+    NM_LAUNCH(c, "spmm_heavy", k_spmm_heavy<LPR, SCOL><<<gh, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.heavy, g.seg_e0, g.seg_h,
+                                                      g.n_heavy_segs, hsum, ldh));
   }
   // rows per group: enough blocks for ~16 resident 256-thread blocks per SM
   int64_t row_blocks = ceil_div(g.n, GPB);
@@ -365,6 +584,12 @@ void spmm(Ctx &c, const Graph &g, const SpmmArgs &p) {
     return;
   }
   switch (variant) {
+    case 21: spmm_wr_impl<1, false>(c, g, p); break;
+    case 22: spmm_wr_impl<2, false>(c, g, p); break;
+    case 23: spmm_wr_impl<3, false>(c, g, p); break;
+    case 11: spmm_seg_impl<1, false>(c, g, p); break;
+    case 12: spmm_seg_impl<2, false>(c, g, p); break;
+    case 13: spmm_seg_impl<3, false>(c, g, p); break;
     case 0: spmm_impl<8, false, 4>(c, g, p); break;
     case 1: spmm_impl<8, false, 5>(c, g, p); break;
     case 8: spmm_impl<16, false, 5>(c, g, p); break;
