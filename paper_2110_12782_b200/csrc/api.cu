@@ -1,5 +1,7 @@
 // api.cu — the C ABI of include/netmfp.h: argument checking, host/device
 // marshalling, error codes.  All compute is in the other translation units.
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -123,6 +125,21 @@ int netmfp_ctx_create(int device, void *stream, netmfp_ctx **out) {
     NM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
     NM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // reserve working memory up front (NETMFP_POOL_RESERVE_GB, default 24 GiB or
+    // half the free memory) so that steps never grow the pool mid-stream
+    {
+      size_t fr = 0, tot = 0;
+      NM_CUDA(cudaMemGetInfo(&fr, &tot));
+      const char *ev = getenv("NETMFP_POOL_RESERVE_GB");
+      size_t want = (size_t)(ev ? atof(ev) : 24.0) << 30;
+      want = std::min(want, fr / 2);
+      if (want > 0) {
+        void *tmp = nullptr;
+        if (cudaMallocAsync(&tmp, want, x->c.stream) == cudaSuccess) cudaFreeAsync(tmp, x->c.stream);
+        cudaGetLastError();
+        NM_CUDA(cudaStreamSynchronize(x->c.stream));
+      }
+    }
     *out = x;
   });
 }

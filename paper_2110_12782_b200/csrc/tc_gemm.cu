@@ -40,6 +40,14 @@
 #include "kernels.cuh"
 #include "tc_common.cuh"
 
+#ifdef TC_PROF
+__device__ unsigned long long g_tcprof[1024 * 8];
+#define TCP_T0() const unsigned long long _t0 = clock64()
+#define TCP_ADD(slot) atomicAdd(&g_tcprof[(blockIdx.x % 1024) * 8 + (slot)], clock64() - _t0)
+#else
+#define TCP_T0()
+#define TCP_ADD(slot)
+#endif
 namespace netmfp {
 namespace tc {
 
@@ -60,6 +68,7 @@ struct GramP {
   int na_blk, nb_blk;  // 32-col blocks staged of A and (if !sym) B
   int nunits;
   GUnit u[kMaxUnits];
+  int a3d, b3d;     // operand loaded as one 3-D box {32, BK, nblk} (ld covers all blocks)
   uint32_t tcols;   // TMEM allocation
   int stages;
   const int32_t *wdeg;  // optional row weights
@@ -112,9 +121,16 @@ __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUten
         uint8_t *st = base + s * stage_bytes;
         mbar_expect_tx(&full[s], (uint32_t)(nblk * BLK));
         const int row = (int)(r0 + (int64_t)kc * BK);
-        for (int b = 0; b < p.na_blk; ++b) tma_load_2d(st + b * BLK, &tmA, b * 32, row, &full[s]);
-        if (!SYM)
-          for (int b = 0; b < p.nb_blk; ++b) tma_load_2d(st + (p.na_blk + b) * BLK, &tmB, b * 32, row, &full[s]);
+        if (p.a3d)
+          tma_load_3d(st, &tmA, 0, row, 0, &full[s]);
+        else
+          for (int b = 0; b < p.na_blk; ++b) tma_load_2d(st + b * BLK, &tmA, b * 32, row, &full[s]);
+        if (!SYM) {
+          if (p.b3d)
+            tma_load_3d(st + p.na_blk * BLK, &tmB, 0, row, 0, &full[s]);
+          else
+            for (int b = 0; b < p.nb_blk; ++b) tma_load_2d(st + (p.na_blk + b) * BLK, &tmB, b * 32, row, &full[s]);
+        }
       }
     }
   } else if (warp == 1) {
@@ -264,12 +280,10 @@ struct GemmP {
   int K;          // contraction length
   int nk;         // K chunks of 32
   int ntot;       // MMA N total (multiple of 16)
-  int nsub, nsub_w;  // N subtiles (each <= 256)
-  int nbox, box_rows;  // TMA boxes for Bᵀ rows (box_rows each)
+  int nh, hr;     // output columns split into nh parts of hr (<= 256) columns
   int tri;        // B upper triangular: chunk kb touches columns >= 32 kb
-  int64_t ntiles;
+  int64_t nitems; // (M tile, part) work items
   int stages;
-  uint32_t tcols;
   float *C;
   int64_t ldc;
   int64_t ccols;  // valid output columns
@@ -277,19 +291,27 @@ struct GemmP {
   float rexp;
 };
 
-__global__ void __launch_bounds__(NT, 1) k_gemm_tc(const __grid_constant__ CUtensorMap tmA,
-                                                   const __grid_constant__ CUtensorMap tmBh,
-                                                   const __grid_constant__ CUtensorMap tmBl, const GemmP p) {
+// items = (M tile t, column part h), h fastest so that both parts of a tile
+// read the same A rows back to back (the second time from L2).  The A tile
+// goes to TMEM (hi and lo parts written by 4 "split" warps with tcgen05.st),
+// so the MMAs (kind::tf32, A from TMEM) only read Bᵀ from shared memory; every
+// item accumulates into one of two TMEM buffers and 4 separate epilogue warps
+// drain the previous one while the next item's MMAs run.
+// TMEM columns: acc[0] [0, hr), acc[1] [hr, 2hr), A stage s [2hr + 64s, +64).
+constexpr int NTG = 320;  // 10 warps: TMA, MMA, 4 split, 4 epilogue
+__global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUtensorMap tmA,
+                                                    const __grid_constant__ CUtensorMap tmBh, const GemmP p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = align1024(smem_raw);
-  constexpr int ABYTES = 128 * 128;  // 128 rows × 32 fp32
-  const int bbytes = p.ntot * 128;
-  const int stage_bytes = 2 * ABYTES + 2 * bbytes;
+  constexpr int ABYTES = 128 * 128;  // 128 rows × 32 fp32 (raw, SWIZZLE_128B)
+  const int bbytes = p.hr * 128;     // one part of Bᵀ (hi or lo)
+  const int stage_bytes = ABYTES + 2 * bbytes;
   const int S = p.stages;
   uint64_t *bars = reinterpret_cast<uint64_t *>(base + S * stage_bytes);
   uint64_t *full = bars, *split = bars + S, *empty = bars + 2 * S;
-  uint64_t *done = bars + 3 * S, *tfree = bars + 3 * S + 1;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * S + 2);
+  uint64_t *done = bars + 3 * S, *tfree = bars + 3 * S + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * S + 4);
+  float *tpose = reinterpret_cast<float *>(bars + 3 * S + 6);  // 4 warps × 32 × 33
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -298,124 +320,174 @@ __global__ void __launch_bounds__(NT, 1) k_gemm_tc(const __grid_constant__ CUten
       mbar_init(&split[s], kWorkers);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
-    mbar_init(tfree, kWorkers);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&done[b], 1);
+      mbar_init(&tfree[b], kWorkers);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 1) tmem_alloc(tmem_slot, p.tcols);
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t tA = tmem + (uint32_t)(2 * p.hr);
 
   if (warp == 0) {
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmBh);
-      tma_prefetch_desc(&tmBl);
       int64_t g = 0;
-      for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      for (int64_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
+        const int64_t t = it / p.nh;
+        const int h = (int)(it % p.nh);
         for (int kc = 0; kc < p.nk; ++kc, ++g) {
           const int s = (int)(g % S);
           const int64_t use = g / S;
-          if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
-          uint8_t *st = base + s * stage_bytes;
-          mbar_expect_tx(&full[s], (uint32_t)(ABYTES + 2 * p.nbox * p.box_rows * 128));
-          tma_load_2d(st, &tmA, kc * 32, (int)(t * 128), &full[s]);
-          uint8_t *bh = st + 2 * ABYTES, *bl = bh + bbytes;
-          for (int b = 0; b < p.nbox; ++b) {
-            tma_load_2d(bh + b * p.box_rows * 128, &tmBh, kc * 32, b * p.box_rows, &full[s]);
-            tma_load_2d(bl + b * p.box_rows * 128, &tmBl, kc * 32, b * p.box_rows, &full[s]);
+          if (use > 0) {
+            TCP_T0();
+            mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+            TCP_ADD(0);
           }
+          uint8_t *st = base + s * stage_bytes;
+          mbar_expect_tx(&full[s], (uint32_t)(ABYTES + 2 * bbytes));
+          tma_load_2d(st, &tmA, kc * 32, (int)(t * 128), &full[s]);
+          tma_load_4d(st + ABYTES, &tmBh, 0, 0, h, 2 * kc, &full[s]);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      int64_t g = 0, it = 0;
-      for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
-        if (it > 0) mbar_wait(tfree, (uint32_t)((it - 1) & 1));
+      int64_t g = 0, ic = 0;
+      for (int64_t it = blockIdx.x; it < p.nitems; it += gridDim.x, ++ic) {
+        const int h = (int)(it % p.nh);
+        const int buf = (int)(ic & 1);
+        const int64_t use_b = ic >> 1;
+        if (use_b > 0) {
+          TCP_T0();
+          mbar_wait(&tfree[buf], (uint32_t)((use_b - 1) & 1));
+          TCP_ADD(1);
+        }
         tc_fence_after();
+        const int pc0 = h * p.hr, pc1 = pc0 + p.hr;  // this part's output columns
         for (int kc = 0; kc < p.nk; ++kc, ++g) {
           const int s = (int)(g % S);
           const int64_t use = g / S;
-          mbar_wait(&split[s], (uint32_t)(use & 1));
+          {
+            TCP_T0();
+            mbar_wait(&split[s], (uint32_t)(use & 1));
+            TCP_ADD(2);
+          }
           tc_fence_after();
-          const uint32_t ahi = smem_u32(base + s * stage_bytes), alo = ahi + ABYTES;
-          const uint32_t bhi = alo + ABYTES, blo = bhi + bbytes;
-          for (int sb = 0; sb < p.nsub; ++sb) {
-            int c0 = sb * p.nsub_w;
-            const int c1 = c0 + p.nsub_w;
-            if (p.tri) {
-              const int cmin = (kc * 32) & ~15;
-              if (c1 <= cmin) continue;
-              c0 = max(c0, cmin);
-            }
-            const int N = c1 - c0;
+          const uint32_t bhi = smem_u32(base + s * stage_bytes) + ABYTES, blo = bhi + bbytes;
+          const uint32_t ahi = tA + (uint32_t)(64 * s), alo = ahi + 32;
+          int c0 = pc0;
+          if (p.tri) c0 = max(c0, (kc * 32) & ~15);
+          if (c0 < pc1) {
+            const int N = pc1 - c0;
             const uint32_t idesc = make_idesc(N, 0, 0);
-            const uint32_t d = tmem + (uint32_t)c0;
+            const uint32_t d = tmem + (uint32_t)(buf * p.hr + (c0 - pc0));
+            const uint32_t bo = (uint32_t)(c0 - pc0) * 128;
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {
               const uint32_t ko = ks * 32;
               // every column is first touched by K-chunk 0 (tri: chunk kb only
               // adds to columns >= 32 kb), so chunk 0 / kstep 0 starts the sums
               const uint32_t acc0 = (kc == 0 && ks == 0) ? 0u : 1u;
-              mma_tf32(d, make_desc(ahi + ko, 16, 1024), make_desc(bhi + c0 * 128 + ko, 16, 1024), idesc, acc0);
-              mma_tf32(d, make_desc(ahi + ko, 16, 1024), make_desc(blo + c0 * 128 + ko, 16, 1024), idesc, 1u);
-              mma_tf32(d, make_desc(alo + ko, 16, 1024), make_desc(bhi + c0 * 128 + ko, 16, 1024), idesc, 1u);
+              mma_tf32_ts(d, ahi + ks * 8, make_desc(bhi + bo + ko, 16, 1024), idesc, acc0);
+              mma_tf32_ts(d, ahi + ks * 8, make_desc(blo + bo + ko, 16, 1024), idesc, 1u);
+              mma_tf32_ts(d, alo + ks * 8, make_desc(bhi + bo + ko, 16, 1024), idesc, 1u);
             }
           }
           mma_commit(&empty[s]);
         }
-        mma_commit(done);
+        mma_commit(&done[buf]);
       }
     }
-  } else {
-    const int wt = threadIdx.x - 64;
+  } else if (warp < 6) {
+    // split warps: this thread's A row (raw, from the swizzled smem tile) → TMEM hi / lo
     const int q = warp & 3;
-    int64_t g = 0, it = 0;
-    for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
+    const int r = 32 * q + lane;
+    const int wt = threadIdx.x - 64;
+    int64_t g = 0;
+    for (int64_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
       for (int kc = 0; kc < p.nk; ++kc, ++g) {
         const int s = (int)(g % S);
         const int64_t use = g / S;
-        mbar_wait(&full[s], (uint32_t)(use & 1));
-        float4 *raw = reinterpret_cast<float4 *>(base + s * stage_bytes);
-        float4 *lo = raw + ABYTES / 16;
-        for (int i = wt; i < ABYTES / 16; i += kWorkers) {
-          const float4 v = raw[i];
-          lo[i] = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
-                              v.w - tf32_trunc(v.w));
+        {
+          TCP_T0();
+          mbar_wait(&full[s], (uint32_t)(use & 1));
+          if (wt == 0) TCP_ADD(3);
         }
-        fence_async_smem();
+        const uint8_t *rowp = base + s * stage_bytes + r * 128;
+        float hi[32], lo[32];
+#pragma unroll
+        for (int cch = 0; cch < 8; ++cch) {
+          const float4 v = *reinterpret_cast<const float4 *>(rowp + ((cch ^ (r & 7)) << 4));
+          hi[4 * cch] = v.x; hi[4 * cch + 1] = v.y; hi[4 * cch + 2] = v.z; hi[4 * cch + 3] = v.w;
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) lo[i] = hi[i] - tf32_trunc(hi[i]);
+        const uint32_t ta = tA + ((uint32_t)(32 * q) << 16) + (uint32_t)(64 * s);
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
+        tmem_wait_st();
+        tc_fence_before();
         mbar_arrive(&split[s]);
       }
-      mbar_wait(done, (uint32_t)(it & 1));
+    }
+  } else {
+    // epilogue warps: drain acc[buf] through a per-warp 32×32 smem transpose
+    const int q = warp & 3;
+    const int et = threadIdx.x - 192;
+    float *tb = tpose + (size_t)q * 32 * 33;
+    int64_t ic = 0;
+    for (int64_t it = blockIdx.x; it < p.nitems; it += gridDim.x, ++ic) {
+      const int64_t t = it / p.nh;
+      const int h = (int)(it % p.nh);
+      const int buf = (int)(ic & 1);
+      {
+        TCP_T0();
+        mbar_wait(&done[buf], (uint32_t)((ic >> 1) & 1));
+        if (et == 0) TCP_ADD(4);
+      }
+      TCP_T0();
       tc_fence_after();
-      const int64_t row = t * 128 + 32 * q + lane;
+      const int64_t r0 = t * 128 + 32 * q;
+      const int64_t row = r0 + lane;
       float sc = 1.f;
       if (p.deg && row < p.n) sc = deg_pow_dev(p.deg, row, p.rexp);
-      float *dst = p.C + row * p.ldc;
-      for (int c = 0; c < p.ntot; c += 16) {
-        float v[16];
-        tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c, v);
-        if (row < p.n && c < p.ccols) {
-          if (c + 16 <= p.ccols) {
+      const int pc0 = h * p.hr;
+      for (int c = 0; c < p.hr; c += 64) {
+        uint32_t v[2][32];
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * p.hr + c);
+        tmem_ld32_nowait(ta, v[0]);
+        if (c + 32 < p.hr) tmem_ld32_nowait(ta + 32, v[1]);
+        tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 16; i += 4)
-              *reinterpret_cast<float4 *>(dst + c + i) =
-                  make_float4(sc * v[i], sc * v[i + 1], sc * v[i + 2], sc * v[i + 3]);
-          } else {
-            for (int i = 0; c + i < p.ccols; ++i) dst[c + i] = sc * v[i];
+        for (int hh = 0; hh < 2; ++hh) {
+          if (c + 32 * hh >= p.hr) break;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) tb[lane * 33 + i] = sc * __uint_as_float(v[hh][i]);
+          __syncwarp();
+          const int cl = c + 32 * hh + lane;
+          const int col = pc0 + cl;
+          if (col < p.ccols && cl < p.hr) {
+#pragma unroll 8
+            for (int rr = 0; rr < 32; ++rr)
+              if (r0 + rr < p.n) p.C[(r0 + rr) * p.ldc + col] = tb[rr * 33 + lane];
           }
+          __syncwarp();
         }
       }
       tc_fence_before();
-      mbar_arrive(tfree);
+      mbar_arrive(&tfree[buf]);
+      if (et == 0) TCP_ADD(5);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, p.tcols);
+  if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
 }  // namespace tc
@@ -453,6 +525,31 @@ CUtensorMap make_map(const float *p, int64_t rows, int64_t cols, int64_t ld, int
                                            : CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(NETMFP_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
+CUtensorMap make_map_nd(const float *p, int rank, const int64_t *dims, const int64_t *strides_bytes, const int *box,
+                        MapSwizzle sw) {
+  NM_REQUIRE(((uintptr_t)p & 15) == 0 && rank >= 1 && rank <= 5, "tensor map: alignment / rank");
+  CUtensorMap m;
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = (cuuint64_t)dims[i];
+    b[i] = (cuuint32_t)box[i];
+    es[i] = 1u;
+  }
+  for (int i = 0; i + 1 < rank; ++i) {
+    NM_REQUIRE(strides_bytes[i] % 16 == 0, "tensor map: strides must be multiples of 16 B");
+    st[i] = (cuuint64_t)strides_bytes[i];
+  }
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float *>(p), d, st, b, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           sw == SW128_32B ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                           : sw == SW64    ? CU_TENSOR_MAP_SWIZZLE_64B
+                                           : CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(NETMFP_ERR_CUDA, "cuTensorMapEncodeTiled (nd) failed: " + std::to_string((int)r));
   return m;
 }
 
@@ -545,8 +642,18 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
   int64_t nchain = std::max<int64_t>(1, std::min<int64_t>((int64_t)c.num_sms * waves, ceil_div(n, BK)));
   const int64_t kslab = (ceil_div(n, nchain) + BK - 1) / BK * BK;
   nchain = ceil_div(n, kslab);
-  CUtensorMap ma = make_map(A.p, n, a, A.ld, BK, SW128_32B);
-  CUtensorMap mb = sym ? ma : make_map(B.p, n, b, B.ld, BK, SW128_32B);
+  // one 3-D box per operand when the row pitch covers every 32-column block
+  // (the view then reads the ld padding of the last block: those columns only
+  // feed output rows/cols >= a, b, which are never reduced)
+  const bool a3d = A.ld >= 32 * na_blk, b3d = B.ld >= 32 * nb_blk;
+  auto map3 = [&](const Mat &M, int nblk) {
+    const int64_t dims[3] = {32, n, nblk};
+    const int64_t str[2] = {M.ld * 4, 128};
+    const int box[3] = {32, BK, nblk};
+    return make_map_nd(M.p, 3, dims, str, box, SW128_32B);
+  };
+  CUtensorMap ma = a3d ? map3(A, na_blk) : make_map(A.p, n, a, A.ld, BK, SW128_32B);
+  CUtensorMap mb = sym ? ma : (b3d ? map3(B, nb_blk) : make_map(B.p, n, b, B.ld, BK, SW128_32B));
   DBuf<float> part((size_t)nchain * total, c.stream);
   for (auto &grp : groups) {
     GramP p{};
@@ -561,6 +668,8 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
       w += grp[i].nw;
     }
     p.tcols = tmem_cols_for(w);
+    p.a3d = a3d ? 1 : 0;
+    p.b3d = b3d ? 1 : 0;
     p.wdeg = deg;
     p.wexp = wexp;
     p.part_stride = total;
@@ -586,12 +695,14 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
   NM_LAUNCH(c, "tc_gram_reduce", k_gram_reduce2<<<ceil_div(a * b, 256), 256, 0, c.stream>>>(tmp.p, RG, a, b, G, ldg));
 }
 
-// Bᵀ hi/lo: Bt_hi[j][k] = rna_tf32(B[k][j]), Bt_lo[j][k] = (float)(B[k][j] - hi), zero padded
-__global__ void k_bt_split(const double *__restrict__ Bs, int64_t ldb, int64_t K, int64_t N, int64_t nrows, int64_t ldt,
-                           float *__restrict__ hi, float *__restrict__ lo) {
+// Bᵀ hi/lo for the TMA, chunk-major: Bt[kc][part][j][kk] (part 0 = hi = rna_tf32(B[k][j]),
+// part 1 = lo = B − hi, k = 32 kc + kk), zero padded to nrows × 32 nk
+__global__ void k_bt_split(const double *__restrict__ Bs, int64_t ldb, int64_t K, int64_t N, int64_t nrows, int64_t nk,
+                           float *__restrict__ Bt) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= nrows * ldt) return;
-  const int64_t j = idx / ldt, k = idx % ldt;
+  if (idx >= nk * nrows * 32) return;
+  const int64_t kk = idx & 31, j = (idx >> 5) % nrows, kc = idx / (32 * nrows);
+  const int64_t k = kc * 32 + kk;
   float h = 0.f, l = 0.f;
   if (j < N && k < K) {
     const double x = Bs[k * ldb + j];
@@ -600,8 +711,9 @@ __global__ void k_bt_split(const double *__restrict__ Bs, int64_t ldb, int64_t K
     h = __uint_as_float(r);
     l = (float)(x - (double)h);
   }
-  hi[idx] = h;
-  lo[idx] = l;
+  float *base = Bt + kc * 2 * nrows * 32;
+  base[j * 32 + kk] = h;
+  base[nrows * 32 + j * 32 + kk] = l;
 }
 
 // C[n×b] = rs ⊙ (A[n×a] · Bs[a×b])
@@ -609,50 +721,48 @@ static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ld
                               float rexp, const Mat &C, bool tri) {
   using namespace tc;
   const int64_t n = A.rows, K = A.cols;
+  // output columns in nh parts of hr (multiple of 16, <= 192) so that two
+  // accumulators and the TMEM A stages fit the 512 TMEM columns
   const int c16 = (int)((bcols + 15) / 16) * 16;
-  const int nsub = (c16 + 255) / 256;
-  const int nsub_w = ((c16 / nsub) + 15) / 16 * 16;
-  const int ntot = nsub * nsub_w;
-  NM_REQUIRE(ntot <= 304, "tc_gemm_tall: at most 304 output columns per call");
-  const int nbox = (ntot + 255) / 256;
-  const int box_rows = ntot / nbox;  // multiple of 8 (ntot multiple of 16, nbox <= 2)
-  NM_REQUIRE(box_rows % 8 == 0 && box_rows * nbox == ntot, "tc_gemm_tall: box split");
-  const int64_t ldt = pad32(K);
-  DBuf<float> bh((size_t)ntot * ldt, c.stream), bl((size_t)ntot * ldt, c.stream);
-  NM_LAUNCH(c, "bt_split", k_bt_split<<<ceil_div((int64_t)ntot * ldt, 256), 256, 0, c.stream>>>(Bs, ldb, K, bcols, ntot,
-                                                                                                   ldt, bh.p, bl.p));
+  const int nh = (c16 + 191) / 192;
+  const int hr = ((c16 + nh - 1) / nh + 15) / 16 * 16;
+  const int ntot = nh * hr;
+  const int64_t nk = ceil_div(K, 32);
+  DBuf<float> bt((size_t)nk * 2 * ntot * 32, c.stream);
+  NM_LAUNCH(c, "bt_split", k_bt_split<<<ceil_div(nk * ntot * 32, 256), 256, 0, c.stream>>>(Bs, ldb, K, bcols, ntot, nk,
+                                                                                             bt.p));
   CUtensorMap ma = make_map(A.p, n, K, A.ld, 128);
-  CUtensorMap mh = make_map(bh.p, ntot, ldt, ldt, box_rows);
-  CUtensorMap ml = make_map(bl.p, ntot, ldt, ldt, box_rows);
+  const int64_t bdims[4] = {32, hr, nh, 2 * nk};
+  const int64_t bstr[3] = {128, (int64_t)hr * 128, (int64_t)ntot * 128};
+  const int bbox[4] = {32, hr, 1, 2};  // one part (hi + lo) per box
+  CUtensorMap mb = make_map_nd(bt.p, 4, bdims, bstr, bbox, SW128);
   GemmP p{};
   p.n = n;
   p.K = (int)K;
-  p.nk = (int)ceil_div(K, 32);
+  p.nk = (int)nk;
   p.ntot = ntot;
-  p.nsub = nsub;
-  p.nsub_w = nsub_w;
-  p.nbox = nbox;
-  p.box_rows = box_rows;
+  p.nh = nh;
+  p.hr = hr;
   p.tri = tri ? 1 : 0;
-  p.ntiles = ceil_div(n, 128);
-  p.tcols = tmem_cols_for(ntot);
+  p.nitems = ceil_div(n, 128) * nh;
   p.C = C.p;
   p.ldc = C.ld;
   p.ccols = bcols;
   p.deg = deg;
   p.rexp = rexp;
-  const size_t stage = (size_t)2 * 128 * 128 + (size_t)2 * ntot * 128;
-  const int S = (int)std::min<size_t>(4, (kSmemMax - 1024 - 256) / stage);
+  const size_t tpose = (size_t)4 * 32 * 33 * 4;
+  const size_t stage = (size_t)128 * 128 + (size_t)2 * hr * 128;
+  const int S = (int)std::min<size_t>(std::min<size_t>(4, (512 - 2 * hr) / 64), (kSmemMax - 1024 - 256 - tpose) / stage);
   NM_REQUIRE(S >= 2, "tc_gemm_tall: stage does not fit");
   p.stages = S;
-  const size_t smem = 1024 + S * stage + (3 * S + 3) * 8 + 16;
+  const size_t smem = 1024 + S * stage + (3 * S + 6) * 8 + tpose;
   static bool attr = false;
   if (!attr) {
     NM_CUDA(cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
     attr = true;
   }
-  const int64_t grid = std::min<int64_t>(p.ntiles, c.num_sms);
-  NM_LAUNCH(c, "tc_gemm_tall", k_gemm_tc<<<(unsigned)grid, NT, smem, c.stream>>>(ma, mh, ml, p));
+  const int64_t grid = std::min<int64_t>(p.nitems, c.num_sms);
+  NM_LAUNCH(c, "tc_gemm_tall", k_gemm_tc<<<(unsigned)grid, NTG, smem, c.stream>>>(ma, mb, p));
 }
 
 void tc_gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcols, const int32_t *deg, float rexp,
