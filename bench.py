@@ -283,8 +283,17 @@ def run_ours(args):
         alg_bytes = n_spmm_l * bytes_l + n_spmm_d * bytes_d
         per_step_ms = spmm_ms / args.steps
         achieved = alg_bytes / (per_step_ms * 1e-3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
+        if os.path.exists(tp) and args.workload == 2:
+            tj = json.load(open(tp))["spmm_family_bytes_per_application"]
+            traffic = (n_spmm_l * tj["freigs_n_x_286"] + n_spmm_d * tj["chebyshev_n_x_128"]) / (n_spmm_l + n_spmm_d)
         roof = {"kernel": "spmm (spmm_rows + spmm_heavy)", "bound": "hbm", "achieved": achieved,
-                "peak": peaks["hbm"], "unit": "GB/s", "frac": achieved / peaks["hbm"], "traffic": None,
+                "peak": peaks["hbm"], "unit": "GB/s", "frac": achieved / peaks["hbm"],
+                "traffic": traffic,
+                "traffic_note": "ncu dram read+write bytes per SpMM application (rows+heavy launches), "
+                                "profiles/r01_traffic.json; algorithmic bytes per application: "
+                                f"{alg_bytes / (n_spmm_l + n_spmm_d):.4g}",
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peaks['src']})",
                 "share_of_step": per_step_ms / ms,
                 "edge_cols_per_s": (n_spmm_l * nnz * l + n_spmm_d * nnz * d) / (per_step_ms * 1e-3),

@@ -8,7 +8,8 @@ nsass = int(sys.argv[sys.argv.index("--sass") + 1]) if "--sass" in sys.argv else
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(raw)))
 h = r[0]
-want = [("gpu__time_duration.sum", "ms"), ("dram__bytes_read.sum", "GB rd"), ("dram__bytes_write.sum", "GB wr"),
+units = r[1]
+want = [("gpu__time_duration.sum", "time"), ("dram__bytes_read.sum", "GB rd"), ("dram__bytes_write.sum", "GB wr"),
         ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram%"),
         ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm%"),
         ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor%"),
@@ -22,7 +23,7 @@ for row in r[2:]:
     if kre and not re.search(kre, name):
         continue
     print(name[:90])
-    print("   " + "  ".join(f"{lab}={row[i]}" for i, lab in cols))
+    print("   " + "  ".join(f"{lab}={row[i]}{'[' + units[i] + ']' if units[i] in ('us', 'ms', 'ns', 'Gbyte', 'Mbyte', 'Kbyte', 'byte') else ''}" for i, lab in cols))
 if nsass:
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] +
                          (["-k", "regex:" + kre] if kre else []), capture_output=True, text=True).stdout
