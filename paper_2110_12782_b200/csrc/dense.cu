@@ -245,10 +245,11 @@ __global__ void k_gaussian(Mat O, uint32_t k0, uint32_t k1, const int32_t *__res
   int64_t i = idx / O.cols, j = idx % O.cols;
   U4 ctr{(uint32_t)j, (uint32_t)(i & 0xFFFFFFFF), (uint32_t)((uint64_t)i >> 32), kTagOmega};
   U4 w = philox4x32_10(ctr, k0, k1);
-  double u0 = ((double)w.x + 0.5) * 2.3283064365386963e-10;  // 2^-32
-  double u1 = ((double)w.y + 0.5) * 2.3283064365386963e-10;
-  double g = sqrt(-2.0 * log(u0)) * cospi(2.0 * u1);
-  O.p[i * O.ld + j] = (float)g * dpow_scale(deg, i, rexp);
+  // Box–Muller in fp32 (the block is fp32; |error| ~1e-7 relative to the fp64 oracle)
+  const float u0 = ((float)w.x + 0.5f) * 2.3283064365386963e-10f;  // 2^-32
+  const float u1 = ((float)w.y + 0.5f) * 2.3283064365386963e-10f;
+  const float g = sqrtf(-2.f * logf(u0)) * cospif(2.f * u1);
+  O.p[i * O.ld + j] = g * dpow_scale(deg, i, rexp);
 }
 
 void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, float rexp) {
@@ -261,6 +262,29 @@ __global__ void k_row_scale(Mat Y, const int32_t *__restrict__ deg, float rexp) 
   if (idx >= Y.rows * Y.cols) return;
   int64_t i = idx / Y.cols, j = idx % Y.cols;
   Y.p[i * Y.ld + j] *= dpow_scale(deg, i, rexp);
+}
+
+// Dst[i, :] = d_i^-e · Src[i, :]  (float4; lds, ldd, cols multiples of 4 or tail handled)
+__global__ void k_scale_copy(Mat Src, Mat Dst, const int32_t *__restrict__ deg, float rexp) {
+  const int64_t c4 = (Src.cols + 3) / 4;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= Src.rows * c4) return;
+  const int64_t i = idx / c4, j = (idx % c4) * 4;
+  const float sc = dpow_scale(deg, i, rexp);
+  const float *src = Src.p + i * Src.ld + j;
+  float *dst = Dst.p + i * Dst.ld + j;
+  if (j + 4 <= Src.cols) {
+    const float4 v = *reinterpret_cast<const float4 *>(src);
+    *reinterpret_cast<float4 *>(dst) = make_float4(sc * v.x, sc * v.y, sc * v.z, sc * v.w);
+  } else {
+    for (int64_t t = j; t < Src.cols; ++t) dst[t - j] = sc * src[t - j];
+  }
+}
+
+void scale_copy_block(Ctx &c, const Mat &Src, const Mat &Dst, const int32_t *deg, float rexp) {
+  NM_REQUIRE(Src.ld % 4 == 0 && Dst.ld % 4 == 0, "scale_copy: ld % 4 == 0");
+  const int64_t tot = Src.rows * ((Src.cols + 3) / 4);
+  NM_LAUNCH(c, "scale_copy", k_scale_copy<<<ceil_div(tot, 256), 256, 0, c.stream>>>(Src, Dst, deg, rexp));
 }
 
 void row_scale_block(Ctx &c, const Mat &Y, const int32_t *deg, float rexp) {

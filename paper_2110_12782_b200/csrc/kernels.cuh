@@ -51,6 +51,8 @@ void gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, const 
 bool tc_enabled();
 // Ω = randn(n, l) from Philox [R1], row-scaled by d_i^-e (deg != null)
 void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, float rexp);
+// Dst[i, :] = d_i^-e Src[i, :]
+void scale_copy_block(Ctx &c, const Mat &Src, const Mat &Dst, const int32_t *deg, float rexp);
 // Y[i, :] *= d_i^-e
 void row_scale_block(Ctx &c, const Mat &Y, const int32_t *deg, float rexp);
 // copy with ld conversion (device-to-device)

@@ -114,8 +114,7 @@ void factor_pair(Ctx &c, const Graph &g, double alpha, int T, const Mat &U, cons
   NM_CUDA(cudaMemcpyAsync(C, acc.p, (size_t)k * k * 8, cudaMemcpyDeviceToDevice, s));
   scale_cols64(c, C, k, k, k, lam, 1);
   // F = D^(-1+α) U
-  copy_block(c, U.p, U.ld, F.p, F.ld, U.rows, U.cols);
-  row_scale_block(c, F, g.deg, (float)(1.0 - alpha));
+  scale_copy_block(c, U, F, g.deg, (float)(1.0 - alpha));
 }
 
 __global__ void k_sqrt_abs(const double *lam, int d, double *out) {

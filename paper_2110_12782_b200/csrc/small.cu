@@ -667,6 +667,64 @@ __global__ void k_bisect(const double *__restrict__ d, const double *__restrict_
   w[m] = 0.5 * (lo + hi);
 }
 
+// Eigenvalue m (ascending) by multisection: one warp per eigenvalue, the 32
+// lanes evaluate Sturm counts at 32 interior points of the current bracket
+// and a ballot picks the sub-interval holding the m-th eigenvalue (5 bits per
+// round instead of 1); T's diagonal / off-diagonal squares live in shared memory.
+constexpr int MSW = 8;  // warps (eigenvalues) per block
+__global__ void __launch_bounds__(MSW * 32) k_multisect(const double *__restrict__ d, const double *__restrict__ e,
+                                                        int l, double *__restrict__ w) {
+  extern __shared__ double ms_sh[];
+  double *sd = ms_sh, *se2 = ms_sh + l;
+  for (int i = threadIdx.x; i < l; i += blockDim.x) {
+    sd[i] = d[i];
+    se2[i] = (i + 1 < l) ? e[i] * e[i] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int m = blockIdx.x * MSW + (threadIdx.x >> 5);
+  // Gershgorin bracket and pivmin (all lanes, then reduce)
+  double lo = 1e300, hi = -1e300, emax = 0.0;
+  for (int i = lane; i < l; i += 32) {
+    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < l ? fabs(e[i]) : 0.0);
+    lo = fmin(lo, sd[i] - r);
+    hi = fmax(hi, sd[i] + r);
+    emax = fmax(emax, se2[i]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  }
+  if (m >= l) return;
+  const double tnorm = fmax(fabs(lo), fabs(hi));
+  const double eps = 2.220446049250313e-16;
+  const double pivmin = fmax(1e-300, 4.0 * 2.2250738585072014e-308 * fmax(1.0, emax));
+  lo -= 2.0 * eps * tnorm + pivmin;
+  hi += 2.0 * eps * tnorm + pivmin;
+  for (int it = 0; it < 40; ++it) {
+    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin) break;
+    const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
+    int cnt = 0;
+    double q = sd[0] - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0;
+    for (int i = 1; i < l; ++i) {
+      q = sd[i] - x - se2[i - 1] / q;
+      if (fabs(q) < pivmin) q = -pivmin;
+      cnt += q < 0;
+    }
+    const unsigned above = __ballot_sync(0xffffffffu, cnt > m);
+    const int jf = above ? __ffs(above) - 1 : 32;  // first point past eigenvalue m
+    const double nlo = jf == 0 ? lo : lo + (hi - lo) * (double)jf / 33.0;
+    const double nhi = jf == 32 ? hi : lo + (hi - lo) * (double)(jf + 1) / 33.0;
+    if (!(nhi < hi || nlo > lo)) break;  // no progress at this precision
+    lo = nlo;
+    hi = nhi;
+  }
+  if (lane == 0) w[m] = 0.5 * (lo + hi);
+}
+
 // Inverse iteration (dstein-style): one warp per cluster of (near-)degenerate
 // eigenvalues, gap <= 1e-9 ||T|| (isolated eigenvalues converge to vectors whose
 // mutual angle is ~eps ||T|| / gap).  The LU of T - sigma I (dgttrf with partial
@@ -854,7 +912,7 @@ void sym_eig(Ctx &c, double *S, int64_t l64, double *lam, double *V, bool abs_or
     attr = true;
   }
   NM_LAUNCH(c, "tridiag", k_tridiag<<<TDC, TDT, smem, s>>>(S, l, d, e, Hv, hb));
-  NM_LAUNCH(c, "bisect", k_bisect<<<ceil_div(l, 64), 64, 0, s>>>(d, e, l, w));
+  NM_LAUNCH(c, "multisect", k_multisect<<<ceil_div(l, MSW), MSW * 32, (size_t)2 * l * sizeof(double), s>>>(d, e, l, w));
   DBuf<int> cst(l + 1, s), ncl(1, s);
   NM_LAUNCH(c, "clusters", k_clusters<<<1, 32, 0, s>>>(w, d, e, l, cst, ncl));
   int hncl = 0;
