@@ -346,6 +346,69 @@ def run_ours(args):
     return 0
 
 
+def run_dist(args):
+    """--dist: ONE graph row-partitioned over all ranks (north_star):
+    NCCL all-gather of the SpMM input rows, all-reduced Grams.  Strong scaling."""
+    import torch
+    import torch.distributed as td
+    ws, rank, local = dist_init()
+    torch.cuda.set_device(local)
+    import __graft_entry__ as ge
+    ge.build()
+    from paper_2110_12782_b200 import _lib as L
+    from paper_2110_12782_b200 import inputs
+    w, spec = workload(args.workload)
+    n, s_np, t_np = inputs.make_graph(spec)
+    dev = torch.device("cuda", local)
+    src = torch.from_numpy(s_np).to(dev)
+    dst = torch.from_numpy(t_np).to(dev)
+    ctx = L.Context(local)
+    uid = [L.netmfp_dist_unique_id() if rank == 0 else None]
+    if ws > 1:
+        td.broadcast_object_list(uid, src=0)
+    L.netmfp_dist_init(ctx, uid[0], ws, rank)
+    gfull = L.netmfp_build_csr(ctx, n, src, dst)
+    rp, _, _ = gfull.export(ctx)
+    bounds = L.netmfp_partition_rows(rp, ws)
+    del gfull
+    g = L.netmfp_dist_build_csr(ctx, n, src, dst, bounds)
+    prm = L.make_params(**w.params())
+    nl = g.n
+    E = torch.zeros(nl, (w.d + 31) // 32 * 32, dtype=torch.float32, device=dev)[:, :w.d]
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        L.netmfp_embed(ctx, g, prm, E)
+    clocks = ClockSampler(local)
+    barrier(ws)
+    torch.cuda.synchronize()
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ctx.launches
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        L.netmfp_embed(ctx, g, prm, E)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    clk = clocks.stop()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    ms_max = allreduce_max(ms, ws)
+    if rank == 0:
+        line = {"metric": METRIC, "value": ms_max / 1e3, "unit": "s", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": False, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"configs[{args.workload}] {w.name}", "n": n, "mode": "row-partitioned",
+                           "bounds": [int(b) for b in bounds], "parallelism": f"rows{ws}",
+                           "l2": "flushed by a 512 MiB write between timed steps"},
+                "gpu_launches": int((ctx.launches - launches0) // args.steps), "clocks": clk}
+        print(json.dumps(line))
+    if ws > 1:
+        td.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -354,9 +417,12 @@ def main():
     ap.add_argument("--workload", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist", action="store_true", help="one graph row-partitioned over all ranks (strong scaling)")
     args = ap.parse_args()
     if args.impl == "reference":
         sys.exit(run_reference(args))
+    if args.dist:
+        sys.exit(run_dist(args))
     sys.exit(run_ours(args))
 
 

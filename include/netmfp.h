@@ -43,6 +43,8 @@ extern "C" {
 #define NETMFP_ERR_OOM 4      /* device allocation failed                                */
 #define NETMFP_ERR_NCCL 5     /* collective failed (multi-GPU)                           */
 
+#define NETMFP_DIST_ID_BYTES 128  /* size of the communicator id (ncclUniqueId) */
+
 #define NETMFP_MEM_DEVICE 0
 #define NETMFP_MEM_HOST 1
 
@@ -107,6 +109,34 @@ int netmfp_graph_free(netmfp_graph *g);
 /* Split rows into `parts` contiguous ranges of near-equal nnz + rows cost
  * (north_star: "the CSR is row-partitioned"); bounds int64[parts+1], host. */
 int netmfp_partition_rows(const int64_t *rowptr_host, int64_t n, int32_t parts, int64_t *bounds);
+
+/* ---- multi-GPU: row-partitioned CSR (north_star) ------------------------------
+ * One process per GPU.  Rank r owns rows [bounds[r], bounds[r+1]) of the graph
+ * and of every n×c block; each SpMM all-gathers its input block (NCCL
+ * broadcasts from every rank into one n×c buffer, over NVLink), Gram
+ * matrices and the sketch's gathered rows are all-reduced, the small fp64
+ * problems are replicated, and Ω, Ψ, Π are counter-based (every rank draws its
+ * own rows).  With one rank (the default) no collective is issued.  NCCL is
+ * loaded at run time (libnccl.so.2); failures return NETMFP_ERR_NCCL. */
+/* Write a fresh communicator id (NETMFP_DIST_ID_BYTES bytes, host) on one rank. */
+int netmfp_dist_unique_id(void *id);
+/* Join the communicator (collective over all ranks; the context's device). */
+int netmfp_dist_init(netmfp_ctx *ctx, const void *id, int32_t nranks, int32_t rank);
+/* Build this rank's CSR rows [bounds[rank], bounds[rank+1]) (bounds: nranks+1
+ * host int64, 0 .. n; NULL = equal row counts; netmfp_partition_rows gives an
+ * nnz-balanced split) with global column ids.  src/dst must contain every
+ * (undirected) edge incident to those rows (the full list is fine).  Collective
+ * (vol(G) is all-reduced).  Then netmfp_embed / netmfp_eig / netmfp_propagate
+ * on this graph take and return this rank's rows of every n×c block. */
+int netmfp_dist_build_csr(netmfp_ctx *ctx, int64_t n, const int32_t *src, const int32_t *dst, int64_t m_in,
+                          const int64_t *bounds, int mem, netmfp_graph **out);
+/* CSR of rows [row0, row1) only (global column ids; no communicator; vol(G)
+ * reported is the local nnz).  netmfp_spmm on such a graph takes the FULL n×c
+ * input block and writes the row1−row0 output rows — one rank's SpMM. */
+int netmfp_build_csr_rows(netmfp_ctx *ctx, int64_t n, const int32_t *src, const int32_t *dst, int64_t m_in,
+                          int64_t row0, int64_t row1, int mem, netmfp_graph **out);
+/* First global row, n, vol(G) of a (possibly partitioned) graph. */
+int netmfp_graph_rows(const netmfp_graph *g, int64_t *row0, int64_t *n_global, int64_t *nnz_global);
 
 /* ---- a2: the normalized SpMM (the hot operator) --------------------------- */
 

@@ -65,7 +65,13 @@ _SIGS = {
     "netmfp_cheb_coeffs": (C.c_int, [_i32, _d, _d, _p]),
     "netmfp_embed": (C.c_int, [_p, _p, C.POINTER(Params), _p, _i64, _p, _p, C.c_int]),
     "netmfp_embed_edges": (C.c_int, [_p, _i64, _p, _p, _i64, C.POINTER(Params), _p, _i64, _p, C.c_int]),
+    "netmfp_dist_unique_id": (C.c_int, [_p]),
+    "netmfp_dist_init": (C.c_int, [_p, _p, _i32, _i32]),
+    "netmfp_dist_build_csr": (C.c_int, [_p, _i64, _p, _p, _i64, _p, C.c_int, C.POINTER(_p)]),
+    "netmfp_graph_rows": (C.c_int, [_p, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)]),
+    "netmfp_build_csr_rows": (C.c_int, [_p, _i64, _p, _p, _i64, _i64, _i64, C.c_int, C.POINTER(_p)]),
 }
+DIST_ID_BYTES = 128
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_L, _name)
     _f.restype = _res
@@ -218,6 +224,48 @@ def netmfp_build_csr(ctx: Context, n: int, src, dst) -> Graph:
     g = Graph(h)
     g.ctx = ctx  # keep the creating context alive as long as the graph
     return g
+
+
+def netmfp_dist_unique_id() -> bytes:
+    """A fresh communicator id (rank 0 creates it; share it, e.g. with
+    torch.distributed.broadcast_object_list)."""
+    buf = C.create_string_buffer(DIST_ID_BYTES)
+    _check(_L.netmfp_dist_unique_id(buf))
+    return buf.raw
+
+
+def netmfp_dist_init(ctx: Context, uid: bytes, nranks: int, rank: int) -> None:
+    buf = C.create_string_buffer(bytes(uid), DIST_ID_BYTES)
+    _check(_L.netmfp_dist_init(ctx.h, buf, nranks, rank))
+
+
+def netmfp_dist_build_csr(ctx: Context, n: int, src, dst, bounds=None) -> Graph:
+    """This rank's rows of the row-partitioned CSR (collective)."""
+    mem = _same_mem(src, dst)
+    h = _p()
+    b = None if bounds is None else np.ascontiguousarray(bounds, dtype=np.int64)
+    _check(_L.netmfp_dist_build_csr(ctx.h, n, _ptr(src), _ptr(dst), len(src), None if b is None else b.ctypes.data,
+                                    mem, C.byref(h)))
+    g = Graph(h)
+    g.ctx = ctx
+    return g
+
+
+def netmfp_build_csr_rows(ctx: Context, n: int, src, dst, row0: int, row1: int) -> Graph:
+    """CSR of rows [row0, row1) with global column ids (one rank's partition)."""
+    mem = _same_mem(src, dst)
+    h = _p()
+    _check(_L.netmfp_build_csr_rows(ctx.h, n, _ptr(src), _ptr(dst), len(src), row0, row1, mem, C.byref(h)))
+    g = Graph(h)
+    g.ctx = ctx
+    return g
+
+
+def netmfp_graph_rows(g: Graph):
+    """(first global row, n, vol(G))."""
+    r0, ng, vol = _i64(), _i64(), _i64()
+    _check(_L.netmfp_graph_rows(g.h, C.byref(r0), C.byref(ng), C.byref(vol)))
+    return r0.value, ng.value, vol.value
 
 
 def netmfp_partition_rows(rowptr: np.ndarray, parts: int) -> np.ndarray:

@@ -16,9 +16,24 @@ OUT = os.path.join(HERE, "libnetmfp.so")
 OBJ = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+def _nccl_include():
+    """nccl.h for the types only (NCCL itself is dlopen'ed at run time)."""
+    cands = []
+    try:
+        import nvidia.nccl  # torch's bundled NCCL
+        cands.append(os.path.join(list(nvidia.nccl.__path__)[0], "include"))
+    except Exception:
+        pass
+    cands.append("/usr/include")
+    for c in cands:
+        if os.path.exists(os.path.join(c, "nccl.h")):
+            return c
+    raise RuntimeError("nccl.h not found")
+
+
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["api.cu", "build_csr.cu", "spmm.cu", "dense.cu", "small.cu", "sketch.cu", "pipeline.cu", "tc_gemm.cu", "sketch_tc.cu", "chol_df.cu"]
+         "-I" + os.path.join(ROOT, "include"), "-I" + _nccl_include()]
+SOURCES = ["api.cu", "build_csr.cu", "spmm.cu", "dense.cu", "small.cu", "sketch.cu", "pipeline.cu", "tc_gemm.cu", "sketch_tc.cu", "chol_df.cu", "dist.cu"]
 
 
 def _deps():
@@ -55,7 +70,7 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
         for _, err in res:
             sys.stderr.write(err)
     objs = [o for o, _ in res]
-    cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stderr)

@@ -149,6 +149,10 @@ int netmfp_ctx_destroy(netmfp_ctx *ctx) {
     if (!ctx) return;
     cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.d_flags) cudaFree(ctx->c.d_flags);
+    try {
+      dist_destroy(ctx->c);
+    } catch (...) {
+    }
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
     delete ctx;
   });
@@ -190,6 +194,67 @@ int netmfp_build_csr(netmfp_ctx *ctx, int64_t n, const int32_t *src, const int32
     Graph *g = build_csr_device(c, n, s.p, t.p, m_in);
     finish(c);
     *out = new netmfp_graph{g};
+  });
+}
+
+int netmfp_dist_unique_id(void *id) {
+  return guarded([&] {
+    NM_REQUIRE(id, "dist_unique_id: NULL");
+    dist_unique_id(id);
+  });
+}
+
+int netmfp_dist_init(netmfp_ctx *ctx, const void *id, int32_t nranks, int32_t rank) {
+  return guarded([&] {
+    NM_REQUIRE(ctx && (id || nranks == 1), "dist_init: NULL argument");
+    dist_init(ctx->c, id, nranks, rank);
+  });
+}
+
+int netmfp_dist_build_csr(netmfp_ctx *ctx, int64_t n, const int32_t *src, const int32_t *dst, int64_t m_in,
+                          const int64_t *bounds, int mem, netmfp_graph **out) {
+  return guarded([&] {
+    NM_REQUIRE(ctx && out, "dist_build_csr: NULL ctx/out");
+    check_mem(mem);
+    NM_REQUIRE(m_in == 0 || (src && dst), "dist_build_csr: NULL edge arrays");
+    Ctx &c = ctx->c;
+    std::vector<int64_t> b(c.nranks + 1);
+    for (int r = 0; r <= c.nranks; ++r) b[r] = bounds ? bounds[r] : n * r / c.nranks;
+    NM_REQUIRE(b[0] == 0 && b[c.nranks] == n, "dist_build_csr: bounds must start at 0 and end at n");
+    for (int r = 0; r < c.nranks; ++r) NM_REQUIRE(b[r] <= b[r + 1], "dist_build_csr: bounds must be non-decreasing");
+    InVec<int32_t> s(c, src, m_in, mem, true), t(c, dst, m_in, mem, true);
+    std::unique_ptr<Graph> g(build_csr_device(c, n, s.p, t.p, m_in, b[c.rank], b[c.rank + 1]));
+    g->bounds = b;
+    // vol(G) = Σ_ranks local nnz
+    DBuf<int64_t> v(1, c.stream);
+    NM_CUDA(cudaMemcpyAsync(v.p, &g->nnz, 8, cudaMemcpyHostToDevice, c.stream));
+    dist_allreduce(c, v.p, 1, DType::I64);
+    NM_CUDA(cudaMemcpyAsync(&g->nnz_global, v.p, 8, cudaMemcpyDeviceToHost, c.stream));
+    finish(c);
+    *out = new netmfp_graph{g.release()};
+  });
+}
+
+int netmfp_build_csr_rows(netmfp_ctx *ctx, int64_t n, const int32_t *src, const int32_t *dst, int64_t m_in,
+                          int64_t row0, int64_t row1, int mem, netmfp_graph **out) {
+  return guarded([&] {
+    NM_REQUIRE(ctx && out, "build_csr_rows: NULL ctx/out");
+    check_mem(mem);
+    NM_REQUIRE(m_in == 0 || (src && dst), "build_csr_rows: NULL edge arrays");
+    Ctx &c = ctx->c;
+    InVec<int32_t> s(c, src, m_in, mem, true), t(c, dst, m_in, mem, true);
+    Graph *g = build_csr_device(c, n, s.p, t.p, m_in, row0, row1);
+    finish(c);
+    *out = new netmfp_graph{g};
+  });
+}
+
+int netmfp_graph_rows(const netmfp_graph *g, int64_t *row0, int64_t *n_global, int64_t *nnz_global) {
+  return guarded([&] {
+    NM_REQUIRE(g, "graph_rows: NULL graph");
+    if (row0) *row0 = g->g->row0;
+    if (n_global) *n_global = g->g->n_global;
+    if (nnz_global) *nnz_global = g->g->nnz_global;
   });
 }
 
@@ -255,7 +320,9 @@ int netmfp_spmm(netmfp_ctx *ctx, const netmfp_graph *gr, double a, double b, con
     check_mem(mem);
     Ctx &c = ctx->c;
     const Graph &g = *gr->g;
-    InMat xi(c, X, g.n, cols, ldx, mem, true), yo(c, Y, g.n, cols, ldy, mem, false);
+    // X: all n_global rows (the columns of A); Y: this graph's rows
+    InMat xi(c, X, g.n_global, cols, ldx, mem, true), yo(c, Y, g.n, cols, ldy, mem, false);
+    NM_REQUIRE(b == 0.0 || g.n == g.n_global, "spmm: column scaling (b != 0) needs the unpartitioned graph");
     DBuf<float> scol;
     SpmmArgs p;
     p.X = xi.m.p; p.ldx = xi.m.ld; p.Y = yo.m.p; p.ldy = yo.m.ld; p.cols = cols; p.a = (float)a;
@@ -426,11 +493,11 @@ static void embed_impl(Ctx &c, const Graph &g, const netmfp_params &p, const Mat
     factor_pair(c, g, p.alpha, p.T, U.m, lam, p.k, F.m, C);            // steps 2-3
   }
   U.buf.release();
-  const double scale = (double)g.nnz / (p.b * p.T);                  // vol(G)/(bT)
+  const double scale = (double)g.nnz_global / (p.b * p.T);           // vol(G)/(bT)
   {
     NM_STAGE(c, "stage_sketch_svd");
     sketch_svd(c, F.m, C, p.k, scale, p.d, p.s2, p.s3, p.z, p.seed, p.logmode, nullptr, sigma_dev, &E,
-               nullptr, nullptr);                                      // steps 4-5
+               nullptr, nullptr, g.row0, g.n_global);                  // steps 4-5
   }
   F.buf.release();
   {

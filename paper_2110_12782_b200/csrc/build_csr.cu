@@ -10,7 +10,8 @@
 namespace netmfp {
 
 __global__ void k_make_keys(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
-                            int64_t m, uint64_t n, uint64_t *__restrict__ keys, int *bad) {
+                            int64_t m, uint64_t n, uint64_t row0, uint64_t row1, uint64_t *__restrict__ keys,
+                            int *bad) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= m) return;
   int32_t s = src[e], t = dst[e];
@@ -22,17 +23,18 @@ __global__ void k_make_keys(const int32_t *__restrict__ src, const int32_t *__re
   if (s == t) {  // self loop: dropped (sentinel row n sorts last)
     keys[2 * e] = keys[2 * e + 1] = n << 32;
   } else {
-    keys[2 * e] = ((uint64_t)s << 32) | (uint32_t)t;
-    keys[2 * e + 1] = ((uint64_t)t << 32) | (uint32_t)s;
+    // rows outside this rank's range [row0, row1) become the sentinel
+    keys[2 * e] = ((uint64_t)s >= row0 && (uint64_t)s < row1) ? (((uint64_t)s << 32) | (uint32_t)t) : (n << 32);
+    keys[2 * e + 1] = ((uint64_t)t >= row0 && (uint64_t)t < row1) ? (((uint64_t)t << 32) | (uint32_t)s) : (n << 32);
   }
 }
 
-// rowptr[u] = first key index with row >= u (lower bound), u in [0, n]
-__global__ void k_rowptr(const uint64_t *__restrict__ keys, int64_t nnz, int64_t n,
+// rowptr[u] = first key index with row >= row0 + u (lower bound), u in [0, n]
+__global__ void k_rowptr(const uint64_t *__restrict__ keys, int64_t nnz, int64_t n, int64_t row0,
                          int64_t *__restrict__ rowptr) {
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u > n) return;
-  uint64_t target = (uint64_t)u << 32;
+  uint64_t target = (uint64_t)(u + row0) << 32;
   int64_t lo = 0, hi = nnz;
   while (lo < hi) {
     int64_t mid = (lo + hi) >> 1;
@@ -78,12 +80,19 @@ static int bits_for(uint64_t v) {
   return b;
 }
 
-Graph *build_csr_device(Ctx &c, int64_t n, const int32_t *src, const int32_t *dst, int64_t m) {
-  NM_REQUIRE(n > 0 && n < (1ll << 31), "build_csr: need 0 < n < 2^31");
+Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t *dst, int64_t m, int64_t row0,
+                        int64_t row1) {
+  NM_REQUIRE(n_all > 0 && n_all < (1ll << 31), "build_csr: need 0 < n < 2^31");
   NM_REQUIRE(m >= 0, "build_csr: m_in < 0");
+  if (row1 < 0) row1 = n_all;
+  NM_REQUIRE(row0 >= 0 && row0 <= row1 && row1 <= n_all, "build_csr: bad row range");
   cudaStream_t s = c.stream;
   auto g = new Graph();
+  const int64_t n = row1 - row0;  // local rows
   g->n = n;
+  g->n_global = n_all;
+  g->row0 = row0;
+  g->bounds = {0, n_all};
   g->device = c.device;
   try {
     int64_t nk = 2 * m;
@@ -91,9 +100,10 @@ Graph *build_csr_device(Ctx &c, int64_t n, const int32_t *src, const int32_t *ds
     DBuf<int> bad(1, s);
     bad.zero();
     if (m > 0) {
-      NM_LAUNCH(c, "make_keys", k_make_keys<<<ceil_div(m, 256), 256, 0, s>>>(src, dst, m, (uint64_t)n, keys, bad));
+      NM_LAUNCH(c, "make_keys", k_make_keys<<<ceil_div(m, 256), 256, 0, s>>>(src, dst, m, (uint64_t)n_all, (uint64_t)row0,
+                                                                             (uint64_t)row1, keys, bad));
     }
-    int end_bit = 32 + bits_for((uint64_t)n);
+    int end_bit = 32 + bits_for((uint64_t)n_all);
     size_t tmp_bytes = 0, tmp2 = 0;
     DBuf<int64_t> nsel(1, s);
     if (nk > 0) {
@@ -119,14 +129,15 @@ Graph *build_csr_device(Ctx &c, int64_t n, const int32_t *src, const int32_t *ds
       uint64_t last = 0;
       NM_CUDA(cudaMemcpyAsync(&last, keys.p + nnz - 1, 8, cudaMemcpyDeviceToHost, s));
       NM_CUDA(cudaStreamSynchronize(s));
-      if ((last >> 32) == (uint64_t)n) --nnz;
+      if ((last >> 32) == (uint64_t)n_all) --nnz;
     }
     g->nnz = nnz;
+    g->nnz_global = nnz;
     g->rowptr.alloc(n + 1, s);
     g->col.alloc(nnz > 0 ? nnz : 1, s);
     g->deg.alloc(n, s);
     DBuf<uint8_t> hflag(n, s);
-    NM_LAUNCH(c, "rowptr", k_rowptr<<<ceil_div(n + 1, 256), 256, 0, s>>>(keys, nnz, n, g->rowptr));
+    NM_LAUNCH(c, "rowptr", k_rowptr<<<ceil_div(n + 1, 256), 256, 0, s>>>(keys, nnz, n, row0, g->rowptr));
     int64_t mx = std::max(nnz, n);
     NM_LAUNCH(c, "col_deg", k_col_deg<<<ceil_div(mx, 256), 256, 0, s>>>(keys, nnz, g->rowptr, n, g->col, g->deg, hflag));
     // heavy rows (degree > kLightCap) for the split SpMM path

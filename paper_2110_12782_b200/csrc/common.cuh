@@ -62,6 +62,10 @@ struct Ctx {
   cudaEvent_t cur_a = nullptr;
   const char *cur_name = nullptr;
   std::vector<std::pair<std::string, std::pair<int64_t, double>>> stats;
+  // row-partitioned multi-GPU (dist.cu); nranks == 1: single GPU
+  int nranks = 1, rank = 0;
+  void *comm = nullptr;  // ncclComm_t
+  int64_t collectives = 0;
 };
 
 inline bool prof_match(const Ctx &c, const char *name) {
@@ -231,7 +235,10 @@ struct Block {
 // graph (device CSR)
 // ----------------------------------------------------------------------------
 struct Graph {
-  int64_t n = 0, nnz = 0;
+  int64_t n = 0, nnz = 0;  // local rows [row0, row0 + n) and their nonzeros
+  int64_t n_global = 0, row0 = 0;
+  int64_t nnz_global = 0;            // vol(G)
+  std::vector<int64_t> bounds;       // row bounds of every rank (nranks + 1), host
   DBuf<int64_t> rowptr;   // n+1
   DBuf<int32_t> col;      // nnz
   DBuf<int32_t> deg;      // n

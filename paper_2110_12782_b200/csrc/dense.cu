@@ -239,11 +239,12 @@ void gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, const 
 // Ω = randn(n, l) (Alg. 2 step 2) with Philox4x32-10 [R1], optional row scale
 // ---------------------------------------------------------------------------
 __global__ void k_gaussian(Mat O, uint32_t k0, uint32_t k1, const int32_t *__restrict__ deg,
-                           float rexp) {
+                           float rexp, int64_t row0) {
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= O.rows * O.cols) return;
   int64_t i = idx / O.cols, j = idx % O.cols;
-  U4 ctr{(uint32_t)j, (uint32_t)(i & 0xFFFFFFFF), (uint32_t)((uint64_t)i >> 32), kTagOmega};
+  const int64_t gi = i + row0;  // global row: every rank draws its own rows of the same Ω
+  U4 ctr{(uint32_t)j, (uint32_t)(gi & 0xFFFFFFFF), (uint32_t)((uint64_t)gi >> 32), kTagOmega};
   U4 w = philox4x32_10(ctr, k0, k1);
   // Box–Muller in fp32 (the block is fp32; |error| ~1e-7 relative to the fp64 oracle)
   const float u0 = ((float)w.x + 0.5f) * 2.3283064365386963e-10f;  // 2^-32
@@ -252,9 +253,10 @@ __global__ void k_gaussian(Mat O, uint32_t k0, uint32_t k1, const int32_t *__res
   O.p[i * O.ld + j] = g * dpow_scale(deg, i, rexp);
 }
 
-void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, float rexp) {
+void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, float rexp, int64_t row0) {
+  if (O.rows * O.cols == 0) return;
   NM_LAUNCH(c, "gaussian", k_gaussian<<<ceil_div(O.rows * O.cols, 256), 256, 0, c.stream>>>(
-      O, (uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32), deg, rexp));
+      O, (uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32), deg, rexp, row0));
 }
 
 __global__ void k_row_scale(Mat Y, const int32_t *__restrict__ deg, float rexp) {

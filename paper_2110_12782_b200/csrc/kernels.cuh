@@ -5,7 +5,19 @@
 namespace netmfp {
 
 // ---- build_csr.cu
-Graph *build_csr_device(Ctx &c, int64_t n, const int32_t *src, const int32_t *dst, int64_t m);
+// CSR of rows [row0, row1) (default: all rows) with global column ids; the
+// edge list must contain every edge incident to those rows.
+Graph *build_csr_device(Ctx &c, int64_t n, const int32_t *src, const int32_t *dst, int64_t m, int64_t row0 = 0,
+                        int64_t row1 = -1);
+
+// ---- dist.cu
+enum class DType { F32, F64, I64 };
+void dist_unique_id(void *out);
+void dist_init(Ctx &c, const void *id, int nranks, int rank);
+void dist_destroy(Ctx &c);
+void dist_allreduce(Ctx &c, void *buf, size_t count, DType t);  // in place, sum
+// full n_global × local.ld block gathered from every rank's rows (identity for one rank)
+const float *dist_gather_rows(Ctx &c, const Graph &g, const Mat &local, DBuf<float> &scratch);
 
 // ---- spmm.cu
 struct SpmmArgs {
@@ -50,7 +62,7 @@ void gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, const 
                    const Mat &C);
 bool tc_enabled();
 // Ω = randn(n, l) from Philox [R1], row-scaled by d_i^-e (deg != null)
-void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, float rexp);
+void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, float rexp, int64_t row0 = 0);
 // Dst[i, :] = d_i^-e Src[i, :]
 void scale_copy_block(Ctx &c, const Mat &Src, const Mat &Dst, const int32_t *deg, float rexp);
 // Y[i, :] *= d_i^-e
@@ -93,13 +105,16 @@ struct SparseSign {
 };
 void gen_sparse_sign(Ctx &c, int64_t n, int64_t h, int64_t z, uint64_t seed, uint32_t tag, SparseSign &S);
 // Y[n×h] = f(scale · A F(rows)ᵀ) Ψ  (Eq. 5 sketch; A = F·C), tensor cores
+// (F holds this rank's rows [row0, row0 + F.rows); the gathered rows are
+// summed over ranks)
 void tc_sketch_y(Ctx &c, const Mat &A, const Mat &F, const int32_t *rows, const float *signs, int64_t h, int z,
-                 float scale, int logmode, const Mat &Y);
+                 float scale, int logmode, const Mat &Y, int64_t row0 = 0);
 // Zf[h×h] (fp32, ldz) = Πᵀ f(scale · FC F ᵀ restricted to Π's rows) Π  (Alg. 4 step 6)
 void tc_sketch_z(Ctx &c, const Mat &FC, const Mat &F, const int32_t *rows, const float *signs, int64_t h, int z,
-                 float scale, int logmode, float *Zf, int64_t ldz);
+                 float scale, int logmode, float *Zf, int64_t ldz, int64_t row0 = 0);
 // Out[h×cols] (fp64) = Ψᵀ X  (sign-gather of rows of X; X fp32 n×cols)
-void sign_gather_T(Ctx &c, const SparseSign &S, const Mat &X, double *Out, int64_t ldo);
+// (X holds rows [row0, row0 + X.rows); rows elsewhere contribute 0)
+void sign_gather_T(Ctx &c, const SparseSign &S, const Mat &X, double *Out, int64_t ldo, int64_t row0 = 0);
 // fp32 -> fp64 copy of an r×c matrix
 void f32_to_f64(Ctx &c, const float *src, int64_t lds, double *dst, int64_t ldd, int64_t rows, int64_t cols);
 

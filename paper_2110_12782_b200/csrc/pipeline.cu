@@ -30,6 +30,7 @@ void cholqr(Ctx &c, const Mat &Y, const Mat &out, const int32_t *deg, float rexp
   Mat cur = Y;
   for (int ps = 0; ps < passes; ++ps) {
     gram(c, cur, cur, nullptr, 0.f, G, l);
+    dist_allreduce(c, G, (size_t)l * l, DType::F64);  // Gram over all ranks' rows
     chol_inv_upper(c, G, l, l, Rinv, c.d_flags);
     const bool last = (ps + 1 == passes);
     if (last) {
@@ -49,16 +50,17 @@ void freigs(Ctx &c, const Graph &g, double alpha, int k, int s1, int q, uint64_t
             double *lam_dev) {
   const int64_t n = g.n, l = (int64_t)k + s1;
   NM_REQUIRE(k >= 1 && s1 >= 0 && q >= 0, "eig: need k >= 1, s1 >= 0, q >= 0");
-  NM_REQUIRE(l <= n, "eig: k + s1 must not exceed n (Alg. 2)");
+  NM_REQUIRE(l <= g.n_global, "eig: k + s1 must not exceed n (Alg. 2)");
   NM_REQUIRE(alpha > 0.0 && alpha <= 0.5, "eig: alpha in (0, 0.5] (PAPER.md:217)");
   cudaStream_t s = c.stream;
   const float a = (float)alpha;
   Block P(n, l, s), T(n, l, s), Y(n, l, s);
+  DBuf<float> xfull;  // all ranks' rows of the SpMM input (multi-GPU only)
   // step 2: Ω = randn(n, l), Y = X Ω
-  gaussian_block(c, P.m, seed, g.deg, a);  // P = D^-α Ω
+  gaussian_block(c, P.m, seed, g.deg, a, g.row0);  // P = D^-α Ω (this rank's rows)
   SpmmArgs sp;
   sp.cols = l;
-  sp.X = P.m.p; sp.ldx = P.m.ld; sp.Y = Y.m.p; sp.ldy = Y.m.ld; sp.a = a;
+  sp.X = dist_gather_rows(c, g, P.m, xfull); sp.ldx = P.m.ld; sp.Y = Y.m.p; sp.ldy = Y.m.ld; sp.a = a;
   spmm(c, g, sp);
   // step 3: Q = orth(Y)
   cholqr(c, Y.m, P.m, g.deg, a, q == 0 ? 2 : 1, &T.m);
@@ -66,11 +68,11 @@ void freigs(Ctx &c, const Graph &g, double alpha, int k, int s1, int q, uint64_t
   for (int it = 0; it < q; ++it) {
     SpmmArgs s1a;
     s1a.cols = l;
-    s1a.X = P.m.p; s1a.ldx = P.m.ld; s1a.Y = T.m.p; s1a.ldy = T.m.ld; s1a.a = 2.f * a;
+    s1a.X = dist_gather_rows(c, g, P.m, xfull); s1a.ldx = P.m.ld; s1a.Y = T.m.p; s1a.ldy = T.m.ld; s1a.a = 2.f * a;
     spmm(c, g, s1a);  // T = D^-2α A P = D^-α (X Q)
     SpmmArgs s2a;
     s2a.cols = l;
-    s2a.X = T.m.p; s2a.ldx = T.m.ld; s2a.Y = Y.m.p; s2a.ldy = Y.m.ld; s2a.a = a;
+    s2a.X = dist_gather_rows(c, g, T.m, xfull); s2a.ldx = T.m.ld; s2a.Y = Y.m.p; s2a.ldy = Y.m.ld; s2a.a = a;
     spmm(c, g, s2a);  // Y = D^-α A T = X X Q
     cholqr(c, Y.m, P.m, g.deg, a, it + 1 == q ? 2 : 1, &T.m);
   }
@@ -78,10 +80,12 @@ void freigs(Ctx &c, const Graph &g, double alpha, int k, int s1, int q, uint64_t
   // step 7: S = Qᵀ X Q = Pᵀ A P
   SpmmArgs s3;
   s3.cols = l;
-  s3.X = P.m.p; s3.ldx = P.m.ld; s3.Y = T.m.p; s3.ldy = T.m.ld; s3.a = 0.f;
+  s3.X = dist_gather_rows(c, g, P.m, xfull); s3.ldx = P.m.ld; s3.Y = T.m.p; s3.ldy = T.m.ld; s3.a = 0.f;
   spmm(c, g, s3);
+  xfull.release();
   DBuf<double> S((size_t)l * l, s), lam(l, s), V((size_t)l * l, s);
   gram(c, P.m, T.m, nullptr, 0.f, S, l);
+  dist_allreduce(c, S, (size_t)l * l, DType::F64);
   symmetrize64(c, S, l, l);
   // step 8: [Û, Λ] = eig(S), ordered by |λ| [R3]
   {
@@ -101,6 +105,7 @@ void factor_pair(Ctx &c, const Graph &g, double alpha, int T, const Mat &U, cons
   DBuf<double> K((size_t)k * k, s), Pw((size_t)k * k, s), Pn((size_t)k * k, s), acc((size_t)k * k, s);
   // K = Uᵀ D^(-1+2α) U Λ
   gram(c, U, U, g.deg, (float)(1.0 - 2.0 * alpha), K, k);
+  dist_allreduce(c, K, (size_t)k * k, DType::F64);
   scale_cols64(c, K, k, k, k, lam, 0);
   // Σ_{r=1}^T K^(r-1)
   set_identity64(c, acc, k, k);
@@ -129,11 +134,12 @@ __global__ void k_abs(const double *lam, int d, double *out) {
 // Alg. 4
 void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int d, int s2, int s3, int z,
                 uint64_t seed, int logmode, const Mat *Uout, double *sigma_dev, const Mat *Eout,
-                const Mat *Yout, double *Zout) {
-  const int64_t n = F.rows;
+                const Mat *Yout, double *Zout, int64_t row0, int64_t n_global) {
+  const int64_t n = F.rows;  // this rank's rows [row0, row0 + n) of n_global
+  if (n_global < 0) n_global = n;
   const int64_t h2 = (int64_t)d + s2, h3 = (int64_t)d + s3;
   NM_REQUIRE(d >= 1 && s2 >= 0 && s3 >= 0, "sketch_svd: need d >= 1, s2, s3 >= 0");
-  NM_REQUIRE(h2 <= n && h3 <= n * (int64_t)z, "sketch_svd: d + s2 must not exceed n");
+  NM_REQUIRE(h2 <= n_global && h3 <= n_global * (int64_t)z, "sketch_svd: d + s2 must not exceed n");
   NM_REQUIRE(h3 >= h2, "sketch_svd: need s3 >= s2 (PAPER.md:413)");
   cudaStream_t s = c.stream;
   const float fs = (float)scale;
@@ -141,7 +147,7 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
   SparseSign Psi;
   {
     NM_STAGE(c, "stage_gen_sparse_sign");
-    gen_sparse_sign(c, n, h2, z, seed, kTagPsi, Psi);
+    gen_sparse_sign(c, n_global, h2, z, seed, kTagPsi, Psi);
   }
   // FC = F · C
   Block FC(n, k, s);
@@ -150,7 +156,7 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
   Block Y(n, h2, s), Qb(n, h2, s), Tb(n, h2, s);
   {
     NM_STAGE(c, "stage_sketch_y");
-    tc_sketch_y(c, FC.m, F, Psi.rows, Psi.signs, h2, z, fs, logmode, Y.m);
+    tc_sketch_y(c, FC.m, F, Psi.rows, Psi.signs, h2, z, fs, logmode, Y.m, row0);
   }
   if (Yout) copy_block(c, Y.m.p, Y.m.ld, Yout->p, Yout->ld, n, h2);
   // step 4: Q = orth(Y)   (CholeskyQR2 [R7])
@@ -160,19 +166,20 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
   SparseSign Pi;
   {
     NM_STAGE(c, "stage_gen_sparse_sign");
-    gen_sparse_sign(c, n, h3, z, seed, kTagPi, Pi);
+    gen_sparse_sign(c, n_global, h3, z, seed, kTagPi, Pi);
   }
   // step 6: Z = Πᵀ f(scale F(p,:) C F(p,:)ᵀ) Π  (both sides restricted to Π's coordinates)
   NM_STAGE(c, "stage_sketch_z_core");
   DBuf<double> Z((size_t)h3 * h3, s), PtQ((size_t)h3 * h2, s);
   {
     DBuf<float> Zf((size_t)h3 * h3, s);
-    tc_sketch_z(c, FC.m, F, Pi.rows, Pi.signs, h3, z, fs, logmode, Zf, h3);
+    tc_sketch_z(c, FC.m, F, Pi.rows, Pi.signs, h3, z, fs, logmode, Zf, h3, row0);
     f32_to_f64(c, Zf, h3, Z, h3, h3, h3);
   }
   if (Zout) NM_CUDA(cudaMemcpyAsync(Zout, Z.p, (size_t)h3 * h3 * 8, cudaMemcpyDeviceToDevice, s));
   // step 7: S = (ΠᵀQ)† Z (QᵀΠ)†  via the normal equations in fp64
-  sign_gather_T(c, Pi, Qb.m, PtQ, h2);
+  sign_gather_T(c, Pi, Qb.m, PtQ, h2, row0);
+  dist_allreduce(c, PtQ, (size_t)h3 * h2, DType::F64);
   DBuf<double> N((size_t)h2 * h2, s), Ninv((size_t)h2 * h2, s), Rinv((size_t)h2 * h2, s);
   DBuf<double> W((size_t)h2 * h3, s), WZ((size_t)h2 * h3, s), S((size_t)h2 * h2, s);
   gemm64(c, true, false, h2, h2, h3, 1.0, PtQ, h2, PtQ, h2, 0.0, N, h2);  // N = AᵀA
@@ -233,10 +240,11 @@ void propagate(Ctx &c, const Graph &g, const Mat &E, int order, double mu, doubl
   cudaStream_t s = c.stream;
   const int64_t n = E.rows, d = E.cols;
   Block Z1(n, d, s), Acc(n, d, s);
+  DBuf<float> xfull;  // all ranks' rows of the SpMM input (multi-GPU only)
   // Z_1 = L~ E = -D^-1 A E ;  Acc = c0 E + c1 Z_1
   SpmmArgs a;
   a.cols = d;
-  a.X = E.p; a.ldx = E.ld; a.Y = Z1.m.p; a.ldy = Z1.m.ld; a.a = 1.f; a.coef = -1.f;
+  a.X = dist_gather_rows(c, g, E, xfull); a.ldx = E.ld; a.Y = Z1.m.p; a.ldy = Z1.m.ld; a.a = 1.f; a.coef = -1.f;
   a.acc_in = E.p; a.ldai = E.ld; a.acc_out = Acc.m.p; a.ldacc = Acc.m.ld;
   a.acc_scale = (float)cf[0]; a.gamma = (float)cf[1];
   spmm(c, g, a);
@@ -245,7 +253,7 @@ void propagate(Ctx &c, const Graph &g, const Mat &E, int order, double mu, doubl
   for (int r = 2; r <= order; ++r) {
     SpmmArgs b;
     b.cols = d;
-    b.X = zcur.p; b.ldx = zcur.ld;
+    b.X = dist_gather_rows(c, g, zcur, xfull); b.ldx = zcur.ld;
     b.Y = zprev.p; b.ldy = zprev.ld;
     b.prev = zprev.p; b.ldp = zprev.ld; b.beta = -1.f;
     b.a = 1.f; b.coef = -2.f;

@@ -47,18 +47,21 @@ void gen_sparse_sign(Ctx &c, int64_t n, int64_t h, int64_t z, uint64_t seed, uin
 
 // Out[j, :] = Σ_t sign[j,t] X[rows[j,t], :]  (fp64 accumulate)
 __global__ void k_sign_gather(const int32_t *__restrict__ rows, const float *__restrict__ signs, int64_t h, int z,
-                              Mat X, double *__restrict__ Out, int64_t ldo) {
+                              Mat X, int64_t row0, double *__restrict__ Out, int64_t ldo) {
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= h * X.cols) return;
   int64_t j = idx / X.cols, cc = idx % X.cols;
   double s = 0.0;
-  for (int t = 0; t < z; ++t) s += (double)signs[j * z + t] * (double)X.p[(int64_t)rows[j * z + t] * X.ld + cc];
+  for (int t = 0; t < z; ++t) {
+    const int64_t r = (int64_t)rows[j * z + t] - row0;
+    if (r >= 0 && r < X.rows) s += (double)signs[j * z + t] * (double)X.p[r * X.ld + cc];
+  }
   Out[j * ldo + cc] = s;
 }
 
-void sign_gather_T(Ctx &c, const SparseSign &S, const Mat &X, double *Out, int64_t ldo) {
-  NM_LAUNCH(c, "sign_gather", k_sign_gather<<<ceil_div(S.h * X.cols, 256), 256, 0, c.stream>>>(S.rows, S.signs, S.h,
-                                                                                                 (int)S.z, X, Out, ldo));
+void sign_gather_T(Ctx &c, const SparseSign &S, const Mat &X, double *Out, int64_t ldo, int64_t row0) {
+  NM_LAUNCH(c, "sign_gather", k_sign_gather<<<ceil_div(S.h * X.cols, 256), 256, 0, c.stream>>>(
+                                  S.rows, S.signs, S.h, (int)S.z, X, row0, Out, ldo));
 }
 
 __global__ void k_f32_to_f64(const float *__restrict__ src, int64_t lds, double *__restrict__ dst, int64_t ldd,

@@ -325,9 +325,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant_
 // rows of X at the sparse-sign coordinates, one zp-group per column c:
 // out row c·zp + t = X[rows[c·z + t]] for t < z, zero for the padding (sign 0);
 // optional tf32 lo part and the sign vector
-__global__ void k_gather_groups(const float *__restrict__ X, int64_t ldx, const int32_t *__restrict__ rows,
-                                const float *__restrict__ signs, int64_t h, int z, int zp, int k, int64_t ldb,
-                                float *__restrict__ hi, float *__restrict__ lo, float *__restrict__ sgn) {
+__global__ void k_gather_groups(const float *__restrict__ X, int64_t ldx, int64_t row0, int64_t nloc,
+                                const int32_t *__restrict__ rows, const float *__restrict__ signs, int64_t h, int z,
+                                int zp, int k, int64_t ldb, float *__restrict__ hi, float *__restrict__ lo,
+                                float *__restrict__ sgn) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nr = h * zp;
   if (idx >= nr * ldb) return;
@@ -335,7 +336,10 @@ __global__ void k_gather_groups(const float *__restrict__ X, int64_t ldx, const 
   const int64_t c = j / zp;
   const int t = (int)(j % zp);
   float x = 0.f;
-  if (t < z && kk < k) x = X[(int64_t)rows[c * z + t] * ldx + kk];
+  if (t < z && kk < k) {
+    const int64_t r = (int64_t)rows[c * z + t] - row0;  // rows of other ranks contribute 0
+    if (r >= 0 && r < nloc) x = X[r * ldx + kk];
+  }
   hi[idx] = x;
   if (lo) lo[idx] = x - tc::tf32_trunc(x);
   if (kk == 0) sgn[j] = t < z ? signs[c * z + t] : 0.f;
@@ -403,7 +407,7 @@ static void launch_sketch(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mh, 
 
 // Y[n × h] = f(scale · A F(rows)ᵀ) Ψ  (Y mode; A = F·C, Ψ = (rows, signs) with z per column)
 void tc_sketch_y(Ctx &c, const Mat &A, const Mat &F, const int32_t *rows, const float *signs, int64_t h, int z,
-                 float scale, int logmode, const Mat &Y) {
+                 float scale, int logmode, const Mat &Y, int64_t row0) {
   using namespace tcs;
   NM_REQUIRE(A.cols == F.cols && Y.rows == A.rows && Y.cols == h, "tc_sketch_y: shapes");
   NM_REQUIRE(z >= 2 && z <= 64, "tc_sketch_y: 2 <= z <= 64");
@@ -416,7 +420,10 @@ void tc_sketch_y(Ctx &c, const Mat &A, const Mat &F, const int32_t *rows, const 
   DBuf<float> bh((size_t)ncols * ldb, c.stream), bl((size_t)ncols * ldb, c.stream), sg(pad4(ncols) + NW, c.stream);
   NM_CUDA(cudaMemsetAsync(sg.p, 0, sg.n * 4, c.stream));
   NM_LAUNCH(c, "gather_groups", k_gather_groups<<<ceil_div(ncols * ldb, 256), 256, 0, c.stream>>>(
-                                    F.p, F.ld, rows, signs, h, z, zp, k, ldb, bh.p, bl.p, sg.p));
+                                    F.p, F.ld, row0, F.rows, rows, signs, h, z, zp, k, ldb, bh.p, bl.p, sg.p));
+  // each gathered row lives on exactly one rank: the sum over ranks is exact
+  dist_allreduce(c, bh.p, (size_t)ncols * ldb, DType::F32);
+  dist_allreduce(c, bl.p, (size_t)ncols * ldb, DType::F32);
   CUtensorMap ma = make_map(A.p, n, k, A.ld, 128, SW128, BK);
   CUtensorMap mh = make_map(bh.p, ncols, k, ldb, NW, SW128, BK);
   CUtensorMap ml = make_map(bl.p, ncols, k, ldb, NW, SW128, BK);
@@ -440,7 +447,7 @@ void tc_sketch_y(Ctx &c, const Mat &A, const Mat &F, const int32_t *rows, const 
 
 // Z[h × h] = Πᵀ f(scale · FC(rows) F(rows)ᵀ) Π  (Z mode), fp32 output with ldz
 void tc_sketch_z(Ctx &c, const Mat &FC, const Mat &F, const int32_t *rows, const float *signs, int64_t h, int z,
-                 float scale, int logmode, float *Zf, int64_t ldz) {
+                 float scale, int logmode, float *Zf, int64_t ldz, int64_t row0) {
   using namespace tcs;
   NM_REQUIRE(FC.cols == F.cols, "tc_sketch_z: shapes");
   NM_REQUIRE(z >= 2 && z <= 64, "tc_sketch_z: 2 <= z <= 64");
@@ -453,9 +460,12 @@ void tc_sketch_z(Ctx &c, const Mat &FC, const Mat &F, const int32_t *rows, const
   NM_CUDA(cudaMemsetAsync(sg.p, 0, sg.n * 4, c.stream));
   NM_CUDA(cudaMemsetAsync(rs.p, 0, rs.n * 4, c.stream));
   NM_LAUNCH(c, "gather_groups", k_gather_groups<<<ceil_div(nr * ldb, 256), 256, 0, c.stream>>>(
-                                    FC.p, FC.ld, rows, signs, h, z, zp, k, ldb, ah.p, nullptr, rs.p));
+                                    FC.p, FC.ld, row0, FC.rows, rows, signs, h, z, zp, k, ldb, ah.p, nullptr, rs.p));
   NM_LAUNCH(c, "gather_groups", k_gather_groups<<<ceil_div(nr * ldb, 256), 256, 0, c.stream>>>(
-                                    F.p, F.ld, rows, signs, h, z, zp, k, ldb, bh.p, bl.p, sg.p));
+                                    F.p, F.ld, row0, F.rows, rows, signs, h, z, zp, k, ldb, bh.p, bl.p, sg.p));
+  dist_allreduce(c, ah.p, (size_t)nr * ldb, DType::F32);
+  dist_allreduce(c, bh.p, (size_t)nr * ldb, DType::F32);
+  dist_allreduce(c, bl.p, (size_t)nr * ldb, DType::F32);
   if (zp > 32) NM_CUDA(cudaMemset2DAsync(Zf, ldz * 4, 0, h * 4, h, c.stream));
   CUtensorMap ma = make_map(ah.p, nr, k, ldb, 128, SW128, BK);
   CUtensorMap mh = make_map(bh.p, nr, k, ldb, NW, SW128, BK);

@@ -262,3 +262,47 @@ def test_cfg2_full_size_sampled(L, ctx):
     Xh = Xp.cpu().numpy()
     ref = O.spmm_scaled_rows(rp, col, deg, Xh, rows, spec.alpha, spec.alpha)
     assert relf(Y.cpu().numpy()[rows], ref) <= 1e-5
+
+
+# ---------------------------------------------------------------- row partitions
+@pytest.mark.parametrize("name", ["rmat_s13", "star1500", "cfg0"])
+def test_build_csr_rows_is_a_slice(L, ctx, graphs, name):
+    n, s, t, g, (rp, col, deg) = graphs[name]
+    for b0, b1 in [(0, n // 3), (n // 3, n), (n // 2, n // 2 + 17)]:
+        gp = L.netmfp_build_csr_rows(ctx, n, dev(s), dev(t), b0, b1)
+        prp, pcol, pdeg = gp.export(ctx)
+        assert np.array_equal(prp, rp[b0:b1 + 1] - rp[b0])
+        assert np.array_equal(pcol, col[rp[b0]:rp[b1]])
+        assert np.array_equal(pdeg, deg[b0:b1])
+        assert L.netmfp_graph_rows(gp)[:2] == (b0, n)
+
+
+@pytest.mark.parametrize("cols", [3, 128, 286])
+def test_partition_spmm_rows(L, ctx, graphs, cols):
+    n, s, t, g, (rp, col, deg) = graphs["rmat_s13"]
+    X = np.random.default_rng(cols).standard_normal((n, cols)).astype(np.float32)
+    Xd = padded(n, cols)
+    Xd.copy_(dev(X))
+    ref = O.spmm_scaled(rp, col, deg, X.astype(np.float64), 0.45, 0.0)
+    bounds = L.netmfp_partition_rows(rp, 3)
+    for r in range(3):
+        b0, b1 = int(bounds[r]), int(bounds[r + 1])
+        gp = L.netmfp_build_csr_rows(ctx, n, dev(s), dev(t), b0, b1)
+        Yd = padded(b1 - b0, cols)
+        L.netmfp_spmm(ctx, gp, 0.45, 0.0, Xd, Yd)       # full X in, this partition's rows out
+        assert relf(Yd.cpu().numpy(), ref[b0:b1]) <= 1e-5
+
+
+def test_dist_one_rank_is_the_single_gpu_path(L, ctx, graphs):
+    n, s, t, g, _ = graphs["er600"]
+    c1 = L.Context(0)
+    L.netmfp_dist_init(c1, b"\0" * L.DIST_ID_BYTES, 1, 0)
+    gd = L.netmfp_dist_build_csr(c1, n, dev(s), dev(t))
+    assert L.netmfp_graph_rows(gd) == (0, n, g.nnz)
+    prm = L.make_params(alpha=0.45, k=24, s1=8, q=2, T=10, b=1.0, d=12, s2=12, s3=100, z=8, prop_order=6,
+                        mu=0.2, theta=0.5, seed=3, logmode=0)
+    E1 = padded(n, 12)
+    E2 = padded(n, 12)
+    L.netmfp_embed(ctx, g, prm, E1)
+    L.netmfp_embed(c1, gd, prm, E2)
+    assert torch.equal(E1, E2)
