@@ -5,6 +5,9 @@
 // Deterministic and bit-exact (integer work only).
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace netmfp {
@@ -45,32 +48,32 @@ __global__ void k_rowptr(const uint64_t *__restrict__ keys, int64_t nnz, int64_t
 
 __global__ void k_col_deg(const uint64_t *__restrict__ keys, int64_t nnz,
                           const int64_t *__restrict__ rowptr, int64_t n, int32_t *__restrict__ col,
-                          int32_t *__restrict__ deg, uint8_t *__restrict__ heavy_flag) {
+                          int32_t *__restrict__ deg, uint8_t *__restrict__ heavy_flag, int light_cap) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < nnz) col[i] = (int32_t)(keys[i] & 0xFFFFFFFFu);
   if (i < n) {
     int64_t dg = rowptr[i + 1] - rowptr[i];
     deg[i] = (int32_t)dg;
-    heavy_flag[i] = dg > kLightCap ? 1 : 0;
+    heavy_flag[i] = dg > light_cap ? 1 : 0;
   }
 }
 
 __global__ void k_heavy_seg_map(const int32_t *__restrict__ heavy, int64_t nh, const int64_t *__restrict__ seg_ptr,
                                 const int64_t *__restrict__ rowptr, int64_t *__restrict__ seg_e0,
-                                int32_t *__restrict__ seg_h) {
+                                int32_t *__restrict__ seg_h, int heavy_seg) {
   const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (h >= nh) return;
   const int64_t b = rowptr[heavy[h]];
   for (int64_t sg = seg_ptr[h]; sg < seg_ptr[h + 1]; ++sg) {
-    seg_e0[sg] = b + (sg - seg_ptr[h]) * kHeavySeg;
+    seg_e0[sg] = b + (sg - seg_ptr[h]) * heavy_seg;
     seg_h[sg] = (int32_t)h;
   }
 }
 
 __global__ void k_heavy_segs(const int32_t *__restrict__ heavy, int64_t nh,
-                             const int32_t *__restrict__ deg, int64_t *__restrict__ nseg) {
+                             const int32_t *__restrict__ deg, int64_t *__restrict__ nseg, int heavy_seg) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < nh) nseg[i] = (deg[heavy[i]] + kHeavySeg - 1) / kHeavySeg;
+  if (i < nh) nseg[i] = (deg[heavy[i]] + heavy_seg - 1) / heavy_seg;
   if (i == nh) nseg[i] = 0;
 }
 
@@ -94,6 +97,8 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
   g->row0 = row0;
   g->bounds = {0, n_all};
   g->device = c.device;
+  if (const char *v = getenv("NETMFP_LIGHT_CAP")) g->light_cap = std::max(1, atoi(v));
+  if (const char *v = getenv("NETMFP_HEAVY_SEG")) g->heavy_seg = std::max(1, atoi(v));
   try {
     int64_t nk = 2 * m;
     DBuf<uint64_t> keys(nk > 0 ? nk : 1, s), keys2(nk > 0 ? nk : 1, s);
@@ -139,7 +144,8 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
     DBuf<uint8_t> hflag(n, s);
     NM_LAUNCH(c, "rowptr", k_rowptr<<<ceil_div(n + 1, 256), 256, 0, s>>>(keys, nnz, n, row0, g->rowptr));
     int64_t mx = std::max(nnz, n);
-    NM_LAUNCH(c, "col_deg", k_col_deg<<<ceil_div(mx, 256), 256, 0, s>>>(keys, nnz, g->rowptr, n, g->col, g->deg, hflag));
+    NM_LAUNCH(c, "col_deg", k_col_deg<<<ceil_div(mx, 256), 256, 0, s>>>(keys, nnz, g->rowptr, n, g->col, g->deg, hflag,
+                                                                             g->light_cap));
     // heavy rows (degree > kLightCap) for the split SpMM path
     {
       DBuf<int32_t> hv(n, s);
@@ -158,7 +164,7 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
         NM_CUDA(cudaMemcpyAsync(g->heavy.p, hv.p, nh * 4, cudaMemcpyDeviceToDevice, s));
       g->heavy_seg_ptr.alloc(nh + 1, s);
       DBuf<int64_t> nseg(nh + 1, s);
-      NM_LAUNCH(c, "heavy_segs", k_heavy_segs<<<ceil_div(nh + 1, 256), 256, 0, s>>>(g->heavy, nh, g->deg, nseg));
+      NM_LAUNCH(c, "heavy_segs", k_heavy_segs<<<ceil_div(nh + 1, 256), 256, 0, s>>>(g->heavy, nh, g->deg, nseg, g->heavy_seg));
       size_t tb2 = 0;
       NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, nseg.p, g->heavy_seg_ptr.p, nh + 1, s));
       DBuf<char> tmp2b(tb2, s);
@@ -173,7 +179,7 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
       g->seg_h.alloc(nsegs > 0 ? nsegs : 1, s);
       if (nh > 0)
         NM_LAUNCH(c, "heavy_seg_map", k_heavy_seg_map<<<ceil_div(nh, 128), 128, 0, s>>>(
-                                          g->heavy, nh, g->heavy_seg_ptr, g->rowptr, g->seg_e0, g->seg_h));
+                                          g->heavy, nh, g->heavy_seg_ptr, g->rowptr, g->seg_e0, g->seg_h, g->heavy_seg));
     }
   } catch (...) {
     delete g;

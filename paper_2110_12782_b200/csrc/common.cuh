@@ -234,6 +234,11 @@ struct Block {
 // ----------------------------------------------------------------------------
 // graph (device CSR)
 // ----------------------------------------------------------------------------
+// rows with more neighbours than light_cap are split across warps in segments
+// of heavy_seg entries (spmm.cu); per graph, NETMFP_LIGHT_CAP / NETMFP_HEAVY_SEG
+constexpr int kLightCapDefault = 64;
+constexpr int kHeavySegDefault = 64;
+
 struct Graph {
   int64_t n = 0, nnz = 0;  // local rows [row0, row0 + n) and their nonzeros
   int64_t n_global = 0, row0 = 0;
@@ -247,14 +252,12 @@ struct Graph {
   int64_t heavy_nnz = 0;
   DBuf<int64_t> heavy_seg_ptr;  // per heavy row: first segment index (n_heavy+1)
   int64_t n_heavy_segs = 0;
+  int light_cap = kLightCapDefault, heavy_seg = kHeavySegDefault;
   DBuf<int64_t> seg_e0;  // per heavy segment: first entry
   DBuf<int32_t> seg_h;   // per heavy segment: index into heavy
   int device = 0;
 };
 
-// rows with more neighbours than this are split across warps (spmm.cu)
-constexpr int kLightCap = 64;
-constexpr int kHeavySeg = 64;
 
 // ----------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al. SC'11) — the CUDA side's own implementation of

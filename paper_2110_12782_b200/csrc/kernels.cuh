@@ -38,6 +38,8 @@ struct SpmmArgs {
   int64_t ldacc = 0;
   float acc_scale = 0.f;
   float gamma = 0.f;
+  int light_cap = kLightCapDefault;  // filled from the graph by spmm()
+  int heavy_seg = kHeavySegDefault;
 };
 void spmm(Ctx &c, const Graph &g, const SpmmArgs &p);
 void deg_pow(Ctx &c, const Graph &g, float e, float *out);  // out[i] = d_i^-e (0 if d_i = 0)

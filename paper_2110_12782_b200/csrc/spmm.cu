@@ -6,10 +6,10 @@
 //  * column chunks of CW = 4·LPR floats (128 B at LPR = 8) are the grid's
 //    y-dimension, so all row-blocks of chunk 0 run before chunk 1: the
 //    gathered working set per chunk is n·128 B and stays L2-resident;
-//  * light rows (deg <= kLightCap): one LPR-lane group per row, each lane a
+//  * light rows (deg <= light_cap): one LPR-lane group per row, each lane a
 //    float4 column slice; the group loads LPR column indices in one coalesced
 //    read, shuffles them, and keeps LPR independent 16-B gathers in flight;
-//  * heavy rows (deg > kLightCap, power-law hubs): split into kHeavySeg-nnz
+//  * heavy rows (deg > light_cap, power-law hubs): split into heavy_seg-nnz
 //    segments, one group each, partial sums reduced with float4 atomics into
 //    a small buffer that the light kernel's epilogue reads;
 //  * fused epilogue: row scaling d_u^-a (degree from rowptr, no extra load),
@@ -78,7 +78,7 @@ __device__ __forceinline__ float4 gather_sum(const int32_t *__restrict__ col, in
 }
 
 template <int LPR, bool SCOL>
-__global__ void __launch_bounds__(256) k_spmm_heavy(SpmmArgs p, const int64_t *__restrict__ rowptr,
+__global__ void __launch_bounds__(256, 8) k_spmm_heavy(SpmmArgs p, const int64_t *__restrict__ rowptr,
                                                     const int32_t *__restrict__ col,
                                                     const int32_t *__restrict__ heavy,
                                                     const int64_t *__restrict__ seg_e0,
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) k_spmm_heavy(SpmmArgs p, const int64_t *_
   const int64_t h = __ldg(seg_h + sidx);
   const int64_t e0 = __ldg(seg_e0 + sidx);
   const int64_t re = __ldg(rowptr + __ldg(heavy + h) + 1);
-  const int64_t e1 = min(e0 + (int64_t)kHeavySeg, re);
+  const int64_t e1 = min(e0 + (int64_t)p.heavy_seg, re);
   if (active) {
     float4 acc = gather_sum<SCOL>(col, e0, e1, p.X + c, (uint32_t)p.ldx, p.s_col);
     float *dst = hsum + h * ldh + c;
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(256, MINB) k_spmm_rows(SpmmArgs p, const int64
     if (active && p.acc_out && p.acc_in && p.acc_scale != 0.f)
       a0 = *reinterpret_cast<const float4 *>(p.acc_in + u * p.ldai + c);
     float4 acc;
-    if (dg > kLightCap) {
+    if (dg > p.light_cap) {
       // heavy row: partial sums were reduced by k_spmm_heavy
       int64_t lo = 0, hi = nh - 1;
       while (lo < hi) {
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256) k_spmm_flat(SpmmArgs p, const int64_t *__
     srp[lane] = __ldg(rowptr + min(r0 + lane, n));
     if (lane == 31) srp[32] = __ldg(rowptr + min(r0 + 32, n));
     __syncwarp();
-    const unsigned hmask = __ballot_sync(0xffffffffu, srp[lane + 1] - srp[lane] > kLightCap);
+    const unsigned hmask = __ballot_sync(0xffffffffu, srp[lane + 1] - srp[lane] > p.light_cap);
     const int rb = gi * RPG, re = rb + RPG;
     const unsigned range = (re == 32 ? 0xffffffffu : ((1u << re) - 1u));
     const int64_t gend = srp[re];
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(256) k_spmm_flat(SpmmArgs p, const int64_t *__
       const int64_t u = r0 + ri;
       if (u >= n || !active) return;
       const int64_t dg = srp[ri + 1] - srp[ri];
-      if (dg > kLightCap) {
+      if (dg > p.light_cap) {
         int64_t lo = 0, hi = nh - 1;
         while (lo < hi) {
           int64_t mid = (lo + hi) >> 1;
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(256) k_spmm_seg(SpmmArgs p, const int64_t *__r
     const int rows = (int)min((int64_t)32, n - r0);
     const int64_t rs = __ldg(rowptr + r0 + min(lane, rows));
     const int64_t re = __ldg(rowptr + r0 + min(lane + 1, rows));
-    const unsigned hmask = __ballot_sync(FULL, lane < rows && re - rs > kLightCap);
+    const unsigned hmask = __ballot_sync(FULL, lane < rows && re - rs > p.light_cap);
     const int64_t E0 = __shfl_sync(FULL, rs, 0), E1 = __shfl_sync(FULL, re, rows - 1);
     float4 acc[NV];
 #pragma unroll
@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(256) k_spmm_wr(SpmmArgs p, const int64_t *__re
     float4 acc[NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (dg > kLightCap) {
+    if (dg > p.light_cap) {
       int64_t lo = 0, hi = nh - 1;
       while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
@@ -545,6 +545,126 @@ static void spmm_flat_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
                                                                              g.n_heavy, hsum.p, ldh));
 }
 
+// Two-slice variants: a column pass of cw <= 256 columns (cw = 4·(32 + extra)),
+// lane li owns columns c0 = base + 4 li and, for li < extra, c1 = base + 128 + 4 li.
+// 286 columns thus take two passes of 144 instead of 128 + 128 + 30.
+template <bool SCOL>
+__device__ __forceinline__ void gather_sum2(const int32_t *__restrict__ col, int64_t e0, int64_t e1,
+                                            const float *__restrict__ X0, const float *__restrict__ X1, bool two,
+                                            uint32_t ldx, const float *__restrict__ s_col, float4 &a0,
+                                            float4 &a1) {
+  a0 = make_float4(0.f, 0.f, 0.f, 0.f);
+  a1 = a0;
+  const int32_t *cp = col + e0;
+  int cnt = (int)(e1 - e0);
+  for (; cnt >= 4; cnt -= 4, cp += 4) {
+    const uint32_t v0 = __ldg(cp), v1 = __ldg(cp + 1), v2 = __ldg(cp + 2), v3 = __ldg(cp + 3);
+    float4 x0 = __ldg(reinterpret_cast<const float4 *>(X0 + (uint64_t)v0 * ldx));
+    float4 x1 = __ldg(reinterpret_cast<const float4 *>(X0 + (uint64_t)v1 * ldx));
+    float4 x2 = __ldg(reinterpret_cast<const float4 *>(X0 + (uint64_t)v2 * ldx));
+    float4 x3 = __ldg(reinterpret_cast<const float4 *>(X0 + (uint64_t)v3 * ldx));
+    float4 y0 = make_float4(0.f, 0.f, 0.f, 0.f), y1 = y0, y2 = y0, y3 = y0;
+    if (two) {
+      y0 = __ldg(reinterpret_cast<const float4 *>(X1 + (uint64_t)v0 * ldx));
+      y1 = __ldg(reinterpret_cast<const float4 *>(X1 + (uint64_t)v1 * ldx));
+      y2 = __ldg(reinterpret_cast<const float4 *>(X1 + (uint64_t)v2 * ldx));
+      y3 = __ldg(reinterpret_cast<const float4 *>(X1 + (uint64_t)v3 * ldx));
+    }
+    if (SCOL) {
+      const float s0 = __ldg(s_col + v0), s1 = __ldg(s_col + v1), s2 = __ldg(s_col + v2), s3 = __ldg(s_col + v3);
+      a0 = f4_fma(s0, x0, a0); a0 = f4_fma(s1, x1, a0); a0 = f4_fma(s2, x2, a0); a0 = f4_fma(s3, x3, a0);
+      a1 = f4_fma(s0, y0, a1); a1 = f4_fma(s1, y1, a1); a1 = f4_fma(s2, y2, a1); a1 = f4_fma(s3, y3, a1);
+    } else {
+      a0 = f4_add(f4_add(x0, x1), a0);
+      a0 = f4_add(f4_add(x2, x3), a0);
+      a1 = f4_add(f4_add(y0, y1), a1);
+      a1 = f4_add(f4_add(y2, y3), a1);
+    }
+  }
+  for (; cnt > 0; --cnt, ++cp) {
+    const uint32_t v = __ldg(cp);
+    const float4 x = __ldg(reinterpret_cast<const float4 *>(X0 + (uint64_t)v * ldx));
+    const float4 y = two ? __ldg(reinterpret_cast<const float4 *>(X1 + (uint64_t)v * ldx)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float sc = SCOL ? __ldg(s_col + v) : 1.f;
+    a0 = f4_fma(sc, x, a0);
+    a1 = f4_fma(sc, y, a1);
+  }
+}
+
+template <bool SCOL>
+__global__ void __launch_bounds__(256) k_spmm_heavy2(SpmmArgs p, const int64_t *__restrict__ rowptr,
+                                                     const int32_t *__restrict__ col, const int32_t *__restrict__ heavy,
+                                                     const int64_t *__restrict__ seg_e0,
+                                                     const int32_t *__restrict__ seg_h, int64_t nsegs, int cw,
+                                                     float *__restrict__ hsum, int64_t ldh) {
+  const int li = threadIdx.x & 31;
+  const int64_t sidx = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (sidx >= nsegs) return;
+  const int base = blockIdx.y * cw;
+  const int c0 = base + li * 4, c1 = base + 128 + li * 4;
+  const bool act0 = c0 < p.cols && c0 < base + cw;
+  const bool act1 = c1 < p.cols && c1 < base + cw;
+  const int64_t h = __ldg(seg_h + sidx);
+  const int64_t e0 = __ldg(seg_e0 + sidx);
+  const int64_t re = __ldg(rowptr + __ldg(heavy + h) + 1);
+  const int64_t e1 = min(e0 + (int64_t)p.heavy_seg, re);
+  if (!act0) return;
+  float4 a0, a1;
+  gather_sum2<SCOL>(col, e0, e1, p.X + c0, p.X + (act1 ? c1 : c0), act1, (uint32_t)p.ldx, p.s_col, a0, a1);
+  atomicAdd(reinterpret_cast<float4 *>(hsum + h * ldh + c0), a0);
+  if (act1) atomicAdd(reinterpret_cast<float4 *>(hsum + h * ldh + c1), a1);
+}
+
+template <bool SCOL>
+__global__ void __launch_bounds__(256, 4) k_spmm_rows2(SpmmArgs p, const int64_t *__restrict__ rowptr,
+                                                       const int32_t *__restrict__ col, int64_t n, int cw,
+                                                       const int32_t *__restrict__ heavy, int64_t nh,
+                                                       const float *__restrict__ hsum, int64_t ldh) {
+  const int li = threadIdx.x & 31;
+  const int base = blockIdx.y * cw;
+  const int c0 = base + li * 4, c1 = base + 128 + li * 4;
+  const bool act0 = c0 < p.cols && c0 < base + cw;
+  const bool act1 = c1 < p.cols && c1 < base + cw;
+  const int64_t stride = (int64_t)gridDim.x * 8;
+  for (int64_t u = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); u < n; u += stride) {
+    const int64_t e0 = __ldg(rowptr + u), e1 = __ldg(rowptr + u + 1);
+    const int64_t dg = e1 - e0;
+    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+    if (dg > p.light_cap) {
+      int64_t lo = 0, hi = nh - 1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(heavy + mid) < u) lo = mid + 1; else hi = mid;
+      }
+      if (act0) a0 = *reinterpret_cast<const float4 *>(hsum + lo * ldh + c0);
+      if (act1) a1 = *reinterpret_cast<const float4 *>(hsum + lo * ldh + c1);
+    } else if (act0) {
+      gather_sum2<SCOL>(col, e0, e1, p.X + c0, p.X + (act1 ? c1 : c0), act1, (uint32_t)p.ldx, p.s_col, a0, a1);
+    }
+    if (act0) row_epilogue(p, u, dg, a0, c0);
+    if (act1) row_epilogue(p, u, dg, a1, c1);
+  }
+}
+
+template <bool SCOL>
+static void spmm2_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
+  const int nch = (int)ceil_div(p.cols, 256);
+  const int cw = (int)((ceil_div(p.cols, nch) + 3) / 4 * 4);
+  DBuf<float> hsum;
+  int64_t ldh = pad4(p.cols);
+  if (g.n_heavy > 0) {
+    hsum.alloc((size_t)g.n_heavy * ldh, c.stream);
+    hsum.zero();
+    dim3 gh(ceil_div(g.n_heavy_segs, 8), nch);
+    NM_LAUNCH(c, "spmm_heavy", k_spmm_heavy2<SCOL><<<gh, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.heavy, g.seg_e0,
+                                                                            g.seg_h, g.n_heavy_segs, cw, hsum, ldh));
+  }
+  const int64_t row_blocks = ceil_div(g.n, 8);
+  dim3 grid((unsigned)std::min<int64_t>(row_blocks, (int64_t)c.num_sms * 64), nch);
+  NM_LAUNCH(c, "spmm_rows", k_spmm_rows2<SCOL><<<grid, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.n, cw, g.heavy,
+                                                                          g.n_heavy, hsum.p, ldh));
+}
+
 template <int LPR, bool SCOL, int MINB>
 static void spmm_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
   constexpr int GPB = 256 / LPR;
@@ -567,7 +687,10 @@ static void spmm_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
                                                      hsum.p, ldh));
 }
 
-void spmm(Ctx &c, const Graph &g, const SpmmArgs &p) {
+void spmm(Ctx &c, const Graph &g, const SpmmArgs &p_in) {
+  SpmmArgs p = p_in;
+  p.light_cap = g.light_cap;
+  p.heavy_seg = g.heavy_seg;
   NM_REQUIRE(p.cols > 0 && p.ldx % 4 == 0 && p.ldy % 4 == 0, "spmm: ld must be a multiple of 4");
   NM_REQUIRE(p.ldx < (int64_t)1 << 32, "spmm: ldx must fit 32 bits");
   NM_REQUIRE(((uintptr_t)p.X & 15) == 0 && (!p.Y || ((uintptr_t)p.Y & 15) == 0),
@@ -577,13 +700,16 @@ void spmm(Ctx &c, const Graph &g, const SpmmArgs &p) {
   // tuning variants (NETMFP_SPMM env var, default 0): lanes per row x min blocks/SM
   static int variant = [] {
     const char *v = getenv("NETMFP_SPMM");
-    return v ? atoi(v) : 9;
+    return v ? atoi(v) : 32;
   }();
   if (p.s_col) {
     spmm_impl<32, true, 4>(c, g, p);
     return;
   }
   switch (variant) {
+    case 30: spmm2_impl<false>(c, g, p); break;
+    case 31: spmm_impl<32, false, 6>(c, g, p); break;
+    case 32: spmm_impl<32, false, 8>(c, g, p); break;
     case 21: spmm_wr_impl<1, false>(c, g, p); break;
     case 22: spmm_wr_impl<2, false>(c, g, p); break;
     case 23: spmm_wr_impl<3, false>(c, g, p); break;
