@@ -706,6 +706,27 @@ void spmm(Ctx &c, const Graph &g, const SpmmArgs &p_in) {
     spmm_impl<32, true, 4>(c, g, p);
     return;
   }
+  if (variant == 32 && p.cols > 128 && (p.cols % 128) != 0) {
+    // 128-column passes with a warp per row, then the leftover columns with
+    // narrower lane groups (4 or 2 rows per warp) instead of a mostly idle pass
+    const int64_t main = p.cols / 128 * 128, tail = p.cols - main;
+    SpmmArgs pm = p, pt = p;
+    pm.cols = main;
+    pt.cols = tail;
+    pt.X = p.X + main;
+    if (pt.Y) pt.Y = p.Y + main;
+    if (pt.prev) pt.prev = p.prev + main;
+    if (pt.acc_in) pt.acc_in = p.acc_in + main;
+    if (pt.acc_out) pt.acc_out = p.acc_out + main;
+    spmm_impl<32, false, 8>(c, g, pm);
+    if (tail <= 32)
+      spmm_impl<8, false, 8>(c, g, pt);
+    else if (tail <= 64)
+      spmm_impl<16, false, 8>(c, g, pt);
+    else
+      spmm_impl<32, false, 8>(c, g, pt);
+    return;
+  }
   switch (variant) {
     case 30: spmm2_impl<false>(c, g, p); break;
     case 31: spmm_impl<32, false, 6>(c, g, p); break;
