@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant_
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp (uniform addresses), one elected lane issues
       int64_t g = 0, tcount = 0;
       for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
         const int nt0 = (int)(it % p.nsplit) * per, nt1 = min(p.ntn, nt0 + per);
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant_
           if (use_b > 0) {
             SKP_T0();
             mbar_wait(&tfree[buf], (uint32_t)((use_b - 1) & 1));
-            SKP_ADD(1);
+            if (lane == 0) SKP_ADD(1);
           }
           tc_fence_after();
           const int64_t rem = p.ncols - (int64_t)nt * NW;
@@ -243,22 +243,29 @@ __global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant_
             {
               SKP_T0();
               mbar_wait(&split[s], (uint32_t)(use & 1));
-              SKP_ADD(2);
+              if (lane == 0) SKP_ADD(2);
             }
             tc_fence_after();
+            const bool leader = elect_one();
             const uint32_t ahi = smem_u32(base + s * STAGE), alo = ahi + ABYTES;
             const uint32_t bhi = alo + ABYTES, blo = bhi + BBYTES;
+            const uint64_t dah = make_desc(ahi, 16, 1024), dal = make_desc(alo, 16, 1024);
+            const uint64_t dbh = make_desc(bhi, 16, 1024), dbl = make_desc(blo, 16, 1024);
 #pragma unroll
             for (int ks = 0; ks < BK / 8; ++ks) {
-              const uint32_t ko = ks * 32;
               const uint32_t acc0 = (kc == 0 && ks == 0) ? 0u : 1u;
-              mma_tf32(d, make_desc(ahi + ko, 16, 1024), make_desc(bhi + ko, 16, 1024), idesc, acc0);
-              mma_tf32(d, make_desc(ahi + ko, 16, 1024), make_desc(blo + ko, 16, 1024), idesc, 1u);
-              mma_tf32(d, make_desc(alo + ko, 16, 1024), make_desc(bhi + ko, 16, 1024), idesc, 1u);
+              if (leader) {
+                mma_tf32(d, dah + 2 * ks, dbh + 2 * ks, idesc, acc0);
+                mma_tf32(d, dah + 2 * ks, dbl + 2 * ks, idesc, 1u);
+                mma_tf32(d, dal + 2 * ks, dbh + 2 * ks, idesc, 1u);
+              }
             }
-            mma_commit(&empty[s]);
+            __syncwarp();
+            if (leader) mma_commit(&empty[s]);
+            __syncwarp();
           }
-          mma_commit(&done[buf]);
+          if (elect_one()) mma_commit(&done[buf]);
+          __syncwarp();
         }
       }
     }

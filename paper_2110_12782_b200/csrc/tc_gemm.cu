@@ -134,32 +134,50 @@ __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUten
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp (uniform addresses), one elected lane issues
+      // per-unit constants (TMEM column, descriptor address offsets, instruction descriptor)
+      const int nun = p.nunits;
+      uint32_t ud[kMaxUnits], uao[kMaxUnits], ubo[kMaxUnits], uid[kMaxUnits];
+#pragma unroll
+      for (int ui = 0; ui < kMaxUnits; ++ui) {
+        if (ui >= nun) break;
+        ud[ui] = tmem + (uint32_t)p.u[ui].tcol;
+        uao[ui] = (uint32_t)(p.u[ui].mblk * BLK) >> 4;
+        ubo[ui] = (uint32_t)(p.u[ui].nblk * BLK) >> 4;
+        uid[ui] = make_idesc(p.u[ui].nw, 1, 1);
+      }
       for (int kc = 0; kc < nk; ++kc) {
         const int s = kc % S, use = kc / S;
         mbar_wait(&split[s], (uint32_t)(use & 1));
         tc_fence_after();
+        const bool leader = elect_one();
         const uint32_t raw = smem_u32(base + s * stage_bytes);
         const uint32_t lo = raw + nblk * BLK;
         const uint32_t braw = SYM ? raw : raw + p.na_blk * BLK;
         const uint32_t blo = SYM ? lo : lo + p.na_blk * BLK;
+        // descriptors once per chunk; per unit / K step only the address field moves
+        const uint64_t dA = make_desc_mn32(raw, BLK), dAl = make_desc_mn32(lo, BLK);
+        const uint64_t dB = make_desc_mn32(braw, BLK), dBl = make_desc_mn32(blo, BLK);
 #pragma unroll
         for (int ks = 0; ks < BK / 8; ++ks) {
-          const uint32_t ko = ks * 1024;
-          for (int ui = 0; ui < p.nunits; ++ui) {
-            const GUnit &u = p.u[ui];
-            const uint32_t idesc = make_idesc(u.nw, 1, 1);
-            const uint32_t ao = u.mblk * BLK + ko, bo = u.nblk * BLK + ko;
-            const uint32_t d = tmem + (uint32_t)u.tcol;
+          const uint32_t ko = ks * (1024 >> 4);
+#pragma unroll
+          for (int ui = 0; ui < kMaxUnits; ++ui) {
+            if (ui >= nun) break;
             const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
-            mma_tf32(d, make_desc_mn32(raw + ao, BLK), make_desc_mn32(braw + bo, BLK), idesc, acc0);
-            mma_tf32(d, make_desc_mn32(raw + ao, BLK), make_desc_mn32(blo + bo, BLK), idesc, 1u);
-            mma_tf32(d, make_desc_mn32(lo + ao, BLK), make_desc_mn32(braw + bo, BLK), idesc, 1u);
+            if (leader) {
+              mma_tf32(ud[ui], dA + uao[ui] + ko, dB + ubo[ui] + ko, uid[ui], acc0);
+              mma_tf32(ud[ui], dA + uao[ui] + ko, dBl + ubo[ui] + ko, uid[ui], 1u);
+              mma_tf32(ud[ui], dAl + uao[ui] + ko, dB + ubo[ui] + ko, uid[ui], 1u);
+            }
           }
         }
-        mma_commit(&empty[s]);
+        __syncwarp();
+        if (leader) mma_commit(&empty[s]);
+        __syncwarp();
       }
-      mma_commit(done);
+      if (elect_one()) mma_commit(done);
+      __syncwarp();
     }
   } else {
     // workers: lo split (+ row weights) for every chunk, then the epilogue
@@ -283,7 +301,8 @@ struct GemmP {
   int nh, hr;     // output columns split into nh parts of hr (<= 256) columns
   int tri;        // B upper triangular: chunk kb touches columns >= 32 kb
   int64_t nitems; // (M tile, part) work items
-  int stages;
+  int stages;     // shared-memory ring (A raw + Bᵀ part)
+  int astages;    // TMEM A stages (hi + lo, 64 columns each)
   float *C;
   int64_t ldc;
   int64_t ccols;  // valid output columns
@@ -310,8 +329,10 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
   uint64_t *bars = reinterpret_cast<uint64_t *>(base + S * stage_bytes);
   uint64_t *full = bars, *split = bars + S, *empty = bars + 2 * S;
   uint64_t *done = bars + 3 * S, *tfree = bars + 3 * S + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * S + 4);
-  float *tpose = reinterpret_cast<float *>(bars + 3 * S + 6);  // 4 warps × 32 × 33
+  const int ST = p.astages;
+  uint64_t *aempty = bars + 3 * S + 4;  // TMEM A stage free (MMA done reading it)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * S + 8);
+  float *tpose = reinterpret_cast<float *>(bars + 3 * S + 10);  // 4 warps × 32 × 33
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -324,6 +345,7 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
       mbar_init(&done[b], 1);
       mbar_init(&tfree[b], kWorkers);
     }
+    for (int b = 0; b < ST; ++b) mbar_init(&aempty[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -357,7 +379,7 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // the whole warp runs the loop (uniform addresses); one elected lane issues
       int64_t g = 0, ic = 0;
       for (int64_t it = blockIdx.x; it < p.nitems; it += gridDim.x, ++ic) {
         const int h = (int)(it % p.nh);
@@ -376,32 +398,47 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
           {
             TCP_T0();
             mbar_wait(&split[s], (uint32_t)(use & 1));
-            TCP_ADD(2);
+            if (lane == 0) TCP_ADD(2);
           }
           tc_fence_after();
+          TCP_T0();
           const uint32_t bhi = smem_u32(base + s * stage_bytes) + ABYTES, blo = bhi + bbytes;
-          const uint32_t ahi = tA + (uint32_t)(64 * s), alo = ahi + 32;
+          const int sa = (int)(g % ST);
+          const uint32_t ahi = tA + (uint32_t)(64 * sa), alo = ahi + 32;
           int c0 = pc0;
           if (p.tri) c0 = max(c0, (kc * 32) & ~15);
-          if (c0 < pc1) {
+          if (c0 < pc1 && elect_one()) {
             const int N = pc1 - c0;
             const uint32_t idesc = make_idesc(N, 0, 0);
             const uint32_t d = tmem + (uint32_t)(buf * p.hr + (c0 - pc0));
             const uint32_t bo = (uint32_t)(c0 - pc0) * 128;
+            // descriptors built once per chunk; a K step of 8 tf32 is +32 B = +2 in
+            // the descriptor's address field (lean issue loop: the MMA issue rate,
+            // not the tensor core, bounds kernels that rebuild them per MMA)
+            const uint64_t dbh = make_desc(bhi + bo, 16, 1024), dbl = make_desc(blo + bo, 16, 1024);
+            const uint32_t acc0 = (kc == 0) ? 0u : 1u;
+            // every column is first touched by K-chunk 0 (tri: chunk kb only adds to
+            // columns >= 32 kb), so chunk 0 / kstep 0 starts the sums
+            mma_tf32_ts(d, ahi, dbh, idesc, acc0);
+            mma_tf32_ts(d, ahi, dbl, idesc, 1u);
+            mma_tf32_ts(d, alo, dbh, idesc, 1u);
 #pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
-              const uint32_t ko = ks * 32;
-              // every column is first touched by K-chunk 0 (tri: chunk kb only
-              // adds to columns >= 32 kb), so chunk 0 / kstep 0 starts the sums
-              const uint32_t acc0 = (kc == 0 && ks == 0) ? 0u : 1u;
-              mma_tf32_ts(d, ahi + ks * 8, make_desc(bhi + bo + ko, 16, 1024), idesc, acc0);
-              mma_tf32_ts(d, ahi + ks * 8, make_desc(blo + bo + ko, 16, 1024), idesc, 1u);
-              mma_tf32_ts(d, alo + ks * 8, make_desc(bhi + bo + ko, 16, 1024), idesc, 1u);
+            for (int ks = 1; ks < 4; ++ks) {
+              mma_tf32_ts(d, ahi + ks * 8, dbh + 2 * ks, idesc, 1u);
+              mma_tf32_ts(d, ahi + ks * 8, dbl + 2 * ks, idesc, 1u);
+              mma_tf32_ts(d, alo + ks * 8, dbh + 2 * ks, idesc, 1u);
             }
           }
-          mma_commit(&empty[s]);
+          __syncwarp();
+          if (elect_one()) {
+            mma_commit(&empty[s]);
+            mma_commit(&aempty[sa]);
+          }
+          __syncwarp();
+          if (lane == 0) TCP_ADD(6);
         }
-        mma_commit(&done[buf]);
+        if (elect_one()) mma_commit(&done[buf]);
+        __syncwarp();
       }
     }
   } else if (warp < 6) {
@@ -428,7 +465,11 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
         }
 #pragma unroll
         for (int i = 0; i < 32; ++i) lo[i] = hi[i] - tf32_trunc(hi[i]);
-        const uint32_t ta = tA + ((uint32_t)(32 * q) << 16) + (uint32_t)(64 * s);
+        const int sa = (int)(g % ST);
+        const int64_t ua = g / ST;
+        if (ua > 0) mbar_wait(&aempty[sa], (uint32_t)((ua - 1) & 1));  // MMAs done with this TMEM stage
+        tc_fence_after();
+        const uint32_t ta = tA + ((uint32_t)(32 * q) << 16) + (uint32_t)(64 * sa);
         tmem_st32(ta, hi);
         tmem_st32(ta + 32, lo);
         tmem_wait_st();
@@ -752,10 +793,12 @@ static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ld
   p.rexp = rexp;
   const size_t tpose = (size_t)4 * 32 * 33 * 4;
   const size_t stage = (size_t)128 * 128 + (size_t)2 * hr * 128;
-  const int S = (int)std::min<size_t>(std::min<size_t>(4, (512 - 2 * hr) / 64), (kSmemMax - 1024 - 256 - tpose) / stage);
-  NM_REQUIRE(S >= 2, "tc_gemm_tall: stage does not fit");
+  const int S = (int)std::min<size_t>(6, (kSmemMax - 1024 - 256 - tpose) / stage);
+  const int ST = std::min(4, (512 - 2 * hr) / 64);
+  NM_REQUIRE(S >= 2 && ST >= 2, "tc_gemm_tall: stage does not fit");
   p.stages = S;
-  const size_t smem = 1024 + S * stage + (3 * S + 6) * 8 + tpose;
+  p.astages = ST;
+  const size_t smem = 1024 + S * stage + (3 * S + 10) * 8 + tpose;
   static bool attr = false;
   if (!attr) {
     NM_CUDA(cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));

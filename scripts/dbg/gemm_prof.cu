@@ -26,8 +26,8 @@ int main() {
     cudaMemcpyFromSymbol(hp, g_tcprof, sizeof(hp));
     double tot[8] = {};
     for (int b = 0; b < 148; ++b) for (int i = 0; i < 8; ++i) tot[i] += hp[b * 8 + i] / 148.0;
-    printf("tri=%d %.3f ms (%s): cycles/CTA prod-wait-empty %.0f mma-wait-tfree %.0f mma-wait-split %.0f split-wait-full %.0f epi-wait-done %.0f epi-work %.0f\n",
-           tri, ms, cudaGetErrorString(cudaGetLastError()), tot[0], tot[1], tot[2], tot[3], tot[4], tot[5]);
+    printf("tri=%d %.3f ms (%s): cycles/CTA prod-wait-empty %.0f mma-wait-tfree %.0f mma-wait-split %.0f split-wait-full %.0f epi-wait-done %.0f epi-work %.0f mma-issue %.0f\n",
+           tri, ms, cudaGetErrorString(cudaGetLastError()), tot[0], tot[1], tot[2], tot[3], tot[4], tot[5], tot[6]);
   }
   return 0;
 }
