@@ -291,6 +291,7 @@ int netmfp_graph_free(netmfp_graph *g) {
     gg->rowptr.s = gg->col.s = gg->deg.s = gg->heavy.s = gg->heavy_seg_ptr.s = nullptr;
     gg->seg_e0.s = nullptr;
     gg->seg_h.s = nullptr;
+    gg->hsum_ws.s = gg->hcnt_ws.s = nullptr;
     delete gg;
     delete g;
   });

@@ -255,6 +255,10 @@ struct Graph {
   int light_cap = kLightCapDefault, heavy_seg = kHeavySegDefault;
   DBuf<int64_t> seg_e0;  // per heavy segment: first entry
   DBuf<int32_t> seg_h;   // per heavy segment: index into heavy
+  // fused SpMM scratch, left all-zero by every launch: per heavy row partial
+  // sums (n_heavy x ld) and per (heavy row, column chunk) arrival counters
+  mutable DBuf<float> hsum_ws;
+  mutable DBuf<int32_t> hcnt_ws;
   int device = 0;
 };
 

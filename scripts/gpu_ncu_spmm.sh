@@ -1,3 +1,7 @@
-timeout 300 python scripts/spmm_one.py 286 > gpurun_out/spmm_one.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_spmm_seg" -s 1 -c 1 \
-   -o gpurun_out/prof_spmm286 python scripts/spmm_one.py 286 > gpurun_out/ncu_spmm.log 2>&1; echo ncu=$?
+# ncu --set full of the SpMM launches of the third 286-column and 128-column application (configs[2])
+for spec in "286 8 4" "128 4 2"; do
+set -- $spec
+timeout 300 python scripts/spmm_one.py $1 > gpurun_out/spmm_one_$1.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_spmm" -s $2 -c $3 \
+   -o gpurun_out/prof_spmm$1 python scripts/spmm_one.py $1 > gpurun_out/ncu_spmm$1.log 2>&1; echo ncu$1=$?
+done

@@ -15,7 +15,8 @@ want = [("gpu__time_duration.sum", "time"), ("dram__bytes_read.sum", "GB rd"), (
         ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor%"),
         ("sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed", "hmma%"),
         ("lts__t_bytes.sum", "L2 bytes"), ("lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum", "L2 hit sect"),
-        ("sm__warps_active.avg.pct_of_peak_sustained_active", "occ%"), ("launch__registers_per_thread", "regs"),
+        ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "lts%"), ("l1tex__t_sector_hit_rate.pct", "L1hit%"),
+        ("lts__t_sector_hit_rate.pct", "L2hit%"), ("sm__warps_active.avg.pct_of_peak_sustained_active", "occ%"), ("launch__registers_per_thread", "regs"),
         ("smsp__inst_executed.sum", "inst"), ("launch__grid_size", "grid")]
 cols = [(h.index(k), lab) for k, lab in want if k in h]
 for row in r[2:]:
