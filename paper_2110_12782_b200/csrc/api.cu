@@ -288,10 +288,7 @@ int netmfp_graph_free(netmfp_graph *g) {
     // free on the legacy default stream: the creating context (and its
     // stream) may already be gone
     Graph *gg = g->g;
-    gg->rowptr.s = gg->col.s = gg->deg.s = gg->heavy.s = gg->heavy_seg_ptr.s = nullptr;
-    gg->seg_e0.s = nullptr;
-    gg->seg_h.s = nullptr;
-    gg->hsum_ws.s = gg->hcnt_ws.s = nullptr;
+    gg->detach_streams();
     delete gg;
     delete g;
   });
@@ -477,11 +474,33 @@ int netmfp_propagate(netmfp_ctx *ctx, const netmfp_graph *gr, float *E, int64_t 
   });
 }
 
-static void embed_impl(Ctx &c, const Graph &g, const netmfp_params &p, const Mat &E, double *sigma_dev,
+// The compacted copy of g without its isolated vertices, when embed may run
+// on it: one rank, g not itself a row partition, and enough
+// vertices left for the rank-(k+s1) basis.  Built once per graph and cached.
+static const Graph *embed_graph(Ctx &c, const Graph &g, const netmfp_params &p) {
+  static const bool off = [] {
+    const char *v = getenv("NETMFP_NO_COMPACT");
+    return v && atoi(v);
+  }();
+  if (off || c.nranks != 1 || g.n_orig != 0 || g.row0 != 0 || g.n != g.n_global) return &g;
+  if (!g.compact_checked) {
+    NM_STAGE(c, "stage_compact");
+    g.compact.reset(compact_graph(c, g));
+    g.compact_checked = true;
+  }
+  if (!g.compact || g.compact->n < (int64_t)p.k + p.s1) return &g;
+  return g.compact.get();
+}
+
+static void embed_impl(Ctx &c, const Graph &g_in, const netmfp_params &p, const Mat &E_out, double *sigma_dev,
                        double *lambda_dev) {
   NM_REQUIRE(p.T >= 1 && p.b > 0, "embed: need T >= 1, b > 0");
   cudaStream_t s = c.stream;
+  const Graph &g = *embed_graph(c, g_in, p);
+  const bool compacted = &g != &g_in;
   const int64_t n = g.n;
+  Block Ec(compacted ? n : 0, p.d, s);
+  const Mat E = compacted ? Ec.m : E_out;
   Block U(n, p.k, s), F(n, p.k, s);
   DBuf<double> lam(p.k, s), C((size_t)p.k * p.k, s);
   {
@@ -498,13 +517,15 @@ static void embed_impl(Ctx &c, const Graph &g, const netmfp_params &p, const Mat
   {
     NM_STAGE(c, "stage_sketch_svd");
     sketch_svd(c, F.m, C, p.k, scale, p.d, p.s2, p.s3, p.z, p.seed, p.logmode, nullptr, sigma_dev, &E,
-               nullptr, nullptr, g.row0, g.n_global);                  // steps 4-5
+               nullptr, nullptr, g.row0, compacted ? g.n_orig : g.n_global,
+               compacted ? g.comp_id.p : nullptr);                     // steps 4-5
   }
   F.buf.release();
   {
     NM_STAGE(c, "stage_propagate");
     propagate(c, g, E, p.prop_order, p.mu, p.theta);                   // step 6
   }
+  if (compacted) scatter_rows(c, E, g.orig_id.p, E_out);             // isolated vertices: zero rows [R2]
 }
 
 int netmfp_embed(netmfp_ctx *ctx, const netmfp_graph *gr, const netmfp_params *p, float *E, int64_t lde,

@@ -188,4 +188,107 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
   return g;
 }
 
+// ---------------------------------------------------------------------------
+// Isolated-vertex compaction.  A vertex of degree 0 has a zero
+// row and column in every operator of the method ([R2]: d^e := 0), so every
+// dense block of embed is zero on it; the compacted graph keeps the other
+// vertices in their original order.  Edge offsets are unchanged (isolated
+// rows own no entries), so the heavy-row segment tables carry over as is.
+// ---------------------------------------------------------------------------
+__global__ void k_flag_nz(const int32_t *__restrict__ deg, int64_t n, int32_t *__restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) flag[i] = deg[i] > 0;
+  if (i == n) flag[i] = 0;
+}
+__global__ void k_compact_ids(const int32_t *__restrict__ deg, const int32_t *__restrict__ pos, int64_t n,
+                              int32_t *__restrict__ orig, int32_t *__restrict__ comp) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (deg[i] > 0) {
+    orig[pos[i]] = (int32_t)i;
+    comp[i] = pos[i];
+  } else {
+    comp[i] = -1;
+  }
+}
+__global__ void k_compact_rows(const int32_t *__restrict__ orig, int64_t ne, const int64_t *__restrict__ rowptr,
+                               const int32_t *__restrict__ deg, int64_t nnz, int64_t *__restrict__ rp_c,
+                               int32_t *__restrict__ deg_c) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < ne) {
+    rp_c[j] = rowptr[orig[j]];
+    deg_c[j] = deg[orig[j]];
+  }
+  if (j == ne) rp_c[ne] = nnz;
+}
+__global__ void k_remap_ids(const int32_t *__restrict__ in, int64_t m, const int32_t *__restrict__ comp,
+                            int32_t *__restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < m) out[i] = comp[in[i]];
+}
+
+Graph *compact_graph(Ctx &c, const Graph &g) {
+  if (g.row0 != 0 || g.n != g.n_global || g.n == 0) return nullptr;
+  cudaStream_t s = c.stream;
+  const int64_t n = g.n;
+  DBuf<int32_t> flag(n + 1, s), pos(n + 1, s);
+  NM_LAUNCH(c, "flag_nz", k_flag_nz<<<ceil_div(n + 1, 256), 256, 0, s>>>(g.deg, n, flag));
+  size_t tb = 0;
+  NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.p, pos.p, n + 1, s));
+  DBuf<char> tmp(tb, s);
+  NM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, flag.p, pos.p, n + 1, s));
+  c.launches += 1;
+  int32_t ne32 = 0;
+  NM_CUDA(cudaMemcpyAsync(&ne32, pos.p + n, 4, cudaMemcpyDeviceToHost, s));
+  NM_CUDA(cudaStreamSynchronize(s));
+  const int64_t ne = ne32;
+  if (ne == n || ne == 0) return nullptr;
+  auto gc = new Graph();
+  try {
+    gc->n = gc->n_global = ne;
+    gc->row0 = 0;
+    gc->bounds = {0, ne};
+    gc->nnz = g.nnz;
+    gc->nnz_global = g.nnz_global;
+    gc->device = g.device;
+    gc->light_cap = g.light_cap;
+    gc->heavy_seg = g.heavy_seg;
+    gc->n_orig = n;
+    gc->orig_id.alloc(ne, s);
+    gc->comp_id.alloc(n, s);
+    NM_LAUNCH(c, "compact_ids", k_compact_ids<<<ceil_div(n, 256), 256, 0, s>>>(g.deg, pos, n, gc->orig_id, gc->comp_id));
+    gc->rowptr.alloc(ne + 1, s);
+    gc->deg.alloc(ne, s);
+    NM_LAUNCH(c, "compact_rows", k_compact_rows<<<ceil_div(ne + 1, 256), 256, 0, s>>>(gc->orig_id, ne, g.rowptr, g.deg,
+                                                                                        g.nnz, gc->rowptr, gc->deg));
+    gc->col.alloc(g.nnz > 0 ? g.nnz : 1, s);
+    if (g.nnz > 0)
+      NM_LAUNCH(c, "remap_col", k_remap_ids<<<ceil_div(g.nnz, 256), 256, 0, s>>>(g.col, g.nnz, gc->comp_id, gc->col));
+    gc->n_heavy = g.n_heavy;
+    gc->heavy_nnz = g.heavy_nnz;
+    gc->n_heavy_segs = g.n_heavy_segs;
+    gc->heavy.alloc(g.n_heavy > 0 ? g.n_heavy : 1, s);
+    if (g.n_heavy > 0)
+      NM_LAUNCH(c, "remap_heavy", k_remap_ids<<<ceil_div(g.n_heavy, 256), 256, 0, s>>>(g.heavy, g.n_heavy, gc->comp_id,
+                                                                                        gc->heavy));
+    gc->heavy_seg_ptr.alloc(g.n_heavy + 1, s);
+    NM_CUDA(cudaMemcpyAsync(gc->heavy_seg_ptr.p, g.heavy_seg_ptr.p, (g.n_heavy + 1) * 8, cudaMemcpyDeviceToDevice, s));
+    const int64_t ns = g.n_heavy_segs > 0 ? g.n_heavy_segs : 1;
+    gc->seg_e0.alloc(ns, s);
+    gc->seg_h.alloc(ns, s);
+    NM_CUDA(cudaMemcpyAsync(gc->seg_e0.p, g.seg_e0.p, ns * 8, cudaMemcpyDeviceToDevice, s));
+    NM_CUDA(cudaMemcpyAsync(gc->seg_h.p, g.seg_h.p, ns * 4, cudaMemcpyDeviceToDevice, s));
+  } catch (...) {
+    delete gc;
+    throw;
+  }
+  return gc;
+}
+
+// rows[i] <- comp[rows[i]] (-1 for an isolated vertex: its terms are zero and
+// every row gather skips indices outside this rank's rows)
+void remap_rows(Ctx &c, int32_t *rows, int64_t m, const int32_t *comp) {
+  if (m > 0) NM_LAUNCH(c, "remap_rows", k_remap_ids<<<ceil_div(m, 256), 256, 0, c.stream>>>(rows, m, comp, rows));
+}
+
 }  // namespace netmfp

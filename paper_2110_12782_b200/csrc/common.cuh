@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "../../include/netmfp.h"
@@ -260,6 +261,20 @@ struct Graph {
   mutable DBuf<float> hsum_ws;
   mutable DBuf<int32_t> hcnt_ws;
   int device = 0;
+  // isolated-vertex compaction (embed): for a compacted graph, the original
+  // vertex count, compact -> original ids and original -> compact (-1 for
+  // degree 0); for a full graph, its cached compacted copy (if built)
+  int64_t n_orig = 0;
+  DBuf<int32_t> orig_id, comp_id;
+  mutable std::unique_ptr<Graph> compact;
+  mutable bool compact_checked = false;
+  void detach_streams() {  // free on the legacy stream (owning stream may be gone)
+    rowptr.s = col.s = deg.s = heavy.s = nullptr;
+    heavy_seg_ptr.s = seg_e0.s = nullptr;
+    seg_h.s = hcnt_ws.s = orig_id.s = comp_id.s = nullptr;
+    hsum_ws.s = nullptr;
+    if (compact) compact->detach_streams();
+  }
 };
 
 

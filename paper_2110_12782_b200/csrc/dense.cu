@@ -239,11 +239,12 @@ void gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, const 
 // Ω = randn(n, l) (Alg. 2 step 2) with Philox4x32-10 [R1], optional row scale
 // ---------------------------------------------------------------------------
 __global__ void k_gaussian(Mat O, uint32_t k0, uint32_t k1, const int32_t *__restrict__ deg,
-                           float rexp, int64_t row0) {
+                           float rexp, int64_t row0, const int32_t *__restrict__ ids) {
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= O.rows * O.cols) return;
   int64_t i = idx / O.cols, j = idx % O.cols;
-  const int64_t gi = i + row0;  // global row: every rank draws its own rows of the same Ω
+  // global row: every rank (or compacted graph) draws its own rows of the same Ω
+  const int64_t gi = ids ? (int64_t)ids[i] : i + row0;
   U4 ctr{(uint32_t)j, (uint32_t)(gi & 0xFFFFFFFF), (uint32_t)((uint64_t)gi >> 32), kTagOmega};
   U4 w = philox4x32_10(ctr, k0, k1);
   // Box–Muller in fp32 (the block is fp32; |error| ~1e-7 relative to the fp64 oracle)
@@ -253,10 +254,11 @@ __global__ void k_gaussian(Mat O, uint32_t k0, uint32_t k1, const int32_t *__res
   O.p[i * O.ld + j] = g * dpow_scale(deg, i, rexp);
 }
 
-void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, float rexp, int64_t row0) {
+void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, float rexp, int64_t row0,
+                    const int32_t *ids) {
   if (O.rows * O.cols == 0) return;
   NM_LAUNCH(c, "gaussian", k_gaussian<<<ceil_div(O.rows * O.cols, 256), 256, 0, c.stream>>>(
-      O, (uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32), deg, rexp, row0));
+      O, (uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32), deg, rexp, row0, ids));
 }
 
 __global__ void k_row_scale(Mat Y, const int32_t *__restrict__ deg, float rexp) {
@@ -296,6 +298,20 @@ void row_scale_block(Ctx &c, const Mat &Y, const int32_t *deg, float rexp) {
 void copy_block(Ctx &c, const float *src, int64_t lds, float *dst, int64_t ldd, int64_t rows,
                 int64_t cols) {
   NM_CUDA(cudaMemcpy2DAsync(dst, ldd * 4, src, lds * 4, cols * 4, rows, cudaMemcpyDefault, c.stream));
+}
+
+// Dst = 0 except Dst[ids[i], :] = Src[i, :]  (compacted rows back to all rows)
+__global__ void k_scatter_rows(Mat Src, const int32_t *__restrict__ ids, Mat Dst) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= Src.rows * Src.cols) return;
+  const int64_t i = idx / Src.cols, j = idx % Src.cols;
+  Dst.p[(int64_t)ids[i] * Dst.ld + j] = Src.p[i * Src.ld + j];
+}
+
+void scatter_rows(Ctx &c, const Mat &Src, const int32_t *ids, const Mat &Dst) {
+  NM_CUDA(cudaMemset2DAsync(Dst.p, Dst.ld * 4, 0, Dst.cols * 4, Dst.rows, c.stream));
+  if (Src.rows * Src.cols == 0) return;
+  NM_LAUNCH(c, "scatter_rows", k_scatter_rows<<<ceil_div(Src.rows * Src.cols, 256), 256, 0, c.stream>>>(Src, ids, Dst));
 }
 
 }  // namespace netmfp

@@ -7,6 +7,8 @@ namespace netmfp {
 // ---- build_csr.cu
 // CSR of rows [row0, row1) (default: all rows) with global column ids; the
 // edge list must contain every edge incident to those rows.
+Graph *compact_graph(Ctx &c, const Graph &g);  // nullptr if nothing to drop
+void remap_rows(Ctx &c, int32_t *rows, int64_t m, const int32_t *comp);
 Graph *build_csr_device(Ctx &c, int64_t n, const int32_t *src, const int32_t *dst, int64_t m, int64_t row0 = 0,
                         int64_t row1 = -1);
 
@@ -64,11 +66,14 @@ void gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, const 
                    const Mat &C);
 bool tc_enabled();
 // Ω = randn(n, l) from Philox [R1], row-scaled by d_i^-e (deg != null)
-void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, float rexp, int64_t row0 = 0);
+void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, float rexp, int64_t row0 = 0,
+                    const int32_t *ids = nullptr);  // ids: global row id per row (compacted graphs)
 // Dst[i, :] = d_i^-e Src[i, :]
 void scale_copy_block(Ctx &c, const Mat &Src, const Mat &Dst, const int32_t *deg, float rexp);
 // Y[i, :] *= d_i^-e
 void row_scale_block(Ctx &c, const Mat &Y, const int32_t *deg, float rexp);
+// Dst (all rows) = 0 except Dst[ids[i], :] = Src[i, :]
+void scatter_rows(Ctx &c, const Mat &Src, const int32_t *ids, const Mat &Dst);
 // copy with ld conversion (device-to-device)
 void copy_block(Ctx &c, const float *src, int64_t lds, float *dst, int64_t ldd, int64_t rows,
                 int64_t cols);

@@ -57,7 +57,7 @@ void freigs(Ctx &c, const Graph &g, double alpha, int k, int s1, int q, uint64_t
   Block P(n, l, s), T(n, l, s), Y(n, l, s);
   DBuf<float> xfull;  // all ranks' rows of the SpMM input (multi-GPU only)
   // step 2: Ω = randn(n, l), Y = X Ω
-  gaussian_block(c, P.m, seed, g.deg, a, g.row0);  // P = D^-α Ω (this rank's rows)
+  gaussian_block(c, P.m, seed, g.deg, a, g.row0, g.orig_id.p);  // P = D^-α Ω (this rank's rows)
   SpmmArgs sp;
   sp.cols = l;
   sp.X = dist_gather_rows(c, g, P.m, xfull); sp.ldx = P.m.ld; sp.Y = Y.m.p; sp.ldy = Y.m.ld; sp.a = a;
@@ -134,9 +134,11 @@ __global__ void k_abs(const double *lam, int d, double *out) {
 // Alg. 4
 void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int d, int s2, int s3, int z,
                 uint64_t seed, int logmode, const Mat *Uout, double *sigma_dev, const Mat *Eout,
-                const Mat *Yout, double *Zout, int64_t row0, int64_t n_global) {
+                const Mat *Yout, double *Zout, int64_t row0, int64_t n_global, const int32_t *comp_id) {
   const int64_t n = F.rows;  // this rank's rows [row0, row0 + n) of n_global
   if (n_global < 0) n_global = n;
+  // comp_id (compacted graph): Ψ and Π are drawn over the n_global original
+  // vertices and their rows mapped to compact rows (-1: isolated, zero terms)
   const int64_t h2 = (int64_t)d + s2, h3 = (int64_t)d + s3;
   NM_REQUIRE(d >= 1 && s2 >= 0 && s3 >= 0, "sketch_svd: need d >= 1, s2, s3 >= 0");
   NM_REQUIRE(h2 <= n_global && h3 <= n_global * (int64_t)z, "sketch_svd: d + s2 must not exceed n");
@@ -148,6 +150,7 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
   {
     NM_STAGE(c, "stage_gen_sparse_sign");
     gen_sparse_sign(c, n_global, h2, z, seed, kTagPsi, Psi);
+    if (comp_id) remap_rows(c, Psi.rows, h2 * z, comp_id);
   }
   // FC = F · C
   Block FC(n, k, s);
@@ -167,6 +170,7 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
   {
     NM_STAGE(c, "stage_gen_sparse_sign");
     gen_sparse_sign(c, n_global, h3, z, seed, kTagPi, Pi);
+    if (comp_id) remap_rows(c, Pi.rows, h3 * z, comp_id);
   }
   // step 6: Z = Πᵀ f(scale F(p,:) C F(p,:)ᵀ) Π  (both sides restricted to Π's coordinates)
   NM_STAGE(c, "stage_sketch_z_core");

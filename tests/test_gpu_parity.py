@@ -237,10 +237,44 @@ def test_embed_end_to_end(L, ctx, graphs):
     assert np.abs(lam.cpu().numpy() - ref["lam"]).max() <= 1e-3 * abs(ref["lam"][0])
     sg = sig.cpu().numpy()
     assert np.abs(sg[:4] - ref["sigma"][:4]).max() <= 1e-3 * ref["sigma"][0]
+    assert _match_cols_up_to_sign(E.cpu().numpy(), ref["E"], 4) <= 1e-3
     # host-buffer end-to-end path gives the same embedding
     Eh = np.zeros((n, 16), dtype=np.float32)
     L.netmfp_embed_edges(ctx, n, s, t, L.make_params(**prm), Eh)
     assert relf(Eh, E.cpu().numpy()) <= 1e-4
+
+
+def _match_cols_up_to_sign(E, R, ncols):
+    """max over the leading columns of min(|E_j - R_j|, |E_j + R_j|) / |R_j|"""
+    worst = 0.0
+    for j in range(ncols):
+        r = np.linalg.norm(R[:, j])
+        worst = max(worst, min(np.linalg.norm(E[:, j] - R[:, j]), np.linalg.norm(E[:, j] + R[:, j])) / r)
+    return worst
+
+
+def test_embed_isolated_vertices_compacted(L, ctx):
+    """Isolated vertices interleaved with the graph (embed drops them on the
+    GPU): same λ, σ and embedding as the oracle on the full
+    vertex set, and exactly zero rows for the isolated vertices [R2]."""
+    n0, s0, t0 = inputs.small_graph("er", 600, 3, avg_deg=10.0)
+    n = 900
+    perm = np.random.default_rng(11).permutation(n)[:n0].astype(np.int32)
+    s, t = perm[s0], perm[t0]
+    g = L.netmfp_build_csr(ctx, n, dev(s), dev(t))
+    prm = dict(alpha=0.45, k=32, s1=10, q=3, T=10, b=1.0, d=16, s2=16, s3=160, z=8, prop_order=10,
+               mu=0.2, theta=0.5, seed=5, logmode=0)
+    E = padded(n, 16)
+    sig = torch.zeros(16, dtype=torch.float64, device=DEV)
+    lam = torch.zeros(32, dtype=torch.float64, device=DEV)
+    L.netmfp_embed(ctx, g, L.make_params(**prm), E, sig, lam)
+    ref = O.netmf_plus(n, s, t, **prm)
+    assert np.abs(lam.cpu().numpy() - ref["lam"]).max() <= 1e-3 * abs(ref["lam"][0])
+    assert np.abs(sig.cpu().numpy()[:4] - ref["sigma"][:4]).max() <= 1e-3 * ref["sigma"][0]
+    Eh = E.cpu().numpy()
+    iso = np.setdiff1d(np.arange(n), perm)
+    assert np.all(Eh[iso] == 0.0)
+    assert _match_cols_up_to_sign(Eh, ref["E"], 4) <= 1e-3
 
 
 def test_cfg2_full_size_sampled(L, ctx):
