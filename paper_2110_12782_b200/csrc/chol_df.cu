@@ -6,10 +6,10 @@
 // the critical path is ~2·nb tile steps instead of l column steps on one SM:
 //   Cholesky (L = Rᵀ, right-looking by dependencies):
 //     S_IJ = G_IJ − Σ_{K<J} L_IK L_JKᵀ      (waits for L_IK, L_JK)
-//     L_JJ = chol(S_JJ)                      (warp 0, shared memory)
-//     L_IJ = S_IJ L_JJ⁻ᵀ                     (waits for L_JJ; one row per thread)
+//     L_JJ = chol(S_JJ), X_JJ = L_JJ⁻¹       (one warp, rows in registers)
+//     L_IJ = S_IJ X_JJᵀ                      (waits for L_JJ, X_JJ; a tile GEMM)
 //   inverse X = L⁻¹ (lower):
-//     X_II = L_II⁻¹ ;  X_IJ = −X_II Σ_{K=J}^{I−1} L_IK X_KJ   (waits for X_KJ, X_II)
+//     X_IJ = −X_II Σ_{K=J}^{I−1} L_IK X_KJ    (waits for X_KJ, X_II)
 //   Rinv = Xᵀ.
 // A breakdown (pivot <= 1e-12 × original diagonal, or non-finite) raises a
 // global fail word; every CTA notices it, the grid synchronises and all tiles
@@ -131,11 +131,71 @@ __device__ void tile_add_ab(double *S, const double *A, const double *B) {
   for (int i = 0; i < 4; ++i) S[(r0 + 8 * i) * TL + c] += acc[i];
 }
 
+// OUT = A · Bᵀ  (32×32 smem tiles)
+__device__ void tile_mul_abt(double *OUT, const double *A, const double *B) {
+  const int c = threadIdx.x & 31, r0 = threadIdx.x >> 5;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+  for (int t = 0; t < 32; ++t) {
+    const double b = B[c * TL + t];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] += A[(r0 + 8 * i) * TL + t] * b;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) OUT[(r0 + 8 * i) * TL + c] = acc[i];
+}
+
+// Warp 0: S (32×32, rows >= ib identity) -> L = chol(S) (lower, in S) and
+// X = L⁻¹ (lower, in X).  Right-looking in both halves with the working row
+// (then column) in registers.  The inverse's register window shifts by one
+// row per step (w[m] = row k + m), so one rolled loop body serves every step
+// with register operands (the code runs once per tile from a cold
+// instruction cache).  Returns true on breakdown (pivot <= 1e-12 × piv[j]
+// or non-finite).
+__device__ bool warp_chol_inv(double *S, double *X, double *rinv, const double *piv, int ib) {
+  const int r = threadIdx.x & 31;
+  CDF_MARK(10);
+  double w[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) w[c] = S[r * TL + c];
+  bool bad = false;
+  // factor: fully unrolled (register row), column j of L broadcast through
+  // shared memory
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const double d = __shfl_sync(0xffffffffu, w[j], j);  // S[j][j]
+    bad |= j < ib && (!(d > 1e-12 * piv[j]) || !isfinite(d));
+    const double inv = rsqrt(fmax(d, 1e-300));
+    const double l = r >= j ? w[j] * inv : 0.0;  // L[r][j]
+    S[r * TL + j] = l;
+    if (r == j) rinv[j] = inv;  // 1 / L[j][j]
+    __syncwarp();
+#pragma unroll
+    for (int c = j + 1; c < 32; ++c) w[c] -= l * S[c * TL + j];
+  }
+  __syncwarp();
+  CDF_MARK(12);
+  // X = L⁻¹, lane r owning column r: x_k = acc_k / L[k][k], then the later
+  // rows' partial sums (w[m] = row k + m)
+#pragma unroll
+  for (int i = 0; i < 32; ++i) w[i] = i == r ? 1.0 : 0.0;
+#pragma unroll 1
+  for (int k = 0; k < 32; ++k) {
+    const double xk = w[0] * rinv[k];
+    X[k * TL + r] = xk;
+#pragma unroll
+    for (int m = 1; m < 32; ++m) w[m - 1] = w[m] - S[((k + m) & 31) * TL + k] * xk;
+  }
+  __syncwarp();
+  CDF_MARK(14);
+  return bad;
+}
+
 __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double S[32 * TL], A[32 * TL], B[32 * TL], D[32 * TL];
   __shared__ int bad;
-  __shared__ double piv[32];
+  __shared__ double piv[32], rinv[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // tile of this CTA: t -> (I, J), I >= J, column-major over the lower triangle
   int t = blockIdx.x, J = 0;
@@ -184,44 +244,25 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
     }
     CDF_MARK(4);
     if (alive && I == J) {
-      // factor the diagonal tile (warp 0), rows beyond ib are identity padding
-      if (threadIdx.x == 0) bad = 0;
-      __syncthreads();
-      CDF_MARK(10);
-      // unnormalised right-looking elimination, all threads, one barrier per pivot:
-      // after step j column j holds s_rj and L_rj = s_rj / sqrt(s_jj)
-      if (threadIdx.x < 32 && threadIdx.x >= ib)
-        for (int cc = 0; cc < 32; ++cc) S[threadIdx.x * TL + cc] = (cc == (int)threadIdx.x) ? 1.0 : 0.0;
-      if (threadIdx.x < 32)
+      // factor and invert the diagonal tile (warp 0); rows beyond ib are identity padding
+      if (threadIdx.x < 32) {
+        for (int cc = 0; cc < 32; ++cc)
+          if ((int)threadIdx.x >= ib) S[threadIdx.x * TL + cc] = (cc == (int)threadIdx.x) ? 1.0 : 0.0;
         piv[threadIdx.x] = (int)threadIdx.x < ib
                                ? __ldcg(p.G0 + (int64_t)(32 * I + threadIdx.x) * p.l + 32 * I + threadIdx.x) + shift
                                : 1.0;
-      __syncthreads();
-      for (int j = 0; j < 32; ++j) {
-        const double d = S[j * TL + j];
-        if (threadIdx.x == 0 && j < ib && (!(d > 1e-12 * piv[j]) || !isfinite(d))) bad = 1;
-        const double inv = 1.0 / fmax(d, 1e-300);
-        for (int e = threadIdx.x; e < 32 * 32; e += T) {
-          const int r = e >> 5, cc = e & 31;
-          if (cc > j && r >= cc) S[r * TL + cc] -= S[r * TL + j] * S[cc * TL + j] * inv;
-        }
-        __syncthreads();
+        __syncwarp();
+        const bool b = warp_chol_inv(S, D, rinv, piv, ib);
+        if (threadIdx.x == 0) bad = b;
       }
       __syncthreads();
-      if (threadIdx.x < 32) piv[threadIdx.x] = rsqrt(fmax(S[threadIdx.x * TL + threadIdx.x], 1e-300));
-      __syncthreads();
-      for (int e = threadIdx.x; e < 32 * 32; e += T) {
-        const int r = e >> 5, cc = e & 31;
-        S[r * TL + cc] = (r >= cc) ? S[r * TL + cc] * piv[cc] : 0.0;  // diagonal: s_cc/sqrt(s_cc)
-      }
       CDF_MARK(11);
-      __syncthreads();
-      CDF_MARK(12);
       if (bad) {
         if (threadIdx.x == 0) atomicMax(p.fail, want);
         alive = false;
       } else {
         store_tile(p.G, p.ld, S, 32 * I, 32 * I, ib, ib);
+        store_tile(p.Rinv, p.l, D, 32 * I, 32 * I, ib, ib);  // X_II for the L_IJ GEMMs and the inverse
         CDF_MARK(13);
         publish(p.lflag + I * p.nb + I, want);
         CDF_MARK(7);
@@ -229,20 +270,11 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
     } else if (alive) {
       alive = wait_flag(p, p.lflag + J * p.nb + J, want, attempt);
       if (alive) {
-        load_tile(D, p.G, p.ld, 32 * J, 32 * J, jb, jb);
+        load_tile(D, p.Rinv, p.l, 32 * J, 32 * J, jb, jb);  // X_JJ
         __syncthreads();
-        // L_IJ = S L_JJ⁻ᵀ by column elimination, one barrier per column
-        for (int cc = 0; cc < jb; ++cc) {
-          if (threadIdx.x < 32) S[threadIdx.x * TL + cc] /= D[cc * TL + cc];
-          __syncthreads();
-          for (int e = threadIdx.x; e < 32 * 32; e += T) {
-            const int r = e >> 5, c2 = e & 31;
-            if (c2 > cc && c2 < jb) S[r * TL + c2] -= S[r * TL + cc] * D[c2 * TL + cc];
-          }
-          __syncthreads();
-        }
+        tile_mul_abt(A, S, D);  // L_IJ = S_IJ X_JJᵀ
         __syncthreads();
-        store_tile(p.G, p.ld, S, 32 * I, 32 * J, ib, jb);
+        store_tile(p.G, p.ld, A, 32 * I, 32 * J, ib, jb);
         publish(p.lflag + I * p.nb + J, want);
         CDF_MARK(7);
       }
@@ -260,24 +292,7 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
   // ---- inverse: X = L⁻¹
   const int want = 1;
   if (I == J) {
-    load_tile(A, p.G, p.ld, 32 * I, 32 * I, ib, ib);
-    __syncthreads();
-    // X_II = L_II⁻¹ by forward elimination on the identity, one barrier per row
-    for (int e = threadIdx.x; e < 32 * 32; e += T) D[(e >> 5) * TL + (e & 31)] = ((e >> 5) == (e & 31)) ? 1.0 : 0.0;
-    __syncthreads();
-    for (int rr = 0; rr < ib; ++rr) {
-      if (threadIdx.x < 32) D[rr * TL + threadIdx.x] /= A[rr * TL + rr];
-      __syncthreads();
-      for (int e = threadIdx.x; e < 32 * 32; e += T) {
-        const int r = e >> 5, c2 = e & 31;
-        if (r > rr && r < ib) D[r * TL + c2] -= A[r * TL + rr] * D[rr * TL + c2];
-      }
-      __syncthreads();
-    }
-    for (int e = threadIdx.x; e < 32 * 32; e += T)
-      if ((e >> 5) >= ib || (e & 31) >= ib) D[(e >> 5) * TL + (e & 31)] = 0.0;
-    __syncthreads();
-    store_tile(p.Rinv, p.l, D, 32 * I, 32 * I, ib, ib);
+    // X_II = L_II⁻¹ was stored by the factorisation
     publish(p.xflag + I * p.nb + I, want);
   } else {
     for (int i = threadIdx.x; i < 32 * TL; i += T) S[i] = 0.0;

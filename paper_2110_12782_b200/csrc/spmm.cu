@@ -423,11 +423,20 @@ void spmm(Ctx &c, const Graph &g, const SpmmArgs &p_in) {
   // 128-column passes with a warp per row; the leftover columns (286 = 2·128
   // + 30) as one more launch with narrower lane groups (4 or 2 rows per warp
   // at a time) instead of a mostly idle 128-column pass
-  const int64_t main = p.cols / 128 * 128, tail = p.cols - main;
+  static const int pass_w = [] {
+    const char *v = getenv("NETMFP_SPMM_W");
+    return v ? atoi(v) : 128;
+  }();
+  const int64_t main = p.cols / pass_w * pass_w, tail = p.cols - main;
   if (main > 0) {
     SpmmArgs pm = p;
     pm.cols = main;
-    spmm_fused_impl<32>(c, g, pm);
+    if (pass_w == 64)
+      spmm_fused_impl<16>(c, g, pm);
+    else if (pass_w == 32)
+      spmm_fused_impl<8>(c, g, pm);
+    else
+      spmm_fused_impl<32>(c, g, pm);
   }
   if (tail > 0) {
     SpmmArgs pt = p;

@@ -27,10 +27,17 @@ int main() {
     for (int b = 0; b < 45; ++b) t0 = std::min(t0, t[b * 16]);
     double mx[7] = {};
     for (int b = 0; b < 45; ++b) for (int i = 0; i < 7; ++i) mx[i] = std::max(mx[i], (double)(t[b * 16 + i] - t0));
-    for (int b : {0, 9}) {
-      printf("tile %d:", b);
-      for (int i : {8, 9, 10, 11, 12, 13, 7}) printf(" m%d=%.2f", i, (t[b * 16 + i] - t0) / 1e3);
-      printf("\n");
+    if (rep == 2) {
+      const int nb = 9;
+      int base = 0;
+      for (int J = 0; J < nb; ++J) {
+        const int d = base, o = base + 1;  // (J,J) and (J+1,J)
+        printf("   m9 %.2f m10 %.2f m12 %.2f m14 %.2f m11 %.2f\n", (t[d*16+9]-t0)/1e3, (t[d*16+10]-t0)/1e3, (t[d*16+12]-t0)/1e3, (t[d*16+14]-t0)/1e3, (t[d*16+11]-t0)/1e3);
+        printf("J=%d diag: upd_done %.2f fact_done %.2f pub %.2f | offdiag(J+1,J): upd_done %.2f pub %.2f\n", J,
+               (t[d * 16 + 4] - t0) / 1e3, (t[d * 16 + 11] - t0) / 1e3, (t[d * 16 + 7] - t0) / 1e3,
+               J + 1 < nb ? (t[o * 16 + 4] - t0) / 1e3 : 0.0, J + 1 < nb ? (t[o * 16 + 7] - t0) / 1e3 : 0.0);
+        base += nb - J;
+      }
     }
     printf("\n%.3f ms %s | max over CTAs (us): start %.1f g0sync %.1f chol %.1f sync %.1f inv %.1f sync %.1f end %.1f\n", ms,
            cudaGetErrorString(cudaGetLastError()), mx[0] / 1e3, mx[1] / 1e3, mx[2] / 1e3, mx[3] / 1e3, mx[4] / 1e3,
