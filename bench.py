@@ -40,6 +40,21 @@ def load_peaks():
     return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, sm_max=1965.0, src="fallback")
 
 
+def gather_roofline(achieved_tbps):
+    """Achieved neighbour-row gather throughput vs the measured random-gather
+    peaks (profiles/r01_traffic.json, from scripts/dbg/gather_bench.cu)."""
+    out = {"achieved_TBps": achieved_tbps, "unit": "TB/s (gathered X bytes: 4 * nnz * cols per SpMM)"}
+    tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tp):
+        gr = json.load(open(tp)).get("gather_roofline", {})
+        if gr:
+            out["peak_l2_resident_TBps"] = gr["l2_resident_TBps"]
+            out["peak_table_208MB_TBps"] = gr["table_208MB_TBps"]
+            out["frac_of_l2_resident_peak"] = achieved_tbps / gr["l2_resident_TBps"]
+            out["source"] = gr["source"]
+    return out
+
+
 def workload(idx):
     from paper_2110_12782_b200 import inputs
     w = inputs.CONFIGS[idx]
@@ -303,6 +318,9 @@ def run_ours(args):
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peaks['src']})",
                 "share_of_step": per_step_ms / ms,
                 "edge_cols_per_s": (n_spmm_l * nnz * l + n_spmm_d * nnz * d) / (per_step_ms * 1e-3),
+                # the resource that binds this SpMM: every nonzero brings its
+                # neighbour's row slice into an SM (16 B per lane, L1/L2)
+                "gather": gather_roofline(4.0 * (n_spmm_l * nnz * l + n_spmm_d * nnz * d) / (per_step_ms * 1e-3) / 1e12),
                 "launches_per_step": sum(v[0] for k, v in prof.items() if k.startswith("spmm")) / args.steps}
     else:
         kms = sum(v[1] for k, v in prof.items()) / args.steps

@@ -319,14 +319,19 @@ __device__ __forceinline__ void fused_body(const SpmmArgs &p, int py, int bx, co
     const float4 acc = gather_sum<false>(col, e0, e1, p.X + c, (uint32_t)p.ldx, nullptr);
     atomicAdd(reinterpret_cast<float4 *>(dst), acc);
   }
-  __threadfence();
+  // the group's atomics are ordered before the arrival by the group barrier
+  // and the leader's gpu-scope fence (cumulativity); the leader fences again
+  // after seeing the last arrival, before the group reads the sums
   __syncwarp(gmask);
   int32_t *cnt = hcnt + h * cnt_stride + py;
   int last = 0;
-  if (li == 0) last = atomicAdd(cnt, 1) == (int)(__ldg(seg_ptr + h + 1) - __ldg(seg_ptr + h)) - 1;
+  if (li == 0) {
+    __threadfence();
+    last = atomicAdd(cnt, 1) == (int)(__ldg(seg_ptr + h + 1) - __ldg(seg_ptr + h)) - 1;
+    if (last) __threadfence();
+  }
   last = __shfl_sync(gmask, last, lane / LPR * LPR);
   if (!last) return;
-  __threadfence();
   if (active) {
     const float4 acc = __ldcg(reinterpret_cast<const float4 *>(dst));
     __stcg(reinterpret_cast<float4 *>(dst), make_float4(0.f, 0.f, 0.f, 0.f));
