@@ -525,7 +525,7 @@ static void embed_impl(Ctx &c, const Graph &g_in, const netmfp_params &p, const 
     NM_STAGE(c, "stage_propagate");
     propagate(c, g, E, p.prop_order, p.mu, p.theta);                   // step 6
   }
-  if (compacted) scatter_rows(c, E, g.orig_id.p, E_out);             // isolated vertices: zero rows [R2]
+  if (compacted) scatter_rows(c, E, g.comp_id.p, E_out);             // isolated vertices: zero rows [R2]
 }
 
 int netmfp_embed(netmfp_ctx *ctx, const netmfp_graph *gr, const netmfp_params *p, float *E, int64_t lde,

@@ -214,7 +214,9 @@ inline int64_t pad4(int64_t c) { return (c + 3) / 4 * 4; }
 inline int64_t pad32(int64_t c) { return (c + 31) / 32 * 32; }
 
 // Owned dense fp32 block with ld padded to a multiple of 32 floats (128 B rows
-// segments) and zeroed padding.
+// segments) and zeroed padding columns (contractions read whole 32-column
+// chunks; the cols x rows interior is always written by its producer before
+// it is read, so it is not cleared).
 struct Block {
   DBuf<float> buf;
   Mat m;
@@ -223,7 +225,8 @@ struct Block {
   void alloc(int64_t rows, int64_t cols, cudaStream_t s) {
     int64_t ld = pad32(cols);
     buf.alloc((size_t)rows * ld, s);
-    buf.zero();
+    if (rows > 0 && ld > cols)
+      NM_CUDA(cudaMemset2DAsync(buf.p + cols, ld * sizeof(float), 0, (ld - cols) * sizeof(float), rows, s));
     m.p = buf.p;
     m.rows = rows;
     m.cols = cols;

@@ -238,26 +238,33 @@ void gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, const 
 // ---------------------------------------------------------------------------
 // Ω = randn(n, l) (Alg. 2 step 2) with Philox4x32-10 [R1], optional row scale
 // ---------------------------------------------------------------------------
-__global__ void k_gaussian(Mat O, uint32_t k0, uint32_t k1, const int32_t *__restrict__ deg,
-                           float rexp, int64_t row0, const int32_t *__restrict__ ids) {
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= O.rows * O.cols) return;
-  int64_t i = idx / O.cols, j = idx % O.cols;
-  // global row: every rank (or compacted graph) draws its own rows of the same Ω
-  const int64_t gi = ids ? (int64_t)ids[i] : i + row0;
-  U4 ctr{(uint32_t)j, (uint32_t)(gi & 0xFFFFFFFF), (uint32_t)((uint64_t)gi >> 32), kTagOmega};
-  U4 w = philox4x32_10(ctr, k0, k1);
-  // Box–Muller in fp32 (the block is fp32; |error| ~1e-7 relative to the fp64 oracle)
-  const float u0 = ((float)w.x + 0.5f) * 2.3283064365386963e-10f;  // 2^-32
-  const float u1 = ((float)w.y + 0.5f) * 2.3283064365386963e-10f;
-  const float g = sqrtf(-2.f * logf(u0)) * cospif(2.f * u1);
-  O.p[i * O.ld + j] = g * dpow_scale(deg, i, rexp);
+// A warp per row (grid-stride over rows), lanes over 32 consecutive columns:
+// the row's id and scale d^-e are computed once per row, not per element.
+__global__ void __launch_bounds__(256) k_gaussian(Mat O, uint32_t k0, uint32_t k1, const int32_t *__restrict__ deg,
+                                                  float rexp, int64_t row0, const int32_t *__restrict__ ids) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < O.rows; i += nw) {
+    // global row: every rank (or compacted graph) draws its own rows of the same Ω
+    const int64_t gi = ids ? (int64_t)ids[i] : i + row0;
+    const float sc = dpow_scale(deg, i, rexp);
+    float *orow = O.p + i * O.ld;
+    for (int64_t j = lane; j < O.cols; j += 32) {
+      const U4 w = philox4x32_10(U4{(uint32_t)j, (uint32_t)(gi & 0xFFFFFFFF), (uint32_t)((uint64_t)gi >> 32), kTagOmega},
+                                 k0, k1);
+      // Box–Muller in fp32 (the block is fp32; |error| ~1e-7 relative to the fp64 oracle)
+      const float u0 = ((float)w.x + 0.5f) * 2.3283064365386963e-10f;  // 2^-32
+      const float u1 = ((float)w.y + 0.5f) * 2.3283064365386963e-10f;
+      orow[j] = sqrtf(-2.f * logf(u0)) * cospif(2.f * u1) * sc;
+    }
+  }
 }
 
 void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, float rexp, int64_t row0,
                     const int32_t *ids) {
   if (O.rows * O.cols == 0) return;
-  NM_LAUNCH(c, "gaussian", k_gaussian<<<ceil_div(O.rows * O.cols, 256), 256, 0, c.stream>>>(
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(O.rows, 8), (int64_t)c.num_sms * 16);
+  NM_LAUNCH(c, "gaussian", k_gaussian<<<blocks, 256, 0, c.stream>>>(
       O, (uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32), deg, rexp, row0, ids));
 }
 
@@ -300,18 +307,23 @@ void copy_block(Ctx &c, const float *src, int64_t lds, float *dst, int64_t ldd, 
   NM_CUDA(cudaMemcpy2DAsync(dst, ldd * 4, src, lds * 4, cols * 4, rows, cudaMemcpyDefault, c.stream));
 }
 
-// Dst = 0 except Dst[ids[i], :] = Src[i, :]  (compacted rows back to all rows)
-__global__ void k_scatter_rows(Mat Src, const int32_t *__restrict__ ids, Mat Dst) {
-  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= Src.rows * Src.cols) return;
-  const int64_t i = idx / Src.cols, j = idx % Src.cols;
-  Dst.p[(int64_t)ids[i] * Dst.ld + j] = Src.p[i * Src.ld + j];
+// Dst[i, :] = Src[comp[i], :], or 0 where comp[i] < 0 (compacted rows back
+// to all rows; every element of Dst written once).  A warp per row.
+__global__ void __launch_bounds__(256) k_scatter_rows(Mat Src, const int32_t *__restrict__ comp, Mat Dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  for (int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < Dst.rows; i += nw) {
+    const int32_t r = comp[i];
+    float *d = Dst.p + i * Dst.ld;
+    const float *src = Src.p + (int64_t)(r < 0 ? 0 : r) * Src.ld;
+    for (int64_t j = lane; j < Dst.cols; j += 32) d[j] = r >= 0 ? src[j] : 0.f;
+  }
 }
 
-void scatter_rows(Ctx &c, const Mat &Src, const int32_t *ids, const Mat &Dst) {
-  NM_CUDA(cudaMemset2DAsync(Dst.p, Dst.ld * 4, 0, Dst.cols * 4, Dst.rows, c.stream));
-  if (Src.rows * Src.cols == 0) return;
-  NM_LAUNCH(c, "scatter_rows", k_scatter_rows<<<ceil_div(Src.rows * Src.cols, 256), 256, 0, c.stream>>>(Src, ids, Dst));
+void scatter_rows(Ctx &c, const Mat &Src, const int32_t *comp, const Mat &Dst) {
+  if (Dst.rows * Dst.cols == 0) return;
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(Dst.rows, 8), (int64_t)c.num_sms * 16);
+  NM_LAUNCH(c, "scatter_rows", k_scatter_rows<<<blocks, 256, 0, c.stream>>>(Src, comp, Dst));
 }
 
 }  // namespace netmfp

@@ -72,8 +72,8 @@ void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, flo
 void scale_copy_block(Ctx &c, const Mat &Src, const Mat &Dst, const int32_t *deg, float rexp);
 // Y[i, :] *= d_i^-e
 void row_scale_block(Ctx &c, const Mat &Y, const int32_t *deg, float rexp);
-// Dst (all rows) = 0 except Dst[ids[i], :] = Src[i, :]
-void scatter_rows(Ctx &c, const Mat &Src, const int32_t *ids, const Mat &Dst);
+// Dst[i, :] = Src[comp[i], :] (0 where comp[i] < 0)
+void scatter_rows(Ctx &c, const Mat &Src, const int32_t *comp, const Mat &Dst);
 // copy with ld conversion (device-to-device)
 void copy_block(Ctx &c, const float *src, int64_t lds, float *dst, int64_t ldd, int64_t rows,
                 int64_t cols);

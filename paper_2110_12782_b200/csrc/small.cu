@@ -48,47 +48,64 @@ __device__ double block_sum(double v, double *red) {
 // ---------------------------------------------------------------------------
 // gemm64: C = alpha op(A) op(B) + beta C
 // ---------------------------------------------------------------------------
+// 32×32 output tile per 256-thread CTA (2×2 per thread), K in steps of 32
+// with the next step's operands prefetched into registers while the current
+// one is consumed from shared memory (small l×l problems: the grid, not the
+// FMA rate, is what limits them, so tiles are small and many).
 __global__ void __launch_bounds__(256) k_gemm64(bool ta, bool tb, int64_t M, int64_t N, int64_t K,
                                                 double alpha, const double *__restrict__ A, int64_t lda,
                                                 const double *__restrict__ B, int64_t ldb, double beta,
                                                 double *__restrict__ C, int64_t ldc) {
-  __shared__ double As[16][65];
-  __shared__ double Bs[16][65];
+  __shared__ double As[32][33];  // [k][m]
+  __shared__ double Bs[32][33];  // [k][n]
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  const int64_t m0 = (int64_t)blockIdx.y * 64, n0 = (int64_t)blockIdx.x * 64;
-  double acc[4][4] = {};
-  for (int64_t k0 = 0; k0 < K; k0 += 16) {
-    for (int idx = threadIdx.x; idx < 16 * 64; idx += 256) {
-      int kk = idx / 64, mm = idx % 64;
-      int64_t gm = m0 + mm, gk = k0 + kk;
-      double a = 0.0;
-      if (gm < M && gk < K) a = ta ? A[gk * lda + gm] : A[gm * lda + gk];
-      As[kk][mm] = a;
-      int64_t gn = n0 + mm;
-      double b = 0.0;
-      if (gn < N && gk < K) b = tb ? B[gn * ldb + gk] : B[gk * ldb + gn];
-      Bs[kk][mm] = b;
+  const int64_t m0 = (int64_t)blockIdx.y * 32, n0 = (int64_t)blockIdx.x * 32;
+  // loader mapping: 4 elements of A and 4 of B per thread per K step
+  double ra[4], rb[4];
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = threadIdx.x + 256 * q;  // 0..1023 over a 32×32 tile
+      int kk, mm;
+      if (ta) { mm = idx % 32; kk = idx / 32; } else { kk = idx % 32; mm = idx / 32; }  // coalesced source
+      const int64_t gm = m0 + mm, gk = k0 + kk;
+      ra[q] = (gm < M && gk < K) ? (ta ? A[gk * lda + gm] : A[gm * lda + gk]) : 0.0;
+      int nn;
+      if (tb) { kk = idx % 32; nn = idx / 32; } else { nn = idx % 32; kk = idx / 32; }
+      const int64_t gn = n0 + nn, gk2 = k0 + kk;
+      rb[q] = (gn < N && gk2 < K) ? (tb ? B[gn * ldb + gk2] : B[gk2 * ldb + gn]) : 0.0;
     }
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = threadIdx.x + 256 * q;
+      if (ta) As[idx / 32][idx % 32] = ra[q]; else As[idx % 32][idx / 32] = ra[q];
+      if (tb) Bs[idx % 32][idx / 32] = rb[q]; else Bs[idx / 32][idx % 32] = rb[q];
+    }
+  };
+  double acc[2][2] = {};
+  load(0);
+  for (int64_t k0 = 0; k0 < K; k0 += 32) {
+    stash();
     __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      double a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    if (k0 + 32 < K) load(k0 + 32);
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) {
+      const double a0 = As[kk][ty], a1 = As[kk][ty + 16];
+      const double b0 = Bs[kk][tx], b1 = Bs[kk][tx + 16];
+      acc[0][0] = fma(a0, b0, acc[0][0]);
+      acc[0][1] = fma(a0, b1, acc[0][1]);
+      acc[1][0] = fma(a1, b0, acc[1][0]);
+      acc[1][1] = fma(a1, b1, acc[1][1]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int64_t gm = m0 + ty + 16 * i, gn = n0 + tx + 16 * j;
+    for (int j = 0; j < 2; ++j) {
+      const int64_t gm = m0 + ty + 16 * i, gn = n0 + tx + 16 * j;
       if (gm < M && gn < N) {
         double *c = C + gm * ldc + gn;
         *c = alpha * acc[i][j] + (beta != 0.0 ? beta * *c : 0.0);
@@ -99,7 +116,7 @@ __global__ void __launch_bounds__(256) k_gemm64(bool ta, bool tb, int64_t M, int
 void gemm64(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
             int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc) {
   if (M <= 0 || N <= 0) return;
-  dim3 grid(ceil_div(N, 64), ceil_div(M, 64));
+  dim3 grid(ceil_div(N, 32), ceil_div(M, 32));
   NM_LAUNCH(c, "gemm64", k_gemm64<<<grid, 256, 0, c.stream>>>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc));
 }
 
