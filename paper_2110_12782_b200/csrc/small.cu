@@ -519,12 +519,34 @@ void tri_inv_upper(Ctx &c, const double *R, int64_t ld, double *Rinv, int64_t l)
 // ---------------------------------------------------------------------------
 // symmetric eigensolver
 // ---------------------------------------------------------------------------
+#ifdef TD_PROF
+__device__ unsigned long long g_td_t[8][4][512];
+#define TD_MARK(ph)                                                        \
+  do {                                                                     \
+    if (threadIdx.x == 0 && j < 512) {                                     \
+      unsigned long long _t;                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));               \
+      g_td_t[rank][ph][j] = _t;                                            \
+    }                                                                      \
+  } while (0)
+#else
+#define TD_MARK(ph)
+#endif
 constexpr int TDC = 8;     // cluster size (CTAs) for the tridiagonalisation
 constexpr int TDT = 512;   // threads per CTA
 
 // Householder tridiagonalisation Qᵀ S Q = T, Q = H_0 … H_{l-3}, H_j = I - beta_j v_j v_jᵀ
 // (v_j non-zero on indices j+1..l-1, stored in row j of Hv).  Row i of S lives in
-// CTA i % TDC of the cluster (local row i / TDC).
+// CTA i % TDC of the cluster (local row i / TDC).  Step j, with p = beta A v and
+// K = beta vᵀp / 2:  A -= v pᵀ + p vᵀ - 2K v vᵀ  (= v wᵀ + w vᵀ, w = p - K v).
+// Every exchange is a PUSH into the other CTAs' shared memory (remote stores,
+// no remote loads on the critical path) and a step costs two cluster barriers:
+//   S1: the owner of row j has pushed v_j and beta_j;
+//   S2: every CTA has pushed its rows' p_i and its partial vᵀp.
+// v and beta (pushed before S1) are double-buffered by step parity: a buffer
+// is rewritten two steps later, after every CTA has passed the barrier that
+// follows its last read.  p and the partials are pushed after S1 of the next
+// step, which every CTA reaches only after finishing this step's update.
 __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
     k_tridiag(const double *__restrict__ S, int l, double *__restrict__ dd, double *__restrict__ ee,
               double *__restrict__ Hv, double *__restrict__ hbeta) {
@@ -537,97 +559,89 @@ __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
   // rank to rank), sized for the largest per-rank row count
   const int nmax = (l + TDC - 1) / TDC;
   extern __shared__ double sm[];
-  double *A = sm;                         // nmax × l (first nloc rows used)
-  double *vfull = A + (int64_t)nmax * l;  // l
-  double *wfull = vfull + l;              // l  (own rows' w at their global index)
-  double *pl = wfull + l;                 // nmax
-  double *red = pl + nmax;                // 33
-  double *xchg = red + 40;                // [0] partial vᵀp, [1] beta
+  double *A = sm;                          // nmax × l (first nloc rows used)
+  double *vbuf = A + (int64_t)nmax * l;    // 2 × l
+  double *pf = vbuf + 2 * l;               // l
+  double *pl = pf + l;                     // nmax
+  double *red = pl + nmax;                 // 40
+  double *xchg = red + 40;                 // [parity][TDC] partials, [16 + parity] beta
   for (int64_t idx = tid; idx < (int64_t)nloc * l; idx += nt) {
     int li = (int)(idx / l), k = (int)(idx % l);
     A[idx] = S[(int64_t)(li * TDC + rank) * l + k];
   }
   cl.sync();
   for (int j = 0; j + 2 < l; ++j) {
-    const int owner = j % TDC;
-    // (1) owner: reflector from row j, entries j+1..l-1
+    const int owner = j % TDC, par = j & 1;
+    double *v = vbuf + par * l;
+    TD_MARK(0);
+    // (1) owner: reflector from row j (entries j+1..l-1), pushed to every CTA
     if (rank == owner) {
       const double *x = A + (int64_t)(j / TDC) * l;
       double ss = 0.0;
       for (int k = j + 2 + tid; k < l; k += nt) ss += x[k] * x[k];
       ss = block_sum<TDT>(ss, red);
       const double x0 = x[j + 1];
-      double beta = 0.0, alpha = x0;
+      double beta = 0.0, alpha = x0, v0 = 0.0;
       if (ss > 0.0) {
-        double nrm = sqrt(ss + x0 * x0);
+        const double nrm = sqrt(ss + x0 * x0);
         alpha = x0 >= 0 ? -nrm : nrm;
-        double v0 = x0 - alpha;
+        v0 = x0 - alpha;
         beta = 2.0 / (ss + v0 * v0);
-        for (int k = j + 1 + tid; k < l; k += nt) vfull[k] = (k == j + 1) ? v0 : x[k];
-      } else {
-        for (int k = j + 1 + tid; k < l; k += nt) vfull[k] = 0.0;
       }
+      for (int k = j + 1 + tid; k < l; k += nt) {
+        const double val = ss > 0.0 ? (k == j + 1 ? v0 : x[k]) : 0.0;
+#pragma unroll
+        for (int r = 0; r < TDC; ++r) cl.map_shared_rank(v, r)[k] = val;
+        Hv[(int64_t)j * l + k] = val;
+      }
+      if (tid < TDC) cl.map_shared_rank(xchg, tid)[16 + par] = beta;
       if (tid == 0) {
-        xchg[1] = beta;
         dd[j] = x[j];
         ee[j] = alpha;
         hbeta[j] = beta;
       }
-      __syncthreads();
-      for (int k = j + 1 + tid; k < l; k += nt) Hv[(int64_t)j * l + k] = vfull[k];
     }
+    TD_MARK(1);
     cl.sync();  // S1
-    double beta;
-    if (rank != owner) {
-      double *rv = cl.map_shared_rank(vfull, owner);
-      double *rx = cl.map_shared_rank(xchg, owner);
-      for (int k = j + 1 + tid; k < l; k += nt) vfull[k] = rv[k];
-      beta = rx[1];
-    } else {
-      beta = xchg[1];
-    }
-    __syncthreads();
-    // (2) p_i = beta * A[i, j+1:] · v for own rows i > j; partial vᵀp
+    TD_MARK(2);
+    const double beta = xchg[16 + par];
+    // (2) p_i = beta A[i, j+1:] · v for own rows i > j; partial vᵀp
     double part = 0.0;
     for (int li = wid; li < nloc; li += nt / 32) {
       const int i = li * TDC + rank;
       if (i <= j) continue;
       const double *Ai = A + (int64_t)li * l;
-      double s = 0.0;
-      for (int k = j + 1 + ln; k < l; k += 32) s += Ai[k] * vfull[k];
-      s = warp_sum(s) * beta;
+      double sacc = 0.0;
+      for (int k = j + 1 + ln; k < l; k += 32) sacc += Ai[k] * v[k];
+      sacc = warp_sum(sacc) * beta;
       if (ln == 0) {
-        pl[li] = s;
-        part += s * vfull[i];
+        pl[li] = sacc;
+        part += sacc * v[i];
       }
     }
-    part = block_sum<TDT>(part, red);
-    if (tid == 0) xchg[0] = part;
-    cl.sync();  // S2
-    double K = 0.0;
-    for (int r = 0; r < TDC; ++r) K += *cl.map_shared_rank(xchg, r);
-    K *= 0.5 * beta;
-    // (3) w_i = p_i - K v_i (own rows)
-    for (int li = tid; li < nloc; li += nt) {
+    part = block_sum<TDT>(part, red);  // (its barriers also publish pl)
+    // (3) push own p_i and the partial to every CTA
+    for (int q = tid; q < nloc * TDC; q += nt) {
+      const int li = q / TDC, r = q % TDC;
       const int i = li * TDC + rank;
-      if (i > j) wfull[i] = pl[li] - K * vfull[i];
+      if (i > j) cl.map_shared_rank(pf, r)[i] = pl[li];
     }
-    cl.sync();  // S3
-    // (4) gather w for k > j from the owners, then A_i -= v_i w + w_i v
-    for (int k = j + 1 + tid; k < l; k += nt) {
-      const int r = k % TDC;
-      if (r != rank) wfull[k] = cl.map_shared_rank(wfull, r)[k];
-    }
-    __syncthreads();
+    if (tid < TDC) cl.map_shared_rank(xchg, tid)[par * TDC + rank] = part;
+    TD_MARK(3);
+    cl.sync();  // S2
+    double vtp = 0.0;
+#pragma unroll
+    for (int r = 0; r < TDC; ++r) vtp += xchg[par * TDC + r];
+    const double K2 = vtp * beta;  // 2K
+    // (4) A_i -= v_i p + p_i v - 2K v_i v  (own rows i > j, columns > j)
     for (int li = wid; li < nloc; li += nt / 32) {
       const int i = li * TDC + rank;
       if (i <= j) continue;
       double *Ai = A + (int64_t)li * l;
-      const double vi = vfull[i], wi = wfull[i];
-      for (int k = j + 1 + ln; k < l; k += 32) Ai[k] -= vi * wfull[k] + wi * vfull[k];
+      const double vi = v[i], pi = pf[i], ci = pi - K2 * vi;
+      for (int k = j + 1 + ln; k < l; k += 32) Ai[k] -= vi * pf[k] + ci * v[k];
     }
-    // CTA barrier: the next owner reads its freshly updated row and rewrites
-    // vfull; remote wfull reads are ordered by the next step's S1/S2
+    // CTA barrier: the next owner reads its freshly updated row
     __syncthreads();
   }
   // trailing 2×2 (or 1×1)
@@ -921,11 +935,11 @@ void sym_eig(Ctx &c, double *S, int64_t l64, double *lam, double *V, bool abs_or
   NM_CUDA(cudaMemsetAsync(hb.p, 0, (size_t)l * 8, s));
   NM_CUDA(cudaMemsetAsync(e.p, 0, (size_t)l * 8, s));
   const int nloc = (l + TDC - 1) / TDC;
-  size_t smem = ((size_t)nloc * l + 2 * l + nloc + 48) * sizeof(double);
-  NM_REQUIRE(smem <= 220 * 1024, "sym_eig: l too large for the 8-CTA cluster (l <= ~460)");
+  size_t smem = ((size_t)nloc * l + 3 * l + nloc + 40 + 24) * sizeof(double);
+  NM_REQUIRE(smem <= 227 * 1024, "sym_eig: l too large for the 8-CTA cluster (l <= ~470)");
   static bool attr = false;
   if (!attr) {
-    NM_CUDA(cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    NM_CUDA(cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
   NM_LAUNCH(c, "tridiag", k_tridiag<<<TDC, TDT, smem, s>>>(S, l, d, e, Hv, hb));
