@@ -254,7 +254,7 @@ def run_ours(args):
     ctx.profile(False)
     tot_by = {}
     for k, (c, ms) in prof_all.items():
-        if k.startswith("stage_"):
+        if k.startswith("stage_") or k == "gaps":
             continue
         tot_by[k] = tot_by.get(k, 0.0) + ms
     g = L.netmfp_build_csr(ctx, n, src, dst)

@@ -118,6 +118,29 @@ inline void launched(Ctx &c, const char *what) {
 
 // fold finished intervals into per-kernel (count, total ms); stream must be idle
 inline void prof_collect(Ctx &c) {
+  // "gaps": stream time between consecutive profiled kernels (memsets,
+  // copies, host synchronisation and launch latency) when all are profiled
+  cudaEvent_t prev_end = nullptr;
+  double gap_ms = 0.0;
+  for (auto &pe : c.pending) {
+    if (std::string(pe.name).compare(0, 6, "stage_") == 0) continue;
+    if (prev_end) {
+      float g = 0.f;
+      cudaEventElapsedTime(&g, prev_end, pe.a);
+      gap_ms += g;
+    }
+    prev_end = pe.b;
+  }
+  if (prev_end && c.prof_filter.empty()) {
+    bool found = false;
+    for (auto &s : c.stats)
+      if (s.first == "gaps") {
+        s.second.first += 1;
+        s.second.second += gap_ms;
+        found = true;
+      }
+    if (!found) c.stats.push_back({"gaps", {1, gap_ms}});
+  }
   for (auto &pe : c.pending) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, pe.a, pe.b);

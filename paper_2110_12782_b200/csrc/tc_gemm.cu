@@ -298,7 +298,9 @@ struct GemmP {
   int K;          // contraction length
   int nk;         // K chunks of 32
   int ntot;       // MMA N total (multiple of 16)
-  int nh, hr;     // output columns split into nh parts of hr (<= 256) columns
+  int nh, hr;     // output columns split into nh parts of hr (multiple of 32, <= 192) columns
+  int c16;        // output columns rounded up to 16 (the last part is c16 - (nh-1) hr wide)
+  int bsplit;     // 1: Bᵀ raw fp32, lo formed in shared memory; 0: hi / lo from the host layout
   int tri;        // B upper triangular: chunk kb touches columns >= 32 kb
   int64_t nitems; // (M tile, part) work items
   int stages;     // shared-memory ring (A raw + Bᵀ part)
@@ -319,20 +321,22 @@ struct GemmP {
 // TMEM columns: acc[0] [0, hr), acc[1] [hr, 2hr), A stage s [2hr + 64s, +64).
 constexpr int NTG = 320;  // 10 warps: TMA, MMA, 4 split, 4 epilogue
 __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUtensorMap tmA,
-                                                    const __grid_constant__ CUtensorMap tmBh, const GemmP p) {
+                                                    const __grid_constant__ CUtensorMap tmBh,
+                                                    const __grid_constant__ CUtensorMap tmC, const GemmP p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = align1024(smem_raw);
   constexpr int ABYTES = 128 * 128;  // 128 rows × 32 fp32 (raw, SWIZZLE_128B)
   const int bbytes = p.hr * 128;     // one part of Bᵀ (hi or lo)
   const int stage_bytes = ABYTES + 2 * bbytes;
   const int S = p.stages;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(base + S * stage_bytes);
+  // epilogue staging: 4 warps × 2 buffers × (32 rows × 128 B, SWIZZLE_128B)
+  uint8_t *stg = base + S * stage_bytes;  // stage_bytes is a multiple of 1024
+  uint64_t *bars = reinterpret_cast<uint64_t *>(stg + 4 * 2 * 4096);
   uint64_t *full = bars, *split = bars + S, *empty = bars + 2 * S;
   uint64_t *done = bars + 3 * S, *tfree = bars + 3 * S + 2;
   const int ST = p.astages;
   uint64_t *aempty = bars + 3 * S + 4;  // TMEM A stage free (MMA done reading it)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * S + 8);
-  float *tpose = reinterpret_cast<float *>(bars + 3 * S + 10);  // 4 warps × 32 × 33
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -372,9 +376,12 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
             TCP_ADD(0);
           }
           uint8_t *st = base + s * stage_bytes;
-          mbar_expect_tx(&full[s], (uint32_t)(ABYTES + 2 * bbytes));
+          mbar_expect_tx(&full[s], (uint32_t)(ABYTES + (p.bsplit ? 1 : 2) * bbytes));
           tma_load_2d(st, &tmA, kc * 32, (int)(t * 128), &full[s]);
-          tma_load_4d(st + ABYTES, &tmBh, 0, 0, h, 2 * kc, &full[s]);
+          if (p.bsplit)
+            tma_load_3d(st + ABYTES, &tmBh, 0, h * p.hr, kc, &full[s]);  // raw fp32 Bᵀ part (its lo is made below)
+          else
+            tma_load_4d(st + ABYTES, &tmBh, 0, 0, h, 2 * kc, &full[s]);  // hi and lo parts
         }
       }
     }
@@ -391,7 +398,7 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
           TCP_ADD(1);
         }
         tc_fence_after();
-        const int pc0 = h * p.hr, pc1 = pc0 + p.hr;  // this part's output columns
+        const int pc0 = h * p.hr, pc1 = min(pc0 + p.hr, p.c16);  // this part's output columns
         for (int kc = 0; kc < p.nk; ++kc, ++g) {
           const int s = (int)(g % S);
           const int64_t use = g / S;
@@ -448,6 +455,8 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
     const int wt = threadIdx.x - 64;
     int64_t g = 0;
     for (int64_t it = blockIdx.x; it < p.nitems; it += gridDim.x) {
+      const int h = (int)(it % p.nh);
+      const int brows = min(p.hr, p.c16 - h * p.hr);  // Bᵀ rows the MMAs read
       for (int kc = 0; kc < p.nk; ++kc, ++g) {
         const int s = (int)(g % S);
         const int64_t use = g / S;
@@ -455,6 +464,19 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
           TCP_T0();
           mbar_wait(&full[s], (uint32_t)(use & 1));
           if (wt == 0) TCP_ADD(3);
+        }
+        // Bᵀ lo = x - trunc_tf32(x) next to the raw (= hi) part, same swizzled
+        // positions; written through the generic proxy, read by the MMAs
+        // (async proxy) after the fence below
+        if (p.bsplit) {
+          const float4 *braw = reinterpret_cast<const float4 *>(base + s * stage_bytes + ABYTES);
+          float4 *blo = reinterpret_cast<float4 *>(base + s * stage_bytes + ABYTES + bbytes);
+          for (int i = wt; i < brows * 8; i += kWorkers) {
+            const float4 x = braw[i];
+            blo[i] = make_float4(x.x - tf32_trunc(x.x), x.y - tf32_trunc(x.y), x.z - tf32_trunc(x.z),
+                                 x.w - tf32_trunc(x.w));
+          }
+          fence_proxy_async_smem();
         }
         const uint8_t *rowp = base + s * stage_bytes + r * 128;
         float hi[32], lo[32];
@@ -478,10 +500,13 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
       }
     }
   } else {
-    // epilogue warps: drain acc[buf] through a per-warp 32×32 smem transpose
+    // epilogue warps: acc[buf] rows (lane = row) → swizzled 32×32 staging tile
+    // → one TMA store per tile (rows >= n and columns >= ccols are clipped
+    // by the tensor map); the TMEM buffer is released as soon as it is read
     const int q = warp & 3;
     const int et = threadIdx.x - 192;
-    float *tb = tpose + (size_t)q * 32 * 33;
+    uint8_t *myst = stg + q * 2 * 4096;
+    int nst = 0;  // stores issued by this warp (staging buffer = nst & 1)
     int64_t ic = 0;
     for (int64_t it = blockIdx.x; it < p.nitems; it += gridDim.x, ++ic) {
       const int64_t t = it / p.nh;
@@ -499,32 +524,45 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
       float sc = 1.f;
       if (p.deg && row < p.n) sc = deg_pow_dev(p.deg, row, p.rexp);
       const int pc0 = h * p.hr;
-      for (int c = 0; c < p.hr; c += 64) {
-        uint32_t v[2][32];
-        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * p.hr + c);
-        tmem_ld32_nowait(ta, v[0]);
-        if (c + 32 < p.hr) tmem_ld32_nowait(ta + 32, v[1]);
+      const int nblk = (min(p.hr, p.c16 - pc0) + 31) / 32;  // hr is a multiple of 32
+      for (int cb = 0; cb < nblk; ++cb) {
+        uint32_t v[32];
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * p.hr + 32 * cb);
+        tmem_ld32_nowait(ta, v);
         tmem_wait_ld();
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          if (c + 32 * hh >= p.hr) break;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) tb[lane * 33 + i] = sc * __uint_as_float(v[hh][i]);
-          __syncwarp();
-          const int cl = c + 32 * hh + lane;
-          const int col = pc0 + cl;
-          if (col < p.ccols && cl < p.hr) {
-#pragma unroll 8
-            for (int rr = 0; rr < 32; ++rr)
-              if (r0 + rr < p.n) p.C[(r0 + rr) * p.ldc + col] = tb[rr * 33 + lane];
-          }
+        if (cb + 1 == nblk) {  // accumulator fully read: hand it back to the MMA warp
+          tc_fence_before();
+          mbar_arrive(&tfree[buf]);
+        }
+        uint8_t *sb = myst + (nst & 1) * 4096;
+        if (nst >= 2) {  // the store that last used this buffer has finished reading it
+          if (lane == 0) bulk_wait_read<1>();
           __syncwarp();
         }
+        uint8_t *rowp = sb + lane * 128;
+#pragma unroll
+        for (int cch = 0; cch < 8; ++cch) {
+          float4 o;
+          o.x = sc * __uint_as_float(v[4 * cch]);
+          o.y = sc * __uint_as_float(v[4 * cch + 1]);
+          o.z = sc * __uint_as_float(v[4 * cch + 2]);
+          o.w = sc * __uint_as_float(v[4 * cch + 3]);
+          *reinterpret_cast<float4 *>(rowp + ((cch ^ (lane & 7)) << 4)) = o;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        // (parts are multiples of 32 columns except the last, whose columns
+        // past c16 are >= ccols and clipped by the tensor map)
+        if (lane == 0) {
+          tma_store_2d(&tmC, sb, pc0 + 32 * cb, (int)r0);
+          bulk_commit();
+        }
+        ++nst;
       }
-      tc_fence_before();
-      mbar_arrive(&tfree[buf]);
       if (et == 0) TCP_ADD(5);
     }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
@@ -736,25 +774,27 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
   NM_LAUNCH(c, "tc_gram_reduce", k_gram_reduce2<<<ceil_div(a * b, 256), 256, 0, c.stream>>>(tmp.p, RG, a, b, G, ldg));
 }
 
-// Bᵀ hi/lo for the TMA, chunk-major: Bt[kc][part][j][kk] (part 0 = hi = rna_tf32(B[k][j]),
-// part 1 = lo = B − hi, k = 32 kc + kk), zero padded to nrows × 32 nk
+// Bᵀ for the tensor-core GEMM, zero padded to nrows × 32 nk.  split = 0:
+// Bt[kc][part][j][kk] with part 0 = hi = tf32(B[32 kc + kk][j]) and part 1 =
+// lo = B - hi.  split = 1: Bt[kc][j][kk] = fp32(B) (the kernel reads it as
+// tf32 hi and forms lo = x - trunc_tf32(x) in shared memory).
 __global__ void k_bt_split(const double *__restrict__ Bs, int64_t ldb, int64_t K, int64_t N, int64_t nrows, int64_t nk,
-                           float *__restrict__ Bt) {
+                           float *__restrict__ Bt, int split) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= nk * nrows * 32) return;
   const int64_t kk = idx & 31, j = (idx >> 5) % nrows, kc = idx / (32 * nrows);
   const int64_t k = kc * 32 + kk;
-  float h = 0.f, l = 0.f;
-  if (j < N && k < K) {
-    const double x = Bs[k * ldb + j];
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"((float)x));
-    h = __uint_as_float(r);
-    l = (float)(x - (double)h);
+  const double x = (j < N && k < K) ? Bs[k * ldb + j] : 0.0;
+  if (split) {
+    Bt[idx] = (float)x;
+    return;
   }
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"((float)x));
+  const float h = __uint_as_float(r);
   float *base = Bt + kc * 2 * nrows * 32;
   base[j * 32 + kk] = h;
-  base[nrows * 32 + j * 32 + kk] = l;
+  base[nrows * 32 + j * 32 + kk] = (float)(x - (double)h);
 }
 
 // C[n×b] = rs ⊙ (A[n×a] · Bs[a×b])
@@ -762,21 +802,33 @@ static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ld
                               float rexp, const Mat &C, bool tri) {
   using namespace tc;
   const int64_t n = A.rows, K = A.cols;
-  // output columns in nh parts of hr (multiple of 16, <= 192) so that two
+  // output columns in nh parts of hr (multiple of 32, <= 192) so that two
   // accumulators and the TMEM A stages fit the 512 TMEM columns
   const int c16 = (int)((bcols + 15) / 16) * 16;
   const int nh = (c16 + 191) / 192;
-  const int hr = ((c16 + nh - 1) / nh + 15) / 16 * 16;
+  const int hr = ((c16 + nh - 1) / nh + 31) / 32 * 32;
   const int ntot = nh * hr;
   const int64_t nk = ceil_div(K, 32);
-  DBuf<float> bt((size_t)nk * 2 * ntot * 32, c.stream);
+  static const int bsplit = [] {
+    const char *v = getenv("NETMFP_GEMM_BSPLIT");
+    return v ? atoi(v) : 0;
+  }();
+  DBuf<float> bt((size_t)nk * (bsplit ? 1 : 2) * ntot * 32, c.stream);
   NM_LAUNCH(c, "bt_split", k_bt_split<<<ceil_div(nk * ntot * 32, 256), 256, 0, c.stream>>>(Bs, ldb, K, bcols, ntot, nk,
-                                                                                             bt.p));
+                                                                                             bt.p, bsplit));
   CUtensorMap ma = make_map(A.p, n, K, A.ld, 128);
-  const int64_t bdims[4] = {32, hr, nh, 2 * nk};
-  const int64_t bstr[3] = {128, (int64_t)hr * 128, (int64_t)ntot * 128};
-  const int bbox[4] = {32, hr, 1, 2};  // one part (hi + lo) per box
-  CUtensorMap mb = make_map_nd(bt.p, 4, bdims, bstr, bbox, SW128);
+  CUtensorMap mb;
+  if (bsplit) {
+    const int64_t bdims[3] = {32, ntot, nk};
+    const int64_t bstr[2] = {128, (int64_t)ntot * 128};
+    const int bbox[3] = {32, hr, 1};  // one part of one K chunk per box
+    mb = make_map_nd(bt.p, 3, bdims, bstr, bbox, SW128);
+  } else {
+    const int64_t bdims[4] = {32, hr, nh, 2 * nk};
+    const int64_t bstr[3] = {128, (int64_t)hr * 128, (int64_t)ntot * 128};
+    const int bbox[4] = {32, hr, 1, 2};  // one part (hi + lo) per box
+    mb = make_map_nd(bt.p, 4, bdims, bstr, bbox, SW128);
+  }
   GemmP p{};
   p.n = n;
   p.K = (int)K;
@@ -784,6 +836,8 @@ static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ld
   p.ntot = ntot;
   p.nh = nh;
   p.hr = hr;
+  p.c16 = c16;
+  p.bsplit = bsplit;
   p.tri = tri ? 1 : 0;
   p.nitems = ceil_div(n, 128) * nh;
   p.C = C.p;
@@ -791,21 +845,22 @@ static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ld
   p.ccols = bcols;
   p.deg = deg;
   p.rexp = rexp;
-  const size_t tpose = (size_t)4 * 32 * 33 * 4;
+  const size_t staging = (size_t)4 * 2 * 4096;
   const size_t stage = (size_t)128 * 128 + (size_t)2 * hr * 128;
-  const int S = (int)std::min<size_t>(6, (kSmemMax - 1024 - 256 - tpose) / stage);
+  const int S = (int)std::min<size_t>(6, (kSmemMax - 1024 - 256 - staging) / stage);
   const int ST = std::min(4, (512 - 2 * hr) / 64);
   NM_REQUIRE(S >= 2 && ST >= 2, "tc_gemm_tall: stage does not fit");
   p.stages = S;
   p.astages = ST;
-  const size_t smem = 1024 + S * stage + (3 * S + 10) * 8 + tpose;
+  const size_t smem = 1024 + S * stage + staging + (3 * S + 10) * 8;
   static bool attr = false;
   if (!attr) {
     NM_CUDA(cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
     attr = true;
   }
   const int64_t grid = std::min<int64_t>(p.nitems, c.num_sms);
-  NM_LAUNCH(c, "tc_gemm_tall", k_gemm_tc<<<(unsigned)grid, NTG, smem, c.stream>>>(ma, mb, p));
+  CUtensorMap mc = make_map(C.p, n, bcols, C.ld, 32, SW128, 32);
+  NM_LAUNCH(c, "tc_gemm_tall", k_gemm_tc<<<(unsigned)grid, NTG, smem, c.stream>>>(ma, mb, mc, p));
 }
 
 void tc_gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcols, const int32_t *deg, float rexp,

@@ -1,4 +1,4 @@
-#define TC_PROF
+
 #include "../../paper_2110_12782_b200/csrc/tc_gemm.cu"
 #include <cstdio>
 #include <vector>
