@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <memory>
@@ -128,6 +129,17 @@ inline void prof_collect(Ctx &c) {
       float g = 0.f;
       cudaEventElapsedTime(&g, prev_end, pe.a);
       gap_ms += g;
+      if (getenv("NETMFP_PROF_GAPS") && c.prof_filter.empty()) {  // attribute to the kernel that follows
+        const std::string key = std::string("gap>") + pe.name;
+        bool f = false;
+        for (auto &s : c.stats)
+          if (s.first == key) {
+            s.second.first += 1;
+            s.second.second += g;
+            f = true;
+          }
+        if (!f) c.stats.push_back({key, {1, (double)g}});
+      }
     }
     prev_end = pe.b;
   }
@@ -236,10 +248,12 @@ struct Mat {
 inline int64_t pad4(int64_t c) { return (c + 3) / 4 * 4; }
 inline int64_t pad32(int64_t c) { return (c + 31) / 32 * 32; }
 
-// Owned dense fp32 block with ld padded to a multiple of 32 floats (128 B rows
-// segments) and zeroed padding columns (contractions read whole 32-column
-// chunks; the cols x rows interior is always written by its producer before
-// it is read, so it is not cleared).
+// Owned dense fp32 block with ld padded to a multiple of 32 floats (128 B row
+// segments).  Nothing is cleared: every producer writes the rows × cols
+// interior before it is read, and no consumer's valid output depends on the
+// padding columns (tensor maps clip the contraction dimension at cols; the
+// Gram's padded blocks only feed discarded rows/columns; SpMM lanes past
+// cols are not stored).
 struct Block {
   DBuf<float> buf;
   Mat m;
@@ -248,8 +262,6 @@ struct Block {
   void alloc(int64_t rows, int64_t cols, cudaStream_t s) {
     int64_t ld = pad32(cols);
     buf.alloc((size_t)rows * ld, s);
-    if (rows > 0 && ld > cols)
-      NM_CUDA(cudaMemset2DAsync(buf.p + cols, ld * sizeof(float), 0, (ld - cols) * sizeof(float), rows, s));
     m.p = buf.p;
     m.rows = rows;
     m.cols = cols;
