@@ -699,61 +699,95 @@ __global__ void k_bisect(const double *__restrict__ d, const double *__restrict_
 }
 
 // Eigenvalue m (ascending) by multisection: one warp per eigenvalue, the 32
-// lanes evaluate Sturm counts at 32 interior points of the current bracket
-// and a ballot picks the sub-interval holding the m-th eigenvalue (5 bits per
-// round instead of 1); T's diagonal / off-diagonal squares live in shared memory.
+// lanes evaluate Sturm counts at 64 interior points of the current bracket
+// (two interleaved recurrences per lane) and two ballots pick the
+// sub-interval holding the m-th eigenvalue (6 bits per round instead of 1);
+// T's diagonal / off-diagonal squares live in shared memory.
 constexpr int MSW = 8;  // warps (eigenvalues) per block
+__device__ __forceinline__ double pow2_of_exponent(double m) {  // 2^-e for m = f · 2^e, f in [1, 2)
+  const int e = ((__double2hiint(m) >> 20) & 0x7ff) - 1023;
+  const int be = min(max(1023 - e, 1), 2046);
+  return __hiloint2double(be << 20, 0);
+}
+
+// Sturm count of the (power-of-2 scaled) tridiagonal T at two shifts, by the
+// three-term recurrence p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2} of the
+// leading principal minors (no division on the dependence chain; the pair is
+// rescaled by a power of two every 8 steps).  Count = sign changes of p;
+// an exact zero takes the sign opposite to its predecessor.
+__device__ __forceinline__ void sturm2(const double *sd, const double *se2, int l, double xa, double xb, int &ca,
+                                       int &cb) {
+  double a0 = 1.0, a1 = sd[0] - xa, b0 = 1.0, b1 = sd[0] - xb;
+  if (a1 == 0.0) a1 = -1e-300;
+  if (b1 == 0.0) b1 = -1e-300;
+  ca = a1 < 0.0;
+  cb = b1 < 0.0;
+  for (int i = 1; i < l; ++i) {
+    double a2 = (sd[i] - xa) * a1 - se2[i - 1] * a0;
+    double b2 = (sd[i] - xb) * b1 - se2[i - 1] * b0;
+    if (a2 == 0.0) a2 = -1e-300 * a1;
+    if (b2 == 0.0) b2 = -1e-300 * b1;
+    ca += (a2 < 0.0) != (a1 < 0.0);
+    cb += (b2 < 0.0) != (b1 < 0.0);
+    a0 = a1; a1 = a2;
+    b0 = b1; b1 = b2;
+    if ((i & 7) == 0) {
+      const double sa = pow2_of_exponent(fmax(fabs(a0), fabs(a1)));
+      const double sb = pow2_of_exponent(fmax(fabs(b0), fabs(b1)));
+      a0 *= sa; a1 *= sa;
+      b0 *= sb; b1 *= sb;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(MSW * 32) k_multisect(const double *__restrict__ d, const double *__restrict__ e,
                                                         int l, double *__restrict__ w) {
   extern __shared__ double ms_sh[];
   double *sd = ms_sh, *se2 = ms_sh + l;
+  const int lane = threadIdx.x & 31;
+  // exact power-of-two scale of T to norm <= 1 (Gershgorin), all warps
+  double tn = 0.0;
+  for (int i = lane; i < l; i += 32) {
+    const double r = fabs(d[i]) + (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < l ? fabs(e[i]) : 0.0);
+    tn = fmax(tn, r);
+  }
+  for (int o = 16; o > 0; o >>= 1) tn = fmax(tn, __shfl_xor_sync(0xffffffffu, tn, o));
+  const double inv = tn > 0.0 ? 0.5 * pow2_of_exponent(tn) : 1.0;  // 2^-(e+1): |T| / 2^(e+1) < 1
   for (int i = threadIdx.x; i < l; i += blockDim.x) {
-    sd[i] = d[i];
-    se2[i] = (i + 1 < l) ? e[i] * e[i] : 0.0;
+    sd[i] = d[i] * inv;
+    se2[i] = (i + 1 < l) ? (e[i] * inv) * (e[i] * inv) : 0.0;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
   const int m = blockIdx.x * MSW + (threadIdx.x >> 5);
-  // Gershgorin bracket and pivmin (all lanes, then reduce)
-  double lo = 1e300, hi = -1e300, emax = 0.0;
+  double lo = 1e300, hi = -1e300;
   for (int i = lane; i < l; i += 32) {
-    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < l ? fabs(e[i]) : 0.0);
+    const double r = (i > 0 ? fabs(e[i - 1]) * inv : 0.0) + (i + 1 < l ? fabs(e[i]) * inv : 0.0);
     lo = fmin(lo, sd[i] - r);
     hi = fmax(hi, sd[i] + r);
-    emax = fmax(emax, se2[i]);
   }
   for (int o = 16; o > 0; o >>= 1) {
     lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
     hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
   }
   if (m >= l) return;
-  const double tnorm = fmax(fabs(lo), fabs(hi));
   const double eps = 2.220446049250313e-16;
-  const double pivmin = fmax(1e-300, 4.0 * 2.2250738585072014e-308 * fmax(1.0, emax));
-  lo -= 2.0 * eps * tnorm + pivmin;
-  hi += 2.0 * eps * tnorm + pivmin;
+  lo -= 4.0 * eps + 1e-300;
+  hi += 4.0 * eps + 1e-300;
+  // 64 points per round (two per lane): 6 bits of the eigenvalue per round
   for (int it = 0; it < 40; ++it) {
-    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin) break;
-    const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
-    int cnt = 0;
-    double q = sd[0] - x;
-    if (fabs(q) < pivmin) q = -pivmin;
-    cnt += q < 0;
-    for (int i = 1; i < l; ++i) {
-      q = sd[i] - x - se2[i - 1] / q;
-      if (fabs(q) < pivmin) q = -pivmin;
-      cnt += q < 0;
-    }
-    const unsigned above = __ballot_sync(0xffffffffu, cnt > m);
-    const int jf = above ? __ffs(above) - 1 : 32;  // first point past eigenvalue m
-    const double nlo = jf == 0 ? lo : lo + (hi - lo) * (double)jf / 33.0;
-    const double nhi = jf == 32 ? hi : lo + (hi - lo) * (double)(jf + 1) / 33.0;
+    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 1e-300) break;
+    const double step = (hi - lo) / 65.0;
+    int ca, cb;
+    sturm2(sd, se2, l, lo + step * (double)(lane + 1), lo + step * (double)(lane + 33), ca, cb);
+    const unsigned above_a = __ballot_sync(0xffffffffu, ca > m), above_b = __ballot_sync(0xffffffffu, cb > m);
+    const int jf = above_a ? __ffs(above_a) - 1 : (above_b ? 32 + __ffs(above_b) - 1 : 64);
+    const double nlo = jf == 0 ? lo : lo + step * (double)jf;
+    const double nhi = jf == 64 ? hi : lo + step * (double)(jf + 1);
     if (!(nhi < hi || nlo > lo)) break;  // no progress at this precision
     lo = nlo;
     hi = nhi;
   }
-  if (lane == 0) w[m] = 0.5 * (lo + hi);
+  if (lane == 0) w[m] = 0.5 * (lo + hi) / inv;
 }
 
 // Inverse iteration (dstein-style): one warp per cluster of (near-)degenerate
