@@ -915,21 +915,48 @@ __global__ void k_clusters(const double *__restrict__ w, const double *__restric
 }
 
 // eigenvectors of S: x <- H_0 (H_1 (… H_{l-3} z)); one warp per eigenvector
-__global__ void k_backtransform(const double *__restrict__ Hv, const double *__restrict__ hbeta, int l,
-                                double *__restrict__ Zt) {
+// one warp per eigenvector, held in registers (lane owns entries ln + 32 i);
+// the next reflector is prefetched while the current one is applied (Hv rows
+// are zero at k <= j, so no masking below the reflector's support)
+constexpr int BT_NR = 15;  // l <= 480
+__global__ void __launch_bounds__(256) k_backtransform(const double *__restrict__ Hv, const double *__restrict__ hbeta,
+                                                       int l, double *__restrict__ Zt) {
   const int m = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int ln = threadIdx.x % 32;
   if (m >= l) return;
-  double *x = Zt + (int64_t)m * l;
-  for (int j = l - 3; j >= 0; --j) {
-    const double b = hbeta[j];
-    if (b == 0.0) continue;
+  double *xg = Zt + (int64_t)m * l;
+  double x[BT_NR], vn[BT_NR];
+#pragma unroll
+  for (int i = 0; i < BT_NR; ++i) {
+    const int k = ln + 32 * i;
+    x[i] = k < l ? xg[k] : 0.0;
+  }
+  auto load = [&](int j) {
     const double *v = Hv + (int64_t)j * l;
-    double s = 0.0;
-    for (int k = j + 1 + ln; k < l; k += 32) s += v[k] * x[k];
-    s = warp_sum(s) * b;
-    for (int k = j + 1 + ln; k < l; k += 32) x[k] -= s * v[k];
-    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < BT_NR; ++i) {
+      const int k = ln + 32 * i;
+      vn[i] = k < l ? __ldg(v + k) : 0.0;
+    }
+  };
+  if (l >= 3) load(l - 3);
+  for (int j = l - 3; j >= 0; --j) {
+    double v[BT_NR];
+#pragma unroll
+    for (int i = 0; i < BT_NR; ++i) v[i] = vn[i];
+    const double b = __ldg(hbeta + j);
+    if (j > 0) load(j - 1);
+    double sacc = 0.0;
+#pragma unroll
+    for (int i = 0; i < BT_NR; ++i) sacc = fma(v[i], x[i], sacc);
+    sacc = warp_sum(sacc) * b;
+#pragma unroll
+    for (int i = 0; i < BT_NR; ++i) x[i] = fma(-sacc, v[i], x[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < BT_NR; ++i) {
+    const int k = ln + 32 * i;
+    if (k < l) xg[k] = x[i];
   }
 }
 
@@ -970,7 +997,7 @@ void sym_eig(Ctx &c, double *S, int64_t l64, double *lam, double *V, bool abs_or
   NM_CUDA(cudaMemsetAsync(e.p, 0, (size_t)l * 8, s));
   const int nloc = (l + TDC - 1) / TDC;
   size_t smem = ((size_t)nloc * l + 3 * l + nloc + 40 + 24) * sizeof(double);
-  NM_REQUIRE(smem <= 227 * 1024, "sym_eig: l too large for the 8-CTA cluster (l <= ~470)");
+  NM_REQUIRE(smem <= 227 * 1024 && l <= 32 * BT_NR, "sym_eig: l too large for the 8-CTA cluster (l <= ~470)");
   static bool attr = false;
   if (!attr) {
     NM_CUDA(cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
