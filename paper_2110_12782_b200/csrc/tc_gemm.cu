@@ -267,6 +267,7 @@ __device__ __forceinline__ int64_t gram_locate(const GramRed &R, int64_t i, int6
 __global__ void k_gram_reduce1(const float *__restrict__ part, GramRed R, int64_t per_group, double *__restrict__ tmp) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= R.a * R.b) return;
+  if (R.sym && idx / R.b > idx % R.b) return;  // symmetric: upper triangle only (mirrored in reduce2)
   const int64_t off = gram_locate(R, idx / R.b, idx % R.b);
   const int64_t c0 = blockIdx.y * per_group, c1 = min(c0 + per_group, R.nchain);
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -282,11 +283,13 @@ __global__ void k_gram_reduce1(const float *__restrict__ part, GramRed R, int64_
 }
 
 __global__ void k_gram_reduce2(const double *__restrict__ tmp, int groups, int64_t a, int64_t b, double *__restrict__ G,
-                               int64_t ldg) {
+                               int64_t ldg, bool sym) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= a * b) return;
+  const int64_t i = idx / b, j = idx % b;
+  const int64_t src = (sym && i > j) ? j * b + i : idx;
   double s = 0.0;
-  for (int g = 0; g < groups; ++g) s += tmp[(int64_t)g * a * b + idx];
+  for (int g = 0; g < groups; ++g) s += tmp[(int64_t)g * a * b + src];
   G[(idx / b) * ldg + idx % b] = s;
 }
 
@@ -792,7 +795,7 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
   DBuf<double> tmp((size_t)RG * a * b, c.stream);
   dim3 g1(ceil_div(a * b, 256), RG);
   NM_LAUNCH(c, "tc_gram_reduce", k_gram_reduce1<<<g1, 256, 0, c.stream>>>(part.p, R, per, tmp.p));
-  NM_LAUNCH(c, "tc_gram_reduce", k_gram_reduce2<<<ceil_div(a * b, 256), 256, 0, c.stream>>>(tmp.p, RG, a, b, G, ldg));
+  NM_LAUNCH(c, "tc_gram_reduce", k_gram_reduce2<<<ceil_div(a * b, 256), 256, 0, c.stream>>>(tmp.p, RG, a, b, G, ldg, sym));
 }
 
 // Bᵀ for the tensor-core GEMM, zero padded to nrows × 32 nk.  split = 0:
