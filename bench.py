@@ -206,7 +206,10 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": val * 1e3,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": w.name, "n": n},
+            "data": "synthetic",
+            "config": {"workload": f"configs[{args.workload}] {w.name}", "n": n, "k": w.k, "s1": w.s1, "q": w.q,
+                       "T": w.T, "b": w.b, "d": w.d, "s2": w.s2, "s3": w.s3, "z": w.z, "alpha": w.alpha,
+                       "prop_order": w.prop_order},
             "cpu_baseline": {"value": val, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": val, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
