@@ -533,6 +533,11 @@ __device__ unsigned long long g_td_t[8][4][512];
 #define TD_MARK(ph)
 #endif
 constexpr int TDC = 8;     // cluster size (CTAs) for the tridiagonalisation
+// split cluster barrier (every thread arrives; release / acquire at cluster scope)
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
 constexpr int TDT = 512;   // threads per CTA
 
 // Householder tridiagonalisation Qᵀ S Q = T, Q = H_0 … H_{l-3}, H_j = I - beta_j v_j v_jᵀ
@@ -541,7 +546,9 @@ constexpr int TDT = 512;   // threads per CTA
 // K = beta vᵀp / 2:  A -= v pᵀ + p vᵀ - 2K v vᵀ  (= v wᵀ + w vᵀ, w = p - K v).
 // Every exchange is a PUSH into the other CTAs' shared memory (remote stores,
 // no remote loads on the critical path) and a step costs two cluster barriers:
-//   S1: the owner of row j has pushed v_j and beta_j;
+//   S1: the owner of row j has pushed v_j and beta_j (split arrive / wait:
+//       the owner updates row j first during step j-1's update, pushes the
+//       reflector and arrives before updating its other rows — look-ahead);
 //   S2: every CTA has pushed its rows' p_i and its partial vᵀp.
 // v and beta (pushed before S1) are double-buffered by step parity: a buffer
 // is rewritten two steps later, after every CTA has passed the barrier that
@@ -569,40 +576,45 @@ __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
     int li = (int)(idx / l), k = (int)(idx % l);
     A[idx] = S[(int64_t)(li * TDC + rank) * l + k];
   }
-  cl.sync();
-  for (int j = 0; j + 2 < l; ++j) {
-    const int owner = j % TDC, par = j & 1;
+  __syncthreads();
+  // reflector of step j from row j (entries j+1..l-1; owner CTA only), pushed
+  // with beta_j to every CTA's parity buffer
+  auto reflector = [&](int j) {
+    const int par = j & 1;
     double *v = vbuf + par * l;
-    TD_MARK(0);
-    // (1) owner: reflector from row j (entries j+1..l-1), pushed to every CTA
-    if (rank == owner) {
-      const double *x = A + (int64_t)(j / TDC) * l;
-      double ss = 0.0;
-      for (int k = j + 2 + tid; k < l; k += nt) ss += x[k] * x[k];
-      ss = block_sum<TDT>(ss, red);
-      const double x0 = x[j + 1];
-      double beta = 0.0, alpha = x0, v0 = 0.0;
-      if (ss > 0.0) {
-        const double nrm = sqrt(ss + x0 * x0);
-        alpha = x0 >= 0 ? -nrm : nrm;
-        v0 = x0 - alpha;
-        beta = 2.0 / (ss + v0 * v0);
-      }
-      for (int k = j + 1 + tid; k < l; k += nt) {
-        const double val = ss > 0.0 ? (k == j + 1 ? v0 : x[k]) : 0.0;
-#pragma unroll
-        for (int r = 0; r < TDC; ++r) cl.map_shared_rank(v, r)[k] = val;
-        Hv[(int64_t)j * l + k] = val;
-      }
-      if (tid < TDC) cl.map_shared_rank(xchg, tid)[16 + par] = beta;
-      if (tid == 0) {
-        dd[j] = x[j];
-        ee[j] = alpha;
-        hbeta[j] = beta;
-      }
+    const double *x = A + (int64_t)(j / TDC) * l;
+    double ss = 0.0;
+    for (int k = j + 2 + tid; k < l; k += nt) ss += x[k] * x[k];
+    ss = block_sum<TDT>(ss, red);
+    const double x0 = x[j + 1];
+    double beta = 0.0, alpha = x0, v0 = 0.0;
+    if (ss > 0.0) {
+      const double nrm = sqrt(ss + x0 * x0);
+      alpha = x0 >= 0 ? -nrm : nrm;
+      v0 = x0 - alpha;
+      beta = 2.0 / (ss + v0 * v0);
     }
+    for (int k = j + 1 + tid; k < l; k += nt) {
+      const double val = ss > 0.0 ? (k == j + 1 ? v0 : x[k]) : 0.0;
+#pragma unroll
+      for (int r = 0; r < TDC; ++r) cl.map_shared_rank(v, r)[k] = val;
+      Hv[(int64_t)j * l + k] = val;
+    }
+    if (tid < TDC) cl.map_shared_rank(xchg, tid)[16 + par] = beta;
+    if (tid == 0) {
+      dd[j] = x[j];
+      ee[j] = alpha;
+      hbeta[j] = beta;
+    }
+  };
+  if (l >= 3 && rank == 0) reflector(0);
+  cluster_arrive();  // S1(0)
+  for (int j = 0; j + 2 < l; ++j) {
+    const int par = j & 1;
+    const double *v = vbuf + par * l;
+    TD_MARK(0);
     TD_MARK(1);
-    cl.sync();  // S1
+    cluster_wait();  // S1(j): v_j, beta_j pushed
     TD_MARK(2);
     const double beta = xchg[16 + par];
     // (2) p_i = beta A[i, j+1:] · v for own rows i > j; partial vᵀp
@@ -633,17 +645,31 @@ __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
 #pragma unroll
     for (int r = 0; r < TDC; ++r) vtp += xchg[par * TDC + r];
     const double K2 = vtp * beta;  // 2K
-    // (4) A_i -= v_i p + p_i v - 2K v_i v  (own rows i > j, columns > j)
+    // (4) A_i -= v_i p + p_i v - 2K v_i v  (own rows i > j, columns > j).
+    // Look-ahead: the owner of step j+1 updates row j+1 first, then builds
+    // and pushes reflector j+1 and arrives at S1(j+1) before its other rows.
+    const int jn = j + 1;
+    const bool next_owner = jn + 2 < l && rank == jn % TDC;
+    if (next_owner) {
+      double *Ai = A + (int64_t)(jn / TDC) * l;
+      const double vi = v[jn], pi = pf[jn], ci = pi - K2 * vi;
+      for (int k = j + 1 + tid; k < l; k += nt) Ai[k] -= vi * pf[k] + ci * v[k];
+      __syncthreads();
+      reflector(jn);
+      cluster_arrive();  // S1(j+1)
+    }
     for (int li = wid; li < nloc; li += nt / 32) {
       const int i = li * TDC + rank;
-      if (i <= j) continue;
+      if (i <= j || (next_owner && i == jn)) continue;
       double *Ai = A + (int64_t)li * l;
       const double vi = v[i], pi = pf[i], ci = pi - K2 * vi;
       for (int k = j + 1 + ln; k < l; k += 32) Ai[k] -= vi * pf[k] + ci * v[k];
     }
-    // CTA barrier: the next owner reads its freshly updated row
+    if (!next_owner) cluster_arrive();  // S1(j+1): this CTA is done with v_j, pf and the partials
+    // CTA barrier: rows of this step are final before the next owner reads them
     __syncthreads();
   }
+  if (l >= 3) cluster_wait();  // the last arrive (S1 after the final step)
   // trailing 2×2 (or 1×1)
   if (l >= 2) {
     const int i0 = l - 2, i1 = l - 1;
