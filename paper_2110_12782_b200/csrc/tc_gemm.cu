@@ -71,8 +71,7 @@ struct GramP {
   int a3d, b3d;     // operand loaded as one 3-D box {32, BK, nblk} (ld covers all blocks)
   uint32_t tcols;   // TMEM allocation
   int stages;
-  const int32_t *wdeg;  // optional row weights
-  float wexp;           // weight applied to A (non-sym) or sqrt applied to both (sym)
+  const float *wrow;    // optional per-row weights (d^-wexp, or its square root applied to both sides if sym)
   int64_t part_stride;  // floats per chain partial
   float *part;
 };
@@ -192,13 +191,12 @@ __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUten
       const int n16 = nblk * BLK / 16;
       for (int i = wt; i < n16; i += kWorkers) {
         float4 v = reinterpret_cast<float4 *>(raw)[i];
-        if (p.wdeg) {
+        if (p.wrow) {
           const int blk = i / (BLK / 16);
           const int r = (i % (BLK / 16)) / 8;  // row inside the chunk (128-B rows)
           const int64_t grow = row0 + r;
           if (SYM || blk < p.na_blk) {
-            float w = 0.f;
-            if (grow < p.n) w = deg_pow_dev(p.wdeg, grow, SYM ? 0.5f * p.wexp : p.wexp);
+            const float w = grow < p.n ? __ldg(p.wrow + grow) : 0.f;
             v.x *= w; v.y *= w; v.z *= w; v.w *= w;
             reinterpret_cast<float4 *>(raw)[i] = v;
           }
@@ -687,6 +685,11 @@ static void launch_gram(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, tc
   NM_LAUNCH(c, "tc_gram", tc::k_gram_tc<BK, SYM><<<(unsigned)nchain, tc::NT, smem, c.stream>>>(ma, mb, p));
 }
 
+__global__ void k_gram_wrow(const int32_t *__restrict__ deg, int64_t n, float e, float *__restrict__ w) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) w[i] = tc::deg_pow_dev(deg, i, e);
+}
+
 // G[a×b] (fp64, ldg) = Aᵀ diag(d^-wexp) B over the n rows
 void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg) {
   using namespace tc;
@@ -758,6 +761,12 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
   CUtensorMap ma = a3d ? map3(A, na_blk) : make_map(A.p, n, a, A.ld, BK, SW128_32B);
   CUtensorMap mb = sym ? ma : (b3d ? map3(B, nb_blk) : make_map(B.p, n, b, B.ld, BK, SW128_32B));
   DBuf<float> part((size_t)nchain * total, c.stream);
+  // per-row weights once (d^-wexp on A; sym: d^(-wexp/2) on both sides)
+  DBuf<float> wrow;
+  if (deg) {
+    wrow.alloc(n, c.stream);
+    NM_LAUNCH(c, "gram_wrow", k_gram_wrow<<<ceil_div(n, 256), 256, 0, c.stream>>>(deg, n, sym ? 0.5f * wexp : wexp, wrow.p));
+  }
   for (auto &grp : groups) {
     GramP p{};
     p.n = n;
@@ -773,8 +782,7 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
     p.tcols = tmem_cols_for(w);
     p.a3d = a3d ? 1 : 0;
     p.b3d = b3d ? 1 : 0;
-    p.wdeg = deg;
-    p.wexp = wexp;
+    p.wrow = wrow.p;
     p.part_stride = total;
     p.part = part.p;
     if (sym)
