@@ -227,9 +227,9 @@ void gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcol
 }
 
 void gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, const int32_t *deg, float rexp,
-                   const Mat &C) {
+                   const Mat &C, bool exact) {
   if (tc_enabled() && A.rows >= 128 && A.cols <= 288) {
-    tc_gemm_tall_tri(c, A, Rinv, ldb, A.cols, deg, rexp, C);
+    tc_gemm_tall_tri(c, A, Rinv, ldb, A.cols, deg, rexp, C, exact);
     return;
   }
   gemm_tall(c, A, Rinv, ldb, A.cols, deg, rexp, C);

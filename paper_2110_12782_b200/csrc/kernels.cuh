@@ -60,10 +60,12 @@ void tc_gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t b
                   float rexp, const Mat &C);
 void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg);
 void tc_gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, int64_t bcols, const int32_t *deg,
-                      float rexp, const Mat &C);
-// C = rs · A · Rinv with Rinv (a×a) upper triangular (CholeskyQR's Y R⁻¹)
+                      float rexp, const Mat &C, bool exact = true);
+// C = rs · A · Rinv with Rinv (a×a) upper triangular (CholeskyQR's Y R⁻¹).  exact =
+// false: Rinv rounded to tf32 (the product is exact for that R̃⁻¹: same span,
+// orthonormal to ~1e-3 — for CholeskyQR passes another pass follows)
 void gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, const int32_t *deg, float rexp,
-                   const Mat &C);
+                   const Mat &C, bool exact = true);
 bool tc_enabled();
 // Ω = randn(n, l) from Philox [R1], row-scaled by d_i^-e (deg != null)
 void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, float rexp, int64_t row0 = 0,

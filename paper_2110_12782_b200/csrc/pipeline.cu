@@ -21,8 +21,13 @@ static void check_flag(Ctx &c, const char *what) {
 
 // CholeskyQR (north_star; [R7]): Gram G = YᵀY (fp64), G = RᵀR, out = rs · Y R⁻¹.
 // passes = 2 gives CholeskyQR2 (second pass on the materialised Y R1⁻¹ in tmp).
+// orthonormal = false (a power iteration's intermediate basis, which the next
+// iteration re-orthonormalises; only its span matters) and every pass but the
+// last of a CholeskyQR2: the product uses R⁻¹ rounded to tf32 (exactly that
+// basis change: same span, columns orthonormal to ~1e-3), 2 tensor-core
+// products instead of 3.
 void cholqr(Ctx &c, const Mat &Y, const Mat &out, const int32_t *deg, float rexp, int passes,
-            const Mat *tmp) {
+            const Mat *tmp, bool orthonormal) {
   NM_STAGE(c, "stage_cholqr");
   const int64_t l = Y.cols;
   cudaStream_t s = c.stream;
@@ -34,10 +39,10 @@ void cholqr(Ctx &c, const Mat &Y, const Mat &out, const int32_t *deg, float rexp
     chol_inv_upper(c, G, l, l, Rinv, c.d_flags);
     const bool last = (ps + 1 == passes);
     if (last) {
-      gemm_tall_tri(c, cur, Rinv, l, deg, rexp, out);
+      gemm_tall_tri(c, cur, Rinv, l, deg, rexp, out, orthonormal);
     } else {
       NM_REQUIRE(tmp && tmp->p != cur.p, "cholqr2: needs a scratch block");
-      gemm_tall_tri(c, cur, Rinv, l, nullptr, 0.f, *tmp);
+      gemm_tall_tri(c, cur, Rinv, l, nullptr, 0.f, *tmp, false);
       cur = *tmp;
     }
   }
@@ -63,7 +68,7 @@ void freigs(Ctx &c, const Graph &g, double alpha, int k, int s1, int q, uint64_t
   sp.X = dist_gather_rows(c, g, P.m, xfull); sp.ldx = P.m.ld; sp.Y = Y.m.p; sp.ldy = Y.m.ld; sp.a = a;
   spmm(c, g, sp);
   // step 3: Q = orth(Y)
-  cholqr(c, Y.m, P.m, g.deg, a, q == 0 ? 2 : 1, &T.m);
+  cholqr(c, Y.m, P.m, g.deg, a, q == 0 ? 2 : 1, &T.m, q == 0);
   // steps 4-6: Q = orth(X X Q)
   for (int it = 0; it < q; ++it) {
     SpmmArgs s1a;
@@ -74,7 +79,7 @@ void freigs(Ctx &c, const Graph &g, double alpha, int k, int s1, int q, uint64_t
     s2a.cols = l;
     s2a.X = dist_gather_rows(c, g, T.m, xfull); s2a.ldx = T.m.ld; s2a.Y = Y.m.p; s2a.ldy = Y.m.ld; s2a.a = a;
     spmm(c, g, s2a);  // Y = D^-α A T = X X Q
-    cholqr(c, Y.m, P.m, g.deg, a, it + 1 == q ? 2 : 1, &T.m);
+    cholqr(c, Y.m, P.m, g.deg, a, it + 1 == q ? 2 : 1, &T.m, it + 1 == q);
   }
   check_flag(c, "freigs orthonormalisation");
   // step 7: S = Qᵀ X Q = Pᵀ A P

@@ -3,7 +3,8 @@
 #include "common.cuh"
 
 namespace netmfp {
-void cholqr(Ctx &c, const Mat &Y, const Mat &out, const int32_t *deg, float rexp, int passes, const Mat *tmp);
+void cholqr(Ctx &c, const Mat &Y, const Mat &out, const int32_t *deg, float rexp, int passes, const Mat *tmp,
+            bool orthonormal = true);
 void freigs(Ctx &c, const Graph &g, double alpha, int k, int s1, int q, uint64_t seed, const Mat &U,
             double *lam_dev);
 void factor_pair(Ctx &c, const Graph &g, double alpha, int T, const Mat &U, const double *lam, int k,

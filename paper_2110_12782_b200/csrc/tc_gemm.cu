@@ -304,6 +304,7 @@ struct GemmP {
   int bsplit;     // 1: Bᵀ raw fp32, lo formed in shared memory; 0: hi / lo from the host layout
   int order;      // item order (item_of)
   int skip;       // triangular B: skip the K chunks a part does not need
+  int bexact;     // 1: A_hi B_hi + A_hi B_lo + A_lo B_hi; 0: B rounded to tf32, A_hi B + A_lo B
   int tri;        // B upper triangular: chunk kb touches columns >= 32 kb
   int64_t nitems; // (M tile, part) work items
   int stages;     // shared-memory ring (A raw + Bᵀ part)
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
             TCP_ADD(0);
           }
           uint8_t *st = base + s * stage_bytes;
-          mbar_expect_tx(&full[s], (uint32_t)(ABYTES + (p.bsplit ? 1 : 2) * bbytes));
+          mbar_expect_tx(&full[s], (uint32_t)(ABYTES + ((p.bsplit || !p.bexact) ? 1 : 2) * bbytes));
           tma_load_2d(st, &tmA, kc * 32, (int)(t * 128), &full[s]);
           if (p.bsplit)
             tma_load_3d(st + ABYTES, &tmBh, 0, h * p.hr, kc, &full[s]);  // raw fp32 Bᵀ part (its lo is made below)
@@ -447,14 +448,24 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
             const uint32_t acc0 = (kc == 0) ? 0u : 1u;
             // every column is first touched by K-chunk 0 (tri: chunk kb only adds to
             // columns >= 32 kb), so chunk 0 / kstep 0 starts the sums
-            mma_tf32_ts(d, ahi, dbh, idesc, acc0);
-            mma_tf32_ts(d, ahi, dbl, idesc, 1u);
-            mma_tf32_ts(d, alo, dbh, idesc, 1u);
+            if (p.bexact) {
+              mma_tf32_ts(d, ahi, dbh, idesc, acc0);
+              mma_tf32_ts(d, ahi, dbl, idesc, 1u);
+              mma_tf32_ts(d, alo, dbh, idesc, 1u);
 #pragma unroll
-            for (int ks = 1; ks < 4; ++ks) {
-              mma_tf32_ts(d, ahi + ks * 8, dbh + 2 * ks, idesc, 1u);
-              mma_tf32_ts(d, ahi + ks * 8, dbl + 2 * ks, idesc, 1u);
-              mma_tf32_ts(d, alo + ks * 8, dbh + 2 * ks, idesc, 1u);
+              for (int ks = 1; ks < 4; ++ks) {
+                mma_tf32_ts(d, ahi + ks * 8, dbh + 2 * ks, idesc, 1u);
+                mma_tf32_ts(d, ahi + ks * 8, dbl + 2 * ks, idesc, 1u);
+                mma_tf32_ts(d, alo + ks * 8, dbh + 2 * ks, idesc, 1u);
+              }
+            } else {  // B = tf32(B): A's full fp32 against it (2 products)
+              mma_tf32_ts(d, ahi, dbh, idesc, acc0);
+              mma_tf32_ts(d, alo, dbh, idesc, 1u);
+#pragma unroll
+              for (int ks = 1; ks < 4; ++ks) {
+                mma_tf32_ts(d, ahi + ks * 8, dbh + 2 * ks, idesc, 1u);
+                mma_tf32_ts(d, alo + ks * 8, dbh + 2 * ks, idesc, 1u);
+              }
             }
           }
           __syncwarp();
@@ -831,7 +842,7 @@ __global__ void k_bt_split(const double *__restrict__ Bs, int64_t ldb, int64_t K
 
 // C[n×b] = rs ⊙ (A[n×a] · Bs[a×b])
 static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcols, const int32_t *deg,
-                              float rexp, const Mat &C, bool tri) {
+                              float rexp, const Mat &C, bool tri, bool exact) {
   using namespace tc;
   const int64_t n = A.rows, K = A.cols;
   // output columns in nh parts of hr (multiple of 32, <= 192) so that two
@@ -858,7 +869,7 @@ static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ld
   } else {
     const int64_t bdims[4] = {32, hr, nh, 2 * nk};
     const int64_t bstr[3] = {128, (int64_t)hr * 128, (int64_t)ntot * 128};
-    const int bbox[4] = {32, hr, 1, 2};  // one part (hi + lo) per box
+    const int bbox[4] = {32, hr, 1, exact ? 2 : 1};  // one part (hi + lo, or hi only) per box
     mb = make_map_nd(bt.p, 4, bdims, bstr, bbox, SW128);
   }
   GemmP p{};
@@ -893,6 +904,7 @@ static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ld
   // triangular B: part-major order and the unneeded K chunks skipped (every
   // CTA streams the same Bᵀ chunks at the same time; measured 0.311 -> 0.295
   // ms at n = 406727); full B: parts of a tile side by side (0.351 vs 0.362)
+  p.bexact = exact ? 1 : 0;
   p.order = tri ? 1 : 0;
   p.skip = tri ? 1 : 0;
   const int64_t grid = std::min<int64_t>(p.nitems, c.num_sms);
@@ -908,14 +920,14 @@ void tc_gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t b
     Mat Cg = C;
     Cg.p = C.p + c0;
     Cg.cols = w;
-    tc_gemm_tall_impl(c, A, Bs + c0, ldb, w, deg, rexp, Cg, false);
+    tc_gemm_tall_impl(c, A, Bs + c0, ldb, w, deg, rexp, Cg, false, true);
   }
 }
 
 void tc_gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, int64_t bcols, const int32_t *deg,
-                      float rexp, const Mat &C) {
+                      float rexp, const Mat &C, bool exact) {
   NM_REQUIRE(bcols <= 288 && A.cols == bcols, "tc_gemm_tall_tri: square upper-triangular B, <= 288");
-  tc_gemm_tall_impl(c, A, Rinv, ldb, bcols, deg, rexp, C, true);
+  tc_gemm_tall_impl(c, A, Rinv, ldb, bcols, deg, rexp, C, true, exact);
 }
 
 }  // namespace netmfp
