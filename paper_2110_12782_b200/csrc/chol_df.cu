@@ -193,17 +193,24 @@ __device__ bool warp_chol_inv(double *S, double *X, double *rinv, const double *
 
 __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double S[32 * TL], A[32 * TL], B[32 * TL], D[32 * TL];
+  __shared__ double S[32 * TL], A[32 * TL], B[32 * TL], D[32 * TL], E[32 * TL];
   __shared__ int bad;
   __shared__ double piv[32], rinv[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // tile of this CTA: t -> (I, J), I >= J, column-major over the lower triangle
-  int t = blockIdx.x, J = 0;
-  while (t >= p.nb - J) {
-    t -= p.nb - J;
-    ++J;
+  // tile of this CTA: block 0 -> (0, 0); then the strictly lower tiles
+  // (I, J), I > J, column-major.  The sub-diagonal CTA (J+1, J) also owns the
+  // diagonal tile J+1 (accumulates its updates, factors it right after its own
+  // L_{J+1,J}): one flag hop per block step on the critical path, not two.
+  int I = 0, J = 0;
+  if (blockIdx.x > 0) {
+    int t = blockIdx.x - 1;
+    while (t >= p.nb - 1 - J) {
+      t -= p.nb - 1 - J;
+      ++J;
+    }
+    I = J + 1 + t;
   }
-  const int I = J + t;
+  const bool owns_diag = (I == J) || (I == J + 1);  // (0,0) or a sub-diagonal tile
   const int ib = min(32, p.l - 32 * I), jb = min(32, p.l - 32 * J);
   CDF_MARK(0);
   // save G (for shifted retries) and the original diagonal
@@ -224,13 +231,17 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
     const double shift = attempt == 0 ? 0.0 : maxdiag * 1e-7 * pow(100.0, (double)(attempt - 1));
     const int want = attempt + 1;
     bool alive = true;
-    // S = G_IJ (+ shift on the diagonal)
+    // S = G_IJ (+ shift on the diagonal); a sub-diagonal CTA also keeps the
+    // diagonal tile I in E
     CDF_MARK(8);
     load_tile(S, p.G0, p.l, 32 * I, 32 * J, ib, jb);
+    if (I == J + 1) load_tile(E, p.G0, p.l, 32 * I, 32 * I, ib, ib);
     __syncthreads();
     CDF_MARK(9);
     if (I == J)
       for (int i = threadIdx.x; i < ib; i += T) S[i * TL + i] += shift;
+    if (I == J + 1)
+      for (int i = threadIdx.x; i < ib; i += T) E[i * TL + i] += shift;
     // left-looking updates
     for (int K = 0; K < J && alive; ++K) {
       alive = wait_flag(p, p.lflag + I * p.nb + K, want, attempt) &&
@@ -240,11 +251,31 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
       load_tile(B, p.G, p.ld, 32 * J, 32 * K, jb, 32);
       __syncthreads();
       tile_sub_abt(S, A, B);
+      if (I == J + 1) tile_sub_abt(E, A, A);  // diagonal I: - L_IK L_IKᵀ
       __syncthreads();
     }
     CDF_MARK(4);
-    if (alive && I == J) {
-      // factor and invert the diagonal tile (warp 0); rows beyond ib are identity padding
+    if (alive && I != J) {
+      // L_IJ = S_IJ X_JJᵀ once the diagonal J is factored
+      alive = wait_flag(p, p.lflag + J * p.nb + J, want, attempt);
+      if (alive) {
+        load_tile(D, p.Rinv, p.l, 32 * J, 32 * J, jb, jb);  // X_JJ
+        __syncthreads();
+        tile_mul_abt(A, S, D);  // L_IJ
+        __syncthreads();
+        store_tile(p.G, p.ld, A, 32 * I, 32 * J, ib, jb);
+        publish(p.lflag + I * p.nb + J, want);
+        CDF_MARK(7);
+        if (I == J + 1) {  // the diagonal I gets its last update from this CTA's own tile
+          tile_sub_abt(E, A, A);
+          __syncthreads();
+          for (int i = threadIdx.x; i < 32 * TL; i += T) S[i] = E[i];
+          __syncthreads();
+        }
+      }
+    }
+    if (alive && owns_diag) {
+      // factor and invert the diagonal tile I (warp 0); rows beyond ib are identity padding
       if (threadIdx.x < 32) {
         for (int cc = 0; cc < 32; ++cc)
           if ((int)threadIdx.x >= ib) S[threadIdx.x * TL + cc] = (cc == (int)threadIdx.x) ? 1.0 : 0.0;
@@ -262,20 +293,9 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
         alive = false;
       } else {
         store_tile(p.G, p.ld, S, 32 * I, 32 * I, ib, ib);
-        store_tile(p.Rinv, p.l, D, 32 * I, 32 * I, ib, ib);  // X_II for the L_IJ GEMMs and the inverse
+        store_tile(p.Rinv, p.l, D, 32 * I, 32 * I, ib, ib);  // X_II for the L_JI GEMMs and the inverse
         CDF_MARK(13);
         publish(p.lflag + I * p.nb + I, want);
-        CDF_MARK(7);
-      }
-    } else if (alive) {
-      alive = wait_flag(p, p.lflag + J * p.nb + J, want, attempt);
-      if (alive) {
-        load_tile(D, p.Rinv, p.l, 32 * J, 32 * J, jb, jb);  // X_JJ
-        __syncthreads();
-        tile_mul_abt(A, S, D);  // L_IJ = S_IJ X_JJᵀ
-        __syncthreads();
-        store_tile(p.G, p.ld, A, 32 * I, 32 * J, ib, jb);
-        publish(p.lflag + I * p.nb + J, want);
         CDF_MARK(7);
       }
     }
@@ -291,10 +311,8 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
   if (attempt > 0 && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(p.flag, 1);
   // ---- inverse: X = L⁻¹
   const int want = 1;
-  if (I == J) {
-    // X_II = L_II⁻¹ was stored by the factorisation
-    publish(p.xflag + I * p.nb + I, want);
-  } else {
+  if (owns_diag) publish(p.xflag + I * p.nb + I, want);  // X_II = L_II⁻¹ was stored by the factorisation
+  if (I != J) {
     for (int i = threadIdx.x; i < 32 * TL; i += T) S[i] = 0.0;
     __syncthreads();
     for (int K = J; K < I; ++K) {
@@ -319,15 +337,17 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
   CDF_MARK(4);
   grid.sync();
   CDF_MARK(5);
-  // ---- Rinv = Xᵀ: this CTA transposes its own tile pair
-  if (I == J) {
+  // ---- Rinv = Xᵀ: this CTA transposes its own tile pair (and its diagonal)
+  if (owns_diag) {
     load_tile(A, p.Rinv, p.l, 32 * I, 32 * I, ib, ib);
     __syncthreads();
     for (int i = threadIdx.x; i < 32 * 32; i += T) {
       const int r = i >> 5, c = i & 31;
       if (r < ib && c < ib) p.Rinv[(int64_t)(32 * I + r) * p.l + 32 * I + c] = (c >= r) ? A[c * TL + r] : 0.0;
     }
-  } else {
+    __syncthreads();
+  }
+  if (I != J) {
     load_tile(A, p.Rinv, p.l, 32 * I, 32 * J, ib, jb);
     __syncthreads();
     for (int i = threadIdx.x; i < 32 * 32; i += T) {
@@ -341,11 +361,11 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
 
 }  // namespace cdf
 
-// G = RᵀR → Rinv = R⁻¹ on nb(nb+1)/2 co-resident CTAs (cooperative launch)
+// G = RᵀR → Rinv = R⁻¹ on 1 + nb(nb-1)/2 co-resident CTAs (cooperative launch)
 void chol_inv_df(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *flag) {
   using namespace cdf;
   const int nb = (int)ceil_div(l, 32);
-  const int tiles = nb * (nb + 1) / 2;
+  const int tiles = 1 + nb * (nb - 1) / 2;  // (0,0) and the strictly lower tiles
   DBuf<double> G0((size_t)l * l, c.stream);
   DBuf<int> flags((size_t)2 * nb * nb + 1, c.stream);
   NM_CUDA(cudaMemsetAsync(flags.p, 0, flags.n * sizeof(int), c.stream));

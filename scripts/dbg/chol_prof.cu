@@ -24,9 +24,9 @@ int main() {
     unsigned long long t[64 * 16];
     cudaMemcpyFromSymbol(t, g_cdf_t, sizeof(t));
     unsigned long long t0 = ~0ull;
-    for (int b = 0; b < 45; ++b) t0 = std::min(t0, t[b * 16]);
+    for (int b = 0; b < 37; ++b) t0 = std::min(t0, t[b * 16]);
     double mx[7] = {};
-    for (int b = 0; b < 45; ++b) for (int i = 0; i < 7; ++i) mx[i] = std::max(mx[i], (double)(t[b * 16 + i] - t0));
+    for (int b = 0; b < 37; ++b) for (int i = 0; i < 7; ++i) mx[i] = std::max(mx[i], (double)(t[b * 16 + i] - t0));
     if (rep == 2) {
       const int nb = 9;
       int base = 0;

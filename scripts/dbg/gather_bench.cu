@@ -11,7 +11,7 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
 }
 
 template <int ILP>
-__global__ void __launch_bounds__(256) k_gather(const float4 *__restrict__ X, uint32_t rows, int iters, float4 *out) {
+__global__ void k_gather(const float4 *__restrict__ X, uint32_t rows, int iters, float4 *out) {
   const int lane = threadIdx.x & 31;
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   float4 acc = make_float4(0, 0, 0, 0);
@@ -34,19 +34,25 @@ int main() {
   float4 *X, *out;
   cudaMalloc(&X, maxrows * 512); cudaMemset(X, 0, maxrows * 512); cudaMalloc(&out, 16);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  for (uint32_t rows : {1u << 14, 1u << 16, 1u << 17, 200000u, 1u << 18, 406727u, 1u << 20}) {
-    for (int bps : {4, 8}) {
-      const int grid = sms * bps, iters = 400;
-      for (int rep = 0; rep < 2; ++rep) {
-        cudaEventRecord(e0);
-        k_gather<4><<<grid, 256>>>(X, rows, iters, out);
-        cudaEventRecord(e1);
-        cudaEventSynchronize(e1);
-      }
-      float ms; cudaEventElapsedTime(&ms, e0, e1);
-      const double bytes = (double)grid * 8 * iters * 4 * 512;
-      printf("table %7.1f MB  blocks/SM %d: %.2f TB/s %s\n", rows * 512.0 / 1e6, bps, bytes / ms / 1e9,
-             cudaGetErrorString(cudaGetLastError()));
+  auto run = [&](auto kern, int ilp, uint32_t rows, int bps) {
+    const int grid = sms * bps, iters = 1600 / ilp;
+    float ms = 0;
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(e0);
+      kern<<<grid, 256>>>(X, rows, iters, out);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+    }
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double bytes = (double)grid * 8 * iters * ilp * 512;
+    printf("table %7.1f MB  ILP %2d blocks/SM %d: %.2f TB/s %s\n", rows * 512.0 / 1e6, ilp, bps, bytes / ms / 1e9,
+           cudaGetErrorString(cudaGetLastError()));
+  };
+  for (uint32_t rows : {1u << 16, 406727u}) {
+    for (int bps : {2, 4, 8}) {
+      run(k_gather<4>, 4, rows, bps);
+      run(k_gather<8>, 8, rows, bps);
+      run(k_gather<16>, 16, rows, bps);
     }
   }
   return 0;
