@@ -67,7 +67,9 @@ def dist_init():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
+        import torch
         import torch.distributed as td
+        torch.cuda.set_device(local)  # before the process group: NCCL binds the current device
         td.init_process_group("nccl", init_method="env://")
     return ws, rank, local
 
