@@ -250,28 +250,38 @@ void propagate(Ctx &c, const Graph &g, const Mat &E, int order, double mu, doubl
   const int64_t n = E.rows, d = E.cols;
   Block Z1(n, d, s), Acc(n, d, s);
   DBuf<float> xfull;  // all ranks' rows of the SpMM input (multi-GPU only)
-  // Z_1 = L~ E = -D^-1 A E ;  Acc = c0 E + c1 Z_1
+  // Z_1 = L~ E = -D^-1 A E ;  Acc = c0 E + c1 Z_1  (E is gathered: never its own output)
   SpmmArgs a;
   a.cols = d;
   a.X = dist_gather_rows(c, g, E, xfull); a.ldx = E.ld; a.Y = Z1.m.p; a.ldy = Z1.m.ld; a.a = 1.f; a.coef = -1.f;
   a.acc_in = E.p; a.ldai = E.ld; a.acc_out = Acc.m.p; a.ldacc = Acc.m.ld;
   a.acc_scale = (float)cf[0]; a.gamma = (float)cf[1];
+  if (order == 1) a.Y = nullptr;  // Z_1 itself is not needed
   spmm(c, g, a);
-  // Z_0 lives in E, Z_1 in Z1; Z_{r} overwrites Z_{r-2} in place
+  if (order == 1) {
+    copy_block(c, Acc.m.p, Acc.m.ld, E.p, E.ld, n, d);
+    return;
+  }
+  // Z_0 lives in E, Z_1 in Z1; Z_{r} overwrites Z_{r-2} in place.  The last
+  // step does not need Z_order: its accumulator goes to Z_{order-2}'s buffer
+  // (read there as prev by the same thread, not gathered), which is E when
+  // order is even.
   Mat zprev = E, zcur = Z1.m;
   for (int r = 2; r <= order; ++r) {
+    const bool last = r == order;
     SpmmArgs b;
     b.cols = d;
     b.X = dist_gather_rows(c, g, zcur, xfull); b.ldx = zcur.ld;
-    b.Y = zprev.p; b.ldy = zprev.ld;
+    b.Y = last ? nullptr : zprev.p; b.ldy = zprev.ld;
     b.prev = zprev.p; b.ldp = zprev.ld; b.beta = -1.f;
     b.a = 1.f; b.coef = -2.f;
-    b.acc_in = Acc.m.p; b.ldai = Acc.m.ld; b.acc_out = Acc.m.p; b.ldacc = Acc.m.ld; b.acc_scale = 1.f;
+    b.acc_in = Acc.m.p; b.ldai = Acc.m.ld; b.acc_scale = 1.f;
+    b.acc_out = last ? zprev.p : Acc.m.p; b.ldacc = last ? zprev.ld : Acc.m.ld;
     b.gamma = (float)cf[r];
     spmm(c, g, b);
     std::swap(zprev, zcur);
   }
-  copy_block(c, Acc.m.p, Acc.m.ld, E.p, E.ld, n, d);
+  if (zcur.p != E.p) copy_block(c, zcur.p, zcur.ld, E.p, E.ld, n, d);  // (after the swap: the last acc_out)
 }
 
 }  // namespace netmfp

@@ -301,7 +301,6 @@ struct GemmP {
   int ntot;       // MMA N total (multiple of 16)
   int nh, hr;     // output columns split into nh parts of hr (multiple of 32, <= 192) columns
   int c16;        // output columns rounded up to 16 (the last part is c16 - (nh-1) hr wide)
-  int bsplit;     // 1: Bᵀ raw fp32, lo formed in shared memory; 0: hi / lo from the host layout
   int order;      // item order (item_of)
   int skip;       // triangular B: skip the K chunks a part does not need
   int bexact;     // 1: A_hi B_hi + A_hi B_lo + A_lo B_hi; 0: B rounded to tf32, A_hi B + A_lo B
@@ -397,12 +396,9 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
             TCP_ADD(0);
           }
           uint8_t *st = base + s * stage_bytes;
-          mbar_expect_tx(&full[s], (uint32_t)(ABYTES + ((p.bsplit || !p.bexact) ? 1 : 2) * bbytes));
+          mbar_expect_tx(&full[s], (uint32_t)(ABYTES + (p.bexact ? 2 : 1) * bbytes));
           tma_load_2d(st, &tmA, kc * 32, (int)(t * 128), &full[s]);
-          if (p.bsplit)
-            tma_load_3d(st + ABYTES, &tmBh, 0, h * p.hr, kc, &full[s]);  // raw fp32 Bᵀ part (its lo is made below)
-          else
-            tma_load_4d(st + ABYTES, &tmBh, 0, 0, h, 2 * kc, &full[s]);  // hi and lo parts
+          tma_load_4d(st + ABYTES, &tmBh, 0, 0, h, 2 * kc, &full[s]);  // hi (and lo) parts
         }
       }
     }
@@ -488,7 +484,6 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
     int64_t g = 0;
     for (int64_t kq = 0, it = item_of(p, 0); it >= 0; ++kq, it = item_of(p, kq)) {
       const int h = (int)(it % p.nh);
-      const int brows = min(p.hr, p.c16 - h * p.hr);  // Bᵀ rows the MMAs read
       const int nkp = part_chunks(p, h);
       for (int kc = 0; kc < nkp; ++kc, ++g) {
         const int s = (int)(g % S);
@@ -497,19 +492,6 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
           TCP_T0();
           mbar_wait(&full[s], (uint32_t)(use & 1));
           if (wt == 0) TCP_ADD(3);
-        }
-        // Bᵀ lo = x - trunc_tf32(x) next to the raw (= hi) part, same swizzled
-        // positions; written through the generic proxy, read by the MMAs
-        // (async proxy) after the fence below
-        if (p.bsplit) {
-          const float4 *braw = reinterpret_cast<const float4 *>(base + s * stage_bytes + ABYTES);
-          float4 *blo = reinterpret_cast<float4 *>(base + s * stage_bytes + ABYTES + bbytes);
-          for (int i = wt; i < brows * 8; i += kWorkers) {
-            const float4 x = braw[i];
-            blo[i] = make_float4(x.x - tf32_trunc(x.x), x.y - tf32_trunc(x.y), x.z - tf32_trunc(x.z),
-                                 x.w - tf32_trunc(x.w));
-          }
-          fence_proxy_async_smem();
         }
         const uint8_t *rowp = base + s * stage_bytes + r * 128;
         float hi[32], lo[32];
@@ -817,21 +799,16 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
   NM_LAUNCH(c, "tc_gram_reduce", k_gram_reduce2<<<ceil_div(a * b, 256), 256, 0, c.stream>>>(tmp.p, RG, a, b, G, ldg, sym));
 }
 
-// Bᵀ for the tensor-core GEMM, zero padded to nrows × 32 nk.  split = 0:
-// Bt[kc][part][j][kk] with part 0 = hi = tf32(B[32 kc + kk][j]) and part 1 =
-// lo = B - hi.  split = 1: Bt[kc][j][kk] = fp32(B) (the kernel reads it as
-// tf32 hi and forms lo = x - trunc_tf32(x) in shared memory).
+// Bᵀ for the tensor-core GEMM, zero padded to nrows × 32 nk:
+// Bt[kc][part][j][kk] with part 0 = hi = tf32(B[32 kc + kk][j]) (round to
+// nearest) and part 1 = lo = B - hi
 __global__ void k_bt_split(const double *__restrict__ Bs, int64_t ldb, int64_t K, int64_t N, int64_t nrows, int64_t nk,
-                           float *__restrict__ Bt, int split) {
+                           float *__restrict__ Bt) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= nk * nrows * 32) return;
   const int64_t kk = idx & 31, j = (idx >> 5) % nrows, kc = idx / (32 * nrows);
   const int64_t k = kc * 32 + kk;
   const double x = (j < N && k < K) ? Bs[k * ldb + j] : 0.0;
-  if (split) {
-    Bt[idx] = (float)x;
-    return;
-  }
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"((float)x));
   const float h = __uint_as_float(r);
@@ -852,26 +829,14 @@ static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ld
   const int hr = ((c16 + nh - 1) / nh + 31) / 32 * 32;
   const int ntot = nh * hr;
   const int64_t nk = ceil_div(K, 32);
-  static const int bsplit = [] {
-    const char *v = getenv("NETMFP_GEMM_BSPLIT");
-    return v ? atoi(v) : 0;
-  }();
-  DBuf<float> bt((size_t)nk * (bsplit ? 1 : 2) * ntot * 32, c.stream);
+  DBuf<float> bt((size_t)nk * 2 * ntot * 32, c.stream);
   NM_LAUNCH(c, "bt_split", k_bt_split<<<ceil_div(nk * ntot * 32, 256), 256, 0, c.stream>>>(Bs, ldb, K, bcols, ntot, nk,
-                                                                                             bt.p, bsplit));
+                                                                                             bt.p));
   CUtensorMap ma = make_map(A.p, n, K, A.ld, 128);
-  CUtensorMap mb;
-  if (bsplit) {
-    const int64_t bdims[3] = {32, ntot, nk};
-    const int64_t bstr[2] = {128, (int64_t)ntot * 128};
-    const int bbox[3] = {32, hr, 1};  // one part of one K chunk per box
-    mb = make_map_nd(bt.p, 3, bdims, bstr, bbox, SW128);
-  } else {
-    const int64_t bdims[4] = {32, hr, nh, 2 * nk};
-    const int64_t bstr[3] = {128, (int64_t)hr * 128, (int64_t)ntot * 128};
-    const int bbox[4] = {32, hr, 1, exact ? 2 : 1};  // one part (hi + lo, or hi only) per box
-    mb = make_map_nd(bt.p, 4, bdims, bstr, bbox, SW128);
-  }
+  const int64_t bdims[4] = {32, hr, nh, 2 * nk};
+  const int64_t bstr[3] = {128, (int64_t)hr * 128, (int64_t)ntot * 128};
+  const int bbox[4] = {32, hr, 1, exact ? 2 : 1};  // one part (hi + lo, or hi only) per box
+  CUtensorMap mb = make_map_nd(bt.p, 4, bdims, bstr, bbox, SW128);
   GemmP p{};
   p.n = n;
   p.K = (int)K;
@@ -880,7 +845,6 @@ static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ld
   p.nh = nh;
   p.hr = hr;
   p.c16 = c16;
-  p.bsplit = bsplit;
   p.tri = tri ? 1 : 0;
   p.nitems = ceil_div(n, 128) * nh;
   p.C = C.p;

@@ -213,7 +213,7 @@ def test_sketch_svd_parity(L, ctx, graphs, name, k, d, s2, s3, logmode):
 
 # ---------------------------------------------------------------- propagation
 @pytest.mark.parametrize("name", list(GRAPHS))
-@pytest.mark.parametrize("order,d", [(0, 8), (1, 8), (2, 33), (10, 32)])
+@pytest.mark.parametrize("order,d", [(0, 8), (1, 8), (2, 33), (3, 16), (10, 32)])
 def test_propagate_parity(L, ctx, graphs, name, order, d):
     n, s, t, g, (rp, col, deg) = graphs[name]
     E0 = np.random.default_rng(order).standard_normal((n, d)).astype(np.float32)
