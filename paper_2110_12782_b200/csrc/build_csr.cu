@@ -1,7 +1,8 @@
 // build_csr.cu — row a1: CSR of the undirected simple graph.
 //
-// Edge pairs -> 64-bit keys (u<<32 | v) for both directions (self loops become a
-// sentinel row n) -> CUB radix sort -> unique -> rowptr by per-row binary search.
+// Edge pairs -> 64-bit keys (u << cb | v, cb = bits of a column id) for both
+// directions (self loops become a sentinel row n) -> CUB radix sort over the
+// 2 cb + 1 significant bits -> unique -> rowptr by per-row binary search.
 // Deterministic and bit-exact (integer work only).
 #include <cub/cub.cuh>
 
@@ -13,31 +14,32 @@
 namespace netmfp {
 
 __global__ void k_make_keys(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
-                            int64_t m, uint64_t n, uint64_t row0, uint64_t row1, uint64_t *__restrict__ keys,
+                            int64_t m, uint64_t n, uint64_t row0, uint64_t row1, int cb, uint64_t *__restrict__ keys,
                             int *bad) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= m) return;
   int32_t s = src[e], t = dst[e];
+  const uint64_t sentinel = n << cb;
   if (s < 0 || t < 0 || (uint64_t)s >= n || (uint64_t)t >= n) {
     atomicExch(bad, 1);
-    keys[2 * e] = keys[2 * e + 1] = n << 32;
+    keys[2 * e] = keys[2 * e + 1] = sentinel;
     return;
   }
   if (s == t) {  // self loop: dropped (sentinel row n sorts last)
-    keys[2 * e] = keys[2 * e + 1] = n << 32;
+    keys[2 * e] = keys[2 * e + 1] = sentinel;
   } else {
     // rows outside this rank's range [row0, row1) become the sentinel
-    keys[2 * e] = ((uint64_t)s >= row0 && (uint64_t)s < row1) ? (((uint64_t)s << 32) | (uint32_t)t) : (n << 32);
-    keys[2 * e + 1] = ((uint64_t)t >= row0 && (uint64_t)t < row1) ? (((uint64_t)t << 32) | (uint32_t)s) : (n << 32);
+    keys[2 * e] = ((uint64_t)s >= row0 && (uint64_t)s < row1) ? (((uint64_t)s << cb) | (uint32_t)t) : sentinel;
+    keys[2 * e + 1] = ((uint64_t)t >= row0 && (uint64_t)t < row1) ? (((uint64_t)t << cb) | (uint32_t)s) : sentinel;
   }
 }
 
 // rowptr[u] = first key index with row >= row0 + u (lower bound), u in [0, n]
-__global__ void k_rowptr(const uint64_t *__restrict__ keys, int64_t nnz, int64_t n, int64_t row0,
+__global__ void k_rowptr(const uint64_t *__restrict__ keys, int64_t nnz, int64_t n, int64_t row0, int cb,
                          int64_t *__restrict__ rowptr) {
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u > n) return;
-  uint64_t target = (uint64_t)(u + row0) << 32;
+  uint64_t target = (uint64_t)(u + row0) << cb;
   int64_t lo = 0, hi = nnz;
   while (lo < hi) {
     int64_t mid = (lo + hi) >> 1;
@@ -47,10 +49,10 @@ __global__ void k_rowptr(const uint64_t *__restrict__ keys, int64_t nnz, int64_t
 }
 
 __global__ void k_col_deg(const uint64_t *__restrict__ keys, int64_t nnz,
-                          const int64_t *__restrict__ rowptr, int64_t n, int32_t *__restrict__ col,
+                          const int64_t *__restrict__ rowptr, int64_t n, int cb, int32_t *__restrict__ col,
                           int32_t *__restrict__ deg, uint8_t *__restrict__ heavy_flag, int light_cap) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < nnz) col[i] = (int32_t)(keys[i] & 0xFFFFFFFFu);
+  if (i < nnz) col[i] = (int32_t)(keys[i] & ((1ull << cb) - 1));
   if (i < n) {
     int64_t dg = rowptr[i + 1] - rowptr[i];
     deg[i] = (int32_t)dg;
@@ -101,14 +103,15 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
   if (const char *v = getenv("NETMFP_HEAVY_SEG")) g->heavy_seg = std::max(1, atoi(v));
   try {
     int64_t nk = 2 * m;
+    const int cb = std::max(1, bits_for((uint64_t)(n_all - 1)));  // bits of a column id
     DBuf<uint64_t> keys(nk > 0 ? nk : 1, s), keys2(nk > 0 ? nk : 1, s);
     DBuf<int> bad(1, s);
     bad.zero();
     if (m > 0) {
       NM_LAUNCH(c, "make_keys", k_make_keys<<<ceil_div(m, 256), 256, 0, s>>>(src, dst, m, (uint64_t)n_all, (uint64_t)row0,
-                                                                             (uint64_t)row1, keys, bad));
+                                                                             (uint64_t)row1, cb, keys, bad));
     }
-    int end_bit = 32 + bits_for((uint64_t)n_all);
+    const int end_bit = cb + bits_for((uint64_t)n_all);  // key = row << cb | col, rows up to the sentinel n
     size_t tmp_bytes = 0, tmp2 = 0;
     DBuf<int64_t> nsel(1, s);
     if (nk > 0) {
@@ -134,7 +137,7 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
       uint64_t last = 0;
       NM_CUDA(cudaMemcpyAsync(&last, keys.p + nnz - 1, 8, cudaMemcpyDeviceToHost, s));
       NM_CUDA(cudaStreamSynchronize(s));
-      if ((last >> 32) == (uint64_t)n_all) --nnz;
+      if ((last >> cb) == (uint64_t)n_all) --nnz;
     }
     g->nnz = nnz;
     g->nnz_global = nnz;
@@ -142,9 +145,9 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
     g->col.alloc(nnz > 0 ? nnz : 1, s);
     g->deg.alloc(n, s);
     DBuf<uint8_t> hflag(n, s);
-    NM_LAUNCH(c, "rowptr", k_rowptr<<<ceil_div(n + 1, 256), 256, 0, s>>>(keys, nnz, n, row0, g->rowptr));
+    NM_LAUNCH(c, "rowptr", k_rowptr<<<ceil_div(n + 1, 256), 256, 0, s>>>(keys, nnz, n, row0, cb, g->rowptr));
     int64_t mx = std::max(nnz, n);
-    NM_LAUNCH(c, "col_deg", k_col_deg<<<ceil_div(mx, 256), 256, 0, s>>>(keys, nnz, g->rowptr, n, g->col, g->deg, hflag,
+    NM_LAUNCH(c, "col_deg", k_col_deg<<<ceil_div(mx, 256), 256, 0, s>>>(keys, nnz, g->rowptr, n, cb, g->col, g->deg, hflag,
                                                                              g->light_cap));
     // heavy rows (degree > kLightCap) for the split SpMM path
     {
