@@ -532,7 +532,7 @@ __device__ unsigned long long g_td_t[8][4][512];
 #else
 #define TD_MARK(ph)
 #endif
-constexpr int TDC = 8;     // cluster size (CTAs) for the tridiagonalisation
+constexpr int TDC = 8;     // cluster size (CTAs) for the tridiagonalisation (16: measured slower)
 // split cluster barrier (every thread arrives; release / acquire at cluster scope)
 __device__ __forceinline__ void cluster_arrive() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
@@ -571,7 +571,7 @@ __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
   double *pf = vbuf + 2 * l;               // l
   double *pl = pf + l;                     // nmax
   double *red = pl + nmax;                 // 40
-  double *xchg = red + 40;                 // [parity][TDC] partials, [16 + parity] beta
+  double *xchg = red + 40;                 // [parity][TDC] partials, [2 TDC + parity] beta
   for (int64_t idx = tid; idx < (int64_t)nloc * l; idx += nt) {
     int li = (int)(idx / l), k = (int)(idx % l);
     A[idx] = S[(int64_t)(li * TDC + rank) * l + k];
@@ -600,7 +600,7 @@ __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
       for (int r = 0; r < TDC; ++r) cl.map_shared_rank(v, r)[k] = val;
       Hv[(int64_t)j * l + k] = val;
     }
-    if (tid < TDC) cl.map_shared_rank(xchg, tid)[16 + par] = beta;
+    if (tid < TDC) cl.map_shared_rank(xchg, tid)[2 * TDC + par] = beta;
     if (tid == 0) {
       dd[j] = x[j];
       ee[j] = alpha;
@@ -616,7 +616,7 @@ __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
     TD_MARK(1);
     cluster_wait();  // S1(j): v_j, beta_j pushed
     TD_MARK(2);
-    const double beta = xchg[16 + par];
+    const double beta = xchg[2 * TDC + par];
     // (2) p_i = beta A[i, j+1:] · v for own rows i > j; partial vᵀp
     double part = 0.0;
     for (int li = wid; li < nloc; li += nt / 32) {
@@ -1022,11 +1022,12 @@ void sym_eig(Ctx &c, double *S, int64_t l64, double *lam, double *V, bool abs_or
   NM_CUDA(cudaMemsetAsync(hb.p, 0, (size_t)l * 8, s));
   NM_CUDA(cudaMemsetAsync(e.p, 0, (size_t)l * 8, s));
   const int nloc = (l + TDC - 1) / TDC;
-  size_t smem = ((size_t)nloc * l + 3 * l + nloc + 40 + 24) * sizeof(double);
+  size_t smem = ((size_t)nloc * l + 3 * l + nloc + 40 + 2 * TDC + 8) * sizeof(double);
   NM_REQUIRE(smem <= 227 * 1024 && l <= 32 * BT_NR, "sym_eig: l too large for the 8-CTA cluster (l <= ~470)");
   static bool attr = false;
   if (!attr) {
     NM_CUDA(cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    if (TDC > 8) NM_CUDA(cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }
   NM_LAUNCH(c, "tridiag", k_tridiag<<<TDC, TDT, smem, s>>>(S, l, d, e, Hv, hb));
