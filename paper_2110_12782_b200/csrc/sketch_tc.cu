@@ -24,7 +24,7 @@
 //               box each, issued by three lanes in parallel;
 //   warp 1      tcgen05.mma 3xTF32 (A_hi·B_hi + A_hi·B_lo + A_lo·B_hi) into one
 //               of two 256-column TMEM accumulators (double-buffered);
-//   warps 2-3   split the staged A chunk into lo parts (x − trunc_tf32(x));
+//   warps 2-3, 8-9  split the staged A chunk into lo parts (x − trunc_tf32(x));
 //   warps 4-7   epilogue: tcgen05.ld, f(scale·x)·sign, segmented sums; Y mode
 //               stages a row's 256/zp outputs per N tile in shared memory and
 //               writes them as one contiguous run; Z mode reduces zp lanes
@@ -48,14 +48,14 @@ namespace tcs {
 
 using namespace tc;
 
-constexpr int THREADS = 256;
+constexpr int THREADS = 320;
 constexpr int NW = 256;           // N tile per accumulator
 constexpr int BK = 32;             // K per stage (128-B swizzled rows)
 constexpr int ABYTES = 128 * 128;  // A chunk: 128 rows × 32 fp32
 constexpr int BBYTES = NW * 128;   // B chunk: NW rows × 32 fp32
 constexpr int STAGE = 2 * ABYTES + 2 * BBYTES;
 constexpr int S = 2;
-constexpr int kSplit = 64;  // split threads (warps 2-3)
+constexpr int kSplit = 128;  // split threads (warps 2-3 and 8-9)
 constexpr int kEpi = 128;   // epilogue threads (warps 4-7)
 
 struct SkP {
@@ -269,9 +269,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant_
         }
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < 4 || warp >= 8) {
     // split warps: A lo parts
-    const int st_id = threadIdx.x - 64;
+    const int st_id = warp < 4 ? threadIdx.x - 64 : threadIdx.x - 256 + 64;
     int64_t g = 0;
     for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
       const int nt0 = (int)(it % p.nsplit) * per, nt1 = min(p.ntn, nt0 + per);
