@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
   uint8_t *base = align1024(smem_raw);
   constexpr int ABYTES = 128 * 128;  // 128 rows × 32 fp32 (raw, SWIZZLE_128B)
   const int bbytes = p.hr * 128;     // one part of Bᵀ (hi or lo)
-  const int stage_bytes = ABYTES + 2 * bbytes;
+  const int stage_bytes = ABYTES + (p.bexact ? 2 : 1) * bbytes;  // Bᵀ lo only for the exact product
   const int S = p.stages;
   // epilogue staging: 4 warps × 2 buffers × (32 rows × 128 B, SWIZZLE_128B)
   uint8_t *stg = base + S * stage_bytes;  // stage_bytes is a multiple of 1024
@@ -853,7 +853,7 @@ static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ld
   p.deg = deg;
   p.rexp = rexp;
   const size_t staging = (size_t)4 * 2 * 4096;
-  const size_t stage = (size_t)128 * 128 + (size_t)2 * hr * 128;
+  const size_t stage = (size_t)128 * 128 + (size_t)(exact ? 2 : 1) * hr * 128;  // a multiple of 1024
   const int S = (int)std::min<size_t>(6, (kSmemMax - 1024 - 256 - staging) / stage);
   const int ST = std::min(4, (512 - 2 * hr) / 64);
   NM_REQUIRE(S >= 2 && ST >= 2, "tc_gemm_tall: stage does not fit");
