@@ -303,9 +303,13 @@ def run_ours(args):
         n_spmm_l = 2 * w.q + 2
         n_spmm_d = w.prop_order
         bytes_l = 8 * (nr + 1) + 4 * nnz + 2 * 4 * nr * l
-        # Chebyshev steps: X read, Y write, prev read (r>=2), acc read+write
-        bytes_d = 8 * (nr + 1) + 4 * nnz + 5 * 4 * nr * d
-        alg_bytes = n_spmm_l * bytes_l + n_spmm_d * bytes_d
+        # Chebyshev filter by Clenshaw (pipeline.cu propagate): n'×d block
+        # streams over the N steps — first (gather E, write b) 2, second
+        # (gather b, read E, write b) 3, middle steps (gather b, read b and E,
+        # write b) 4 each, last (gather b_1, read b_2 and E, write E) 4
+        N = w.prop_order
+        cheb_streams = 2 if N == 1 else (2 + 3 if N == 2 else 2 + 3 + 4 * (N - 3) + 4)
+        alg_bytes = n_spmm_l * bytes_l + n_spmm_d * (8 * (nr + 1) + 4 * nnz) + cheb_streams * 4 * nr * d
         per_step_ms = spmm_ms / args.steps
         achieved = alg_bytes / (per_step_ms * 1e-3) / 1e9
         traffic = None

@@ -239,49 +239,70 @@ void cheb_coeffs(int order, double mu, double theta, double *c) {
   for (int r = 0; r <= order; ++r) c[r] /= c0;
 }
 
-// E <- Σ_r c_r T_r(L~) E, L~ = -D^-1 A; Z_{r+1} = 2 L~ Z_r - Z_{r-1} fused in the SpMM
-// epilogue together with Acc += c_{r+1} Z_{r+1}.  E is used as Z_0 storage.
+// E <- Σ_{r=0}^{N} c_r T_r(L~) E, L~ = -D^-1 A (Chebyshev filter [R6]),
+// evaluated by Clenshaw's recurrence (the same polynomial):
+//   b_{N+1} = b_{N+2} = 0,  b_r = c_r E + 2 L~ b_{r+1} - b_{r+2} (r = N..1),
+//   result = c_0 E + L~ b_1 - b_2.
+// N SpMMs as the three-term forward recurrence, but each step streams two
+// blocks and writes one (gathered b_{r+1}; b_{r+2} and E read; b_r written
+// over b_{r+2} by the thread that read it) instead of streaming two and
+// writing two; b_N = c_N E is never materialised (folded into the next two
+// steps' multiple of E), and the last step writes the result into E.
 void propagate(Ctx &c, const Graph &g, const Mat &E, int order, double mu, double theta) {
   if (order <= 0) return;
   NM_REQUIRE(order <= 64, "propagate: order <= 64");
-  std::vector<double> cf(order + 1);
-  cheb_coeffs(order, mu, theta, cf.data());
+  const int N = order;
+  std::vector<double> cf(N + 1);
+  cheb_coeffs(N, mu, theta, cf.data());
   cudaStream_t s = c.stream;
   const int64_t n = E.rows, d = E.cols;
-  Block Z1(n, d, s), Acc(n, d, s);
+  Block B0(n, d, s), B1(n, d, s);
   DBuf<float> xfull;  // all ranks' rows of the SpMM input (multi-GPU only)
-  // Z_1 = L~ E = -D^-1 A E ;  Acc = c0 E + c1 Z_1  (E is gathered: never its own output)
-  SpmmArgs a;
-  a.cols = d;
-  a.X = dist_gather_rows(c, g, E, xfull); a.ldx = E.ld; a.Y = Z1.m.p; a.ldy = Z1.m.ld; a.a = 1.f; a.coef = -1.f;
-  a.acc_in = E.p; a.ldai = E.ld; a.acc_out = Acc.m.p; a.ldacc = Acc.m.ld;
-  a.acc_scale = (float)cf[0]; a.gamma = (float)cf[1];
-  if (order == 1) a.Y = nullptr;  // Z_1 itself is not needed
-  spmm(c, g, a);
-  if (order == 1) {
-    copy_block(c, Acc.m.p, Acc.m.ld, E.p, E.ld, n, d);
+  // one fused step: out = sE·E + coef·D^-1 A X (+ beta·prev)
+  auto step = [&](const Mat &X, double coef, const Mat *prev, double beta, double sE, const Mat &out) {
+    SpmmArgs a;
+    a.cols = d;
+    a.X = dist_gather_rows(c, g, X, xfull);
+    a.ldx = X.ld;
+    a.Y = nullptr;
+    a.a = 1.f;
+    a.coef = (float)coef;
+    if (prev) {
+      a.prev = prev->p;
+      a.ldp = prev->ld;
+      a.beta = (float)beta;
+    }
+    a.acc_in = E.p;
+    a.ldai = E.ld;
+    a.acc_scale = (float)sE;
+    a.gamma = 1.f;
+    a.acc_out = out.p;
+    a.ldacc = out.ld;
+    spmm(c, g, a);
+  };
+  if (N == 1) {  // c0 E + c1 L~ E: E is gathered, so the result goes through a scratch block
+    step(E, -cf[1], nullptr, 0.0, cf[0], B0.m);
+    copy_block(c, B0.m.p, B0.m.ld, E.p, E.ld, n, d);
     return;
   }
-  // Z_0 lives in E, Z_1 in Z1; Z_{r} overwrites Z_{r-2} in place.  The last
-  // step does not need Z_order: its accumulator goes to Z_{order-2}'s buffer
-  // (read there as prev by the same thread, not gathered), which is E when
-  // order is even.
-  Mat zprev = E, zcur = Z1.m;
-  for (int r = 2; r <= order; ++r) {
-    const bool last = r == order;
-    SpmmArgs b;
-    b.cols = d;
-    b.X = dist_gather_rows(c, g, zcur, xfull); b.ldx = zcur.ld;
-    b.Y = last ? nullptr : zprev.p; b.ldy = zprev.ld;
-    b.prev = zprev.p; b.ldp = zprev.ld; b.beta = -1.f;
-    b.a = 1.f; b.coef = -2.f;
-    b.acc_in = Acc.m.p; b.ldai = Acc.m.ld; b.acc_scale = 1.f;
-    b.acc_out = last ? zprev.p : Acc.m.p; b.ldacc = last ? zprev.ld : Acc.m.ld;
-    b.gamma = (float)cf[r];
-    spmm(c, g, b);
-    std::swap(zprev, zcur);
+  // b_{N-1} = c_{N-1} E + 2 L~ (c_N E)
+  Mat bnext = B0.m, bcur = B1.m;  // b_{r+1}, and the buffer b_r will overwrite (b_{r+2})
+  step(E, -2.0 * cf[N], nullptr, 0.0, cf[N - 1], bnext);
+  // b_{N-2} = c_{N-2} E + 2 L~ b_{N-1} - c_N E   (b_N not materialised)
+  // ... b_r = c_r E + 2 L~ b_{r+1} - b_{r+2}, b_r over b_{r+2}
+  for (int r = N - 2; r >= 1; --r) {
+    if (r == N - 2)
+      step(bnext, -2.0, nullptr, 0.0, cf[r] - cf[N], bcur);
+    else
+      step(bnext, -2.0, &bcur, -1.0, cf[r], bcur);
+    std::swap(bnext, bcur);  // bnext = b_r, bcur = b_{r+1}
   }
-  if (zcur.p != E.p) copy_block(c, zcur.p, zcur.ld, E.p, E.ld, n, d);  // (after the swap: the last acc_out)
+  // result = c_0 E + L~ b_1 - b_2 into E (E read and written per element by
+  // one thread, not gathered); N == 2: b_2 = c_2 E
+  if (N == 2)
+    step(bnext, -1.0, nullptr, 0.0, cf[0] - cf[2], E);
+  else
+    step(bnext, -1.0, &bcur, -1.0, cf[0], E);
 }
 
 }  // namespace netmfp

@@ -6,10 +6,10 @@ B="python bench.py --steps 1 --warmup 3 --no-cpu"
 timeout 900 $B > gpurun_out/plain.log 2>&1 && \
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 5000 --csv \
     --log-file gpurun_out/launches_r01.csv $B > gpurun_out/ncu_launch.log 2>&1; echo ncu=$?
-# SpMM: one 286-column application (2 launches) of the 4th step, then one Chebyshev application
+# SpMM: one 286-column application (2 launches) of the 4th step, then one middle Chebyshev (Clenshaw) step
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_spmm_fused -s 114 -c 2 \
     -o gpurun_out/prof_spmm286_r01 $B > gpurun_out/ncu_full1.log 2>&1; echo ncufull1=$?
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_spmm_fused -s 142 -c 1 \
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_spmm_fused -s 145 -c 1 \
     -o gpurun_out/prof_spmm128_r01 $B > gpurun_out/ncu_full2.log 2>&1; echo ncufull2=$?
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_gemm_tc|k_gram_tc|k_sketch_tc|k_chol_df" -s 60 -c 12 \
     -o gpurun_out/prof_tc_r01 $B > gpurun_out/ncu_full3.log 2>&1; echo ncufull3=$?
