@@ -875,8 +875,47 @@ __global__ void __launch_bounds__(IVW * 32) k_invit(const double *__restrict__ d
         piv[i] = 1;
       }
     }
-    for (int i = 0; i < l; ++i)
+    for (int i = 0; i < l; ++i) {
       if (fabs(dg[i]) < tiny) dg[i] = dg[i] < 0 ? -tiny : tiny;
+      dg[i] = 1.0 / dg[i];  // the solves multiply by the reciprocal pivots
+    }
+  }
+  __syncwarp();
+  if (m1 - m0 == 1) {
+    // isolated eigenvalue (the common case): the vector lives in shared
+    // memory (after the LU factors), lane 0 runs the substitutions
+    int8_t *piv_end = reinterpret_cast<int8_t *>(ivs + (int64_t)IVW * 4 * l) + ((IVW * l + 7) & ~7);
+    double *x = reinterpret_cast<double *>(piv_end) + (int64_t)wib * l;
+    for (int i = ln; i < l; i += 32) {
+      U4 r = philox4x32_10(U4{(uint32_t)i, (uint32_t)m0, 0x494E5649u, 0u}, seed, 0x5EEDu);
+      x[i] = ((double)r.x + 0.5) * 2.3283064365386963e-10 - 0.5;
+    }
+    __syncwarp();
+    for (int it = 0; it < 3; ++it) {
+      if (ln == 0) {
+        for (int i = 0; i + 1 < l; ++i) {
+          if (!piv[i]) {
+            x[i + 1] -= dl[i] * x[i];
+          } else {
+            const double t = x[i];
+            x[i] = x[i + 1];
+            x[i + 1] = t - dl[i] * x[i];
+          }
+        }
+        x[l - 1] *= dg[l - 1];
+        if (l > 1) x[l - 2] = (x[l - 2] - du[l - 2] * x[l - 1]) * dg[l - 2];
+        for (int i = l - 3; i >= 0; --i) x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) * dg[i];
+      }
+      __syncwarp();
+      double nrm = 0.0;
+      for (int i = ln; i < l; i += 32) nrm += x[i] * x[i];
+      nrm = sqrt(warp_sum(nrm));
+      const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+      for (int i = ln; i < l; i += 32) x[i] *= inv;
+      __syncwarp();
+    }
+    for (int i = ln; i < l; i += 32) Zt[(int64_t)m0 * l + i] = x[i];
+    return;
   }
   // deterministic random starts in the output rows
   for (int m = m0; m < m1; ++m)
@@ -898,9 +937,9 @@ __global__ void __launch_bounds__(IVW * 32) k_invit(const double *__restrict__ d
           x[i + 1] = t - dl[i] * x[i];
         }
       }
-      x[l - 1] /= dg[l - 1];
-      if (l > 1) x[l - 2] = (x[l - 2] - du[l - 2] * x[l - 1]) / dg[l - 2];
-      for (int i = l - 3; i >= 0; --i) x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) / dg[i];
+      x[l - 1] *= dg[l - 1];
+      if (l > 1) x[l - 2] = (x[l - 2] - du[l - 2] * x[l - 1]) * dg[l - 2];
+      for (int i = l - 3; i >= 0; --i) x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) * dg[i];
     }
     __syncwarp();
     // modified Gram-Schmidt over the cluster
@@ -1037,7 +1076,7 @@ void sym_eig(Ctx &c, double *S, int64_t l64, double *lam, double *V, bool abs_or
   int hncl = 0;
   NM_CUDA(cudaMemcpyAsync(&hncl, ncl.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   NM_CUDA(cudaStreamSynchronize(s));
-  const size_t ivsm = (size_t)IVW * 4 * l * sizeof(double) + (size_t)IVW * l + 16;
+  const size_t ivsm = (size_t)IVW * 4 * l * sizeof(double) + (size_t)IVW * l + 16 + (size_t)IVW * l * sizeof(double);
   static bool attr_iv = false;
   if (!attr_iv) {
     NM_CUDA(cudaFuncSetAttribute(k_invit, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
