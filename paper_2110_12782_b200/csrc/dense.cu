@@ -115,10 +115,10 @@ bool tc_enabled() {
   return on != 0;
 }
 
-void gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg) {
+void gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg, bool exact) {
   NM_REQUIRE(A.rows == B.rows, "gram: row mismatch");
   if (tc_enabled() && A.rows >= 128) {
-    tc_gram(c, A, B, deg, wexp, G, ldg);
+    tc_gram(c, A, B, deg, wexp, G, ldg, exact);
     return;
   }
   const int64_t n = A.rows;

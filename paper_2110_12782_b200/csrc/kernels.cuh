@@ -50,7 +50,10 @@ void deg_pow(Ctx &c, const Graph &g, float e, float *out);  // out[i] = d_i^-e (
 // G[a×b] (fp64, row-major ldg) = Σ_i w_i A[i,:a]ᵀ B[i,:b]; w optional (row weight
 // d_i^-e when wexp != 0, computed from deg).  If A == B and a == b only the
 // upper triangle is computed and mirrored.
-void gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg);
+// exact = false: tf32 products only (~1e-3 relative; for CholeskyQR passes
+// whose output only needs to be a well-conditioned basis of the same span)
+void gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg,
+          bool exact = true);
 // C[n×b] = rs_i · (A[n×a] · Bs[a×b]) with Bs fp64 small (converted to fp32),
 // rs_i = d_i^-e (e = rexp, deg != null) else 1.
 void gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcols, const int32_t *deg,
@@ -58,7 +61,8 @@ void gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcol
 // tensor-core (tcgen05, 3xTF32) versions; shapes: bcols / B.cols <= 288
 void tc_gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcols, const int32_t *deg,
                   float rexp, const Mat &C);
-void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg);
+void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg,
+             bool exact = true);
 void tc_gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, int64_t bcols, const int32_t *deg,
                       float rexp, const Mat &C, bool exact = true);
 // C = rs · A · Rinv with Rinv (a×a) upper triangular (CholeskyQR's Y R⁻¹).  exact =

@@ -23,9 +23,10 @@ static void check_flag(Ctx &c, const char *what) {
 // passes = 2 gives CholeskyQR2 (second pass on the materialised Y R1⁻¹ in tmp).
 // orthonormal = false (a power iteration's intermediate basis, which the next
 // iteration re-orthonormalises; only its span matters) and every pass but the
-// last of a CholeskyQR2: the product uses R⁻¹ rounded to tf32 (exactly that
-// basis change: same span, columns orthonormal to ~1e-3), 2 tensor-core
-// products instead of 3.
+// last of a CholeskyQR2: the Gram is a single tf32 product and the basis
+// change uses R⁻¹ rounded to tf32 (any invertible R keeps the span; the
+// columns come out orthonormal to ~1e-3), 1 and 2 tensor-core products
+// instead of 3.
 void cholqr(Ctx &c, const Mat &Y, const Mat &out, const int32_t *deg, float rexp, int passes,
             const Mat *tmp, bool orthonormal) {
   NM_STAGE(c, "stage_cholqr");
@@ -34,7 +35,9 @@ void cholqr(Ctx &c, const Mat &Y, const Mat &out, const int32_t *deg, float rexp
   DBuf<double> G((size_t)l * l, s), Rinv((size_t)l * l, s);
   Mat cur = Y;
   for (int ps = 0; ps < passes; ++ps) {
-    gram(c, cur, cur, nullptr, 0.f, G, l);
+    // the Gram of a pass whose output is only an intermediate basis (not the
+    // last pass of an orthonormal CholeskyQR) need not be fp32-accurate
+    gram(c, cur, cur, nullptr, 0.f, G, l, orthonormal && ps + 1 == passes);
     dist_allreduce(c, G, (size_t)l * l, DType::F64);  // Gram over all ranks' rows
     chol_inv_upper(c, G, l, l, Rinv, c.d_flags);
     const bool last = (ps + 1 == passes);

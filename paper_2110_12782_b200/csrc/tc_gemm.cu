@@ -74,6 +74,7 @@ struct GramP {
   const float *wrow;    // optional per-row weights (d^-wexp, or its square root applied to both sides if sym)
   int64_t part_stride;  // floats per chain partial
   float *part;
+  int exact;            // 1: 3xTF32 (A_hi B_hi + A_hi B_lo + A_lo B_hi); 0: A_hi B_hi only (no lo parts)
 };
 
 template <int BK, bool SYM>
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUten
   uint8_t *base = align1024(smem_raw);
   constexpr int BLK = BK * 128;  // bytes of one 32-col block of BK rows
   const int nblk = p.na_blk + (SYM ? 0 : p.nb_blk);
-  const int stage_bytes = 2 * nblk * BLK;  // raw + lo
+  const int stage_bytes = (p.exact ? 2 : 1) * nblk * BLK;  // raw (+ lo)
   const int S = p.stages;
   uint64_t *bars = reinterpret_cast<uint64_t *>(base + S * stage_bytes + 3 * BLK);
   uint64_t *full = bars, *split = bars + S, *empty = bars + 2 * S, *done = bars + 3 * S;
@@ -166,8 +167,10 @@ __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUten
             const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
             if (leader) {
               mma_tf32(ud[ui], dA + uao[ui] + ko, dB + ubo[ui] + ko, uid[ui], acc0);
-              mma_tf32(ud[ui], dA + uao[ui] + ko, dBl + ubo[ui] + ko, uid[ui], 1u);
-              mma_tf32(ud[ui], dAl + uao[ui] + ko, dB + ubo[ui] + ko, uid[ui], 1u);
+              if (p.exact) {
+                mma_tf32(ud[ui], dA + uao[ui] + ko, dBl + ubo[ui] + ko, uid[ui], 1u);
+                mma_tf32(ud[ui], dAl + uao[ui] + ko, dB + ubo[ui] + ko, uid[ui], 1u);
+              }
             }
           }
         }
@@ -201,12 +204,14 @@ __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUten
             reinterpret_cast<float4 *>(raw)[i] = v;
           }
         }
-        float4 l;
-        l.x = v.x - tf32_trunc(v.x);
-        l.y = v.y - tf32_trunc(v.y);
-        l.z = v.z - tf32_trunc(v.z);
-        l.w = v.w - tf32_trunc(v.w);
-        reinterpret_cast<float4 *>(lo)[i] = l;
+        if (p.exact) {
+          float4 l;
+          l.x = v.x - tf32_trunc(v.x);
+          l.y = v.y - tf32_trunc(v.y);
+          l.z = v.z - tf32_trunc(v.z);
+          l.w = v.w - tf32_trunc(v.w);
+          reinterpret_cast<float4 *>(lo)[i] = l;
+        }
       }
       fence_async_smem();
       mbar_arrive(&split[s]);
@@ -665,7 +670,7 @@ static void launch_gram(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, tc
                         int ngroup_units_offset) {
   (void)ngroup_units_offset;
   const int nblk = p.na_blk + (SYM ? 0 : p.nb_blk);
-  const size_t stage = (size_t)2 * nblk * BK * 128;
+  const size_t stage = (size_t)(p.exact ? 2 : 1) * nblk * BK * 128;
   int S = (int)std::min<size_t>(6, (kSmemMax - 1024 - 256 - kPadBlocks * BK * 128) / stage);
   NM_REQUIRE(S >= 2, "tc_gram: too many columns for the staged chunk");
   p.stages = S;
@@ -684,7 +689,7 @@ __global__ void k_gram_wrow(const int32_t *__restrict__ deg, int64_t n, float e,
 }
 
 // G[a×b] (fp64, ldg) = Aᵀ diag(d^-wexp) B over the n rows
-void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg) {
+void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg, bool exact) {
   using namespace tc;
   NM_REQUIRE(A.rows == B.rows, "tc_gram: row mismatch");
   const int64_t n = A.rows, a = A.cols, b = B.cols;
@@ -778,6 +783,7 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
     p.wrow = wrow.p;
     p.part_stride = total;
     p.part = part.p;
+    p.exact = exact ? 1 : 0;
     if (sym)
       launch_gram<BKs, true>(c, ma, mb, p, nchain, 0);
     else
