@@ -88,8 +88,21 @@ static void check_mem(int mem) {
 }
 
 static void finish(Ctx &c) {
+  int h = 0;
+  if (!c.flag_checks.empty())
+    NM_CUDA(cudaMemcpyAsync(&h, c.d_flags, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   NM_CUDA(cudaStreamSynchronize(c.stream));
   prof_collect(c);
+  if (!c.flag_checks.empty()) {
+    const std::string what = c.flag_checks.front();
+    c.flag_checks.clear();
+    if (h & (1 << 30)) {
+      NM_CUDA(cudaMemset(c.d_flags, 0, sizeof(int)));
+      throw Error(NETMFP_ERR_NUMERIC, what +
+                                          ": Gram matrix not positive definite even after shifting "
+                                          "(input not of full column rank, PAPER.md:215)");
+    }
+  }
 }
 
 }  // namespace netmfp

@@ -68,6 +68,9 @@ struct Ctx {
   int nranks = 1, rank = 0;
   void *comm = nullptr;  // ncclComm_t
   int64_t collectives = 0;
+  // numeric checks deferred to the end of the ABI call (one synchronisation):
+  // the stage whose Cholesky failure bit (d_flags & 1<<30) is reported
+  std::vector<const char *> flag_checks;
 };
 
 inline bool prof_match(const Ctx &c, const char *name) {

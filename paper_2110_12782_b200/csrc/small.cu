@@ -825,12 +825,12 @@ constexpr int IVW = 4;  // warps per block
 
 __global__ void __launch_bounds__(IVW * 32) k_invit(const double *__restrict__ d, const double *__restrict__ e,
                                                     int l, const double *__restrict__ w,
-                                                    const int *__restrict__ cstart, int ncl,
+                                                    const int *__restrict__ cstart, const int *__restrict__ ncl_dev,
                                                     double *__restrict__ Zt, uint32_t seed) {
   extern __shared__ double ivs[];
   const int wib = threadIdx.x / 32, ln = threadIdx.x % 32;
   const int gw = blockIdx.x * IVW + wib;
-  if (gw >= ncl) return;
+  if (gw >= *ncl_dev) return;  // launched for the worst case (every eigenvalue isolated)
   double *dl = ivs + (int64_t)wib * 4 * l;
   double *dg = dl + l, *du = dg + l, *du2 = du + l;
   int8_t *piv = reinterpret_cast<int8_t *>(ivs + (int64_t)IVW * 4 * l) + wib * l;
@@ -1073,16 +1073,13 @@ void sym_eig(Ctx &c, double *S, int64_t l64, double *lam, double *V, bool abs_or
   NM_LAUNCH(c, "multisect", k_multisect<<<ceil_div(l, MSW), MSW * 32, (size_t)2 * l * sizeof(double), s>>>(d, e, l, w));
   DBuf<int> cst(l + 1, s), ncl(1, s);
   NM_LAUNCH(c, "clusters", k_clusters<<<1, 32, 0, s>>>(w, d, e, l, cst, ncl));
-  int hncl = 0;
-  NM_CUDA(cudaMemcpyAsync(&hncl, ncl.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-  NM_CUDA(cudaStreamSynchronize(s));
   const size_t ivsm = (size_t)IVW * 4 * l * sizeof(double) + (size_t)IVW * l + 16 + (size_t)IVW * l * sizeof(double);
   static bool attr_iv = false;
   if (!attr_iv) {
     NM_CUDA(cudaFuncSetAttribute(k_invit, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_iv = true;
   }
-  NM_LAUNCH(c, "invit", k_invit<<<ceil_div(hncl, IVW), IVW * 32, ivsm, s>>>(d, e, l, w, cst, hncl, Zt, 0x1234567u));
+  NM_LAUNCH(c, "invit", k_invit<<<ceil_div(l, IVW), IVW * 32, ivsm, s>>>(d, e, l, w, cst, ncl, Zt, 0x1234567u));
   NM_LAUNCH(c, "backtransform", k_backtransform<<<ceil_div((int64_t)l * 32, 256), 256, 0, s>>>(Hv, hb, l, Zt));
   NM_LAUNCH(c, "eig_sort", k_eig_sort<<<l, 128, 0, s>>>(w, Zt, l, abs_order, lam, V));
 }
