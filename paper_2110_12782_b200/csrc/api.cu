@@ -5,6 +5,8 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -505,15 +507,47 @@ static const Graph *embed_graph(Ctx &c, const Graph &g, const netmfp_params &p) 
   return g.compact.get();
 }
 
-static void embed_impl(Ctx &c, const Graph &g_in, const netmfp_params &p, const Mat &E_out, double *sigma_dev,
+// Host-side zeroing of a pinned output while the GPU computes (see
+// embed_host_pinned): worker threads memset E's rows, joined before the GPU
+// writes the non-isolated rows.
+struct HostZero {
+  std::vector<std::thread> th;
+  HostZero(float *E, int64_t n, int64_t d, int64_t lde) {
+    const int T = (int)std::max<unsigned>(1, std::min<unsigned>(16, std::thread::hardware_concurrency()));
+    for (int t = 0; t < T; ++t)
+      th.emplace_back([=] {
+        const int64_t r0 = n * t / T, r1 = n * (t + 1) / T;
+        if (lde == d)
+          memset(E + r0 * lde, 0, (size_t)(r1 - r0) * d * sizeof(float));
+        else
+          for (int64_t r = r0; r < r1; ++r) memset(E + r * lde, 0, (size_t)d * sizeof(float));
+      });
+  }
+  void join() {
+    for (auto &t : th)
+      if (t.joinable()) t.join();
+  }
+  ~HostZero() { join(); }
+};
+
+// Device pointer through which the GPU can write a host buffer directly
+// (pinned, mapped memory under unified addressing), or nullptr.
+static float *mapped_device_ptr(float *E) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, E) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return (a.type == cudaMemoryTypeHost && a.devicePointer) ? static_cast<float *>(a.devicePointer) : nullptr;
+}
+
+// Alg. 5 on graph g (compacted or not); E has g.n rows.
+static void embed_core(Ctx &c, const Graph &g, const netmfp_params &p, const Mat &E, double *sigma_dev,
                        double *lambda_dev) {
   NM_REQUIRE(p.T >= 1 && p.b > 0, "embed: need T >= 1, b > 0");
   cudaStream_t s = c.stream;
-  const Graph &g = *embed_graph(c, g_in, p);
-  const bool compacted = &g != &g_in;
+  const bool compacted = g.n_orig != 0;
   const int64_t n = g.n;
-  Block Ec(compacted ? n : 0, p.d, s);
-  const Mat E = compacted ? Ec.m : E_out;
   Block U(n, p.k, s), F(n, p.k, s);
   DBuf<double> lam(p.k, s), C((size_t)p.k * p.k, s);
   {
@@ -538,7 +572,36 @@ static void embed_impl(Ctx &c, const Graph &g_in, const netmfp_params &p, const 
     NM_STAGE(c, "stage_propagate");
     propagate(c, g, E, p.prop_order, p.mu, p.theta);                   // step 6
   }
-  if (compacted) scatter_rows(c, E, g.comp_id.p, E_out);             // isolated vertices: zero rows [R2]
+}
+
+static void embed_impl(Ctx &c, const Graph &g_in, const netmfp_params &p, const Mat &E_out, double *sigma_dev,
+                       double *lambda_dev) {
+  const Graph &g = *embed_graph(c, g_in, p);
+  if (&g == &g_in) {
+    embed_core(c, g, p, E_out, sigma_dev, lambda_dev);
+    return;
+  }
+  Block Ec(g.n, p.d, c.stream);
+  embed_core(c, g, p, Ec.m, sigma_dev, lambda_dev);
+  scatter_rows(c, Ec.m, g.comp_id.p, E_out);  // isolated vertices: zero rows [R2]
+}
+
+// Host output, compacted graph, pinned E: the host zeroes E (threads, while
+// the GPU computes) and the GPU then writes only the n' non-isolated rows
+// straight into it — n' instead of n rows cross the host link.  Returns false
+// (nothing done) when the path does not apply.
+static bool embed_host_pinned(Ctx &c, const Graph &g_in, const netmfp_params &p, float *E, int64_t lde,
+                              double *sigma_dev, double *lambda_dev) {
+  const Graph &g = *embed_graph(c, g_in, p);
+  float *Edev = (&g != &g_in) ? mapped_device_ptr(E) : nullptr;
+  if (!Edev) return false;
+  HostZero zero(E, g_in.n, p.d, lde);
+  Block Ec(g.n, p.d, c.stream);
+  embed_core(c, g, p, Ec.m, sigma_dev, lambda_dev);
+  zero.join();
+  Mat Eh{Edev, g.n_orig, p.d, lde};
+  write_rows(c, Ec.m, g.orig_id.p, Eh);
+  return true;
 }
 
 int netmfp_embed(netmfp_ctx *ctx, const netmfp_graph *gr, const netmfp_params *p, float *E, int64_t lde,
@@ -548,10 +611,13 @@ int netmfp_embed(netmfp_ctx *ctx, const netmfp_graph *gr, const netmfp_params *p
     check_mem(mem);
     Ctx &c = ctx->c;
     const Graph &g = *gr->g;
-    InMat eo(c, E, g.n, p->d, lde, mem, false);
+    NM_REQUIRE(lde >= p->d, "embed: lde < d");
     InVec<double> so(c, sigma, p->d, mem, false), lo(c, lambda, p->k, mem, false);
-    embed_impl(c, g, *p, eo.m, so.p, lo.p);
-    eo.copy_out(c, E, lde, mem);
+    if (!(mem == NETMFP_MEM_HOST && embed_host_pinned(c, g, *p, E, lde, so.p, lo.p))) {
+      InMat eo(c, E, g.n, p->d, lde, mem, false);
+      embed_impl(c, g, *p, eo.m, so.p, lo.p);
+      eo.copy_out(c, E, lde, mem);
+    }
     so.copy_out(c, sigma, p->d, mem);
     lo.copy_out(c, lambda, p->k, mem);
     finish(c);
@@ -570,10 +636,13 @@ int netmfp_embed_edges(netmfp_ctx *ctx, int64_t n, const int32_t *src, const int
       NM_STAGE(c, "stage_build_csr");
       g.reset(build_csr_device(c, n, s.p, t.p, m_in));
     }
-    InMat eo(c, E, n, p->d, lde, mem, false);
+    NM_REQUIRE(lde >= p->d, "embed_edges: lde < d");
     InVec<double> so(c, sigma, p->d, mem, false);
-    embed_impl(c, *g, *p, eo.m, so.p, nullptr);
-    eo.copy_out(c, E, lde, mem);
+    if (!(mem == NETMFP_MEM_HOST && embed_host_pinned(c, *g, *p, E, lde, so.p, nullptr))) {
+      InMat eo(c, E, n, p->d, lde, mem, false);
+      embed_impl(c, *g, *p, eo.m, so.p, nullptr);
+      eo.copy_out(c, E, lde, mem);
+    }
     so.copy_out(c, sigma, p->d, mem);
     finish(c);
   });

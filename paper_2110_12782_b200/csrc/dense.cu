@@ -336,4 +336,29 @@ void scatter_rows(Ctx &c, const Mat &Src, const int32_t *comp, const Mat &Dst) {
   NM_LAUNCH(c, "scatter_rows", k_scatter_rows<<<blocks, 256, 0, c.stream>>>(Src, comp, Dst, vec4));
 }
 
+// Dst[ids[j], :] = Src[j, :] for every row j of Src (the other rows of Dst
+// untouched); Dst may be mapped host memory.  A warp per row.
+__global__ void __launch_bounds__(256) k_write_rows(Mat Src, const int32_t *__restrict__ ids, Mat Dst, bool vec4) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  for (int64_t j = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); j < Src.rows; j += nw) {
+    float *d = Dst.p + (int64_t)ids[j] * Dst.ld;
+    const float *src = Src.p + j * Src.ld;
+    if (vec4) {
+      for (int64_t c = 4 * lane; c < Src.cols; c += 128)
+        *reinterpret_cast<float4 *>(d + c) = *reinterpret_cast<const float4 *>(src + c);
+    } else {
+      for (int64_t c = lane; c < Src.cols; c += 32) d[c] = src[c];
+    }
+  }
+}
+
+void write_rows(Ctx &c, const Mat &Src, const int32_t *ids, const Mat &Dst) {
+  if (Src.rows * Src.cols == 0) return;
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(Src.rows, 8), (int64_t)c.num_sms * 16);
+  const bool vec4 = Src.cols % 4 == 0 && Dst.ld % 4 == 0 && Src.ld % 4 == 0 && ((uintptr_t)Dst.p & 15) == 0 &&
+                    ((uintptr_t)Src.p & 15) == 0;
+  NM_LAUNCH(c, "write_rows", k_write_rows<<<blocks, 256, 0, c.stream>>>(Src, ids, Dst, vec4));
+}
+
 }  // namespace netmfp

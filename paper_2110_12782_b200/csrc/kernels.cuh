@@ -80,6 +80,8 @@ void scale_copy_block(Ctx &c, const Mat &Src, const Mat &Dst, const int32_t *deg
 void row_scale_block(Ctx &c, const Mat &Y, const int32_t *deg, float rexp);
 // Dst[i, :] = Src[comp[i], :] (0 where comp[i] < 0)
 void scatter_rows(Ctx &c, const Mat &Src, const int32_t *comp, const Mat &Dst);
+// Dst[ids[j], :] = Src[j, :] (other Dst rows untouched; Dst may be mapped host memory)
+void write_rows(Ctx &c, const Mat &Src, const int32_t *ids, const Mat &Dst);
 // copy with ld conversion (device-to-device)
 void copy_block(Ctx &c, const float *src, int64_t lds, float *dst, int64_t ldd, int64_t rows,
                 int64_t cols);

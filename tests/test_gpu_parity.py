@@ -275,6 +275,14 @@ def test_embed_isolated_vertices_compacted(L, ctx):
     iso = np.setdiff1d(np.arange(n), perm)
     assert np.all(Eh[iso] == 0.0)
     assert _match_cols_up_to_sign(Eh, ref["E"], 4) <= 1e-3
+    # pinned host output (the GPU writes the n' rows straight into it, the
+    # host zeroes it meanwhile): identical to the device result, whatever the
+    # buffer held before; also with a padded leading dimension
+    for ld in (16, 20):
+        Ep = torch.full((n, ld), float("nan"), dtype=torch.float32).pin_memory()[:, :16]
+        sg2 = np.zeros(16)
+        L.netmfp_embed(ctx, g, L.make_params(**prm), Ep, sg2)
+        assert np.array_equal(Ep.numpy(), Eh) and np.array_equal(sg2, sig.cpu().numpy())
 
 
 def _separated(sig, j, rel=0.01):
