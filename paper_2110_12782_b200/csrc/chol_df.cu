@@ -8,8 +8,8 @@
 //     S_IJ = G_IJ − Σ_{K<J} L_IK L_JKᵀ      (waits for L_IK, L_JK)
 //     L_JJ = chol(S_JJ), X_JJ = L_JJ⁻¹       (one warp, rows in registers)
 //     L_IJ = S_IJ X_JJᵀ                      (waits for L_JJ, X_JJ; a tile GEMM)
-//   inverse X = L⁻¹ (lower):
-//     X_IJ = −X_II Σ_{K=J}^{I−1} L_IK X_KJ    (waits for X_KJ, X_II)
+//   inverse X = L⁻¹ (lower), pipelined behind the factorisation in the same attempt:
+//     X_IJ = −X_II Σ_{K=J}^{I−1} L_IK X_KJ    (waits for L_IK, X_KJ, X_II)
 //   Rinv = Xᵀ.
 // A breakdown (pivot <= 1e-12 × original diagonal, or non-finite) raises a
 // global fail word; every CTA notices it, the grid synchronises and all tiles
@@ -296,7 +296,36 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
         store_tile(p.Rinv, p.l, D, 32 * I, 32 * I, ib, ib);  // X_II for the L_JI GEMMs and the inverse
         CDF_MARK(13);
         publish(p.lflag + I * p.nb + I, want);
+        publish(p.xflag + I * p.nb + I, want);
         CDF_MARK(7);
+      }
+    }
+    // inverse X = L⁻¹ of this tile, pipelined behind the factorisation:
+    // X_IJ = -X_II Σ_{K=J}^{I-1} L_IK X_KJ as its inputs appear (flags of this attempt)
+    if (alive && I != J) {
+      for (int i = threadIdx.x; i < 32 * TL; i += T) S[i] = 0.0;
+      __syncthreads();
+      for (int K = J; K < I && alive; ++K) {
+        alive = (K == J || wait_flag(p, p.lflag + I * p.nb + K, want, attempt)) &&
+                wait_flag(p, p.xflag + K * p.nb + J, want, attempt);
+        if (!alive) break;
+        load_tile(A, p.G, p.ld, 32 * I, 32 * K, ib, 32);    // L_IK
+        load_tile(B, p.Rinv, p.l, 32 * K, 32 * J, 32, jb);  // X_KJ
+        __syncthreads();
+        tile_add_ab(S, A, B);
+        __syncthreads();
+      }
+      if (alive) alive = wait_flag(p, p.xflag + I * p.nb + I, want, attempt);
+      if (alive) {
+        load_tile(A, p.Rinv, p.l, 32 * I, 32 * I, ib, ib);  // X_II
+        for (int i = threadIdx.x; i < 32 * TL; i += T) D[i] = 0.0;
+        __syncthreads();
+        tile_add_ab(D, A, S);  // D = X_II · S
+        __syncthreads();
+        for (int i = threadIdx.x; i < 32 * TL; i += T) D[i] = -D[i];
+        __syncthreads();
+        store_tile(p.Rinv, p.l, D, 32 * I, 32 * J, ib, jb);
+        publish(p.xflag + I * p.nb + J, want);
       }
     }
     CDF_MARK(2);
@@ -309,33 +338,7 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
     return;
   }
   if (attempt > 0 && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(p.flag, 1);
-  // ---- inverse: X = L⁻¹
-  const int want = 1;
-  if (owns_diag) publish(p.xflag + I * p.nb + I, want);  // X_II = L_II⁻¹ was stored by the factorisation
-  if (I != J) {
-    for (int i = threadIdx.x; i < 32 * TL; i += T) S[i] = 0.0;
-    __syncthreads();
-    for (int K = J; K < I; ++K) {
-      wait_flag(p, p.xflag + K * p.nb + J, want, -100);
-      load_tile(A, p.G, p.ld, 32 * I, 32 * K, ib, 32);          // L_IK
-      load_tile(B, p.Rinv, p.l, 32 * K, 32 * J, 32, jb);        // X_KJ
-      __syncthreads();
-      tile_add_ab(S, A, B);
-      __syncthreads();
-    }
-    wait_flag(p, p.xflag + I * p.nb + I, want, -100);
-    load_tile(A, p.Rinv, p.l, 32 * I, 32 * I, ib, ib);          // X_II
-    for (int i = threadIdx.x; i < 32 * TL; i += T) D[i] = 0.0;
-    __syncthreads();
-    tile_add_ab(D, A, S);  // D = X_II · S
-    __syncthreads();
-    for (int i = threadIdx.x; i < 32 * TL; i += T) D[i] = -D[i];
-    __syncthreads();
-    store_tile(p.Rinv, p.l, D, 32 * I, 32 * J, ib, jb);
-    publish(p.xflag + I * p.nb + J, want);
-  }
   CDF_MARK(4);
-  grid.sync();
   CDF_MARK(5);
   // ---- Rinv = Xᵀ: this CTA transposes its own tile pair (and its diagonal)
   if (owns_diag) {
