@@ -200,8 +200,9 @@ int netmfp_sketch_svd(netmfp_ctx *ctx, int64_t n, const float *F, int64_t ldf, c
 /* ---- a8: spectral propagation ----------------------------------------------- */
 
 /* E <- Σ_{r=0}^{p} c_r T_r(L - I) E, L = I - D^-1 A (Alg. 5 step 6),
- * c_r = Chebyshev coefficients of the band-pass kernel [R6].  In place on
- * E n×d fp32 (lde).  p = 0 leaves E unchanged. */
+ * c_r = Chebyshev coefficients of the band-pass kernel [R6], evaluated by
+ * Clenshaw's recurrence (p SpMMs).  In place on E n×d fp32 (lde).  p = 0
+ * leaves E unchanged. */
 int netmfp_propagate(netmfp_ctx *ctx, const netmfp_graph *g, float *E, int64_t lde, int32_t d,
                      int32_t order, double mu, double theta, int mem);
 /* The c_0..c_order used by netmfp_propagate (host output, order+1 doubles). */
@@ -211,7 +212,10 @@ int netmfp_cheb_coeffs(int32_t order, double mu, double theta, double *c);
 
 /* E = NetMF+(G) on a built graph: freigs → K, F, C →
  * single-pass SVD → E = U√Σ → propagation.  E: n×d fp32 (lde); sigma (d fp64)
- * and lambda (k fp64) optional (NULL).  `mem` applies to E, sigma, lambda. */
+ * and lambda (k fp64) optional (NULL).  `mem` applies to E, sigma, lambda.
+ * Isolated vertices are dropped from the computation (their rows of E are 0).
+ * With mem = HOST and E in pinned (page-locked, mapped) memory the device
+ * writes E's non-isolated rows directly while host threads zero the rest. */
 int netmfp_embed(netmfp_ctx *ctx, const netmfp_graph *g, const netmfp_params *p, float *E,
                  int64_t lde, double *sigma, double *lambda, int mem);
 

@@ -17,8 +17,8 @@
 //    float4 atomics; the segment that completes the row runs the epilogue;
 //  * both kinds of work are blocks of ONE launch (interleaved), so the
 //    L2-bound hub gathers overlap the latency-bound light rows;
-//  * fused epilogue: row scaling d_u^-a, optional β·prev (Chebyshev three-term
-//    recurrence) and acc update.
+//  * fused epilogue: row scaling d_u^-a, optional β·prev and σ·acc_in terms
+//    (one Clenshaw step of the Chebyshev filter per SpMM).
 // The general path with a column scale (D^-b, b != 0) keeps the simpler
 // warp-per-row kernels k_spmm_rows / k_spmm_heavy.
 #include "common.cuh"
