@@ -548,18 +548,17 @@ static void embed_core(Ctx &c, const Graph &g, const netmfp_params &p, const Mat
   cudaStream_t s = c.stream;
   const bool compacted = g.n_orig != 0;
   const int64_t n = g.n;
-  Block U(n, p.k, s), F(n, p.k, s);
+  Block F(n, p.k, s);
   DBuf<double> lam(p.k, s), C((size_t)p.k * p.k, s);
   {
     NM_STAGE(c, "stage_freigs");
-    freigs(c, g, p.alpha, p.k, p.s1, p.q, p.seed, U.m, lam);          // Alg. 5 step 1
+    freigs(c, g, p.alpha, p.k, p.s1, p.q, p.seed, F.m, lam, true);    // Alg. 5 step 1 (F = D^(-1+α) U)
   }
   if (lambda_dev) NM_CUDA(cudaMemcpyAsync(lambda_dev, lam.p, p.k * 8, cudaMemcpyDeviceToDevice, s));
   {
     NM_STAGE(c, "stage_factor_pair");
-    factor_pair(c, g, p.alpha, p.T, U.m, lam, p.k, F.m, C);            // steps 2-3
+    factor_pair(c, g, p.alpha, p.T, F.m, lam, p.k, F.m, C, true);      // steps 2-3
   }
-  U.buf.release();
   const double scale = (double)g.nnz_global / (p.b * p.T);           // vol(G)/(bT)
   {
     NM_STAGE(c, "stage_sketch_svd");

@@ -48,7 +48,7 @@ void cholqr(Ctx &c, const Mat &Y, const Mat &out, const int32_t *deg, float rexp
 // (P = D^-α Q) so that every SpMM is an unweighted gather with a row scale:
 //   X Q = D^-α A P;  X X Q = D^-α A (D^-2α A P);  S = Qᵀ X Q = Pᵀ (A P);  U = D^α P Û.
 void freigs(Ctx &c, const Graph &g, double alpha, int k, int s1, int q, uint64_t seed, const Mat &U,
-            double *lam_dev) {
+            double *lam_dev, bool out_F) {
   const int64_t n = g.n, l = (int64_t)k + s1;
   NM_REQUIRE(k >= 1 && s1 >= 0 && q >= 0, "eig: need k >= 1, s1 >= 0, q >= 0");
   NM_REQUIRE(l <= g.n_global, "eig: k + s1 must not exceed n (Alg. 2)");
@@ -94,18 +94,22 @@ void freigs(Ctx &c, const Graph &g, double alpha, int k, int s1, int q, uint64_t
     sym_eig(c, S, l, lam, V, true);
   }
   // step 9-10: U = Q Û(:, 1:k) = D^α P Û(:, 1:k)
-  gemm_tall(c, P.m, V, l, k, g.deg, -a, U);
+  // U = D^α P Û, or (out_F) directly F = D^(-1+α) U = D^(-1+2α) P Û (Eq. 3)
+  gemm_tall(c, P.m, V, l, k, g.deg, out_F ? (float)(1.0 - 2.0 * alpha) : -a, U);
   NM_CUDA(cudaMemcpyAsync(lam_dev, lam.p, (size_t)k * 8, cudaMemcpyDeviceToDevice, s));
 }
 
 // Eq. 3 / Alg. 5 steps 2-3
 void factor_pair(Ctx &c, const Graph &g, double alpha, int T, const Mat &U, const double *lam, int k,
-                 const Mat &F, double *C) {
+                 const Mat &F, double *C, bool u_is_F) {
   NM_REQUIRE(T >= 1, "factor_pair: T >= 1");
   cudaStream_t s = c.stream;
   DBuf<double> K((size_t)k * k, s), Pw((size_t)k * k, s), Pn((size_t)k * k, s), acc((size_t)k * k, s);
-  // K = Uᵀ D^(-1+2α) U Λ
-  gram(c, U, U, g.deg, (float)(1.0 - 2.0 * alpha), K, k);
+  // K = Uᵀ D^(-1+2α) U Λ  (= Fᵀ D F Λ with F = D^(-1+α) U)
+  if (u_is_F)
+    gram(c, U, U, g.deg, -1.f, K, k);
+  else
+    gram(c, U, U, g.deg, (float)(1.0 - 2.0 * alpha), K, k);
   dist_allreduce(c, K, (size_t)k * k, DType::F64);
   scale_cols64(c, K, k, k, k, lam, 0);
   // Σ_{r=1}^T K^(r-1) = S_T with S_m = Σ_{r<m} K^r, P_m = K^m, by the bits of T
@@ -145,7 +149,7 @@ void factor_pair(Ctx &c, const Graph &g, double alpha, int T, const Mat &U, cons
   NM_CUDA(cudaMemcpyAsync(C, acc.p, (size_t)k * k * 8, cudaMemcpyDeviceToDevice, s));
   scale_cols64(c, C, k, k, k, lam, 1);
   // F = D^(-1+α) U
-  scale_copy_block(c, U, F, g.deg, (float)(1.0 - alpha));
+  if (!u_is_F) scale_copy_block(c, U, F, g.deg, (float)(1.0 - alpha));
 }
 
 __global__ void k_sqrt_abs(const double *lam, int d, double *out) {
