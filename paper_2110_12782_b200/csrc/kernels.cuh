@@ -119,14 +119,14 @@ struct SparseSign {
   DBuf<float> signs;   // h*z (±1)
 };
 void gen_sparse_sign(Ctx &c, int64_t n, int64_t h, int64_t z, uint64_t seed, uint32_t tag, SparseSign &S);
-// Y[n×h] = f(scale · A F(rows)ᵀ) Ψ  (Eq. 5 sketch; A = F·C), tensor cores
+// Y[n×h] = f(scale · F C F(rows)ᵀ) Ψ  (Eq. 5 sketch), tensor cores
 // (F holds this rank's rows [row0, row0 + F.rows); the gathered rows are
 // summed over ranks)
-void tc_sketch_y(Ctx &c, const Mat &A, const Mat &F, const int32_t *rows, const float *signs, int64_t h, int z,
-                 float scale, int logmode, const Mat &Y, int64_t row0 = 0);
-// Zf[h×h] (fp32, ldz) = Πᵀ f(scale · FC F ᵀ restricted to Π's rows) Π  (Alg. 4 step 6)
-void tc_sketch_z(Ctx &c, const Mat &FC, const Mat &F, const int32_t *rows, const float *signs, int64_t h, int z,
-                 float scale, int logmode, float *Zf, int64_t ldz, int64_t row0 = 0);
+void tc_sketch_y(Ctx &c, const Mat &F, const double *C, int64_t ldc, const int32_t *rows, const float *signs,
+                 int64_t h, int z, float scale, int logmode, const Mat &Y, int64_t row0 = 0);
+// Zf[h×h] (fp32, ldz) = Πᵀ f(scale · F C Fᵀ restricted to Π's rows) Π  (Alg. 4 step 6)
+void tc_sketch_z(Ctx &c, const Mat &F, const double *C, int64_t ldc, const int32_t *rows, const float *signs,
+                 int64_t h, int z, float scale, int logmode, float *Zf, int64_t ldz, int64_t row0 = 0);
 // Out[h×cols] (fp64) = Ψᵀ X  (sign-gather of rows of X; X fp32 n×cols)
 // (X holds rows [row0, row0 + X.rows); rows elsewhere contribute 0)
 void sign_gather_T(Ctx &c, const SparseSign &S, const Mat &X, double *Out, int64_t ldo, int64_t row0 = 0);

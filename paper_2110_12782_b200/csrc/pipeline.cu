@@ -182,14 +182,11 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
     gen_sparse_sign(c, n_global, h2, z, seed, kTagPsi, Psi);
     if (comp_id) remap_rows(c, Psi.rows, h2 * z, comp_id);
   }
-  // FC = F · C
-  Block FC(n, k, s);
-  gemm_tall(c, F, C, k, k, nullptr, 0.f, FC.m);
   // step 3: Y = f(scale F C F(p,:)ᵀ) Ψ  (Eq. 5, column group by column group of Ψ)
   Block Y(n, h2, s), Qb(n, h2, s), Tb(n, h2, s);
   {
     NM_STAGE(c, "stage_sketch_y");
-    tc_sketch_y(c, FC.m, F, Psi.rows, Psi.signs, h2, z, fs, logmode, Y.m, row0);
+    tc_sketch_y(c, F, C, k, Psi.rows, Psi.signs, h2, z, fs, logmode, Y.m, row0);
   }
   if (Yout) copy_block(c, Y.m.p, Y.m.ld, Yout->p, Yout->ld, n, h2);
   // step 4: Q = orth(Y)   (CholeskyQR2 [R7])
@@ -207,7 +204,7 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
   DBuf<double> Z((size_t)h3 * h3, s), PtQ((size_t)h3 * h2, s);
   {
     DBuf<float> Zf((size_t)h3 * h3, s);
-    tc_sketch_z(c, FC.m, F, Pi.rows, Pi.signs, h3, z, fs, logmode, Zf, h3, row0);
+    tc_sketch_z(c, F, C, k, Pi.rows, Pi.signs, h3, z, fs, logmode, Zf, h3, row0);
     f32_to_f64(c, Zf, h3, Z, h3, h3, h3);
   }
   if (Zout) NM_CUDA(cudaMemcpyAsync(Zout, Z.p, (size_t)h3 * h3 * 8, cudaMemcpyDeviceToDevice, s));

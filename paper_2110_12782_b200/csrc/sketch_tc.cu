@@ -412,26 +412,56 @@ static void launch_sketch(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mh, 
   NM_LAUNCH(c, "sketch_tc", kern<<<grid, THREADS, smem, c.stream>>>(ma, mh, ml, prm));
 }
 
-// Y[n × h] = f(scale · A F(rows)ᵀ) Ψ  (Y mode; A = F·C, Ψ = (rows, signs) with z per column)
-void tc_sketch_y(Ctx &c, const Mat &A, const Mat &F, const int32_t *rows, const float *signs, int64_t h, int z,
-                 float scale, int logmode, const Mat &Y, int64_t row0) {
+namespace tcs {
+// hi = x, lo = x - trunc_tf32(x) of an r × k block (row stride ld; padding columns stay 0)
+__global__ void k_split_hilo(const float *__restrict__ src, int64_t rows, int k, int64_t ld, float *__restrict__ hi,
+                             float *__restrict__ lo) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= rows * ld) return;
+  const float x = (idx % ld) < k ? src[idx] : 0.f;
+  hi[idx] = x;
+  if (lo) lo[idx] = x - tc::tf32_trunc(x);
+}
+__global__ void k_transpose64(const double *__restrict__ C, int64_t k, int64_t ldc, double *__restrict__ Ct) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx < k * k) Ct[(idx % k) * k + idx / k] = C[(idx / k) * ldc + idx % k];
+}
+}  // namespace tcs
+
+// Gathered rows G (nr × k, ld ldb; fp32) times the small fp64 matrix Bs (k × k):
+// out = G Bs (tensor cores for nr >= 128), then hi / lo split into (hi, lo)
+static void rows_times(Ctx &c, float *G, int64_t nr, int k, int64_t ldb, const double *Bs, float *hi, float *lo) {
+  DBuf<float> out((size_t)nr * ldb, c.stream);
+  Mat Gm{G, nr, k, ldb}, Om{out.p, nr, k, ldb};
+  gemm_tall(c, Gm, Bs, k, k, nullptr, 0.f, Om);
+  NM_LAUNCH(c, "split_hilo", tcs::k_split_hilo<<<ceil_div(nr * ldb, 256), 256, 0, c.stream>>>(out.p, nr, k, ldb, hi, lo));
+}
+
+// Y[n × h] = f(scale · F C F(rows)ᵀ) Ψ  (Y mode; Ψ = (rows, signs) with z per column).
+// M̂ = (F C) F_rᵀ = F (F_r Cᵀ)ᵀ: the A operand is F itself and the gathered
+// rows F_r are multiplied by Cᵀ (an h·zp × k × k product) — no n × k F·C block.
+void tc_sketch_y(Ctx &c, const Mat &F, const double *C, int64_t ldc, const int32_t *rows, const float *signs,
+                 int64_t h, int z, float scale, int logmode, const Mat &Y, int64_t row0) {
   using namespace tcs;
-  NM_REQUIRE(A.cols == F.cols && Y.rows == A.rows && Y.cols == h, "tc_sketch_y: shapes");
+  NM_REQUIRE(Y.rows == F.rows && Y.cols == h, "tc_sketch_y: shapes");
   NM_REQUIRE(z >= 2 && z <= 64, "tc_sketch_y: 2 <= z <= 64");
-  const int64_t n = A.rows;
-  const int k = (int)A.cols;
+  const int64_t n = F.rows;
+  const int k = (int)F.cols;
   if (n == 0 || h == 0) return;
   const int zp = pow2_at_least(z);
   const int64_t ncols = h * zp;
   const int64_t ldb = pad32(k);
-  DBuf<float> bh((size_t)ncols * ldb, c.stream), bl((size_t)ncols * ldb, c.stream), sg(pad4(ncols) + NW, c.stream);
+  DBuf<float> g((size_t)ncols * ldb, c.stream), bh((size_t)ncols * ldb, c.stream), bl((size_t)ncols * ldb, c.stream),
+      sg(pad4(ncols) + NW, c.stream);
+  DBuf<double> Ct((size_t)k * k, c.stream);
   NM_CUDA(cudaMemsetAsync(sg.p, 0, sg.n * 4, c.stream));
   NM_LAUNCH(c, "gather_groups", k_gather_groups<<<ceil_div(ncols * ldb, 256), 256, 0, c.stream>>>(
-                                    F.p, F.ld, row0, F.rows, rows, signs, h, z, zp, k, ldb, bh.p, bl.p, sg.p));
+                                    F.p, F.ld, row0, F.rows, rows, signs, h, z, zp, k, ldb, g.p, nullptr, sg.p));
   // each gathered row lives on exactly one rank: the sum over ranks is exact
-  dist_allreduce(c, bh.p, (size_t)ncols * ldb, DType::F32);
-  dist_allreduce(c, bl.p, (size_t)ncols * ldb, DType::F32);
-  CUtensorMap ma = make_map(A.p, n, k, A.ld, 128, SW128, BK);
+  dist_allreduce(c, g.p, (size_t)ncols * ldb, DType::F32);
+  NM_LAUNCH(c, "transpose64", k_transpose64<<<ceil_div((int64_t)k * k, 256), 256, 0, c.stream>>>(C, k, ldc, Ct.p));
+  rows_times(c, g.p, ncols, k, ldb, Ct.p, bh.p, bl.p);  // B rows = F_r Cᵀ
+  CUtensorMap ma = make_map(F.p, n, k, F.ld, 128, SW128, BK);
   CUtensorMap mh = make_map(bh.p, ncols, k, ldb, NW, SW128, BK);
   CUtensorMap ml = make_map(bl.p, ncols, k, ldb, NW, SW128, BK);
   SkP prm{};
@@ -452,11 +482,11 @@ void tc_sketch_y(Ctx &c, const Mat &A, const Mat &F, const int32_t *rows, const 
   launch_sketch(c, ma, mh, ml, prm, sg.p);
 }
 
-// Z[h × h] = Πᵀ f(scale · FC(rows) F(rows)ᵀ) Π  (Z mode), fp32 output with ldz
-void tc_sketch_z(Ctx &c, const Mat &FC, const Mat &F, const int32_t *rows, const float *signs, int64_t h, int z,
-                 float scale, int logmode, float *Zf, int64_t ldz, int64_t row0) {
+// Z[h × h] = Πᵀ f(scale · (F C)(rows) F(rows)ᵀ) Π  (Z mode), fp32 output with ldz;
+// the gathered rows of F times C are the A operand
+void tc_sketch_z(Ctx &c, const Mat &F, const double *C, int64_t ldc, const int32_t *rows, const float *signs,
+                 int64_t h, int z, float scale, int logmode, float *Zf, int64_t ldz, int64_t row0) {
   using namespace tcs;
-  NM_REQUIRE(FC.cols == F.cols, "tc_sketch_z: shapes");
   NM_REQUIRE(z >= 2 && z <= 64, "tc_sketch_z: 2 <= z <= 64");
   const int k = (int)F.cols;
   const int zp = pow2_at_least(z);
@@ -467,12 +497,15 @@ void tc_sketch_z(Ctx &c, const Mat &FC, const Mat &F, const int32_t *rows, const
   NM_CUDA(cudaMemsetAsync(sg.p, 0, sg.n * 4, c.stream));
   NM_CUDA(cudaMemsetAsync(rs.p, 0, rs.n * 4, c.stream));
   NM_LAUNCH(c, "gather_groups", k_gather_groups<<<ceil_div(nr * ldb, 256), 256, 0, c.stream>>>(
-                                    FC.p, FC.ld, row0, FC.rows, rows, signs, h, z, zp, k, ldb, ah.p, nullptr, rs.p));
-  NM_LAUNCH(c, "gather_groups", k_gather_groups<<<ceil_div(nr * ldb, 256), 256, 0, c.stream>>>(
                                     F.p, F.ld, row0, F.rows, rows, signs, h, z, zp, k, ldb, bh.p, bl.p, sg.p));
-  dist_allreduce(c, ah.p, (size_t)nr * ldb, DType::F32);
   dist_allreduce(c, bh.p, (size_t)nr * ldb, DType::F32);
   dist_allreduce(c, bl.p, (size_t)nr * ldb, DType::F32);
+  // A = F(rows) C (the gathered raw rows times C); row signs = the column signs
+  {
+    Mat Gm{bh.p, nr, k, ldb}, Om{ah.p, nr, k, ldb};
+    gemm_tall(c, Gm, C, ldc, k, nullptr, 0.f, Om);
+  }
+  NM_CUDA(cudaMemcpyAsync(rs.p, sg.p, rs.n * 4, cudaMemcpyDeviceToDevice, c.stream));
   if (zp > 32) NM_CUDA(cudaMemset2DAsync(Zf, ldz * 4, 0, h * 4, h, c.stream));
   CUtensorMap ma = make_map(ah.p, nr, k, ldb, 128, SW128, BK);
   CUtensorMap mh = make_map(bh.p, nr, k, ldb, NW, SW128, BK);
