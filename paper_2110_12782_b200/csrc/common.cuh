@@ -279,7 +279,7 @@ struct Block {
 // rows with more neighbours than light_cap are split across warps in segments
 // of heavy_seg entries (spmm.cu); per graph, NETMFP_LIGHT_CAP / NETMFP_HEAVY_SEG
 constexpr int kLightCapDefault = 64;
-constexpr int kHeavySegDefault = 64;
+constexpr int kHeavySegDefault = 128;  // (fused SpMM sweep on configs[2]: 32 0.72, 64 0.69, 128 0.67, 256 0.68 ms)
 
 struct Graph {
   int64_t n = 0, nnz = 0;  // local rows [row0, row0 + n) and their nonzeros

@@ -19,5 +19,7 @@ L.netmfp_embed_edges(ctx, n, src, dst, prm, E)
 pr = ctx.profile_read()
 ctx.profile(False)
 gaps = sorted(((k, v) for k, v in pr.items() if k.startswith("gap")), key=lambda x: -x[1][1])
+kern = sum(v[1] for k, v in pr.items() if not k.startswith("gap") and not k.startswith("stage_"))
+print(f"kernels total {kern:.3f} ms; stages: " + ", ".join(f"{k[6:]} {v[1]:.2f}" for k, v in pr.items() if k.startswith("stage_")))
 for k, (cnt, ms) in gaps[:25]:
     print(f"{k:40s} {cnt:5d} {ms:8.3f} ms")
