@@ -539,6 +539,7 @@ __device__ __forceinline__ void cluster_arrive() {
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
 constexpr int TDT = 512;   // threads per CTA
+static_assert(TDT / 32 == 16, "tridiagonalisation partial slots assume 16 warps");
 
 // Householder tridiagonalisation Qᵀ S Q = T, Q = H_0 … H_{l-3}, H_j = I - beta_j v_j v_jᵀ
 // (v_j non-zero on indices j+1..l-1, stored in row j of Hv).  Row i of S lives in
@@ -552,8 +553,10 @@ constexpr int TDT = 512;   // threads per CTA
 //   S2: every CTA has pushed its rows' p_i and its partial vᵀp.
 // v and beta (pushed before S1) are double-buffered by step parity: a buffer
 // is rewritten two steps later, after every CTA has passed the barrier that
-// follows its last read.  p and the partials are pushed after S1 of the next
-// step, which every CTA reaches only after finishing this step's update.
+// follows its last read.  p and the partials are pushed after S1 and are
+// double-buffered the same way (the owner of step j+1 arrives at S1(j+1)
+// before its other rows are updated with p_j, so step j+1's pushes must not
+// land in p_j's buffer).
 __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
     k_tridiag(const double *__restrict__ S, int l, double *__restrict__ dd, double *__restrict__ ee,
               double *__restrict__ Hv, double *__restrict__ hbeta) {
@@ -568,10 +571,9 @@ __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
   extern __shared__ double sm[];
   double *A = sm;                          // nmax × l (first nloc rows used)
   double *vbuf = A + (int64_t)nmax * l;    // 2 × l
-  double *pf = vbuf + 2 * l;               // l
-  double *pl = pf + l;                     // nmax
-  double *red = pl + nmax;                 // 40
-  double *xchg = red + 40;                 // [parity][TDC] partials, [2 TDC + parity] beta
+  double *pfb = vbuf + 2 * l;              // 2 × l (p, double-buffered like v)
+  double *red = pfb + 2 * l;               // 40
+  double *xchg = red + 40;                 // [parity][TDC][16 warps] partials, [32 TDC + parity] beta
   for (int64_t idx = tid; idx < (int64_t)nloc * l; idx += nt) {
     int li = (int)(idx / l), k = (int)(idx % l);
     A[idx] = S[(int64_t)(li * TDC + rank) * l + k];
@@ -600,7 +602,7 @@ __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
       for (int r = 0; r < TDC; ++r) cl.map_shared_rank(v, r)[k] = val;
       Hv[(int64_t)j * l + k] = val;
     }
-    if (tid < TDC) cl.map_shared_rank(xchg, tid)[2 * TDC + par] = beta;
+    if (tid < TDC) cl.map_shared_rank(xchg, tid)[32 * TDC + par] = beta;
     if (tid == 0) {
       dd[j] = x[j];
       ee[j] = alpha;
@@ -612,12 +614,15 @@ __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
   for (int j = 0; j + 2 < l; ++j) {
     const int par = j & 1;
     const double *v = vbuf + par * l;
+    double *pf = pfb + par * l;
     TD_MARK(0);
     TD_MARK(1);
     cluster_wait();  // S1(j): v_j, beta_j pushed
     TD_MARK(2);
-    const double beta = xchg[2 * TDC + par];
-    // (2) p_i = beta A[i, j+1:] · v for own rows i > j; partial vᵀp
+    const double beta = xchg[32 * TDC + par];
+    // (2) p_i = beta A[i, j+1:] · v for own rows i > j, pushed to every CTA by
+    // the warp that computed it; per-warp partials of vᵀp pushed likewise
+    // (no CTA barrier in this phase)
     double part = 0.0;
     for (int li = wid; li < nloc; li += nt / 32) {
       const int i = li * TDC + rank;
@@ -626,24 +631,15 @@ __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
       double sacc = 0.0;
       for (int k = j + 1 + ln; k < l; k += 32) sacc += Ai[k] * v[k];
       sacc = warp_sum(sacc) * beta;
-      if (ln == 0) {
-        pl[li] = sacc;
-        part += sacc * v[i];
-      }
+      if (ln < TDC) cl.map_shared_rank(pf, ln)[i] = sacc;
+      part += sacc * v[i];
     }
-    part = block_sum<TDT>(part, red);  // (its barriers also publish pl)
-    // (3) push own p_i and the partial to every CTA
-    for (int q = tid; q < nloc * TDC; q += nt) {
-      const int li = q / TDC, r = q % TDC;
-      const int i = li * TDC + rank;
-      if (i > j) cl.map_shared_rank(pf, r)[i] = pl[li];
-    }
-    if (tid < TDC) cl.map_shared_rank(xchg, tid)[par * TDC + rank] = part;
+    if (ln < TDC) cl.map_shared_rank(xchg, ln)[par * TDC * 16 + rank * 16 + wid] = part;
     TD_MARK(3);
     cl.sync();  // S2
     double vtp = 0.0;
-#pragma unroll
-    for (int r = 0; r < TDC; ++r) vtp += xchg[par * TDC + r];
+    for (int q = ln; q < TDC * 16; q += 32) vtp += xchg[par * TDC * 16 + q];
+    vtp = warp_sum(vtp);
     const double K2 = vtp * beta;  // 2K
     // (4) A_i -= v_i p + p_i v - 2K v_i v  (own rows i > j, columns > j).
     // Look-ahead: the owner of step j+1 updates row j+1 first, then builds
@@ -1061,7 +1057,7 @@ void sym_eig(Ctx &c, double *S, int64_t l64, double *lam, double *V, bool abs_or
   NM_CUDA(cudaMemsetAsync(hb.p, 0, (size_t)l * 8, s));
   NM_CUDA(cudaMemsetAsync(e.p, 0, (size_t)l * 8, s));
   const int nloc = (l + TDC - 1) / TDC;
-  size_t smem = ((size_t)nloc * l + 3 * l + nloc + 40 + 2 * TDC + 8) * sizeof(double);
+  size_t smem = ((size_t)nloc * l + 4 * l + 40 + 32 * TDC + 8) * sizeof(double);
   NM_REQUIRE(smem <= 227 * 1024 && l <= 32 * BT_NR, "sym_eig: l too large for the 8-CTA cluster (l <= ~470)");
   static bool attr = false;
   if (!attr) {
