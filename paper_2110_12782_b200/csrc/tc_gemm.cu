@@ -21,9 +21,15 @@
 //   as-is and fed to the MMA as MN-major operands (no transposition): a
 //   column block of 32 fp32 = one 128-B swizzle row, 8 rows = one 1-KB atom.
 //   One CTA reduces a K-slab ("chain") of rows into all output tiles it owns
-//   (Σ widths ≤ 512 TMEM columns), then writes an fp32 partial; partials are
-//   summed in fp64 by a deterministic two-level reduction.  Chains are kept
-//   short (≈2k rows) because the tensor core's fp32 accumulation truncates.
+//   (Σ widths ≤ 512 TMEM columns), then writes an fp32 partial (units stored
+//   column-major: coalesced stores); partials are summed in fp64 by a
+//   deterministic reduction.  Exact chains are kept short (≈2k rows) because
+//   the tensor core's fp32 accumulation truncates.  A tf32-only Gram without
+//   row weights has nothing to prepare per chunk: the MMA issuer consumes the
+//   TMA stage directly.  The issue loop reads host-computed per-unit
+//   constants from the parameter space (uniform datapath, ~15 instructions
+//   per MMA); with them in registers the issuer, not the tensor core, was the
+//   bottleneck.
 // GEMM  C = diag(rs)·A·B (B small, fp64 on input): persistent over 128-row
 //   tiles of A (K-major operand straight from the row-major block); Bᵀ hi/lo
 //   are prepared once in fp32 and streamed per K-chunk from L2.  With
@@ -74,17 +80,20 @@ struct GramP {
   const float *wrow;    // optional per-row weights (d^-wexp, or its square root applied to both sides if sym)
   int64_t part_stride;  // floats per chain partial
   float *part;
+  // issue constants per unit (host-computed so the MMA issuer reads them from
+  // the parameter space with a uniform index: no per-MMA register moves)
+  uint32_t uao[kMaxUnits], ubo[kMaxUnits], utc[kMaxUnits], uid[kMaxUnits];
   int exact;            // 1: 3xTF32 (A_hi B_hi + A_hi B_lo + A_lo B_hi); 0: A_hi B_hi only (no lo parts)
 };
 
-template <int BK, bool SYM>
+template <int BK, bool SYM, bool EXACT>
 __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUtensorMap tmA,
                                                    const __grid_constant__ CUtensorMap tmB, const GramP p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = align1024(smem_raw);
   constexpr int BLK = BK * 128;  // bytes of one 32-col block of BK rows
   const int nblk = p.na_blk + (SYM ? 0 : p.nb_blk);
-  const int stage_bytes = (p.exact ? 2 : 1) * nblk * BLK;  // raw (+ lo)
+  const int stage_bytes = (EXACT ? 2 : 1) * nblk * BLK;  // raw (+ lo)
   const int S = p.stages;
   uint64_t *bars = reinterpret_cast<uint64_t *>(base + S * stage_bytes + 3 * BLK);
   uint64_t *full = bars, *split = bars + S, *empty = bars + 2 * S, *done = bars + 3 * S;
@@ -95,6 +104,9 @@ __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUten
   const int64_t r0 = chain * p.kslab;
   const int64_t r1 = min(r0 + p.kslab, p.n);
   const int nk = (int)((r1 - r0 + BK - 1) / BK);
+  // nothing to prepare per chunk (no lo parts, no row weights): the MMA
+  // issuer consumes the TMA-filled stage directly
+  const bool direct = !EXACT && !p.wrow;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -117,7 +129,11 @@ __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUten
       if (!SYM) tma_prefetch_desc(&tmB);
       for (int kc = 0; kc < nk; ++kc) {
         const int s = kc % S, use = kc / S;
-        if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+        {
+          TCP_T0();
+          if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+          TCP_ADD(0);
+        }
         uint8_t *st = base + s * stage_bytes;
         mbar_expect_tx(&full[s], (uint32_t)(nblk * BLK));
         const int row = (int)(r0 + (int64_t)kc * BK);
@@ -135,48 +151,42 @@ __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUten
     }
   } else if (warp == 1) {
     {  // whole warp (uniform addresses), one elected lane issues
-      // per-unit constants (TMEM column, descriptor address offsets, instruction descriptor)
-      const int nun = p.nunits;
-      uint32_t ud[kMaxUnits], uao[kMaxUnits], ubo[kMaxUnits], uid[kMaxUnits];
-#pragma unroll
-      for (int ui = 0; ui < kMaxUnits; ++ui) {
-        if (ui >= nun) break;
-        ud[ui] = tmem + (uint32_t)p.u[ui].tcol;
-        uao[ui] = (uint32_t)(p.u[ui].mblk * BLK) >> 4;
-        ubo[ui] = (uint32_t)(p.u[ui].nblk * BLK) >> 4;
-        uid[ui] = make_idesc(p.u[ui].nw, 1, 1);
-      }
       for (int kc = 0; kc < nk; ++kc) {
         const int s = kc % S, use = kc / S;
-        mbar_wait(&split[s], (uint32_t)(use & 1));
+        {
+          TCP_T0();
+          mbar_wait(direct ? &full[s] : &split[s], (uint32_t)(use & 1));
+          if (lane == 0) TCP_ADD(2);
+        }
+        TCP_T0();
         tc_fence_after();
-        const bool leader = elect_one();
-        const uint32_t raw = smem_u32(base + s * stage_bytes);
-        const uint32_t lo = raw + nblk * BLK;
-        const uint32_t braw = SYM ? raw : raw + p.na_blk * BLK;
-        const uint32_t blo = SYM ? lo : lo + p.na_blk * BLK;
-        // descriptors once per chunk; per unit / K step only the address field moves
-        const uint64_t dA = make_desc_mn32(raw, BLK), dAl = make_desc_mn32(lo, BLK);
-        const uint64_t dB = make_desc_mn32(braw, BLK), dBl = make_desc_mn32(blo, BLK);
+        if (elect_one()) {
+          const uint32_t raw = smem_u32(base + s * stage_bytes);
+          const uint32_t lo = raw + nblk * BLK;
+          const uint32_t braw = SYM ? raw : raw + p.na_blk * BLK;
+          const uint32_t blo = SYM ? lo : lo + p.na_blk * BLK;
+          // descriptors once per chunk; per unit / K step only the address field moves
+          const uint64_t dA = make_desc_mn32(raw, BLK), dAl = make_desc_mn32(lo, BLK);
+          const uint64_t dB = make_desc_mn32(braw, BLK), dBl = make_desc_mn32(blo, BLK);
 #pragma unroll
-        for (int ks = 0; ks < BK / 8; ++ks) {
-          const uint32_t ko = ks * (1024 >> 4);
-#pragma unroll
-          for (int ui = 0; ui < kMaxUnits; ++ui) {
-            if (ui >= nun) break;
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint32_t ko = ks * (1024 >> 4);
             const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
-            if (leader) {
-              mma_tf32(ud[ui], dA + uao[ui] + ko, dB + ubo[ui] + ko, uid[ui], acc0);
-              if (p.exact) {
-                mma_tf32(ud[ui], dA + uao[ui] + ko, dBl + ubo[ui] + ko, uid[ui], 1u);
-                mma_tf32(ud[ui], dAl + uao[ui] + ko, dB + ubo[ui] + ko, uid[ui], 1u);
+#pragma unroll 1
+            for (int ui = 0; ui < p.nunits; ++ui) {
+              const uint32_t d = tmem + p.utc[ui], id = p.uid[ui];
+              const uint32_t ao = p.uao[ui] + ko, bo = p.ubo[ui] + ko;
+              mma_tf32(d, dA + ao, dB + bo, id, acc0);
+              if (EXACT) {
+                mma_tf32(d, dA + ao, dBl + bo, id, 1u);
+                mma_tf32(d, dAl + ao, dB + bo, id, 1u);
               }
             }
           }
+          mma_commit(&empty[s]);
         }
         __syncwarp();
-        if (leader) mma_commit(&empty[s]);
-        __syncwarp();
+        if (lane == 0) TCP_ADD(5);
       }
       if (elect_one()) mma_commit(done);
       __syncwarp();
@@ -185,9 +195,14 @@ __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUten
     // workers: lo split (+ row weights) for every chunk, then the epilogue
     const int wt = threadIdx.x - 64;  // 0..127
     const int q = warp & 3;
-    for (int kc = 0; kc < nk; ++kc) {
+    for (int kc = 0; kc < (direct ? 0 : nk); ++kc) {
       const int s = kc % S, use = kc / S;
-      mbar_wait(&full[s], (uint32_t)(use & 1));
+      {
+        TCP_T0();
+        mbar_wait(&full[s], (uint32_t)(use & 1));
+        if (wt == 0) TCP_ADD(3);
+      }
+      TCP_T0();
       uint8_t *raw = base + s * stage_bytes;
       uint8_t *lo = raw + nblk * BLK;
       const int64_t row0 = r0 + (int64_t)kc * BK;
@@ -204,7 +219,7 @@ __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUten
             reinterpret_cast<float4 *>(raw)[i] = v;
           }
         }
-        if (p.exact) {
+        if (EXACT) {
           float4 l;
           l.x = v.x - tf32_trunc(v.x);
           l.y = v.y - tf32_trunc(v.y);
@@ -215,25 +230,25 @@ __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUten
       }
       fence_async_smem();
       mbar_arrive(&split[s]);
+      if (wt == 0) TCP_ADD(6);
     }
     // epilogue: TMEM lanes 32q..32q+31 = rows of every unit's 128-row M tile
-    mbar_wait(done, 0);
+    {
+      TCP_T0();
+      mbar_wait(done, 0);
+      if (wt == 0) TCP_ADD(4);
+    }
     tc_fence_after();
     const int r = 32 * q + lane;
     float *dst0 = p.part + chain * p.part_stride;
     for (int ui = 0; ui < p.nunits; ++ui) {
       const GUnit &u = p.u[ui];
-      float *dst = dst0 + u.off + (int64_t)r * u.nw;
+      float *dst = dst0 + u.off + r;  // column-major unit: lanes write consecutive rows
       for (int c = 0; c < u.nw; c += 16) {
         float v[16];
         tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(u.tcol + c), v);
-        if (nk == 0) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.f;
-        }
-#pragma unroll
-        for (int i = 0; i < 16; i += 4)
-          *reinterpret_cast<float4 *>(dst + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        for (int i = 0; i < 16; ++i) __stcs(dst + (int64_t)(c + i) * 128, nk == 0 ? 0.f : v[i]);
       }
     }
     (void)wt;
@@ -252,48 +267,49 @@ struct GramRed {
   int64_t nchain, part_stride;
 };
 
-__device__ __forceinline__ int64_t gram_locate(const GramRed &R, int64_t i, int64_t j) {
-  for (int pass = 0; pass < 2; ++pass) {
-    const int64_t mt = i / 128;
-    for (int ui = 0; ui < R.nunits; ++ui) {
-      const GUnit &u = R.u[ui];
-      const int64_t n0 = (int64_t)u.nblk * 32;
-      if (u.mblk / 4 == mt && j >= n0 && j < n0 + u.nw) return u.off + (i - 128 * mt) * u.nw + (j - n0);
-    }
-    const int64_t t = i;
-    i = j;
-    j = t;
-  }
-  return -1;
-}
-
-__global__ void k_gram_reduce1(const float *__restrict__ part, GramRed R, int64_t per_group, double *__restrict__ tmp) {
-  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= R.a * R.b) return;
-  if (R.sym && idx / R.b > idx % R.b) return;  // symmetric: upper triangle only (mirrored in reduce2)
-  const int64_t off = gram_locate(R, idx / R.b, idx % R.b);
-  const int64_t c0 = blockIdx.y * per_group, c1 = min(c0 + per_group, R.nchain);
+// G = Σ_chains partials, one block per 32 consecutive partial positions (a
+// partial unit is stored column-major, position = off + 128·col + row, so the
+// epilogue's stores and these loads are coalesced); warp w sums chains
+// w, w+8, … in a fixed order and the 8 warp sums are added in warp order
+// (deterministic).  Symmetric: only i <= j is reduced and mirrored.
+constexpr int kRedWarps = 8;
+__global__ void __launch_bounds__(32 * kRedWarps) k_gram_reduce(const float *__restrict__ part, GramRed R,
+                                                               double *__restrict__ G, int64_t ldg) {
+  __shared__ double red[kRedWarps][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t pos = blockIdx.x * 32LL + lane;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int64_t c = c0;
-  for (; c + 4 <= c1; c += 4) {
-    s0 += (double)__ldg(part + c * R.part_stride + off);
-    s1 += (double)__ldg(part + (c + 1) * R.part_stride + off);
-    s2 += (double)__ldg(part + (c + 2) * R.part_stride + off);
-    s3 += (double)__ldg(part + (c + 3) * R.part_stride + off);
+  if (pos < R.part_stride) {
+    const float *src = part + pos;
+    int64_t c = warp;
+    for (; c + 3 * kRedWarps < R.nchain; c += 4 * kRedWarps) {
+      s0 += (double)__ldg(src + c * R.part_stride);
+      s1 += (double)__ldg(src + (c + kRedWarps) * R.part_stride);
+      s2 += (double)__ldg(src + (c + 2 * kRedWarps) * R.part_stride);
+      s3 += (double)__ldg(src + (c + 3 * kRedWarps) * R.part_stride);
+    }
+    for (; c < R.nchain; c += kRedWarps) s0 += (double)__ldg(src + c * R.part_stride);
   }
-  for (; c < c1; ++c) s0 += (double)__ldg(part + c * R.part_stride + off);
-  tmp[blockIdx.y * R.a * R.b + idx] = (s0 + s1) + (s2 + s3);
-}
-
-__global__ void k_gram_reduce2(const double *__restrict__ tmp, int groups, int64_t a, int64_t b, double *__restrict__ G,
-                               int64_t ldg, bool sym) {
-  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= a * b) return;
-  const int64_t i = idx / b, j = idx % b;
-  const int64_t src = (sym && i > j) ? j * b + i : idx;
+  red[warp][lane] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (warp != 0 || pos >= R.part_stride) return;
   double s = 0.0;
-  for (int g = 0; g < groups; ++g) s += tmp[(int64_t)g * a * b + src];
-  G[(idx / b) * ldg + idx % b] = s;
+#pragma unroll
+  for (int w = 0; w < kRedWarps; ++w) s += red[w][lane];
+  for (int ui = 0; ui < R.nunits; ++ui) {
+    const GUnit &u = R.u[ui];
+    const int64_t loc = pos - u.off;
+    if (loc < 0 || loc >= 128LL * u.nw) continue;
+    const int64_t i = (int64_t)u.mblk * 32 + loc % 128, j = (int64_t)u.nblk * 32 + loc / 128;
+    if (i >= R.a || j >= R.b) return;
+    if (!R.sym) {
+      G[i * ldg + j] = s;
+    } else if (i <= j) {
+      G[i * ldg + j] = s;
+      G[j * ldg + i] = s;
+    }
+    return;
+  }
 }
 
 // ===========================================================================
@@ -671,16 +687,24 @@ static void launch_gram(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, tc
   (void)ngroup_units_offset;
   const int nblk = p.na_blk + (SYM ? 0 : p.nb_blk);
   const size_t stage = (size_t)(p.exact ? 2 : 1) * nblk * BK * 128;
+  for (int ui = 0; ui < p.nunits; ++ui) {
+    p.uao[ui] = (uint32_t)(p.u[ui].mblk * BK * 128) >> 4;
+    p.ubo[ui] = (uint32_t)(p.u[ui].nblk * BK * 128) >> 4;
+    p.utc[ui] = (uint32_t)p.u[ui].tcol;
+    p.uid[ui] = tc::make_idesc(p.u[ui].nw, 1, 1);
+  }
+  auto kern = p.exact ? tc::k_gram_tc<BK, SYM, true> : tc::k_gram_tc<BK, SYM, false>;
   int S = (int)std::min<size_t>(6, (kSmemMax - 1024 - 256 - kPadBlocks * BK * 128) / stage);
   NM_REQUIRE(S >= 2, "tc_gram: too many columns for the staged chunk");
   p.stages = S;
   const size_t smem = 1024 + S * stage + kPadBlocks * BK * 128 + (3 * S + 2) * 8 + 16;
   static bool attr = false;
   if (!attr) {
-    NM_CUDA(cudaFuncSetAttribute(tc::k_gram_tc<BK, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
+    NM_CUDA(cudaFuncSetAttribute(tc::k_gram_tc<BK, SYM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
+    NM_CUDA(cudaFuncSetAttribute(tc::k_gram_tc<BK, SYM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
     attr = true;
   }
-  NM_LAUNCH(c, "tc_gram", tc::k_gram_tc<BK, SYM><<<(unsigned)nchain, tc::NT, smem, c.stream>>>(ma, mb, p));
+  NM_LAUNCH(c, "tc_gram", kern<<<(unsigned)nchain, tc::NT, smem, c.stream>>>(ma, mb, p));
 }
 
 __global__ void k_gram_wrow(const int32_t *__restrict__ deg, int64_t n, float e, float *__restrict__ w) {
@@ -799,12 +823,8 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
   R.sym = sym;
   R.nchain = nchain;
   R.part_stride = total;
-  const int RG = (int)std::min<int64_t>(16, nchain);
-  const int64_t per = ceil_div(nchain, RG);
-  DBuf<double> tmp((size_t)RG * a * b, c.stream);
-  dim3 g1(ceil_div(a * b, 256), RG);
-  NM_LAUNCH(c, "tc_gram_reduce", k_gram_reduce1<<<g1, 256, 0, c.stream>>>(part.p, R, per, tmp.p));
-  NM_LAUNCH(c, "tc_gram_reduce", k_gram_reduce2<<<ceil_div(a * b, 256), 256, 0, c.stream>>>(tmp.p, RG, a, b, G, ldg, sym));
+  NM_LAUNCH(c, "tc_gram_reduce",
+            k_gram_reduce<<<ceil_div(total, 32), 32 * kRedWarps, 0, c.stream>>>(part.p, R, G, ldg));
 }
 
 // Bᵀ for the tensor-core GEMM, zero padded to nrows × 32 nk:

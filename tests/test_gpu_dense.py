@@ -107,3 +107,20 @@ def test_sym_eig_graph_ritz(L, ctx):
     Q = np.linalg.qr(Y)[0]
     S = Q.T @ O.normalized_spmm(rp, col, deg, Q, 0.45)
     _check_eig(L, ctx, (S + S.T) / 2)
+
+
+@pytest.mark.parametrize("l", [17, 286, 460])
+def test_sym_eig_repeatable(L, ctx, l):
+    """The cluster tridiagonalisation exchanges data through other CTAs' shared
+    memory with a fixed reduction order: repeated runs must agree bit for bit
+    (a buffer overwritten before its last read shows up as run-to-run noise)."""
+    A = np.random.default_rng(l + 1).standard_normal((l, l))
+    S = torch.from_numpy((A + A.T) / 2).to(DEV)
+    outs = []
+    for _ in range(12):
+        lam = torch.zeros(l, dtype=torch.float64, device=DEV)
+        V = torch.zeros(l, l, dtype=torch.float64, device=DEV)
+        L.netmfp_sym_eig(ctx, S.clone(), lam, V, True)
+        outs.append((lam.cpu().numpy(), V.cpu().numpy()))
+    for lam, V in outs[1:]:
+        assert np.array_equal(lam, outs[0][0]) and np.array_equal(V, outs[0][1])
