@@ -145,42 +145,51 @@ __device__ void tile_mul_abt(double *OUT, const double *A, const double *B) {
   for (int i = 0; i < 4; ++i) OUT[(r0 + 8 * i) * TL + c] = acc[i];
 }
 
-// Warp 0: S (32×32, rows >= ib identity) -> L = chol(S) (lower, in S) and
-// X = L⁻¹ (lower, in X).  Right-looking in both halves with the working row
-// (then column) in registers.  The inverse's register window shifts by one
-// row per step (w[m] = row k + m), so one rolled loop body serves every step
-// with register operands (the code runs once per tile from a cold
-// instruction cache).  Returns true on breakdown (pivot <= 1e-12 × piv[j]
-// or non-finite).
-__device__ bool warp_chol_inv(double *S, double *X, double *rinv, const double *piv, int ib) {
+// Warps 0 and 1: S (32×32, rows >= ib identity) -> L = chol(S) (lower, in S)
+// and X = L⁻¹ (lower, in X).  Warp 0 factors right-looking with its row in
+// registers, column j of L broadcast through shared memory, and publishes its
+// progress after every column; warp 1 inverts one step behind (inverse step k
+// needs only column k of L and 1/L[k][k]), so the inverse overlaps the factor
+// instead of following it.  The inverse's register window shifts by one row
+// per step (w[m] = row k + m), so one rolled loop body serves every step with
+// register operands (the code runs once per tile from a cold instruction
+// cache).  Returns (warp 0) true on breakdown (pivot <= 1e-12 × piv[j] or
+// non-finite).
+__device__ bool warp_chol_inv(double *S, double *X, double *rinv, const double *piv, int ib, volatile int *prog) {
   const int r = threadIdx.x & 31;
-  CDF_MARK(10);
   double w[32];
+  if (threadIdx.x < 32) {
+    CDF_MARK(10);
 #pragma unroll
-  for (int c = 0; c < 32; ++c) w[c] = S[r * TL + c];
-  bool bad = false;
-  // factor: fully unrolled (register row), column j of L broadcast through
-  // shared memory
+    for (int c = 0; c < 32; ++c) w[c] = S[r * TL + c];
+    bool bad = false;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const double d = __shfl_sync(0xffffffffu, w[j], j);  // S[j][j]
-    bad |= j < ib && (!(d > 1e-12 * piv[j]) || !isfinite(d));
-    const double inv = rsqrt(fmax(d, 1e-300));
-    const double l = r >= j ? w[j] * inv : 0.0;  // L[r][j]
-    S[r * TL + j] = l;
-    if (r == j) rinv[j] = inv;  // 1 / L[j][j]
+    for (int j = 0; j < 32; ++j) {
+      const double d = __shfl_sync(0xffffffffu, w[j], j);  // S[j][j]
+      bad |= j < ib && (!(d > 1e-12 * piv[j]) || !isfinite(d));
+      const double inv = rsqrt(fmax(d, 1e-300));
+      const double l = r >= j ? w[j] * inv : 0.0;  // L[r][j]
+      S[r * TL + j] = l;
+      if (r == j) rinv[j] = inv;  // 1 / L[j][j]
+      __threadfence_block();
+      __syncwarp();
+      if (r == 0) *prog = j + 1;  // column j and rinv[j] are final
+#pragma unroll
+      for (int c = j + 1; c < 32; ++c) w[c] -= l * S[c * TL + j];
+    }
     __syncwarp();
-#pragma unroll
-    for (int c = j + 1; c < 32; ++c) w[c] -= l * S[c * TL + j];
+    CDF_MARK(12);
+    return bad;
   }
-  __syncwarp();
-  CDF_MARK(12);
   // X = L⁻¹, lane r owning column r: x_k = acc_k / L[k][k], then the later
   // rows' partial sums (w[m] = row k + m)
 #pragma unroll
   for (int i = 0; i < 32; ++i) w[i] = i == r ? 1.0 : 0.0;
 #pragma unroll 1
   for (int k = 0; k < 32; ++k) {
+    while (*prog <= k) {
+    }
+    __threadfence_block();
     const double xk = w[0] * rinv[k];
     X[k * TL + r] = xk;
 #pragma unroll
@@ -188,7 +197,7 @@ __device__ bool warp_chol_inv(double *S, double *X, double *rinv, const double *
   }
   __syncwarp();
   CDF_MARK(14);
-  return bad;
+  return false;
 }
 
 __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
@@ -196,6 +205,7 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
   __shared__ double S[32 * TL], A[32 * TL], B[32 * TL], D[32 * TL], E[32 * TL];
   __shared__ int bad;
   __shared__ double piv[32], rinv[32];
+  __shared__ int prog;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // tile of this CTA: block 0 -> (0, 0); then the strictly lower tiles
   // (I, J), I > J, column-major.  The sub-diagonal CTA (J+1, J) also owns the
@@ -282,8 +292,11 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
         piv[threadIdx.x] = (int)threadIdx.x < ib
                                ? __ldcg(p.G0 + (int64_t)(32 * I + threadIdx.x) * p.l + 32 * I + threadIdx.x) + shift
                                : 1.0;
-        __syncwarp();
-        const bool b = warp_chol_inv(S, D, rinv, piv, ib);
+        if (threadIdx.x == 0) prog = 0;
+      }
+      __syncthreads();
+      if (threadIdx.x < 64) {
+        const bool b = warp_chol_inv(S, D, rinv, piv, ib, &prog);
         if (threadIdx.x == 0) bad = b;
       }
       __syncthreads();
