@@ -13,7 +13,8 @@
 //   Rinv = Xᵀ.
 // A breakdown (pivot <= 1e-12 × original diagonal, or non-finite) raises a
 // global fail word; every CTA notices it, the grid synchronises and all tiles
-// restart from the saved G with a diagonal shift (shifted CholeskyQR), as the
+// restart from G (never written: L has its own buffer) with a diagonal shift
+// (shifted CholeskyQR), as the
 // single-CTA kernels in small.cu do.  Launched cooperatively (co-residency of
 // the ≤ nb(nb+1)/2 CTAs is required by the spin waits).
 #include <cooperative_groups.h>
@@ -52,10 +53,10 @@ __device__ __forceinline__ void st_release(int *p, int v) {
 }
 
 struct DfP {
-  double *G;   // l×l (ld), overwritten: L in the lower tiles
+  const double *G;  // l×l (ld), read only
   int64_t ld;
   int l, nb;
-  double *G0;  // saved copy of G (l×l, ld = l)
+  double *L;   // l×l (ld = l): L in the lower tiles
   double *Rinv;  // l×l (ld = l); holds X = L⁻¹ (lower) before the final transpose
   int *lflag, *xflag;  // nb×nb ready flags (value = attempt + 1)
   int *fail;           // 0 = ok, else attempt+1 of the failing attempt
@@ -223,14 +224,11 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
   const bool owns_diag = (I == J) || (I == J + 1);  // (0,0) or a sub-diagonal tile
   const int ib = min(32, p.l - 32 * I), jb = min(32, p.l - 32 * J);
   CDF_MARK(0);
-  // save G (for shifted retries) and the original diagonal
-  for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < (int64_t)p.l * p.l; i += (int64_t)gridDim.x * T)
-    p.G0[i] = p.G[(i / p.l) * p.ld + i % p.l];
-  grid.sync();
+  // G stays intact (L goes to its own buffer), so a shifted retry restarts from it
   CDF_MARK(1);
   __shared__ double red[T / 32];
   double maxdiag = 0.0;
-  for (int i = threadIdx.x; i < p.l; i += T) maxdiag = fmax(maxdiag, __ldcg(p.G0 + (int64_t)i * p.l + i));
+  for (int i = threadIdx.x; i < p.l; i += T) maxdiag = fmax(maxdiag, __ldcg(p.G + (int64_t)i * p.ld + i));
   for (int o = 16; o > 0; o >>= 1) maxdiag = fmax(maxdiag, __shfl_xor_sync(0xffffffffu, maxdiag, o));
   if (lane == 0) red[warp] = maxdiag;
   __syncthreads();
@@ -244,8 +242,8 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
     // S = G_IJ (+ shift on the diagonal); a sub-diagonal CTA also keeps the
     // diagonal tile I in E
     CDF_MARK(8);
-    load_tile(S, p.G0, p.l, 32 * I, 32 * J, ib, jb);
-    if (I == J + 1) load_tile(E, p.G0, p.l, 32 * I, 32 * I, ib, ib);
+    load_tile(S, p.G, p.ld, 32 * I, 32 * J, ib, jb);
+    if (I == J + 1) load_tile(E, p.G, p.ld, 32 * I, 32 * I, ib, ib);
     __syncthreads();
     CDF_MARK(9);
     if (I == J)
@@ -257,8 +255,8 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
       alive = wait_flag(p, p.lflag + I * p.nb + K, want, attempt) &&
               wait_flag(p, p.lflag + J * p.nb + K, want, attempt);
       if (!alive) break;
-      load_tile(A, p.G, p.ld, 32 * I, 32 * K, ib, 32);
-      load_tile(B, p.G, p.ld, 32 * J, 32 * K, jb, 32);
+      load_tile(A, p.L, p.l, 32 * I, 32 * K, ib, 32);
+      load_tile(B, p.L, p.l, 32 * J, 32 * K, jb, 32);
       __syncthreads();
       tile_sub_abt(S, A, B);
       if (I == J + 1) tile_sub_abt(E, A, A);  // diagonal I: - L_IK L_IKᵀ
@@ -273,7 +271,7 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
         __syncthreads();
         tile_mul_abt(A, S, D);  // L_IJ
         __syncthreads();
-        store_tile(p.G, p.ld, A, 32 * I, 32 * J, ib, jb);
+        store_tile(p.L, p.l, A, 32 * I, 32 * J, ib, jb);
         publish(p.lflag + I * p.nb + J, want);
         CDF_MARK(7);
         if (I == J + 1) {  // the diagonal I gets its last update from this CTA's own tile
@@ -290,7 +288,7 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
         for (int cc = 0; cc < 32; ++cc)
           if ((int)threadIdx.x >= ib) S[threadIdx.x * TL + cc] = (cc == (int)threadIdx.x) ? 1.0 : 0.0;
         piv[threadIdx.x] = (int)threadIdx.x < ib
-                               ? __ldcg(p.G0 + (int64_t)(32 * I + threadIdx.x) * p.l + 32 * I + threadIdx.x) + shift
+                               ? __ldcg(p.G + (int64_t)(32 * I + threadIdx.x) * p.ld + 32 * I + threadIdx.x) + shift
                                : 1.0;
         if (threadIdx.x == 0) prog = 0;
       }
@@ -305,7 +303,7 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
         if (threadIdx.x == 0) atomicMax(p.fail, want);
         alive = false;
       } else {
-        store_tile(p.G, p.ld, S, 32 * I, 32 * I, ib, ib);
+        store_tile(p.L, p.l, S, 32 * I, 32 * I, ib, ib);
         store_tile(p.Rinv, p.l, D, 32 * I, 32 * I, ib, ib);  // X_II for the L_JI GEMMs and the inverse
         CDF_MARK(13);
         publish(p.lflag + I * p.nb + I, want);
@@ -322,7 +320,7 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
         alive = (K == J || wait_flag(p, p.lflag + I * p.nb + K, want, attempt)) &&
                 wait_flag(p, p.xflag + K * p.nb + J, want, attempt);
         if (!alive) break;
-        load_tile(A, p.G, p.ld, 32 * I, 32 * K, ib, 32);    // L_IK
+        load_tile(A, p.L, p.l, 32 * I, 32 * K, ib, 32);    // L_IK
         load_tile(B, p.Rinv, p.l, 32 * K, 32 * J, 32, jb);  // X_KJ
         __syncthreads();
         tile_add_ab(S, A, B);
@@ -382,7 +380,7 @@ void chol_inv_df(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *fl
   using namespace cdf;
   const int nb = (int)ceil_div(l, 32);
   const int tiles = 1 + nb * (nb - 1) / 2;  // (0,0) and the strictly lower tiles
-  DBuf<double> G0((size_t)l * l, c.stream);
+  DBuf<double> L((size_t)l * l, c.stream);
   DBuf<int> flags((size_t)2 * nb * nb + 1, c.stream);
   NM_CUDA(cudaMemsetAsync(flags.p, 0, flags.n * sizeof(int), c.stream));
   DfP p{};
@@ -390,7 +388,7 @@ void chol_inv_df(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *fl
   p.ld = ld;
   p.l = (int)l;
   p.nb = nb;
-  p.G0 = G0.p;
+  p.L = L.p;
   p.Rinv = Rinv;
   p.lflag = flags.p;
   p.xflag = flags.p + nb * nb;
