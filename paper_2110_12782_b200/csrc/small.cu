@@ -720,12 +720,14 @@ __global__ void k_bisect(const double *__restrict__ d, const double *__restrict_
   w[m] = 0.5 * (lo + hi);
 }
 
-// Eigenvalue m (ascending) by multisection: one warp per eigenvalue, the 32
-// lanes evaluate Sturm counts at 64 interior points of the current bracket
-// (two interleaved recurrences per lane) and two ballots pick the
-// sub-interval holding the m-th eigenvalue (6 bits per round instead of 1);
-// T's diagonal / off-diagonal squares live in shared memory.
-constexpr int MSW = 8;  // warps (eigenvalues) per block
+// Eigenvalue m (ascending) by multisection: one block of MSW warps per
+// eigenvalue, its lanes evaluate Sturm counts at 64·MSW interior points of
+// the current bracket (two interleaved recurrences per lane) and ballots pick
+// the sub-interval holding the m-th eigenvalue (7 bits per round instead of
+// 1); T's diagonal / off-diagonal squares live in shared memory.  The Sturm
+// recurrences are fp64-issue bound: small blocks spread the l eigenvalues
+// over every SM (one or two warps per SM sub-partition).
+constexpr int MSW = 2;  // warps per block, all on one eigenvalue (64·MSW points per round)
 __device__ __forceinline__ double pow2_of_exponent(double m) {  // 2^-e for m = f · 2^e, f in [1, 2)
   const int e = ((__double2hiint(m) >> 20) & 0x7ff) - 1023;
   const int be = min(max(1023 - e, 1), 2046);
@@ -780,7 +782,8 @@ __global__ void __launch_bounds__(MSW * 32) k_multisect(const double *__restrict
     se2[i] = (i + 1 < l) ? (e[i] * inv) * (e[i] * inv) : 0.0;
   }
   __syncthreads();
-  const int m = blockIdx.x * MSW + (threadIdx.x >> 5);
+  const int m = blockIdx.x, wi = threadIdx.x >> 5;
+  __shared__ unsigned masks[2 * MSW];
   double lo = 1e300, hi = -1e300;
   for (int i = lane; i < l; i += 32) {
     const double r = (i > 0 ? fabs(e[i - 1]) * inv : 0.0) + (i + 1 < l ? fabs(e[i]) * inv : 0.0);
@@ -791,25 +794,36 @@ __global__ void __launch_bounds__(MSW * 32) k_multisect(const double *__restrict
     lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
     hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
   }
-  if (m >= l) return;
   const double eps = 2.220446049250313e-16;
   lo -= 4.0 * eps + 1e-300;
   hi += 4.0 * eps + 1e-300;
-  // 64 points per round (two per lane): 6 bits of the eigenvalue per round
+  // 64·MSW points per round (two per lane; warp wi takes points 64 wi + 1 ..
+  // 64 wi + 64).  Every
+  // thread takes the same (block-uniform) decision from the shared ballots.
+  constexpr int NP = 64 * MSW;
   for (int it = 0; it < 40; ++it) {
     if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 1e-300) break;
-    const double step = (hi - lo) / 65.0;
+    const double step = (hi - lo) / (double)(NP + 1);
     int ca, cb;
-    sturm2(sd, se2, l, lo + step * (double)(lane + 1), lo + step * (double)(lane + 33), ca, cb);
+    sturm2(sd, se2, l, lo + step * (double)(64 * wi + lane + 1), lo + step * (double)(64 * wi + lane + 33), ca, cb);
     const unsigned above_a = __ballot_sync(0xffffffffu, ca > m), above_b = __ballot_sync(0xffffffffu, cb > m);
-    const int jf = above_a ? __ffs(above_a) - 1 : (above_b ? 32 + __ffs(above_b) - 1 : 64);
+    if (lane == 0) {
+      masks[2 * wi] = above_a;
+      masks[2 * wi + 1] = above_b;
+    }
+    __syncthreads();
+    int jf = NP;
+#pragma unroll
+    for (int q = 2 * MSW - 1; q >= 0; --q)
+      if (masks[q]) jf = 32 * q + __ffs(masks[q]) - 1;
+    __syncthreads();
     const double nlo = jf == 0 ? lo : lo + step * (double)jf;
-    const double nhi = jf == 64 ? hi : lo + step * (double)(jf + 1);
+    const double nhi = jf == NP ? hi : lo + step * (double)(jf + 1);
     if (!(nhi < hi || nlo > lo)) break;  // no progress at this precision
     lo = nlo;
     hi = nhi;
   }
-  if (lane == 0) w[m] = 0.5 * (lo + hi) / inv;
+  if (threadIdx.x == 0) w[m] = 0.5 * (lo + hi) / inv;
 }
 
 // Inverse iteration (dstein-style): one warp per cluster of (near-)degenerate
@@ -1066,7 +1080,7 @@ void sym_eig(Ctx &c, double *S, int64_t l64, double *lam, double *V, bool abs_or
     attr = true;
   }
   NM_LAUNCH(c, "tridiag", k_tridiag<<<TDC, TDT, smem, s>>>(S, l, d, e, Hv, hb));
-  NM_LAUNCH(c, "multisect", k_multisect<<<ceil_div(l, MSW), MSW * 32, (size_t)2 * l * sizeof(double), s>>>(d, e, l, w));
+  NM_LAUNCH(c, "multisect", k_multisect<<<l, MSW * 32, (size_t)2 * l * sizeof(double), s>>>(d, e, l, w));
   DBuf<int> cst(l + 1, s), ncl(1, s);
   NM_LAUNCH(c, "clusters", k_clusters<<<1, 32, 0, s>>>(w, d, e, l, cst, ncl));
   const size_t ivsm = (size_t)IVW * 4 * l * sizeof(double) + (size_t)IVW * l + 16 + (size_t)IVW * l * sizeof(double);

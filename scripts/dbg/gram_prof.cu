@@ -1,7 +1,6 @@
 // Gram timing harness: tc_gram at the configs[2] block shape (n' × 286, ld 288),
 // exact (3xTF32) and inexact (tf32), symmetric.  nvcc -gencode arch=compute_100a,code=sm_100a
 // -O3 -std=c++17 -I.. scripts/dbg/gram_prof.cu -lcuda -o scripts/dbg/gram_prof
-#define TC_PROF
 #include "../../paper_2110_12782_b200/csrc/tc_gemm.cu"
 #include <cstdio>
 using namespace netmfp;
