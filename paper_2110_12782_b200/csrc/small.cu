@@ -51,7 +51,10 @@ __device__ double block_sum(double v, double *red) {
 // 32×32 output tile per 256-thread CTA (2×2 per thread), K in steps of 32
 // with the next step's operands prefetched into registers while the current
 // one is consumed from shared memory (small l×l problems: the grid, not the
-// FMA rate, is what limits them, so tiles are small and many).
+// FMA rate, is what limits them, so tiles are small and many).  Long K is
+// split over the CTAs of a cluster (gridDim.z = cluster size); rank 0 adds
+// the other ranks' partial tiles from their shared memory in rank order
+// (deterministic).
 __global__ void __launch_bounds__(256) k_gemm64(bool ta, bool tb, int64_t M, int64_t N, int64_t K,
                                                 double alpha, const double *__restrict__ A, int64_t lda,
                                                 const double *__restrict__ B, int64_t ldb, double beta,
@@ -60,6 +63,8 @@ __global__ void __launch_bounds__(256) k_gemm64(bool ta, bool tb, int64_t M, int
   __shared__ double Bs[32][33];  // [k][n]
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const int64_t m0 = (int64_t)blockIdx.y * 32, n0 = (int64_t)blockIdx.x * 32;
+  const int64_t kchunk = (K + 32 * gridDim.z - 1) / (32 * gridDim.z) * 32;
+  const int64_t kb = (int64_t)blockIdx.z * kchunk, ke = min(K, kb + kchunk);
   // loader mapping: 4 elements of A and 4 of B per thread per K step
   double ra[4], rb[4];
   auto load = [&](int64_t k0) {
@@ -69,11 +74,11 @@ __global__ void __launch_bounds__(256) k_gemm64(bool ta, bool tb, int64_t M, int
       int kk, mm;
       if (ta) { mm = idx % 32; kk = idx / 32; } else { kk = idx % 32; mm = idx / 32; }  // coalesced source
       const int64_t gm = m0 + mm, gk = k0 + kk;
-      ra[q] = (gm < M && gk < K) ? (ta ? A[gk * lda + gm] : A[gm * lda + gk]) : 0.0;
+      ra[q] = (gm < M && gk < ke) ? (ta ? A[gk * lda + gm] : A[gm * lda + gk]) : 0.0;
       int nn;
       if (tb) { kk = idx % 32; nn = idx / 32; } else { nn = idx % 32; kk = idx / 32; }
       const int64_t gn = n0 + nn, gk2 = k0 + kk;
-      rb[q] = (gn < N && gk2 < K) ? (tb ? B[gn * ldb + gk2] : B[gk2 * ldb + gn]) : 0.0;
+      rb[q] = (gn < N && gk2 < ke) ? (tb ? B[gn * ldb + gk2] : B[gk2 * ldb + gn]) : 0.0;
     }
   };
   auto stash = [&]() {
@@ -85,11 +90,11 @@ __global__ void __launch_bounds__(256) k_gemm64(bool ta, bool tb, int64_t M, int
     }
   };
   double acc[2][2] = {};
-  load(0);
-  for (int64_t k0 = 0; k0 < K; k0 += 32) {
+  load(kb);
+  for (int64_t k0 = kb; k0 < ke; k0 += 32) {
     stash();
     __syncthreads();
-    if (k0 + 32 < K) load(k0 + 32);
+    if (k0 + 32 < ke) load(k0 + 32);
 #pragma unroll 8
     for (int kk = 0; kk < 32; ++kk) {
       const double a0 = As[kk][ty], a1 = As[kk][ty + 16];
@@ -100,6 +105,21 @@ __global__ void __launch_bounds__(256) k_gemm64(bool ta, bool tb, int64_t M, int
       acc[1][1] = fma(a1, b1, acc[1][1]);
     }
     __syncthreads();
+  }
+  if (gridDim.z > 1) {
+    __shared__ double part[4][256];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) part[q][threadIdx.x] = acc[q / 2][q % 2];
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    if (blockIdx.z == 0)
+      for (unsigned r = 1; r < gridDim.z; ++r) {
+        const double *rp = cl.map_shared_rank(&part[0][0], r);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q / 2][q % 2] += rp[q * 256 + threadIdx.x];
+      }
+    cl.sync();  // remote partials stay alive until rank 0 has read them
+    if (blockIdx.z != 0) return;
   }
 #pragma unroll
   for (int i = 0; i < 2; ++i)
@@ -116,8 +136,23 @@ __global__ void __launch_bounds__(256) k_gemm64(bool ta, bool tb, int64_t M, int
 void gemm64(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double *A,
             int64_t lda, const double *B, int64_t ldb, double beta, double *C, int64_t ldc) {
   if (M <= 0 || N <= 0) return;
-  dim3 grid(ceil_div(N, 32), ceil_div(M, 32));
-  NM_LAUNCH(c, "gemm64", k_gemm64<<<grid, 256, 0, c.stream>>>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc));
+  const int64_t tiles = ceil_div(N, 32) * ceil_div(M, 32);
+  // split K over a cluster while the tile grid leaves SMs idle (<= 2 CTAs per SM)
+  int split = 1;
+  while (split < 8 && tiles * split * 2 <= 2 * c.num_sms && K >= 64 * split * 2) split *= 2;
+  dim3 grid(ceil_div(N, 32), ceil_div(M, 32), split);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.stream = c.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = split;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  NM_LAUNCH(c, "gemm64", NM_CUDA(cudaLaunchKernelEx(&cfg, k_gemm64, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc)));
 }
 
 __global__ void k_symmetrize(double *S, int64_t l, int64_t ld) {
