@@ -124,3 +124,22 @@ def test_sym_eig_repeatable(L, ctx, l):
         outs.append((lam.cpu().numpy(), V.cpu().numpy()))
     for lam, V in outs[1:]:
         assert np.array_equal(lam, outs[0][0]) and np.array_equal(V, outs[0][1])
+
+
+def test_gram_orth_repeatable(L, ctx):
+    """Gram partials are reduced in a fixed order and the CholeskyQR tile
+    dataflow publishes through release/acquire flags: repeated calls on the
+    same input must agree bit for bit."""
+    n, c = 90001, 286
+    Y = (np.random.default_rng(5).standard_normal((n, c)) * np.logspace(0, 1, c)[None, :]).astype(np.float32)
+    Yd = padded(n, c); Yd.copy_(torch.from_numpy(Y))
+    G0 = Q0 = None
+    for _ in range(6):
+        G = torch.zeros(c, c, dtype=torch.float64, device=DEV)
+        L.netmfp_gram(ctx, Yd, Yd, G)
+        Qd = padded(n, c)
+        L.netmfp_orthonormalize(ctx, Yd, Qd, 2)
+        if G0 is None:
+            G0, Q0 = G.clone(), Qd.clone()
+        else:
+            assert torch.equal(G, G0) and torch.equal(Qd, Q0)
