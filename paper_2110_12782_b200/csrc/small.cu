@@ -836,8 +836,11 @@ __global__ void __launch_bounds__(MSW * 32) k_multisect(const double *__restrict
   // 64 wi + 64).  Every
   // thread takes the same (block-uniform) decision from the shared ballots.
   constexpr int NP = 64 * MSW;
+  // stop at 2 ulp relative or 4 eps absolute in the scaled T (||T|| in [1/2, 1)):
+  // eigenvalues near 0 are only determined to ~eps ||T|| by the Householder
+  // reduction anyway, and bisecting them to 1e-300 took up to 40 rounds
   for (int it = 0; it < 40; ++it) {
-    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 1e-300) break;
+    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 4.0 * eps) break;
     const double step = (hi - lo) / (double)(NP + 1);
     int ca, cb;
     sturm2(sd, se2, l, lo + step * (double)(64 * wi + lane + 1), lo + step * (double)(64 * wi + lane + 33), ca, cb);
