@@ -895,38 +895,50 @@ __global__ void __launch_bounds__(IVW * 32) k_invit(const double *__restrict__ d
   double sigma = 0.0;
   for (int m = m0; m < m1; ++m) sigma += w[m];
   sigma /= (m1 - m0);
+  // T - sigma I loaded by the whole warp (one serial lane would wait on every
+  // global load in turn), then factored by lane 0
+  for (int i = ln; i < l; i += 32) {
+    dg[i] = d[i] - sigma;
+    if (i + 1 < l) { dl[i] = e[i]; du[i] = e[i]; }
+    du2[i] = 0.0;
+    piv[i] = 0;
+  }
+  __syncwarp();
   if (ln == 0) {
-    for (int i = 0; i < l; ++i) {
-      dg[i] = d[i] - sigma;
-      if (i + 1 < l) { dl[i] = e[i]; du[i] = e[i]; }
-      du2[i] = 0.0;
-      piv[i] = 0;
-    }
+    // dgttrf with the running pivot row (g = dg[i], u = du[i] as updated so
+    // far) carried in registers: the dependence chain stays out of shared memory
+    double g = dg[0], u = l > 1 ? du[0] : 0.0;
     for (int i = 0; i + 1 < l; ++i) {
-      if (fabs(dg[i]) >= fabs(dl[i])) {
-        if (dg[i] != 0.0) {
-          double f = dl[i] / dg[i];
+      const double lo = dl[i], gn = dg[i + 1], un = i + 2 < l ? du[i + 1] : 0.0;
+      if (fabs(g) >= fabs(lo)) {
+        double gnew = gn;
+        if (g != 0.0) {
+          const double f = lo / g;
           dl[i] = f;
-          dg[i + 1] -= f * du[i];
+          gnew = gn - f * u;
         }
+        dg[i] = g;
+        du[i] = u;
+        g = gnew;
+        u = un;
       } else {
-        double f = dg[i] / dl[i];
-        dg[i] = dl[i];
+        const double f = g / lo;
+        dg[i] = lo;
         dl[i] = f;
-        double t = du[i];
-        du[i] = dg[i + 1];
-        dg[i + 1] = t - f * dg[i + 1];
-        if (i + 2 < l) {
-          du2[i] = du[i + 1];
-          du[i + 1] = -f * du[i + 1];
-        }
+        du[i] = gn;
+        g = u - f * gn;
+        if (i + 2 < l) du2[i] = un;
+        u = -f * un;
         piv[i] = 1;
       }
     }
-    for (int i = 0; i < l; ++i) {
-      if (fabs(dg[i]) < tiny) dg[i] = dg[i] < 0 ? -tiny : tiny;
-      dg[i] = 1.0 / dg[i];  // the solves multiply by the reciprocal pivots
-    }
+    dg[l - 1] = g;
+  }
+  __syncwarp();
+  for (int i = ln; i < l; i += 32) {
+    double gi = dg[i];
+    if (fabs(gi) < tiny) gi = gi < 0 ? -tiny : tiny;
+    dg[i] = 1.0 / gi;  // the solves multiply by the reciprocal pivots
   }
   __syncwarp();
   if (m1 - m0 == 1) {
@@ -941,18 +953,27 @@ __global__ void __launch_bounds__(IVW * 32) k_invit(const double *__restrict__ d
     __syncwarp();
     for (int it = 0; it < 3; ++it) {
       if (ln == 0) {
+        // the substitutions carry the running entries in registers, so the
+        // dependence chain is one FMA per step (no shared-memory round trip)
+        double cur = x[0];
         for (int i = 0; i + 1 < l; ++i) {
+          const double nxt = x[i + 1];
           if (!piv[i]) {
-            x[i + 1] -= dl[i] * x[i];
+            x[i] = cur;
+            cur = nxt - dl[i] * cur;
           } else {
-            const double t = x[i];
-            x[i] = x[i + 1];
-            x[i + 1] = t - dl[i] * x[i];
+            x[i] = nxt;
+            cur = cur - dl[i] * nxt;
           }
         }
-        x[l - 1] *= dg[l - 1];
-        if (l > 1) x[l - 2] = (x[l - 2] - du[l - 2] * x[l - 1]) * dg[l - 2];
-        for (int i = l - 3; i >= 0; --i) x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) * dg[i];
+        double x1 = cur * dg[l - 1], x2 = 0.0;  // x[i+1], x[i+2]
+        x[l - 1] = x1;
+        for (int i = l - 2; i >= 0; --i) {
+          const double xi = (x[i] - du[i] * x1 - (i + 2 < l ? du2[i] * x2 : 0.0)) * dg[i];
+          x[i] = xi;
+          x2 = x1;
+          x1 = xi;
+        }
       }
       __syncwarp();
       double nrm = 0.0;
