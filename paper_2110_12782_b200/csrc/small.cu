@@ -1053,7 +1053,8 @@ __global__ void k_clusters(const double *__restrict__ w, const double *__restric
 // the next reflector is prefetched while the current one is applied (Hv rows
 // are zero at k <= j, so no masking below the reflector's support)
 constexpr int BT_NR = 15;  // l <= 480
-__global__ void __launch_bounds__(256) k_backtransform(const double *__restrict__ Hv, const double *__restrict__ hbeta,
+constexpr int BT_T = 64;  // 2 warps per block: the l eigenvectors spread over every SM
+__global__ void __launch_bounds__(BT_T) k_backtransform(const double *__restrict__ Hv, const double *__restrict__ hbeta,
                                                        int l, double *__restrict__ Zt) {
   const int m = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int ln = threadIdx.x % 32;
@@ -1080,10 +1081,14 @@ __global__ void __launch_bounds__(256) k_backtransform(const double *__restrict_
     for (int i = 0; i < BT_NR; ++i) v[i] = vn[i];
     const double b = __ldg(hbeta + j);
     if (j > 0) load(j - 1);
-    double sacc = 0.0;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;  // three short chains instead of one of BT_NR
 #pragma unroll
-    for (int i = 0; i < BT_NR; ++i) sacc = fma(v[i], x[i], sacc);
-    sacc = warp_sum(sacc) * b;
+    for (int i = 0; i < BT_NR; i += 3) {
+      s0 = fma(v[i], x[i], s0);
+      if (i + 1 < BT_NR) s1 = fma(v[i + 1], x[i + 1], s1);
+      if (i + 2 < BT_NR) s2 = fma(v[i + 2], x[i + 2], s2);
+    }
+    const double sacc = warp_sum((s0 + s1) + s2) * b;
 #pragma unroll
     for (int i = 0; i < BT_NR; ++i) x[i] = fma(-sacc, v[i], x[i]);
   }
@@ -1149,7 +1154,7 @@ void sym_eig(Ctx &c, double *S, int64_t l64, double *lam, double *V, bool abs_or
     attr_iv = true;
   }
   NM_LAUNCH(c, "invit", k_invit<<<ceil_div(l, IVW), IVW * 32, ivsm, s>>>(d, e, l, w, cst, ncl, Zt, 0x1234567u));
-  NM_LAUNCH(c, "backtransform", k_backtransform<<<ceil_div((int64_t)l * 32, 256), 256, 0, s>>>(Hv, hb, l, Zt));
+  NM_LAUNCH(c, "backtransform", k_backtransform<<<ceil_div((int64_t)l * 32, BT_T), BT_T, 0, s>>>(Hv, hb, l, Zt));
   NM_LAUNCH(c, "eig_sort", k_eig_sort<<<l, 128, 0, s>>>(w, Zt, l, abs_order, lam, V));
 }
 
