@@ -62,17 +62,23 @@ def philox4x32_10(c0, c1, c2, c3, k0, k1):
 def gaussian_matrix(n: int, cols: int, seed: int, tag: int = TAG_OMEGA) -> np.ndarray:
     """Omega = randn(n, cols) of Alg. 2 step 2 [R1].
 
-    Entry (i, j): Philox4x32-10 on counter (j, i mod 2^32, i >> 32, tag),
-    key (seed mod 2^32, seed >> 32); Box–Muller on the first two words:
-    u_t = (w_t + 1/2) 2^-32, g = sqrt(-2 ln u_0) cos(2 pi u_1)."""
-    i = np.repeat(np.arange(n, dtype=np.uint64), cols)
-    j = np.tile(np.arange(cols, dtype=np.uint64), n)
-    w0, w1, _, _ = philox4x32_10(j, i & MASK32, i >> np.uint64(32), tag,
-                                 seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF)
-    u0 = (w0.astype(np.float64) + 0.5) * 2.0 ** -32
-    u1 = (w1.astype(np.float64) + 0.5) * 2.0 ** -32
-    g = np.sqrt(-2.0 * np.log(u0)) * np.cos(2.0 * np.pi * u1)
-    return g.reshape(n, cols)
+    Entries (i, 4q .. 4q+3): Philox4x32-10 on counter (q, i mod 2^32, i >> 32,
+    tag), key (seed mod 2^32, seed >> 32); u_t = (w_t + 1/2) 2^-32 and
+    Box–Muller with both outputs of each word pair:
+      g(i, 4q)   = r_0 cos(2 pi u_1),  g(i, 4q+1) = r_0 sin(2 pi u_1),
+      g(i, 4q+2) = r_2 cos(2 pi u_3),  g(i, 4q+3) = r_2 sin(2 pi u_3),
+    r_t = sqrt(-2 ln u_t)."""
+    nq = (cols + 3) // 4
+    i = np.repeat(np.arange(n, dtype=np.uint64), nq)
+    q = np.tile(np.arange(nq, dtype=np.uint64), n)
+    w0, w1, w2, w3 = philox4x32_10(q, i & MASK32, i >> np.uint64(32), tag,
+                                   seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF)
+    u0, u1, u2, u3 = ((w.astype(np.float64) + 0.5) * 2.0 ** -32 for w in (w0, w1, w2, w3))
+    r0 = np.sqrt(-2.0 * np.log(u0))
+    r2 = np.sqrt(-2.0 * np.log(u2))
+    g = np.stack([r0 * np.cos(2.0 * np.pi * u1), r0 * np.sin(2.0 * np.pi * u1),
+                  r2 * np.cos(2.0 * np.pi * u3), r2 * np.sin(2.0 * np.pi * u3)], axis=-1)
+    return g.reshape(n, 4 * nq)[:, :cols]
 
 
 def gen_sparse_sign(n: int, h: int, z: int, seed: int, tag: int):
