@@ -267,7 +267,7 @@ struct GramRed {
   int64_t nchain, part_stride;
 };
 
-// G = Σ_chains partials, one block per 32 consecutive partial positions (a
+// G = Σ_chains partials, one block per 128 consecutive partial positions (a
 // partial unit is stored column-major, position = off + 128·col + row, so the
 // epilogue's stores and these loads are coalesced); warp w sums chains
 // w, w+8, … in a fixed order and the 8 warp sums are added in warp order
@@ -275,27 +275,35 @@ struct GramRed {
 constexpr int kRedWarps = 8;
 __global__ void __launch_bounds__(32 * kRedWarps) k_gram_reduce(const float *__restrict__ part, GramRed R,
                                                                double *__restrict__ G, int64_t ldg) {
-  __shared__ double red[kRedWarps][32];
+  // 128 positions per block, 4 per lane (16-B loads); warp w sums chains
+  // w, w+8, … in order, the 8 warp sums are added in warp order
+  __shared__ double red[kRedWarps][128];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t pos = blockIdx.x * 32LL + lane;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  if (pos < R.part_stride) {
-    const float *src = part + pos;
+  const int64_t p4 = blockIdx.x * 128LL + 4 * lane;  // part_stride is a multiple of 4
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  if (p4 < R.part_stride) {
+    const float *src = part + p4;
     int64_t c = warp;
-    for (; c + 3 * kRedWarps < R.nchain; c += 4 * kRedWarps) {
-      s0 += (double)__ldg(src + c * R.part_stride);
-      s1 += (double)__ldg(src + (c + kRedWarps) * R.part_stride);
-      s2 += (double)__ldg(src + (c + 2 * kRedWarps) * R.part_stride);
-      s3 += (double)__ldg(src + (c + 3 * kRedWarps) * R.part_stride);
+    for (; c + kRedWarps < R.nchain; c += 2 * kRedWarps) {
+      const float4 a = __ldg(reinterpret_cast<const float4 *>(src + c * R.part_stride));
+      const float4 b = __ldg(reinterpret_cast<const float4 *>(src + (c + kRedWarps) * R.part_stride));
+      s[0] += (double)a.x; s[1] += (double)a.y; s[2] += (double)a.z; s[3] += (double)a.w;
+      s[0] += (double)b.x; s[1] += (double)b.y; s[2] += (double)b.z; s[3] += (double)b.w;
     }
-    for (; c < R.nchain; c += kRedWarps) s0 += (double)__ldg(src + c * R.part_stride);
+    if (c < R.nchain) {
+      const float4 a = __ldg(reinterpret_cast<const float4 *>(src + c * R.part_stride));
+      s[0] += (double)a.x; s[1] += (double)a.y; s[2] += (double)a.z; s[3] += (double)a.w;
+    }
   }
-  red[warp][lane] = (s0 + s1) + (s2 + s3);
-  __syncthreads();
-  if (warp != 0 || pos >= R.part_stride) return;
-  double s = 0.0;
 #pragma unroll
-  for (int w = 0; w < kRedWarps; ++w) s += red[w][lane];
+  for (int t = 0; t < 4; ++t) red[warp][4 * lane + t] = s[t];
+  __syncthreads();
+  if (threadIdx.x >= 128) return;
+  const int64_t pos = blockIdx.x * 128LL + threadIdx.x;
+  if (pos >= R.part_stride) return;
+  double sum = 0.0;
+#pragma unroll
+  for (int w = 0; w < kRedWarps; ++w) sum += red[w][threadIdx.x];
   for (int ui = 0; ui < R.nunits; ++ui) {
     const GUnit &u = R.u[ui];
     const int64_t loc = pos - u.off;
@@ -303,10 +311,10 @@ __global__ void __launch_bounds__(32 * kRedWarps) k_gram_reduce(const float *__r
     const int64_t i = (int64_t)u.mblk * 32 + loc % 128, j = (int64_t)u.nblk * 32 + loc / 128;
     if (i >= R.a || j >= R.b) return;
     if (!R.sym) {
-      G[i * ldg + j] = s;
+      G[i * ldg + j] = sum;
     } else if (i <= j) {
-      G[i * ldg + j] = s;
-      G[j * ldg + i] = s;
+      G[i * ldg + j] = sum;
+      G[j * ldg + i] = sum;
     }
     return;
   }
@@ -824,7 +832,7 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
   R.nchain = nchain;
   R.part_stride = total;
   NM_LAUNCH(c, "tc_gram_reduce",
-            k_gram_reduce<<<ceil_div(total, 32), 32 * kRedWarps, 0, c.stream>>>(part.p, R, G, ldg));
+            k_gram_reduce<<<ceil_div(total, 128), 32 * kRedWarps, 0, c.stream>>>(part.p, R, G, ldg));
 }
 
 // Bᵀ for the tensor-core GEMM, zero padded to nrows × 32 nk:
