@@ -35,6 +35,14 @@ __global__ void k_make_keys(const int32_t *__restrict__ src, const int32_t *__re
 }
 
 // rowptr[u] = first key index with row >= row0 + u (lower bound), u in [0, n]
+// nnz = unique keys minus the sentinel row n (the last unique key if present),
+// so the host reads it together with the error flag in one round trip
+__global__ void k_nnz(const uint64_t *__restrict__ keys, const int64_t *__restrict__ nuniq, uint64_t n_all, int cb,
+                      int64_t *__restrict__ nnz) {
+  const int64_t u = *nuniq;
+  *nnz = (u > 0 && (keys[u - 1] >> cb) == n_all) ? u - 1 : u;
+}
+
 __global__ void k_rowptr(const uint64_t *__restrict__ keys, int64_t nnz, int64_t n, int64_t row0, int cb,
                          int64_t *__restrict__ rowptr) {
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -125,20 +133,15 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
     } else {
       nsel.zero();
     }
-    int64_t nuniq = 0;
+    // drop the sentinel (row n) if present: it is the last unique key
+    DBuf<int64_t> dnnz(1, s);
+    NM_LAUNCH(c, "nnz", k_nnz<<<1, 1, 0, s>>>(keys, nsel, (uint64_t)n_all, cb, dnnz));
+    int64_t nnz = 0;
     int hbad = 0;
-    NM_CUDA(cudaMemcpyAsync(&nuniq, nsel.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    NM_CUDA(cudaMemcpyAsync(&nnz, dnnz.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     NM_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     NM_CUDA(cudaStreamSynchronize(s));
     NM_REQUIRE(!hbad, "build_csr: vertex id out of [0, n)");
-    // drop the sentinel (row n) if present: it is the last unique key
-    int64_t nnz = nuniq;
-    if (nnz > 0) {
-      uint64_t last = 0;
-      NM_CUDA(cudaMemcpyAsync(&last, keys.p + nnz - 1, 8, cudaMemcpyDeviceToHost, s));
-      NM_CUDA(cudaStreamSynchronize(s));
-      if ((last >> cb) == (uint64_t)n_all) --nnz;
-    }
     g->nnz = nnz;
     g->nnz_global = nnz;
     g->rowptr.alloc(n + 1, s);
