@@ -567,7 +567,7 @@ __device__ unsigned long long g_td_t[8][4][512];
 #else
 #define TD_MARK(ph)
 #endif
-constexpr int TDC = 8;     // cluster size (CTAs) for the tridiagonalisation (16: measured slower)
+constexpr int TDC = 8;     // cluster size (CTAs) for the tridiagonalisation (4 and 16: measured slower)
 // split cluster barrier (every thread arrives; release / acquire at cluster scope)
 __device__ __forceinline__ void cluster_arrive() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
