@@ -17,7 +17,7 @@ import scipy.sparse as sp
 __all__ = [
     "philox4x32_10", "gaussian_matrix", "gen_sparse_sign", "TAG_OMEGA", "TAG_PSI", "TAG_PI",
     "build_csr", "deg_pow", "spmm_scaled", "spmm_scaled_rows", "normalized_spmm",
-    "eig_svd", "freigs", "factor_pair", "trunc_log", "log1p_trunc", "elementwise_log",
+    "eig_svd", "orth_range", "freigs", "factor_pair", "trunc_log", "log1p_trunc", "elementwise_log",
     "sketch_y", "sketch_z", "sparse_sign_apply_T", "core_solve", "single_pass_svd", "embedding_from_svd",
     "cheb_coeffs", "spectral_propagate", "netmf_plus", "sym_eig_abs_sorted",
 ]
@@ -210,6 +210,26 @@ def eig_svd(Y):
     return Q, S, V
 
 
+def orth_range(Y, rtol: float = 1e-12):
+    """Q = orth(Y) of Alg. 4 step 4 ("Q = orth(Y)"; :305 realises
+    it with eigSVD).  With full column rank this IS eigSVD (same steps, same Q).
+    PAPER.md:215 notes eigSVD's numerical issue when Y lacks full column rank;
+    then orth(Y) is an orthonormal basis of range(Y): the eigen-directions of
+    B = Y^T Y with D_i <= rtol * D_1 are dropped (DESIGN.md [R10]; e.g. a Psi
+    column whose z rows are all isolated vertices gives an exactly-zero column
+    of Y).  Returns Q with rank(Y) columns."""
+    Y = np.asarray(Y, dtype=np.float64)
+    B = Y.T @ Y
+    D, V = np.linalg.eigh(B)
+    order = np.argsort(D)[::-1]
+    D, V = D[order], V[:, order]
+    r = int(np.sum(D > rtol * D[0])) if D[0] > 0 else 0
+    if r == 0:
+        raise np.linalg.LinAlgError("orth: Y is zero")
+    S = np.sqrt(D[:r])
+    return Y @ (V[:, :r] / S[None, :])
+
+
 def sym_eig_abs_sorted(S):
     """[U, Lambda] = eig(S) for symmetric S, ordered by descending |lambda|
     (ties: descending signed value) [R3]."""
@@ -331,7 +351,7 @@ def single_pass_svd(F, C, scale: float, d: int, s2: int, s3: int, z: int, seed: 
     n = F.shape[0]
     rows_psi, sg_psi, p_psi = gen_sparse_sign(n, d + s2, z, seed, TAG_PSI)       # step 2
     Y = sketch_y(F, C, scale, rows_psi, sg_psi, p_psi, logmode)                  # step 3
-    Q, _, _ = eig_svd(Y)                                                         # step 4
+    Q = orth_range(Y)                                                            # step 4 [R10]
     rows_pi, sg_pi, p_pi = gen_sparse_sign(n, d + s3, z, seed, TAG_PI)           # step 5
     Z = sketch_z(F, C, scale, rows_pi, sg_pi, p_pi, logmode)                     # step 6
     PtQ = sparse_sign_apply_T(rows_pi, sg_pi, Q)

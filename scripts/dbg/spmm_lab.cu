@@ -1,0 +1,934 @@
+// spmm_lab.cu — standalone SpMM variant lab on a real CSR (tuning aid, not product).
+// Usage: spmm_lab <csr.bin> [cold_deg_max ...]
+//   csr.bin: int64 n, int64 nnz, int64 rowptr[n+1], int32 col[nnz]
+// Times Y[:, 0:C] = D^-a A X[:, 0:C] (ld 288) for kernel variants, L2 flushed
+// before every repetition; checks each variant against variant 0.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t e = (x);                                                               \
+    if (e != cudaSuccess) {                                                            \
+      fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e)); \
+      exit(1);                                                                         \
+    }                                                                                  \
+  } while (0)
+
+enum : int { H_COL = 1, H_Y = 2, H_X = 4, H_DET = 8 };
+
+struct G {
+  const int64_t *rowptr;
+  const int32_t *col;   // plain
+  const int32_t *colt;  // bit 31 set: cold column
+  int64_t n;
+  const int32_t *heavy;
+  const int64_t *seg_ptr, *seg_e0;
+  const int32_t *seg_h;
+  int64_t nsegs;
+  float *hsum;     // atomic variant: n_heavy x 128 per pass (y)
+  float *segsum;   // det variant: nsegs x 128 per pass
+  int32_t *hcnt;
+  int light_cap, heavy_seg, nblk_tile;
+  const float *X;
+  float *Y;
+  int ldx, cols;
+  float a;
+  int colbase, fold;  // fold: cols [fold0 + 16*py + 4*li] for li < 4 handled by each pass
+};
+
+__device__ __forceinline__ uint64_t pol_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+template <int HINT>
+__device__ __forceinline__ int32_t ldcol(const int32_t *p, uint64_t pf) {
+  if (HINT & H_COL) {
+    int32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pf));
+    return v;
+  }
+  return __ldg(p);
+}
+// gather of one neighbour row slice: hot -> evict_last, cold -> L1 no_allocate + evict_first
+template <int HINT>
+__device__ __forceinline__ float4 ldx(const float *Xc, uint32_t v, uint32_t ld, uint64_t pf, uint64_t pl) {
+  if (HINT & H_X) {
+    const bool cold = v >> 31;
+    const float *p = Xc + (uint64_t)(v & 0x7fffffffu) * ld;
+    float4 r;
+    if (cold)
+      asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                   : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(pf));
+    else
+      asm volatile("ld.global.nc.L1::evict_last.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                   : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(pl));
+    return r;
+  }
+  return __ldg(reinterpret_cast<const float4 *>(Xc + (uint64_t)(v & 0x7fffffffu) * ld));
+}
+template <int HINT>
+__device__ __forceinline__ void sty(float *p, float4 v, uint64_t pf) {
+  if (HINT & H_Y)
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
+                 "f"(v.y), "f"(v.z), "f"(v.w), "l"(pf));
+  else
+    *reinterpret_cast<float4 *>(p) = v;
+}
+__device__ __forceinline__ float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ float rsc(int d, float a) { return d > 0 ? exp2f(-a * __log2f((float)d)) : 0.f; }
+
+template <int HINT>
+__device__ __forceinline__ float4 gsum(const int32_t *col, int64_t e0, int64_t e1, const float *Xc, uint32_t ld,
+                                       uint64_t pf, uint64_t pl) {
+  float4 acc = make_float4(0, 0, 0, 0);
+  const int32_t *cp = col + e0;
+  int cnt = (int)(e1 - e0);
+  for (; cnt >= 4; cnt -= 4, cp += 4) {
+    const uint32_t v0 = ldcol<HINT>(cp, pf), v1 = ldcol<HINT>(cp + 1, pf), v2 = ldcol<HINT>(cp + 2, pf),
+                   v3 = ldcol<HINT>(cp + 3, pf);
+    const float4 x0 = ldx<HINT>(Xc, v0, ld, pf, pl), x1 = ldx<HINT>(Xc, v1, ld, pf, pl);
+    const float4 x2 = ldx<HINT>(Xc, v2, ld, pf, pl), x3 = ldx<HINT>(Xc, v3, ld, pf, pl);
+    acc = add4(add4(add4(x0, x1), add4(x2, x3)), acc);
+  }
+  for (; cnt > 0; --cnt, ++cp) acc = add4(ldx<HINT>(Xc, ldcol<HINT>(cp, pf), ld, pf, pl), acc);
+  return acc;
+}
+
+// LPR lanes per row (one float4 each): pass width 4*LPR columns; grid.y = pass
+template <int LPR, int HINT, int MINB = 8>
+__global__ void __launch_bounds__(256, MINB) k_lab(G g, int nblk_heavy) {
+  const int py = blockIdx.y, bx = blockIdx.x;
+  const uint64_t pf = pol_first(), pl = pol_last();
+  const int32_t *col = (HINT & H_X) ? g.colt : g.col;
+  const uint32_t ld = g.ldx;
+  const int m = min(nblk_heavy, g.nblk_tile);
+  bool is_heavy;
+  int idx;
+  if (bx < 2 * m) {
+    is_heavy = (bx & 1) == 0;
+    idx = bx >> 1;
+  } else {
+    is_heavy = nblk_heavy > g.nblk_tile;
+    idx = m + (bx - 2 * m);
+  }
+  const int lane = threadIdx.x & 31;
+  constexpr int GPW = 32 / LPR;
+  const int gq = lane / LPR, li = lane % LPR;
+  const int c = g.colbase + py * (LPR * 4) + li * 4;
+  const float *Xc = g.X + c;
+  if (!is_heavy) {
+    if (idx >= g.nblk_tile) return;
+    const int64_t ntiles = (g.n + 31) >> 5;
+    for (int64_t t = (int64_t)idx * 8 + (threadIdx.x >> 5); t < ntiles; t += (int64_t)g.nblk_tile * 8) {
+      const int64_t u0 = t << 5;
+      const int nrows = (int)min((int64_t)32, g.n - u0);
+      const int64_t rp = __ldg(g.rowptr + u0 + min(lane, nrows));
+      const int64_t rpn = __ldg(g.rowptr + u0 + min(lane + 1, nrows));
+      const int dl = (int)(rpn - rp);
+      const bool hv = dl > g.light_cap;
+      const unsigned hmask = __ballot_sync(0xffffffffu, hv);
+      uint32_t k0 = 0, k1 = 0, k2 = 0, k3 = 0;
+      if (!hv) {
+        if (dl > 0) k0 = ldcol<HINT>(col + rp, pf);
+        if (dl > 1) k1 = ldcol<HINT>(col + rp + 1, pf);
+        if (dl > 2) k2 = ldcol<HINT>(col + rp + 2, pf);
+        if (dl > 3) k3 = ldcol<HINT>(col + rp + 3, pf);
+      }
+      const float sl = rsc(dl, g.a);
+      const int64_t eb = __shfl_sync(0xffffffffu, rp, 0);
+      const int rel = (int)(rp - eb);
+#pragma unroll 1
+      for (int j = 0; j < LPR; ++j) {
+        const int r = gq + j * GPW;
+        const int d = __shfl_sync(0xffffffffu, dl, r);
+        const int ro = __shfl_sync(0xffffffffu, rel, r);
+        const float sr = __shfl_sync(0xffffffffu, sl, r);
+        const uint32_t q0 = __shfl_sync(0xffffffffu, k0, r), q1 = __shfl_sync(0xffffffffu, k1, r);
+        const uint32_t q2 = __shfl_sync(0xffffffffu, k2, r), q3 = __shfl_sync(0xffffffffu, k3, r);
+        if (r >= nrows || c >= g.cols || ((hmask >> r) & 1u)) continue;
+        float4 acc = make_float4(0, 0, 0, 0);
+        if (d > 0) {
+          acc = ldx<HINT>(Xc, q0, ld, pf, pl);
+          if (d > 1) {
+            const float4 x1 = ldx<HINT>(Xc, q1, ld, pf, pl);
+            float4 x2 = make_float4(0, 0, 0, 0), x3 = x2;
+            if (d > 2) x2 = ldx<HINT>(Xc, q2, ld, pf, pl);
+            if (d > 3) x3 = ldx<HINT>(Xc, q3, ld, pf, pl);
+            acc = add4(add4(x1, acc), add4(x2, x3));
+            if (d > 4) acc = add4(gsum<HINT>(col, eb + ro + 4, eb + ro + d, Xc, ld, pf, pl), acc);
+          }
+        }
+        sty<HINT>(g.Y + (u0 + r) * ld + c, make_float4(sr * acc.x, sr * acc.y, sr * acc.z, sr * acc.w), pf);
+      }
+    }
+    return;
+  }
+  constexpr int GPB = 256 / LPR;
+  const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (lane / LPR * LPR));
+  const int64_t sidx = (int64_t)idx * GPB + threadIdx.x / LPR;
+  if (sidx >= g.nsegs) return;
+  const int64_t h = __ldg(g.seg_h + sidx);
+  const int64_t e0 = __ldg(g.seg_e0 + sidx);
+  const int64_t u = __ldg(g.heavy + h);
+  const int64_t rb = __ldg(g.rowptr + u), re = __ldg(g.rowptr + u + 1);
+  const int64_t e1 = min(e0 + (int64_t)g.heavy_seg, re);
+  const int64_t s0 = __ldg(g.seg_ptr + h), s1 = __ldg(g.seg_ptr + h + 1);
+  const int pw = LPR * 4;  // pass width
+  float *dst = (HINT & H_DET) ? g.segsum + ((int64_t)py * g.nsegs + sidx) * pw + li * 4
+                              : g.hsum + ((int64_t)py * 1 + 0) * 0 + h * 288 + c;
+  const bool act = c < g.cols;
+  const float4 acc = act ? gsum<HINT>(col, e0, e1, Xc, ld, pf, pl) : make_float4(0, 0, 0, 0);
+  if (HINT & H_DET)
+    __stcg(reinterpret_cast<float4 *>(dst), acc);
+  else if (act)
+    atomicAdd(reinterpret_cast<float4 *>(dst), acc);
+  __syncwarp(gmask);
+  int32_t *cnt = g.hcnt + h * 4 + py;
+  int last = 0;
+  if (li == 0) {
+    __threadfence();
+    last = atomicAdd(cnt, 1) == (int)(s1 - s0) - 1;
+    if (last) __threadfence();
+  }
+  last = __shfl_sync(gmask, last, lane / LPR * LPR);
+  if (!last) return;
+  float4 tot;
+  if (HINT & H_DET) {
+    // fixed-order sum of the row's segment partials: deterministic
+    const float *sp = g.segsum + ((int64_t)py * g.nsegs + s0) * pw + li * 4;
+    tot = make_float4(0, 0, 0, 0);
+    int64_t ns = s1 - s0, j = 0;
+    for (; j + 4 <= ns; j += 4) {
+      const float4 a0 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 0) * pw));
+      const float4 a1 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 1) * pw));
+      const float4 a2 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 2) * pw));
+      const float4 a3 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 3) * pw));
+      tot = add4(tot, a0);
+      tot = add4(tot, a1);
+      tot = add4(tot, a2);
+      tot = add4(tot, a3);
+    }
+    for (; j < ns; ++j) tot = add4(tot, __ldcg(reinterpret_cast<const float4 *>(sp + j * pw)));
+  } else {
+    tot = __ldcg(reinterpret_cast<const float4 *>(dst));
+    __stcg(reinterpret_cast<float4 *>(dst), make_float4(0, 0, 0, 0));
+  }
+  const float sr = rsc((int)(re - rb), g.a);
+  if (act) sty<HINT>(g.Y + u * ld + c, make_float4(sr * tot.x, sr * tot.y, sr * tot.z, sr * tot.w), pf);
+  if (li == 0) *cnt = 0;
+}
+
+
+// ---------------------------------------------------------------- v2: flat edge walk, coalesced index windows
+__device__ __forceinline__ float4 ld4(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }
+
+template <int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_v2(G g, int nblk_heavy) {
+  const int py = blockIdx.y, bx = blockIdx.x;
+  const int32_t *col = g.col;
+  const uint32_t ld = g.ldx;
+  const int m = min(nblk_heavy, g.nblk_tile);
+  bool is_heavy;
+  int idx;
+  if (bx < 2 * m) {
+    is_heavy = (bx & 1) == 0;
+    idx = bx >> 1;
+  } else {
+    is_heavy = nblk_heavy > g.nblk_tile;
+    idx = m + (bx - 2 * m);
+  }
+  const int lane = threadIdx.x & 31;
+  const int c = py * 128 + lane * 4;
+  const float *Xc = g.X + c;
+  const unsigned FULL = 0xffffffffu;
+  const float4 z4 = make_float4(0, 0, 0, 0);
+  if (!is_heavy) {
+    if (idx >= g.nblk_tile) return;
+    const int64_t ntiles = (g.n + 31) >> 5;
+    for (int64_t t = (int64_t)idx * 8 + (threadIdx.x >> 5); t < ntiles; t += (int64_t)g.nblk_tile * 8) {
+      const int64_t u0 = t << 5;
+      const int nrows = (int)min((int64_t)32, g.n - u0);
+      const int64_t rp = __ldg(g.rowptr + u0 + min(lane, nrows));
+      const int64_t rpn = __ldg(g.rowptr + u0 + min(lane + 1, nrows));
+      const int dl = (int)(rpn - rp);
+      const unsigned hmask = __ballot_sync(FULL, dl > g.light_cap && lane < nrows);
+      const float sl = rsc(dl, g.a);
+      const int64_t ee = __shfl_sync(FULL, rpn, nrows - 1);
+      int64_t e = __shfl_sync(FULL, rp, 0);
+      int r = 0;
+      int64_t rend = __shfl_sync(FULL, rpn, 0);
+      int64_t wb = e;
+      uint32_t myidx = (wb + lane < ee) ? __ldg(col + wb + lane) : 0u;
+      float4 acc = z4;
+      while (true) {
+        // settle on the next light row that still has edges, writing finished rows
+        while (r < nrows && (e >= rend || ((hmask >> r) & 1u))) {
+          if ((hmask >> r) & 1u) {
+            e = rend;
+          } else {
+            const float s = __shfl_sync(FULL, sl, r);
+            *reinterpret_cast<float4 *>(g.Y + (u0 + r) * ld + c) = make_float4(s * acc.x, s * acc.y, s * acc.z, s * acc.w);
+            acc = z4;
+          }
+          ++r;
+          rend = __shfl_sync(FULL, rpn, min(r, 31));
+        }
+        if (r >= nrows) break;
+        // batch limit: the next heavy row's first edge (or the tile end)
+        const unsigned hm = (r < 31) ? (hmask >> (r + 1)) << (r + 1) : 0u;
+        const int64_t hstart = __shfl_sync(FULL, rp, hm ? __ffs(hm) - 1 : 0);
+        const int64_t limit = hm ? hstart : ee;
+        if (e + U > wb + 32) {
+          wb = e;
+          myidx = (wb + lane < ee) ? __ldg(col + wb + lane) : 0u;
+        }
+        float4 x[U];
+        const int base = (int)(e - wb);
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const uint32_t v = __shfl_sync(FULL, myidx, base + q);
+          x[q] = (e + q < limit) ? ld4(Xc + (uint64_t)v * ld) : z4;
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          if (e + q >= limit) break;
+          while (e + q >= rend) {
+            const float s = __shfl_sync(FULL, sl, r);
+            *reinterpret_cast<float4 *>(g.Y + (u0 + r) * ld + c) = make_float4(s * acc.x, s * acc.y, s * acc.z, s * acc.w);
+            acc = z4;
+            ++r;
+            rend = __shfl_sync(FULL, rpn, min(r, 31));
+          }
+          acc = add4(acc, x[q]);
+        }
+        e = min(e + U, limit);
+      }
+    }
+    return;
+  }
+  const int64_t sidx = (int64_t)idx * 8 + (threadIdx.x >> 5);
+  if (sidx >= g.nsegs) return;
+  const int64_t h = __ldg(g.seg_h + sidx);
+  const int64_t e0 = __ldg(g.seg_e0 + sidx);
+  const int64_t u = __ldg(g.heavy + h);
+  const int64_t rb = __ldg(g.rowptr + u), re = __ldg(g.rowptr + u + 1);
+  const int64_t e1 = min(e0 + (int64_t)g.heavy_seg, re);
+  const int64_t s0 = __ldg(g.seg_ptr + h), s1 = __ldg(g.seg_ptr + h + 1);
+  const int cnt = (int)(e1 - e0);  // <= 128
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) w[i] = (32 * i + lane < cnt) ? __ldg(col + e0 + 32 * i + lane) : 0u;
+  float4 acc = z4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (32 * i >= cnt) break;
+#pragma unroll
+    for (int j = 0; j < 32; j += U) {
+      if (32 * i + j >= cnt) break;
+      float4 x[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const uint32_t v = __shfl_sync(FULL, w[i], j + q);
+        x[q] = (32 * i + j + q < cnt) ? ld4(Xc + (uint64_t)v * ld) : z4;
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) acc = add4(acc, x[q]);
+    }
+  }
+  float *dst = g.segsum + ((int64_t)py * g.nsegs + sidx) * 128 + lane * 4;
+  __stcg(reinterpret_cast<float4 *>(dst), acc);
+  __syncwarp();
+  int32_t *cntp = g.hcnt + h * 4 + py;
+  int last = 0;
+  if (lane == 0) {
+    __threadfence();
+    last = atomicAdd(cntp, 1) == (int)(s1 - s0) - 1;
+    if (last) __threadfence();
+  }
+  last = __shfl_sync(FULL, last, 0);
+  if (!last) return;
+  const float *sp = g.segsum + ((int64_t)py * g.nsegs + s0) * 128 + lane * 4;
+  float4 tot = z4;
+  const int64_t ns = s1 - s0;
+  int64_t j = 0;
+  for (; j + 4 <= ns; j += 4) {
+    const float4 a0 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 0) * 128));
+    const float4 a1 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 1) * 128));
+    const float4 a2 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 2) * 128));
+    const float4 a3 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 3) * 128));
+    tot = add4(add4(add4(add4(tot, a0), a1), a2), a3);
+  }
+  for (; j < ns; ++j) tot = add4(tot, __ldcg(reinterpret_cast<const float4 *>(sp + j * 128)));
+  const float sr = rsc((int)(re - rb), g.a);
+  *reinterpret_cast<float4 *>(g.Y + u * ld + c) = make_float4(sr * tot.x, sr * tot.y, sr * tot.z, sr * tot.w);
+  if (lane == 0) *cntp = 0;
+}
+
+
+// ---------------------------------------------------------------- fold: 128-col pass + 16 tail columns (lanes 0..3)
+__device__ __forceinline__ void gsum2(const int32_t *col, int64_t e0, int64_t e1, const float *Xc, const float *Xe,
+                                      bool ex, uint32_t ld, float4 &acc, float4 &acc2) {
+  const int32_t *cp = col + e0;
+  int cnt = (int)(e1 - e0);
+  const float4 z = make_float4(0, 0, 0, 0);
+  for (; cnt >= 4; cnt -= 4, cp += 4) {
+    const uint32_t v0 = __ldg(cp), v1 = __ldg(cp + 1), v2 = __ldg(cp + 2), v3 = __ldg(cp + 3);
+    const float4 x0 = ld4(Xc + (uint64_t)v0 * ld), x1 = ld4(Xc + (uint64_t)v1 * ld);
+    const float4 x2 = ld4(Xc + (uint64_t)v2 * ld), x3 = ld4(Xc + (uint64_t)v3 * ld);
+    float4 y0 = z, y1 = z, y2 = z, y3 = z;
+    if (ex) {
+      y0 = ld4(Xe + (uint64_t)v0 * ld);
+      y1 = ld4(Xe + (uint64_t)v1 * ld);
+      y2 = ld4(Xe + (uint64_t)v2 * ld);
+      y3 = ld4(Xe + (uint64_t)v3 * ld);
+    }
+    acc = add4(add4(add4(x0, x1), add4(x2, x3)), acc);
+    acc2 = add4(add4(add4(y0, y1), add4(y2, y3)), acc2);
+  }
+  for (; cnt > 0; --cnt, ++cp) {
+    const uint32_t v = __ldg(cp);
+    acc = add4(ld4(Xc + (uint64_t)v * ld), acc);
+    if (ex) acc2 = add4(ld4(Xe + (uint64_t)v * ld), acc2);
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fold(G g, int nblk_heavy) {
+  const int py = blockIdx.y, bx = blockIdx.x;
+  const int32_t *col = g.col;
+  const uint32_t ld = g.ldx;
+  const int m = min(nblk_heavy, g.nblk_tile);
+  bool is_heavy;
+  int idx;
+  if (bx < 2 * m) {
+    is_heavy = (bx & 1) == 0;
+    idx = bx >> 1;
+  } else {
+    is_heavy = nblk_heavy > g.nblk_tile;
+    idx = m + (bx - 2 * m);
+  }
+  const int lane = threadIdx.x & 31;
+  const int c = py * 128 + lane * 4;
+  const int ce = g.fold + 16 * py + 4 * (lane & 3);
+  const bool ex = lane < 4 && ce < g.cols;
+  const float *Xc = g.X + c, *Xe = g.X + ce;
+  const float4 z = make_float4(0, 0, 0, 0);
+  if (!is_heavy) {
+    if (idx >= g.nblk_tile) return;
+    const int64_t ntiles = (g.n + 31) >> 5;
+    for (int64_t t = (int64_t)idx * 8 + (threadIdx.x >> 5); t < ntiles; t += (int64_t)g.nblk_tile * 8) {
+      const int64_t u0 = t << 5;
+      const int nrows = (int)min((int64_t)32, g.n - u0);
+      const int64_t rp = __ldg(g.rowptr + u0 + min(lane, nrows));
+      const int64_t rpn = __ldg(g.rowptr + u0 + min(lane + 1, nrows));
+      const int dl = (int)(rpn - rp);
+      const bool hv = dl > g.light_cap;
+      const unsigned hmask = __ballot_sync(0xffffffffu, hv);
+      uint32_t k0 = 0, k1 = 0, k2 = 0, k3 = 0;
+      if (!hv) {
+        if (dl > 0) k0 = __ldg(col + rp);
+        if (dl > 1) k1 = __ldg(col + rp + 1);
+        if (dl > 2) k2 = __ldg(col + rp + 2);
+        if (dl > 3) k3 = __ldg(col + rp + 3);
+      }
+      const float sl = rsc(dl, g.a);
+      const int64_t eb = __shfl_sync(0xffffffffu, rp, 0);
+      const int rel = (int)(rp - eb);
+#pragma unroll 1
+      for (int r = 0; r < 32; ++r) {
+        const int d = __shfl_sync(0xffffffffu, dl, r);
+        const int ro = __shfl_sync(0xffffffffu, rel, r);
+        const float sr = __shfl_sync(0xffffffffu, sl, r);
+        const uint32_t q0 = __shfl_sync(0xffffffffu, k0, r), q1 = __shfl_sync(0xffffffffu, k1, r);
+        const uint32_t q2 = __shfl_sync(0xffffffffu, k2, r), q3 = __shfl_sync(0xffffffffu, k3, r);
+        if (r >= nrows || ((hmask >> r) & 1u)) continue;
+        float4 acc = z, acc2 = z;
+        if (d > 0) {
+          acc = ld4(Xc + (uint64_t)q0 * ld);
+          if (ex) acc2 = ld4(Xe + (uint64_t)q0 * ld);
+          if (d > 1) {
+            float4 x1 = ld4(Xc + (uint64_t)q1 * ld), x2 = z, x3 = z, y1 = z, y2 = z, y3 = z;
+            if (ex) y1 = ld4(Xe + (uint64_t)q1 * ld);
+            if (d > 2) { x2 = ld4(Xc + (uint64_t)q2 * ld); if (ex) y2 = ld4(Xe + (uint64_t)q2 * ld); }
+            if (d > 3) { x3 = ld4(Xc + (uint64_t)q3 * ld); if (ex) y3 = ld4(Xe + (uint64_t)q3 * ld); }
+            acc = add4(add4(x1, acc), add4(x2, x3));
+            acc2 = add4(add4(y1, acc2), add4(y2, y3));
+            if (d > 4) gsum2(col, eb + ro + 4, eb + ro + d, Xc, Xe, ex, ld, acc, acc2);
+          }
+        }
+        float *yr = g.Y + (u0 + r) * ld;
+        *reinterpret_cast<float4 *>(yr + c) = make_float4(sr * acc.x, sr * acc.y, sr * acc.z, sr * acc.w);
+        if (ex) *reinterpret_cast<float4 *>(yr + ce) = make_float4(sr * acc2.x, sr * acc2.y, sr * acc2.z, sr * acc2.w);
+      }
+    }
+    return;
+  }
+  const int64_t sidx = (int64_t)idx * 8 + (threadIdx.x >> 5);
+  if (sidx >= g.nsegs) return;
+  const int64_t h = __ldg(g.seg_h + sidx);
+  const int64_t e0 = __ldg(g.seg_e0 + sidx);
+  const int64_t u = __ldg(g.heavy + h);
+  const int64_t rb = __ldg(g.rowptr + u), re = __ldg(g.rowptr + u + 1);
+  const int64_t e1 = min(e0 + (int64_t)g.heavy_seg, re);
+  const int64_t s0 = __ldg(g.seg_ptr + h), s1 = __ldg(g.seg_ptr + h + 1);
+  float4 acc = z, acc2 = z;
+  gsum2(col, e0, e1, Xc, Xe, ex, ld, acc, acc2);
+  // partial slot: 144 floats per segment (128 main + 16 folded)
+  float *dst = g.segsum + ((int64_t)py * g.nsegs + sidx) * 144;
+  __stcg(reinterpret_cast<float4 *>(dst + lane * 4), acc);
+  if (lane < 4) __stcg(reinterpret_cast<float4 *>(dst + 128 + lane * 4), acc2);
+  __syncwarp();
+  int32_t *cntp = g.hcnt + h * 4 + py;
+  int last = 0;
+  if (lane == 0) {
+    __threadfence();
+    last = atomicAdd(cntp, 1) == (int)(s1 - s0) - 1;
+    if (last) __threadfence();
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  const float *sp = g.segsum + ((int64_t)py * g.nsegs + s0) * 144;
+  float4 tot = z, tot2 = z;
+  const int64_t ns = s1 - s0;
+  for (int64_t j = 0; j < ns; ++j) {
+    tot = add4(tot, __ldcg(reinterpret_cast<const float4 *>(sp + j * 144 + lane * 4)));
+    if (lane < 4) tot2 = add4(tot2, __ldcg(reinterpret_cast<const float4 *>(sp + j * 144 + 128 + lane * 4)));
+  }
+  const float sr = rsc((int)(re - rb), g.a);
+  float *yr = g.Y + u * ld;
+  *reinterpret_cast<float4 *>(yr + c) = make_float4(sr * tot.x, sr * tot.y, sr * tot.z, sr * tot.w);
+  if (ex) *reinterpret_cast<float4 *>(yr + ce) = make_float4(sr * tot2.x, sr * tot2.y, sr * tot2.z, sr * tot2.w);
+  if (lane == 0) *cntp = 0;
+}
+
+
+// ---------------------------------------------------------------- async: cp.async ring per warp (no registers per gather in flight)
+template <bool CA>
+__device__ __forceinline__ void cpa16(uint32_t saddr, const float *g) {
+  if (CA)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g));
+  else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+
+// Stream the neighbour rows of edges [eb, ee) through the warp's S-slot ring;
+// rows of the tile (lane r: rpn = end of row r) are flushed at their ends.
+template <int S, bool CA, bool ROWS>
+__device__ __forceinline__ float4 ring_walk(const int32_t *__restrict__ col, int64_t eb, int64_t ee, const float *Xc,
+                                            uint32_t ld, uint32_t ring, int lane, int64_t rpn, float sl, float *Yrow0,
+                                            int nrows, uint32_t ldy, int c) {
+  const unsigned FULL = 0xffffffffu;
+  int64_t wb = eb;
+  uint32_t myidx = (wb + lane < ee) ? __ldg(col + wb + lane) : 0u;
+  int64_t ei = eb;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    if (ei < ee) {
+      if (ei >= wb + 32) {
+        wb += 32;
+        myidx = (wb + lane < ee) ? __ldg(col + wb + lane) : 0u;
+      }
+      const uint32_t v = __shfl_sync(FULL, myidx, (int)(ei - wb));
+      cpa16<CA>(ring + s * 512, Xc + (uint64_t)v * ld);
+    }
+    cpa_commit();
+    ++ei;
+  }
+  float4 acc = make_float4(0, 0, 0, 0);
+  int r = 0;
+  int64_t rend = ROWS ? __shfl_sync(FULL, rpn, 0) : ee;
+  int slot = 0;
+  for (int64_t ec = eb; ec < ee; ++ec) {
+    if (ROWS) {
+      while (ec >= rend) {
+        const float s = __shfl_sync(FULL, sl, r);
+        *reinterpret_cast<float4 *>(Yrow0 + (uint64_t)r * ldy + c) = make_float4(s * acc.x, s * acc.y, s * acc.z, s * acc.w);
+        acc = make_float4(0, 0, 0, 0);
+        ++r;
+        rend = __shfl_sync(FULL, rpn, r);
+      }
+    }
+    cpa_wait<S - 1>();
+    acc = add4(acc, lds4(ring + slot * 512));
+    if (ei < ee) {
+      if (ei >= wb + 32) {
+        wb += 32;
+        myidx = (wb + lane < ee) ? __ldg(col + wb + lane) : 0u;
+      }
+      const uint32_t v = __shfl_sync(FULL, myidx, (int)(ei - wb));
+      cpa16<CA>(ring + slot * 512, Xc + (uint64_t)v * ld);
+    }
+    cpa_commit();
+    ++ei;
+    slot = (slot + 1 == S) ? 0 : slot + 1;
+  }
+  if (ROWS) {
+    while (r < nrows) {
+      const float s = __shfl_sync(FULL, sl, r);
+      *reinterpret_cast<float4 *>(Yrow0 + (uint64_t)r * ldy + c) = make_float4(s * acc.x, s * acc.y, s * acc.z, s * acc.w);
+      acc = make_float4(0, 0, 0, 0);
+      ++r;
+    }
+  }
+  return acc;
+}
+
+// requires heavy rows to be the LAST rows (no heavy row inside a light tile) except tiles crossing n_light
+template <int S, int MINB, bool CA>
+__global__ void __launch_bounds__(256, MINB) k_async(G g, int nblk_heavy, int64_t n_light) {
+  extern __shared__ __align__(16) float sm_ring[];
+  const int py = blockIdx.y, bx = blockIdx.x;
+  const int32_t *col = g.col;
+  const uint32_t ld = g.ldx;
+  const int m = min(nblk_heavy, g.nblk_tile);
+  bool is_heavy;
+  int idx;
+  if (bx < 2 * m) {
+    is_heavy = (bx & 1) == 0;
+    idx = bx >> 1;
+  } else {
+    is_heavy = nblk_heavy > g.nblk_tile;
+    idx = m + (bx - 2 * m);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int c = py * 128 + lane * 4;
+  const float *Xc = g.X + c;
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sm_ring) + wid * (S * 512) + lane * 16;
+  if (!is_heavy) {
+    if (idx >= g.nblk_tile) return;
+    const int64_t ntiles = (n_light + 31) >> 5;
+    for (int64_t t = (int64_t)idx * 8 + wid; t < ntiles; t += (int64_t)g.nblk_tile * 8) {
+      const int64_t u0 = t << 5;
+      const int nrows = (int)min((int64_t)32, n_light - u0);
+      const int64_t rp = __ldg(g.rowptr + u0 + min(lane, nrows));
+      const int64_t rpn = __ldg(g.rowptr + u0 + min(lane + 1, nrows));
+      const int dl = (int)(rpn - rp);
+      const float sl = rsc(dl, g.a);
+      const int64_t eb = __shfl_sync(0xffffffffu, rp, 0), ee = __shfl_sync(0xffffffffu, rpn, nrows - 1);
+      ring_walk<S, CA, true>(col, eb, ee, Xc, ld, ring, lane, rpn, sl, g.Y + u0 * ld, nrows, ld, c);
+    }
+    return;
+  }
+  const int64_t sidx = (int64_t)idx * 8 + wid;
+  if (sidx >= g.nsegs) return;
+  const int64_t h = __ldg(g.seg_h + sidx);
+  const int64_t e0 = __ldg(g.seg_e0 + sidx);
+  const int64_t u = __ldg(g.heavy + h);
+  const int64_t rb = __ldg(g.rowptr + u), re = __ldg(g.rowptr + u + 1);
+  const int64_t e1 = min(e0 + (int64_t)g.heavy_seg, re);
+  const int64_t s0 = __ldg(g.seg_ptr + h), s1 = __ldg(g.seg_ptr + h + 1);
+  const float4 acc = ring_walk<S, CA, false>(col, e0, e1, Xc, ld, ring, lane, 0, 0.f, nullptr, 0, 0, c);
+  float *dst = g.segsum + ((int64_t)py * g.nsegs + sidx) * 128 + lane * 4;
+  __stcg(reinterpret_cast<float4 *>(dst), acc);
+  __syncwarp();
+  int32_t *cntp = g.hcnt + h * 4 + py;
+  int last = 0;
+  if (lane == 0) {
+    __threadfence();
+    last = atomicAdd(cntp, 1) == (int)(s1 - s0) - 1;
+    if (last) __threadfence();
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  const float *sp = g.segsum + ((int64_t)py * g.nsegs + s0) * 128 + lane * 4;
+  float4 tot = make_float4(0, 0, 0, 0);
+  const int64_t ns = s1 - s0;
+  int64_t j = 0;
+  for (; j + 4 <= ns; j += 4) {
+    const float4 a0 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 0) * 128));
+    const float4 a1 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 1) * 128));
+    const float4 a2 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 2) * 128));
+    const float4 a3 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 3) * 128));
+    tot = add4(add4(add4(add4(tot, a0), a1), a2), a3);
+  }
+  for (; j < ns; ++j) tot = add4(tot, __ldcg(reinterpret_cast<const float4 *>(sp + j * 128)));
+  const float sr = rsc((int)(re - rb), g.a);
+  *reinterpret_cast<float4 *>(g.Y + u * ld + c) = make_float4(sr * tot.x, sr * tot.y, sr * tot.z, sr * tot.w);
+  if (lane == 0) *cntp = 0;
+}
+
+__global__ void k_init(float *x, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    uint32_t h = (uint32_t)i * 2654435761u ^ (uint32_t)(i >> 32);
+    h ^= h >> 15;
+    h *= 2246822519u;
+    h ^= h >> 13;
+    x[i] = (float)(h & 0xffffff) / 16777216.f - 0.5f;
+  }
+}
+
+int main(int argc, char **argv) {
+  FILE *f = fopen(argv[1], "rb");
+  int64_t n, nnz;
+  if (fread(&n, 8, 1, f) != 1 || fread(&nnz, 8, 1, f) != 1) return 1;
+  std::vector<int64_t> rp(n + 1);
+  std::vector<int32_t> col(nnz);
+  if (fread(rp.data(), 8, n + 1, f) != (size_t)n + 1 || fread(col.data(), 4, nnz, f) != (size_t)nnz) return 1;
+  fclose(f);
+  const int light_cap = 64, heavy_seg = 128;
+  std::vector<int32_t> heavy;
+  std::vector<int64_t> seg_ptr{0}, seg_e0;
+  std::vector<int32_t> seg_h, deg(n);
+  for (int64_t u = 0; u < n; ++u) {
+    deg[u] = (int)(rp[u + 1] - rp[u]);
+    if (deg[u] > light_cap) {
+      heavy.push_back((int)u);
+      int ns = (deg[u] + heavy_seg - 1) / heavy_seg;
+      for (int s = 0; s < ns; ++s) {
+        seg_e0.push_back(rp[u] + (int64_t)s * heavy_seg);
+        seg_h.push_back((int)heavy.size() - 1);
+      }
+      seg_ptr.push_back((int64_t)seg_e0.size());
+    }
+  }
+  const int64_t nh = heavy.size(), nsegs = seg_e0.size();
+  printf("n=%lld nnz=%lld heavy=%lld segs=%lld\n", (long long)n, (long long)nnz, (long long)nh, (long long)nsegs);
+  int num_sms = 148;
+  CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, 0));
+  auto up = [](const void *h, size_t b) {
+    void *d;
+    CK(cudaMalloc(&d, b ? b : 4));
+    if (b) CK(cudaMemcpy(d, h, b, cudaMemcpyHostToDevice));
+    return d;
+  };
+  G g{};
+  g.rowptr = (int64_t *)up(rp.data(), rp.size() * 8);
+  g.col = (int32_t *)up(col.data(), col.size() * 4);
+  int32_t *colt;
+  CK(cudaMalloc(&colt, nnz * 4));
+  g.colt = colt;
+  g.n = n;
+  g.heavy = (int32_t *)up(heavy.data(), nh * 4);
+  g.seg_ptr = (int64_t *)up(seg_ptr.data(), seg_ptr.size() * 8);
+  g.seg_e0 = (int64_t *)up(seg_e0.data(), nsegs * 8);
+  g.seg_h = (int32_t *)up(seg_h.data(), nsegs * 4);
+  g.nsegs = nsegs;
+  CK(cudaMalloc(&g.hsum, nh * 288 * 4));
+  CK(cudaMemset(g.hsum, 0, nh * 288 * 4));
+  CK(cudaMalloc(&g.segsum, nsegs * 288 * 4));
+  CK(cudaMalloc(&g.hcnt, nh * 4 * 4));
+  CK(cudaMemset(g.hcnt, 0, nh * 4 * 4));
+  g.light_cap = light_cap;
+  g.heavy_seg = heavy_seg;
+  g.ldx = 288;
+  g.a = 0.45f;
+  float *X, *Y, *Yref;
+  CK(cudaMalloc(&X, n * 288 * 4));
+  CK(cudaMalloc(&Y, n * 288 * 4));
+  CK(cudaMalloc(&Yref, n * 288 * 4));
+  k_init<<<(n * 288 + 255) / 256, 256>>>(X, n * 288);
+  g.X = X;
+  char *flush;
+  CK(cudaMalloc(&flush, 512 << 20));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  std::vector<float> hy(n * 288), hr(n * 288);
+
+  std::vector<int> colds;
+  for (int i = 2; i < argc; ++i) colds.push_back(atoi(argv[i]));
+  if (colds.empty()) colds = {2, 4, 8};
+
+  auto run = [&](const char *name, auto kern, int lpr, int passes, int cols, bool ref, int reps = 10, int colbase = 0, int fold = 0, bool chk_from = false) {
+    G gg = g;
+    gg.Y = ref ? Yref : Y;
+    gg.cols = cols;
+    gg.colbase = colbase;
+    gg.fold = fold;
+    const int64_t ntiles = (n + 31) / 32;
+    gg.nblk_tile = (int)std::min<int64_t>((ntiles + 7) / 8, (int64_t)num_sms * 32);
+    const int nbh = (int)((nsegs + 256 / lpr - 1) / (256 / lpr));
+    dim3 grid(gg.nblk_tile + nbh, passes);
+    std::vector<float> ts;
+    for (int r = 0; r < reps; ++r) {
+      CK(cudaMemset(flush, r, 512 << 20));
+      cudaEventRecord(e0);
+      kern<<<grid, 256>>>(gg, nbh);
+      cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1));
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ts.push_back(ms);
+    }
+    CK(cudaGetLastError());
+    std::sort(ts.begin(), ts.end());
+    double err = 0, mx = 0;
+    if (!ref) {
+      CK(cudaMemcpy(hy.data(), Y, n * 288 * 4, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < n; ++i)
+        for (int c = 0; c < cols; ++c) { if (c < 256 && chk_from) continue;
+          err = std::max(err, (double)fabsf(hy[i * 288 + c] - hr[i * 288 + c]));
+          mx = std::max(mx, (double)fabsf(hr[i * 288 + c]));
+        }
+    }
+    const double gath = 4.0 * nnz * (cols - colbase) / (ts[reps / 2] * 1e-3) / 1e12;
+    const double alg = (8.0 * (n + 1) + 4.0 * nnz + 8.0 * n * (cols - colbase)) / (ts[reps / 2] * 1e-3) / 1e9;
+    printf("%-34s cols=%3d  med %.4f ms  min %.4f  gather %.2f TB/s  alg %.0f GB/s  err %.2e/%.2e\n", name, cols,
+           ts[reps / 2], ts[0], gath, alg, err, mx);
+    fflush(stdout);
+  };
+  // reference: 2 x 128 plain
+  run("ref (atomic, no hints) 2x128", k_lab<32, 0>, 32, 2, 256, true, 3);
+  run("ref tail 30 (LPR 8)", k_lab<8, 0>, 8, 1, 286, true, 3, 256);
+  CK(cudaMemcpy(hr.data(), Yref, n * 288 * 4, cudaMemcpyDeviceToHost));
+  run("tail 30 (LPR 8)", k_lab<8, 0>, 8, 1, 286, false, 10, 256, 0, true);
+  run("tail 30 (LPR 8) det", k_lab<8, H_DET>, 8, 1, 286, false, 10, 256, 0, true);
+
+  // ---- heavy-last relabelled copy: light rows first (original order), heavy rows last
+  {
+    std::vector<int32_t> nid(n);
+    int64_t nl = 0;
+    for (int64_t u = 0; u < n; ++u)
+      if (deg[u] <= light_cap) nid[u] = (int32_t)nl++;
+    int64_t q = nl;
+    for (int64_t u = 0; u < n; ++u)
+      if (deg[u] > light_cap) nid[u] = (int32_t)q++;
+    std::vector<int64_t> orow(n);
+    for (int64_t u = 0; u < n; ++u) orow[nid[u]] = u;
+    std::vector<int64_t> rp2(n + 1, 0);
+    std::vector<int32_t> col2(nnz);
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t u = orow[i];
+      rp2[i + 1] = rp2[i] + deg[u];
+      for (int64_t e = rp[u]; e < rp[u + 1]; ++e) col2[rp2[i] + (e - rp[u])] = nid[col[e]];
+      std::sort(col2.begin() + rp2[i], col2.begin() + rp2[i + 1]);
+    }
+    std::vector<int32_t> heavy2;
+    std::vector<int64_t> seg_ptr2{0}, seg_e02;
+    std::vector<int32_t> seg_h2;
+    for (int64_t i = nl; i < n; ++i) {
+      heavy2.push_back((int)i);
+      const int d = (int)(rp2[i + 1] - rp2[i]);
+      const int ns = (d + heavy_seg - 1) / heavy_seg;
+      for (int s2 = 0; s2 < ns; ++s2) {
+        seg_e02.push_back(rp2[i] + (int64_t)s2 * heavy_seg);
+        seg_h2.push_back((int)heavy2.size() - 1);
+      }
+      seg_ptr2.push_back((int64_t)seg_e02.size());
+    }
+    G g2 = g;
+    g2.rowptr = (int64_t *)up(rp2.data(), rp2.size() * 8);
+    g2.col = (int32_t *)up(col2.data(), col2.size() * 4);
+    g2.heavy = (int32_t *)up(heavy2.data(), heavy2.size() * 4);
+    g2.seg_ptr = (int64_t *)up(seg_ptr2.data(), seg_ptr2.size() * 8);
+    g2.seg_e0 = (int64_t *)up(seg_e02.data(), seg_e02.size() * 8);
+    g2.seg_h = (int32_t *)up(seg_h2.data(), seg_h2.size() * 4);
+    // X2[nid[v]] = X[v]
+    std::vector<float> hx(n * 288), hx2(n * 288);
+    CK(cudaMemcpy(hx.data(), X, n * 288 * 4, cudaMemcpyDeviceToHost));
+    for (int64_t v = 0; v < n; ++v) std::copy(hx.begin() + v * 288, hx.begin() + v * 288 + 288, hx2.begin() + (int64_t)nid[v] * 288);
+    float *X2;
+    CK(cudaMalloc(&X2, n * 288 * 4));
+    CK(cudaMemcpy(X2, hx2.data(), n * 288 * 4, cudaMemcpyHostToDevice));
+    g2.X = X2;
+    auto run2 = [&](const char *name, auto kern, int smem, bool async, int reps = 10) {
+      G gg = g2;
+      gg.Y = Y;
+      gg.cols = 256;
+      gg.colbase = 0;
+      const int64_t ntl = async ? (nl + 31) / 32 : (n + 31) / 32;
+      gg.nblk_tile = (int)std::min<int64_t>((ntl + 7) / 8, (int64_t)num_sms * 32);
+      const int nbh = (int)((nsegs + 7) / 8);
+      dim3 grid(gg.nblk_tile + nbh, 2);
+      if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      std::vector<float> ts;
+      for (int r = 0; r < reps; ++r) {
+        CK(cudaMemset(flush, r, 512 << 20));
+        cudaEventRecord(e0);
+        if (async)
+          ((void (*)(G, int, int64_t))kern)<<<grid, 256, smem>>>(gg, nbh, nl);
+        else
+          ((void (*)(G, int))kern)<<<grid, 256, smem>>>(gg, nbh);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ts.push_back(ms);
+      }
+      CK(cudaGetLastError());
+      std::sort(ts.begin(), ts.end());
+      CK(cudaMemcpy(hy.data(), Y, n * 288 * 4, cudaMemcpyDeviceToHost));
+      double err = 0, mx = 0;
+      for (int64_t u = 0; u < n; ++u)
+        for (int c = 0; c < 256; ++c) {
+          err = std::max(err, (double)fabsf(hy[(int64_t)nid[u] * 288 + c] - hr[u * 288 + c]));
+          mx = std::max(mx, (double)fabsf(hr[u * 288 + c]));
+        }
+      const double gath = 4.0 * nnz * 256 / (ts[reps / 2] * 1e-3) / 1e12;
+      const double alg = (8.0 * (n + 1) + 4.0 * nnz + 8.0 * n * 256) / (ts[reps / 2] * 1e-3) / 1e9;
+      printf("%-34s cols=256  med %.4f ms  min %.4f  gather %.2f TB/s  alg %.0f GB/s  err %.2e/%.2e\n", name, ts[reps / 2],
+             ts[0], gath, alg, err, mx);
+      fflush(stdout);
+    };
+    printf("-- heavy-last relabel: %lld light rows\n", (long long)nl);
+    run2("relabel plain 2x128", k_lab<32, 0>, 0, false);
+    run2("relabel det 2x128", k_lab<32, H_DET>, 0, false);
+    run2("async S4 minb8 cg", k_async<4, 8, false>, 8 * 4 * 512, true);
+    run2("async S8 minb6 cg", k_async<8, 6, false>, 8 * 8 * 512, true);
+    run2("async S8 minb6 ca", k_async<8, 6, true>, 8 * 8 * 512, true);
+    run2("async S8 minb4 cg", k_async<8, 4, false>, 8 * 8 * 512, true);
+    run2("async S16 minb3 cg", k_async<16, 3, false>, 8 * 16 * 512, true);
+    run2("async S16 minb3 ca", k_async<16, 3, true>, 8 * 16 * 512, true);
+    run2("async S32 minb1 cg", k_async<32, 1, false>, 8 * 32 * 512, true);
+    run2("async S12 minb4 cg", k_async<12, 4, false>, 8 * 12 * 512, true);
+  }
+  run("plain 2x128", k_lab<32, 0>, 32, 2, 256, false);
+  run("det 2x128", k_lab<32, H_DET>, 32, 2, 256, false);
+  run("det+col 2x128", k_lab<32, H_DET | H_COL>, 32, 2, 256, false);
+  run("det+col+Y 2x128", k_lab<32, H_DET | H_COL | H_Y>, 32, 2, 256, false);
+  run("v2 U4 minb8", k_v2<4, 8>, 32, 2, 256, false);
+  run("v2 U4 minb6", k_v2<4, 6>, 32, 2, 256, false);
+  run("v2 U8 minb6", k_v2<8, 6>, 32, 2, 256, false);
+  run("v2 U8 minb5", k_v2<8, 5>, 32, 2, 256, false);
+  run("v2 U8 minb4", k_v2<8, 4>, 32, 2, 256, false);
+  run("v2 U16 minb4", k_v2<16, 4>, 32, 2, 256, false);
+  run("v2 U16 minb3", k_v2<16, 3>, 32, 2, 256, false);
+  run("plain 2x128 minb6", k_lab<32, 0, 6>, 32, 2, 256, false);
+  run("det+col+Y 2x128 minb6", k_lab<32, H_DET | H_COL | H_Y, 6>, 32, 2, 256, false);
+  run("plain 4x64", k_lab<16, 0>, 16, 4, 256, false);
+  run("det+col+Y 4x64", k_lab<16, H_DET | H_COL | H_Y>, 16, 4, 256, false);
+  for (int cd : colds) {
+    std::vector<int32_t> ct(nnz);
+    int64_t ncold = 0;
+    for (int64_t i = 0; i < nnz; ++i) {
+      bool cold = deg[col[i]] <= cd;
+      ncold += cold;
+      ct[i] = col[i] | (cold ? (int32_t)0x80000000u : 0);
+    }
+    CK(cudaMemcpy(colt, ct.data(), nnz * 4, cudaMemcpyHostToDevice));
+    char nm[64];
+    printf("-- cold = deg <= %d: %.3f of references\n", cd, (double)ncold / nnz);
+    snprintf(nm, sizeof nm, "all hints 2x128 (cold<=%d)", cd);
+    run(nm, k_lab<32, H_DET | H_COL | H_Y | H_X>, 32, 2, 256, false);
+    snprintf(nm, sizeof nm, "all hints 4x64 (cold<=%d)", cd);
+    run(nm, k_lab<16, H_DET | H_COL | H_Y | H_X>, 16, 4, 256, false);
+    snprintf(nm, sizeof nm, "all hints 2x128 minb6 (cold<=%d)", cd);
+    run(nm, k_lab<32, H_DET | H_COL | H_Y | H_X, 6>, 32, 2, 256, false);
+    snprintf(nm, sizeof nm, "X hints only 2x128 (cold<=%d)", cd);
+    run(nm, k_lab<32, H_DET | H_X>, 32, 2, 256, false);
+  }
+  printf("done\n");
+  return 0;
+}

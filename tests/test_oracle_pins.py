@@ -163,6 +163,28 @@ def test_eig_svd_vs_textbook_svd(seed):
     assert np.linalg.norm(Q @ Q.T - Qr @ Qr.T) < 1e-8
 
 
+@pytest.mark.parametrize("seed", range(3))
+def test_orth_range_rank_deficient(seed):
+    """Alg. 4 step 4 orth(Y) [R10]: full rank -> exactly eigSVD's Q; with
+    exactly-zero and repeated columns -> rank(Y) orthonormal columns whose
+    projector equals the textbook one (numpy SVD of Y, left vectors of the
+    nonzero singular values)."""
+    rng = np.random.default_rng(seed)
+    Y = rng.standard_normal((300, 20))
+    assert np.array_equal(O.orth_range(Y), O.eig_svd(Y)[0])
+    Y[:, [3, 11]] = 0.0                     # a Psi column drawing only isolated rows
+    Y[:, 7] = 2.0 * Y[:, 5]                 # a dependent column
+    Q = O.orth_range(Y)
+    assert Q.shape[1] == 17
+    assert np.abs(Q.T @ Q - np.eye(17)).max() < 1e-10
+    U, s, _ = np.linalg.svd(Y, full_matrices=False)
+    Ur = U[:, s > 1e-8 * s[0]]
+    assert Ur.shape[1] == 17
+    assert np.linalg.norm(Q @ Q.T - Ur @ Ur.T) < 1e-8
+    with pytest.raises(np.linalg.LinAlgError):
+        O.eig_svd(Y)                        # eigSVD itself needs full column rank (PAPER.md:215)
+
+
 # ---------------------------------------------------------------- freigs
 def _op(rp, col, deg, a):
     return lambda X: O.normalized_spmm(rp, col, deg, X, a)
