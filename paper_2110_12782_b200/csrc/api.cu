@@ -1,6 +1,7 @@
 // api.cu — the C ABI of include/netmfp.h: argument checking, host/device
 // marshalling, error codes.  All compute is in the other translation units.
 #include <algorithm>
+#include <exception>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -89,6 +90,47 @@ static void check_mem(int mem) {
   NM_REQUIRE(mem == NETMFP_MEM_DEVICE || mem == NETMFP_MEM_HOST, "mem must be NETMFP_MEM_DEVICE or _HOST");
 }
 
+// Every entry point runs on its context's device (the caller's current
+// device is restored on return).  If the call throws, pending deferred numeric
+// checks and the device status flags are dropped so that the next call does
+// not report this call's failure.
+struct DevScope {
+  Ctx &c;
+  int prev = -1;
+  int unwinding0;
+  explicit DevScope(Ctx &cc) : c(cc), unwinding0(std::uncaught_exceptions()) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != c.device) NM_CUDA(cudaSetDevice(c.device));
+  }
+  ~DevScope() {
+    if (std::uncaught_exceptions() > unwinding0) {
+      cudaStreamSynchronize(c.stream);
+      cudaGetLastError();
+      c.flag_checks.clear();
+      if (c.d_flags) cudaMemsetAsync(c.d_flags, 0, 16, c.stream);
+      cudaStreamSynchronize(c.stream);
+      c.pending.clear();
+    }
+    if (prev >= 0 && prev != c.device) cudaSetDevice(prev);
+  }
+  DevScope(const DevScope &) = delete;
+  DevScope &operator=(const DevScope &) = delete;
+};
+
+// All netmfp_params fields, checked before any work is queued (Alg. 5's
+// inputs; the stages re-check what they use).
+static void check_params(const netmfp_params &p, int64_t n) {
+  NM_REQUIRE(p.alpha > 0.0 && p.alpha <= 0.5, "params: alpha in (0, 0.5] (PAPER.md:217)");
+  NM_REQUIRE(p.k >= 1 && p.s1 >= 0 && p.q >= 0, "params: need k >= 1, s1 >= 0, q >= 0");
+  NM_REQUIRE((int64_t)p.k + p.s1 <= n, "params: k + s1 must not exceed n (Alg. 2)");
+  NM_REQUIRE(p.T >= 1 && p.b > 0.0, "params: need T >= 1, b > 0 (Eq. 1)");
+  NM_REQUIRE(p.d >= 1 && p.s2 >= 0 && p.s3 >= p.s2, "params: need d >= 1, 0 <= s2 <= s3 (PAPER.md:413)");
+  NM_REQUIRE((int64_t)p.d + p.s2 <= n, "params: d + s2 must not exceed n (Alg. 4)");
+  NM_REQUIRE(p.z >= 2 && p.z <= 64 && p.z <= n, "params: need 2 <= z <= min(n, 64) (Alg. 3)");
+  NM_REQUIRE(p.prop_order >= 0 && p.prop_order <= 64, "params: prop_order in [0, 64]");
+  NM_REQUIRE(p.logmode == NETMFP_LOG_TRUNC || p.logmode == NETMFP_LOG_LOG1P, "params: bad logmode");
+}
+
 static void finish(Ctx &c) {
   int h = 0;
   if (!c.flag_checks.empty())
@@ -162,8 +204,12 @@ int netmfp_ctx_create(int device, void *stream, netmfp_ctx **out) {
 int netmfp_ctx_destroy(netmfp_ctx *ctx) {
   return guarded([&] {
     if (!ctx) return;
+    cudaSetDevice(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.d_flags) cudaFree(ctx->c.d_flags);
+    ctx->c.spmm_part.release();  // stream-ordered frees before the stream goes
+    ctx->c.spmm_cnt.release();
+    cudaStreamSynchronize(ctx->c.stream);
     try {
       dist_destroy(ctx->c);
     } catch (...) {
@@ -187,6 +233,7 @@ int netmfp_ctx_profile(netmfp_ctx *ctx, int enable, const char *filter) {
 int netmfp_ctx_profile_read(netmfp_ctx *ctx, char *buf, size_t len) {
   return guarded([&] {
     NM_REQUIRE(ctx && buf && len > 0, "ctx_profile_read: bad arguments");
+    DevScope _dev(ctx->c);
     NM_CUDA(cudaStreamSynchronize(ctx->c.stream));
     prof_collect(ctx->c);
     std::string out;
@@ -205,6 +252,7 @@ int netmfp_build_csr(netmfp_ctx *ctx, int64_t n, const int32_t *src, const int32
     check_mem(mem);
     NM_REQUIRE(m_in == 0 || (src && dst), "build_csr: NULL edge arrays");
     Ctx &c = ctx->c;
+    DevScope _dev(c);
     InVec<int32_t> s(c, src, m_in, mem, true), t(c, dst, m_in, mem, true);
     Graph *g = build_csr_device(c, n, s.p, t.p, m_in);
     finish(c);
@@ -222,6 +270,7 @@ int netmfp_dist_unique_id(void *id) {
 int netmfp_dist_init(netmfp_ctx *ctx, const void *id, int32_t nranks, int32_t rank) {
   return guarded([&] {
     NM_REQUIRE(ctx && (id || nranks == 1), "dist_init: NULL argument");
+    DevScope _dev(ctx->c);
     dist_init(ctx->c, id, nranks, rank);
   });
 }
@@ -233,6 +282,7 @@ int netmfp_dist_build_csr(netmfp_ctx *ctx, int64_t n, const int32_t *src, const 
     check_mem(mem);
     NM_REQUIRE(m_in == 0 || (src && dst), "dist_build_csr: NULL edge arrays");
     Ctx &c = ctx->c;
+    DevScope _dev(c);
     std::vector<int64_t> b(c.nranks + 1);
     for (int r = 0; r <= c.nranks; ++r) b[r] = bounds ? bounds[r] : n * r / c.nranks;
     NM_REQUIRE(b[0] == 0 && b[c.nranks] == n, "dist_build_csr: bounds must start at 0 and end at n");
@@ -257,6 +307,7 @@ int netmfp_build_csr_rows(netmfp_ctx *ctx, int64_t n, const int32_t *src, const 
     check_mem(mem);
     NM_REQUIRE(m_in == 0 || (src && dst), "build_csr_rows: NULL edge arrays");
     Ctx &c = ctx->c;
+    DevScope _dev(c);
     InVec<int32_t> s(c, src, m_in, mem, true), t(c, dst, m_in, mem, true);
     Graph *g = build_csr_device(c, n, s.p, t.p, m_in, row0, row1);
     finish(c);
@@ -288,6 +339,7 @@ int netmfp_graph_export(netmfp_ctx *ctx, const netmfp_graph *gr, int64_t *rowptr
     NM_REQUIRE(ctx && gr, "graph_export: NULL");
     check_mem(mem);
     Ctx &c = ctx->c;
+    DevScope _dev(c);
     const Graph &g = *gr->g;
     auto kind = mem == NETMFP_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     if (rowptr) NM_CUDA(cudaMemcpyAsync(rowptr, g.rowptr.p, (g.n + 1) * 8, kind, c.stream));
@@ -303,9 +355,13 @@ int netmfp_graph_free(netmfp_graph *g) {
     // free on the legacy default stream: the creating context (and its
     // stream) may already be gone
     Graph *gg = g->g;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(gg->device);
     gg->detach_streams();
     delete gg;
     delete g;
+    if (prev >= 0) cudaSetDevice(prev);
   });
 }
 
@@ -332,6 +388,7 @@ int netmfp_spmm(netmfp_ctx *ctx, const netmfp_graph *gr, double a, double b, con
     NM_REQUIRE(ctx && gr && X && Y, "spmm: NULL argument");
     check_mem(mem);
     Ctx &c = ctx->c;
+    DevScope _dev(c);
     const Graph &g = *gr->g;
     // X: all n_global rows (the columns of A); Y: this graph's rows
     InMat xi(c, X, g.n_global, cols, ldx, mem, true), yo(c, Y, g.n, cols, ldy, mem, false);
@@ -356,6 +413,7 @@ int netmfp_gram(netmfp_ctx *ctx, int64_t n, const float *A, int64_t lda, int64_t
     NM_REQUIRE(ctx && A && B && G, "gram: NULL argument");
     check_mem(mem);
     Ctx &c = ctx->c;
+    DevScope _dev(c);
     InMat ai(c, A, n, a, lda, mem, true);
     std::unique_ptr<InMat> bi;
     Mat bm = ai.m;
@@ -376,6 +434,7 @@ int netmfp_orthonormalize(netmfp_ctx *ctx, int64_t n, int64_t cc, const float *Y
     NM_REQUIRE(ctx && Y && Q && passes >= 1 && passes <= 3 && n >= cc, "orthonormalize: bad arguments");
     check_mem(mem);
     Ctx &c = ctx->c;
+    DevScope _dev(c);
     InMat yi(c, Y, n, cc, ldy, mem, true), qo(c, Q, n, cc, ldq, mem, false);
     Block tmp(n, cc, c.stream);
     cholqr(c, yi.m, qo.m, nullptr, 0.f, passes, &tmp.m);
@@ -397,6 +456,7 @@ int netmfp_sym_eig(netmfp_ctx *ctx, const double *S, int64_t l, double *lam, dou
     NM_REQUIRE(ctx && S && lam && V && l >= 1, "sym_eig: bad arguments");
     check_mem(mem);
     Ctx &c = ctx->c;
+    DevScope _dev(c);
     InVec<double> si(c, S, l * l, mem, true), lo(c, lam, l, mem, false), vo(c, V, l * l, mem, false);
     DBuf<double> work(l * l, c.stream);  // sym_eig overwrites its input
     NM_CUDA(cudaMemcpyAsync(work.p, si.p, l * l * 8, cudaMemcpyDeviceToDevice, c.stream));
@@ -413,6 +473,7 @@ int netmfp_eig(netmfp_ctx *ctx, const netmfp_graph *gr, double alpha, int32_t k,
     NM_REQUIRE(ctx && gr && U && lambda, "eig: NULL argument");
     check_mem(mem);
     Ctx &c = ctx->c;
+    DevScope _dev(c);
     const Graph &g = *gr->g;
     InMat uo(c, U, g.n, k, ldu, mem, false);
     InVec<double> lo(c, lambda, k, mem, false);
@@ -430,6 +491,7 @@ int netmfp_factor_pair(netmfp_ctx *ctx, const netmfp_graph *gr, double alpha, in
     NM_REQUIRE(ctx && gr && U && lambda && F && C, "factor_pair: NULL argument");
     check_mem(mem);
     Ctx &c = ctx->c;
+    DevScope _dev(c);
     const Graph &g = *gr->g;
     InMat ui(c, U, g.n, k, ldu, mem, true), fo(c, F, g.n, k, ldf, mem, false);
     InVec<double> li(c, lambda, k, mem, true), co(c, C, (int64_t)k * k, mem, false);
@@ -449,6 +511,7 @@ int netmfp_sketch_svd(netmfp_ctx *ctx, int64_t n, const float *F, int64_t ldf, c
     NM_REQUIRE(logmode == NETMFP_LOG_TRUNC || logmode == NETMFP_LOG_LOG1P, "sketch_svd: bad logmode");
     check_mem(mem);
     Ctx &c = ctx->c;
+    DevScope _dev(c);
     InMat fi(c, F, n, k, ldf, mem, true);
     InVec<double> ci(c, C, (int64_t)k * k, mem, true);
     const int64_t h2 = (int64_t)d + s2, h3 = (int64_t)d + s3;
@@ -481,6 +544,7 @@ int netmfp_propagate(netmfp_ctx *ctx, const netmfp_graph *gr, float *E, int64_t 
     NM_REQUIRE(ctx && gr && E, "propagate: NULL argument");
     check_mem(mem);
     Ctx &c = ctx->c;
+    DevScope _dev(c);
     const Graph &g = *gr->g;
     InMat ei(c, E, g.n, d, lde, mem, true);
     propagate(c, g, ei.m, order, mu, theta);
@@ -609,7 +673,9 @@ int netmfp_embed(netmfp_ctx *ctx, const netmfp_graph *gr, const netmfp_params *p
     NM_REQUIRE(ctx && gr && p && E, "embed: NULL argument");
     check_mem(mem);
     Ctx &c = ctx->c;
+    DevScope _dev(c);
     const Graph &g = *gr->g;
+    check_params(*p, g.n_global);
     NM_REQUIRE(lde >= p->d, "embed: lde < d");
     InVec<double> so(c, sigma, p->d, mem, false), lo(c, lambda, p->k, mem, false);
     if (!(mem == NETMFP_MEM_HOST && embed_host_pinned(c, g, *p, E, lde, so.p, lo.p))) {
@@ -629,6 +695,8 @@ int netmfp_embed_edges(netmfp_ctx *ctx, int64_t n, const int32_t *src, const int
     NM_REQUIRE(ctx && p && E, "embed_edges: NULL argument");
     check_mem(mem);
     Ctx &c = ctx->c;
+    DevScope _dev(c);
+    check_params(*p, n);
     InVec<int32_t> s(c, src, m_in, mem, true), t(c, dst, m_in, mem, true);
     std::unique_ptr<Graph> g;
     {

@@ -150,8 +150,9 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
     DBuf<uint8_t> hflag(n, s);
     NM_LAUNCH(c, "rowptr", k_rowptr<<<ceil_div(n + 1, 256), 256, 0, s>>>(keys, nnz, n, row0, cb, g->rowptr));
     int64_t mx = std::max(nnz, n);
-    NM_LAUNCH(c, "col_deg", k_col_deg<<<ceil_div(mx, 256), 256, 0, s>>>(keys, nnz, g->rowptr, n, cb, g->col, g->deg, hflag,
-                                                                             g->light_cap));
+    if (mx > 0)  // an empty row range (a rank with no rows) has nothing to fill
+      NM_LAUNCH(c, "col_deg", k_col_deg<<<ceil_div(mx, 256), 256, 0, s>>>(keys, nnz, g->rowptr, n, cb, g->col, g->deg,
+                                                                               hflag, g->light_cap));
     // heavy rows (degree > kLightCap) for the split SpMM path
     {
       DBuf<int32_t> hv(n, s);

@@ -287,9 +287,14 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
       if (threadIdx.x < 32) {
         for (int cc = 0; cc < 32; ++cc)
           if ((int)threadIdx.x >= ib) S[threadIdx.x * TL + cc] = (cc == (int)threadIdx.x) ? 1.0 : 0.0;
-        piv[threadIdx.x] = (int)threadIdx.x < ib
-                               ? __ldcg(p.G + (int64_t)(32 * I + threadIdx.x) * p.ld + 32 * I + threadIdx.x) + shift
-                               : 1.0;
+        const double g0 = (int)threadIdx.x < ib
+                              ? __ldcg(p.G + (int64_t)(32 * I + threadIdx.x) * p.ld + 32 * I + threadIdx.x)
+                              : 1.0;
+        // an exactly-zero column of the Gram's input (zero row and column of
+        // G, so of S): identity pivot — that column of Y R⁻¹ stays zero and
+        // the others are untouched, i.e. orth on range(Y) [R10]
+        if ((int)threadIdx.x < ib && g0 == 0.0) S[threadIdx.x * TL + threadIdx.x] = 1.0;
+        piv[threadIdx.x] = (int)threadIdx.x < ib ? (g0 == 0.0 ? 1.0 : g0 + shift) : 1.0;
         if (threadIdx.x == 0) prog = 0;
       }
       __syncthreads();

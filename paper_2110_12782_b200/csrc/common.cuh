@@ -6,9 +6,12 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <memory>
+#include <tuple>
 #include <vector>
 
 #include "../../include/netmfp.h"
@@ -41,6 +44,63 @@ void set_last_error(const std::string &msg);
     if (!(cond)) throw ::netmfp::Error(NETMFP_ERR_ARG, (msg));       \
   } while (0)
 
+// stream-ordered device buffer (cudaMallocAsync pool; freed on scope exit)
+template <class T>
+struct DBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count) NM_CUDA(cudaMallocAsync((void **)&p, count * sizeof(T), st));
+  }
+  void zero() {
+    if (n) NM_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  T *get() const { return p; }
+  operator T *() const { return p; }
+  DBuf(const DBuf &) = delete;
+  DBuf &operator=(const DBuf &) = delete;
+  DBuf(DBuf &&o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf &operator=(DBuf &&o) noexcept {
+    release();
+    p = o.p; n = o.n; s = o.s;
+    o.p = nullptr; o.n = 0;
+    return *this;
+  }
+  ~DBuf() { release(); }
+};
+
+// Kernel attributes are per (kernel, device): set an attribute on the current
+// device unless this value (or, for the dynamic shared memory limit, a larger
+// one) is already set there.  Thread-safe; replaces per-process static guards.
+inline void func_attr(const void *kern, cudaFuncAttribute a, int v) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void *, int, int>, int> done;
+  int dev = 0;
+  NM_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_tuple(kern, dev, (int)a);
+  auto it = done.find(key);
+  if (it != done.end() && (it->second == v || (a == cudaFuncAttributeMaxDynamicSharedMemorySize && it->second >= v)))
+    return;
+  NM_CUDA(cudaFuncSetAttribute(kern, a, v));
+  done[key] = v;
+}
+template <class K>
+inline void smem_attr(K kern, size_t bytes) {
+  func_attr(reinterpret_cast<const void *>(kern), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 // ----------------------------------------------------------------------------
 // context
 // ----------------------------------------------------------------------------
@@ -71,6 +131,11 @@ struct Ctx {
   // numeric checks deferred to the end of the ABI call (one synchronisation):
   // the stage whose Cholesky failure bit (d_flags & 1<<30) is reported
   std::vector<const char *> flag_checks;
+  // SpMM heavy-row scratch owned by the context (one stream: launches on it
+  // are ordered): per (column pass, heavy segment) partial sums, and per
+  // (heavy row, column pass) arrival counters that every launch leaves zero
+  DBuf<float> spmm_part;
+  DBuf<int32_t> spmm_cnt;
 };
 
 inline bool prof_match(const Ctx &c, const char *name) {
@@ -205,42 +270,6 @@ struct StageScope {
     ::netmfp::launched(c, name);  \
   } while (0)
 
-// stream-ordered device buffer (cudaMallocAsync pool; freed on scope exit)
-template <class T>
-struct DBuf {
-  T *p = nullptr;
-  size_t n = 0;
-  cudaStream_t s = nullptr;
-  DBuf() = default;
-  DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
-  void alloc(size_t count, cudaStream_t st) {
-    release();
-    s = st;
-    n = count;
-    if (count) NM_CUDA(cudaMallocAsync((void **)&p, count * sizeof(T), st));
-  }
-  void zero() {
-    if (n) NM_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
-  }
-  void release() {
-    if (p) cudaFreeAsync(p, s);
-    p = nullptr;
-    n = 0;
-  }
-  T *get() const { return p; }
-  operator T *() const { return p; }
-  DBuf(const DBuf &) = delete;
-  DBuf &operator=(const DBuf &) = delete;
-  DBuf(DBuf &&o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
-  DBuf &operator=(DBuf &&o) noexcept {
-    release();
-    p = o.p; n = o.n; s = o.s;
-    o.p = nullptr; o.n = 0;
-    return *this;
-  }
-  ~DBuf() { release(); }
-};
-
 // Dense fp32 block view: rows × cols, row-major, leading dimension ld.
 struct Mat {
   float *p = nullptr;
@@ -297,10 +326,6 @@ struct Graph {
   int light_cap = kLightCapDefault, heavy_seg = kHeavySegDefault;
   DBuf<int64_t> seg_e0;  // per heavy segment: first entry
   DBuf<int32_t> seg_h;   // per heavy segment: index into heavy
-  // fused SpMM scratch, left all-zero by every launch: per heavy row partial
-  // sums (n_heavy x ld) and per (heavy row, column chunk) arrival counters
-  mutable DBuf<float> hsum_ws;
-  mutable DBuf<int32_t> hcnt_ws;
   int device = 0;
   // isolated-vertex compaction (embed): for a compacted graph, the original
   // vertex count, compact -> original ids and original -> compact (-1 for
@@ -312,8 +337,7 @@ struct Graph {
   void detach_streams() {  // free on the legacy stream (owning stream may be gone)
     rowptr.s = col.s = deg.s = heavy.s = nullptr;
     heavy_seg_ptr.s = seg_e0.s = nullptr;
-    seg_h.s = hcnt_ws.s = orig_id.s = comp_id.s = nullptr;
-    hsum_ws.s = nullptr;
+    seg_h.s = orig_id.s = comp_id.s = nullptr;
     if (compact) compact->detach_streams();
   }
 };

@@ -107,21 +107,22 @@ __global__ void k_gram_reduce(const float *__restrict__ part, int nslab, int64_t
   G[i * ldg + j] = s;
 }
 
-bool tc_enabled() {
-  static int on = [] {
-    const char *v = getenv("NETMFP_TC");
-    return v ? atoi(v) : 1;
-  }();
-  return on != 0;
-}
+// Blocks of >= 128 rows (one tensor-core M tile) take the tcgen05 kernels of
+// tc_gemm.cu, whatever their width; only blocks with fewer rows than one M
+// tile (tiny graphs) use the CUDA-core kernels below.  There is no switch.
+constexpr int64_t kTcMinRows = 128;
 
 void gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg, bool exact) {
   NM_REQUIRE(A.rows == B.rows, "gram: row mismatch");
-  if (tc_enabled() && A.rows >= 128) {
+  if (A.rows >= kTcMinRows) {
     tc_gram(c, A, B, deg, wexp, G, ldg, exact);
     return;
   }
   const int64_t n = A.rows;
+  if (n == 0 || A.cols == 0 || B.cols == 0) {
+    if (A.cols > 0 && B.cols > 0) NM_CUDA(cudaMemset2DAsync(G, ldg * 8, 0, B.cols * 8, A.cols, c.stream));
+    return;
+  }
   const bool sym = (A.p == B.p && A.cols == B.cols && A.ld == B.ld);
   const int ta = (int)ceil_div(A.cols, GT), tb = (int)ceil_div(B.cols, GT);
   const int tiles = sym ? ta * (ta + 1) / 2 : ta * tb;
@@ -218,17 +219,18 @@ void gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcol
                float rexp, const Mat &C) {
   NM_REQUIRE(A.rows == C.rows && C.cols == bcols, "gemm_tall: shape mismatch");
   NM_REQUIRE(C.p != A.p, "gemm_tall: in-place not supported");
-  if (tc_enabled() && A.rows >= 128) {
+  if (A.rows >= kTcMinRows) {
     tc_gemm_tall(c, A, Bs, ldb, bcols, deg, rexp, C);
     return;
   }
+  if (A.rows == 0) return;
   dim3 grid(ceil_div(A.rows, TM), ceil_div(bcols, TN));
   NM_LAUNCH(c, "gemm_tall", k_gemm_tall<<<grid, 256, 0, c.stream>>>(A, Bs, ldb, bcols, deg, rexp, C));
 }
 
 void gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, const int32_t *deg, float rexp,
                    const Mat &C, bool exact) {
-  if (tc_enabled() && A.rows >= 128 && A.cols <= 288) {
+  if (A.rows >= kTcMinRows) {
     tc_gemm_tall_tri(c, A, Rinv, ldb, A.cols, deg, rexp, C, exact);
     return;
   }

@@ -58,7 +58,7 @@ void gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, do
 // rs_i = d_i^-e (e = rexp, deg != null) else 1.
 void gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcols, const int32_t *deg,
                float rexp, const Mat &C);
-// tensor-core (tcgen05, 3xTF32) versions; shapes: bcols / B.cols <= 288
+// tensor-core (tcgen05, 3xTF32) versions (any width: outputs in column groups of <= 288)
 void tc_gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcols, const int32_t *deg,
                   float rexp, const Mat &C);
 void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg,
@@ -70,7 +70,6 @@ void tc_gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, int
 // orthonormal to ~1e-3 — for CholeskyQR passes another pass follows)
 void gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, const int32_t *deg, float rexp,
                    const Mat &C, bool exact = true);
-bool tc_enabled();
 // Ω = randn(n, l) from Philox [R1], row-scaled by d_i^-e (deg != null)
 void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, float rexp, int64_t row0 = 0,
                     const int32_t *ids = nullptr);  // ids: global row id per row (compacted graphs)

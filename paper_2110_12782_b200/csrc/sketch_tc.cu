@@ -398,11 +398,7 @@ static void launch_sketch(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mh, 
 #undef SK_CASE
     default: NM_REQUIRE(false, "tc_sketch: unsupported group size");
   }
-  static bool attr_set[64 * 4] = {};
-  if (!attr_set[prm.epi]) {
-    NM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set[prm.epi] = true;
-  }
+  smem_attr(kern, smem);
   // enough items for every SM: split the N tiles of an M tile when M tiles are few
   prm.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(prm.ntn, ceil_div(2 * (int64_t)c.num_sms, prm.nmt)));
   const int per = (prm.ntn + prm.nsplit - 1) / prm.nsplit;

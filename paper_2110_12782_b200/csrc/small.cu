@@ -242,8 +242,10 @@ __global__ void __launch_bounds__(1024) k_cholesky(double *G, int l, int64_t ld,
       for (int j = 0; j < jb; ++j) {
         if (tid == 0) {
           double piv = P[j * CHP + j];
-          double ref = G0[(int64_t)(J + j) * l + J + j] + shift;
-          if (!(piv > 1e-12 * ref) || !isfinite(piv)) fail = 1;
+          const double g0 = G0[(int64_t)(J + j) * l + J + j];
+          double ref = g0 + shift;
+          if (g0 == 0.0) P[j * CHP + j] = 1.0;  // exactly-zero column: identity pivot [R10]
+          else if (!(piv > 1e-12 * ref) || !isfinite(piv)) fail = 1;
           else P[j * CHP + j] = sqrt(piv);
         }
         __syncthreads();
@@ -288,11 +290,7 @@ void cholesky_upper(Ctx &c, double *G, int64_t l, int64_t ld, int *flag) {
   NM_REQUIRE(l > 0 && l <= 4096, "cholesky: l out of range");
   DBuf<double> G0((size_t)l * l, c.stream);
   size_t smem = (size_t)l * CHP * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    NM_CUDA(cudaFuncSetAttribute(k_cholesky, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  smem_attr(k_cholesky, 200 * 1024);
   NM_REQUIRE(smem <= 200 * 1024, "cholesky: l too large for one CTA panel");
   NM_LAUNCH(c, "cholesky", k_cholesky<<<1, 1024, smem, c.stream>>>(G, (int)l, ld, G0, flag));
 }
@@ -382,8 +380,12 @@ __global__ void __launch_bounds__(CI_T) k_chol_inv(double *G, int l, int64_t ld,
       if (warp == 0) {
         bool bad = false;
         for (int j = 0; j < jb; ++j) {
-          const double d = R2[j * CI_LD + j];
-          if (!(d > 1e-12 * (diag0[J + j] + shift)) || !isfinite(d)) bad = true;
+          // an exactly-zero column of the Gram's input (zero row and column
+          // of G) gets an identity pivot: that column of Y R⁻¹ stays zero and
+          // the others are untouched — orth on range(Y) [R10]
+          const bool zc = diag0[J + j] == 0.0;
+          const double d = zc ? 1.0 : R2[j * CI_LD + j];
+          if (!zc && (!(d > 1e-12 * (diag0[J + j] + shift)) || !isfinite(d))) bad = true;
           const double sq = sqrt(fmax(d, 1e-300));
           __syncwarp();
           if (lane == j) R2[j * CI_LD + j] = sq;
@@ -512,11 +514,7 @@ void chol_inv_upper(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int 
   }
   DBuf<double> G0((size_t)l * l, c.stream);
   const size_t smem = ((size_t)2 * CI_R + 32 * CI_LD) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    NM_CUDA(cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  smem_attr(k_chol_inv, smem);
   NM_LAUNCH(c, "chol_inv", k_chol_inv<<<1, CI_T, smem, c.stream>>>(G, (int)l, ld, G0, Rinv, flag));
 }
 
@@ -542,11 +540,7 @@ __global__ void k_trinv(const double *__restrict__ R, int64_t ld, double *__rest
 void tri_inv_upper(Ctx &c, const double *R, int64_t ld, double *Rinv, int64_t l) {
   const int wpb = 8;
   size_t smem = (size_t)wpb * l * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    NM_CUDA(cudaFuncSetAttribute(k_trinv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  smem_attr(k_trinv, 200 * 1024);
   NM_REQUIRE(smem <= 200 * 1024, "tri_inv: l too large");
   NM_LAUNCH(c, "trinv", k_trinv<<<ceil_div(l, wpb), wpb * 32, smem, c.stream>>>(R, ld, Rinv, (int)l));
 }
@@ -1137,22 +1131,14 @@ void sym_eig(Ctx &c, double *S, int64_t l64, double *lam, double *V, bool abs_or
   const int nloc = (l + TDC - 1) / TDC;
   size_t smem = ((size_t)nloc * l + 4 * l + 40 + 32 * TDC + 8) * sizeof(double);
   NM_REQUIRE(smem <= 227 * 1024 && l <= 32 * BT_NR, "sym_eig: l too large for the 8-CTA cluster (l <= ~470)");
-  static bool attr = false;
-  if (!attr) {
-    NM_CUDA(cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    if (TDC > 8) NM_CUDA(cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr = true;
-  }
+  smem_attr(k_tridiag, 227 * 1024);
+  if (TDC > 8) func_attr(reinterpret_cast<const void *>(k_tridiag), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   NM_LAUNCH(c, "tridiag", k_tridiag<<<TDC, TDT, smem, s>>>(S, l, d, e, Hv, hb));
   NM_LAUNCH(c, "multisect", k_multisect<<<l, MSW * 32, (size_t)2 * l * sizeof(double), s>>>(d, e, l, w));
   DBuf<int> cst(l + 1, s), ncl(1, s);
   NM_LAUNCH(c, "clusters", k_clusters<<<1, 32, 0, s>>>(w, d, e, l, cst, ncl));
   const size_t ivsm = (size_t)IVW * 4 * l * sizeof(double) + (size_t)IVW * l + 16 + (size_t)IVW * l * sizeof(double);
-  static bool attr_iv = false;
-  if (!attr_iv) {
-    NM_CUDA(cudaFuncSetAttribute(k_invit, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr_iv = true;
-  }
+  smem_attr(k_invit, 200 * 1024);
   NM_LAUNCH(c, "invit", k_invit<<<ceil_div(l, IVW), IVW * 32, ivsm, s>>>(d, e, l, w, cst, ncl, Zt, 0x1234567u));
   NM_LAUNCH(c, "backtransform", k_backtransform<<<ceil_div((int64_t)l * 32, BT_T), BT_T, 0, s>>>(Hv, hb, l, Zt));
   NM_LAUNCH(c, "eig_sort", k_eig_sort<<<l, 128, 0, s>>>(w, Zt, l, abs_order, lam, V));

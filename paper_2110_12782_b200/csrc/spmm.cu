@@ -13,8 +13,10 @@
 //    round of X gathers (every lane reads the same column index — an L1
 //    broadcast — and its own 16 B of the neighbour's row);
 //  * heavy rows (deg > light_cap, power-law hubs): split into heavy_seg-nnz
-//    segments, one warp each, partial sums added into a scratch row with
-//    float4 atomics; the segment that completes the row runs the epilogue;
+//    segments, one warp each; every segment stores its partial sum in its own
+//    scratch slot and the segment that completes the row (arrival counter)
+//    adds the row's partials in segment order and runs the epilogue — the
+//    result does not depend on the order segments finish (deterministic);
 //  * both kinds of work are blocks of ONE launch (interleaved), so the
 //    L2-bound hub gathers overlap the latency-bound light rows;
 //  * fused epilogue: row scaling d_u^-a, optional β·prev and σ·acc_in terms
@@ -84,13 +86,15 @@ __device__ __forceinline__ float4 gather_sum(const int32_t *__restrict__ col, in
   return acc;
 }
 
+// per heavy segment: its partial sum into its own slot part[sidx, :] (the
+// row kernel adds a row's slots in segment order: deterministic)
 template <int LPR, bool SCOL>
 __global__ void __launch_bounds__(256, 8) k_spmm_heavy(SpmmArgs p, const int64_t *__restrict__ rowptr,
                                                     const int32_t *__restrict__ col,
                                                     const int32_t *__restrict__ heavy,
                                                     const int64_t *__restrict__ seg_e0,
                                                     const int32_t *__restrict__ seg_h, int64_t nsegs,
-                                                    float *__restrict__ hsum, int64_t ldh) {
+                                                    float *__restrict__ part, int64_t ldh) {
   constexpr int GPB = 256 / LPR;
   const int li = threadIdx.x % LPR;
   const int gi = threadIdx.x / LPR;
@@ -104,8 +108,7 @@ __global__ void __launch_bounds__(256, 8) k_spmm_heavy(SpmmArgs p, const int64_t
   const int64_t e1 = min(e0 + (int64_t)p.heavy_seg, re);
   if (active) {
     float4 acc = gather_sum<SCOL>(col, e0, e1, p.X + c, (uint32_t)p.ldx, p.s_col);
-    float *dst = hsum + h * ldh + c;
-    atomicAdd(reinterpret_cast<float4 *>(dst), acc);
+    *reinterpret_cast<float4 *>(part + sidx * ldh + c) = acc;
   }
 }
 
@@ -113,7 +116,8 @@ template <int LPR, bool SCOL, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_spmm_rows(SpmmArgs p, const int64_t *__restrict__ rowptr,
                                                    const int32_t *__restrict__ col, int64_t n,
                                                    const int32_t *__restrict__ heavy, int64_t nh,
-                                                   const float *__restrict__ hsum, int64_t ldh) {
+                                                   const int64_t *__restrict__ seg_ptr,
+                                                   const float *__restrict__ part, int64_t ldh) {
   constexpr int GPB = 256 / LPR;
   const int li = threadIdx.x % LPR;
   const int gi = threadIdx.x / LPR;
@@ -132,14 +136,16 @@ __global__ void __launch_bounds__(256, MINB) k_spmm_rows(SpmmArgs p, const int64
       a0 = *reinterpret_cast<const float4 *>(p.acc_in + u * p.ldai + c);
     float4 acc;
     if (dg > p.light_cap) {
-      // heavy row: partial sums were reduced by k_spmm_heavy
+      // heavy row: its segments' partial sums (k_spmm_heavy), added in order
       int64_t lo = 0, hi = nh - 1;
       while (lo < hi) {
         int64_t mid = (lo + hi) >> 1;
         if (heavy[mid] < u) lo = mid + 1; else hi = mid;
       }
-      acc = active ? *reinterpret_cast<const float4 *>(hsum + lo * ldh + c)
-                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (active)
+        for (int64_t sg = seg_ptr[lo]; sg < seg_ptr[lo + 1]; ++sg)
+          acc = f4_add(*reinterpret_cast<const float4 *>(part + sg * ldh + c), acc);
     } else if (active) {
       acc = gather_sum<SCOL>(col, e0, e1, p.X + c, (uint32_t)p.ldx, p.s_col);
     }
@@ -270,17 +276,17 @@ __device__ __forceinline__ void spmm_tile_rows(const SpmmArgs &p, const int64_t 
 // Fused SpMM: one launch whose blocks alternate between heavy-row segments
 // (L2-bandwidth-bound gathers of hub rows) and 32-row tiles (latency-bound
 // light rows), so the two kinds of work overlap instead of running back to
-// back.  A heavy segment adds its partial sum into hsum with float4 atomics;
-// the group that brings a (row, column pass) counter to the row's segment
-// count applies the epilogue and returns hsum and the counter to zero, so the
-// scratch needs no clearing between launches.  `py` is the column pass of
+// back.  A heavy segment stores its partial sum in its own slot; the group
+// that brings a (row, column pass) counter to the row's segment count adds
+// the row's slots in segment order, applies the epilogue and returns the
+// counter to zero, so the counters need no clearing between launches.  `py` is the column pass of
 // this geometry (4·LPR columns), `cnt_stride` the counters per heavy row.
 template <int LPR, bool GEN>
 __device__ __forceinline__ void fused_body(const SpmmArgs &p, int py, int bx, const int64_t *__restrict__ rowptr,
                                            const int32_t *__restrict__ col, int64_t n,
                                            const int32_t *__restrict__ heavy, const int64_t *__restrict__ seg_ptr,
                                            const int64_t *__restrict__ seg_e0, const int32_t *__restrict__ seg_h,
-                                           int64_t nsegs, float *__restrict__ hsum, int64_t ldh,
+                                           int64_t nsegs, float *__restrict__ part,
                                            int32_t *__restrict__ hcnt, int cnt_stride, int nblk_heavy,
                                            int nblk_tile) {
   constexpr int GPB = 256 / LPR;
@@ -314,28 +320,41 @@ __device__ __forceinline__ void fused_body(const SpmmArgs &p, int py, int bx, co
   const int64_t u = __ldg(heavy + h);
   const int64_t rb = __ldg(rowptr + u), re = __ldg(rowptr + u + 1);
   const int64_t e1 = min(e0 + (int64_t)p.heavy_seg, re);
-  float *dst = hsum + h * ldh + c;
-  if (active) {
-    const float4 acc = gather_sum<false>(col, e0, e1, p.X + c, (uint32_t)p.ldx, nullptr);
-    atomicAdd(reinterpret_cast<float4 *>(dst), acc);
-  }
-  // the group's atomics are ordered before the arrival by the group barrier
+  // this segment's slot of the pass: part[(py * nsegs + sidx) * 4·LPR + 4·li]
+  constexpr int PW = LPR * 4;
+  float *slot = part + ((int64_t)py * nsegs + sidx) * PW + li * 4;
+  const float4 acc = active ? gather_sum<false>(col, e0, e1, p.X + c, (uint32_t)p.ldx, nullptr)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+  __stcg(reinterpret_cast<float4 *>(slot), acc);
+  // the group's stores are ordered before the arrival by the group barrier
   // and the leader's gpu-scope fence (cumulativity); the leader fences again
-  // after seeing the last arrival, before the group reads the sums
+  // after seeing the last arrival, before the group reads the partials
   __syncwarp(gmask);
+  const int64_t s0 = __ldg(seg_ptr + h), s1 = __ldg(seg_ptr + h + 1);
   int32_t *cnt = hcnt + h * cnt_stride + py;
   int last = 0;
   if (li == 0) {
     __threadfence();
-    last = atomicAdd(cnt, 1) == (int)(__ldg(seg_ptr + h + 1) - __ldg(seg_ptr + h)) - 1;
+    last = atomicAdd(cnt, 1) == (int)(s1 - s0) - 1;
     if (last) __threadfence();
   }
   last = __shfl_sync(gmask, last, lane / LPR * LPR);
   if (!last) return;
   if (active) {
-    const float4 acc = __ldcg(reinterpret_cast<const float4 *>(dst));
-    __stcg(reinterpret_cast<float4 *>(dst), make_float4(0.f, 0.f, 0.f, 0.f));
-    slice_epilogue<GEN>(p, u, c, p.coef * row_scale((int)(re - rb), p.a), acc);
+    // the row's partials in segment order (independent of arrival order)
+    const float *sp = part + ((int64_t)py * nsegs + s0) * PW + li * 4;
+    const int64_t ns = s1 - s0;
+    float4 tot = make_float4(0.f, 0.f, 0.f, 0.f);
+    int64_t j = 0;
+    for (; j + 4 <= ns; j += 4) {
+      const float4 a0 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 0) * PW));
+      const float4 a1 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 1) * PW));
+      const float4 a2 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 2) * PW));
+      const float4 a3 = __ldcg(reinterpret_cast<const float4 *>(sp + (j + 3) * PW));
+      tot = f4_add(a3, f4_add(a2, f4_add(a1, f4_add(a0, tot))));
+    }
+    for (; j < ns; ++j) tot = f4_add(__ldcg(reinterpret_cast<const float4 *>(sp + j * PW)), tot);
+    slice_epilogue<GEN>(p, u, c, p.coef * row_scale((int)(re - rb), p.a), tot);
   }
   if (li == 0) *cnt = 0;
 }
@@ -349,8 +368,7 @@ struct FusedGraph {
   const int64_t *seg_ptr, *seg_e0;
   const int32_t *seg_h;
   int64_t nsegs;
-  float *hsum;
-  int64_t ldh;
+  float *part;  // (column pass, segment) partial sums: passes x nsegs x 4·LPR
   int32_t *hcnt;
   int nblk_tile;
 };
@@ -358,7 +376,7 @@ struct FusedGraph {
 template <int LPR, int MINB, bool GEN>
 __global__ void __launch_bounds__(256, MINB) k_spmm_fused(SpmmArgs p, FusedGraph fg, int nblk_heavy) {
   fused_body<LPR, GEN>(p, blockIdx.y, blockIdx.x, fg.rowptr, fg.col, fg.n, fg.heavy, fg.seg_ptr, fg.seg_e0, fg.seg_h,
-                       fg.nsegs, fg.hsum, fg.ldh, fg.hcnt, gridDim.y, nblk_heavy, fg.nblk_tile);
+                       fg.nsegs, fg.part, fg.hcnt, gridDim.y, nblk_heavy, fg.nblk_tile);
 }
 
 // Warp-per-row path for a column scale s_col (general D^-a A D^-b): heavy
@@ -368,39 +386,36 @@ static void spmm_rows_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
   constexpr int GPB = 256 / LPR;
   constexpr int CW = LPR * 4;
   const unsigned chunks = ceil_div(p.cols, CW);
-  DBuf<float> hsum;
+  DBuf<float> part;
   int64_t ldh = pad4(p.cols);
   if (g.n_heavy > 0) {
-    hsum.alloc((size_t)g.n_heavy * ldh, c.stream);
-    hsum.zero();
+    part.alloc((size_t)g.n_heavy_segs * ldh, c.stream);
     dim3 gh(ceil_div(g.n_heavy_segs, GPB), chunks);
     NM_LAUNCH(c, "spmm_heavy", k_spmm_heavy<LPR, SCOL><<<gh, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.heavy, g.seg_e0, g.seg_h,
-                                                      g.n_heavy_segs, hsum, ldh));
+                                                      g.n_heavy_segs, part, ldh));
   }
   int64_t row_blocks = ceil_div(g.n, GPB);
   int64_t cap = (int64_t)c.num_sms * 64;
   dim3 grid((unsigned)std::min<int64_t>(row_blocks, cap), chunks);
   NM_LAUNCH(c, "spmm_rows", k_spmm_rows<LPR, SCOL, MINB><<<grid, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.n, g.heavy, g.n_heavy,
-                                                     hsum.p, ldh));
+                                                     g.heavy_seg_ptr.p, part.p, ldh));
 }
 
 template <int LPR>
 static void spmm_fused_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
   const unsigned passes = ceil_div(p.cols, LPR * 4);
-  const int64_t ldh = pad4(p.cols);
   if (g.n_heavy > 0) {
-    const size_t need = (size_t)g.n_heavy * ldh, needc = (size_t)g.n_heavy * passes;
-    if (g.hsum_ws.n < need) {
-      g.hsum_ws.alloc(need, c.stream);
-      g.hsum_ws.zero();
-    }
-    if (g.hcnt_ws.n < needc) {
-      g.hcnt_ws.alloc(needc, c.stream);
-      g.hcnt_ws.zero();
+    // context-owned scratch (one stream per context: launches are ordered);
+    // counters are allocated zeroed and every launch leaves them zero
+    const size_t need = (size_t)g.n_heavy_segs * passes * LPR * 4, needc = (size_t)g.n_heavy * passes;
+    if (c.spmm_part.n < need) c.spmm_part.alloc(need, c.stream);
+    if (c.spmm_cnt.n < needc) {
+      c.spmm_cnt.alloc(needc, c.stream);
+      c.spmm_cnt.zero();
     }
   }
   FusedGraph fg{g.rowptr, g.col, g.n, g.heavy, g.heavy_seg_ptr, g.seg_e0, g.seg_h, g.n_heavy_segs,
-                g.hsum_ws.p, ldh, g.hcnt_ws.p, 0};
+                c.spmm_part.p, c.spmm_cnt.p, 0};
   const int64_t ntiles = ceil_div(g.n, 32);
   fg.nblk_tile = (int)std::min<int64_t>(ceil_div(ntiles, 8), (int64_t)c.num_sms * 32);
   const int nbh = g.n_heavy > 0 ? (int)ceil_div(g.n_heavy_segs, 256 / LPR) : 0;

@@ -706,12 +706,8 @@ static void launch_gram(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, tc
   NM_REQUIRE(S >= 2, "tc_gram: too many columns for the staged chunk");
   p.stages = S;
   const size_t smem = 1024 + S * stage + kPadBlocks * BK * 128 + (3 * S + 2) * 8 + 16;
-  static bool attr = false;
-  if (!attr) {
-    NM_CUDA(cudaFuncSetAttribute(tc::k_gram_tc<BK, SYM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
-    NM_CUDA(cudaFuncSetAttribute(tc::k_gram_tc<BK, SYM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
-    attr = true;
-  }
+  smem_attr(tc::k_gram_tc<BK, SYM, true>, kSmemMax);
+  smem_attr(tc::k_gram_tc<BK, SYM, false>, kSmemMax);
   NM_LAUNCH(c, "tc_gram", kern<<<(unsigned)nchain, tc::NT, smem, c.stream>>>(ma, mb, p));
 }
 
@@ -896,11 +892,7 @@ static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ld
   p.stages = S;
   p.astages = ST;
   const size_t smem = 1024 + S * stage + staging + (3 * S + 10) * 8;
-  static bool attr = false;
-  if (!attr) {
-    NM_CUDA(cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
-    attr = true;
-  }
+  smem_attr(k_gemm_tc, kSmemMax);
   // triangular B: part-major order and the unneeded K chunks skipped (every
   // CTA streams the same Bᵀ chunks at the same time; measured 0.311 -> 0.295
   // ms at n = 406727); full B: parts of a tile side by side (0.351 vs 0.362)
@@ -926,8 +918,21 @@ void tc_gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t b
 
 void tc_gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, int64_t bcols, const int32_t *deg,
                       float rexp, const Mat &C, bool exact) {
-  NM_REQUIRE(bcols <= 288 && A.cols == bcols, "tc_gemm_tall_tri: square upper-triangular B, <= 288");
-  tc_gemm_tall_impl(c, A, Rinv, ldb, bcols, deg, rexp, C, true, exact);
+  NM_REQUIRE(A.cols == bcols, "tc_gemm_tall_tri: square upper-triangular B");
+  if (bcols <= 288) {
+    tc_gemm_tall_impl(c, A, Rinv, ldb, bcols, deg, rexp, C, true, exact);
+    return;
+  }
+  // wider: column groups of <= 288; group [c0, c0 + w) needs only the first
+  // c0 + w rows of the upper-triangular B (the rest are zero)
+  for (int64_t c0 = 0; c0 < bcols; c0 += 288) {
+    const int64_t w = std::min<int64_t>(288, bcols - c0);
+    Mat Ak = A, Cg = C;
+    Ak.cols = c0 + w;
+    Cg.p = C.p + c0;
+    Cg.cols = w;
+    tc_gemm_tall_impl(c, Ak, Rinv + c0, ldb, w, deg, rexp, Cg, false, exact);
+  }
 }
 
 }  // namespace netmfp

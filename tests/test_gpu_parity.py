@@ -201,14 +201,15 @@ def test_sketch_svd_parity(L, ctx, graphs, name, k, d, s2, s3, logmode):
     assert relf(Zsk.cpu().numpy(), Zo) <= 1e-4
     Uref, sref, Vref, Q = O.single_pass_svd(F64, Co, scale, d, s2, s3, z, seed, logmode)
     sg = sig.cpu().numpy()
-    assert np.abs(sg[:4] - sref[:4]).max() <= 1e-3 * sref[0]
+    lead = sref >= 1e-2 * sref[0]          # "leading" singular values
+    assert np.abs(sg - sref)[lead].max() <= 1e-3 * sref[0]
     assert np.abs(sg - sref).max() <= 1e-2 * sref[0]
     Ug = Ud.cpu().numpy().astype(np.float64)
     assert np.abs(Ug.T @ Ug - np.eye(d)).max() <= 1e-3
     # rank-d reconstruction U diag(sigma) U^T agrees (sign/rotation free)
     Eg = E.cpu().numpy().astype(np.float64)
     Eo = O.embedding_from_svd(Uref, sref)
-    assert relf(Eg @ Eg.T, Eo @ Eo.T) <= 1e-2
+    assert relf(Eg @ Eg.T, Eo @ Eo.T) <= 1e-3
 
 
 # ---------------------------------------------------------------- propagation
