@@ -11,7 +11,16 @@ family, timed live with CUDA events (netmfp_ctx_profile) during the timed
 steps.  `cpu_baseline` / `--impl reference` = the fp64 oracle on host cores
 over a bounded sample of the same workload, extrapolated to one embedding.
 
-python bench.py [--gpus N] [--steps K] [--warmup W] [--workload I] [--impl ours|reference]
+Multi-GPU (north_star): under torchrun with WORLD_SIZE = N > 1
+(or `--gpus N`, which relaunches itself under torch.distributed.run) the step
+is ONE graph row-partitioned over the N ranks — netmfp_dist_build_csr (each
+rank sorts only its rows' keys) + netmfp_embed (per-SpMM NCCL all-gather of the
+block, all-reduced Grams) — strong scaling, max over ranks, with the bytes
+each rank receives per step and the achieved NVLink GB/s.  `--comm host` runs
+the same schedule with the host-staged communicator over gloo (functional
+check with several ranks on one GPU; its times are not NVLink numbers).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--workload I] [--impl ours|reference] [--comm nccl|host]
 """
 from __future__ import annotations
 
@@ -55,6 +64,15 @@ def gather_roofline(achieved_tbps):
     return out
 
 
+# the paper's own CPU-machine numbers, for context only (another machine, other graphs)
+PAPER_CONTEXT = {
+    "machine": "2x Intel Xeon E5-2699 v4 (88 vCores), 1.5 TB RAM (PAPER.md:411)",
+    "BlogCatalog_s": 2.0, "YouTube_s": 32.0, "Friendster_min": 17.7, "ClueWeb_min": 38.9, "Hyperlink2012_h": 1.2,
+    "source": "PAPER.md:451-458 (Table 'Efficiency comparison', NetMF+ column)",
+    "note": "configs[1] is BlogCatalog-sized (n=10,312, m=333,983); ClueWeb has 0.98B vertices / 75B edges",
+}
+
+
 def workload(idx):
     from paper_2110_12782_b200 import inputs
     w = inputs.CONFIGS[idx]
@@ -62,15 +80,15 @@ def workload(idx):
     return w, spec
 
 
-def dist_init():
+def dist_init(backend="nccl"):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch
         import torch.distributed as td
-        torch.cuda.set_device(local)  # before the process group: NCCL binds the current device
-        td.init_process_group("nccl", init_method="env://")
+        torch.cuda.set_device(local % torch.cuda.device_count())  # before the group: NCCL binds the device
+        td.init_process_group(backend, init_method="env://")
     return ws, rank, local
 
 
@@ -79,7 +97,8 @@ def allreduce_max(x, ws):
         return x
     import torch
     import torch.distributed as td
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    on_gpu = td.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
     td.all_reduce(t, op=td.ReduceOp.MAX)
     return float(t.item())
 
@@ -187,7 +206,8 @@ def oracle_sample(w, n, src, dst, budget_s=20.0):
     sample = (f"oracle stages on the configs[{w.name}] shapes: build_csr, 1 of {n_spmm} SpMMs "
               f"n×{l}, 1 of {n_orth} eigSVDs n×{l}, Eq.5 sketch on {ns}/{n} rows, Z sketch on "
               f"{vs}/{v} p-rows (quadratic scaling), 1 of {w.prop_order} propagation SpMMs n×{w.d}; "
-              f"sum extrapolated to one embedding")
+              f"sum extrapolated to one embedding (an ESTIMATE: the sketch stages run on a random F with C = I "
+              f"of the right shapes, not on the embedding's own F, C)")
     return total, cores, sample
 
 
@@ -212,7 +232,9 @@ def run_reference(args):
             "config": {"workload": f"configs[{args.workload}] {w.name}", "n": n, "k": w.k, "s1": w.s1, "q": w.q,
                        "T": w.T, "b": w.b, "d": w.d, "s2": w.s2, "s3": w.s3, "z": w.z, "alpha": w.alpha,
                        "prop_order": w.prop_order},
-            "cpu_baseline": {"value": val, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": val, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample,
+                             "extrapolated": True},
+            "estimate": "per-step value extrapolated from timed oracle stages (see cpu_baseline.sample)",
             "e2e": {"value": val, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -298,39 +320,7 @@ def run_ours(args):
 
     # roofline of the dominant kernel family
     if dom == "spmm":
-        # per SpMM launch set: algorithmic bytes = rowptr + col + X read + Y write (+ prev/acc)
-        spmm_ms = sum(v[1] for k, v in prof.items() if k.startswith("spmm"))
-        n_spmm_l = 2 * w.q + 2
-        n_spmm_d = w.prop_order
-        bytes_l = 8 * (nr + 1) + 4 * nnz + 2 * 4 * nr * l
-        # Chebyshev filter by Clenshaw (pipeline.cu propagate): n'×d block
-        # streams over the N steps — first (gather E, write b) 2, second
-        # (gather b, read E, write b) 3, middle steps (gather b, read b and E,
-        # write b) 4 each, last (gather b_1, read b_2 and E, write E) 4
-        N = w.prop_order
-        cheb_streams = 2 if N == 1 else (2 + 3 if N == 2 else 2 + 3 + 4 * (N - 3) + 4)
-        alg_bytes = n_spmm_l * bytes_l + n_spmm_d * (8 * (nr + 1) + 4 * nnz) + cheb_streams * 4 * nr * d
-        per_step_ms = spmm_ms / args.steps
-        achieved = alg_bytes / (per_step_ms * 1e-3) / 1e9
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
-        if os.path.exists(tp) and args.workload == 2:
-            tj = json.load(open(tp))["spmm_family_bytes_per_application"]
-            traffic = (n_spmm_l * tj["freigs_n_x_286"] + n_spmm_d * tj["chebyshev_n_x_128"]) / (n_spmm_l + n_spmm_d)
-        roof = {"kernel": "spmm (k_spmm_fused: light-row tiles + heavy-row segments)", "bound": "hbm",
-                "achieved": achieved,
-                "peak": peaks["hbm"], "unit": "GB/s", "frac": achieved / peaks["hbm"],
-                "traffic": traffic,
-                "traffic_note": "ncu dram read+write bytes per SpMM application (its k_spmm_fused launches), "
-                                "profiles/r01_traffic.json; algorithmic bytes per application: "
-                                f"{alg_bytes / (n_spmm_l + n_spmm_d):.4g} (rows = {nr})",
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peaks['src']})",
-                "share_of_step": per_step_ms / ms,
-                "edge_cols_per_s": (n_spmm_l * nnz * l + n_spmm_d * nnz * d) / (per_step_ms * 1e-3),
-                # the resource that binds this SpMM: every nonzero brings its
-                # neighbour's row slice into an SM (16 B per lane, L1/L2)
-                "gather": gather_roofline(4.0 * (n_spmm_l * nnz * l + n_spmm_d * nnz * d) / (per_step_ms * 1e-3) / 1e12),
-                "launches_per_step": sum(v[0] for k, v in prof.items() if k.startswith("spmm")) / args.steps}
+        roof = spmm_roofline(prof, args.steps, w, nr, nnz, ms, peaks, args.workload)
     else:
         kms = sum(v[1] for k, v in prof.items()) / args.steps
         roof = {"kernel": dom, "bound": "alu", "achieved": None, "peak": None, "unit": "TFLOP/s",
@@ -374,10 +364,12 @@ def run_ours(args):
                                             if not k.startswith("stage_")][:14]),
                 "stage_ms_per_step": {k[6:]: v[1] for k, v in sorted(prof_all.items(), key=lambda x: -x[1][1])
                                       if k.startswith("stage_")},
-                "clocks": clk}
+                "clocks": clk,
+                "paper_context": PAPER_CONTEXT}
         if ws == 1 and not args.no_cpu:
             v, cores, sample = oracle_sample(w, n, s_np, t_np)
-            line["cpu_baseline"] = {"value": v, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample}
+            line["cpu_baseline"] = {"value": v, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample,
+                                    "extrapolated": True}
         print(json.dumps(line))
     if ws > 1:
         import torch.distributed as td
@@ -385,67 +377,230 @@ def run_ours(args):
     return 0
 
 
+def spmm_roofline(prof, steps, w, nr, nnz, ms, peaks, workload_idx, per_rank=""):
+    """Roofline object of the SpMM family: algorithmic bytes of
+    every normalized SpMM of one embedding (rowptr + col + X read + Y write,
+    Clenshaw streams for the propagation) / their CUDA-event time."""
+    spmm_ms = sum(v[1] for k, v in prof.items() if k.startswith("spmm"))
+    l, d = w.k + w.s1, w.d
+    n_spmm_l = 2 * w.q + 2
+    n_spmm_d = w.prop_order
+    bytes_l = 8 * (nr + 1) + 4 * nnz + 2 * 4 * nr * l
+    # Chebyshev filter by Clenshaw (pipeline.cu propagate): n'×d block
+    # streams over the N steps — first (gather E, write b) 2, second
+    # (gather b, read E, write b) 3, middle steps (gather b, read b and E,
+    # write b) 4 each, last (gather b_1, read b_2 and E, write E) 4
+    N = w.prop_order
+    cheb_streams = 0 if N == 0 else 2 if N == 1 else (2 + 3 if N == 2 else 2 + 3 + 4 * (N - 3) + 4)
+    alg_bytes = n_spmm_l * bytes_l + n_spmm_d * (8 * (nr + 1) + 4 * nnz) + cheb_streams * 4 * nr * d
+    per_step_ms = spmm_ms / steps
+    achieved = alg_bytes / (per_step_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "r02_traffic.json")
+    if not os.path.exists(tp):
+        tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tp) and workload_idx == 2 and not per_rank:
+        tj = json.load(open(tp))["spmm_family_bytes_per_application"]
+        traffic = (n_spmm_l * tj["freigs_n_x_286"] + n_spmm_d * tj["chebyshev_n_x_128"]) / (n_spmm_l + n_spmm_d)
+    return {"kernel": "spmm (k_spmm_fused: light-row tiles + heavy-row segments)", "bound": "hbm",
+            "achieved": achieved, "peak": peaks["hbm"], "unit": "GB/s", "frac": achieved / peaks["hbm"],
+            "traffic": traffic,
+            "traffic_note": "ncu dram read+write bytes per SpMM application (its k_spmm_fused launches), "
+                            f"{os.path.relpath(tp, ROOT)}; algorithmic bytes per application: "
+                            f"{alg_bytes / max(1, n_spmm_l + n_spmm_d):.4g} (rows = {nr}{per_rank})",
+            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peaks['src']})",
+            "share_of_step": per_step_ms / ms,
+            "edge_cols_per_s": (n_spmm_l * nnz * l + n_spmm_d * nnz * d) / (per_step_ms * 1e-3),
+            # the resource that binds this SpMM: every nonzero brings its
+            # neighbour's row slice into an SM (16 B per lane, L1/L2)
+            "gather": gather_roofline(4.0 * (n_spmm_l * nnz * l + n_spmm_d * nnz * d) / (per_step_ms * 1e-3) / 1e12),
+            "launches_per_step": sum(v[0] for k, v in prof.items() if k.startswith("spmm")) / steps}
+
+
+def make_edges(args, w, spec, dev):
+    """The workload's edge list, resident in HBM (int32 src, dst) + host copies
+    for the e2e leg.  configs[0..2]: inputs.make_graph (numpy, the parity
+    tests' graphs); configs[3], [4] (billions of edges): the same R-MAT recipe
+    drawn on the GPU (inputs.rmat_device)."""
+    import torch
+    from paper_2110_12782_b200 import inputs
+    if spec["kind"] == "rmat" and spec["scale"] > 22:
+        src, dst = inputs.rmat_device(spec["scale"], spec["edge_factor"], spec["a"], spec["b"], spec["c"],
+                                      spec["seed"], dev)
+        return 1 << spec["scale"], src, dst, "synthetic (R-MAT drawn on the GPU, inputs.rmat_device)"
+    n, s_np, t_np = inputs.make_graph(spec)
+    return n, torch.from_numpy(s_np).to(dev), torch.from_numpy(t_np).to(dev), "synthetic"
+
+
+def partition_bounds(n, src, dst, ws):
+    """Row partition for ONE graph over ws ranks (same on every rank): contiguous
+    ranges of near-equal (degree + 1) cost, degrees estimated from the raw
+    edge list (duplicates counted) — no full CSR on any rank."""
+    import torch
+    deg = torch.bincount(src.long(), minlength=n) + torch.bincount(dst.long(), minlength=n)
+    cost = torch.cumsum(deg + 1, 0)
+    tot = int(cost[-1])
+    tgt = torch.tensor([tot * r // ws for r in range(1, ws)], dtype=cost.dtype, device=cost.device)
+    inner = torch.searchsorted(cost, tgt).cpu().numpy().tolist() if ws > 1 else []
+    b = [0] + [int(x) for x in inner] + [n]
+    for r in range(1, ws + 1):  # every rank at least one row
+        b[r] = max(b[r], b[r - 1] + 1)
+    for r in range(ws - 1, -1, -1):
+        b[r] = min(b[r], b[r + 1] - 1)
+    return np.array(b, dtype=np.int64)
+
+
 def run_dist(args):
-    """--dist: ONE graph row-partitioned over all ranks (north_star):
-    NCCL all-gather of the SpMM input rows, all-reduced Grams.  Strong scaling."""
+    """ONE graph row-partitioned over all ranks (north_star):
+    each step = netmfp_dist_build_csr + netmfp_embed, NCCL all-gather of the
+    SpMM input rows and all-reduced Grams.  Strong scaling; max over ranks."""
     import torch
     import torch.distributed as td
-    ws, rank, local = dist_init()
-    torch.cuda.set_device(local)
+    ws, rank, local = dist_init(backend="gloo" if args.comm == "host" else "nccl")
+    ndev = torch.cuda.device_count()
+    dev_idx = local % ndev
+    torch.cuda.set_device(dev_idx)
     import __graft_entry__ as ge
     ge.build()
     from paper_2110_12782_b200 import _lib as L
-    from paper_2110_12782_b200 import inputs
+    peaks = load_peaks()
     w, spec = workload(args.workload)
-    n, s_np, t_np = inputs.make_graph(spec)
-    dev = torch.device("cuda", local)
-    src = torch.from_numpy(s_np).to(dev)
-    dst = torch.from_numpy(t_np).to(dev)
-    ctx = L.Context(local)
-    uid = [L.netmfp_dist_unique_id() if rank == 0 else None]
-    if ws > 1:
-        td.broadcast_object_list(uid, src=0)
-    L.netmfp_dist_init(ctx, uid[0], ws, rank)
-    gfull = L.netmfp_build_csr(ctx, n, src, dst)
-    rp, _, _ = gfull.export(ctx)
-    bounds = L.netmfp_partition_rows(rp, ws)
-    del gfull
-    g = L.netmfp_dist_build_csr(ctx, n, src, dst, bounds)
+    dev = torch.device("cuda", dev_idx)
+    n, src, dst, data = make_edges(args, w, spec, dev)
+    m = int(src.numel())
+    bounds = partition_bounds(n, src, dst, ws)
+    ctx = L.Context(dev_idx)
+    if args.comm == "host":
+        L.netmfp_dist_init_ops(ctx, ws, rank, lambda a: td.all_reduce(torch.from_numpy(a)),
+                               lambda a, root: td.broadcast(torch.from_numpy(a), src=root))
+    else:
+        uid = [L.netmfp_dist_unique_id() if rank == 0 else None]
+        if ws > 1:
+            td.broadcast_object_list(uid, src=0)
+        L.netmfp_dist_init(ctx, uid[0], ws, rank)
     prm = L.make_params(**w.params())
-    nl = g.n
+    nl = int(bounds[rank + 1] - bounds[rank])
     E = torch.zeros(nl, (w.d + 31) // 32 * 32, dtype=torch.float32, device=dev)[:, :w.d]
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
-    for _ in range(args.warmup):
+    state = {}
+
+    def step():
+        g = L.netmfp_dist_build_csr(ctx, n, src, dst, bounds)
         L.netmfp_embed(ctx, g, prm, E)
-    clocks = ClockSampler(local)
+        state["g"] = g
+
+    for _ in range(args.warmup):
+        step()
+    # one profiled (untimed) step: per-kernel / per-stage breakdown
+    ctx.profile(True, "")
+    step()
+    prof_all = ctx.profile_read()
+    ctx.profile(False)
+    g = state["g"]
+    r0, ng, vol = L.netmfp_graph_rows(g)
+    nnz_local = g.nnz
+    L.netmfp_dist_stats(ctx)
+    ctx.profile(True, "spmm,stage_comm")
+    launches0 = ctx.launches
+    clocks = ClockSampler(dev_idx)
     barrier(ws)
     torch.cuda.synchronize()
     clocks.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    launches0 = ctx.launches
     for i in range(args.steps):
         flush.zero_()
         ev[i][0].record(stream)
-        L.netmfp_embed(ctx, g, prm, E)
+        step()
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     barrier(ws)
     clk = clocks.stop()
-    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    launches = ctx.launches - launches0
+    comm_bytes, ncoll = L.netmfp_dist_stats(ctx)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(step_ms))
     ms_max = allreduce_max(ms, ws)
+    comm_ms = sum(v[1] for k, v in prof.items() if k.startswith("stage_comm")) / args.steps
+    bytes_step = comm_bytes / args.steps
+    # rows this rank's blocks hold after isolated-vertex compaction
+    n_iso_local = int((g.export(ctx)[2] == 0).sum())
+    nr = nl - n_iso_local
+    roof = spmm_roofline(prof, args.steps, w, nr, nnz_local, ms, peaks, args.workload,
+                         per_rank=f" on rank {rank} of {ws}")
+    roof["nvlink"] = {"bytes_per_step_received": bytes_step, "collectives_per_step": ncoll / args.steps,
+                      "comm_ms_per_step": comm_ms,
+                      "achieved_GBps": (bytes_step / (comm_ms * 1e-3) / 1e9) if comm_ms > 0 else None,
+                      "peak_GBps": 770.0,
+                      "peak_source": "B200_PROFILING.md: measured peer copy, per direction (900 nominal)",
+                      "comm": "NCCL" if args.comm == "nccl" else "host-staged (gloo): not an NVLink figure"}
+    if roof["nvlink"]["achieved_GBps"]:
+        roof["nvlink"]["frac"] = roof["nvlink"]["achieved_GBps"] / 770.0
+    # e2e through the C ABI with host buffers: the edge list in, this rank's E rows out
+    s_h = src.cpu().pin_memory()
+    t_h = dst.cpu().pin_memory()
+    E_h = torch.zeros(nl, w.d, dtype=torch.float32).pin_memory()
+    e2e_ms = []
+    for i in range(max(2, min(args.steps, 3)) + 1):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier(ws)
+        t0 = time.perf_counter()
+        gh = L.netmfp_dist_build_csr(ctx, n, s_h, t_h, bounds)
+        L.netmfp_embed(ctx, gh, prm, E_h)
+        dt = (time.perf_counter() - t0) * 1e3
+        del gh
+        if i > 0:
+            e2e_ms.append(dt)
+    e2e = allreduce_max(float(np.mean(e2e_ms)), ws)
+    line_rank = {"bytes": bytes_step, "comm_ms": comm_ms, "ms": ms, "rows": nl, "nnz": int(nnz_local)}
+    all_ranks = [None] * ws
+    if ws > 1:
+        td.all_gather_object(all_ranks, line_rank)
+    else:
+        all_ranks = [line_rank]
     if rank == 0:
         line = {"metric": METRIC, "value": ms_max / 1e3, "unit": "s", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": False, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": f"configs[{args.workload}] {w.name}", "n": n, "mode": "row-partitioned",
-                           "bounds": [int(b) for b in bounds], "parallelism": f"rows{ws}",
-                           "l2": "flushed by a 512 MiB write between timed steps"},
-                "gpu_launches": int((ctx.launches - launches0) // args.steps), "clocks": clk}
+                "vs_baseline": None, "dtype": "f32", "data": data,
+                "config": {"workload": f"configs[{args.workload}] {w.name}", "n": n, "edges_in": m,
+                           "nnz": int(vol), "k": w.k, "s1": w.s1, "q": w.q, "T": w.T, "b": w.b, "d": w.d,
+                           "s2": w.s2, "s3": w.s3, "z": w.z, "alpha": w.alpha, "prop_order": w.prop_order,
+                           "mode": "row-partitioned (one graph over all ranks)",
+                           "bounds": [int(x) for x in bounds], "parallelism": f"rows{ws}",
+                           "comm": args.comm, "l2": "flushed by a 512 MiB write between timed steps"},
+                "e2e": {"value": e2e / 1e3, "unit": "s", "h2d_bytes_per_step": int(2 * 4 * m),
+                        "d2h_bytes_per_step": int(nl * w.d * 4),
+                        "note": "per rank: the whole edge list in (pinned), this rank's E rows out; max over ranks"},
+                "step_ms": [round(x, 3) for x in step_ms],
+                "gpu_launches": int(launches // args.steps),
+                "roofline": roof,
+                "per_rank": all_ranks,
+                "kernel_ms_per_step": dict([(k, v[1]) for k, v in sorted(prof_all.items(), key=lambda x: -x[1][1])
+                                            if not k.startswith("stage_")][:14]),
+                "stage_ms_per_step": {k[6:]: v[1] for k, v in sorted(prof_all.items(), key=lambda x: -x[1][1])
+                                      if k.startswith("stage_")},
+                "clocks": clk,
+                "paper_context": PAPER_CONTEXT}
         print(json.dumps(line))
     if ws > 1:
         td.destroy_process_group()
     return 0
+
+
+def relaunch(args):
+    """`--gpus N` outside torchrun: start N ranks of this script under
+    torch.distributed.run (127.0.0.1 rendezvous) and return its exit code."""
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -456,11 +611,16 @@ def main():
     ap.add_argument("--workload", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--dist", action="store_true", help="one graph row-partitioned over all ranks (strong scaling)")
+    ap.add_argument("--dist", action="store_true", help="row-partitioned path even with one rank")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "host"],
+                    help="host: host-staged communicator over gloo (functional, several ranks per GPU)")
     args = ap.parse_args()
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         sys.exit(run_reference(args))
-    if args.dist:
+    if args.gpus > 1 and ws == 1:
+        sys.exit(relaunch(args))
+    if ws > 1 or args.dist:
         sys.exit(run_dist(args))
     sys.exit(run_ours(args))
 

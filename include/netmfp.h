@@ -122,12 +122,41 @@ int netmfp_partition_rows(const int64_t *rowptr_host, int64_t n, int32_t parts, 
 int netmfp_dist_unique_id(void *id);
 /* Join the communicator (collective over all ranks; the context's device). */
 int netmfp_dist_init(netmfp_ctx *ctx, const void *id, int32_t nranks, int32_t rank);
+/* Host-staged communicator (instead of NCCL): the library synchronises its
+ * stream, copies the operand to host memory, calls the callback and copies
+ * the result back.  Callbacks return 0 on success (else NETMFP_ERR_NCCL is
+ * reported) and must be collective over all ranks in call order, like the
+ * NCCL calls they replace:
+ *   allreduce_sum(user, buf, count, dtype): buf[0..count) = Σ_ranks buf, in place;
+ *   broadcast(user, buf, count, dtype, root): buf[0..count) = root's buf.
+ * dtype: NETMFP_DT_F32 / _F64 / _I64 / _I32 / _U8.  Used to execute the
+ * multi-rank schedule where NCCL cannot run (several ranks on one GPU in
+ * tests, CPU-side process groups); the NVLink path is netmfp_dist_init. */
+#define NETMFP_DT_F32 0
+#define NETMFP_DT_F64 1
+#define NETMFP_DT_I64 2
+#define NETMFP_DT_I32 3
+#define NETMFP_DT_U8 4
+typedef struct netmfp_comm_ops {
+  void *user;
+  int (*allreduce_sum)(void *user, void *buf, int64_t count, int32_t dtype);
+  int (*broadcast)(void *user, void *buf, int64_t count, int32_t dtype, int32_t root);
+} netmfp_comm_ops;
+int netmfp_dist_init_ops(netmfp_ctx *ctx, const netmfp_comm_ops *ops, int32_t nranks, int32_t rank);
+/* Bytes this rank received in collectives since the last call (all-gathers:
+ * the other ranks' rows; all-reduces: the reduced payload), and how many
+ * collectives were issued; both counters are reset. */
+int netmfp_dist_stats(netmfp_ctx *ctx, int64_t *bytes, int64_t *collectives);
 /* Build this rank's CSR rows [bounds[rank], bounds[rank+1]) (bounds: nranks+1
- * host int64, 0 .. n; NULL = equal row counts; netmfp_partition_rows gives an
+ * host int64, strictly increasing from 0 to n — every rank owns >= 1 row; NULL = equal row counts; netmfp_partition_rows gives an
  * nnz-balanced split) with global column ids.  src/dst must contain every
- * (undirected) edge incident to those rows (the full list is fine).  Collective
- * (vol(G) is all-reduced).  Then netmfp_embed / netmfp_eig / netmfp_propagate
- * on this graph take and return this rank's rows of every n×c block. */
+ * (undirected) edge incident to those rows (the full list is fine: only the
+ * rank's own edges are sorted, so device memory is O(m/nranks) beyond the
+ * input).  Collective (vol(G) is all-reduced).  Then netmfp_embed /
+ * netmfp_eig / netmfp_propagate on this graph take and return this rank's rows
+ * of every n×c block; netmfp_embed drops isolated vertices from the blocks
+ * (every rank learns all degrees by one all-gather) and returns
+ * zero rows for them [R2]. */
 int netmfp_dist_build_csr(netmfp_ctx *ctx, int64_t n, const int32_t *src, const int32_t *dst, int64_t m_in,
                           const int64_t *bounds, int mem, netmfp_graph **out);
 /* CSR of rows [row0, row1) only (global column ids; no communicator; vol(G)

@@ -70,6 +70,8 @@ _SIGS = {
     "netmfp_dist_build_csr": (C.c_int, [_p, _i64, _p, _p, _i64, _p, C.c_int, C.POINTER(_p)]),
     "netmfp_graph_rows": (C.c_int, [_p, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)]),
     "netmfp_build_csr_rows": (C.c_int, [_p, _i64, _p, _p, _i64, _i64, _i64, C.c_int, C.POINTER(_p)]),
+    "netmfp_dist_init_ops": (C.c_int, [_p, _p, _i32, _i32]),
+    "netmfp_dist_stats": (C.c_int, [_p, C.POINTER(_i64), C.POINTER(_i64)]),
 }
 DIST_ID_BYTES = 128
 for _name, (_res, _args) in _SIGS.items():
@@ -237,6 +239,51 @@ def netmfp_dist_unique_id() -> bytes:
 def netmfp_dist_init(ctx: Context, uid: bytes, nranks: int, rank: int) -> None:
     buf = C.create_string_buffer(bytes(uid), DIST_ID_BYTES)
     _check(_L.netmfp_dist_init(ctx.h, buf, nranks, rank))
+
+
+_ALLRED = C.CFUNCTYPE(C.c_int, _p, _p, _i64, _i32)
+_BCAST = C.CFUNCTYPE(C.c_int, _p, _p, _i64, _i32, _i32)
+
+
+class CommOps(C.Structure):
+    """netmfp_comm_ops (include/netmfp.h): host-staged communicator callbacks."""
+    _fields_ = [("user", _p), ("allreduce_sum", _ALLRED), ("broadcast", _BCAST)]
+
+
+_DT_CTYPES = {0: C.c_float, 1: C.c_double, 2: C.c_int64, 3: C.c_int32, 4: C.c_uint8}
+
+
+def netmfp_dist_init_ops(ctx: Context, nranks: int, rank: int, allreduce_sum, broadcast) -> None:
+    """Join a host-staged communicator: allreduce_sum(a) and broadcast(a, root)
+    act in place on numpy views of the library's host staging buffers (e.g.
+    torch.distributed gloo calls on torch.from_numpy(a)); collective over ranks."""
+    def _view(buf, count, dt):
+        return np.ctypeslib.as_array((_DT_CTYPES[dt] * count).from_address(buf))
+
+    def _ar(user, buf, count, dt):
+        try:
+            allreduce_sum(_view(buf, count, dt))
+            return 0
+        except Exception:  # reported as NETMFP_ERR_NCCL by the library
+            return 1
+
+    def _bc(user, buf, count, dt, root):
+        try:
+            broadcast(_view(buf, count, dt), root)
+            return 0
+        except Exception:
+            return 1
+
+    ops = CommOps(None, _ALLRED(_ar), _BCAST(_bc))
+    ctx._comm_ops = ops  # keep the callbacks alive as long as the context
+    _check(_L.netmfp_dist_init_ops(ctx.h, C.byref(ops), nranks, rank))
+
+
+def netmfp_dist_stats(ctx: Context):
+    """(bytes received in collectives, collectives) since the last call."""
+    b, k = _i64(), _i64()
+    _check(_L.netmfp_dist_stats(ctx.h, C.byref(b), C.byref(k)))
+    return b.value, k.value
 
 
 def netmfp_dist_build_csr(ctx: Context, n: int, src, dst, bounds=None) -> Graph:

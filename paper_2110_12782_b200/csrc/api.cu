@@ -275,6 +275,24 @@ int netmfp_dist_init(netmfp_ctx *ctx, const void *id, int32_t nranks, int32_t ra
   });
 }
 
+int netmfp_dist_init_ops(netmfp_ctx *ctx, const netmfp_comm_ops *ops, int32_t nranks, int32_t rank) {
+  return guarded([&] {
+    NM_REQUIRE(ctx && ops, "dist_init_ops: NULL argument");
+    DevScope _dev(ctx->c);
+    dist_init_ops(ctx->c, *ops, nranks, rank);
+  });
+}
+
+int netmfp_dist_stats(netmfp_ctx *ctx, int64_t *bytes, int64_t *collectives) {
+  return guarded([&] {
+    NM_REQUIRE(ctx, "dist_stats: NULL ctx");
+    if (bytes) *bytes = ctx->c.comm_bytes;
+    if (collectives) *collectives = ctx->c.collectives;
+    ctx->c.comm_bytes = 0;
+    ctx->c.collectives = 0;
+  });
+}
+
 int netmfp_dist_build_csr(netmfp_ctx *ctx, int64_t n, const int32_t *src, const int32_t *dst, int64_t m_in,
                           const int64_t *bounds, int mem, netmfp_graph **out) {
   return guarded([&] {
@@ -286,7 +304,7 @@ int netmfp_dist_build_csr(netmfp_ctx *ctx, int64_t n, const int32_t *src, const 
     std::vector<int64_t> b(c.nranks + 1);
     for (int r = 0; r <= c.nranks; ++r) b[r] = bounds ? bounds[r] : n * r / c.nranks;
     NM_REQUIRE(b[0] == 0 && b[c.nranks] == n, "dist_build_csr: bounds must start at 0 and end at n");
-    for (int r = 0; r < c.nranks; ++r) NM_REQUIRE(b[r] <= b[r + 1], "dist_build_csr: bounds must be non-decreasing");
+    for (int r = 0; r < c.nranks; ++r) NM_REQUIRE(b[r] < b[r + 1], "dist_build_csr: every rank needs >= 1 row (bounds strictly increasing)");
     InVec<int32_t> s(c, src, m_in, mem, true), t(c, dst, m_in, mem, true);
     std::unique_ptr<Graph> g(build_csr_device(c, n, s.p, t.p, m_in, b[c.rank], b[c.rank + 1]));
     g->bounds = b;
@@ -554,20 +572,33 @@ int netmfp_propagate(netmfp_ctx *ctx, const netmfp_graph *gr, float *E, int64_t 
 }
 
 // The compacted copy of g without its isolated vertices, when embed may run
-// on it: one rank, g not itself a row partition, and enough
-// vertices left for the rank-(k+s1) basis.  Built once per graph and cached.
+// on it: g is the whole graph (one rank) or one rank's rows of a
+// graph partitioned for this communicator, not itself compacted, and enough
+// vertices remain for the rank-(k+s1) basis.  Built once per graph and cached
+// (under the graph's lock); a partitioned graph all-gathers the degrees.
 static const Graph *embed_graph(Ctx &c, const Graph &g, const netmfp_params &p) {
   static const bool off = [] {
     const char *v = getenv("NETMFP_NO_COMPACT");
     return v && atoi(v);
   }();
-  if (off || c.nranks != 1 || g.n_orig != 0 || g.row0 != 0 || g.n != g.n_global) return &g;
+  if (off || g.n_orig != 0) return &g;
+  const bool whole = g.row0 == 0 && g.n == g.n_global;
+  if (c.nranks == 1 && !whole) return &g;  // a row slice used without a communicator
+  if (c.nranks > 1 && (int)g.bounds.size() != c.nranks + 1) return &g;
+  std::lock_guard<std::mutex> lk(g.compact_mu);
   if (!g.compact_checked) {
     NM_STAGE(c, "stage_compact");
-    g.compact.reset(compact_graph(c, g));
+    DBuf<int32_t> degall;
+    const int32_t *da = g.deg.p;
+    if (c.nranks > 1) {
+      degall.alloc(g.n_global, c.stream);
+      dist_allgather_i32(c, g.deg.p, g.bounds, degall.p);
+      da = degall.p;
+    }
+    g.compact.reset(compact_graph(c, g, da));
     g.compact_checked = true;
   }
-  if (!g.compact || g.compact->n < (int64_t)p.k + p.s1) return &g;
+  if (!g.compact || g.compact->n_global < (int64_t)p.k + p.s1) return &g;
   return g.compact.get();
 }
 
@@ -646,7 +677,9 @@ static void embed_impl(Ctx &c, const Graph &g_in, const netmfp_params &p, const 
   }
   Block Ec(g.n, p.d, c.stream);
   embed_core(c, g, p, Ec.m, sigma_dev, lambda_dev);
-  scatter_rows(c, Ec.m, g.comp_id.p, E_out);  // isolated vertices: zero rows [R2]
+  // this rank's original rows [g_in.row0, +g_in.n) from its compact rows
+  // [g.row0, +g.n); isolated vertices: zero rows [R2]
+  scatter_rows(c, Ec.m, g.comp_id.p + g_in.row0, E_out, g.row0);
 }
 
 // Host output, compacted graph, pinned E: the host zeroes E (threads, while
@@ -655,6 +688,7 @@ static void embed_impl(Ctx &c, const Graph &g_in, const netmfp_params &p, const 
 // (nothing done) when the path does not apply.
 static bool embed_host_pinned(Ctx &c, const Graph &g_in, const netmfp_params &p, float *E, int64_t lde,
                               double *sigma_dev, double *lambda_dev) {
+  if (c.nranks > 1) return false;  // partitioned: the staged copy of this rank's rows
   const Graph &g = *embed_graph(c, g_in, p);
   float *Edev = (&g != &g_in) ? mapped_device_ptr(E) : nullptr;
   if (!Edev) return false;

@@ -34,6 +34,56 @@ __global__ void k_make_keys(const int32_t *__restrict__ src, const int32_t *__re
   }
 }
 
+// Row-range builds (one rank's rows [row0, row1)): only the keys of this
+// rank's rows are made and sorted — O(m / nranks) device memory for the sort
+// instead of 2m keys.  Pass 1 counts them (and flags bad ids), pass 2 appends
+// them with warp-aggregated atomics (order irrelevant: they are sorted next).
+__device__ __forceinline__ int local_dirs(int32_t s, int32_t t, uint64_t row0, uint64_t row1) {
+  if (s == t) return 0;  // self loop: dropped
+  return ((uint64_t)s >= row0 && (uint64_t)s < row1 ? 1 : 0) | ((uint64_t)t >= row0 && (uint64_t)t < row1 ? 2 : 0);
+}
+__global__ void k_count_local(const int32_t *__restrict__ src, const int32_t *__restrict__ dst, int64_t m, uint64_t n,
+                              uint64_t row0, uint64_t row1, unsigned long long *__restrict__ cnt, int *bad) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int c = 0;
+  if (e < m) {
+    const int32_t s = src[e], t = dst[e];
+    if (s < 0 || t < 0 || (uint64_t)s >= n || (uint64_t)t >= n) {
+      atomicExch(bad, 1);
+    } else {
+      const int d = local_dirs(s, t, row0, row1);
+      c = (d & 1) + (d >> 1);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, (unsigned long long)c);
+}
+__global__ void k_make_keys_local(const int32_t *__restrict__ src, const int32_t *__restrict__ dst, int64_t m,
+                                  uint64_t n, uint64_t row0, uint64_t row1, int cb, uint64_t *__restrict__ keys,
+                                  unsigned long long *__restrict__ pos) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int d = 0;
+  int32_t s = 0, t = 0;
+  if (e < m) {
+    s = src[e];
+    t = dst[e];
+    if (s >= 0 && t >= 0 && (uint64_t)s < n && (uint64_t)t < n) d = local_dirs(s, t, row0, row1);
+  }
+  const int c = (d & 1) + (d >> 1);
+  int incl = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  unsigned long long base = 0;
+  if (lane == 31 && incl) base = atomicAdd(pos, (unsigned long long)incl);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  uint64_t at = base + (uint64_t)(incl - c);
+  if (d & 1) keys[at++] = ((uint64_t)s << cb) | (uint32_t)t;
+  if (d & 2) keys[at] = ((uint64_t)t << cb) | (uint32_t)s;
+}
+
 // rowptr[u] = first key index with row >= row0 + u (lower bound), u in [0, n]
 // nnz = unique keys minus the sentinel row n (the last unique key if present),
 // so the host reads it together with the error flag in one round trip
@@ -110,12 +160,33 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
   if (const char *v = getenv("NETMFP_LIGHT_CAP")) g->light_cap = std::max(1, atoi(v));
   if (const char *v = getenv("NETMFP_HEAVY_SEG")) g->heavy_seg = std::max(1, atoi(v));
   try {
+    const bool part = row0 > 0 || row1 < n_all;  // one rank's rows: sort only their keys
     int64_t nk = 2 * m;
     const int cb = std::max(1, bits_for((uint64_t)(n_all - 1)));  // bits of a column id
-    DBuf<uint64_t> keys(nk > 0 ? nk : 1, s), keys2(nk > 0 ? nk : 1, s);
     DBuf<int> bad(1, s);
     bad.zero();
-    if (m > 0) {
+    DBuf<unsigned long long> kcnt;
+    if (part) {
+      kcnt.alloc(2, s);
+      kcnt.zero();
+      unsigned long long hk = 0;
+      int hb = 0;
+      if (m > 0)
+        NM_LAUNCH(c, "count_local", k_count_local<<<ceil_div(m, 256), 256, 0, s>>>(src, dst, m, (uint64_t)n_all,
+                                                                                  (uint64_t)row0, (uint64_t)row1,
+                                                                                  kcnt.p, bad));
+      NM_CUDA(cudaMemcpyAsync(&hk, kcnt.p, 8, cudaMemcpyDeviceToHost, s));
+      NM_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, s));
+      NM_CUDA(cudaStreamSynchronize(s));
+      NM_REQUIRE(!hb, "build_csr: vertex id out of [0, n)");
+      nk = (int64_t)hk;
+    }
+    DBuf<uint64_t> keys(nk > 0 ? nk : 1, s), keys2(nk > 0 ? nk : 1, s);
+    if (part && nk > 0) {
+      NM_LAUNCH(c, "make_keys_local", k_make_keys_local<<<ceil_div(m, 256), 256, 0, s>>>(
+                                          src, dst, m, (uint64_t)n_all, (uint64_t)row0, (uint64_t)row1, cb, keys,
+                                          kcnt.p + 1));
+    } else if (!part && m > 0) {
       NM_LAUNCH(c, "make_keys", k_make_keys<<<ceil_div(m, 256), 256, 0, s>>>(src, dst, m, (uint64_t)n_all, (uint64_t)row0,
                                                                              (uint64_t)row1, cb, keys, bad));
     }
@@ -201,6 +272,9 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
 // dense block of embed is zero on it; the compacted graph keeps the other
 // vertices in their original order.  Edge offsets are unchanged (isolated
 // rows own no entries), so the heavy-row segment tables carry over as is.
+// Works on one rank's rows [b0, b1) of a row-partitioned graph too: `degall`
+// holds every vertex's degree (all-gathered), compact ids are global, and the
+// rank keeps the image [pos[b0], pos[b1]) of its rows.
 // ---------------------------------------------------------------------------
 __global__ void k_flag_nz(const int32_t *__restrict__ deg, int64_t n, int32_t *__restrict__ flag) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -208,23 +282,24 @@ __global__ void k_flag_nz(const int32_t *__restrict__ deg, int64_t n, int32_t *_
   if (i == n) flag[i] = 0;
 }
 __global__ void k_compact_ids(const int32_t *__restrict__ deg, const int32_t *__restrict__ pos, int64_t n,
-                              int32_t *__restrict__ orig, int32_t *__restrict__ comp) {
+                              int64_t b0, int64_t b1, int64_t row0c, int32_t *__restrict__ orig,
+                              int32_t *__restrict__ comp) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (deg[i] > 0) {
-    orig[pos[i]] = (int32_t)i;
     comp[i] = pos[i];
+    if (i >= b0 && i < b1) orig[pos[i] - row0c] = (int32_t)i;
   } else {
     comp[i] = -1;
   }
 }
-__global__ void k_compact_rows(const int32_t *__restrict__ orig, int64_t ne, const int64_t *__restrict__ rowptr,
-                               const int32_t *__restrict__ deg, int64_t nnz, int64_t *__restrict__ rp_c,
-                               int32_t *__restrict__ deg_c) {
+__global__ void k_compact_rows(const int32_t *__restrict__ orig, int64_t ne, int64_t b0,
+                               const int64_t *__restrict__ rowptr, const int32_t *__restrict__ deg, int64_t nnz,
+                               int64_t *__restrict__ rp_c, int32_t *__restrict__ deg_c) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j < ne) {
-    rp_c[j] = rowptr[orig[j]];
-    deg_c[j] = deg[orig[j]];
+    rp_c[j] = rowptr[orig[j] - b0];
+    deg_c[j] = deg[orig[j] - b0];
   }
   if (j == ne) rp_c[ne] = nnz;
 }
@@ -233,41 +308,57 @@ __global__ void k_remap_ids(const int32_t *__restrict__ in, int64_t m, const int
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < m) out[i] = comp[in[i]];
 }
+// local row index -> local compact row index
+__global__ void k_remap_local(const int32_t *__restrict__ in, int64_t m, const int32_t *__restrict__ comp, int64_t b0,
+                              int64_t row0c, int32_t *__restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < m) out[i] = (int32_t)(comp[b0 + in[i]] - row0c);
+}
 
-Graph *compact_graph(Ctx &c, const Graph &g) {
-  if (g.row0 != 0 || g.n != g.n_global || g.n == 0) return nullptr;
+Graph *compact_graph(Ctx &c, const Graph &g, const int32_t *degall) {
+  const int64_t n_all = g.n_global;
+  if (n_all == 0) return nullptr;
   cudaStream_t s = c.stream;
-  const int64_t n = g.n;
-  DBuf<int32_t> flag(n + 1, s), pos(n + 1, s);
-  NM_LAUNCH(c, "flag_nz", k_flag_nz<<<ceil_div(n + 1, 256), 256, 0, s>>>(g.deg, n, flag));
+  const int64_t b0 = g.row0, b1 = g.row0 + g.n;
+  DBuf<int32_t> flag(n_all + 1, s), pos(n_all + 1, s);
+  NM_LAUNCH(c, "flag_nz", k_flag_nz<<<ceil_div(n_all + 1, 256), 256, 0, s>>>(degall, n_all, flag));
   size_t tb = 0;
-  NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.p, pos.p, n + 1, s));
+  NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.p, pos.p, n_all + 1, s));
   DBuf<char> tmp(tb, s);
-  NM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, flag.p, pos.p, n + 1, s));
+  NM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, flag.p, pos.p, n_all + 1, s));
   c.launches += 1;
-  int32_t ne32 = 0;
-  NM_CUDA(cudaMemcpyAsync(&ne32, pos.p + n, 4, cudaMemcpyDeviceToHost, s));
+  // compact images of every rank's bounds (bounds.back() = n_all: the total)
+  std::vector<int64_t> bounds = g.bounds.size() >= 2 ? g.bounds : std::vector<int64_t>{0, n_all};
+  std::vector<int32_t> pb(bounds.size());
+  for (size_t r = 0; r < bounds.size(); ++r)
+    NM_CUDA(cudaMemcpyAsync(&pb[r], pos.p + bounds[r], 4, cudaMemcpyDeviceToHost, s));
+  int32_t p0 = 0, p1 = 0;
+  NM_CUDA(cudaMemcpyAsync(&p0, pos.p + b0, 4, cudaMemcpyDeviceToHost, s));
+  NM_CUDA(cudaMemcpyAsync(&p1, pos.p + b1, 4, cudaMemcpyDeviceToHost, s));
   NM_CUDA(cudaStreamSynchronize(s));
-  const int64_t ne = ne32;
-  if (ne == n || ne == 0) return nullptr;
+  const int64_t ne_all = pb.back(), row0c = p0, ne = (int64_t)p1 - p0;
+  if (ne_all == n_all || ne_all == 0) return nullptr;
   auto gc = new Graph();
   try {
-    gc->n = gc->n_global = ne;
-    gc->row0 = 0;
-    gc->bounds = {0, ne};
+    gc->n = ne;
+    gc->n_global = ne_all;
+    gc->row0 = row0c;
+    gc->bounds.assign(pb.begin(), pb.end());
     gc->nnz = g.nnz;
     gc->nnz_global = g.nnz_global;
     gc->device = g.device;
     gc->light_cap = g.light_cap;
     gc->heavy_seg = g.heavy_seg;
-    gc->n_orig = n;
-    gc->orig_id.alloc(ne, s);
-    gc->comp_id.alloc(n, s);
-    NM_LAUNCH(c, "compact_ids", k_compact_ids<<<ceil_div(n, 256), 256, 0, s>>>(g.deg, pos, n, gc->orig_id, gc->comp_id));
+    gc->n_orig = n_all;
+    gc->orig_id.alloc(ne > 0 ? ne : 1, s);
+    gc->comp_id.alloc(n_all, s);
+    NM_LAUNCH(c, "compact_ids", k_compact_ids<<<ceil_div(n_all, 256), 256, 0, s>>>(degall, pos, n_all, b0, b1, row0c,
+                                                                                    gc->orig_id, gc->comp_id));
     gc->rowptr.alloc(ne + 1, s);
-    gc->deg.alloc(ne, s);
-    NM_LAUNCH(c, "compact_rows", k_compact_rows<<<ceil_div(ne + 1, 256), 256, 0, s>>>(gc->orig_id, ne, g.rowptr, g.deg,
-                                                                                        g.nnz, gc->rowptr, gc->deg));
+    gc->deg.alloc(ne > 0 ? ne : 1, s);
+    NM_LAUNCH(c, "compact_rows", k_compact_rows<<<ceil_div(ne + 1, 256), 256, 0, s>>>(gc->orig_id, ne, b0, g.rowptr,
+                                                                                        g.deg, g.nnz, gc->rowptr,
+                                                                                        gc->deg));
     gc->col.alloc(g.nnz > 0 ? g.nnz : 1, s);
     if (g.nnz > 0)
       NM_LAUNCH(c, "remap_col", k_remap_ids<<<ceil_div(g.nnz, 256), 256, 0, s>>>(g.col, g.nnz, gc->comp_id, gc->col));
@@ -276,8 +367,9 @@ Graph *compact_graph(Ctx &c, const Graph &g) {
     gc->n_heavy_segs = g.n_heavy_segs;
     gc->heavy.alloc(g.n_heavy > 0 ? g.n_heavy : 1, s);
     if (g.n_heavy > 0)
-      NM_LAUNCH(c, "remap_heavy", k_remap_ids<<<ceil_div(g.n_heavy, 256), 256, 0, s>>>(g.heavy, g.n_heavy, gc->comp_id,
-                                                                                        gc->heavy));
+      NM_LAUNCH(c, "remap_heavy", k_remap_local<<<ceil_div(g.n_heavy, 256), 256, 0, s>>>(g.heavy, g.n_heavy,
+                                                                                         gc->comp_id, b0, row0c,
+                                                                                         gc->heavy));
     gc->heavy_seg_ptr.alloc(g.n_heavy + 1, s);
     NM_CUDA(cudaMemcpyAsync(gc->heavy_seg_ptr.p, g.heavy_seg_ptr.p, (g.n_heavy + 1) * 8, cudaMemcpyDeviceToDevice, s));
     const int64_t ns = g.n_heavy_segs > 0 ? g.n_heavy_segs : 1;

@@ -127,7 +127,10 @@ struct Ctx {
   // row-partitioned multi-GPU (dist.cu); nranks == 1: single GPU
   int nranks = 1, rank = 0;
   void *comm = nullptr;  // ncclComm_t
+  netmfp_comm_ops ops{};  // host-staged communicator (netmfp_dist_init_ops) when ops_on
+  bool ops_on = false;
   int64_t collectives = 0;
+  int64_t comm_bytes = 0;  // bytes received in collectives (netmfp_dist_stats)
   // numeric checks deferred to the end of the ABI call (one synchronisation):
   // the stage whose Cholesky failure bit (d_flags & 1<<30) is reported
   std::vector<const char *> flag_checks;
@@ -334,6 +337,7 @@ struct Graph {
   DBuf<int32_t> orig_id, comp_id;
   mutable std::unique_ptr<Graph> compact;
   mutable bool compact_checked = false;
+  mutable std::mutex compact_mu;  // the cached compacted copy is built once
   void detach_streams() {  // free on the legacy stream (owning stream may be gone)
     rowptr.s = col.s = deg.s = heavy.s = nullptr;
     heavy_seg_ptr.s = seg_e0.s = nullptr;

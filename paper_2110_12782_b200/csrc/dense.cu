@@ -331,13 +331,14 @@ void copy_block(Ctx &c, const float *src, int64_t lds, float *dst, int64_t ldd, 
   NM_CUDA(cudaMemcpy2DAsync(dst, ldd * 4, src, lds * 4, cols * 4, rows, cudaMemcpyDefault, c.stream));
 }
 
-// Dst[i, :] = Src[comp[i], :], or 0 where comp[i] < 0 (compacted rows back
-// to all rows; every element of Dst written once).  A warp per row.
-__global__ void __launch_bounds__(256) k_scatter_rows(Mat Src, const int32_t *__restrict__ comp, Mat Dst, bool vec4) {
+// Dst[i, :] = Src[comp[i] - sub, :], or 0 where comp[i] < 0 (compacted rows
+// back to all rows; every element of Dst written once).  A warp per row.
+__global__ void __launch_bounds__(256) k_scatter_rows(Mat Src, const int32_t *__restrict__ comp, Mat Dst, bool vec4,
+                                                      int64_t sub) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * 8;
   for (int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < Dst.rows; i += nw) {
-    const int32_t r = comp[i];
+    const int64_t r = comp[i] < 0 ? -1 : comp[i] - sub;
     float *d = Dst.p + i * Dst.ld;
     const float *src = Src.p + (int64_t)(r < 0 ? 0 : r) * Src.ld;
     if (vec4) {
@@ -350,12 +351,12 @@ __global__ void __launch_bounds__(256) k_scatter_rows(Mat Src, const int32_t *__
   }
 }
 
-void scatter_rows(Ctx &c, const Mat &Src, const int32_t *comp, const Mat &Dst) {
+void scatter_rows(Ctx &c, const Mat &Src, const int32_t *comp, const Mat &Dst, int64_t sub) {
   if (Dst.rows * Dst.cols == 0) return;
   const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(Dst.rows, 8), (int64_t)c.num_sms * 16);
   const bool vec4 = Dst.cols % 4 == 0 && Dst.ld % 4 == 0 && Src.ld % 4 == 0 && ((uintptr_t)Dst.p & 15) == 0 &&
                     ((uintptr_t)Src.p & 15) == 0;
-  NM_LAUNCH(c, "scatter_rows", k_scatter_rows<<<blocks, 256, 0, c.stream>>>(Src, comp, Dst, vec4));
+  NM_LAUNCH(c, "scatter_rows", k_scatter_rows<<<blocks, 256, 0, c.stream>>>(Src, comp, Dst, vec4, sub));
 }
 
 // Dst[ids[j], :] = Src[j, :] for every row j of Src (the other rows of Dst

@@ -6,11 +6,15 @@
 // the copy torch already mapped into the process, else the system one), so the
 // single-GPU library has no link-time NCCL dependency.  With nranks == 1 every
 // helper is a no-op / identity: the single-GPU path IS the distributed path
-// with one rank, which is how the GPU parity tests cover it.
+// with one rank.  A host-staged communicator (netmfp_comm_ops callbacks) can
+// stand in for NCCL: same calls at the same points, operands staged through
+// host memory — the multi-rank tests use it with several processes on one GPU
+// (no kernel ever waits on another rank's kernel).
 #include <dlfcn.h>
 #include <nccl.h>
 
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -83,15 +87,90 @@ void dist_init(Ctx &c, const void *id, int nranks, int rank) {
 void dist_destroy(Ctx &c) {
   if (c.comm) nccl().commDestroy((ncclComm_t)c.comm);
   c.comm = nullptr;
+  c.ops_on = false;
   c.nranks = 1;
   c.rank = 0;
 }
 
+static size_t dt_size(DType t) {
+  return t == DType::F32 || t == DType::I32 ? 4 : t == DType::U8 ? 1 : 8;
+}
+static int32_t dt_code(DType t) {
+  return t == DType::F32 ? NETMFP_DT_F32 : t == DType::F64 ? NETMFP_DT_F64 : t == DType::I64 ? NETMFP_DT_I64
+                                                     : t == DType::I32 ? NETMFP_DT_I32 : NETMFP_DT_U8;
+}
+static ncclDataType_t nccl_dt(DType t) {
+  return t == DType::F32 ? ncclFloat32 : t == DType::F64 ? ncclFloat64 : t == DType::I64 ? ncclInt64
+                                                 : t == DType::I32 ? ncclInt32 : ncclUint8;
+}
+
+void dist_init_ops(Ctx &c, const netmfp_comm_ops &ops, int nranks, int rank) {
+  NM_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "dist_init_ops: bad rank / nranks");
+  NM_REQUIRE(nranks == 1 || (ops.allreduce_sum && ops.broadcast), "dist_init_ops: missing callbacks");
+  dist_destroy(c);
+  c.nranks = nranks;
+  c.rank = rank;
+  c.ops = ops;
+  c.ops_on = nranks > 1;
+}
+
+static void ops_check(int rc, const char *what) {
+  if (rc != 0) throw Error(NETMFP_ERR_NCCL, std::string(what) + ": communicator callback failed");
+}
+
 void dist_allreduce(Ctx &c, void *buf, size_t count, DType t) {
   if (c.nranks == 1 || count == 0) return;
-  const ncclDataType_t dt = t == DType::F32 ? ncclFloat32 : t == DType::F64 ? ncclFloat64 : ncclInt64;
-  nccl_check(nccl().allReduce(buf, buf, count, dt, ncclSum, (ncclComm_t)c.comm, c.stream), "ncclAllReduce");
+  NM_STAGE(c, "stage_comm_allreduce");
+  const size_t bytes = count * dt_size(t);
+  c.comm_bytes += (int64_t)bytes;
   c.collectives++;
+  if (c.ops_on) {
+    std::vector<char> h(bytes);
+    NM_CUDA(cudaMemcpyAsync(h.data(), buf, bytes, cudaMemcpyDeviceToHost, c.stream));
+    NM_CUDA(cudaStreamSynchronize(c.stream));
+    ops_check(c.ops.allreduce_sum(c.ops.user, h.data(), (int64_t)count, dt_code(t)), "allreduce");
+    NM_CUDA(cudaMemcpyAsync(buf, h.data(), bytes, cudaMemcpyHostToDevice, c.stream));
+    NM_CUDA(cudaStreamSynchronize(c.stream));
+    return;
+  }
+  nccl_check(nccl().allReduce(buf, buf, count, nccl_dt(t), ncclSum, (ncclComm_t)c.comm, c.stream), "ncclAllReduce");
+}
+
+// all-gather-v of row blocks: rank r's `rows_r * row_elems` elements land at
+// out + bounds[r] * row_elems (the local block is read from `local`)
+static void gather_blocks(Ctx &c, const void *local, const std::vector<int64_t> &bounds, int64_t row_elems, DType t,
+                          void *out) {
+  const size_t es = dt_size(t);
+  const int64_t n_all = bounds[c.nranks];
+  const int64_t mine = bounds[c.rank + 1] - bounds[c.rank];
+  c.comm_bytes += (int64_t)((n_all - mine) * row_elems * es);
+  c.collectives++;
+  if (c.ops_on) {
+    std::vector<char> h((size_t)n_all * row_elems * es);
+    if (mine > 0)
+      NM_CUDA(cudaMemcpyAsync(h.data() + (size_t)bounds[c.rank] * row_elems * es, local, (size_t)mine * row_elems * es,
+                              cudaMemcpyDeviceToHost, c.stream));
+    NM_CUDA(cudaStreamSynchronize(c.stream));
+    for (int r = 0; r < c.nranks; ++r) {
+      const int64_t rows = bounds[r + 1] - bounds[r];
+      if (rows == 0) continue;
+      ops_check(c.ops.broadcast(c.ops.user, h.data() + (size_t)bounds[r] * row_elems * es, rows * row_elems,
+                                dt_code(t), r),
+                "broadcast");
+    }
+    NM_CUDA(cudaMemcpyAsync(out, h.data(), h.size(), cudaMemcpyHostToDevice, c.stream));
+    NM_CUDA(cudaStreamSynchronize(c.stream));
+    return;
+  }
+  nccl_check(nccl().groupStart(), "ncclGroupStart");
+  for (int r = 0; r < c.nranks; ++r) {
+    const int64_t rows = bounds[r + 1] - bounds[r];
+    if (rows == 0) continue;
+    nccl_check(nccl().broadcast(local, static_cast<char *>(out) + (size_t)bounds[r] * row_elems * es,
+                                (size_t)(rows * row_elems), nccl_dt(t), r, (ncclComm_t)c.comm, c.stream),
+               "ncclBroadcast");
+  }
+  nccl_check(nccl().groupEnd(), "ncclGroupEnd");
 }
 
 const float *dist_gather_rows(Ctx &c, const Graph &g, const Mat &local, DBuf<float> &scratch) {
@@ -100,19 +179,21 @@ const float *dist_gather_rows(Ctx &c, const Graph &g, const Mat &local, DBuf<flo
     return local.p;
   }
   NM_REQUIRE((int)g.bounds.size() == c.nranks + 1, "gather: graph not partitioned for this communicator");
+  NM_STAGE(c, "stage_comm_gather");
   const int64_t ld = local.ld;
   scratch.alloc((size_t)g.n_global * ld, c.stream);
-  nccl_check(nccl().groupStart(), "ncclGroupStart");
-  for (int r = 0; r < c.nranks; ++r) {
-    const int64_t rows = g.bounds[r + 1] - g.bounds[r];
-    if (rows == 0) continue;
-    nccl_check(nccl().broadcast(local.p, scratch.p + g.bounds[r] * ld, (size_t)rows * ld, ncclFloat32, r,
-                                (ncclComm_t)c.comm, c.stream),
-               "ncclBroadcast");
-  }
-  nccl_check(nccl().groupEnd(), "ncclGroupEnd");
-  c.collectives++;
+  gather_blocks(c, local.p, g.bounds, ld, DType::F32, scratch.p);
   return scratch.p;
+}
+
+void dist_allgather_i32(Ctx &c, const int32_t *local, const std::vector<int64_t> &bounds, int32_t *out) {
+  if (c.nranks == 1) {
+    if (bounds[1] > 0 && out != local)
+      NM_CUDA(cudaMemcpyAsync(out, local, (size_t)bounds[1] * 4, cudaMemcpyDeviceToDevice, c.stream));
+    return;
+  }
+  NM_STAGE(c, "stage_comm_gather");
+  gather_blocks(c, local, bounds, 1, DType::I32, out);
 }
 
 }  // namespace netmfp

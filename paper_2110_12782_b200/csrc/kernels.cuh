@@ -7,17 +7,21 @@ namespace netmfp {
 // ---- build_csr.cu
 // CSR of rows [row0, row1) (default: all rows) with global column ids; the
 // edge list must contain every edge incident to those rows.
-Graph *compact_graph(Ctx &c, const Graph &g);  // nullptr if nothing to drop
+// nullptr if nothing to drop; degall = every vertex's degree (g.deg for one rank)
+Graph *compact_graph(Ctx &c, const Graph &g, const int32_t *degall);
 void remap_rows(Ctx &c, int32_t *rows, int64_t m, const int32_t *comp);
 Graph *build_csr_device(Ctx &c, int64_t n, const int32_t *src, const int32_t *dst, int64_t m, int64_t row0 = 0,
                         int64_t row1 = -1);
 
 // ---- dist.cu
-enum class DType { F32, F64, I64 };
+enum class DType { F32, F64, I64, I32, U8 };
 void dist_unique_id(void *out);
 void dist_init(Ctx &c, const void *id, int nranks, int rank);
 void dist_destroy(Ctx &c);
+void dist_init_ops(Ctx &c, const netmfp_comm_ops &ops, int nranks, int rank);
 void dist_allreduce(Ctx &c, void *buf, size_t count, DType t);  // in place, sum
+// out[0, n_global) = every rank's local int32 vector (rank r's at bounds[r])
+void dist_allgather_i32(Ctx &c, const int32_t *local, const std::vector<int64_t> &bounds, int32_t *out);
 // full n_global × local.ld block gathered from every rank's rows (identity for one rank)
 const float *dist_gather_rows(Ctx &c, const Graph &g, const Mat &local, DBuf<float> &scratch);
 
@@ -78,7 +82,7 @@ void scale_copy_block(Ctx &c, const Mat &Src, const Mat &Dst, const int32_t *deg
 // Y[i, :] *= d_i^-e
 void row_scale_block(Ctx &c, const Mat &Y, const int32_t *deg, float rexp);
 // Dst[i, :] = Src[comp[i], :] (0 where comp[i] < 0)
-void scatter_rows(Ctx &c, const Mat &Src, const int32_t *comp, const Mat &Dst);
+void scatter_rows(Ctx &c, const Mat &Src, const int32_t *comp, const Mat &Dst, int64_t sub = 0);
 // Dst[ids[j], :] = Src[j, :] (other Dst rows untouched; Dst may be mapped host memory)
 void write_rows(Ctx &c, const Mat &Src, const int32_t *ids, const Mat &Dst);
 // copy with ld conversion (device-to-device)

@@ -203,3 +203,35 @@ def small_graph(kind: str, n: int, seed: int, **kw):
         s, t = rmat(sc, kw.get("edge_factor", 4), 0.57, 0.19, 0.19, seed)
         return 1 << sc, s, t
     raise ValueError(kind)
+
+
+def rmat_device(scale: int, edge_factor: int, a: float, b: float, c: float, seed: int, device,
+                chunk: int = 1 << 26):
+    """The R-MAT recipe of `rmat` (same quadrant rule, most significant bit
+    first, no noise, no permutation, duplicates and self loops kept) drawn on a
+    GPU with torch's generator — for the billion-edge configs[3]/[4], where
+    host numpy generation would take hours.  A different random stream than
+    `rmat`: the same graph distribution, not the same graph.  Returns int32
+    (src, dst) tensors on `device`; every rank calling it with the same seed
+    gets the same edge list."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    total = edge_factor * (1 << scale)
+    ab, abc = a + b, a + b + c
+    src = torch.empty(total, dtype=torch.int32, device=device)
+    dst = torch.empty(total, dtype=torch.int32, device=device)
+    for s0 in range(0, total, chunk):
+        cnt = min(chunk, total - s0)
+        u = torch.zeros(cnt, dtype=torch.int32, device=device)
+        v = torch.zeros(cnt, dtype=torch.int32, device=device)
+        for lvl in range(scale):
+            r = torch.rand(cnt, generator=g, device=device)
+            bit = 1 << (scale - 1 - lvl)
+            down = r >= ab
+            right = ((r >= a) & (r < ab)) | (r >= abc)
+            u |= down.to(torch.int32) * bit
+            v |= right.to(torch.int32) * bit
+        src[s0:s0 + cnt] = u
+        dst[s0:s0 + cnt] = v
+    return src, dst

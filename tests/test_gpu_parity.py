@@ -414,3 +414,31 @@ def test_dist_one_rank_is_the_single_gpu_path(L, ctx, graphs):
     L.netmfp_embed(ctx, g, prm, E1)
     L.netmfp_embed(c1, gd, prm, E2)
     assert torch.equal(E1, E2)
+
+
+@pytest.mark.parametrize("name", ["rmat_s13", "star1500"])
+def test_repeatable_on_power_law_graphs(L, ctx, graphs, name):
+    """Heavy rows (hubs split over many segments) are reduced in segment order,
+    so SpMM and the whole embedding are bitwise repeatable."""
+    n, s, t, g, (rp, col, deg) = graphs[name]
+    assert deg.max() > 128                      # several heavy segments per hub
+    X = padded(n, 286)
+    X.copy_(torch.randn(n, 286, device=DEV))
+    Y1, Y2 = padded(n, 286), padded(n, 286)
+    L.netmfp_spmm(ctx, g, 0.45, 0.45, X, Y1)
+    L.netmfp_spmm(ctx, g, 0.45, 0.45, X, Y2)
+    assert torch.equal(Y1, Y2)
+    L.netmfp_spmm(ctx, g, 0.45, 0.0, X, Y1)
+    L.netmfp_spmm(ctx, g, 0.45, 0.0, X, Y2)
+    assert torch.equal(Y1, Y2)
+    prm = L.make_params(alpha=0.45, k=32, s1=10, q=3, T=10, b=1.0, d=16, s2=16, s3=160, z=8, prop_order=10,
+                        mu=0.2, theta=0.5, seed=5, logmode=0)
+    outs = []
+    for _ in range(2):
+        E = padded(n, 16)
+        sig = torch.zeros(16, dtype=torch.float64, device=DEV)
+        lam = torch.zeros(32, dtype=torch.float64, device=DEV)
+        L.netmfp_embed(ctx, g, prm, E, sig, lam)
+        outs.append((E, sig, lam))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
