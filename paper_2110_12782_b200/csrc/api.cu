@@ -583,14 +583,14 @@ static const Graph *embed_graph(Ctx &c, const Graph &g, const netmfp_params &p) 
   }();
   if (off || g.n_orig != 0) return &g;
   const bool whole = g.row0 == 0 && g.n == g.n_global;
-  if (c.nranks == 1 && !whole) return &g;  // a row slice used without a communicator
-  if (c.nranks > 1 && (int)g.bounds.size() != c.nranks + 1) return &g;
+  if (c.nranks == 1 && !c.comm && !whole) return &g;  // a row slice used without a communicator
+  if ((c.nranks > 1 || c.comm) && (int)g.bounds.size() != c.nranks + 1) return &g;
   std::lock_guard<std::mutex> lk(g.compact_mu);
   if (!g.compact_checked) {
     NM_STAGE(c, "stage_compact");
     DBuf<int32_t> degall;
     const int32_t *da = g.deg.p;
-    if (c.nranks > 1) {
+    if (c.nranks > 1 || c.comm) {
       degall.alloc(g.n_global, c.stream);
       dist_allgather_i32(c, g.deg.p, g.bounds, degall.p);
       da = degall.p;
@@ -688,7 +688,7 @@ static void embed_impl(Ctx &c, const Graph &g_in, const netmfp_params &p, const 
 // (nothing done) when the path does not apply.
 static bool embed_host_pinned(Ctx &c, const Graph &g_in, const netmfp_params &p, float *E, int64_t lde,
                               double *sigma_dev, double *lambda_dev) {
-  if (c.nranks > 1) return false;  // partitioned: the staged copy of this rank's rows
+  if (c.nranks > 1 || c.comm) return false;  // partitioned: the staged copy of this rank's rows
   const Graph &g = *embed_graph(c, g_in, p);
   float *Edev = (&g != &g_in) ? mapped_device_ptr(E) : nullptr;
   if (!Edev) return false;

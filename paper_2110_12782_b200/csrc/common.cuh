@@ -127,6 +127,7 @@ struct Ctx {
   // row-partitioned multi-GPU (dist.cu); nranks == 1: single GPU
   int nranks = 1, rank = 0;
   void *comm = nullptr;  // ncclComm_t
+  cudaStream_t comm_stream = nullptr;  // NCCL stream (overlaps all-gathers with SpMM passes)
   netmfp_comm_ops ops{};  // host-staged communicator (netmfp_dist_init_ops) when ops_on
   bool ops_on = false;
   int64_t collectives = 0;

@@ -13,6 +13,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -75,18 +76,28 @@ void dist_init(Ctx &c, const void *id, int nranks, int rank) {
   dist_destroy(c);
   c.nranks = nranks;
   c.rank = rank;
-  if (nranks == 1) return;
+  // one rank: no communicator (every helper is the identity) unless
+  // NETMFP_DIST_FORCE_COMM=1 — then the NCCL path runs with one rank (its
+  // collectives are copies), which the single-GPU tests use to execute it
+  const char *fc = getenv("NETMFP_DIST_FORCE_COMM");
+  if (nranks == 1 && !(fc && atoi(fc))) return;
   ncclUniqueId uid;
   std::memcpy(&uid, id, sizeof(uid));
   ncclComm_t comm;
   NM_CUDA(cudaSetDevice(c.device));
   nccl_check(nccl().commInitRank(&comm, nranks, uid, rank), "ncclCommInitRank");
   c.comm = comm;
+  NM_CUDA(cudaStreamCreateWithFlags(&c.comm_stream, cudaStreamNonBlocking));
 }
 
 void dist_destroy(Ctx &c) {
   if (c.comm) nccl().commDestroy((ncclComm_t)c.comm);
   c.comm = nullptr;
+  if (c.comm_stream) {
+    cudaStreamSynchronize(c.comm_stream);
+    cudaStreamDestroy(c.comm_stream);
+  }
+  c.comm_stream = nullptr;
   c.ops_on = false;
   c.nranks = 1;
   c.rank = 0;
@@ -118,8 +129,10 @@ static void ops_check(int rc, const char *what) {
   if (rc != 0) throw Error(NETMFP_ERR_NCCL, std::string(what) + ": communicator callback failed");
 }
 
+static bool dist_active(const Ctx &c) { return c.nranks > 1 || c.comm != nullptr; }
+
 void dist_allreduce(Ctx &c, void *buf, size_t count, DType t) {
-  if (c.nranks == 1 || count == 0) return;
+  if (!dist_active(c) || count == 0) return;
   NM_STAGE(c, "stage_comm_allreduce");
   const size_t bytes = count * dt_size(t);
   c.comm_bytes += (int64_t)bytes;
@@ -174,7 +187,7 @@ static void gather_blocks(Ctx &c, const void *local, const std::vector<int64_t> 
 }
 
 const float *dist_gather_rows(Ctx &c, const Graph &g, const Mat &local, DBuf<float> &scratch) {
-  if (c.nranks == 1) {
+  if (!dist_active(c)) {
     NM_REQUIRE(g.n == g.n_global, "partitioned graph used without a communicator (netmfp_dist_init)");
     return local.p;
   }
@@ -186,8 +199,99 @@ const float *dist_gather_rows(Ctx &c, const Graph &g, const Mat &local, DBuf<flo
   return scratch.p;
 }
 
+void dist_spmm(Ctx &c, const Graph &g, const Mat &local, const SpmmArgs &p, DBuf<float> &scratch) {
+  if (!dist_active(c)) {
+    NM_REQUIRE(g.n == g.n_global, "partitioned graph used without a communicator (netmfp_dist_init)");
+    SpmmArgs q = p;
+    q.X = local.p;
+    q.ldx = local.ld;
+    spmm(c, g, q);
+    return;
+  }
+  NM_REQUIRE((int)g.bounds.size() == c.nranks + 1, "gather: graph not partitioned for this communicator");
+  if (c.ops_on) {  // host-staged: whole block, then the SpMM
+    SpmmArgs q = p;
+    q.X = dist_gather_rows(c, g, local, scratch);
+    q.ldx = local.ld;
+    spmm(c, g, q);
+    return;
+  }
+  // NCCL: column slices of <= 128 (the SpMM's pass width), each packed
+  // contiguous (n_local x ld_j) and broadcast from every rank into its own
+  // n_global x ld_j buffer on the communicator's stream; the compute stream
+  // waits for slice j only before pass j, so slice j+1 crosses NVLink while
+  // pass j gathers.
+  const int64_t cols = p.cols, nl = g.n, ng = g.n_global;
+  std::vector<int64_t> c0s, ws, lds, offs;
+  int64_t tot = 0;
+  for (int64_t c0 = 0; c0 < cols; c0 += 128) {
+    const int64_t w = std::min<int64_t>(128, cols - c0), ldj = pad4(w);
+    c0s.push_back(c0);
+    ws.push_back(w);
+    lds.push_back(ldj);
+    offs.push_back(tot);
+    tot += (ng + nl) * ldj;
+  }
+  const size_t nsl = c0s.size();
+  scratch.alloc((size_t)tot, c.stream);
+  for (size_t j = 0; j < nsl; ++j) {
+    float *send = scratch.p + offs[j] + ng * lds[j];
+    if (nl > 0)
+      NM_CUDA(cudaMemcpy2DAsync(send, lds[j] * 4, local.p + c0s[j], local.ld * 4, ws[j] * 4, nl,
+                                cudaMemcpyDeviceToDevice, c.stream));
+  }
+  cudaEvent_t packed;
+  NM_CUDA(cudaEventCreateWithFlags(&packed, cudaEventDisableTiming));
+  NM_CUDA(cudaEventRecord(packed, c.stream));
+  NM_CUDA(cudaStreamWaitEvent(c.comm_stream, packed, 0));
+  cudaEventDestroy(packed);
+  std::vector<cudaEvent_t> arrived(nsl);
+  const bool prof = c.prof && prof_match(c, "stage_comm_gather");
+  for (size_t j = 0; j < nsl; ++j) {
+    cudaEvent_t pa = nullptr, pb = nullptr;
+    if (prof) {
+      pa = prof_event(c);
+      cudaEventRecord(pa, c.comm_stream);
+    }
+    const float *send = scratch.p + offs[j] + ng * lds[j];
+    float *recv = scratch.p + offs[j];
+    nccl_check(nccl().groupStart(), "ncclGroupStart");
+    for (int r = 0; r < c.nranks; ++r) {
+      const int64_t rows = g.bounds[r + 1] - g.bounds[r];
+      if (rows == 0) continue;
+      nccl_check(nccl().broadcast(send, recv + g.bounds[r] * lds[j], (size_t)(rows * lds[j]), ncclFloat32, r,
+                                  (ncclComm_t)c.comm, c.comm_stream),
+                 "ncclBroadcast");
+    }
+    nccl_check(nccl().groupEnd(), "ncclGroupEnd");
+    if (prof) {
+      pb = prof_event(c);
+      cudaEventRecord(pb, c.comm_stream);
+      c.pending.push_back({pa, pb, "stage_comm_gather"});
+    }
+    NM_CUDA(cudaEventCreateWithFlags(&arrived[j], cudaEventDisableTiming));
+    NM_CUDA(cudaEventRecord(arrived[j], c.comm_stream));
+    c.comm_bytes += (ng - nl) * lds[j] * 4;
+    c.collectives++;
+  }
+  for (size_t j = 0; j < nsl; ++j) {
+    NM_CUDA(cudaStreamWaitEvent(c.stream, arrived[j], 0));
+    cudaEventDestroy(arrived[j]);
+    SpmmArgs q = p;
+    const int64_t c0 = c0s[j];
+    q.X = scratch.p + offs[j];
+    q.ldx = lds[j];
+    q.cols = ws[j];
+    if (q.Y) q.Y += c0;
+    if (q.prev) q.prev += c0;
+    if (q.acc_in) q.acc_in += c0;
+    if (q.acc_out) q.acc_out += c0;
+    spmm(c, g, q);
+  }
+}
+
 void dist_allgather_i32(Ctx &c, const int32_t *local, const std::vector<int64_t> &bounds, int32_t *out) {
-  if (c.nranks == 1) {
+  if (!dist_active(c)) {
     if (bounds[1] > 0 && out != local)
       NM_CUDA(cudaMemcpyAsync(out, local, (size_t)bounds[1] * 4, cudaMemcpyDeviceToDevice, c.stream));
     return;

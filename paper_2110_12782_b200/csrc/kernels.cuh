@@ -48,6 +48,11 @@ struct SpmmArgs {
   int heavy_seg = kHeavySegDefault;
 };
 void spmm(Ctx &c, const Graph &g, const SpmmArgs &p);
+// SpMM of a row-partitioned block: `local` is this rank's rows of X; the
+// input rows of every rank are all-gathered (NCCL: by column slices on the
+// communicator's stream, each slice's SpMM pass starting as soon as its rows
+// arrived, overlapping the next slice's transfer).  One rank: spmm on local.
+void dist_spmm(Ctx &c, const Graph &g, const Mat &local, const SpmmArgs &p, DBuf<float> &scratch);
 void deg_pow(Ctx &c, const Graph &g, float e, float *out);  // out[i] = d_i^-e (0 if d_i = 0)
 
 // ---- dense.cu (tall-skinny fp32 blocks, fp64 small results)

@@ -61,28 +61,28 @@ void freigs(Ctx &c, const Graph &g, double alpha, int k, int s1, int q, uint64_t
   gaussian_block(c, P.m, seed, g.deg, a, g.row0, g.orig_id.p);  // P = D^-α Ω (this rank's rows)
   SpmmArgs sp;
   sp.cols = l;
-  sp.X = dist_gather_rows(c, g, P.m, xfull); sp.ldx = P.m.ld; sp.Y = Y.m.p; sp.ldy = Y.m.ld; sp.a = a;
-  spmm(c, g, sp);
+  sp.Y = Y.m.p; sp.ldy = Y.m.ld; sp.a = a;
+  dist_spmm(c, g, P.m, sp, xfull);
   // step 3: Q = orth(Y)
   cholqr(c, Y.m, P.m, g.deg, a, q == 0 ? 2 : 1, &T.m, q == 0);
   // steps 4-6: Q = orth(X X Q)
   for (int it = 0; it < q; ++it) {
     SpmmArgs s1a;
     s1a.cols = l;
-    s1a.X = dist_gather_rows(c, g, P.m, xfull); s1a.ldx = P.m.ld; s1a.Y = T.m.p; s1a.ldy = T.m.ld; s1a.a = 2.f * a;
-    spmm(c, g, s1a);  // T = D^-2α A P = D^-α (X Q)
+    s1a.Y = T.m.p; s1a.ldy = T.m.ld; s1a.a = 2.f * a;
+    dist_spmm(c, g, P.m, s1a, xfull);  // T = D^-2α A P = D^-α (X Q)
     SpmmArgs s2a;
     s2a.cols = l;
-    s2a.X = dist_gather_rows(c, g, T.m, xfull); s2a.ldx = T.m.ld; s2a.Y = Y.m.p; s2a.ldy = Y.m.ld; s2a.a = a;
-    spmm(c, g, s2a);  // Y = D^-α A T = X X Q
+    s2a.Y = Y.m.p; s2a.ldy = Y.m.ld; s2a.a = a;
+    dist_spmm(c, g, T.m, s2a, xfull);  // Y = D^-α A T = X X Q
     cholqr(c, Y.m, P.m, g.deg, a, it + 1 == q ? 2 : 1, &T.m, it + 1 == q);
   }
   check_flag(c, "freigs orthonormalisation");
   // step 7: S = Qᵀ X Q = Pᵀ A P
   SpmmArgs s3;
   s3.cols = l;
-  s3.X = dist_gather_rows(c, g, P.m, xfull); s3.ldx = P.m.ld; s3.Y = T.m.p; s3.ldy = T.m.ld; s3.a = 0.f;
-  spmm(c, g, s3);
+  s3.Y = T.m.p; s3.ldy = T.m.ld; s3.a = 0.f;
+  dist_spmm(c, g, P.m, s3, xfull);
   xfull.release();
   DBuf<double> S((size_t)l * l, s), lam(l, s), V((size_t)l * l, s);
   gram(c, P.m, T.m, nullptr, 0.f, S, l);
@@ -284,8 +284,7 @@ void propagate(Ctx &c, const Graph &g, const Mat &E, int order, double mu, doubl
   auto step = [&](const Mat &X, double coef, const Mat *prev, double beta, double sE, const Mat &out) {
     SpmmArgs a;
     a.cols = d;
-    a.X = dist_gather_rows(c, g, X, xfull);
-    a.ldx = X.ld;
+
     a.Y = nullptr;
     a.a = 1.f;
     a.coef = (float)coef;
@@ -300,7 +299,7 @@ void propagate(Ctx &c, const Graph &g, const Mat &E, int order, double mu, doubl
     a.gamma = 1.f;
     a.acc_out = out.p;
     a.ldacc = out.ld;
-    spmm(c, g, a);
+    dist_spmm(c, g, X, a, xfull);
   };
   if (N == 1) {  // c0 E + c1 L~ E: E is gathered, so the result goes through a scratch block
     step(E, -cf[1], nullptr, 0.0, cf[0], B0.m);

@@ -48,12 +48,13 @@ int main() {
     printf("table %7.1f MB  ILP %2d blocks/SM %d: %.2f TB/s %s\n", rows * 512.0 / 1e6, ilp, bps, bytes / ms / 1e9,
            cudaGetErrorString(cudaGetLastError()));
   };
-  for (uint32_t rows : {1u << 16, 406727u}) {
-    for (int bps : {2, 4, 8}) {
-      run(k_gather<4>, 4, rows, bps);
-      run(k_gather<8>, 8, rows, bps);
-      run(k_gather<16>, 16, rows, bps);
-    }
+  // table sizes of profiles/r01_gather_roofline.txt (8.4 MB .. 537 MB; 406727 rows =
+  // one 128-column pass of configs[2]'s compacted X), then the ILP sweep at 208 MB
+  for (uint32_t rows : {16384u, 65536u, 131072u, 200000u, 262144u, 406727u, 1048576u})
+    for (int bps : {4, 8}) run(k_gather<4>, 4, rows, bps);
+  for (int bps : {2, 4, 8}) {
+    run(k_gather<8>, 8, 406727u, bps);
+    run(k_gather<16>, 16, 406727u, bps);
   }
   return 0;
 }

@@ -21,7 +21,7 @@
     }                                                                                  \
   } while (0)
 
-enum : int { H_COL = 1, H_Y = 2, H_X = 4, H_DET = 8 };
+enum : int { H_COL = 1, H_Y = 2, H_X = 4, H_DET = 8, H_NACOL = 16, H_NAX = 32, H_U8 = 64 };
 
 struct G {
   const int64_t *rowptr;
@@ -60,6 +60,11 @@ __device__ __forceinline__ int32_t ldcol(const int32_t *p, uint64_t pf) {
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pf));
     return v;
   }
+  if (HINT & H_NACOL) {
+    int32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+  }
   return __ldg(p);
 }
 // gather of one neighbour row slice: hot -> evict_last, cold -> L1 no_allocate + evict_first
@@ -75,6 +80,12 @@ __device__ __forceinline__ float4 ldx(const float *Xc, uint32_t v, uint32_t ld, 
     else
       asm volatile("ld.global.nc.L1::evict_last.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                    : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(pl));
+    return r;
+  }
+  if (HINT & H_NAX) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(Xc + (uint64_t)(v & 0x7fffffffu) * ld));
     return r;
   }
   return __ldg(reinterpret_cast<const float4 *>(Xc + (uint64_t)(v & 0x7fffffffu) * ld));
@@ -96,6 +107,17 @@ __device__ __forceinline__ float4 gsum(const int32_t *col, int64_t e0, int64_t e
   float4 acc = make_float4(0, 0, 0, 0);
   const int32_t *cp = col + e0;
   int cnt = (int)(e1 - e0);
+  if (HINT & H_U8) {
+    for (; cnt >= 8; cnt -= 8, cp += 8) {
+      uint32_t v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = ldcol<HINT>(cp + q, pf);
+      float4 x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = ldx<HINT>(Xc, v[q], ld, pf, pl);
+      acc = add4(add4(add4(add4(x[0], x[1]), add4(x[2], x[3])), add4(add4(x[4], x[5]), add4(x[6], x[7]))), acc);
+    }
+  }
   for (; cnt >= 4; cnt -= 4, cp += 4) {
     const uint32_t v0 = ldcol<HINT>(cp, pf), v1 = ldcol<HINT>(cp + 1, pf), v2 = ldcol<HINT>(cp + 2, pf),
                    v3 = ldcol<HINT>(cp + 3, pf);
@@ -793,6 +815,19 @@ int main(int argc, char **argv) {
   run("ref (atomic, no hints) 2x128", k_lab<32, 0>, 32, 2, 256, true, 3);
   run("ref tail 30 (LPR 8)", k_lab<8, 0>, 8, 1, 286, true, 3, 256);
   CK(cudaMemcpy(hr.data(), Yref, n * 288 * 4, cudaMemcpyDeviceToHost));
+  run("plain 2x128", k_lab<32, 0>, 32, 2, 256, false);
+  run("det 2x128", k_lab<32, H_DET>, 32, 2, 256, false);
+  run("det U8 2x128 minb8", k_lab<32, H_DET | H_U8>, 32, 2, 256, false);
+  run("det U8 2x128 minb6", k_lab<32, H_DET | H_U8, 6>, 32, 2, 256, false);
+  run("det U8 2x128 minb5", k_lab<32, H_DET | H_U8, 5>, 32, 2, 256, false);
+  run("det nacol 2x128", k_lab<32, H_DET | H_NACOL>, 32, 2, 256, false);
+  run("det nax 2x128", k_lab<32, H_DET | H_NAX>, 32, 2, 256, false);
+  run("det nacol+nax 2x128", k_lab<32, H_DET | H_NACOL | H_NAX>, 32, 2, 256, false);
+  run("det U8 nacol 2x128 minb6", k_lab<32, H_DET | H_U8 | H_NACOL, 6>, 32, 2, 256, false);
+  if (!getenv("LAB_ALL")) {
+    printf("done\n");
+    return 0;
+  }
   run("tail 30 (LPR 8)", k_lab<8, 0>, 8, 1, 286, false, 10, 256, 0, true);
   run("tail 30 (LPR 8) det", k_lab<8, H_DET>, 8, 1, 286, false, 10, 256, 0, true);
 

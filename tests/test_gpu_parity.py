@@ -442,3 +442,29 @@ def test_repeatable_on_power_law_graphs(L, ctx, graphs, name):
         outs.append((E, sig, lam))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+def test_dist_nccl_path_with_one_rank(L, ctx, graphs):
+    """The NCCL code path itself (per-slice all-gathers on the communicator's
+    stream overlapping the SpMM passes, all-reduces, degree all-gather and
+    compaction of the partition) executed with a one-rank communicator
+    (NETMFP_DIST_FORCE_COMM=1): bitwise the single-GPU result."""
+    import os
+    n, s, t, g, (rp, col, deg) = graphs["rmat_s13"]
+    os.environ["NETMFP_DIST_FORCE_COMM"] = "1"
+    try:
+        c1 = L.Context(0)
+        L.netmfp_dist_init(c1, L.netmfp_dist_unique_id(), 1, 0)
+    finally:
+        del os.environ["NETMFP_DIST_FORCE_COMM"]
+    gd = L.netmfp_dist_build_csr(c1, n, dev(s), dev(t))
+    prm = L.make_params(alpha=0.45, k=40, s1=16, q=2, T=10, b=1.0, d=24, s2=24, s3=150, z=8, prop_order=6,
+                        mu=0.2, theta=0.5, seed=3, logmode=0)
+    E1, E2 = padded(n, 24), padded(n, 24)
+    s1, s2 = torch.zeros(24, dtype=torch.float64, device=DEV), torch.zeros(24, dtype=torch.float64, device=DEV)
+    L.netmfp_embed(ctx, g, prm, E1, s1)
+    L.netmfp_dist_stats(c1)
+    L.netmfp_embed(c1, gd, prm, E2, s2)
+    nbytes, ncoll = L.netmfp_dist_stats(c1)
+    assert ncoll > 0                      # the collectives were issued
+    assert torch.equal(s1, s2) and torch.equal(E1, E2)
