@@ -51,9 +51,9 @@ def load_peaks():
 
 def gather_roofline(achieved_tbps):
     """Achieved neighbour-row gather throughput vs the measured random-gather
-    peaks (profiles/r01_traffic.json, from scripts/dbg/gather_bench.cu)."""
+    peaks (profiles/r02_traffic.json, from scripts/dbg/gather_bench.cu)."""
     out = {"achieved_TBps": achieved_tbps, "unit": "TB/s (gathered X bytes: 4 * nnz * cols per SpMM)"}
-    tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "r02_traffic.json")
     if os.path.exists(tp):
         gr = json.load(open(tp)).get("gather_roofline", {})
         if gr:

@@ -197,9 +197,9 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
       NM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys.p, keys2.p, nk, 0, end_bit, s));
       NM_CUDA(cub::DeviceSelect::Unique(nullptr, tmp2, keys2.p, keys.p, nsel.p, nk, s));
       DBuf<char> tmp(std::max(tmp_bytes, tmp2), s);
-      NM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, keys.p, keys2.p, nk, 0, end_bit, s));
+      NM_PROF(c, "cub_radix_sort", NM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, keys.p, keys2.p, nk, 0, end_bit, s)));
       c.launches += 4;
-      NM_CUDA(cub::DeviceSelect::Unique(tmp.p, tmp2, keys2.p, keys.p, nsel.p, nk, s));
+      NM_PROF(c, "cub_unique", NM_CUDA(cub::DeviceSelect::Unique(tmp.p, tmp2, keys2.p, keys.p, nsel.p, nk, s)));
       c.launches += 2;
     } else {
       nsel.zero();

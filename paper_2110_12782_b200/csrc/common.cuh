@@ -267,6 +267,24 @@ struct StageScope {
 #define NM_STAGE_CAT(a, b) NM_STAGE_CAT2(a, b)
 #define NM_STAGE(c, name) ::netmfp::StageScope NM_STAGE_CAT(_stage_, __LINE__)(c, name)
 
+// a library call that launches kernels itself (CUB): profiled like one of
+// ours (per-kernel stats, so it is not counted as an idle gap); the caller
+// adds its kernel count to c.launches
+inline void prof_end(Ctx &c) {
+  if (c.cur_name) {
+    cudaEvent_t b = prof_event(c);
+    cudaEventRecord(b, c.stream);
+    c.pending.push_back({c.cur_a, b, c.cur_name});
+    c.cur_name = nullptr;
+  }
+}
+#define NM_PROF(c, name, ...)      \
+  do {                             \
+    ::netmfp::prof_begin(c, name); \
+    __VA_ARGS__;                   \
+    ::netmfp::prof_end(c);         \
+  } while (0)
+
 #define NM_LAUNCH(c, name, ...)   \
   do {                            \
     ::netmfp::prof_begin(c, name); \
