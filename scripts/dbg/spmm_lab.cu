@@ -21,7 +21,7 @@
     }                                                                                  \
   } while (0)
 
-enum : int { H_COL = 1, H_Y = 2, H_X = 4, H_DET = 8, H_NACOL = 16, H_NAX = 32, H_U8 = 64 };
+enum : int { H_COL = 1, H_Y = 2, H_X = 4, H_DET = 8, H_NACOL = 16, H_NAX = 32, H_U8 = 64, H_COOP = 128, H_COOP8 = 256 };
 
 struct G {
   const int64_t *rowptr;
@@ -100,6 +100,33 @@ __device__ __forceinline__ void sty(float *p, float4 v, uint64_t pf) {
 }
 __device__ __forceinline__ float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
 __device__ __forceinline__ float rsc(int d, float a) { return d > 0 ? exp2f(-a * __log2f((float)d)) : 0.f; }
+
+// heavy segment, whole warp: indices loaded coalesced (32 per load), broadcast by shuffle
+template <int U>
+__device__ __forceinline__ float4 gsum_coop(const int32_t *col, int64_t e0, int64_t e1, const float *Xc, uint32_t ld) {
+  const int lane = threadIdx.x & 31;
+  float4 acc = make_float4(0, 0, 0, 0);
+  for (int64_t wb = e0; wb < e1; wb += 32) {
+    const int cnt = (int)min((int64_t)32, e1 - wb);
+    const uint32_t myidx = lane < cnt ? __ldg(col + wb + lane) : 0u;
+    int j = 0;
+    for (; j + U <= cnt; j += U) {
+      float4 x[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const uint32_t v = __shfl_sync(0xffffffffu, myidx, j + q);
+        x[q] = __ldg(reinterpret_cast<const float4 *>(Xc + (uint64_t)v * ld));
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) acc = add4(acc, x[q]);
+    }
+    for (; j < cnt; ++j) {
+      const uint32_t v = __shfl_sync(0xffffffffu, myidx, j);
+      acc = add4(acc, __ldg(reinterpret_cast<const float4 *>(Xc + (uint64_t)v * ld)));
+    }
+  }
+  return acc;
+}
 
 template <int HINT>
 __device__ __forceinline__ float4 gsum(const int32_t *col, int64_t e0, int64_t e1, const float *Xc, uint32_t ld,
@@ -212,7 +239,11 @@ __global__ void __launch_bounds__(256, MINB) k_lab(G g, int nblk_heavy) {
   float *dst = (HINT & H_DET) ? g.segsum + ((int64_t)py * g.nsegs + sidx) * pw + li * 4
                               : g.hsum + ((int64_t)py * 1 + 0) * 0 + h * 288 + c;
   const bool act = c < g.cols;
-  const float4 acc = act ? gsum<HINT>(col, e0, e1, Xc, ld, pf, pl) : make_float4(0, 0, 0, 0);
+  float4 acc;
+  if ((HINT & (H_COOP | H_COOP8)) && LPR == 32)
+    acc = (HINT & H_COOP8) ? gsum_coop<8>(col, e0, e1, Xc, ld) : gsum_coop<4>(col, e0, e1, Xc, ld);
+  else
+    acc = act ? gsum<HINT>(col, e0, e1, Xc, ld, pf, pl) : make_float4(0, 0, 0, 0);
   if (HINT & H_DET)
     __stcg(reinterpret_cast<float4 *>(dst), acc);
   else if (act)
@@ -690,6 +721,75 @@ __global__ void __launch_bounds__(256, MINB) k_async(G g, int nblk_heavy, int64_
   if (lane == 0) *cntp = 0;
 }
 
+
+// ---------------------------------------------------------------- gather-only ceiling
+// The exact access stream of one 128-column pass (every nonzero's neighbour
+// row slice, in CSR order) with nothing else: each warp takes a contiguous
+// chunk of the col array, loads 32 indices coalesced, and gathers the rows
+// U at a time (indices by shuffle), summing them; no row boundaries, no
+// epilogue, no Y writes.  An upper bound for any SpMM pass on this layout.
+template <int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_gather_ceiling(const int32_t *__restrict__ col, int64_t nnz,
+                                                               const float *__restrict__ X, uint32_t ld, int64_t chunk,
+                                                               float *__restrict__ sink) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t e0 = w * chunk, e1 = min(nnz, e0 + chunk);
+  const float *Xc = X + blockIdx.y * 128 + lane * 4;
+  float4 acc = make_float4(0, 0, 0, 0);
+  for (int64_t wb = e0; wb < e1; wb += 32) {
+    const int cnt = (int)min((int64_t)32, e1 - wb);
+    const uint32_t myidx = lane < cnt ? __ldg(col + wb + lane) : 0u;
+    for (int j = 0; j < cnt; j += U) {
+      float4 x[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const uint32_t v = __shfl_sync(0xffffffffu, myidx, (j + q) & 31);
+        x[q] = (j + q < cnt) ? __ldg(reinterpret_cast<const float4 *>(Xc + (uint64_t)v * ld)) : make_float4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) acc = add4(acc, x[q]);
+    }
+  }
+  if (acc.x == 1234.5f) sink[0] = acc.y;
+}
+
+
+// ---------------------------------------------------------------- split: heavy-only kernel (coalesced indices)
+template <int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_heavy_coop(G g) {
+  const int py = blockIdx.y, lane = threadIdx.x & 31;
+  const int64_t sidx = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (sidx >= g.nsegs) return;
+  const int c = py * 128 + lane * 4;
+  const float *Xc = g.X + c;
+  const int64_t h = __ldg(g.seg_h + sidx);
+  const int64_t e0 = __ldg(g.seg_e0 + sidx);
+  const int64_t u = __ldg(g.heavy + h);
+  const int64_t rb = __ldg(g.rowptr + u), re = __ldg(g.rowptr + u + 1);
+  const int64_t e1 = min(e0 + (int64_t)g.heavy_seg, re);
+  const float4 acc = gsum_coop<U>(g.col, e0, e1, Xc, (uint32_t)g.ldx);
+  float *dst = g.segsum + ((int64_t)py * g.nsegs + sidx) * 128 + lane * 4;
+  __stcg(reinterpret_cast<float4 *>(dst), acc);
+  __syncwarp();
+  const int64_t s0 = __ldg(g.seg_ptr + h), s1 = __ldg(g.seg_ptr + h + 1);
+  int32_t *cntp = g.hcnt + h * 4 + py;
+  int last = 0;
+  if (lane == 0) {
+    __threadfence();
+    last = atomicAdd(cntp, 1) == (int)(s1 - s0) - 1;
+    if (last) __threadfence();
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  const float *sp = g.segsum + ((int64_t)py * g.nsegs + s0) * 128 + lane * 4;
+  float4 tot = make_float4(0, 0, 0, 0);
+  for (int64_t j = 0; j < s1 - s0; ++j) tot = add4(tot, __ldcg(reinterpret_cast<const float4 *>(sp + j * 128)));
+  const float sr = rsc((int)(re - rb), g.a);
+  *reinterpret_cast<float4 *>(g.Y + u * g.ldx + c) = make_float4(sr * tot.x, sr * tot.y, sr * tot.z, sr * tot.w);
+  if (lane == 0) *cntp = 0;
+}
+
 __global__ void k_init(float *x, int64_t n) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) {
@@ -817,6 +917,10 @@ int main(int argc, char **argv) {
   CK(cudaMemcpy(hr.data(), Yref, n * 288 * 4, cudaMemcpyDeviceToHost));
   run("plain 2x128", k_lab<32, 0>, 32, 2, 256, false);
   run("det 2x128", k_lab<32, H_DET>, 32, 2, 256, false);
+  run("det coop4 2x128", k_lab<32, H_DET | H_COOP>, 32, 2, 256, false);
+  run("det coop8 2x128", k_lab<32, H_DET | H_COOP8>, 32, 2, 256, false);
+  run("det coop8 2x128 minb6", k_lab<32, H_DET | H_COOP8, 6>, 32, 2, 256, false);
+  run("det coop4 2x128 minb6", k_lab<32, H_DET | H_COOP, 6>, 32, 2, 256, false);
   run("det U8 2x128 minb8", k_lab<32, H_DET | H_U8>, 32, 2, 256, false);
   run("det U8 2x128 minb6", k_lab<32, H_DET | H_U8, 6>, 32, 2, 256, false);
   run("det U8 2x128 minb5", k_lab<32, H_DET | H_U8, 5>, 32, 2, 256, false);
@@ -824,6 +928,132 @@ int main(int argc, char **argv) {
   run("det nax 2x128", k_lab<32, H_DET | H_NAX>, 32, 2, 256, false);
   run("det nacol+nax 2x128", k_lab<32, H_DET | H_NACOL | H_NAX>, 32, 2, 256, false);
   run("det U8 nacol 2x128 minb6", k_lab<32, H_DET | H_U8 | H_NACOL, 6>, 32, 2, 256, false);
+  {
+    float *sink;
+    CK(cudaMalloc(&sink, 16));
+    auto runc = [&](const char *name, auto kern, int wpsm) {
+      // one warp per chunk, wpsm resident warps per SM
+      const int64_t nwarps = (int64_t)num_sms * wpsm;
+      const int64_t chunk = (nnz + nwarps - 1) / nwarps;
+      dim3 grid((unsigned)((nwarps + 7) / 8), 2);
+      std::vector<float> ts;
+      for (int r = 0; r < 10; ++r) {
+        CK(cudaMemset(flush, r, 512 << 20));
+        cudaEventRecord(e0);
+        kern<<<grid, 256>>>(g.col, nnz, X, 288u, chunk, sink);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ts.push_back(ms);
+      }
+      CK(cudaGetLastError());
+      std::sort(ts.begin(), ts.end());
+      printf("%-34s cols=256  med %.4f ms  min %.4f  gather %.2f TB/s\n", name, ts[5], ts[0],
+             4.0 * nnz * 256 / (ts[5] * 1e-3) / 1e12);
+      fflush(stdout);
+    };
+    runc("ceiling U4 64 warps/SM", k_gather_ceiling<4, 8>, 64);
+    runc("ceiling U8 64 warps/SM", k_gather_ceiling<8, 8>, 64);
+    runc("ceiling U8 48 warps/SM", k_gather_ceiling<8, 6>, 48);
+    runc("ceiling U16 32 warps/SM", k_gather_ceiling<16, 4>, 32);
+    runc("ceiling U4 32 warps/SM", k_gather_ceiling<4, 8>, 32);
+  }
+  {
+    cudaStream_t s2;
+    CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    cudaEvent_t ea, eb;
+    cudaEventCreate(&ea);
+    cudaEventCreate(&eb);
+    // light tiles only (k_lab with no heavy blocks), heavy segments only, both concurrently
+    auto runsplit = [&](const char *name, auto hkern, int mode, int reps = 10) {
+      G gg = g;
+      gg.Y = Y;
+      gg.cols = 256;
+      gg.colbase = 0;
+      const int64_t ntiles = (n + 31) / 32;
+      gg.nblk_tile = (int)std::min<int64_t>((ntiles + 7) / 8, (int64_t)num_sms * 32);
+      const int nbh = (int)((nsegs + 7) / 8);
+      std::vector<float> ts;
+      for (int r = 0; r < reps; ++r) {
+        CK(cudaMemset(flush, r, 512 << 20));
+        cudaEventRecord(e0);
+        cudaEventRecord(ea);
+        CK(cudaStreamWaitEvent(s2, ea, 0));
+        if (mode & 1) k_lab<32, H_DET><<<dim3(gg.nblk_tile, 2), 256>>>(gg, 0);
+        if (mode & 2) hkern<<<dim3(nbh, 2), 256, 0, s2>>>(gg);
+        cudaEventRecord(eb, s2);
+        CK(cudaStreamWaitEvent(0, eb, 0));
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ts.push_back(ms);
+      }
+      CK(cudaGetLastError());
+      std::sort(ts.begin(), ts.end());
+      double err = 0, mx = 0;
+      if (mode == 3) {
+        CK(cudaMemcpy(hy.data(), Y, n * 288 * 4, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; ++i)
+          for (int c = 0; c < 256; ++c) {
+            err = std::max(err, (double)fabsf(hy[i * 288 + c] - hr[i * 288 + c]));
+            mx = std::max(mx, (double)fabsf(hr[i * 288 + c]));
+          }
+      }
+      printf("%-34s cols=256  med %.4f ms  min %.4f  err %.2e/%.2e\n", name, ts[reps / 2], ts[0], err, mx);
+      fflush(stdout);
+    };
+    runsplit("light tiles only", k_heavy_coop<4, 8>, 1);
+    {
+      auto lightonly = [&](const char *name, auto kern) {
+        G gg = g; gg.Y = Y; gg.cols = 256;
+        const int64_t ntiles = (n + 31) / 32;
+        gg.nblk_tile = (int)std::min<int64_t>((ntiles + 7) / 8, (int64_t)num_sms * 32);
+        std::vector<float> ts;
+        for (int r = 0; r < 10; ++r) {
+          CK(cudaMemset(flush, r, 512 << 20));
+          cudaEventRecord(e0);
+          kern<<<dim3(gg.nblk_tile, 2), 256>>>(gg, 0);
+          cudaEventRecord(e1);
+          CK(cudaEventSynchronize(e1));
+          float ms;
+          cudaEventElapsedTime(&ms, e0, e1);
+          ts.push_back(ms);
+        }
+        CK(cudaGetLastError());
+        std::sort(ts.begin(), ts.end());
+        printf("%-34s cols=256  med %.4f ms\n", name, ts[5]);
+      };
+      lightonly("light v2 U4 minb8", k_v2<4, 8>);
+      lightonly("light v2 U4 minb6", k_v2<4, 6>);
+      lightonly("light v2 U8 minb4", k_v2<8, 4>);
+      lightonly("light v2 U8 minb5", k_v2<8, 5>);
+      lightonly("light plain minb6", k_lab<32, H_DET, 6>);
+    }
+    runsplit("heavy plain only (k_lab)", k_heavy_coop<4, 8>, 0);
+    runsplit("heavy coop4 only", k_heavy_coop<4, 8>, 2);
+    runsplit("heavy coop8 only minb6", k_heavy_coop<8, 6>, 2);
+    runsplit("split light + coop4 (2 streams)", k_heavy_coop<4, 8>, 3);
+    runsplit("split light + coop8 minb6", k_heavy_coop<8, 6>, 3);
+    {
+      G gg = g; gg.Y = Y; gg.cols = 256; gg.nblk_tile = 0;
+      const int nbh = (int)((nsegs + 7) / 8);
+      std::vector<float> ts;
+      for (int r = 0; r < 10; ++r) {
+        CK(cudaMemset(flush, r, 512 << 20));
+        cudaEventRecord(e0);
+        k_lab<32, H_DET><<<dim3(nbh, 2), 256>>>(gg, nbh);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ts.push_back(ms);
+      }
+      std::sort(ts.begin(), ts.end());
+      printf("%-34s cols=256  med %.4f ms\n", "heavy plain only (k_lab segs)", ts[5]);
+    }
+  }
   if (!getenv("LAB_ALL")) {
     printf("done\n");
     return 0;
