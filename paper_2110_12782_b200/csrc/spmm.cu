@@ -325,6 +325,10 @@ __device__ __forceinline__ void fused_body(const SpmmArgs &p, int py, int bx, co
   float *slot = part + ((int64_t)py * nsegs + sidx) * PW + li * 4;
   const float4 acc = active ? gather_sum<false>(col, e0, e1, p.X + c, (uint32_t)p.ldx, nullptr)
                             : make_float4(0.f, 0.f, 0.f, 0.f);
+  if (e0 == rb && e1 == re) {  // the whole row in one segment: no partial, no counter
+    if (active) slice_epilogue<GEN>(p, u, c, p.coef * row_scale((int)(re - rb), p.a), acc);
+    return;
+  }
   __stcg(reinterpret_cast<float4 *>(slot), acc);
   // the group's stores are ordered before the arrival by the group barrier
   // and the leader's gpu-scope fence (cumulativity); the leader fences again
