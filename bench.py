@@ -61,6 +61,10 @@ def gather_roofline(achieved_tbps):
             out["peak_table_208MB_TBps"] = gr["table_208MB_TBps"]
             out["frac_of_l2_resident_peak"] = achieved_tbps / gr["l2_resident_TBps"]
             out["source"] = gr["source"]
+            if "access_stream_ceiling_TBps" in gr:
+                out["access_stream_ceiling_TBps"] = gr["access_stream_ceiling_TBps"]
+                out["frac_of_access_stream_ceiling"] = achieved_tbps / gr["access_stream_ceiling_TBps"]
+                out["access_stream_source"] = gr["access_stream_source"]
     return out
 
 
