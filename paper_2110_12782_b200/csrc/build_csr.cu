@@ -93,10 +93,11 @@ __global__ void k_nnz(const uint64_t *__restrict__ keys, const int64_t *__restri
   *nnz = (u > 0 && (keys[u - 1] >> cb) == n_all) ? u - 1 : u;
 }
 
-__global__ void k_rowptr(const uint64_t *__restrict__ keys, int64_t nnz, int64_t n, int64_t row0, int cb,
-                         int64_t *__restrict__ rowptr) {
+__global__ void k_rowptr(const uint64_t *__restrict__ keys, const int64_t *__restrict__ dnnz, int64_t n, int64_t row0,
+                         int cb, int64_t *__restrict__ rowptr) {
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u > n) return;
+  const int64_t nnz = *dnnz;
   uint64_t target = (uint64_t)(u + row0) << cb;
   int64_t lo = 0, hi = nnz;
   while (lo < hi) {
@@ -106,10 +107,11 @@ __global__ void k_rowptr(const uint64_t *__restrict__ keys, int64_t nnz, int64_t
   rowptr[u] = lo;
 }
 
-__global__ void k_col_deg(const uint64_t *__restrict__ keys, int64_t nnz,
+__global__ void k_col_deg(const uint64_t *__restrict__ keys, const int64_t *__restrict__ dnnz,
                           const int64_t *__restrict__ rowptr, int64_t n, int cb, int32_t *__restrict__ col,
                           int32_t *__restrict__ deg, uint8_t *__restrict__ heavy_flag, int light_cap) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nnz = *dnnz;
   if (i < nnz) col[i] = (int32_t)(keys[i] & ((1ull << cb) - 1));
   if (i < n) {
     int64_t dg = rowptr[i + 1] - rowptr[i];
@@ -118,11 +120,11 @@ __global__ void k_col_deg(const uint64_t *__restrict__ keys, int64_t nnz,
   }
 }
 
-__global__ void k_heavy_seg_map(const int32_t *__restrict__ heavy, int64_t nh, const int64_t *__restrict__ seg_ptr,
-                                const int64_t *__restrict__ rowptr, int64_t *__restrict__ seg_e0,
-                                int32_t *__restrict__ seg_h, int heavy_seg) {
+__global__ void k_heavy_seg_map(const int32_t *__restrict__ heavy, const int64_t *__restrict__ dnh,
+                                const int64_t *__restrict__ seg_ptr, const int64_t *__restrict__ rowptr,
+                                int64_t *__restrict__ seg_e0, int32_t *__restrict__ seg_h, int heavy_seg) {
   const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (h >= nh) return;
+  if (h >= *dnh) return;
   const int64_t b = rowptr[heavy[h]];
   for (int64_t sg = seg_ptr[h]; sg < seg_ptr[h + 1]; ++sg) {
     seg_e0[sg] = b + (sg - seg_ptr[h]) * heavy_seg;
@@ -130,12 +132,17 @@ __global__ void k_heavy_seg_map(const int32_t *__restrict__ heavy, int64_t nh, c
   }
 }
 
-__global__ void k_heavy_segs(const int32_t *__restrict__ heavy, int64_t nh,
+// segments per heavy row, zero-padded to n + 1 entries (the heavy count nh is
+// a device value): the exclusive scan of all n + 1 gives seg_ptr[0..nh] and
+// the total at every index >= nh
+__global__ void k_heavy_segs(const int32_t *__restrict__ heavy, const int64_t *__restrict__ dnh, int64_t n,
                              const int32_t *__restrict__ deg, int64_t *__restrict__ nseg, int heavy_seg) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < nh) nseg[i] = (deg[heavy[i]] + heavy_seg - 1) / heavy_seg;
-  if (i == nh) nseg[i] = 0;
+  if (i > n) return;
+  nseg[i] = i < *dnh ? (deg[heavy[i]] + heavy_seg - 1) / heavy_seg : 0;
 }
+
+__global__ void k_flag_nz(const int32_t *__restrict__ deg, int64_t n, int32_t *__restrict__ flag);
 
 static int bits_for(uint64_t v) {
   int b = 0;
@@ -204,61 +211,80 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
     } else {
       nsel.zero();
     }
+    // Everything below sizes its buffers from upper bounds known on the host
+    // (nnz <= nk, heavy rows <= n, segments <= nk / heavy_seg + n) and reads
+    // the actual counts from device memory, so the build synchronises with
+    // the host once, at the end, to fill the graph's host-side counts.
     // drop the sentinel (row n) if present: it is the last unique key
-    DBuf<int64_t> dnnz(1, s);
+    DBuf<int64_t> dnnz(1, s), dnh(1, s);
     NM_LAUNCH(c, "nnz", k_nnz<<<1, 1, 0, s>>>(keys, nsel, (uint64_t)n_all, cb, dnnz));
-    int64_t nnz = 0;
+    const int64_t nnz_cap = nk;
+    g->rowptr.alloc(n + 1, s);
+    g->col.alloc(nnz_cap > 0 ? nnz_cap : 1, s);
+    g->deg.alloc(n > 0 ? n : 1, s);
+    DBuf<uint8_t> hflag(n > 0 ? n : 1, s);
+    NM_LAUNCH(c, "rowptr", k_rowptr<<<ceil_div(n + 1, 256), 256, 0, s>>>(keys, dnnz, n, row0, cb, g->rowptr));
+    const int64_t mx = std::max(nnz_cap, n);
+    if (mx > 0)  // an empty row range (a rank with no rows) has nothing to fill
+      NM_LAUNCH(c, "col_deg", k_col_deg<<<ceil_div(mx, 256), 256, 0, s>>>(keys, dnnz, g->rowptr, n, cb, g->col, g->deg,
+                                                                               hflag, g->light_cap));
+    // heavy rows (degree > light_cap) for the split SpMM path
+    g->heavy.alloc(n > 0 ? n : 1, s);
+    if (n > 0) {
+      size_t tb = 0;
+      cub::CountingInputIterator<int32_t> it(0);
+      NM_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, hflag.p, g->heavy.p, dnh.p, n, s));
+      DBuf<char> tmp(tb, s);
+      NM_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, it, hflag.p, g->heavy.p, dnh.p, n, s));
+      c.launches += 2;
+    } else {
+      dnh.zero();
+    }
+    g->heavy_seg_ptr.alloc(n + 1, s);
+    {
+      DBuf<int64_t> nseg(n + 1, s);
+      NM_LAUNCH(c, "heavy_segs", k_heavy_segs<<<ceil_div(n + 1, 256), 256, 0, s>>>(g->heavy, dnh, n, g->deg, nseg,
+                                                                                  g->heavy_seg));
+      size_t tb2 = 0;
+      NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, nseg.p, g->heavy_seg_ptr.p, n + 1, s));
+      DBuf<char> tmp2b(tb2, s);
+      NM_CUDA(cub::DeviceScan::ExclusiveSum(tmp2b.p, tb2, nseg.p, g->heavy_seg_ptr.p, n + 1, s));
+      c.launches += 1;
+    }
+    // per segment: first entry and heavy-row index (no search in the SpMM)
+    const int64_t seg_cap = nnz_cap / g->heavy_seg + n + 1;
+    g->seg_e0.alloc(seg_cap, s);
+    g->seg_h.alloc(seg_cap, s);
+    if (n > 0)
+      NM_LAUNCH(c, "heavy_seg_map", k_heavy_seg_map<<<ceil_div(n, 128), 128, 0, s>>>(
+                                        g->heavy, dnh, g->heavy_seg_ptr, g->rowptr, g->seg_e0, g->seg_h, g->heavy_seg));
+    // a whole graph: the scan of (degree > 0) for isolated-vertex compaction
+    int32_t hne = -1;
+    if (!part && n > 0) {
+      DBuf<int32_t> flag(n + 1, s);
+      g->nz_pos.alloc(n + 1, s);
+      NM_LAUNCH(c, "flag_nz", k_flag_nz<<<ceil_div(n + 1, 256), 256, 0, s>>>(g->deg, n, flag));
+      size_t tb3 = 0;
+      NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb3, flag.p, g->nz_pos.p, n + 1, s));
+      DBuf<char> tmp3(tb3, s);
+      NM_CUDA(cub::DeviceScan::ExclusiveSum(tmp3.p, tb3, flag.p, g->nz_pos.p, n + 1, s));
+      c.launches += 1;
+      NM_CUDA(cudaMemcpyAsync(&hne, g->nz_pos.p + n, 4, cudaMemcpyDeviceToHost, s));
+    }
+    // the one host round trip: nnz, the bad-id flag, heavy rows, segments
+    int64_t hc[3] = {0, 0, 0};
     int hbad = 0;
-    NM_CUDA(cudaMemcpyAsync(&nnz, dnnz.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    NM_CUDA(cudaMemcpyAsync(&hc[0], dnnz.p, 8, cudaMemcpyDeviceToHost, s));
+    NM_CUDA(cudaMemcpyAsync(&hc[1], dnh.p, 8, cudaMemcpyDeviceToHost, s));
+    NM_CUDA(cudaMemcpyAsync(&hc[2], g->heavy_seg_ptr.p + n, 8, cudaMemcpyDeviceToHost, s));
     NM_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     NM_CUDA(cudaStreamSynchronize(s));
     NM_REQUIRE(!hbad, "build_csr: vertex id out of [0, n)");
-    g->nnz = nnz;
-    g->nnz_global = nnz;
-    g->rowptr.alloc(n + 1, s);
-    g->col.alloc(nnz > 0 ? nnz : 1, s);
-    g->deg.alloc(n, s);
-    DBuf<uint8_t> hflag(n, s);
-    NM_LAUNCH(c, "rowptr", k_rowptr<<<ceil_div(n + 1, 256), 256, 0, s>>>(keys, nnz, n, row0, cb, g->rowptr));
-    int64_t mx = std::max(nnz, n);
-    if (mx > 0)  // an empty row range (a rank with no rows) has nothing to fill
-      NM_LAUNCH(c, "col_deg", k_col_deg<<<ceil_div(mx, 256), 256, 0, s>>>(keys, nnz, g->rowptr, n, cb, g->col, g->deg,
-                                                                               hflag, g->light_cap));
-    // heavy rows (degree > kLightCap) for the split SpMM path
-    {
-      DBuf<int32_t> hv(n, s);
-      size_t tb = 0;
-      cub::CountingInputIterator<int32_t> it(0);
-      NM_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, hflag.p, hv.p, nsel.p, n, s));
-      DBuf<char> tmp(tb, s);
-      NM_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, it, hflag.p, hv.p, nsel.p, n, s));
-      c.launches += 2;
-      int64_t nh = 0;
-      NM_CUDA(cudaMemcpyAsync(&nh, nsel.p, 8, cudaMemcpyDeviceToHost, s));
-      NM_CUDA(cudaStreamSynchronize(s));
-      g->n_heavy = nh;
-      g->heavy.alloc(nh > 0 ? nh : 1, s);
-      if (nh > 0)
-        NM_CUDA(cudaMemcpyAsync(g->heavy.p, hv.p, nh * 4, cudaMemcpyDeviceToDevice, s));
-      g->heavy_seg_ptr.alloc(nh + 1, s);
-      DBuf<int64_t> nseg(nh + 1, s);
-      NM_LAUNCH(c, "heavy_segs", k_heavy_segs<<<ceil_div(nh + 1, 256), 256, 0, s>>>(g->heavy, nh, g->deg, nseg, g->heavy_seg));
-      size_t tb2 = 0;
-      NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, nseg.p, g->heavy_seg_ptr.p, nh + 1, s));
-      DBuf<char> tmp2b(tb2, s);
-      NM_CUDA(cub::DeviceScan::ExclusiveSum(tmp2b.p, tb2, nseg.p, g->heavy_seg_ptr.p, nh + 1, s));
-      c.launches += 1;
-      int64_t nsegs = 0;
-      NM_CUDA(cudaMemcpyAsync(&nsegs, g->heavy_seg_ptr.p + nh, 8, cudaMemcpyDeviceToHost, s));
-      NM_CUDA(cudaStreamSynchronize(s));
-      g->n_heavy_segs = nsegs;
-      // per segment: first entry and heavy-row index (no search in the SpMM)
-      g->seg_e0.alloc(nsegs > 0 ? nsegs : 1, s);
-      g->seg_h.alloc(nsegs > 0 ? nsegs : 1, s);
-      if (nh > 0)
-        NM_LAUNCH(c, "heavy_seg_map", k_heavy_seg_map<<<ceil_div(nh, 128), 128, 0, s>>>(
-                                          g->heavy, nh, g->heavy_seg_ptr, g->rowptr, g->seg_e0, g->seg_h, g->heavy_seg));
-    }
+    g->nnz = hc[0];
+    g->nnz_global = hc[0];
+    g->n_heavy = hc[1];
+    g->n_heavy_segs = hc[2];
+    g->n_nonisolated = hne;
   } catch (...) {
     delete g;
     throw;
@@ -320,22 +346,35 @@ Graph *compact_graph(Ctx &c, const Graph &g, const int32_t *degall) {
   if (n_all == 0) return nullptr;
   cudaStream_t s = c.stream;
   const int64_t b0 = g.row0, b1 = g.row0 + g.n;
-  DBuf<int32_t> flag(n_all + 1, s), pos(n_all + 1, s);
-  NM_LAUNCH(c, "flag_nz", k_flag_nz<<<ceil_div(n_all + 1, 256), 256, 0, s>>>(degall, n_all, flag));
-  size_t tb = 0;
-  NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.p, pos.p, n_all + 1, s));
-  DBuf<char> tmp(tb, s);
-  NM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, flag.p, pos.p, n_all + 1, s));
-  c.launches += 1;
-  // compact images of every rank's bounds (bounds.back() = n_all: the total)
   std::vector<int64_t> bounds = g.bounds.size() >= 2 ? g.bounds : std::vector<int64_t>{0, n_all};
   std::vector<int32_t> pb(bounds.size());
-  for (size_t r = 0; r < bounds.size(); ++r)
-    NM_CUDA(cudaMemcpyAsync(&pb[r], pos.p + bounds[r], 4, cudaMemcpyDeviceToHost, s));
   int32_t p0 = 0, p1 = 0;
-  NM_CUDA(cudaMemcpyAsync(&p0, pos.p + b0, 4, cudaMemcpyDeviceToHost, s));
-  NM_CUDA(cudaMemcpyAsync(&p1, pos.p + b1, 4, cudaMemcpyDeviceToHost, s));
-  NM_CUDA(cudaStreamSynchronize(s));
+  DBuf<int32_t> pos_own;
+  const int32_t *pos = nullptr;
+  const bool whole = b0 == 0 && b1 == n_all;
+  if (whole && g.n_nonisolated >= 0 && degall == g.deg.p) {
+    // the build's scan: no host round trip here
+    pos = g.nz_pos.p;
+    p0 = 0;
+    p1 = (int32_t)g.n_nonisolated;
+    pb = {0, (int32_t)g.n_nonisolated};
+  } else {
+    DBuf<int32_t> flag(n_all + 1, s);
+    pos_own.alloc(n_all + 1, s);
+    NM_LAUNCH(c, "flag_nz", k_flag_nz<<<ceil_div(n_all + 1, 256), 256, 0, s>>>(degall, n_all, flag));
+    size_t tb = 0;
+    NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.p, pos_own.p, n_all + 1, s));
+    DBuf<char> tmp(tb, s);
+    NM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, flag.p, pos_own.p, n_all + 1, s));
+    c.launches += 1;
+    pos = pos_own.p;
+    // compact images of every rank's bounds (bounds.back() = n_all: the total)
+    for (size_t r = 0; r < bounds.size(); ++r)
+      NM_CUDA(cudaMemcpyAsync(&pb[r], pos + bounds[r], 4, cudaMemcpyDeviceToHost, s));
+    NM_CUDA(cudaMemcpyAsync(&p0, pos + b0, 4, cudaMemcpyDeviceToHost, s));
+    NM_CUDA(cudaMemcpyAsync(&p1, pos + b1, 4, cudaMemcpyDeviceToHost, s));
+    NM_CUDA(cudaStreamSynchronize(s));
+  }
   const int64_t ne_all = pb.back(), row0c = p0, ne = (int64_t)p1 - p0;
   if (ne_all == n_all || ne_all == 0) return nullptr;
   auto gc = new Graph();

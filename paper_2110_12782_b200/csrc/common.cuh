@@ -354,13 +354,17 @@ struct Graph {
   // degree 0); for a full graph, its cached compacted copy (if built)
   int64_t n_orig = 0;
   DBuf<int32_t> orig_id, comp_id;
+  // a whole graph's exclusive scan of (degree > 0) and its total, computed by
+  // the build before its one host round trip, so compaction needs none
+  DBuf<int32_t> nz_pos;
+  int64_t n_nonisolated = -1;
   mutable std::unique_ptr<Graph> compact;
   mutable bool compact_checked = false;
   mutable std::mutex compact_mu;  // the cached compacted copy is built once
   void detach_streams() {  // free on the legacy stream (owning stream may be gone)
     rowptr.s = col.s = deg.s = heavy.s = nullptr;
     heavy_seg_ptr.s = seg_e0.s = nullptr;
-    seg_h.s = orig_id.s = comp_id.s = nullptr;
+    seg_h.s = orig_id.s = comp_id.s = nz_pos.s = nullptr;
     if (compact) compact->detach_streams();
   }
 };
