@@ -436,11 +436,13 @@ def make_edges(args, w, spec, dev):
 
 def partition_bounds(n, src, dst, ws):
     """Row partition for ONE graph over ws ranks (same on every rank): contiguous
-    ranges of near-equal (degree + 1) cost, degrees estimated from the raw
-    edge list (duplicates counted) — no full CSR on any rank."""
+    ranges of near-equal (degree + 1) cost over the non-isolated vertices
+    (isolated rows are compacted away by embed and cost nothing), degrees
+    estimated from the raw edge list (duplicates counted) — no full CSR on
+    any rank."""
     import torch
     deg = torch.bincount(src.long(), minlength=n) + torch.bincount(dst.long(), minlength=n)
-    cost = torch.cumsum(deg + 1, 0)
+    cost = torch.cumsum(deg + (deg > 0).to(deg.dtype), 0)
     tot = int(cost[-1])
     tgt = torch.tensor([tot * r // ws for r in range(1, ws)], dtype=cost.dtype, device=cost.device)
     inner = torch.searchsorted(cost, tgt).cpu().numpy().tolist() if ws > 1 else []
