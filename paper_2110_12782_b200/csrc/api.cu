@@ -1,6 +1,7 @@
 // api.cu — the C ABI of include/netmfp.h: argument checking, host/device
 // marshalling, error codes.  All compute is in the other translation units.
 #include <algorithm>
+#include <chrono>
 #include <exception>
 #include <cstdlib>
 #include <cstring>
@@ -132,6 +133,17 @@ static void check_params(const netmfp_params &p, int64_t n) {
 }
 
 static void finish(Ctx &c) {
+  static const bool dbg = getenv("NETMFP_DEBUG_ENQUEUE") != nullptr;
+  if (dbg) {  // host time to enqueue the call vs its device time (is the host the bottleneck?)
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, c.stream);
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaEventSynchronize(e);
+    const double wait_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "netmfp: host waited %.3f ms for the device after enqueueing\n", wait_ms);
+    cudaEventDestroy(e);
+  }
   int h = 0;
   if (!c.flag_checks.empty())
     NM_CUDA(cudaMemcpyAsync(&h, c.d_flags, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
