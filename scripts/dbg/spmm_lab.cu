@@ -21,7 +21,7 @@
     }                                                                                  \
   } while (0)
 
-enum : int { H_COL = 1, H_Y = 2, H_X = 4, H_DET = 8, H_NACOL = 16, H_NAX = 32, H_U8 = 64, H_COOP = 128, H_COOP8 = 256, H_YCS = 512, H_PCG = 1024 };
+enum : int { H_COL = 1, H_Y = 2, H_X = 4, H_DET = 8, H_NACOL = 16, H_NAX = 32, H_U8 = 64, H_COOP = 128, H_COOP8 = 256, H_YCS = 512, H_PCG = 1024, H_PAIR = 2048 };
 
 struct G {
   const int64_t *rowptr;
@@ -201,6 +201,55 @@ __global__ void __launch_bounds__(256, MINB) k_lab(G g, int nblk_heavy) {
       const float sl = rsc(dl, g.a);
       const int64_t eb = __shfl_sync(0xffffffffu, rp, 0);
       const int rel = (int)(rp - eb);
+      if ((HINT & H_PAIR) && LPR == 32) {
+        // pairs of consecutive light rows with degree <= 2: both rows' gathers in flight together
+#pragma unroll 1
+        for (int r = 0; r < nrows;) {
+          const int rn = min(r + 1, 31);
+          const int d = __shfl_sync(0xffffffffu, dl, r), dn = __shfl_sync(0xffffffffu, dl, rn);
+          const float sr = __shfl_sync(0xffffffffu, sl, r), sn = __shfl_sync(0xffffffffu, sl, rn);
+          const uint32_t q0 = __shfl_sync(0xffffffffu, k0, r), q1 = __shfl_sync(0xffffffffu, k1, r);
+          const uint32_t p0 = __shfl_sync(0xffffffffu, k0, rn), p1 = __shfl_sync(0xffffffffu, k1, rn);
+          const bool hr = (hmask >> r) & 1u, hn = (hmask >> rn) & 1u;
+          const bool pair = r + 1 < nrows && !hr && !hn && d >= 1 && d <= 2 && dn >= 1 && dn <= 2;
+          if (pair) {
+            float4 x0 = ldx<HINT>(Xc, q0, ld, pf, pl), y0 = ldx<HINT>(Xc, p0, ld, pf, pl);
+            float4 x1 = make_float4(0, 0, 0, 0), y1 = x1;
+            if (d > 1) x1 = ldx<HINT>(Xc, q1, ld, pf, pl);
+            if (dn > 1) y1 = ldx<HINT>(Xc, p1, ld, pf, pl);
+            x0 = add4(x0, x1);
+            y0 = add4(y0, y1);
+            sty<HINT>(g.Y + (u0 + r) * ld + c, make_float4(sr * x0.x, sr * x0.y, sr * x0.z, sr * x0.w), pf);
+            sty<HINT>(g.Y + (u0 + rn) * ld + c, make_float4(sn * y0.x, sn * y0.y, sn * y0.z, sn * y0.w), pf);
+            r += 2;
+            continue;
+          }
+          if (!hr) {
+            const int ro = __shfl_sync(0xffffffffu, rel, r);
+            const uint32_t q2 = __shfl_sync(0xffffffffu, k2, r), q3 = __shfl_sync(0xffffffffu, k3, r);
+            float4 acc = make_float4(0, 0, 0, 0);
+            if (d > 0) {
+              acc = ldx<HINT>(Xc, q0, ld, pf, pl);
+              if (d > 1) {
+                const float4 x1 = ldx<HINT>(Xc, q1, ld, pf, pl);
+                float4 x2 = make_float4(0, 0, 0, 0), x3 = x2;
+                if (d > 2) x2 = ldx<HINT>(Xc, q2, ld, pf, pl);
+                if (d > 3) x3 = ldx<HINT>(Xc, q3, ld, pf, pl);
+                acc = add4(add4(x1, acc), add4(x2, x3));
+                if (d > 4) acc = add4(gsum<HINT>(col, eb + ro + 4, eb + ro + d, Xc, ld, pf, pl), acc);
+              }
+            }
+            sty<HINT>(g.Y + (u0 + r) * ld + c, make_float4(sr * acc.x, sr * acc.y, sr * acc.z, sr * acc.w), pf);
+          } else {
+            // keep the shuffles uniform
+            __shfl_sync(0xffffffffu, rel, r);
+            __shfl_sync(0xffffffffu, k2, r);
+            __shfl_sync(0xffffffffu, k3, r);
+          }
+          r += 1;
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int j = 0; j < LPR; ++j) {
         const int r = gq + j * GPW;
@@ -938,6 +987,8 @@ int main(int argc, char **argv) {
   CK(cudaMemcpy(hr.data(), Yref, n * 288 * 4, cudaMemcpyDeviceToHost));
   run("plain 2x128", k_lab<32, 0>, 32, 2, 256, false);
   run("det 2x128", k_lab<32, H_DET>, 32, 2, 256, false);
+  run("det pair 2x128", k_lab<32, H_DET | H_PAIR>, 32, 2, 256, false);
+  run("det pair 2x128 minb6", k_lab<32, H_DET | H_PAIR, 6>, 32, 2, 256, false);
   run("det ycs 2x128", k_lab<32, H_DET | H_YCS>, 32, 2, 256, false);
   run("det Ypolicy 2x128", k_lab<32, H_DET | H_Y>, 32, 2, 256, false);
   run("det coop4 2x128", k_lab<32, H_DET | H_COOP>, 32, 2, 256, false);
@@ -1053,6 +1104,7 @@ int main(int argc, char **argv) {
       lightonly("light v2 U8 minb4", k_v2<8, 4>);
       lightonly("light v2 U8 minb5", k_v2<8, 5>);
       lightonly("light plain minb6", k_lab<32, H_DET, 6>);
+      lightonly("light pair", k_lab<32, H_DET | H_PAIR>);
     }
     runsplit("heavy plain only (k_lab)", k_heavy_coop<4, 8>, 0);
     runsplit("heavy coop4 only", k_heavy_coop<4, 8>, 2);
