@@ -359,7 +359,13 @@ def single_pass_svd(F, C, scale: float, d: int, s2: int, s3: int, z: int, seed: 
     Uh, sig, Vht = np.linalg.svd(S)                                              # step 8
     U = Q @ Uh[:, :d]                                                            # step 9
     V = Q @ Vht.T[:, :d]
-    return U, sig[:d], V, Q
+    sig = sig[:d]
+    if sig.size < d:  # rank(Y) < d [R10]: Sigma^(1:d,1:d) has zeros past the rank
+        pad = d - sig.size
+        sig = np.concatenate([sig, np.zeros(pad)])
+        U = np.concatenate([U, np.zeros((U.shape[0], pad))], axis=1)
+        V = np.concatenate([V, np.zeros((V.shape[0], pad))], axis=1)
+    return U, sig, V, Q
 
 
 def embedding_from_svd(U, sigma):

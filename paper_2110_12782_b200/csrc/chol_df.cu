@@ -61,6 +61,8 @@ struct DfP {
   int *lflag, *xflag;  // nb×nb ready flags (value = attempt + 1)
   int *fail;           // 0 = ok, else attempt+1 of the failing attempt
   int *flag;           // caller's status word (shift counter, 1<<30 on failure)
+  double drop_tol;     // > 0: a pivot below drop_tol × its diagonal marks a dependent column
+  int *dropped;        // l: attempt+1 of the attempt that dropped column j (else 0)
 };
 
 // wait until *f >= want (or the attempt failed); returns false on failure
@@ -156,7 +158,8 @@ __device__ void tile_mul_abt(double *OUT, const double *A, const double *B) {
 // register operands (the code runs once per tile from a cold instruction
 // cache).  Returns (warp 0) true on breakdown (pivot <= 1e-12 × piv[j] or
 // non-finite).
-__device__ bool warp_chol_inv(double *S, double *X, double *rinv, const double *piv, int ib, volatile int *prog) {
+__device__ bool warp_chol_inv(double *S, double *X, double *rinv, const double *piv, int ib, volatile int *prog,
+                              double drop_tol, int *dropped, int want) {
   const int r = threadIdx.x & 31;
   double w[32];
   if (threadIdx.x < 32) {
@@ -166,8 +169,17 @@ __device__ bool warp_chol_inv(double *S, double *X, double *rinv, const double *
     bool bad = false;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      const double d = __shfl_sync(0xffffffffu, w[j], j);  // S[j][j]
-      bad |= j < ib && (!(d > 1e-12 * piv[j]) || !isfinite(d));
+      double d = __shfl_sync(0xffffffffu, w[j], j);  // S[j][j]
+      // a (numerically) dependent column of an orthonormalising pass: its
+      // Schur pivot is rounding noise; identity pivot, and its column of R⁻¹
+      // is zeroed at the end (that column of Q comes out exactly zero, the
+      // pseudo-inverse semantics of orth on range(Y) [R10])
+      const bool drop = drop_tol > 0.0 && j < ib && isfinite(d) && d < drop_tol * piv[j];
+      if (drop) {
+        d = 1.0;
+        if (r == 0) dropped[j] = want;
+      }
+      bad |= j < ib && !drop && (!(d > 1e-12 * piv[j]) || !isfinite(d));
       const double inv = rsqrt(fmax(d, 1e-300));
       const double l = r >= j ? w[j] * inv : 0.0;  // L[r][j]
       S[r * TL + j] = l;
@@ -299,7 +311,7 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
       }
       __syncthreads();
       if (threadIdx.x < 64) {
-        const bool b = warp_chol_inv(S, D, rinv, piv, ib, &prog);
+        const bool b = warp_chol_inv(S, D, rinv, piv, ib, &prog, p.drop_tol, p.dropped + 32 * I, want);
         if (threadIdx.x == 0) bad = b;
       }
       __syncthreads();
@@ -362,7 +374,8 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
     __syncthreads();
     for (int i = threadIdx.x; i < 32 * 32; i += T) {
       const int r = i >> 5, c = i & 31;
-      if (r < ib && c < ib) p.Rinv[(int64_t)(32 * I + r) * p.l + 32 * I + c] = (c >= r) ? A[c * TL + r] : 0.0;
+      const bool dz = p.drop_tol > 0.0 && c < ib && __ldcg(p.dropped + 32 * I + c) == attempt + 1;
+      if (r < ib && c < ib) p.Rinv[(int64_t)(32 * I + r) * p.l + 32 * I + c] = (c >= r && !dz) ? A[c * TL + r] : 0.0;
     }
     __syncthreads();
   }
@@ -371,7 +384,8 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
     __syncthreads();
     for (int i = threadIdx.x; i < 32 * 32; i += T) {
       const int r = i >> 5, c = i & 31;
-      if (r < jb && c < ib) p.Rinv[(int64_t)(32 * J + r) * p.l + 32 * I + c] = A[c * TL + r];
+      const bool dz = p.drop_tol > 0.0 && c < ib && __ldcg(p.dropped + 32 * I + c) == attempt + 1;
+      if (r < jb && c < ib) p.Rinv[(int64_t)(32 * J + r) * p.l + 32 * I + c] = dz ? 0.0 : A[c * TL + r];
       if (r < ib && c < jb) p.Rinv[(int64_t)(32 * I + r) * p.l + 32 * J + c] = 0.0;
     }
   }
@@ -381,12 +395,12 @@ __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
 }  // namespace cdf
 
 // G = RᵀR → Rinv = R⁻¹ on 1 + nb(nb-1)/2 co-resident CTAs (cooperative launch)
-void chol_inv_df(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *flag) {
+void chol_inv_df(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *flag, double drop_tol) {
   using namespace cdf;
   const int nb = (int)ceil_div(l, 32);
   const int tiles = 1 + nb * (nb - 1) / 2;  // (0,0) and the strictly lower tiles
   DBuf<double> L((size_t)l * l, c.stream);
-  DBuf<int> flags((size_t)2 * nb * nb + 1, c.stream);
+  DBuf<int> flags((size_t)2 * nb * nb + 1 + 32 * nb, c.stream);
   NM_CUDA(cudaMemsetAsync(flags.p, 0, flags.n * sizeof(int), c.stream));
   DfP p{};
   p.G = G;
@@ -399,6 +413,8 @@ void chol_inv_df(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *fl
   p.xflag = flags.p + nb * nb;
   p.fail = flags.p + 2 * nb * nb;
   p.flag = flag;
+  p.drop_tol = drop_tol;
+  p.dropped = flags.p + 2 * nb * nb + 1;
   void *args[] = {&p};
   NM_LAUNCH(c, "chol_df", NM_CUDA(cudaLaunchCooperativeKernel((void *)k_chol_df, dim3(tiles), dim3(T), args, 0,
                                                                 c.stream)));

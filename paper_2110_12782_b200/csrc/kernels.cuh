@@ -101,9 +101,11 @@ void copy_block(Ctx &c, const float *src, int64_t lds, float *dst, int64_t ldd, 
 void cholesky_upper(Ctx &c, double *G, int64_t l, int64_t ld, int *flag);
 // G = RᵀR (l×l, ld) → Rinv = R⁻¹ (l×l upper, ld = l); G is overwritten.
 // Shifted retry and *flag protocol as cholesky_upper.
-void chol_inv_upper(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *flag);
+// drop_tol > 0 (orthonormalising passes): a Schur pivot below drop_tol × its
+// diagonal marks a numerically dependent column, whose column of R⁻¹ is zero [R10]
+void chol_inv_upper(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *flag, double drop_tol = 0.0);
 // the same on nb(nb+1)/2 cooperative CTAs (chol_df.cu), nb = ceil(l/32)
-void chol_inv_df(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *flag);
+void chol_inv_df(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *flag, double drop_tol = 0.0);
 // Rinv = R^-1 for upper triangular R (l×l)
 void tri_inv_upper(Ctx &c, const double *R, int64_t ld, double *Rinv, int64_t l);
 // symmetric eigendecomposition (cyclic Jacobi), S overwritten; V (l×l) gets

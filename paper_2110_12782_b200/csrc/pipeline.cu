@@ -32,7 +32,10 @@ void cholqr(Ctx &c, const Mat &Y, const Mat &out, const int32_t *deg, float rexp
     // last pass of an orthonormal CholeskyQR) need not be fp32-accurate
     gram(c, cur, cur, nullptr, 0.f, G, l, orthonormal && ps + 1 == passes);
     dist_allreduce(c, G, (size_t)l * l, DType::F64);  // Gram over all ranks' rows
-    chol_inv_upper(c, G, l, l, Rinv, c.d_flags);
+    // the pass whose output must be orthonormal drops numerically dependent
+    // columns (pivot < 1e-8 of the column's own diagonal): after a first pass
+    // such a column is rounding noise inside span(Y) [R10]
+    chol_inv_upper(c, G, l, l, Rinv, c.d_flags, orthonormal && ps + 1 == passes && passes > 1 ? 1e-8 : 0.0);
     const bool last = (ps + 1 == passes);
     if (last) {
       gemm_tall_tri(c, cur, Rinv, l, deg, rexp, out, orthonormal);

@@ -314,12 +314,13 @@ constexpr int CI_R = CI_MAXL * CI_LD;      // doubles per big region
 constexpr int CI_K = (CI_MAXL * 32 + CI_T - 1) / CI_T;  // outputs per thread
 
 __global__ void __launch_bounds__(CI_T) k_chol_inv(double *G, int l, int64_t ld, double *G0, double *Rinv,
-                                                   int *flag) {
+                                                   int *flag, double drop_tol) {
   extern __shared__ double sm[];
   double *R1 = sm;             // phase 1: L rows chunk [rows][33];   phase 2: L_I rows [32][l+1]
   double *R2 = sm + CI_R;      // phase 1: panel P [rows][33];        phase 2: X chunk / T [32][l+1]
   double *R3 = sm + 2 * CI_R;  // phase 1: LsT chunk [32][33];        phase 2: X_II [32][33]
   __shared__ double diag0[CI_MAXL];
+  __shared__ unsigned char dropped[CI_MAXL];  // dependent columns of the successful attempt
   __shared__ int fail;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t idx = tid; idx < (int64_t)l * l; idx += CI_T) G0[idx] = G[(idx / l) * ld + idx % l];
@@ -338,6 +339,7 @@ __global__ void __launch_bounds__(CI_T) k_chol_inv(double *G, int l, int64_t ld,
       }
     }
     if (tid == 0) fail = 0;
+    for (int i = tid; i < l; i += CI_T) dropped[i] = 0;
     __syncthreads();
     for (int J = 0; J < l; J += 32) {
       const int jb = min(32, l - J), rows = l - J, np = rows * jb;
@@ -384,8 +386,14 @@ __global__ void __launch_bounds__(CI_T) k_chol_inv(double *G, int l, int64_t ld,
           // of G) gets an identity pivot: that column of Y R⁻¹ stays zero and
           // the others are untouched — orth on range(Y) [R10]
           const bool zc = diag0[J + j] == 0.0;
-          const double d = zc ? 1.0 : R2[j * CI_LD + j];
-          if (!zc && (!(d > 1e-12 * (diag0[J + j] + shift)) || !isfinite(d))) bad = true;
+          double d = zc ? 1.0 : R2[j * CI_LD + j];
+          // numerically dependent column of an orthonormalising pass [R10]
+          const bool dr = !zc && drop_tol > 0.0 && isfinite(d) && d < drop_tol * (diag0[J + j] + shift);
+          if (dr) {
+            d = 1.0;
+            if (lane == 0) dropped[J + j] = 1;
+          }
+          if (!zc && !dr && (!(d > 1e-12 * (diag0[J + j] + shift)) || !isfinite(d))) bad = true;
           const double sq = sqrt(fmax(d, 1e-300));
           __syncwarp();
           if (lane == j) R2[j * CI_LD + j] = sq;
@@ -499,12 +507,16 @@ __global__ void __launch_bounds__(CI_T) k_chol_inv(double *G, int l, int64_t ld,
       Rinv[j * l + i] = 0.0;
     }
   }
+  __syncthreads();
+  // dependent columns: zero columns of R⁻¹ (Q's column comes out exactly zero)
+  for (int64_t idx = tid; idx < (int64_t)l * l; idx += CI_T)
+    if (dropped[idx % l]) Rinv[idx] = 0.0;
 }
 
-void chol_inv_upper(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *flag) {
+void chol_inv_upper(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int *flag, double drop_tol) {
   // tile dataflow on many SMs while the lower triangle fits in co-resident CTAs
   if (l > 64 && (l + 31) / 32 * ((l + 31) / 32 + 1) / 2 <= c.num_sms) {
-    chol_inv_df(c, G, l, ld, Rinv, flag);
+    chol_inv_df(c, G, l, ld, Rinv, flag, drop_tol);
     return;
   }
   if (l > CI_MAXL) {
@@ -515,7 +527,7 @@ void chol_inv_upper(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int 
   DBuf<double> G0((size_t)l * l, c.stream);
   const size_t smem = ((size_t)2 * CI_R + 32 * CI_LD) * sizeof(double);
   smem_attr(k_chol_inv, smem);
-  NM_LAUNCH(c, "chol_inv", k_chol_inv<<<1, CI_T, smem, c.stream>>>(G, (int)l, ld, G0, Rinv, flag));
+  NM_LAUNCH(c, "chol_inv", k_chol_inv<<<1, CI_T, smem, c.stream>>>(G, (int)l, ld, G0, Rinv, flag, drop_tol));
 }
 
 // ---------------------------------------------------------------------------

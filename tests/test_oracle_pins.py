@@ -435,3 +435,28 @@ def test_netmf_plus_exact_regime():
     Mp = B.netmf_dense(A, 5, 1.0)
     U, S, Vt = np.linalg.svd(Mp)
     assert np.allclose(out["sigma"], S[:5], rtol=1e-7)
+
+
+def test_single_pass_svd_rank_below_d_pads_zeros():
+    """Alg. 4 step 9 Sigma = Sigma^(1:d,1:d) [R5] with rank(Y) < d [R10]: the
+    singular values past the rank are zero and their columns of U are zero;
+    the leading ones equal the exact SVD of the (low-rank) Eq. 1 matrix."""
+    rng = np.random.default_rng(3)
+    n, k = 60, 3
+    F = rng.standard_normal((n, k))
+    C = np.diag([3.0, 2.0, 1.0])
+    U, sig, V, Q = O.single_pass_svd(F, C, 1.0, 8, 4, 40, 4, 7, 1)   # log1p: rank(f(F C F^T)) can exceed k
+    assert sig.shape == (8,) and U.shape == (n, 8)
+    r = Q.shape[1]
+    if r < 8:
+        assert np.all(sig[r:] == 0.0) and np.all(U[:, r:] == 0.0)
+    # a rank-2 matrix through trunc_log: Y has rank <= its nonzero pattern allows
+    F2 = np.zeros((n, 2))
+    F2[:5] = rng.uniform(1.0, 2.0, (5, 2))        # M = F2 F2^T > 1 only on a 5x5 block
+    U2, sig2, _, Q2 = O.single_pass_svd(F2, np.eye(2), 10.0, 8, 4, 40, n, 7, 0)   # z = n: dense signs, exact regime
+    M = O.trunc_log(10.0 * F2 @ F2.T)
+    ex = np.linalg.svd(M, compute_uv=False)
+    assert Q2.shape[1] <= 5 and np.all(sig2[Q2.shape[1]:] == 0.0)
+    r2 = int((ex > 1e-6 * ex[0]).sum())          # orth_range keeps sigma > 1e-6 sigma_1 (eigenvalues > 1e-12)
+    lead = int((ex > 1e-3 * ex[0]).sum())
+    assert Q2.shape[1] == r2 and np.allclose(sig2[:lead], ex[:lead], rtol=1e-6)
