@@ -1129,6 +1129,90 @@ int main(int argc, char **argv) {
       printf("%-34s cols=256  med %.4f ms\n", "heavy plain only (k_lab segs)", ts[5]);
     }
   }
+  if (getenv("LAB_ORDER")) {
+    // vertex orders of the compacted graph: 1 = light rows sorted by their smallest
+    // neighbour (rows sharing a hub land in one tile: L1 reuse), heavy rows after;
+    // 2 = every row sorted by its smallest neighbour
+    const int mode = atoi(getenv("LAB_ORDER"));
+    std::vector<int64_t> keyv(n);
+    for (int64_t u = 0; u < n; ++u) keyv[u] = deg[u] > 0 ? col[rp[u]] : (int64_t)n;
+    std::vector<int64_t> ord(n);
+    for (int64_t u = 0; u < n; ++u) ord[u] = u;
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
+      const bool ha = mode == 1 && deg[a] > light_cap, hb = mode == 1 && deg[b] > light_cap;
+      if (ha != hb) return !ha;
+      if (ha) return a < b;
+      return keyv[a] < keyv[b];
+    });
+    std::vector<int32_t> nid(n);
+    for (int64_t i = 0; i < n; ++i) nid[ord[i]] = (int32_t)i;
+    std::vector<int64_t> rp2(n + 1, 0);
+    std::vector<int32_t> col2(nnz);
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t u = ord[i];
+      rp2[i + 1] = rp2[i] + deg[u];
+      for (int64_t e = rp[u]; e < rp[u + 1]; ++e) col2[rp2[i] + (e - rp[u])] = nid[col[e]];
+      std::sort(col2.begin() + rp2[i], col2.begin() + rp2[i + 1]);
+    }
+    std::vector<int32_t> heavy2, seg_h2;
+    std::vector<int64_t> seg_ptr2{0}, seg_e02;
+    for (int64_t i = 0; i < n; ++i) {
+      const int d = (int)(rp2[i + 1] - rp2[i]);
+      if (d <= light_cap) continue;
+      heavy2.push_back((int)i);
+      for (int s2 = 0; s2 < (d + heavy_seg - 1) / heavy_seg; ++s2) {
+        seg_e02.push_back(rp2[i] + (int64_t)s2 * heavy_seg);
+        seg_h2.push_back((int)heavy2.size() - 1);
+      }
+      seg_ptr2.push_back((int64_t)seg_e02.size());
+    }
+    G g2 = g;
+    g2.rowptr = (int64_t *)up(rp2.data(), rp2.size() * 8);
+    g2.col = (int32_t *)up(col2.data(), col2.size() * 4);
+    g2.heavy = (int32_t *)up(heavy2.data(), heavy2.size() * 4);
+    g2.seg_ptr = (int64_t *)up(seg_ptr2.data(), seg_ptr2.size() * 8);
+    g2.seg_e0 = (int64_t *)up(seg_e02.data(), seg_e02.size() * 8);
+    g2.seg_h = (int32_t *)up(seg_h2.data(), seg_h2.size() * 4);
+    std::vector<float> hx(n * 288), hx2(n * 288);
+    CK(cudaMemcpy(hx.data(), X, n * 288 * 4, cudaMemcpyDeviceToHost));
+    for (int64_t v = 0; v < n; ++v) std::copy(hx.begin() + v * 288, hx.begin() + v * 288 + 288, hx2.begin() + (int64_t)nid[v] * 288);
+    float *X2;
+    CK(cudaMalloc(&X2, n * 288 * 4));
+    CK(cudaMemcpy(X2, hx2.data(), n * 288 * 4, cudaMemcpyHostToDevice));
+    g2.X = X2;
+    for (int pass = 0; pass < 2; ++pass) {
+      G gg = g2;
+      gg.Y = Y;
+      gg.cols = 256;
+      gg.colbase = 0;
+      const int64_t ntl = (n + 31) / 32;
+      gg.nblk_tile = (int)std::min<int64_t>((ntl + 7) / 8, (int64_t)num_sms * 32);
+      const int nbh = pass == 0 ? (int)((nsegs + 7) / 8) : 0;
+      std::vector<float> ts;
+      for (int r = 0; r < 10; ++r) {
+        CK(cudaMemset(flush, r, 512 << 20));
+        cudaEventRecord(e0);
+        k_lab<32, H_DET><<<dim3(gg.nblk_tile + nbh, 2), 256>>>(gg, nbh);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ts.push_back(ms);
+      }
+      CK(cudaGetLastError());
+      std::sort(ts.begin(), ts.end());
+      double err = 0;
+      if (pass == 0) {
+        CK(cudaMemcpy(hy.data(), Y, n * 288 * 4, cudaMemcpyDeviceToHost));
+        for (int64_t u = 0; u < n; ++u)
+          for (int c = 0; c < 256; ++c)
+            err = std::max(err, (double)fabsf(hy[(int64_t)nid[u] * 288 + c] - hr[u * 288 + c]));
+      }
+      printf("order %d %s: med %.4f ms  err %.2e\n", mode, pass == 0 ? "det 2x128 (all rows)" : "light tiles only",
+             ts[5], err);
+    }
+    return 0;
+  }
   if (!getenv("LAB_ALL")) {
     printf("done\n");
     return 0;
