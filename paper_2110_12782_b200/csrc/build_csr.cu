@@ -1,7 +1,8 @@
 // build_csr.cu — row a1: CSR of the undirected simple graph.
 //
 // Edge pairs -> 64-bit keys (u << cb | v, cb = bits of a column id) for both
-// directions (self loops become a sentinel row n) -> CUB radix sort over the
+// directions (self loops become the sentinel key (n-1, n-1): a self loop
+// itself, so no real edge has it, and it sorts last) -> CUB radix sort over the
 // 2 cb + 1 significant bits -> unique -> rowptr by per-row binary search.
 // Deterministic and bit-exact (integer work only).
 #include <cub/cub.cuh>
@@ -19,13 +20,13 @@ __global__ void k_make_keys(const int32_t *__restrict__ src, const int32_t *__re
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= m) return;
   int32_t s = src[e], t = dst[e];
-  const uint64_t sentinel = n << cb;
+  const uint64_t sentinel = ((n - 1) << cb) | (n - 1);  // the key of the self loop (n-1, n-1)
   if (s < 0 || t < 0 || (uint64_t)s >= n || (uint64_t)t >= n) {
     atomicExch(bad, 1);
     keys[2 * e] = keys[2 * e + 1] = sentinel;
     return;
   }
-  if (s == t) {  // self loop: dropped (sentinel row n sorts last)
+  if (s == t) {  // self loop: dropped (the sentinel sorts last)
     keys[2 * e] = keys[2 * e + 1] = sentinel;
   } else {
     // rows outside this rank's range [row0, row1) become the sentinel
@@ -85,12 +86,12 @@ __global__ void k_make_keys_local(const int32_t *__restrict__ src, const int32_t
 }
 
 // rowptr[u] = first key index with row >= row0 + u (lower bound), u in [0, n]
-// nnz = unique keys minus the sentinel row n (the last unique key if present),
-// so the host reads it together with the error flag in one round trip
+// nnz = unique keys minus the sentinel (the last unique key if present)
 __global__ void k_nnz(const uint64_t *__restrict__ keys, const int64_t *__restrict__ nuniq, uint64_t n_all, int cb,
                       int64_t *__restrict__ nnz) {
   const int64_t u = *nuniq;
-  *nnz = (u > 0 && (keys[u - 1] >> cb) == n_all) ? u - 1 : u;
+  const uint64_t sentinel = ((n_all - 1) << cb) | (n_all - 1);
+  *nnz = (u > 0 && keys[u - 1] == sentinel) ? u - 1 : u;
 }
 
 __global__ void k_rowptr(const uint64_t *__restrict__ keys, const int64_t *__restrict__ dnnz, int64_t n, int64_t row0,
@@ -197,7 +198,9 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
       NM_LAUNCH(c, "make_keys", k_make_keys<<<ceil_div(m, 256), 256, 0, s>>>(src, dst, m, (uint64_t)n_all, (uint64_t)row0,
                                                                              (uint64_t)row1, cb, keys, bad));
     }
-    const int end_bit = cb + bits_for((uint64_t)n_all);  // key = row << cb | col, rows up to the sentinel n
+    // key = row << cb | col with rows < n: 2 cb significant bits (one radix
+    // pass fewer than with a sentinel row n at 2^20 vertices)
+    const int end_bit = cb + bits_for((uint64_t)(n_all - 1));
     size_t tmp_bytes = 0, tmp2 = 0;
     DBuf<int64_t> nsel(1, s);
     if (nk > 0) {
@@ -215,7 +218,7 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
     // (nnz <= nk, heavy rows <= n, segments <= nk / heavy_seg + n) and reads
     // the actual counts from device memory, so the build synchronises with
     // the host once, at the end, to fill the graph's host-side counts.
-    // drop the sentinel (row n) if present: it is the last unique key
+    // drop the sentinel if present: it is the last unique key
     DBuf<int64_t> dnnz(1, s), dnh(1, s);
     NM_LAUNCH(c, "nnz", k_nnz<<<1, 1, 0, s>>>(keys, nsel, (uint64_t)n_all, cb, dnnz));
     const int64_t nnz_cap = nk;
