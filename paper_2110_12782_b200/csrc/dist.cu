@@ -131,6 +131,24 @@ static void ops_check(int rc, const char *what) {
 
 static bool dist_active(const Ctx &c) { return c.nranks > 1 || c.comm != nullptr; }
 
+// Every NCCL call of a context goes to its communicator stream, in program
+// order (one stream per communicator: no cross-stream ordering question for
+// NCCL), fenced to the compute stream by events on both sides.
+static void comm_after_compute(Ctx &c) {
+  cudaEvent_t e;
+  NM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  NM_CUDA(cudaEventRecord(e, c.stream));
+  NM_CUDA(cudaStreamWaitEvent(c.comm_stream, e, 0));
+  cudaEventDestroy(e);
+}
+static void compute_after_comm(Ctx &c) {
+  cudaEvent_t e;
+  NM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  NM_CUDA(cudaEventRecord(e, c.comm_stream));
+  NM_CUDA(cudaStreamWaitEvent(c.stream, e, 0));
+  cudaEventDestroy(e);
+}
+
 void dist_allreduce(Ctx &c, void *buf, size_t count, DType t) {
   if (!dist_active(c) || count == 0) return;
   NM_STAGE(c, "stage_comm_allreduce");
@@ -146,7 +164,10 @@ void dist_allreduce(Ctx &c, void *buf, size_t count, DType t) {
     NM_CUDA(cudaStreamSynchronize(c.stream));
     return;
   }
-  nccl_check(nccl().allReduce(buf, buf, count, nccl_dt(t), ncclSum, (ncclComm_t)c.comm, c.stream), "ncclAllReduce");
+  comm_after_compute(c);
+  nccl_check(nccl().allReduce(buf, buf, count, nccl_dt(t), ncclSum, (ncclComm_t)c.comm, c.comm_stream),
+             "ncclAllReduce");
+  compute_after_comm(c);
 }
 
 // all-gather-v of row blocks: rank r's `rows_r * row_elems` elements land at
@@ -175,15 +196,17 @@ static void gather_blocks(Ctx &c, const void *local, const std::vector<int64_t> 
     NM_CUDA(cudaStreamSynchronize(c.stream));
     return;
   }
+  comm_after_compute(c);
   nccl_check(nccl().groupStart(), "ncclGroupStart");
   for (int r = 0; r < c.nranks; ++r) {
     const int64_t rows = bounds[r + 1] - bounds[r];
     if (rows == 0) continue;
     nccl_check(nccl().broadcast(local, static_cast<char *>(out) + (size_t)bounds[r] * row_elems * es,
-                                (size_t)(rows * row_elems), nccl_dt(t), r, (ncclComm_t)c.comm, c.stream),
+                                (size_t)(rows * row_elems), nccl_dt(t), r, (ncclComm_t)c.comm, c.comm_stream),
                "ncclBroadcast");
   }
   nccl_check(nccl().groupEnd(), "ncclGroupEnd");
+  compute_after_comm(c);
 }
 
 const float *dist_gather_rows(Ctx &c, const Graph &g, const Mat &local, DBuf<float> &scratch) {
