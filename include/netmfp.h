@@ -182,8 +182,11 @@ int netmfp_gram(netmfp_ctx *ctx, int64_t n, const float *A, int64_t lda, int64_t
                 int64_t ldb, int64_t b, double *G, int mem);
 /* Q = orth(Y): CholeskyQR (passes = 1) or CholeskyQR2 (passes = 2), the
  * "orth"/"eigSVD" step of Alg. 2 steps 3, 5 and Alg. 4 step 4 [R7].
- * Y, Q: n×c fp32 (ldy, ldq); requires n >= c and Y of full column rank
- * (else NETMFP_ERR_NUMERIC). */
+ * Y, Q: n×c fp32 (ldy, ldq); requires n >= c.  An exactly-zero column of Y
+ * gives a zero column of Q; with passes >= 2 a numerically dependent column
+ * (Schur pivot below 1e-8 of its diagonal in the second pass) does too, so Q
+ * spans range(Y) [R10].  NETMFP_ERR_NUMERIC if the factorisation still fails
+ * after shifted retries. */
 int netmfp_orthonormalize(netmfp_ctx *ctx, int64_t n, int64_t c, const float *Y, int64_t ldy, float *Q,
                           int64_t ldq, int32_t passes, int mem);
 /* [V, Λ] = eig(S) of a symmetric l×l fp64 matrix (row-major): Alg. 2 step 8,
@@ -218,7 +221,9 @@ int netmfp_factor_pair(netmfp_ctx *ctx, const netmfp_graph *g, double alpha, int
  * Y = f(scale F C F(p,:)ᵀ)Ψ (Eq. 5), Q = orth(Y), Z = Πᵀ f(scale F(p,:) C F(p,:)ᵀ) Π,
  * S = (ΠᵀQ)† Z (QᵀΠ)†, svd(S).  F: n×k fp32 (ldf); C: k×k fp64.
  * Outputs (any may be NULL): U n×d fp32 (ldu), sigma d fp64, and the raw
- * embedding E = U √Σ (Alg. 5 step 5) n×d fp32 (lde).
+ * embedding E = U √Σ (Alg. 5 step 5) n×d fp32 (lde).  orth(Y) spans range(Y)
+ * (zero / dependent columns of Y are dropped [R10]); when rank(Y) < d the
+ * trailing singular values are zero.
  * Optional sketch outputs for parity tests (NULL to skip): Ysk n×(d+s2) fp32
  * (ldy) and Zsk (d+s3)×(d+s3) fp64. */
 int netmfp_sketch_svd(netmfp_ctx *ctx, int64_t n, const float *F, int64_t ldf, const double *C,
