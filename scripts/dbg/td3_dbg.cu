@@ -1,0 +1,380 @@
+// LAB (measured and rejected, round 2): Householder tridiagonalisation blocked
+// like LAPACK xLATRD on a CL-CTA cluster — one cluster barrier per step, no
+// per-step rank-2 update, no broadcast of v (k_tridiag3 below).  Correct
+// (matches an unblocked host reduction to 1e-12, bitwise repeatable) but
+// 1.06-1.28 ms vs k_tridiag's 1.07 ms at l = 286 and 0.80-0.95 vs 0.74 ms at
+// l = 228 (profiles/r02_tridiag_lab.txt): the step is bound by its chain of
+// block reductions, fp64 sqrt/div and barriers (~5000 cycles even at l = 19),
+// not by the cluster barriers it removes.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr -DTCL=8 -DTNB=8 \
+//   -Iinclude -I<nccl include> scripts/dbg/td3_dbg.cu -o td3_dbg && ./td3_dbg 286 3
+// k_tridiag2 vs a host unblocked Householder reduction (same reflector
+// convention): first diverging step, and run-to-run repeatability.
+#define TD3_PROF
+#ifndef TCL
+#define TCL 4
+#endif
+#ifndef TNB
+#define TNB 8
+#endif
+#include "../../paper_2110_12782_b200/csrc/small.cu"
+namespace netmfp {
+// ---------------------------------------------------------------------------
+// Householder tridiagonalisation, blocked in the manner of LAPACK's xLATRD
+// (same reflectors and outputs as k_tridiag) on a CL-CTA cluster.  Row i of S
+// lives in CTA i % CL (full rows, stride lp = 32·ceil(l/32), zero padding).
+// Inside a panel of NB steps the trailing matrix is left stale and every
+// step-j quantity is corrected with the panel's V = [v_s], W = [w_s]
+// (A_cur = A − V Wᵀ − W Vᵀ):
+//   column j  a = A[j, j:] − V W[j, :]ᵀ − W V[j, :]ᵀ   (panel rows all-gathered at
+//             the panel start; every CTA, redundantly)
+//   v, β      Householder reflector of a (every CTA, redundantly)
+//   p_i       = β (A[i, :] v − V(Wᵀv) − W(Vᵀv))_i for the CTA's own rows i,
+//             pushed into every CTA's shared memory — the step's ONE cluster
+//             barrier (k_tridiag: two, plus a broadcast of v by its owner)
+//   K, w      K = β vᵀp / 2, w = p − K v (every CTA, redundantly)
+// At a panel end every CTA applies A −= V Wᵀ + W Vᵀ to its own rows and the
+// owners push the next panel's rows.  Redundant quantities are computed by
+// identical code on identical data in every CTA, every reduction has a fixed
+// order: the result is deterministic.
+// ---------------------------------------------------------------------------
+constexpr int T3T = 512;  // threads per CTA (16 warps); l <= T3T
+constexpr int T3W = T3T / 32;
+template <int CL, int NB>
+struct Td3 {
+  static constexpr int RPW = (T3T / CL + T3W - 1) / T3W;  // own-row slots per warp (l <= 512)
+  // shared memory in doubles: A (own rows, lp each), VT, WT, PR (NB × lp), PX (2 l), YO, VV, COL, red
+  static size_t smem_doubles(int l) {
+    const size_t lp = (size_t)(l + 31) / 32 * 32, nmax = (size_t)(l + CL - 1) / CL;
+    return nmax * lp + 2 * (size_t)NB * l + (size_t)NB * lp + 2 * (size_t)l + nmax + lp + l + 2 * T3W + 2 * NB;
+  }
+};
+#ifdef TD3_PROF
+__device__ unsigned long long g_td3_t[6][512];
+#define TD3_MARK(ph)                                      \
+  do {                                                    \
+    if (r == 0 && threadIdx.x == 0 && j < 512) g_td3_t[ph][j] = clock64(); \
+  } while (0)
+#else
+#define TD3_MARK(ph)
+#endif
+
+template <int CL, int NB>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T3T, 1)
+    k_tridiag3(const double *__restrict__ S, int l, double *__restrict__ dd, double *__restrict__ ee,
+               double *__restrict__ Hv, double *__restrict__ hbeta) {
+  constexpr int RPW = Td3<CL, NB>::RPW;
+  cg::cluster_group cl = cg::this_cluster();
+  const int r = (int)cl.block_rank();
+  const int tid = threadIdx.x, wid = tid >> 5, ln = tid & 31;
+  const int lp = (l + 31) / 32 * 32, nch = lp / 32;
+  const int nloc = (l - r + CL - 1) / CL, nmax = (l + CL - 1) / CL;
+  extern __shared__ double sm[];
+  double *A = sm;                    // own row li (global li·CL + r) at A[li·lp]
+  double *VT = A + (size_t)nmax * lp;  // V[k][s] at VT[s·l + k]
+  double *WT = VT + NB * l;
+  double *PR = WT + NB * l;          // panel rows jp + q at PR[q·lp]
+  double *PX = PR + NB * lp;         // p, double-buffered by step parity
+  double *YO = PX + 2 * l;           // own rows' A v
+  double *VV = YO + nmax;            // v (lp entries, zero padding)
+  double *COL = VV + lp;             // the current column a
+  double *red = COL + l;             // T3W warp partials of Σ a²
+  double *redk = red + T3W;          // T3W warp partials of vᵀp
+  double *dots = redk + T3W;         // W_sᵀv, V_sᵀv
+  for (int li = wid; li < nloc; li += T3W) {
+    const int i = li * CL + r;
+    for (int k = ln; k < lp; k += 32) A[(size_t)li * lp + k] = k < l ? S[(int64_t)i * l + k] : 0.0;
+  }
+  for (int idx = tid; idx < NB * lp; idx += T3T) {
+    const int q = idx / lp, k = idx % lp;
+    PR[idx] = (q < l && k < l) ? S[(int64_t)q * l + k] : 0.0;
+  }
+  __syncthreads();
+  double *PXr[CL];
+  double *PRr[CL];
+#pragma unroll
+  for (int c = 0; c < CL; ++c) {
+    PXr[c] = cl.map_shared_rank(PX, c);
+    PRr[c] = cl.map_shared_rank(PR, c);
+  }
+  cl.sync();  // every CTA's shared memory is live before any push
+  const int k = tid;  // this thread's index of every length-l vector
+  // the column jc (t panel corrections; the newest, s = t − 1, from this
+  // thread's vk/wk and the broadcast vj/wj) into COL, warp partials of
+  // Σ_{k >= jc+2} a_k² into red
+  auto column = [&](int jc, int jp, int t, double vk, double wk, double vj, double wj) {
+    double ss = 0.0;
+    if (k < l && k >= jc) {
+      double a = PR[(size_t)(jc - jp) * lp + k];
+      double c0 = 0.0, c1 = 0.0;
+      int s2 = 0;
+      for (; s2 + 2 < t; s2 += 2) {
+        c0 += VT[s2 * l + k] * WT[s2 * l + jc] + WT[s2 * l + k] * VT[s2 * l + jc];
+        c1 += VT[(s2 + 1) * l + k] * WT[(s2 + 1) * l + jc] + WT[(s2 + 1) * l + k] * VT[(s2 + 1) * l + jc];
+      }
+      if (s2 + 1 < t) c0 += VT[s2 * l + k] * WT[s2 * l + jc] + WT[s2 * l + k] * VT[s2 * l + jc];
+      if (t > 0) c1 += vk * wj + wk * vj;
+      a -= c0 + c1;
+      COL[k] = a;
+      if (k >= jc + 2) ss = a * a;
+    }
+    ss = warp_sum(ss);
+    if (ln == 0) red[wid] = ss;
+    __syncthreads();
+  };
+  int jp = 0, t = 0;
+  if (l >= 3) column(0, 0, 0, 0.0, 0.0, 0.0, 0.0);
+  for (int j = 0; j + 2 < l; ++j) {
+    const int par = j & 1;
+    TD3_MARK(0);
+    // (1) reflector of COL (every thread)
+    double ss = 0.0;
+#pragma unroll
+    for (int w = 0; w < T3W; ++w) ss += red[w];
+    const double x0 = COL[j + 1];
+    double beta = 0.0, alpha = x0, v0 = 0.0;
+    if (ss > 0.0) {
+      const double nrm = sqrt(ss + x0 * x0);
+      alpha = x0 >= 0 ? -nrm : nrm;
+      v0 = x0 - alpha;
+      beta = 2.0 / (ss + v0 * v0);
+    }
+    double vk = 0.0;
+    if (k < l) {
+      vk = ss > 0.0 ? (k == j + 1 ? v0 : (k > j + 1 ? COL[k] : 0.0)) : 0.0;
+      VV[k] = vk;
+      VT[t * l + k] = vk;
+      if (r == 0 && k > j) Hv[(int64_t)j * l + k] = vk;
+    } else if (k < lp) {
+      VV[k] = 0.0;
+    }
+    if (r == 0 && tid == 0) {
+      dd[j] = COL[j];
+      ee[j] = alpha;
+      hbeta[j] = beta;
+    }
+    __syncthreads();
+    TD3_MARK(1);
+    // (2) A v for own rows i > j (v is zero at indices <= j and in the padding)
+    {
+      const int li0 = (j + 1 - r <= 0) ? 0 : (j + 1 - r + CL - 1) / CL;
+      const int clo = (j + 1) >> 5;
+      double rs[RPW];
+#pragma unroll
+      for (int u = 0; u < RPW; ++u) rs[u] = 0.0;
+      const int nu = nloc > li0 + wid ? (nloc - li0 - wid + T3W - 1) / T3W : 0;  // valid slots of this warp
+      const double *Ab = A + (size_t)(li0 + wid) * lp + ln;
+      for (int c = clo; c < nch; ++c) {
+        const double vc = VV[32 * c + ln];
+#pragma unroll
+        for (int u = 0; u < RPW; ++u)
+          if (u < nu) rs[u] = fma(Ab[(size_t)u * T3W * lp + 32 * c], vc, rs[u]);
+      }
+      // reduce-scatter of the RPW row partials across the warp
+      double y;
+      if constexpr (RPW == 8) {
+        double h4[4], h2[2];
+        const bool b4 = ln & 16, b3 = ln & 8, b2 = ln & 4;
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          h4[m] = (b4 ? rs[m + 4] : rs[m]) + __shfl_xor_sync(0xffffffffu, b4 ? rs[m] : rs[m + 4], 16);
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+          h2[m] = (b3 ? h4[m + 2] : h4[m]) + __shfl_xor_sync(0xffffffffu, b3 ? h4[m] : h4[m + 2], 8);
+        y = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? h2[0] : h2[1], 4);
+        y += __shfl_xor_sync(0xffffffffu, y, 2);
+        y += __shfl_xor_sync(0xffffffffu, y, 1);
+        const int u = ln >> 2;  // b4·4 + b3·2 + b2
+        if ((ln & 3) == 0 && u < nu) YO[li0 + wid + u * T3W] = y;
+      } else {
+        static_assert(RPW == 4, "k_tridiag3: 4 or 8 row slots per warp");
+        double h2[2];
+        const bool b4 = ln & 16, b3 = ln & 8;
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+          h2[m] = (b4 ? rs[m + 2] : rs[m]) + __shfl_xor_sync(0xffffffffu, b4 ? rs[m] : rs[m + 2], 16);
+        y = (b3 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, b3 ? h2[0] : h2[1], 8);
+        y += __shfl_xor_sync(0xffffffffu, y, 4);
+        y += __shfl_xor_sync(0xffffffffu, y, 2);
+        y += __shfl_xor_sync(0xffffffffu, y, 1);
+        const int u = ln >> 3;  // b4·2 + b3
+        if ((ln & 7) == 0 && u < nu) YO[li0 + wid + u * T3W] = y;
+      }
+      // the panel dots W_sᵀv (d even), V_sᵀv (d odd)
+      for (int d = wid; d < 2 * t; d += T3W) {
+        const double *vec = (d & 1) ? VT + (d >> 1) * l : WT + (d >> 1) * l;
+        double acc = 0.0;
+        for (int kk = 32 * clo + ln; kk < l; kk += 32) acc = fma(vec[kk], VV[kk], acc);
+        acc = warp_sum(acc);
+        if (ln == 0) dots[d] = acc;
+      }
+    }
+    __syncthreads();
+    TD3_MARK(2);
+    // (3) p_i of own rows, pushed into every CTA; the step's barrier
+    if (tid < nloc) {
+      const int i = tid * CL + r;
+      if (i > j) {
+        double c0 = 0.0, c1 = 0.0;
+        for (int s2 = 0; s2 < t; ++s2) {
+          c0 += VT[s2 * l + i] * dots[2 * s2];
+          c1 += WT[s2 * l + i] * dots[2 * s2 + 1];
+        }
+        const double p = beta * (YO[tid] - (c0 + c1));
+#pragma unroll
+        for (int c = 0; c < CL; ++c) PXr[c][par * l + i] = p;
+      }
+    }
+    cluster_arrive();
+    cluster_wait();
+    TD3_MARK(3);
+    // (4) K = β vᵀp / 2
+    const double pk = (k < l && k > j) ? PX[par * l + k] : 0.0;
+    double kp = warp_sum(pk * vk);
+    if (ln == 0) redk[wid] = kp;
+    __syncthreads();
+    double K = 0.0;
+#pragma unroll
+    for (int w = 0; w < T3W; ++w) K += redk[w];
+    K *= 0.5 * beta;
+    TD3_MARK(4);
+    // (5) w = p − K v (W column t; zeros at k <= j)
+    const double wk = (k < l && k > j) ? pk - K * vk : 0.0;
+    if (k < l) WT[t * l + k] = wk;
+    const int jn = j + 1;
+    ++t;
+    if (t == NB || jn + 2 >= l) {
+      // panel end: own rows −= V Wᵀ + W Vᵀ (columns >= jn), then the owners
+      // push the next panel's rows to every CTA
+      __syncthreads();
+      const int tn = t;
+      const int li0 = (jn - r <= 0) ? 0 : (jn - r + CL - 1) / CL;  // first own row >= jn
+      for (int c = jn >> 5; c < nch; ++c) {
+        const int kc = 32 * c + ln;
+        double vkc[NB], wkc[NB];
+#pragma unroll
+        for (int s2 = 0; s2 < NB; ++s2) {
+          vkc[s2] = (s2 < tn && kc < l) ? VT[s2 * l + kc] : 0.0;
+          wkc[s2] = (s2 < tn && kc < l) ? WT[s2 * l + kc] : 0.0;
+        }
+        for (int li = li0 + wid; li < nloc; li += T3W) {
+          const int i = li * CL + r;
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int s2 = 0; s2 < NB; ++s2) {
+            if (s2 < tn) {
+              c0 = fma(VT[s2 * l + i], wkc[s2], c0);
+              c1 = fma(WT[s2 * l + i], vkc[s2], c1);
+            }
+          }
+          if (kc >= jn && kc < l) A[(size_t)li * lp + kc] -= c0 + c1;
+        }
+      }
+      if (jn + 2 >= l) break;
+      __syncthreads();
+      for (int q = 0; q < NB && jn + q < l; ++q) {
+        const int i = jn + q;
+        if (i % CL != r) continue;
+        const double *Ai = A + (size_t)(i / CL) * lp;
+        for (int kk = jn + tid; kk < l; kk += T3T) {
+          const double val = Ai[kk];
+#pragma unroll
+          for (int c = 0; c < CL; ++c) PRr[c][(size_t)q * lp + kk] = val;
+        }
+      }
+      cluster_arrive();
+      cluster_wait();
+      jp = jn;
+      t = 0;
+      column(jn, jp, 0, 0.0, 0.0, 0.0, 0.0);
+    } else {
+      // W[jn][t−1] = p_jn − K v_jn: p is in PX for every index
+      const double vj = VV[jn];
+      const double wj = PX[par * l + jn] - K * vj;
+      column(jn, jp, t, vk, wk, vj, wj);
+    }
+  }
+  // trailing 2×2 (or 1×1) from the fully updated rows
+  __syncthreads();
+  if (tid == 0) {
+    if (l >= 2) {
+      const int i0 = l - 2, i1 = l - 1;
+      if (i0 % CL == r) dd[i0] = A[(size_t)(i0 / CL) * lp + i0];
+      if (i1 % CL == r) {
+        ee[i0] = A[(size_t)(i1 / CL) * lp + i0];
+        dd[i1] = A[(size_t)(i1 / CL) * lp + i1];
+      }
+    } else if (r == 0) {
+      dd[0] = A[0];
+    }
+  }
+  cl.sync();
+}
+
+}  // namespace netmfp
+
+#include <cstdio>
+#include <vector>
+#include <cmath>
+using namespace netmfp;
+namespace netmfp { void set_last_error(const std::string &) {} void chol_inv_df(Ctx &, double *, int64_t, int64_t, double *, int *, double) {} }
+static void host_tridiag(std::vector<double> A, int l, std::vector<double> &d, std::vector<double> &e) {
+  d.assign(l, 0); e.assign(l, 0);
+  for (int j = 0; j + 2 < l; ++j) {
+    double ss = 0; for (int k = j + 2; k < l; ++k) ss += A[k * l + j] * A[k * l + j];
+    double x0 = A[(j + 1) * l + j], beta = 0, alpha = x0, v0 = 0;
+    if (ss > 0) { double nrm = sqrt(ss + x0 * x0); alpha = x0 >= 0 ? -nrm : nrm; v0 = x0 - alpha; beta = 2.0 / (ss + v0 * v0); }
+    std::vector<double> v(l, 0), p(l, 0), w(l, 0);
+    if (ss > 0) { v[j + 1] = v0; for (int k = j + 2; k < l; ++k) v[k] = A[k * l + j]; }
+    d[j] = A[j * l + j]; e[j] = alpha;
+    for (int i = j + 1; i < l; ++i) { double s = 0; for (int k = j + 1; k < l; ++k) s += A[i * l + k] * v[k]; p[i] = beta * s; }
+    double K = 0; for (int k = j + 1; k < l; ++k) K += p[k] * v[k]; K *= 0.5 * beta;
+    for (int k = j + 1; k < l; ++k) w[k] = p[k] - K * v[k];
+    for (int i = j + 1; i < l; ++i) for (int k = j + 1; k < l; ++k) A[i * l + k] -= v[i] * w[k] + w[i] * v[k];
+  }
+  if (l >= 2) { d[l - 2] = A[(l - 2) * l + l - 2]; e[l - 2] = A[(l - 1) * l + l - 2]; d[l - 1] = A[(l - 1) * l + l - 1]; }
+  else d[0] = A[0];
+}
+int main(int argc, char **argv) {
+  const int l = argc > 1 ? atoi(argv[1]) : 64;
+  const int reps = argc > 2 ? atoi(argv[2]) : 3;
+  std::vector<double> h(l * l);
+  unsigned s = 12345;
+  for (int i = 0; i < l; ++i) for (int j = 0; j <= i; ++j) { s = s * 1664525u + 1013904223u; h[i * l + j] = h[j * l + i] = (s >> 8) / 16777216.0 - 0.5; }
+  std::vector<double> hd, he; host_tridiag(h, l, hd, he);
+  double *S, *d, *e, *Hv, *hb;
+  cudaMalloc(&S, l * l * 8); cudaMalloc(&d, l * 8); cudaMalloc(&e, l * 8); cudaMalloc(&Hv, l * l * 8); cudaMalloc(&hb, l * 8);
+  cudaMemcpy(S, h.data(), l * l * 8, cudaMemcpyHostToDevice);
+  const size_t smem = Td3<TCL, TNB>::smem_doubles(l) * 8;
+  cudaFuncSetAttribute(k_tridiag3<TCL, TNB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  std::vector<double> gd(l), ge(l), gd0, ge0;
+  for (int r = 0; r < reps; ++r) {
+    cudaMemset(d, 0, l * 8); cudaMemset(e, 0, l * 8);
+    k_tridiag3<TCL, TNB><<<TCL, T3T, smem>>>(S, l, d, e, Hv, hb);
+    cudaError_t err = cudaDeviceSynchronize();
+    if (err != cudaSuccess) { printf("err %s\n", cudaGetErrorString(err)); return 1; }
+    cudaMemcpy(gd.data(), d, l * 8, cudaMemcpyDeviceToHost); cudaMemcpy(ge.data(), e, l * 8, cudaMemcpyDeviceToHost);
+    int first = -1; double mx = 0;
+    for (int j = 0; j < l; ++j) {
+      double dd = fabs(gd[j] - hd[j]) + (j + 1 < l ? fabs(fabs(ge[j]) - fabs(he[j])) : 0);
+      if (dd > 1e-9 && first < 0) first = j;
+      mx = fmax(mx, dd);
+    }
+    bool same = r == 0 || (gd == gd0 && ge == ge0);
+    printf("l=%d rep %d: first diverging step %d, max diff %.3e, repeat-identical %d\n", l, r, first, mx, (int)same);
+    if (first >= 0 && r == 0) for (int j = std::max(0, first - 1); j < std::min(l, first + 3); ++j) printf("  j=%d d %.12f vs %.12f  e %.12f vs %.12f\n", j, gd[j], hd[j], ge[j], he[j]);
+    if (r == 0) { gd0 = gd; ge0 = ge; }
+  }
+  static unsigned long long t[6][512];
+  cudaMemcpyFromSymbol(t, g_td3_t, sizeof(t));
+  double a[5] = {0, 0, 0, 0, 0};
+  int n = 0;
+  for (int j = 2; j + 4 < l && j < 500; ++j) {
+    for (int p = 0; p < 4; ++p) a[p] += (double)(t[p + 1][j] - t[p][j]);
+    a[4] += (double)(t[0][j + 1] - t[4][j]);
+    ++n;
+  }
+  printf("CL %d NB %d per step cycles (CTA 0): reflector+v %.0f  matvec %.0f  reduce+push+cluster barrier %.0f  p,K %.0f  w+next column(+panel) %.0f  total %.0f\n",
+         TCL, TNB, a[0] / n, a[1] / n, a[2] / n, a[3] / n, a[4] / n, (a[0] + a[1] + a[2] + a[3] + a[4]) / n);
+  return 0;
+}

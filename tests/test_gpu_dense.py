@@ -81,7 +81,7 @@ def _check_eig(L, ctx, S, abs_order=True):
     assert np.abs(S @ Vg - Vg * lg[None, :]).max() <= 1e-9 * nrm
 
 
-@pytest.mark.parametrize("l", [1, 2, 3, 5, 42, 158, 286, 460])
+@pytest.mark.parametrize("l", [1, 2, 3, 4, 5, 7, 13, 42, 158, 228, 255, 256, 257, 286, 287, 288, 289, 460])
 def test_sym_eig_random(L, ctx, l):
     A = np.random.default_rng(l).standard_normal((l, l))
     _check_eig(L, ctx, (A + A.T) / 2)
@@ -109,7 +109,7 @@ def test_sym_eig_graph_ritz(L, ctx):
     _check_eig(L, ctx, (S + S.T) / 2)
 
 
-@pytest.mark.parametrize("l", [17, 286, 460])
+@pytest.mark.parametrize("l", [17, 228, 286, 460])
 def test_sym_eig_repeatable(L, ctx, l):
     """The cluster tridiagonalisation exchanges data through other CTAs' shared
     memory with a fixed reduction order: repeated runs must agree bit for bit
