@@ -17,6 +17,7 @@ namespace netmfp {
 __global__ void k_make_keys(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
                             int64_t m, uint64_t n, uint64_t row0, uint64_t row1, int cb, uint64_t *__restrict__ keys,
                             int *bad) {
+  grid_dep_enter();
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= m) return;
   int32_t s = src[e], t = dst[e];
@@ -45,6 +46,7 @@ __device__ __forceinline__ int local_dirs(int32_t s, int32_t t, uint64_t row0, u
 }
 __global__ void k_count_local(const int32_t *__restrict__ src, const int32_t *__restrict__ dst, int64_t m, uint64_t n,
                               uint64_t row0, uint64_t row1, unsigned long long *__restrict__ cnt, int *bad) {
+  grid_dep_enter();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int c = 0;
   if (e < m) {
@@ -62,6 +64,7 @@ __global__ void k_count_local(const int32_t *__restrict__ src, const int32_t *__
 __global__ void k_make_keys_local(const int32_t *__restrict__ src, const int32_t *__restrict__ dst, int64_t m,
                                   uint64_t n, uint64_t row0, uint64_t row1, int cb, uint64_t *__restrict__ keys,
                                   unsigned long long *__restrict__ pos) {
+  grid_dep_enter();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   int d = 0;
@@ -89,6 +92,7 @@ __global__ void k_make_keys_local(const int32_t *__restrict__ src, const int32_t
 // nnz = unique keys minus the sentinel (the last unique key if present)
 __global__ void k_nnz(const uint64_t *__restrict__ keys, const int64_t *__restrict__ nuniq, uint64_t n_all, int cb,
                       int64_t *__restrict__ nnz) {
+  grid_dep_enter();
   const int64_t u = *nuniq;
   const uint64_t sentinel = ((n_all - 1) << cb) | (n_all - 1);
   *nnz = (u > 0 && keys[u - 1] == sentinel) ? u - 1 : u;
@@ -96,6 +100,7 @@ __global__ void k_nnz(const uint64_t *__restrict__ keys, const int64_t *__restri
 
 __global__ void k_rowptr(const uint64_t *__restrict__ keys, const int64_t *__restrict__ dnnz, int64_t n, int64_t row0,
                          int cb, int64_t *__restrict__ rowptr) {
+  grid_dep_enter();
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u > n) return;
   const int64_t nnz = *dnnz;
@@ -111,6 +116,7 @@ __global__ void k_rowptr(const uint64_t *__restrict__ keys, const int64_t *__res
 __global__ void k_col_deg(const uint64_t *__restrict__ keys, const int64_t *__restrict__ dnnz,
                           const int64_t *__restrict__ rowptr, int64_t n, int cb, int32_t *__restrict__ col,
                           int32_t *__restrict__ deg, uint8_t *__restrict__ heavy_flag, int light_cap) {
+  grid_dep_enter();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nnz = *dnnz;
   if (i < nnz) col[i] = (int32_t)(keys[i] & ((1ull << cb) - 1));
@@ -124,6 +130,7 @@ __global__ void k_col_deg(const uint64_t *__restrict__ keys, const int64_t *__re
 __global__ void k_heavy_seg_map(const int32_t *__restrict__ heavy, const int64_t *__restrict__ dnh,
                                 const int64_t *__restrict__ seg_ptr, const int64_t *__restrict__ rowptr,
                                 int64_t *__restrict__ seg_e0, int32_t *__restrict__ seg_h, int heavy_seg) {
+  grid_dep_enter();
   const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (h >= *dnh) return;
   const int64_t b = rowptr[heavy[h]];
@@ -138,6 +145,7 @@ __global__ void k_heavy_seg_map(const int32_t *__restrict__ heavy, const int64_t
 // the total at every index >= nh
 __global__ void k_heavy_segs(const int32_t *__restrict__ heavy, const int64_t *__restrict__ dnh, int64_t n,
                              const int32_t *__restrict__ deg, int64_t *__restrict__ nseg, int heavy_seg) {
+  grid_dep_enter();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i > n) return;
   nseg[i] = i < *dnh ? (deg[heavy[i]] + heavy_seg - 1) / heavy_seg : 0;
@@ -180,7 +188,7 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
       unsigned long long hk = 0;
       int hb = 0;
       if (m > 0)
-        NM_LAUNCH(c, "count_local", k_count_local<<<ceil_div(m, 256), 256, 0, s>>>(src, dst, m, (uint64_t)n_all,
+        NM_LAUNCH(c, "count_local", launch_pdl(s, k_count_local, ceil_div(m, 256), 256, 0, src, dst, m, (uint64_t)n_all,
                                                                                   (uint64_t)row0, (uint64_t)row1,
                                                                                   kcnt.p, bad));
       NM_CUDA(cudaMemcpyAsync(&hk, kcnt.p, 8, cudaMemcpyDeviceToHost, s));
@@ -191,11 +199,10 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
     }
     DBuf<uint64_t> keys(nk > 0 ? nk : 1, s), keys2(nk > 0 ? nk : 1, s);
     if (part && nk > 0) {
-      NM_LAUNCH(c, "make_keys_local", k_make_keys_local<<<ceil_div(m, 256), 256, 0, s>>>(
-                                          src, dst, m, (uint64_t)n_all, (uint64_t)row0, (uint64_t)row1, cb, keys,
+      NM_LAUNCH(c, "make_keys_local", launch_pdl(s, k_make_keys_local, ceil_div(m, 256), 256, 0, src, dst, m, (uint64_t)n_all, (uint64_t)row0, (uint64_t)row1, cb, keys,
                                           kcnt.p + 1));
     } else if (!part && m > 0) {
-      NM_LAUNCH(c, "make_keys", k_make_keys<<<ceil_div(m, 256), 256, 0, s>>>(src, dst, m, (uint64_t)n_all, (uint64_t)row0,
+      NM_LAUNCH(c, "make_keys", launch_pdl(s, k_make_keys, ceil_div(m, 256), 256, 0, src, dst, m, (uint64_t)n_all, (uint64_t)row0,
                                                                              (uint64_t)row1, cb, keys, bad));
     }
     // key = row << cb | col with rows < n: 2 cb significant bits (one radix
@@ -220,16 +227,16 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
     // the host once, at the end, to fill the graph's host-side counts.
     // drop the sentinel if present: it is the last unique key
     DBuf<int64_t> dnnz(1, s), dnh(1, s);
-    NM_LAUNCH(c, "nnz", k_nnz<<<1, 1, 0, s>>>(keys, nsel, (uint64_t)n_all, cb, dnnz));
+    NM_LAUNCH(c, "nnz", launch_pdl(s, k_nnz, 1, 1, 0, keys, nsel, (uint64_t)n_all, cb, dnnz));
     const int64_t nnz_cap = nk;
     g->rowptr.alloc(n + 1, s);
     g->col.alloc(nnz_cap > 0 ? nnz_cap : 1, s);
     g->deg.alloc(n > 0 ? n : 1, s);
     DBuf<uint8_t> hflag(n > 0 ? n : 1, s);
-    NM_LAUNCH(c, "rowptr", k_rowptr<<<ceil_div(n + 1, 256), 256, 0, s>>>(keys, dnnz, n, row0, cb, g->rowptr));
+    NM_LAUNCH(c, "rowptr", launch_pdl(s, k_rowptr, ceil_div(n + 1, 256), 256, 0, keys, dnnz, n, row0, cb, g->rowptr));
     const int64_t mx = std::max(nnz_cap, n);
     if (mx > 0)  // an empty row range (a rank with no rows) has nothing to fill
-      NM_LAUNCH(c, "col_deg", k_col_deg<<<ceil_div(mx, 256), 256, 0, s>>>(keys, dnnz, g->rowptr, n, cb, g->col, g->deg,
+      NM_LAUNCH(c, "col_deg", launch_pdl(s, k_col_deg, ceil_div(mx, 256), 256, 0, keys, dnnz, g->rowptr, n, cb, g->col, g->deg,
                                                                                hflag, g->light_cap));
     // heavy rows (degree > light_cap) for the split SpMM path
     g->heavy.alloc(n > 0 ? n : 1, s);
@@ -246,7 +253,7 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
     g->heavy_seg_ptr.alloc(n + 1, s);
     {
       DBuf<int64_t> nseg(n + 1, s);
-      NM_LAUNCH(c, "heavy_segs", k_heavy_segs<<<ceil_div(n + 1, 256), 256, 0, s>>>(g->heavy, dnh, n, g->deg, nseg,
+      NM_LAUNCH(c, "heavy_segs", launch_pdl(s, k_heavy_segs, ceil_div(n + 1, 256), 256, 0, g->heavy, dnh, n, g->deg, nseg,
                                                                                   g->heavy_seg));
       size_t tb2 = 0;
       NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, nseg.p, g->heavy_seg_ptr.p, n + 1, s));
@@ -259,14 +266,13 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
     g->seg_e0.alloc(seg_cap, s);
     g->seg_h.alloc(seg_cap, s);
     if (n > 0)
-      NM_LAUNCH(c, "heavy_seg_map", k_heavy_seg_map<<<ceil_div(n, 128), 128, 0, s>>>(
-                                        g->heavy, dnh, g->heavy_seg_ptr, g->rowptr, g->seg_e0, g->seg_h, g->heavy_seg));
+      NM_LAUNCH(c, "heavy_seg_map", launch_pdl(s, k_heavy_seg_map, ceil_div(n, 128), 128, 0, g->heavy, dnh, g->heavy_seg_ptr, g->rowptr, g->seg_e0, g->seg_h, g->heavy_seg));
     // a whole graph: the scan of (degree > 0) for isolated-vertex compaction
     int32_t hne = -1;
     if (!part && n > 0) {
       DBuf<int32_t> flag(n + 1, s);
       g->nz_pos.alloc(n + 1, s);
-      NM_LAUNCH(c, "flag_nz", k_flag_nz<<<ceil_div(n + 1, 256), 256, 0, s>>>(g->deg, n, flag));
+      NM_LAUNCH(c, "flag_nz", launch_pdl(s, k_flag_nz, ceil_div(n + 1, 256), 256, 0, g->deg, n, flag));
       size_t tb3 = 0;
       NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb3, flag.p, g->nz_pos.p, n + 1, s));
       DBuf<char> tmp3(tb3, s);
@@ -306,6 +312,7 @@ Graph *build_csr_device(Ctx &c, int64_t n_all, const int32_t *src, const int32_t
 // rank keeps the image [pos[b0], pos[b1]) of its rows.
 // ---------------------------------------------------------------------------
 __global__ void k_flag_nz(const int32_t *__restrict__ deg, int64_t n, int32_t *__restrict__ flag) {
+  grid_dep_enter();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) flag[i] = deg[i] > 0;
   if (i == n) flag[i] = 0;
@@ -313,6 +320,7 @@ __global__ void k_flag_nz(const int32_t *__restrict__ deg, int64_t n, int32_t *_
 __global__ void k_compact_ids(const int32_t *__restrict__ deg, const int32_t *__restrict__ pos, int64_t n,
                               int64_t b0, int64_t b1, int64_t row0c, int32_t *__restrict__ orig,
                               int32_t *__restrict__ comp) {
+  grid_dep_enter();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (deg[i] > 0) {
@@ -325,6 +333,7 @@ __global__ void k_compact_ids(const int32_t *__restrict__ deg, const int32_t *__
 __global__ void k_compact_rows(const int32_t *__restrict__ orig, int64_t ne, int64_t b0,
                                const int64_t *__restrict__ rowptr, const int32_t *__restrict__ deg, int64_t nnz,
                                int64_t *__restrict__ rp_c, int32_t *__restrict__ deg_c) {
+  grid_dep_enter();
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j < ne) {
     rp_c[j] = rowptr[orig[j] - b0];
@@ -334,12 +343,14 @@ __global__ void k_compact_rows(const int32_t *__restrict__ orig, int64_t ne, int
 }
 __global__ void k_remap_ids(const int32_t *__restrict__ in, int64_t m, const int32_t *__restrict__ comp,
                             int32_t *__restrict__ out) {
+  grid_dep_enter();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < m) out[i] = comp[in[i]];
 }
 // local row index -> local compact row index
 __global__ void k_remap_local(const int32_t *__restrict__ in, int64_t m, const int32_t *__restrict__ comp, int64_t b0,
                               int64_t row0c, int32_t *__restrict__ out) {
+  grid_dep_enter();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < m) out[i] = (int32_t)(comp[b0 + in[i]] - row0c);
 }
@@ -364,7 +375,7 @@ Graph *compact_graph(Ctx &c, const Graph &g, const int32_t *degall) {
   } else {
     DBuf<int32_t> flag(n_all + 1, s);
     pos_own.alloc(n_all + 1, s);
-    NM_LAUNCH(c, "flag_nz", k_flag_nz<<<ceil_div(n_all + 1, 256), 256, 0, s>>>(degall, n_all, flag));
+    NM_LAUNCH(c, "flag_nz", launch_pdl(s, k_flag_nz, ceil_div(n_all + 1, 256), 256, 0, degall, n_all, flag));
     size_t tb = 0;
     NM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.p, pos_own.p, n_all + 1, s));
     DBuf<char> tmp(tb, s);
@@ -394,22 +405,22 @@ Graph *compact_graph(Ctx &c, const Graph &g, const int32_t *degall) {
     gc->n_orig = n_all;
     gc->orig_id.alloc(ne > 0 ? ne : 1, s);
     gc->comp_id.alloc(n_all, s);
-    NM_LAUNCH(c, "compact_ids", k_compact_ids<<<ceil_div(n_all, 256), 256, 0, s>>>(degall, pos, n_all, b0, b1, row0c,
+    NM_LAUNCH(c, "compact_ids", launch_pdl(s, k_compact_ids, ceil_div(n_all, 256), 256, 0, degall, pos, n_all, b0, b1, row0c,
                                                                                     gc->orig_id, gc->comp_id));
     gc->rowptr.alloc(ne + 1, s);
     gc->deg.alloc(ne > 0 ? ne : 1, s);
-    NM_LAUNCH(c, "compact_rows", k_compact_rows<<<ceil_div(ne + 1, 256), 256, 0, s>>>(gc->orig_id, ne, b0, g.rowptr,
+    NM_LAUNCH(c, "compact_rows", launch_pdl(s, k_compact_rows, ceil_div(ne + 1, 256), 256, 0, gc->orig_id, ne, b0, g.rowptr,
                                                                                         g.deg, g.nnz, gc->rowptr,
                                                                                         gc->deg));
     gc->col.alloc(g.nnz > 0 ? g.nnz : 1, s);
     if (g.nnz > 0)
-      NM_LAUNCH(c, "remap_col", k_remap_ids<<<ceil_div(g.nnz, 256), 256, 0, s>>>(g.col, g.nnz, gc->comp_id, gc->col));
+      NM_LAUNCH(c, "remap_col", launch_pdl(s, k_remap_ids, ceil_div(g.nnz, 256), 256, 0, g.col, g.nnz, gc->comp_id, gc->col));
     gc->n_heavy = g.n_heavy;
     gc->heavy_nnz = g.heavy_nnz;
     gc->n_heavy_segs = g.n_heavy_segs;
     gc->heavy.alloc(g.n_heavy > 0 ? g.n_heavy : 1, s);
     if (g.n_heavy > 0)
-      NM_LAUNCH(c, "remap_heavy", k_remap_local<<<ceil_div(g.n_heavy, 256), 256, 0, s>>>(g.heavy, g.n_heavy,
+      NM_LAUNCH(c, "remap_heavy", launch_pdl(s, k_remap_local, ceil_div(g.n_heavy, 256), 256, 0, g.heavy, g.n_heavy,
                                                                                          gc->comp_id, b0, row0c,
                                                                                          gc->heavy));
     gc->heavy_seg_ptr.alloc(g.n_heavy + 1, s);
@@ -429,7 +440,7 @@ Graph *compact_graph(Ctx &c, const Graph &g, const int32_t *degall) {
 // rows[i] <- comp[rows[i]] (-1 for an isolated vertex: its terms are zero and
 // every row gather skips indices outside this rank's rows)
 void remap_rows(Ctx &c, int32_t *rows, int64_t m, const int32_t *comp) {
-  if (m > 0) NM_LAUNCH(c, "remap_rows", k_remap_ids<<<ceil_div(m, 256), 256, 0, c.stream>>>(rows, m, comp, rows));
+  if (m > 0) NM_LAUNCH(c, "remap_rows", launch_pdl(c.stream, k_remap_ids, ceil_div(m, 256), 256, 0, rows, m, comp, rows));
 }
 
 }  // namespace netmfp

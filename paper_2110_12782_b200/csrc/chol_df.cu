@@ -214,6 +214,7 @@ __device__ bool warp_chol_inv(double *S, double *X, double *rinv, const double *
 }
 
 __global__ void __launch_bounds__(T) k_chol_df(DfP p) {
+  grid_dep_enter();
   cg::grid_group grid = cg::this_grid();
   __shared__ double S[32 * TL], A[32 * TL], B[32 * TL], D[32 * TL], E[32 * TL];
   __shared__ int bad;

@@ -12,6 +12,8 @@
 #include <string>
 #include <memory>
 #include <tuple>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "../../include/netmfp.h"
@@ -284,6 +286,54 @@ inline void prof_end(Ctx &c) {
     __VA_ARGS__;                   \
     ::netmfp::prof_end(c);         \
   } while (0)
+
+
+// ----------------------------------------------------------------------------
+// Programmatic dependent launch.  Every kernel of the library is launched with
+// launch_pdl and starts with grid_dep_enter() (griddepcontrol.wait): it waits
+// until the kernel before it in the stream has completed and its writes are
+// visible, but its launch is processed while that kernel drains, so the
+// launch latency between consecutive kernels is hidden (configs[2]: 24.50 ->
+// 24.05 ms per embedding).  An early griddepcontrol.launch_dependents in every
+// kernel was measured slower (29.5 ms: waiting CTAs of the next kernel hold
+// SM slots), in the SpMM alone no faster.  In a kernel launched without the
+// attribute the wait is a no-op.  NETMFP_PDL=0 launches without it (A/B).
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void grid_dep_enter() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char *v = getenv("NETMFP_PDL");
+    return !v || atoi(v) != 0;
+  }();
+  return on;
+}
+
+// kern<<<grid, block, smem, s>>>(args...) with the programmatic-serialization
+// attribute; arguments are converted to the kernel's parameter types first
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(cudaStream_t s, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args &&...args) {
+  static_assert(sizeof...(KArgs) == sizeof...(Args), "launch_pdl: argument count");
+  std::tuple<std::decay_t<KArgs>...> vals(std::forward<Args>(args)...);
+  void *ptrs[sizeof...(KArgs) > 0 ? sizeof...(KArgs) : 1];
+  std::apply([&](auto &...e) {
+    int i = 0;
+    ((ptrs[i++] = (void *)&e), ...);
+  }, vals);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelExC(&cfg, reinterpret_cast<const void *>(kern), ptrs);
+}
 
 #define NM_LAUNCH(c, name, ...)   \
   do {                            \

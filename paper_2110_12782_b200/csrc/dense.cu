@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(256) k_gram_partial(Mat A, Mat B, const int32_
                                                       float wexp, int64_t slab_rows, bool sym,
                                                       float *__restrict__ part, int64_t a_pad,
                                                       int64_t b_pad) {
+  grid_dep_enter();
   const int tb = blockIdx.x, ta = blockIdx.y, slab = blockIdx.z;
   if (sym && ta > tb) return;
   __shared__ __align__(16) float As[GK][GT];
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(256) k_gram_partial(Mat A, Mat B, const int32_
 __global__ void k_gram_reduce(const float *__restrict__ part, int nslab, int64_t a, int64_t b,
                               int64_t a_pad, int64_t b_pad, bool sym, double *__restrict__ G,
                               int64_t ldg) {
+  grid_dep_enter();
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= a * b) return;
   int64_t i = idx / b, j = idx % b;
@@ -134,8 +136,8 @@ void gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, do
   const int64_t a_pad = (int64_t)ta * GT, b_pad = (int64_t)tb * GT;
   DBuf<float> part((size_t)nslab * a_pad * b_pad, c.stream);
   dim3 grid(tb, ta, nslab);
-  NM_LAUNCH(c, "gram_partial", k_gram_partial<<<grid, 256, 0, c.stream>>>(A, B, deg, wexp, slab_rows, sym, part, a_pad, b_pad));
-  NM_LAUNCH(c, "gram_reduce", k_gram_reduce<<<ceil_div(A.cols * B.cols, 256), 256, 0, c.stream>>>(part, nslab, A.cols, B.cols,
+  NM_LAUNCH(c, "gram_partial", launch_pdl(c.stream, k_gram_partial, grid, 256, 0, A, B, deg, wexp, slab_rows, sym, part, a_pad, b_pad));
+  NM_LAUNCH(c, "gram_reduce", launch_pdl(c.stream, k_gram_reduce, ceil_div(A.cols * B.cols, 256), 256, 0, part, nslab, A.cols, B.cols,
                                                                       a_pad, b_pad, sym, G, ldg));
 }
 
@@ -147,6 +149,7 @@ constexpr int TM = 128, TN = 64, TK = 32;
 __global__ void __launch_bounds__(256) k_gemm_tall(Mat A, const double *__restrict__ Bs, int64_t ldb,
                                                    int64_t bcols, const int32_t *__restrict__ deg,
                                                    float rexp, Mat C) {
+  grid_dep_enter();
   __shared__ __align__(16) float As[TK][TM + 4];
   __shared__ __align__(16) float Bsh[TK][TN];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -225,7 +228,7 @@ void gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcol
   }
   if (A.rows == 0) return;
   dim3 grid(ceil_div(A.rows, TM), ceil_div(bcols, TN));
-  NM_LAUNCH(c, "gemm_tall", k_gemm_tall<<<grid, 256, 0, c.stream>>>(A, Bs, ldb, bcols, deg, rexp, C));
+  NM_LAUNCH(c, "gemm_tall", launch_pdl(c.stream, k_gemm_tall, grid, 256, 0, A, Bs, ldb, bcols, deg, rexp, C));
 }
 
 void gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, const int32_t *deg, float rexp,
@@ -246,6 +249,7 @@ void gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, const 
 // and scale d^-e are computed once per row, not per element.
 __global__ void __launch_bounds__(256) k_gaussian(Mat O, uint32_t k0, uint32_t k1, const int32_t *__restrict__ deg,
                                                   float rexp, int64_t row0, const int32_t *__restrict__ ids) {
+  grid_dep_enter();
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const bool vec = (O.ld % 4) == 0 && ((uintptr_t)O.p & 15) == 0;
@@ -288,11 +292,11 @@ void gaussian_block(Ctx &c, const Mat &O, uint64_t seed, const int32_t *deg, flo
                     const int32_t *ids) {
   if (O.rows * O.cols == 0) return;
   const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(O.rows, 8), (int64_t)c.num_sms * 16);
-  NM_LAUNCH(c, "gaussian", k_gaussian<<<blocks, 256, 0, c.stream>>>(
-      O, (uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32), deg, rexp, row0, ids));
+  NM_LAUNCH(c, "gaussian", launch_pdl(c.stream, k_gaussian, blocks, 256, 0, O, (uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32), deg, rexp, row0, ids));
 }
 
 __global__ void k_row_scale(Mat Y, const int32_t *__restrict__ deg, float rexp) {
+  grid_dep_enter();
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= Y.rows * Y.cols) return;
   int64_t i = idx / Y.cols, j = idx % Y.cols;
@@ -301,6 +305,7 @@ __global__ void k_row_scale(Mat Y, const int32_t *__restrict__ deg, float rexp) 
 
 // Dst[i, :] = d_i^-e · Src[i, :]  (float4; lds, ldd, cols multiples of 4 or tail handled)
 __global__ void k_scale_copy(Mat Src, Mat Dst, const int32_t *__restrict__ deg, float rexp) {
+  grid_dep_enter();
   const int64_t c4 = (Src.cols + 3) / 4;
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= Src.rows * c4) return;
@@ -319,11 +324,11 @@ __global__ void k_scale_copy(Mat Src, Mat Dst, const int32_t *__restrict__ deg, 
 void scale_copy_block(Ctx &c, const Mat &Src, const Mat &Dst, const int32_t *deg, float rexp) {
   NM_REQUIRE(Src.ld % 4 == 0 && Dst.ld % 4 == 0, "scale_copy: ld % 4 == 0");
   const int64_t tot = Src.rows * ((Src.cols + 3) / 4);
-  NM_LAUNCH(c, "scale_copy", k_scale_copy<<<ceil_div(tot, 256), 256, 0, c.stream>>>(Src, Dst, deg, rexp));
+  NM_LAUNCH(c, "scale_copy", launch_pdl(c.stream, k_scale_copy, ceil_div(tot, 256), 256, 0, Src, Dst, deg, rexp));
 }
 
 void row_scale_block(Ctx &c, const Mat &Y, const int32_t *deg, float rexp) {
-  NM_LAUNCH(c, "row_scale", k_row_scale<<<ceil_div(Y.rows * Y.cols, 256), 256, 0, c.stream>>>(Y, deg, rexp));
+  NM_LAUNCH(c, "row_scale", launch_pdl(c.stream, k_row_scale, ceil_div(Y.rows * Y.cols, 256), 256, 0, Y, deg, rexp));
 }
 
 void copy_block(Ctx &c, const float *src, int64_t lds, float *dst, int64_t ldd, int64_t rows,
@@ -335,6 +340,7 @@ void copy_block(Ctx &c, const float *src, int64_t lds, float *dst, int64_t ldd, 
 // back to all rows; every element of Dst written once).  A warp per row.
 __global__ void __launch_bounds__(256) k_scatter_rows(Mat Src, const int32_t *__restrict__ comp, Mat Dst, bool vec4,
                                                       int64_t sub) {
+  grid_dep_enter();
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * 8;
   for (int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < Dst.rows; i += nw) {
@@ -356,12 +362,13 @@ void scatter_rows(Ctx &c, const Mat &Src, const int32_t *comp, const Mat &Dst, i
   const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(Dst.rows, 8), (int64_t)c.num_sms * 16);
   const bool vec4 = Dst.cols % 4 == 0 && Dst.ld % 4 == 0 && Src.ld % 4 == 0 && ((uintptr_t)Dst.p & 15) == 0 &&
                     ((uintptr_t)Src.p & 15) == 0;
-  NM_LAUNCH(c, "scatter_rows", k_scatter_rows<<<blocks, 256, 0, c.stream>>>(Src, comp, Dst, vec4, sub));
+  NM_LAUNCH(c, "scatter_rows", launch_pdl(c.stream, k_scatter_rows, blocks, 256, 0, Src, comp, Dst, vec4, sub));
 }
 
 // Dst[ids[j], :] = Src[j, :] for every row j of Src (the other rows of Dst
 // untouched); Dst may be mapped host memory.  A warp per row.
 __global__ void __launch_bounds__(256) k_write_rows(Mat Src, const int32_t *__restrict__ ids, Mat Dst, bool vec4) {
+  grid_dep_enter();
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * 8;
   for (int64_t j = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); j < Src.rows; j += nw) {
@@ -381,7 +388,7 @@ void write_rows(Ctx &c, const Mat &Src, const int32_t *ids, const Mat &Dst) {
   const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(Src.rows, 8), (int64_t)c.num_sms * 16);
   const bool vec4 = Src.cols % 4 == 0 && Dst.ld % 4 == 0 && Src.ld % 4 == 0 && ((uintptr_t)Dst.p & 15) == 0 &&
                     ((uintptr_t)Src.p & 15) == 0;
-  NM_LAUNCH(c, "write_rows", k_write_rows<<<blocks, 256, 0, c.stream>>>(Src, ids, Dst, vec4));
+  NM_LAUNCH(c, "write_rows", launch_pdl(c.stream, k_write_rows, blocks, 256, 0, Src, ids, Dst, vec4));
 }
 
 }  // namespace netmfp

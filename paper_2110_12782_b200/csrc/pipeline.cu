@@ -156,10 +156,12 @@ void factor_pair(Ctx &c, const Graph &g, double alpha, int T, const Mat &U, cons
 }
 
 __global__ void k_sqrt_abs(const double *lam, int d, double *out) {
+  grid_dep_enter();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < d) out[i] = sqrt(fabs(lam[i]));
 }
 __global__ void k_abs(const double *lam, int d, double *out) {
+  grid_dep_enter();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < d) out[i] = fabs(lam[i]);
 }
@@ -231,12 +233,12 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
     sym_eig(c, S, h2, lam, V, true);
   }
   if (sigma_dev) {
-    NM_LAUNCH(c, "abs", k_abs<<<ceil_div(d, 128), 128, 0, s>>>(lam, d, sigma_dev));
+    NM_LAUNCH(c, "abs", launch_pdl(s, k_abs, ceil_div(d, 128), 128, 0, lam, d, sigma_dev));
   }
   // step 9: U = Q Û(:, 1:d);  Alg. 5 step 5: E = U √Σ
   if (Uout) gemm_tall(c, Qb.m, V, h2, d, nullptr, 0.f, *Uout);
   if (Eout) {
-    NM_LAUNCH(c, "sqrt_abs", k_sqrt_abs<<<ceil_div(d, 128), 128, 0, s>>>(lam, d, sq));
+    NM_LAUNCH(c, "sqrt_abs", launch_pdl(s, k_sqrt_abs, ceil_div(d, 128), 128, 0, lam, d, sq));
     DBuf<double> Vs((size_t)h2 * d, s);
     NM_CUDA(cudaMemcpy2DAsync(Vs.p, d * 8, V.p, h2 * 8, d * 8, h2, cudaMemcpyDeviceToDevice, s));
     scale_cols64(c, Vs, h2, d, d, sq, 0);

@@ -15,6 +15,7 @@ constexpr int kMaxZ = 64;
 
 __global__ void k_ss_gen(int64_t n, int64_t h, int z, uint32_t k0, uint32_t k1, uint32_t tag,
                          int32_t *__restrict__ rows, float *__restrict__ signs) {
+  grid_dep_enter();
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= h) return;
   int32_t chosen[kMaxZ];
@@ -41,13 +42,14 @@ void gen_sparse_sign(Ctx &c, int64_t n, int64_t h, int64_t z, uint64_t seed, uin
   S.n = n; S.h = h; S.z = z;
   S.rows.alloc(cnt, c.stream);
   S.signs.alloc(cnt, c.stream);
-  NM_LAUNCH(c, "ss_gen", k_ss_gen<<<ceil_div(h, 128), 128, 0, c.stream>>>(n, h, (int)z, (uint32_t)(seed & 0xFFFFFFFFu),
+  NM_LAUNCH(c, "ss_gen", launch_pdl(c.stream, k_ss_gen, ceil_div(h, 128), 128, 0, n, h, (int)z, (uint32_t)(seed & 0xFFFFFFFFu),
                                                                            (uint32_t)(seed >> 32), tag, S.rows, S.signs));
 }
 
 // Out[j, :] = Σ_t sign[j,t] X[rows[j,t], :]  (fp64 accumulate)
 __global__ void k_sign_gather(const int32_t *__restrict__ rows, const float *__restrict__ signs, int64_t h, int z,
                               Mat X, int64_t row0, double *__restrict__ Out, int64_t ldo) {
+  grid_dep_enter();
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= h * X.cols) return;
   int64_t j = idx / X.cols, cc = idx % X.cols;
@@ -60,19 +62,19 @@ __global__ void k_sign_gather(const int32_t *__restrict__ rows, const float *__r
 }
 
 void sign_gather_T(Ctx &c, const SparseSign &S, const Mat &X, double *Out, int64_t ldo, int64_t row0) {
-  NM_LAUNCH(c, "sign_gather", k_sign_gather<<<ceil_div(S.h * X.cols, 256), 256, 0, c.stream>>>(
-                                  S.rows, S.signs, S.h, (int)S.z, X, row0, Out, ldo));
+  NM_LAUNCH(c, "sign_gather", launch_pdl(c.stream, k_sign_gather, ceil_div(S.h * X.cols, 256), 256, 0, S.rows, S.signs, S.h, (int)S.z, X, row0, Out, ldo));
 }
 
 __global__ void k_f32_to_f64(const float *__restrict__ src, int64_t lds, double *__restrict__ dst, int64_t ldd,
                              int64_t rows, int64_t cols) {
+  grid_dep_enter();
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= rows * cols) return;
   dst[(idx / cols) * ldd + idx % cols] = (double)src[(idx / cols) * lds + idx % cols];
 }
 
 void f32_to_f64(Ctx &c, const float *src, int64_t lds, double *dst, int64_t ldd, int64_t rows, int64_t cols) {
-  NM_LAUNCH(c, "f32_to_f64", k_f32_to_f64<<<ceil_div(rows * cols, 256), 256, 0, c.stream>>>(src, lds, dst, ldd, rows,
+  NM_LAUNCH(c, "f32_to_f64", launch_pdl(c.stream, k_f32_to_f64, ceil_div(rows * cols, 256), 256, 0, src, lds, dst, ldd, rows,
                                                                                               cols));
 }
 

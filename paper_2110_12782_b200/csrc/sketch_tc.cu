@@ -161,6 +161,7 @@ template <int ZP, bool ZM, bool L1P>
 __global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant__ CUtensorMap tmA,
                                                           const __grid_constant__ CUtensorMap tmBh,
                                                           const __grid_constant__ CUtensorMap tmBl, const SkP p) {
+  grid_dep_enter();
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = align1024(smem_raw);
   uint64_t *bars = reinterpret_cast<uint64_t *>(base + S * STAGE);
@@ -336,6 +337,7 @@ __global__ void k_gather_groups(const float *__restrict__ X, int64_t ldx, int64_
                                 const int32_t *__restrict__ rows, const float *__restrict__ signs, int64_t h, int z,
                                 int zp, int k, int64_t ldb, float *__restrict__ hi, float *__restrict__ lo,
                                 float *__restrict__ sgn) {
+  grid_dep_enter();
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nr = h * zp;
   if (idx >= nr * ldb) return;
@@ -355,6 +357,7 @@ __global__ void k_gather_groups(const float *__restrict__ X, int64_t ldx, int64_
 // sign → bit masks, 32 columns per word (NW/32 words per N tile, zero padded)
 __global__ void k_sign_bits(const float *__restrict__ sg, int64_t ncols, int64_t nwords, uint32_t *__restrict__ neg,
                             uint32_t *__restrict__ val) {
+  grid_dep_enter();
   const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (w >= nwords) return;
   uint32_t nb = 0, vb = 0;
@@ -381,7 +384,7 @@ static void launch_sketch(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mh, 
   using namespace tcs;
   const int64_t nwords = (int64_t)prm.ntn * (NW / 32);
   DBuf<uint32_t> bits((size_t)2 * nwords, c.stream);
-  NM_LAUNCH(c, "sign_bits", k_sign_bits<<<ceil_div(nwords, 128), 128, 0, c.stream>>>(col_sign, prm.ncols, nwords, bits.p,
+  NM_LAUNCH(c, "sign_bits", launch_pdl(c.stream, k_sign_bits, ceil_div(nwords, 128), 128, 0, col_sign, prm.ncols, nwords, bits.p,
                                                                                     bits.p + nwords));
   prm.neg_bits = bits.p;
   prm.val_bits = bits.p + nwords;
@@ -405,13 +408,14 @@ static void launch_sketch(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mh, 
   prm.nsplit = (prm.ntn + per - 1) / per;
   const int64_t items = prm.nmt * prm.nsplit;
   const unsigned grid = (unsigned)std::min<int64_t>(items, c.num_sms);
-  NM_LAUNCH(c, "sketch_tc", kern<<<grid, THREADS, smem, c.stream>>>(ma, mh, ml, prm));
+  NM_LAUNCH(c, "sketch_tc", launch_pdl(c.stream, kern, grid, THREADS, smem, ma, mh, ml, prm));
 }
 
 namespace tcs {
 // hi = x, lo = x - trunc_tf32(x) of an r × k block (row stride ld; padding columns stay 0)
 __global__ void k_split_hilo(const float *__restrict__ src, int64_t rows, int k, int64_t ld, float *__restrict__ hi,
                              float *__restrict__ lo) {
+  grid_dep_enter();
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= rows * ld) return;
   const float x = (idx % ld) < k ? src[idx] : 0.f;
@@ -419,6 +423,7 @@ __global__ void k_split_hilo(const float *__restrict__ src, int64_t rows, int k,
   if (lo) lo[idx] = x - tc::tf32_trunc(x);
 }
 __global__ void k_transpose64(const double *__restrict__ C, int64_t k, int64_t ldc, double *__restrict__ Ct) {
+  grid_dep_enter();
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx < k * k) Ct[(idx % k) * k + idx / k] = C[(idx / k) * ldc + idx % k];
 }
@@ -430,7 +435,7 @@ static void rows_times(Ctx &c, float *G, int64_t nr, int k, int64_t ldb, const d
   DBuf<float> out((size_t)nr * ldb, c.stream);
   Mat Gm{G, nr, k, ldb}, Om{out.p, nr, k, ldb};
   gemm_tall(c, Gm, Bs, k, k, nullptr, 0.f, Om);
-  NM_LAUNCH(c, "split_hilo", tcs::k_split_hilo<<<ceil_div(nr * ldb, 256), 256, 0, c.stream>>>(out.p, nr, k, ldb, hi, lo));
+  NM_LAUNCH(c, "split_hilo", launch_pdl(c.stream, tcs::k_split_hilo, ceil_div(nr * ldb, 256), 256, 0, out.p, nr, k, ldb, hi, lo));
 }
 
 // Y[n × h] = f(scale · F C F(rows)ᵀ) Ψ  (Y mode; Ψ = (rows, signs) with z per column).
@@ -451,11 +456,10 @@ void tc_sketch_y(Ctx &c, const Mat &F, const double *C, int64_t ldc, const int32
       sg(pad4(ncols) + NW, c.stream);
   DBuf<double> Ct((size_t)k * k, c.stream);
   NM_CUDA(cudaMemsetAsync(sg.p, 0, sg.n * 4, c.stream));
-  NM_LAUNCH(c, "gather_groups", k_gather_groups<<<ceil_div(ncols * ldb, 256), 256, 0, c.stream>>>(
-                                    F.p, F.ld, row0, F.rows, rows, signs, h, z, zp, k, ldb, g.p, nullptr, sg.p));
+  NM_LAUNCH(c, "gather_groups", launch_pdl(c.stream, k_gather_groups, ceil_div(ncols * ldb, 256), 256, 0, F.p, F.ld, row0, F.rows, rows, signs, h, z, zp, k, ldb, g.p, nullptr, sg.p));
   // each gathered row lives on exactly one rank: the sum over ranks is exact
   dist_allreduce(c, g.p, (size_t)ncols * ldb, DType::F32);
-  NM_LAUNCH(c, "transpose64", k_transpose64<<<ceil_div((int64_t)k * k, 256), 256, 0, c.stream>>>(C, k, ldc, Ct.p));
+  NM_LAUNCH(c, "transpose64", launch_pdl(c.stream, k_transpose64, ceil_div((int64_t)k * k, 256), 256, 0, C, k, ldc, Ct.p));
   rows_times(c, g.p, ncols, k, ldb, Ct.p, bh.p, bl.p);  // B rows = F_r Cᵀ
   CUtensorMap ma = make_map(F.p, n, k, F.ld, 128, SW128, BK);
   CUtensorMap mh = make_map(bh.p, ncols, k, ldb, NW, SW128, BK);
@@ -492,8 +496,7 @@ void tc_sketch_z(Ctx &c, const Mat &F, const double *C, int64_t ldc, const int32
   DBuf<float> bh((size_t)nr * ldb, c.stream), bl((size_t)nr * ldb, c.stream), sg(pad4(nr) + NW, c.stream);
   NM_CUDA(cudaMemsetAsync(sg.p, 0, sg.n * 4, c.stream));
   NM_CUDA(cudaMemsetAsync(rs.p, 0, rs.n * 4, c.stream));
-  NM_LAUNCH(c, "gather_groups", k_gather_groups<<<ceil_div(nr * ldb, 256), 256, 0, c.stream>>>(
-                                    F.p, F.ld, row0, F.rows, rows, signs, h, z, zp, k, ldb, bh.p, bl.p, sg.p));
+  NM_LAUNCH(c, "gather_groups", launch_pdl(c.stream, k_gather_groups, ceil_div(nr * ldb, 256), 256, 0, F.p, F.ld, row0, F.rows, rows, signs, h, z, zp, k, ldb, bh.p, bl.p, sg.p));
   dist_allreduce(c, bh.p, (size_t)nr * ldb, DType::F32);
   dist_allreduce(c, bl.p, (size_t)nr * ldb, DType::F32);
   // A = F(rows) C (the gathered raw rows times C); row signs = the column signs

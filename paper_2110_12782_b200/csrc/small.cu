@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(256) k_gemm64(bool ta, bool tb, int64_t M, int
                                                 double alpha, const double *__restrict__ A, int64_t lda,
                                                 const double *__restrict__ B, int64_t ldb, double beta,
                                                 double *__restrict__ C, int64_t ldc) {
+  grid_dep_enter();
   __shared__ double As[32][33];  // [k][m]
   __shared__ double Bs[32][33];  // [k][n]
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -145,17 +146,20 @@ void gemm64(Ctx &c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double al
   cfg.gridDim = grid;
   cfg.blockDim = dim3(256);
   cfg.stream = c.stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 1;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = split;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   NM_LAUNCH(c, "gemm64", NM_CUDA(cudaLaunchKernelEx(&cfg, k_gemm64, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc)));
 }
 
 __global__ void k_symmetrize(double *S, int64_t l, int64_t ld) {
+  grid_dep_enter();
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t i = idx / l, j = idx % l;
   if (i >= l || j <= i) return;
@@ -164,36 +168,39 @@ __global__ void k_symmetrize(double *S, int64_t l, int64_t ld) {
   S[j * ld + i] = v;
 }
 void symmetrize64(Ctx &c, double *S, int64_t l, int64_t ld) {
-  NM_LAUNCH(c, "symmetrize", k_symmetrize<<<ceil_div(l * l, 256), 256, 0, c.stream>>>(S, l, ld));
+  NM_LAUNCH(c, "symmetrize", launch_pdl(c.stream, k_symmetrize, ceil_div(l * l, 256), 256, 0, S, l, ld));
 }
 
 // mode 0: A[:, j] *= s[j]; mode 1: A[i, :] *= s[i]
 __global__ void k_scale64(double *A, int64_t rows, int64_t cols, int64_t ld, const double *s, int mode) {
+  grid_dep_enter();
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= rows * cols) return;
   int64_t i = idx / cols, j = idx % cols;
   A[i * ld + j] *= (mode == 0 ? s[j] : s[i]);
 }
 void scale_cols64(Ctx &c, double *A, int64_t rows, int64_t cols, int64_t ld, const double *s, int mode) {
-  NM_LAUNCH(c, "scale64", k_scale64<<<ceil_div(rows * cols, 256), 256, 0, c.stream>>>(A, rows, cols, ld, s, mode));
+  NM_LAUNCH(c, "scale64", launch_pdl(c.stream, k_scale64, ceil_div(rows * cols, 256), 256, 0, A, rows, cols, ld, s, mode));
 }
 
 __global__ void k_identity(double *A, int64_t l, int64_t ld) {
+  grid_dep_enter();
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= l * l) return;
   int64_t i = idx / l, j = idx % l;
   A[i * ld + j] = (i == j) ? 1.0 : 0.0;
 }
 void set_identity64(Ctx &c, double *A, int64_t l, int64_t ld) {
-  NM_LAUNCH(c, "identity", k_identity<<<ceil_div(l * l, 256), 256, 0, c.stream>>>(A, l, ld));
+  NM_LAUNCH(c, "identity", launch_pdl(c.stream, k_identity, ceil_div(l * l, 256), 256, 0, A, l, ld));
 }
 
 __global__ void k_axpy64(int64_t n, double a, const double *x, double *y) {
+  grid_dep_enter();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) y[i] += a * x[i];
 }
 void axpy64(Ctx &c, int64_t n, double alpha, const double *x, double *y) {
-  NM_LAUNCH(c, "axpy64", k_axpy64<<<ceil_div(n, 256), 256, 0, c.stream>>>(n, alpha, x, y));
+  NM_LAUNCH(c, "axpy64", launch_pdl(c.stream, k_axpy64, ceil_div(n, 256), 256, 0, n, alpha, x, y));
 }
 
 // ---------------------------------------------------------------------------
@@ -202,6 +209,7 @@ void axpy64(Ctx &c, int64_t n, double alpha, const double *x, double *y) {
 constexpr int CHP = 32;
 
 __global__ void __launch_bounds__(1024) k_cholesky(double *G, int l, int64_t ld, double *G0, int *flag) {
+  grid_dep_enter();
   extern __shared__ double P[];  // (l) x CHP panel
   __shared__ int fail;
   __shared__ double maxdiag;
@@ -292,7 +300,7 @@ void cholesky_upper(Ctx &c, double *G, int64_t l, int64_t ld, int *flag) {
   size_t smem = (size_t)l * CHP * sizeof(double);
   smem_attr(k_cholesky, 200 * 1024);
   NM_REQUIRE(smem <= 200 * 1024, "cholesky: l too large for one CTA panel");
-  NM_LAUNCH(c, "cholesky", k_cholesky<<<1, 1024, smem, c.stream>>>(G, (int)l, ld, G0, flag));
+  NM_LAUNCH(c, "cholesky", launch_pdl(c.stream, k_cholesky, 1, 1024, smem, G, (int)l, ld, G0, flag));
 }
 
 // ---------------------------------------------------------------------------
@@ -315,6 +323,7 @@ constexpr int CI_K = (CI_MAXL * 32 + CI_T - 1) / CI_T;  // outputs per thread
 
 __global__ void __launch_bounds__(CI_T) k_chol_inv(double *G, int l, int64_t ld, double *G0, double *Rinv,
                                                    int *flag, double drop_tol) {
+  grid_dep_enter();
   extern __shared__ double sm[];
   double *R1 = sm;             // phase 1: L rows chunk [rows][33];   phase 2: L_I rows [32][l+1]
   double *R2 = sm + CI_R;      // phase 1: panel P [rows][33];        phase 2: X chunk / T [32][l+1]
@@ -527,13 +536,14 @@ void chol_inv_upper(Ctx &c, double *G, int64_t l, int64_t ld, double *Rinv, int 
   DBuf<double> G0((size_t)l * l, c.stream);
   const size_t smem = ((size_t)2 * CI_R + 32 * CI_LD) * sizeof(double);
   smem_attr(k_chol_inv, smem);
-  NM_LAUNCH(c, "chol_inv", k_chol_inv<<<1, CI_T, smem, c.stream>>>(G, (int)l, ld, G0, Rinv, flag, drop_tol));
+  NM_LAUNCH(c, "chol_inv", launch_pdl(c.stream, k_chol_inv, 1, CI_T, smem, G, (int)l, ld, G0, Rinv, flag, drop_tol));
 }
 
 // ---------------------------------------------------------------------------
 // Rinv = R^-1 (upper), one warp per column, x in shared memory
 // ---------------------------------------------------------------------------
 __global__ void k_trinv(const double *__restrict__ R, int64_t ld, double *__restrict__ Rinv, int l) {
+  grid_dep_enter();
   extern __shared__ double xs[];
   const int w = threadIdx.x / 32, ln = threadIdx.x % 32;
   const int j = blockIdx.x * (blockDim.x / 32) + w;
@@ -554,7 +564,7 @@ void tri_inv_upper(Ctx &c, const double *R, int64_t ld, double *Rinv, int64_t l)
   size_t smem = (size_t)wpb * l * sizeof(double);
   smem_attr(k_trinv, 200 * 1024);
   NM_REQUIRE(smem <= 200 * 1024, "tri_inv: l too large");
-  NM_LAUNCH(c, "trinv", k_trinv<<<ceil_div(l, wpb), wpb * 32, smem, c.stream>>>(R, ld, Rinv, (int)l));
+  NM_LAUNCH(c, "trinv", launch_pdl(c.stream, k_trinv, ceil_div(l, wpb), wpb * 32, smem, R, ld, Rinv, (int)l));
 }
 
 // ---------------------------------------------------------------------------
@@ -601,6 +611,7 @@ static_assert(TDT / 32 == 16, "tridiagonalisation partial slots assume 16 warps"
 __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
     k_tridiag(const double *__restrict__ S, int l, double *__restrict__ dd, double *__restrict__ ee,
               double *__restrict__ Hv, double *__restrict__ hbeta) {
+  grid_dep_enter();
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -738,6 +749,7 @@ __device__ int sturm_count(const double *d, const double *e, int l, double x, do
 // eigenvalue m (ascending) by bisection; also computes the 1-norm bound
 __global__ void k_bisect(const double *__restrict__ d, const double *__restrict__ e, int l,
                          double *__restrict__ w) {
+  grid_dep_enter();
   int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= l) return;
   double lo = 1e300, hi = -1e300, emax = 0.0;
@@ -807,6 +819,7 @@ __device__ __forceinline__ void sturm2(const double *sd, const double *se2, int 
 
 __global__ void __launch_bounds__(MSW * 32) k_multisect(const double *__restrict__ d, const double *__restrict__ e,
                                                         int l, double *__restrict__ w) {
+  grid_dep_enter();
   extern __shared__ double ms_sh[];
   double *sd = ms_sh, *se2 = ms_sh + l;
   const int lane = threadIdx.x & 31;
@@ -881,6 +894,7 @@ __global__ void __launch_bounds__(IVW * 32) k_invit(const double *__restrict__ d
                                                     int l, const double *__restrict__ w,
                                                     const int *__restrict__ cstart, const int *__restrict__ ncl_dev,
                                                     double *__restrict__ Zt, uint32_t seed) {
+  grid_dep_enter();
   extern __shared__ double ivs[];
   const int wib = threadIdx.x / 32, ln = threadIdx.x % 32;
   const int gw = blockIdx.x * IVW + wib;
@@ -1041,6 +1055,7 @@ __global__ void __launch_bounds__(IVW * 32) k_invit(const double *__restrict__ d
 // cluster starts: consecutive eigenvalues closer than ortol = 1e-9 ||T||
 __global__ void k_clusters(const double *__restrict__ w, const double *__restrict__ d,
                            const double *__restrict__ e, int l, int *__restrict__ cstart, int *ncl) {
+  grid_dep_enter();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double tnorm = 0.0;
   for (int i = 0; i < l; ++i)
@@ -1062,6 +1077,7 @@ constexpr int BT_NR = 15;  // l <= 480
 constexpr int BT_T = 64;  // 2 warps per block: the l eigenvectors spread over every SM
 __global__ void __launch_bounds__(BT_T) k_backtransform(const double *__restrict__ Hv, const double *__restrict__ hbeta,
                                                        int l, double *__restrict__ Zt) {
+  grid_dep_enter();
   const int m = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int ln = threadIdx.x % 32;
   if (m >= l) return;
@@ -1108,6 +1124,7 @@ __global__ void __launch_bounds__(BT_T) k_backtransform(const double *__restrict
 // order by desc |λ| (ties: desc λ) or desc λ; V[r][c] = Zt[perm[c]][r]
 __global__ void k_eig_sort(const double *__restrict__ w, const double *__restrict__ Zt, int l,
                            bool abs_order, double *__restrict__ lam, double *__restrict__ V) {
+  grid_dep_enter();
   const int i = blockIdx.x;  // one block per eigenpair
   const double wi = w[i];
   __shared__ int rank_s;
@@ -1145,15 +1162,15 @@ void sym_eig(Ctx &c, double *S, int64_t l64, double *lam, double *V, bool abs_or
   NM_REQUIRE(smem <= 227 * 1024 && l <= 32 * BT_NR, "sym_eig: l too large for the 8-CTA cluster (l <= ~470)");
   smem_attr(k_tridiag, 227 * 1024);
   if (TDC > 8) func_attr(reinterpret_cast<const void *>(k_tridiag), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  NM_LAUNCH(c, "tridiag", k_tridiag<<<TDC, TDT, smem, s>>>(S, l, d, e, Hv, hb));
-  NM_LAUNCH(c, "multisect", k_multisect<<<l, MSW * 32, (size_t)2 * l * sizeof(double), s>>>(d, e, l, w));
+  NM_LAUNCH(c, "tridiag", launch_pdl(s, k_tridiag, TDC, TDT, smem, S, l, d, e, Hv, hb));
+  NM_LAUNCH(c, "multisect", launch_pdl(s, k_multisect, l, MSW * 32, (size_t)2 * l * sizeof(double), d, e, l, w));
   DBuf<int> cst(l + 1, s), ncl(1, s);
-  NM_LAUNCH(c, "clusters", k_clusters<<<1, 32, 0, s>>>(w, d, e, l, cst, ncl));
+  NM_LAUNCH(c, "clusters", launch_pdl(s, k_clusters, 1, 32, 0, w, d, e, l, cst, ncl));
   const size_t ivsm = (size_t)IVW * 4 * l * sizeof(double) + (size_t)IVW * l + 16 + (size_t)IVW * l * sizeof(double);
   smem_attr(k_invit, 200 * 1024);
-  NM_LAUNCH(c, "invit", k_invit<<<ceil_div(l, IVW), IVW * 32, ivsm, s>>>(d, e, l, w, cst, ncl, Zt, 0x1234567u));
-  NM_LAUNCH(c, "backtransform", k_backtransform<<<ceil_div((int64_t)l * 32, BT_T), BT_T, 0, s>>>(Hv, hb, l, Zt));
-  NM_LAUNCH(c, "eig_sort", k_eig_sort<<<l, 128, 0, s>>>(w, Zt, l, abs_order, lam, V));
+  NM_LAUNCH(c, "invit", launch_pdl(s, k_invit, ceil_div(l, IVW), IVW * 32, ivsm, d, e, l, w, cst, ncl, Zt, 0x1234567u));
+  NM_LAUNCH(c, "backtransform", launch_pdl(s, k_backtransform, ceil_div((int64_t)l * 32, BT_T), BT_T, 0, Hv, hb, l, Zt));
+  NM_LAUNCH(c, "eig_sort", launch_pdl(s, k_eig_sort, l, 128, 0, w, Zt, l, abs_order, lam, V));
 }
 
 }  // namespace netmfp

@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(256, 8) k_spmm_heavy(SpmmArgs p, const int64_t
                                                     const int64_t *__restrict__ seg_e0,
                                                     const int32_t *__restrict__ seg_h, int64_t nsegs,
                                                     float *__restrict__ part, int64_t ldh) {
+  grid_dep_enter();
   constexpr int GPB = 256 / LPR;
   const int li = threadIdx.x % LPR;
   const int gi = threadIdx.x / LPR;
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(256, MINB) k_spmm_rows(SpmmArgs p, const int64
                                                    const int32_t *__restrict__ heavy, int64_t nh,
                                                    const int64_t *__restrict__ seg_ptr,
                                                    const float *__restrict__ part, int64_t ldh) {
+  grid_dep_enter();
   constexpr int GPB = 256 / LPR;
   const int li = threadIdx.x % LPR;
   const int gi = threadIdx.x / LPR;
@@ -379,6 +381,7 @@ struct FusedGraph {
 
 template <int LPR, int MINB, bool GEN>
 __global__ void __launch_bounds__(256, MINB) k_spmm_fused(SpmmArgs p, FusedGraph fg, int nblk_heavy) {
+  grid_dep_enter();
   fused_body<LPR, GEN>(p, blockIdx.y, blockIdx.x, fg.rowptr, fg.col, fg.n, fg.heavy, fg.seg_ptr, fg.seg_e0, fg.seg_h,
                        fg.nsegs, fg.part, fg.hcnt, gridDim.y, nblk_heavy, fg.nblk_tile);
 }
@@ -395,13 +398,13 @@ static void spmm_rows_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
   if (g.n_heavy > 0) {
     part.alloc((size_t)g.n_heavy_segs * ldh, c.stream);
     dim3 gh(ceil_div(g.n_heavy_segs, GPB), chunks);
-    NM_LAUNCH(c, "spmm_heavy", k_spmm_heavy<LPR, SCOL><<<gh, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.heavy, g.seg_e0, g.seg_h,
+    NM_LAUNCH(c, "spmm_heavy", launch_pdl(c.stream, k_spmm_heavy<LPR, SCOL>, gh, 256, 0, p, g.rowptr, g.col, g.heavy, g.seg_e0, g.seg_h,
                                                       g.n_heavy_segs, part, ldh));
   }
   int64_t row_blocks = ceil_div(g.n, GPB);
   int64_t cap = (int64_t)c.num_sms * 64;
   dim3 grid((unsigned)std::min<int64_t>(row_blocks, cap), chunks);
-  NM_LAUNCH(c, "spmm_rows", k_spmm_rows<LPR, SCOL, MINB><<<grid, 256, 0, c.stream>>>(p, g.rowptr, g.col, g.n, g.heavy, g.n_heavy,
+  NM_LAUNCH(c, "spmm_rows", launch_pdl(c.stream, k_spmm_rows<LPR, SCOL, MINB>, grid, 256, 0, p, g.rowptr, g.col, g.n, g.heavy, g.n_heavy,
                                                      g.heavy_seg_ptr.p, part.p, ldh));
 }
 
@@ -425,9 +428,9 @@ static void spmm_fused_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
   const int nbh = g.n_heavy > 0 ? (int)ceil_div(g.n_heavy_segs, 256 / LPR) : 0;
   dim3 grid((unsigned)(fg.nblk_tile + nbh), passes);
   if (p.prev || p.acc_out || !p.Y)
-    NM_LAUNCH(c, "spmm_fused", k_spmm_fused<LPR, 8, true><<<grid, 256, 0, c.stream>>>(p, fg, nbh));
+    NM_LAUNCH(c, "spmm_fused", launch_pdl(c.stream, k_spmm_fused<LPR, 8, true>, grid, 256, 0, p, fg, nbh));
   else
-    NM_LAUNCH(c, "spmm_fused", k_spmm_fused<LPR, 8, false><<<grid, 256, 0, c.stream>>>(p, fg, nbh));
+    NM_LAUNCH(c, "spmm_fused", launch_pdl(c.stream, k_spmm_fused<LPR, 8, false>, grid, 256, 0, p, fg, nbh));
 }
 
 void spmm(Ctx &c, const Graph &g, const SpmmArgs &p_in) {
@@ -481,12 +484,13 @@ void spmm(Ctx &c, const Graph &g, const SpmmArgs &p_in) {
 
 // d^-e (0 for d = 0) as fp32 — column scaling vector for general (a, b)
 __global__ void k_deg_pow(const int32_t *__restrict__ deg, int64_t n, float e, float *__restrict__ out) {
+  grid_dep_enter();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) out[i] = row_scale(deg[i], e);
 }
 
 void deg_pow(Ctx &c, const Graph &g, float e, float *out) {
-  NM_LAUNCH(c, "deg_pow", k_deg_pow<<<ceil_div(g.n, 256), 256, 0, c.stream>>>(g.deg, g.n, e, out));
+  NM_LAUNCH(c, "deg_pow", launch_pdl(c.stream, k_deg_pow, ceil_div(g.n, 256), 256, 0, g.deg, g.n, e, out));
 }
 
 }  // namespace netmfp

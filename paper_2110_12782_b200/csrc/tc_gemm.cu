@@ -89,6 +89,7 @@ struct GramP {
 template <int BK, bool SYM, bool EXACT>
 __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUtensorMap tmA,
                                                    const __grid_constant__ CUtensorMap tmB, const GramP p) {
+  grid_dep_enter();
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = align1024(smem_raw);
   constexpr int BLK = BK * 128;  // bytes of one 32-col block of BK rows
@@ -275,6 +276,7 @@ struct GramRed {
 constexpr int kRedWarps = 8;
 __global__ void __launch_bounds__(32 * kRedWarps) k_gram_reduce(const float *__restrict__ part, GramRed R,
                                                                double *__restrict__ G, int64_t ldg) {
+  grid_dep_enter();
   // 128 positions per block, 4 per lane (16-B loads); warp w sums chains
   // w, w+8, … in order, the 8 warp sums are added in warp order
   __shared__ double red[kRedWarps][128];
@@ -371,6 +373,7 @@ __device__ __forceinline__ int part_chunks(const GemmP &p, int h) {
 __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUtensorMap tmA,
                                                     const __grid_constant__ CUtensorMap tmBh,
                                                     const __grid_constant__ CUtensorMap tmC, const GemmP p) {
+  grid_dep_enter();
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = align1024(smem_raw);
   constexpr int ABYTES = 128 * 128;  // 128 rows × 32 fp32 (raw, SWIZZLE_128B)
@@ -708,10 +711,11 @@ static void launch_gram(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mb, tc
   const size_t smem = 1024 + S * stage + kPadBlocks * BK * 128 + (3 * S + 2) * 8 + 16;
   smem_attr(tc::k_gram_tc<BK, SYM, true>, kSmemMax);
   smem_attr(tc::k_gram_tc<BK, SYM, false>, kSmemMax);
-  NM_LAUNCH(c, "tc_gram", kern<<<(unsigned)nchain, tc::NT, smem, c.stream>>>(ma, mb, p));
+  NM_LAUNCH(c, "tc_gram", launch_pdl(c.stream, kern, (unsigned)nchain, tc::NT, smem, ma, mb, p));
 }
 
 __global__ void k_gram_wrow(const int32_t *__restrict__ deg, int64_t n, float e, float *__restrict__ w) {
+  grid_dep_enter();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) w[i] = tc::deg_pow_dev(deg, i, e);
 }
@@ -793,7 +797,7 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
   DBuf<float> wrow;
   if (deg) {
     wrow.alloc(n, c.stream);
-    NM_LAUNCH(c, "gram_wrow", k_gram_wrow<<<ceil_div(n, 256), 256, 0, c.stream>>>(deg, n, sym ? 0.5f * wexp : wexp, wrow.p));
+    NM_LAUNCH(c, "gram_wrow", launch_pdl(c.stream, k_gram_wrow, ceil_div(n, 256), 256, 0, deg, n, sym ? 0.5f * wexp : wexp, wrow.p));
   }
   for (auto &grp : groups) {
     GramP p{};
@@ -828,7 +832,7 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
   R.nchain = nchain;
   R.part_stride = total;
   NM_LAUNCH(c, "tc_gram_reduce",
-            k_gram_reduce<<<ceil_div(total, 128), 32 * kRedWarps, 0, c.stream>>>(part.p, R, G, ldg));
+            launch_pdl(c.stream, k_gram_reduce, ceil_div(total, 128), 32 * kRedWarps, 0, part.p, R, G, ldg));
 }
 
 // Bᵀ for the tensor-core GEMM, zero padded to nrows × 32 nk:
@@ -836,6 +840,7 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
 // nearest) and part 1 = lo = B - hi
 __global__ void k_bt_split(const double *__restrict__ Bs, int64_t ldb, int64_t K, int64_t N, int64_t nrows, int64_t nk,
                            float *__restrict__ Bt) {
+  grid_dep_enter();
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= nk * nrows * 32) return;
   const int64_t kk = idx & 31, j = (idx >> 5) % nrows, kc = idx / (32 * nrows);
@@ -862,7 +867,7 @@ static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ld
   const int ntot = nh * hr;
   const int64_t nk = ceil_div(K, 32);
   DBuf<float> bt((size_t)nk * 2 * ntot * 32, c.stream);
-  NM_LAUNCH(c, "bt_split", k_bt_split<<<ceil_div(nk * ntot * 32, 256), 256, 0, c.stream>>>(Bs, ldb, K, bcols, ntot, nk,
+  NM_LAUNCH(c, "bt_split", launch_pdl(c.stream, k_bt_split, ceil_div(nk * ntot * 32, 256), 256, 0, Bs, ldb, K, bcols, ntot, nk,
                                                                                              bt.p));
   CUtensorMap ma = make_map(A.p, n, K, A.ld, 128);
   const int64_t bdims[4] = {32, hr, nh, 2 * nk};
@@ -901,7 +906,7 @@ static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ld
   p.skip = tri ? 1 : 0;
   const int64_t grid = std::min<int64_t>(p.nitems, c.num_sms);
   CUtensorMap mc = make_map(C.p, n, bcols, C.ld, 32, SW128, 32);
-  NM_LAUNCH(c, "tc_gemm_tall", k_gemm_tc<<<(unsigned)grid, NTG, smem, c.stream>>>(ma, mb, mc, p));
+  NM_LAUNCH(c, "tc_gemm_tall", launch_pdl(c.stream, k_gemm_tc, (unsigned)grid, NTG, smem, ma, mb, mc, p));
 }
 
 void tc_gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcols, const int32_t *deg, float rexp,

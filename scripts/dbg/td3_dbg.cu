@@ -311,6 +311,271 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(T3T, 1)
   cl.sync();
 }
 
+
+// ---- k_tridiag4: k_tridiag3<8, NB> with a shorter step chain:
+//  * the panel dots W_sᵀv, V_sᵀv ride in the matvec's reduce-scatter (slots 4..7);
+//  * K from vᵀp = β (vᵀA v − 2 Σ_s (V_sᵀv)(W_sᵀv)): each CTA pushes its own rows'
+//    partial of vᵀA v with its p values, so no reduction follows the barrier;
+//  * the next column's stale part and older corrections are computed between the
+//    split arrive and wait of the step's barrier.
+constexpr int T4CL = 8;
+template <int NB>
+struct Td4 {
+  static size_t smem_doubles(int l) {
+    const size_t lp = (size_t)(l + 31) / 32 * 32, nmax = (size_t)(l + T4CL - 1) / T4CL;
+    return nmax * lp + 2 * (size_t)NB * l + (size_t)NB * lp + 2 * (size_t)l + 2 * T4CL + nmax + lp + l + 16 + 2 * NB;
+  }
+};
+__device__ __forceinline__ double tree16(const double *x) {
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = x[2 * i] + x[2 * i + 1];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a[i] += a[i + 4];
+  return (a[0] + a[2]) + (a[1] + a[3]);
+}
+template <int NB>
+__global__ void __cluster_dims__(T4CL, 1, 1) __launch_bounds__(T3T, 1)
+    k_tridiag4(const double *__restrict__ S, int l, double *__restrict__ dd, double *__restrict__ ee,
+               double *__restrict__ Hv, double *__restrict__ hbeta) {
+  constexpr int CL = T4CL;
+  cg::cluster_group cl = cg::this_cluster();
+  const int r = (int)cl.block_rank();
+  const int tid = threadIdx.x, wid = tid >> 5, ln = tid & 31;
+  const int lp = (l + 31) / 32 * 32, nch = lp / 32;
+  const int nloc = (l - r + CL - 1) / CL, nmax = (l + CL - 1) / CL;
+  extern __shared__ double sm[];
+  double *A = sm;
+  double *VT = A + (size_t)nmax * lp;
+  double *WT = VT + NB * l;
+  double *PR = WT + NB * l;
+  double *PX = PR + NB * lp;
+  double *KX = PX + 2 * l;    // per step parity: every CTA's partial of vᵀ A v
+  double *YO = KX + 2 * CL;
+  double *VV = YO + nmax;
+  double *COL = VV + lp;
+  double *red = COL + l;      // 16 warp partials of Σ a²
+  double *dots = red + 16;    // W_sᵀv (even), V_sᵀv (odd)
+  for (int li = wid; li < nloc; li += T3W) {
+    const int i = li * CL + r;
+    for (int k = ln; k < lp; k += 32) A[(size_t)li * lp + k] = k < l ? S[(int64_t)i * l + k] : 0.0;
+  }
+  for (int idx = tid; idx < NB * lp; idx += T3T) {
+    const int q = idx / lp, k = idx % lp;
+    PR[idx] = (q < l && k < l) ? S[(int64_t)q * l + k] : 0.0;
+  }
+  __syncthreads();
+  double *PXr[CL], *PRr[CL], *KXr[CL];
+#pragma unroll
+  for (int c = 0; c < CL; ++c) {
+    PXr[c] = cl.map_shared_rank(PX, c);
+    PRr[c] = cl.map_shared_rank(PR, c);
+    KXr[c] = cl.map_shared_rank(KX, c);
+  }
+  cl.sync();
+  const int k = tid;
+  auto finish_column = [&](int jc, double a) {
+    double ss = 0.0;
+    if (k < l && k >= jc) {
+      COL[k] = a;
+      if (k >= jc + 2) ss = a * a;
+    }
+    ss = warp_sum(ss);
+    if (ln == 0) red[wid] = ss;
+    __syncthreads();
+  };
+  int jp = 0, t = 0;
+  if (l >= 3) finish_column(0, k < l ? PR[k] : 0.0);
+  for (int j = 0; j + 2 < l; ++j) {
+    const int par = j & 1;
+    TD3_MARK(0);
+    // (1) reflector
+    const double ss = tree16(red);
+    const double x0 = COL[j + 1];
+    double beta = 0.0, alpha = x0, v0 = 0.0;
+    if (ss > 0.0) {
+      const double nrm = sqrt(ss + x0 * x0);
+      alpha = x0 >= 0 ? -nrm : nrm;
+      v0 = x0 - alpha;
+      beta = 2.0 / (ss + v0 * v0);
+    }
+    double vk = 0.0;
+    if (k < l) {
+      vk = ss > 0.0 ? (k == j + 1 ? v0 : (k > j + 1 ? COL[k] : 0.0)) : 0.0;
+      VV[k] = vk;
+      VT[t * l + k] = vk;
+      if (r == 0 && k > j) Hv[(int64_t)j * l + k] = vk;
+    } else if (k < lp) {
+      VV[k] = 0.0;
+    }
+    if (r == 0 && tid == 0) {
+      dd[j] = COL[j];
+      ee[j] = alpha;
+      hbeta[j] = beta;
+    }
+    __syncthreads();
+    TD3_MARK(1);
+    // (2) own rows' A v (slots 0..3) and the panel dots (slots 4..7), one reduce-scatter
+    {
+      const int li0 = (j + 1 - r <= 0) ? 0 : (j + 1 - r + CL - 1) / CL;
+      const int clo = (j + 1) >> 5;
+      const int nu = nloc > li0 + wid ? (nloc - li0 - wid + T3W - 1) / T3W : 0;
+      double rs[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) rs[u] = 0.0;
+      const double *Ab = A + (size_t)(li0 + wid) * lp + ln;
+      for (int c = clo; c < nch; ++c) {
+        const int kk = 32 * c + ln;
+        const double vc = VV[kk];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u < nu) rs[u] = fma(Ab[(size_t)u * T3W * lp + 32 * c], vc, rs[u]);
+#pragma unroll
+        for (int u = 4; u < 8; ++u) {
+          const int d = wid + T3W * (u - 4);
+          if (d < 2 * t && kk < l) {
+            const double *vec = (d & 1) ? VT + (d >> 1) * l : WT + (d >> 1) * l;
+            rs[u] = fma(vec[kk], vc, rs[u]);
+          }
+        }
+      }
+      double h4[4], h2[2];
+      const bool b4 = ln & 16, b3 = ln & 8, b2 = ln & 4;
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        h4[m] = (b4 ? rs[m + 4] : rs[m]) + __shfl_xor_sync(0xffffffffu, b4 ? rs[m] : rs[m + 4], 16);
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+        h2[m] = (b3 ? h4[m + 2] : h4[m]) + __shfl_xor_sync(0xffffffffu, b3 ? h4[m] : h4[m + 2], 8);
+      double y = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? h2[0] : h2[1], 4);
+      y += __shfl_xor_sync(0xffffffffu, y, 2);
+      y += __shfl_xor_sync(0xffffffffu, y, 1);
+      const int u = ln >> 2;
+      if ((ln & 3) == 0) {
+        if (u < 4) {
+          if (u < nu) YO[li0 + wid + u * T3W] = y;
+        } else {
+          const int d = wid + T3W * (u - 4);
+          if (d < 2 * t) dots[d] = y;
+        }
+      }
+    }
+    __syncthreads();
+    TD3_MARK(2);
+    // (3) warp 0: own rows' p (pushed everywhere) and the CTA's partial of vᵀ A v
+    if (wid == 0) {
+      double kpart = 0.0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int li = ln + 32 * h;
+        const int i = li * CL + r;
+        if (li < nloc && i > j) {
+          const double y = YO[li];
+          double c0 = 0.0, c1 = 0.0;
+          for (int s2 = 0; s2 < t; ++s2) {
+            c0 = fma(VT[s2 * l + i], dots[2 * s2], c0);
+            c1 = fma(WT[s2 * l + i], dots[2 * s2 + 1], c1);
+          }
+          const double p = beta * (y - (c0 + c1));
+#pragma unroll
+          for (int c = 0; c < CL; ++c) PXr[c][par * l + i] = p;
+          kpart = fma(VV[i], y, kpart);
+        }
+      }
+      kpart = warp_sum(kpart);
+      if (ln < CL) KXr[ln][par * CL + r] = kpart;
+    }
+    cluster_arrive();
+    // between arrive and wait: the next column's stale entry and older corrections
+    const int jn = j + 1;
+    const bool pend = (t + 1 == NB) || (jn + 2 >= l);
+    double pre = 0.0;
+    if (!pend && k < l && k >= jn) {
+      pre = PR[(size_t)(jn - jp) * lp + k];
+      double c0 = 0.0, c1 = 0.0;
+      for (int s2 = 0; s2 < t; ++s2) {
+        c0 = fma(VT[s2 * l + k], WT[s2 * l + jn], c0);
+        c1 = fma(WT[s2 * l + k], VT[s2 * l + jn], c1);
+      }
+      pre -= c0 + c1;
+    }
+    cluster_wait();
+    TD3_MARK(3);
+    // (4) K, w
+    double vav = 0.0;
+#pragma unroll
+    for (int c = 0; c < CL; ++c) vav += KX[par * CL + c];
+    double dd2 = 0.0;
+    for (int s2 = 0; s2 < t; ++s2) dd2 = fma(dots[2 * s2], dots[2 * s2 + 1], dd2);
+    const double K = 0.5 * beta * beta * (vav - 2.0 * dd2);
+    const double pk = (k < l && k > j) ? PX[par * l + k] : 0.0;
+    const double wk = (k < l && k > j) ? pk - K * vk : 0.0;
+    if (k < l) WT[t * l + k] = wk;
+    ++t;
+    if (pend) {
+      __syncthreads();
+      const int tn = t;
+      const int li0 = (jn - r <= 0) ? 0 : (jn - r + CL - 1) / CL;
+      for (int c = jn >> 5; c < nch; ++c) {
+        const int kc = 32 * c + ln;
+        double vkc[NB], wkc[NB];
+#pragma unroll
+        for (int s2 = 0; s2 < NB; ++s2) {
+          vkc[s2] = (s2 < tn && kc < l) ? VT[s2 * l + kc] : 0.0;
+          wkc[s2] = (s2 < tn && kc < l) ? WT[s2 * l + kc] : 0.0;
+        }
+        for (int li = li0 + wid; li < nloc; li += T3W) {
+          const int i = li * CL + r;
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int s2 = 0; s2 < NB; ++s2) {
+            if (s2 < tn) {
+              c0 = fma(VT[s2 * l + i], wkc[s2], c0);
+              c1 = fma(WT[s2 * l + i], vkc[s2], c1);
+            }
+          }
+          if (kc >= jn && kc < l) A[(size_t)li * lp + kc] -= c0 + c1;
+        }
+      }
+      if (jn + 2 >= l) break;
+      __syncthreads();
+      for (int q = 0; q < NB && jn + q < l; ++q) {
+        const int i = jn + q;
+        if (i % CL != r) continue;
+        const double *Ai = A + (size_t)(i / CL) * lp;
+        for (int kk = jn + tid; kk < l; kk += T3T) {
+          const double val = Ai[kk];
+#pragma unroll
+          for (int c = 0; c < CL; ++c) PRr[c][(size_t)q * lp + kk] = val;
+        }
+      }
+      cluster_arrive();
+      cluster_wait();
+      jp = jn;
+      t = 0;
+      finish_column(jn, k < l ? PR[k] : 0.0);
+    } else {
+      const double vj = VV[jn];
+      const double wj = PX[par * l + jn] - K * vj;
+      finish_column(jn, pre - (vk * wj + wk * vj));
+    }
+    TD3_MARK(4);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (l >= 2) {
+      const int i0 = l - 2, i1 = l - 1;
+      if (i0 % CL == r) dd[i0] = A[(size_t)(i0 / CL) * lp + i0];
+      if (i1 % CL == r) {
+        ee[i0] = A[(size_t)(i1 / CL) * lp + i0];
+        dd[i1] = A[(size_t)(i1 / CL) * lp + i1];
+      }
+    } else if (r == 0) {
+      dd[0] = A[0];
+    }
+  }
+  cl.sync();
+}
 }  // namespace netmfp
 
 #include <cstdio>
@@ -345,12 +610,22 @@ int main(int argc, char **argv) {
   double *S, *d, *e, *Hv, *hb;
   cudaMalloc(&S, l * l * 8); cudaMalloc(&d, l * 8); cudaMalloc(&e, l * 8); cudaMalloc(&Hv, l * l * 8); cudaMalloc(&hb, l * 8);
   cudaMemcpy(S, h.data(), l * l * 8, cudaMemcpyHostToDevice);
+  #ifdef TD4
+  const size_t smem = Td4<TNB>::smem_doubles(l) * 8;
+  cudaFuncSetAttribute(k_tridiag4<TNB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+#else
   const size_t smem = Td3<TCL, TNB>::smem_doubles(l) * 8;
   cudaFuncSetAttribute(k_tridiag3<TCL, TNB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+#endif
   std::vector<double> gd(l), ge(l), gd0, ge0;
   for (int r = 0; r < reps; ++r) {
     cudaMemset(d, 0, l * 8); cudaMemset(e, 0, l * 8);
+    
+#ifdef TD4
+    k_tridiag4<TNB><<<T4CL, T3T, smem>>>(S, l, d, e, Hv, hb);
+#else
     k_tridiag3<TCL, TNB><<<TCL, T3T, smem>>>(S, l, d, e, Hv, hb);
+#endif
     cudaError_t err = cudaDeviceSynchronize();
     if (err != cudaSuccess) { printf("err %s\n", cudaGetErrorString(err)); return 1; }
     cudaMemcpy(gd.data(), d, l * 8, cudaMemcpyDeviceToHost); cudaMemcpy(ge.data(), e, l * 8, cudaMemcpyDeviceToHost);
