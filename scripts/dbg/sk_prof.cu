@@ -5,7 +5,7 @@
 #include <cstdio>
 #include <vector>
 using namespace netmfp;
-namespace netmfp { void set_last_error(const std::string &) {} }
+namespace netmfp { void set_last_error(const std::string &) {} void dist_allreduce(Ctx &, void *, size_t, DType) {} }
 int main() {
   Ctx c; cudaStreamCreate(&c.stream);
   cudaDeviceProp prop; cudaGetDeviceProperties(&prop, 0); c.num_sms = prop.multiProcessorCount;
@@ -18,14 +18,17 @@ int main() {
   for (int i = 0; i < h * z; ++i) { hr[i] = (i * 7919) % n; hs[i] = (i & 1) ? 1.f : -1.f; }
   cudaMemcpy(rows, hr.data(), h * z * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(sg, hs.data(), h * z * 4, cudaMemcpyHostToDevice);
-  Mat Am{A, n, k, k}, Fm{F, n, k, k}, Ym{Y, n, h, 256};
+  Mat Fm{F, n, k, k}, Ym{Y, n, h, 256};
+  double *Cd; cudaMalloc(&Cd, k * k * 8);
+  { std::vector<double> I(k * k, 0.0); for (int i = 0; i < k; ++i) I[i * k + i] = 1.0; cudaMemcpy(Cd, I.data(), k * k * 8, cudaMemcpyHostToDevice); }
+  { std::vector<float> hf(n * k); for (int64_t i = 0; i < n * k; ++i) hf[i] = ((i * 2654435761u) % 1000) * 1e-3f - 0.5f; cudaMemcpy(F, hf.data(), n * k * 4, cudaMemcpyHostToDevice); }
   try {
     for (int rep = 0; rep < 3; ++rep) {
       unsigned long long zero[148 * 8] = {};
       cudaMemcpyToSymbol(g_skprof, zero, sizeof(zero));
       cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
       cudaEventRecord(e0, c.stream);
-      tc_sketch_y(c, Am, Fm, rows, sg, h, z, 6e5f, 0, Ym);
+      tc_sketch_y(c, Fm, Cd, k, rows, sg, h, z, 6e5f, 0, Ym, 0);
       cudaEventRecord(e1, c.stream);
       cudaStreamSynchronize(c.stream);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
