@@ -310,23 +310,31 @@ def run_ours(args):
         ev[i][0].record(stream)
         step()
         ev[i][1].record(stream)
+        if i == 0:
+            # the dominant family's launches are event-timed in the first timed
+            # step only: an event between two kernels breaks their programmatic
+            # dependent launch, so the other steps run as a user's would
+            # (reading syncs the host between steps, outside the step's events)
+            prof = ctx.profile_read()
+            ctx.profile(False)
     torch.cuda.synchronize()
     barrier(ws)
     clk = clocks.stop()
     launches = ctx.launches - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(step_ms))
-    prof = ctx.profile_read()
-    ctx.profile(False)
     ms_max = allreduce_max(ms, ws)
 
     # roofline of the dominant kernel family
+    # (profiled: the first timed step)
     if dom == "spmm":
-        roof = spmm_roofline(prof, args.steps, w, nr, nnz, ms, peaks, args.workload)
+        roof = spmm_roofline(prof, 1, w, nr, nnz, step_ms[0], peaks, args.workload)
     else:
-        kms = sum(v[1] for k, v in prof.items()) / args.steps
+        kms = sum(v[1] for k, v in prof.items())
         roof = {"kernel": dom, "bound": "alu", "achieved": None, "peak": None, "unit": "TFLOP/s",
-                "frac": None, "traffic": None, "share_of_step": kms / ms}
+                "frac": None, "traffic": None, "share_of_step": kms / step_ms[0]}
+    roof["timed_in"] = "timed step 1 of K (CUDA events around each of its launches of the family)"
+    kern_sum = sum(v[1] for k, v in prof_all.items() if not k.startswith("stage_") and k != "gaps")
 
     # e2e through the C ABI with pinned host buffers
     s_h = torch.from_numpy(s_np).pin_memory()
@@ -364,6 +372,13 @@ def run_ours(args):
                 "roofline": roof,
                 "kernel_ms_per_step": dict([(k, v[1]) for k, v in sorted(prof_all.items(), key=lambda x: -x[1][1])
                                             if not k.startswith("stage_")][:14]),
+                "gaps_ms": {"profiled_step": prof_all.get("gaps", (0, None))[1],
+                            "kernel_sum_profiled_step": kern_sum,
+                            "unprofiled_step": float(np.mean(step_ms[1:])) if len(step_ms) > 1 else None,
+                            "note": "idle stream time between kernels of the fully profiled (untimed) step, where "
+                                    "CUDA events around every launch also break programmatic dependent launch; an "
+                                    "unprofiled step (timed steps 2..K) is shorter than that step's kernel-time sum, "
+                                    "so its idle time is below what per-launch events resolve"},
                 "stage_ms_per_step": {k[6:]: v[1] for k, v in sorted(prof_all.items(), key=lambda x: -x[1][1])
                                       if k.startswith("stage_")},
                 "clocks": clk,
@@ -584,6 +599,13 @@ def run_dist(args):
                 "per_rank": all_ranks,
                 "kernel_ms_per_step": dict([(k, v[1]) for k, v in sorted(prof_all.items(), key=lambda x: -x[1][1])
                                             if not k.startswith("stage_")][:14]),
+                "gaps_ms": {"profiled_step": prof_all.get("gaps", (0, None))[1],
+                            "kernel_sum_profiled_step": kern_sum,
+                            "unprofiled_step": float(np.mean(step_ms[1:])) if len(step_ms) > 1 else None,
+                            "note": "idle stream time between kernels of the fully profiled (untimed) step, where "
+                                    "CUDA events around every launch also break programmatic dependent launch; an "
+                                    "unprofiled step (timed steps 2..K) is shorter than that step's kernel-time sum, "
+                                    "so its idle time is below what per-launch events resolve"},
                 "stage_ms_per_step": {k[6:]: v[1] for k, v in sorted(prof_all.items(), key=lambda x: -x[1][1])
                                       if k.startswith("stage_")},
                 "clocks": clk,
