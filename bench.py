@@ -543,6 +543,7 @@ def run_dist(args):
     ms = float(np.mean(step_ms))
     ms_max = allreduce_max(ms, ws)
     comm_ms = sum(v[1] for k, v in prof.items() if k.startswith("stage_comm")) / args.steps
+    kern_sum = sum(v[1] for k, v in prof_all.items() if not k.startswith("stage_") and k != "gaps")
     bytes_step = comm_bytes / args.steps
     # rows this rank's blocks hold after isolated-vertex compaction
     n_iso_local = int((g.export(ctx)[2] == 0).sum())

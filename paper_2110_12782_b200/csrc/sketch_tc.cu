@@ -29,6 +29,8 @@
 //               stages a row's 256/zp outputs per N tile in shared memory and
 //               writes them as one contiguous run; Z mode reduces zp lanes
 //               with shuffles and stores one value per (row group, col group).
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "tc_common.cuh"
@@ -85,22 +87,25 @@ __device__ __forceinline__ float apply_f(float x, int logmode) {
 // One 128 × NW accumulator tile → f, signs, segmented sums (see file header).
 // f is evaluated as ln2 · log2(max(scale x, 1)) (trunc_log) or log1p(max(scale x, 0)).
 // Column signs come as bit masks (neg, valid) of the N tile, 32 columns a word.
-template <int ZP, bool ZM, bool L1P>
-__device__ __forceinline__ void epi_tile(const SkP &p, uint32_t tb, int nt, int64_t row, float rsign, int lane) {
-  const int64_t j0 = (int64_t)nt * NW;
-  const int ncol = (int)min((int64_t)NW, p.ncols - j0);
-  uint32_t neg[NW / 32], val[NW / 32];
+// CW columns starting at column cbeg of the N tile (tb addresses column cbeg;
+// cbeg is a multiple of 32 and of the group size)
+template <int ZP, bool ZM, bool L1P, int CW = NW>
+__device__ __forceinline__ void epi_tile(const SkP &p, uint32_t tb, int nt, int64_t row, float rsign, int lane,
+                                         float xs = 1.f, int cbeg = 0) {
+  const int64_t j0 = (int64_t)nt * NW + cbeg;
+  const int ncol = (int)min((int64_t)CW, p.ncols - j0);
+  uint32_t neg[CW / 32], val[CW / 32];
 #pragma unroll
-  for (int w = 0; w < NW / 32; ++w) {
-    neg[w] = __ldg(p.neg_bits + nt * (NW / 32) + w);
-    val[w] = __ldg(p.val_bits + nt * (NW / 32) + w);
+  for (int w = 0; w < CW / 32; ++w) {
+    neg[w] = __ldg(p.neg_bits + (j0 >> 5) + w);
+    val[w] = __ldg(p.val_bits + (j0 >> 5) + w);
   }
-  const float sc = p.scale;
+  const float sc = p.scale * xs;
   constexpr float kLn2 = 0.69314718055994531f;
   float run = 0.f;
   float outs[16 / ZP > 0 ? 16 / ZP : 1];
 #pragma unroll
-  for (int cc = 0; cc < NW; cc += 16) {
+  for (int cc = 0; cc < CW; cc += 16) {
     if (cc < ncol) {
       float x[16];
       tmem_ld16(tb + (uint32_t)cc, x);
@@ -330,6 +335,232 @@ __global__ void __launch_bounds__(THREADS, 1) k_sketch_tc(const __grid_constant_
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// ---------------------------------------------------------------------------
+// Y mode with fp16-split operands.  Both operands are pre-split in global
+// memory: x·2^e = hi + lo with hi = fp16(x·2^e), lo = fp16(x·2^e − hi), the
+// power-of-two scale 2^e per row of A (max |A_i| in [2^14, 2^15)) and one
+// for all of B, so hi + lo carries ~22 significant bits like tf32 hi + lo,
+// and C = A_hi·B_hi + A_hi·B_lo + A_lo·B_hi (tcgen05.mma.kind::f16, fp32
+// accumulation) is within ~2^-22 relative of the fp32 product, as 3xTF32.
+// An fp16 MMA does twice the K of a tf32 one in the same time, and with the
+// split done once per operand no stage waits for split warps:
+//   warp 0      TMA: A hi/lo (128 rows × 64 fp16), B hi/lo (NW rows × 64)
+//   warp 1      tcgen05.mma kind::f16 ×3 per 16-deep K step
+//   warps 2-9   epilogue, two warps per TMEM lane quadrant (warp % 4), each
+//               on one half of the N tile's columns; the row's scale
+//               2^-e_i · 2^-e_B folded into the f(scale·x) multiply (with the
+//               MMA work halved, four epilogue warps were the bottleneck)
+// ---------------------------------------------------------------------------
+constexpr int HT = 320;
+constexpr int kEpiH = 256;  // epilogue threads: warps 2-9, two per TMEM lane quadrant
+constexpr int HBK = 64;                 // fp16 K per stage: one 128-B swizzled row
+constexpr int HABYTES = 128 * 128;      // A hi (or lo) chunk
+constexpr int HBBYTES = NW * 128;       // B hi (or lo) chunk
+constexpr int HSTAGE = 2 * HABYTES + 2 * HBBYTES;
+constexpr int HS = 2;
+// kind::f16 (fp16 A, B), D = f32, M = 128, both K-major
+__host__ __device__ constexpr uint32_t make_idesc_f16(int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+template <int ZP, bool L1P>
+__global__ void __launch_bounds__(HT, 1) k_sketch_h(const __grid_constant__ CUtensorMap tmAh,
+                                                    const __grid_constant__ CUtensorMap tmAl,
+                                                    const __grid_constant__ CUtensorMap tmBh,
+                                                    const __grid_constant__ CUtensorMap tmBl, const SkP p,
+                                                    const float *__restrict__ rinv, const int *__restrict__ bexp) {
+  grid_dep_enter();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = align1024(smem_raw);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(base + HS * HSTAGE);
+  uint64_t *full = bars, *empty = bars + HS;
+  uint64_t *done = bars + 2 * HS, *tfree = bars + 2 * HS + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * HS + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nitems = p.nmt * p.nsplit;
+  const int per = (p.ntn + p.nsplit - 1) / p.nsplit;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < HS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&done[b], 1);
+      mbar_init(&tfree[b], kEpiH);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmAh);
+      tma_prefetch_desc(&tmAl);
+      tma_prefetch_desc(&tmBh);
+      tma_prefetch_desc(&tmBl);
+    }
+    int64_t g = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int64_t mt = it / p.nsplit;
+      const int nt0 = (int)(it % p.nsplit) * per, nt1 = min(p.ntn, nt0 + per);
+      for (int nt = nt0; nt < nt1; ++nt) {
+        for (int kc = 0; kc < p.nk; ++kc, ++g) {
+          const int s = (int)(g % HS);
+          const int64_t use = g / HS;
+          if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+          uint8_t *st = base + s * HSTAGE;
+          if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)HSTAGE);
+          __syncwarp();
+          if (lane == 0) tma_load_2d(st, &tmAh, kc * HBK, (int)(mt * 128), &full[s]);
+          if (lane == 1) tma_load_2d(st + HABYTES, &tmAl, kc * HBK, (int)(mt * 128), &full[s]);
+          if (lane == 2) tma_load_2d(st + 2 * HABYTES, &tmBh, kc * HBK, nt * NW, &full[s]);
+          if (lane == 3) tma_load_2d(st + 2 * HABYTES + HBBYTES, &tmBl, kc * HBK, nt * NW, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    int64_t g = 0, tcount = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int nt0 = (int)(it % p.nsplit) * per, nt1 = min(p.ntn, nt0 + per);
+      for (int nt = nt0; nt < nt1; ++nt, ++tcount) {
+        const int buf = (int)(tcount & 1);
+        const int64_t use_b = tcount >> 1;
+        if (use_b > 0) mbar_wait(&tfree[buf], (uint32_t)((use_b - 1) & 1));
+        tc_fence_after();
+        const int64_t rem = p.ncols - (int64_t)nt * NW;
+        const int N = (int)std::min<int64_t>(NW, (rem + 15) / 16 * 16);
+        const uint32_t idesc = make_idesc_f16(N);
+        const uint32_t d = tmem + (uint32_t)(buf * NW);
+        for (int kc = 0; kc < p.nk; ++kc, ++g) {
+          const int s = (int)(g % HS);
+          const int64_t use = g / HS;
+          mbar_wait(&full[s], (uint32_t)(use & 1));
+          tc_fence_after();
+          const bool leader = elect_one();
+          const uint32_t ah = smem_u32(base + s * HSTAGE), al = ah + HABYTES;
+          const uint32_t bh = al + HABYTES, bl = bh + HBBYTES;
+          const uint64_t dah = make_desc(ah, 16, 1024), dal = make_desc(al, 16, 1024);
+          const uint64_t dbh = make_desc(bh, 16, 1024), dbl = make_desc(bl, 16, 1024);
+#pragma unroll
+          for (int ks = 0; ks < HBK / 16; ++ks) {
+            const uint32_t acc0 = (kc == 0 && ks == 0) ? 0u : 1u;
+            if (leader) {
+              mma_f16(d, dah + 2 * ks, dbh + 2 * ks, idesc, acc0);
+              mma_f16(d, dah + 2 * ks, dbl + 2 * ks, idesc, 1u);
+              mma_f16(d, dal + 2 * ks, dbh + 2 * ks, idesc, 1u);
+            }
+          }
+          __syncwarp();
+          if (leader) mma_commit(&empty[s]);
+          __syncwarp();
+        }
+        if (elect_one()) mma_commit(&done[buf]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // epilogue warps 2-9: TMEM lane quadrant q = warp % 4, column half hf
+    const int q = warp & 3;
+    const int hf = (warp - 2) >> 2;
+    const int r = 32 * q + lane;
+    const float bsc = ldexpf(1.f, -(14 - *bexp));
+    int64_t tcount = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int64_t mt = it / p.nsplit;
+      const int nt0 = (int)(it % p.nsplit) * per, nt1 = min(p.ntn, nt0 + per);
+      const int64_t row = mt * 128 + r;
+      const float xs = row < p.m ? __ldg(rinv + row) * bsc : 0.f;
+      for (int nt = nt0; nt < nt1; ++nt, ++tcount) {
+        const int buf = (int)(tcount & 1);
+        mbar_wait(&done[buf], (uint32_t)((tcount >> 1) & 1));
+        tc_fence_after();
+        const uint32_t tb = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * NW + hf * (NW / 2));
+        epi_tile<ZP, false, L1P, NW / 2>(p, tb, nt, row, 1.f, lane, xs, hf * (NW / 2));
+        tc_fence_before();
+        mbar_arrive(&tfree[buf]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// max over rows of ilogb(max_k |x|) (B's common exponent)
+__global__ void k_rows_maxexp(const float *__restrict__ src, int64_t rows, int k, int64_t lds, int *__restrict__ gexp) {
+  grid_dep_enter();
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  float m = 0.f;
+  if (idx < rows * k) m = fabsf(src[(idx / k) * lds + idx % k]);
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(gexp, ilogbf(m));
+}
+// fp16 hi/lo split of a row-major fp32 block (rows × k, stride lds) into
+// rows × kp (zero padded): a warp per row; the row's scale 2^e puts its
+// largest |x| in [2^14, 2^15) (gexp == nullptr) or uses the common exponent
+// *gexp; rinv[row] = 2^-e (per-row mode)
+__global__ void k_split_f16(const float *__restrict__ src, int64_t rows, int k, int64_t lds, int kp,
+                            __half *__restrict__ hi, __half *__restrict__ lo, float *__restrict__ rinv,
+                            const int *__restrict__ gexp) {
+  grid_dep_enter();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  // lane owns 8 consecutive entries per 256: two 16-B loads, one 16-B store per plane
+  const bool vec = (k % 8) == 0 && (lds % 4) == 0 && ((uintptr_t)src & 15) == 0;
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < rows; i += nw) {
+    const float *x = src + i * lds;
+    int e;
+    if (gexp) {
+      e = 14 - *gexp;
+    } else {
+      float m = 0.f;
+      if (vec) {
+        for (int c = 8 * lane; c < k; c += 256) {
+          const float4 a = *reinterpret_cast<const float4 *>(x + c), b = *reinterpret_cast<const float4 *>(x + c + 4);
+          m = fmaxf(m, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
+          m = fmaxf(m, fmaxf(fmaxf(fabsf(b.x), fabsf(b.y)), fmaxf(fabsf(b.z), fabsf(b.w))));
+        }
+      } else {
+        for (int c = lane; c < k; c += 32) m = fmaxf(m, fabsf(x[c]));
+      }
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      e = m > 0.f ? 14 - ilogbf(m) : 0;
+      if (lane == 0) rinv[i] = ldexpf(1.f, -e);
+    }
+    for (int c = 8 * lane; c < kp; c += 256) {
+      float v[8];
+      if (vec && c + 8 <= k) {
+        const float4 a = *reinterpret_cast<const float4 *>(x + c), b = *reinterpret_cast<const float4 *>(x + c + 4);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+      } else {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[t] = c + t < k ? x[c + t] : 0.f;
+      }
+      __align__(16) __half h[8], l[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const float y = ldexpf(v[t], e);
+        h[t] = __float2half_rn(y);
+        l[t] = __float2half_rn(y - __half2float(h[t]));
+      }
+      *reinterpret_cast<uint4 *>(hi + i * kp + c) = *reinterpret_cast<const uint4 *>(h);
+      *reinterpret_cast<uint4 *>(lo + i * kp + c) = *reinterpret_cast<const uint4 *>(l);
+    }
+  }
+}
+
 // rows of X at the sparse-sign coordinates, one zp-group per column c:
 // out row c·zp + t = X[rows[c·z + t]] for t < z, zero for the padding (sign 0);
 // optional tf32 lo part and the sign vector
@@ -411,6 +642,35 @@ static void launch_sketch(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mh, 
   NM_LAUNCH(c, "sketch_tc", launch_pdl(c.stream, kern, grid, THREADS, smem, ma, mh, ml, prm));
 }
 
+static void launch_sketch_h(Ctx &c, const CUtensorMap &mah, const CUtensorMap &mal, const CUtensorMap &mbh,
+                            const CUtensorMap &mbl, tcs::SkP &prm, const float *col_sign, const float *rinv,
+                            const int *bexp) {
+  using namespace tcs;
+  const int64_t nwords = (int64_t)prm.ntn * (NW / 32);
+  DBuf<uint32_t> bits((size_t)2 * nwords, c.stream);
+  NM_LAUNCH(c, "sign_bits", launch_pdl(c.stream, k_sign_bits, ceil_div(nwords, 128), 128, 0, col_sign, prm.ncols, nwords,
+                                       bits.p, bits.p + nwords));
+  prm.neg_bits = bits.p;
+  prm.val_bits = bits.p + nwords;
+  const size_t smem = 1024 + (size_t)HS * HSTAGE + (2 * HS + 4) * 8 + 16;
+  auto kern = k_sketch_h<8, false>;
+  switch (prm.zp * 2 + (prm.logmode ? 1 : 0)) {
+#define SKH_CASE(ZP, L1P) \
+  case (ZP) * 2 + (L1P): kern = k_sketch_h<ZP, L1P>; break;
+    SKH_CASE(2, 0) SKH_CASE(4, 0) SKH_CASE(8, 0) SKH_CASE(16, 0) SKH_CASE(32, 0) SKH_CASE(64, 0)
+    SKH_CASE(2, 1) SKH_CASE(4, 1) SKH_CASE(8, 1) SKH_CASE(16, 1) SKH_CASE(32, 1) SKH_CASE(64, 1)
+#undef SKH_CASE
+    default: NM_REQUIRE(false, "tc_sketch: unsupported group size");
+  }
+  smem_attr(kern, smem);
+  prm.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(prm.ntn, ceil_div(2 * (int64_t)c.num_sms, prm.nmt)));
+  const int per = (prm.ntn + prm.nsplit - 1) / prm.nsplit;
+  prm.nsplit = (prm.ntn + per - 1) / per;
+  const int64_t items = prm.nmt * prm.nsplit;
+  const unsigned grid = (unsigned)std::min<int64_t>(items, c.num_sms);
+  NM_LAUNCH(c, "sketch_tc", launch_pdl(c.stream, kern, grid, HT, smem, mah, mal, mbh, mbl, prm, rinv, bexp));
+}
+
 namespace tcs {
 // hi = x, lo = x - trunc_tf32(x) of an r × k block (row stride ld; padding columns stay 0)
 __global__ void k_split_hilo(const float *__restrict__ src, int64_t rows, int k, int64_t ld, float *__restrict__ hi,
@@ -460,6 +720,51 @@ void tc_sketch_y(Ctx &c, const Mat &F, const double *C, int64_t ldc, const int32
   // each gathered row lives on exactly one rank: the sum over ranks is exact
   dist_allreduce(c, g.p, (size_t)ncols * ldb, DType::F32);
   NM_LAUNCH(c, "transpose64", launch_pdl(c.stream, k_transpose64, ceil_div((int64_t)k * k, 256), 256, 0, C, k, ldc, Ct.p));
+  static const bool f16 = [] {
+    const char *v = getenv("NETMFP_SKETCH_F16");
+    return !v || atoi(v) != 0;
+  }();
+  if (f16) {
+    // fp16-split operands (k_sketch_h): B rows = F_r Cᵀ in fp32, then both
+    // operands split once into hi/lo fp16 planes
+    DBuf<float> bt((size_t)ncols * ldb, c.stream);
+    {
+      Mat Gm{g.p, ncols, k, ldb}, Om{bt.p, ncols, k, ldb};
+      gemm_tall(c, Gm, Ct.p, k, k, nullptr, 0.f, Om);
+    }
+    const int kp = (int)((k + HBK - 1) / HBK * HBK);
+    DBuf<__half> ah((size_t)n * kp, c.stream), al((size_t)n * kp, c.stream);
+    DBuf<__half> bhh((size_t)ncols * kp, c.stream), blh((size_t)ncols * kp, c.stream);
+    DBuf<float> rinv(n, c.stream);
+    DBuf<int> bexp(1, c.stream);
+    NM_CUDA(cudaMemsetAsync(bexp.p, 0x80, sizeof(int), c.stream));
+    NM_LAUNCH(c, "rows_maxexp", launch_pdl(c.stream, k_rows_maxexp, ceil_div(ncols * k, 256), 256, 0, bt.p, ncols, k,
+                                           ldb, bexp.p));
+    NM_LAUNCH(c, "split_f16", launch_pdl(c.stream, k_split_f16, ceil_div(ncols, 8), 256, 0, bt.p, ncols, k, ldb, kp,
+                                         bhh.p, blh.p, nullptr, bexp.p));
+    NM_LAUNCH(c, "split_f16", launch_pdl(c.stream, k_split_f16,
+                                         (unsigned)std::min<int64_t>(ceil_div(n, 8), (int64_t)c.num_sms * 16), 256, 0,
+                                         F.p, n, k, F.ld, kp, ah.p, al.p, rinv.p, nullptr));
+    CUtensorMap mah = make_map_f16(ah.p, n, kp, kp, 128), mal = make_map_f16(al.p, n, kp, kp, 128);
+    CUtensorMap mbh = make_map_f16(bhh.p, ncols, kp, kp, NW), mbl = make_map_f16(blh.p, ncols, kp, kp, NW);
+    SkP prm{};
+    prm.m = n;
+    prm.k = kp;
+    prm.nk = kp / HBK;
+    prm.ncols = ncols;
+    prm.ntn = (int)ceil_div(ncols, NW);
+    prm.nmt = ceil_div(n, 128);
+    prm.zp = zp;
+    prm.lzp = __builtin_ctz(zp);
+    prm.h = h;
+    prm.scale = scale;
+    prm.logmode = logmode;
+    prm.row_sign = nullptr;
+    prm.out = Y.p;
+    prm.ldo = Y.ld;
+    launch_sketch_h(c, mah, mal, mbh, mbl, prm, sg.p, rinv.p, bexp.p);
+    return;
+  }
   rows_times(c, g.p, ncols, k, ldb, Ct.p, bh.p, bl.p);  // B rows = F_r Cᵀ
   CUtensorMap ma = make_map(F.p, n, k, F.ld, 128, SW128, BK);
   CUtensorMap mh = make_map(bh.p, ncols, k, ldb, NW, SW128, BK);

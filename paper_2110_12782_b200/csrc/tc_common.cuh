@@ -222,6 +222,8 @@ __device__ __forceinline__ float deg_pow_dev(const int32_t *deg, int64_t i, floa
 enum MapSwizzle { SW128 = 0, SW128_32B = 1, SW64 = 2 };
 CUtensorMap make_map(const float *p, int64_t rows, int64_t cols, int64_t ld, int box_rows, MapSwizzle sw = SW128,
                      int box_cols = 32);
+// 2-D fp16 row-major, SWIZZLE_128B (box_cols = 64 fills a 128-B row)
+CUtensorMap make_map_f16(const void *p, int64_t rows, int64_t cols, int64_t ld, int box_rows, int box_cols = 64);
 // general fp32 tensor map: rank dims (innermost first), byte strides of dims 1..rank-1, box
 CUtensorMap make_map_nd(const float *p, int rank, const int64_t *dims, const int64_t *strides_bytes,
                         const int *box, MapSwizzle sw);

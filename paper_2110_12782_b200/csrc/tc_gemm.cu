@@ -654,6 +654,21 @@ CUtensorMap make_map(const float *p, int64_t rows, int64_t cols, int64_t ld, int
   return m;
 }
 
+// 2-D fp16 row-major [rows][cols] (row stride ld elements), box {box_cols, box_rows}, SWIZZLE_128B
+CUtensorMap make_map_f16(const void *p, int64_t rows, int64_t cols, int64_t ld, int box_rows, int box_cols) {
+  NM_REQUIRE(((uintptr_t)p & 15) == 0 && ld % 8 == 0, "tensor map (fp16): 16-byte aligned base and ld % 8 == 0 required");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1u, 1u};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(p), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(NETMFP_ERR_CUDA, "cuTensorMapEncodeTiled (fp16) failed: " + std::to_string((int)r));
+  return m;
+}
+
 CUtensorMap make_map_nd(const float *p, int rank, const int64_t *dims, const int64_t *strides_bytes, const int *box,
                         MapSwizzle sw) {
   NM_REQUIRE(((uintptr_t)p & 15) == 0 && rank >= 1 && rank <= 5, "tensor map: alignment / rank");
