@@ -89,7 +89,7 @@ __device__ __forceinline__ float apply_f(float x, int logmode) {
 // Column signs come as bit masks (neg, valid) of the N tile, 32 columns a word.
 // CW columns starting at column cbeg of the N tile (tb addresses column cbeg;
 // cbeg is a multiple of 32 and of the group size)
-template <int ZP, bool ZM, bool L1P, int CW = NW>
+template <int ZP, bool ZM, bool L1P, int CW = NW, bool VMASK = true>
 __device__ __forceinline__ void epi_tile(const SkP &p, uint32_t tb, int nt, int64_t row, float rsign, int lane,
                                          float xs = 1.f, int cbeg = 0) {
   const int64_t j0 = (int64_t)nt * NW + cbeg;
@@ -114,8 +114,9 @@ __device__ __forceinline__ void epi_tile(const SkP &p, uint32_t tb, int nt, int6
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         float v = L1P ? log1pf(fmaxf(sc * x[i], 0.f)) : __log2f(fmaxf(sc * x[i], 1.f));
-        v = ((vb >> i) & 1u) ? v : 0.f;
-        run += ((nb >> i) & 1u) ? -v : v;
+        // VMASK = false: padding columns have all-zero B rows, so f(0) = 0 already
+        if (VMASK) v = ((vb >> i) & 1u) ? v : 0.f;
+        run += __uint_as_float(__float_as_uint(v) ^ ((nb << (31 - i)) & 0x80000000u));  // sign s_{c,t}
         if (((i + 1) % ZP) == 0 || (ZP > 16 && i == 15 && ((cc + 16) % ZP) == 0)) {
           const float res = L1P ? run : run * kLn2;
           run = 0.f;
@@ -487,7 +488,7 @@ __global__ void __launch_bounds__(HT, 1) k_sketch_h(const __grid_constant__ CUte
         mbar_wait(&done[buf], (uint32_t)((tcount >> 1) & 1));
         tc_fence_after();
         const uint32_t tb = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * NW + hf * (NW / 2));
-        epi_tile<ZP, false, L1P, NW / 2>(p, tb, nt, row, 1.f, lane, xs, hf * (NW / 2));
+        epi_tile<ZP, false, L1P, NW / 2, false>(p, tb, nt, row, 1.f, lane, xs, hf * (NW / 2));
         tc_fence_before();
         mbar_arrive(&tfree[buf]);
       }
