@@ -371,7 +371,7 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t d
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
-template <int ZP, bool L1P>
+template <int ZP, bool ZM, bool L1P>
 __global__ void __launch_bounds__(HT, 1) k_sketch_h(const __grid_constant__ CUtensorMap tmAh,
                                                     const __grid_constant__ CUtensorMap tmAl,
                                                     const __grid_constant__ CUtensorMap tmBh,
@@ -483,12 +483,13 @@ __global__ void __launch_bounds__(HT, 1) k_sketch_h(const __grid_constant__ CUte
       const int nt0 = (int)(it % p.nsplit) * per, nt1 = min(p.ntn, nt0 + per);
       const int64_t row = mt * 128 + r;
       const float xs = row < p.m ? __ldg(rinv + row) * bsc : 0.f;
+      const float rsign = (ZM && row < p.m) ? __ldg(p.row_sign + row) : 1.f;
       for (int nt = nt0; nt < nt1; ++nt, ++tcount) {
         const int buf = (int)(tcount & 1);
         mbar_wait(&done[buf], (uint32_t)((tcount >> 1) & 1));
         tc_fence_after();
         const uint32_t tb = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * NW + hf * (NW / 2));
-        epi_tile<ZP, false, L1P, NW / 2, false>(p, tb, nt, row, 1.f, lane, xs, hf * (NW / 2));
+        epi_tile<ZP, ZM, L1P, NW / 2, false>(p, tb, nt, row, rsign, lane, xs, hf * (NW / 2));
         tc_fence_before();
         mbar_arrive(&tfree[buf]);
       }
@@ -643,6 +644,15 @@ static void launch_sketch(Ctx &c, const CUtensorMap &ma, const CUtensorMap &mh, 
   NM_LAUNCH(c, "sketch_tc", launch_pdl(c.stream, kern, grid, THREADS, smem, ma, mh, ml, prm));
 }
 
+// fp16-split sketches (k_sketch_h); NETMFP_SKETCH_F16=0 keeps 3xTF32 (A/B measurements)
+static bool sketch_f16() {
+  static const bool on = [] {
+    const char *v = getenv("NETMFP_SKETCH_F16");
+    return !v || atoi(v) != 0;
+  }();
+  return on;
+}
+
 static void launch_sketch_h(Ctx &c, const CUtensorMap &mah, const CUtensorMap &mal, const CUtensorMap &mbh,
                             const CUtensorMap &mbl, tcs::SkP &prm, const float *col_sign, const float *rinv,
                             const int *bexp) {
@@ -654,12 +664,14 @@ static void launch_sketch_h(Ctx &c, const CUtensorMap &mah, const CUtensorMap &m
   prm.neg_bits = bits.p;
   prm.val_bits = bits.p + nwords;
   const size_t smem = 1024 + (size_t)HS * HSTAGE + (2 * HS + 4) * 8 + 16;
-  auto kern = k_sketch_h<8, false>;
-  switch (prm.zp * 2 + (prm.logmode ? 1 : 0)) {
-#define SKH_CASE(ZP, L1P) \
-  case (ZP) * 2 + (L1P): kern = k_sketch_h<ZP, L1P>; break;
-    SKH_CASE(2, 0) SKH_CASE(4, 0) SKH_CASE(8, 0) SKH_CASE(16, 0) SKH_CASE(32, 0) SKH_CASE(64, 0)
-    SKH_CASE(2, 1) SKH_CASE(4, 1) SKH_CASE(8, 1) SKH_CASE(16, 1) SKH_CASE(32, 1) SKH_CASE(64, 1)
+  auto kern = k_sketch_h<8, false, false>;
+  switch (prm.zp * 4 + (prm.row_sign ? 2 : 0) + (prm.logmode ? 1 : 0)) {
+#define SKH_CASE(ZP, ZM, L1P) \
+  case (ZP) * 4 + (ZM) * 2 + (L1P): kern = k_sketch_h<ZP, ZM, L1P>; break;
+    SKH_CASE(2, 0, 0) SKH_CASE(4, 0, 0) SKH_CASE(8, 0, 0) SKH_CASE(16, 0, 0) SKH_CASE(32, 0, 0) SKH_CASE(64, 0, 0)
+    SKH_CASE(2, 0, 1) SKH_CASE(4, 0, 1) SKH_CASE(8, 0, 1) SKH_CASE(16, 0, 1) SKH_CASE(32, 0, 1) SKH_CASE(64, 0, 1)
+    SKH_CASE(2, 1, 0) SKH_CASE(4, 1, 0) SKH_CASE(8, 1, 0) SKH_CASE(16, 1, 0) SKH_CASE(32, 1, 0) SKH_CASE(64, 1, 0)
+    SKH_CASE(2, 1, 1) SKH_CASE(4, 1, 1) SKH_CASE(8, 1, 1) SKH_CASE(16, 1, 1) SKH_CASE(32, 1, 1) SKH_CASE(64, 1, 1)
 #undef SKH_CASE
     default: NM_REQUIRE(false, "tc_sketch: unsupported group size");
   }
@@ -721,11 +733,7 @@ void tc_sketch_y(Ctx &c, const Mat &F, const double *C, int64_t ldc, const int32
   // each gathered row lives on exactly one rank: the sum over ranks is exact
   dist_allreduce(c, g.p, (size_t)ncols * ldb, DType::F32);
   NM_LAUNCH(c, "transpose64", launch_pdl(c.stream, k_transpose64, ceil_div((int64_t)k * k, 256), 256, 0, C, k, ldc, Ct.p));
-  static const bool f16 = [] {
-    const char *v = getenv("NETMFP_SKETCH_F16");
-    return !v || atoi(v) != 0;
-  }();
-  if (f16) {
+  if (sketch_f16()) {
     // fp16-split operands (k_sketch_h): B rows = F_r Cᵀ in fp32, then both
     // operands split once into hi/lo fp16 planes
     DBuf<float> bt((size_t)ncols * ldb, c.stream);
@@ -812,6 +820,40 @@ void tc_sketch_z(Ctx &c, const Mat &F, const double *C, int64_t ldc, const int32
   }
   NM_CUDA(cudaMemcpyAsync(rs.p, sg.p, rs.n * 4, cudaMemcpyDeviceToDevice, c.stream));
   if (zp > 32) NM_CUDA(cudaMemset2DAsync(Zf, ldz * 4, 0, h * 4, h, c.stream));
+  if (sketch_f16()) {
+    // fp16-split operands as in tc_sketch_y: A = F(rows) C per-row scaled, B = F(rows) one common scale
+    const int kp = (int)((k + HBK - 1) / HBK * HBK);
+    DBuf<__half> a16h((size_t)nr * kp, c.stream), a16l((size_t)nr * kp, c.stream);
+    DBuf<__half> b16h((size_t)nr * kp, c.stream), b16l((size_t)nr * kp, c.stream);
+    DBuf<float> rinv(nr, c.stream);
+    DBuf<int> bexp(1, c.stream);
+    NM_CUDA(cudaMemsetAsync(bexp.p, 0x80, sizeof(int), c.stream));
+    NM_LAUNCH(c, "rows_maxexp", launch_pdl(c.stream, k_rows_maxexp, ceil_div(nr * k, 256), 256, 0, bh.p, nr, k, ldb,
+                                           bexp.p));
+    NM_LAUNCH(c, "split_f16", launch_pdl(c.stream, k_split_f16, ceil_div(nr, 8), 256, 0, bh.p, nr, k, ldb, kp,
+                                         b16h.p, b16l.p, nullptr, bexp.p));
+    NM_LAUNCH(c, "split_f16", launch_pdl(c.stream, k_split_f16, ceil_div(nr, 8), 256, 0, ah.p, nr, k, ldb, kp,
+                                         a16h.p, a16l.p, rinv.p, nullptr));
+    CUtensorMap mah = make_map_f16(a16h.p, nr, kp, kp, 128), mal = make_map_f16(a16l.p, nr, kp, kp, 128);
+    CUtensorMap mbh = make_map_f16(b16h.p, nr, kp, kp, NW), mbl = make_map_f16(b16l.p, nr, kp, kp, NW);
+    SkP prm{};
+    prm.m = nr;
+    prm.k = kp;
+    prm.nk = kp / HBK;
+    prm.ncols = nr;
+    prm.ntn = (int)ceil_div(nr, NW);
+    prm.nmt = ceil_div(nr, 128);
+    prm.zp = zp;
+    prm.lzp = __builtin_ctz(zp);
+    prm.h = h;
+    prm.scale = scale;
+    prm.logmode = logmode;
+    prm.row_sign = rs.p;
+    prm.out = Zf;
+    prm.ldo = ldz;
+    launch_sketch_h(c, mah, mal, mbh, mbl, prm, sg.p, rinv.p, bexp.p);
+    return;
+  }
   CUtensorMap ma = make_map(ah.p, nr, k, ldb, 128, SW128, BK);
   CUtensorMap mh = make_map(bh.p, nr, k, ldb, NW, SW128, BK);
   CUtensorMap ml = make_map(bl.p, nr, k, ldb, NW, SW128, BK);
