@@ -259,30 +259,41 @@ __global__ void __launch_bounds__(256) k_gaussian(Mat O, uint32_t k0, uint32_t k
     const int64_t gi = ids ? (int64_t)ids[i] : i + row0;
     const float sc = dpow_scale(deg, i, rexp);
     float *orow = O.p + i * O.ld;
-    for (int64_t q = lane; q < nq; q += 32) {
-      const U4 w = philox4x32_10(U4{(uint32_t)q, (uint32_t)(gi & 0xFFFFFFFF), (uint32_t)((uint64_t)gi >> 32), kTagOmega},
-                                 k0, k1);
-      // Box–Muller in fp32 (the block is fp32; |error| ~1e-7 relative to the fp64 oracle)
-      const float u0 = ((float)w.x + 0.5f) * 2.3283064365386963e-10f;  // 2^-32
-      const float u1 = ((float)w.y + 0.5f) * 2.3283064365386963e-10f;
-      const float u2 = ((float)w.z + 0.5f) * 2.3283064365386963e-10f;
-      const float u3 = ((float)w.w + 0.5f) * 2.3283064365386963e-10f;
-      // MUFU log2 / sin / cos (abs. error ~1e-6 on a N(0,1) draw; the oracle
-      // draws in fp64): (cos, sin)(2π u) = -(cos, sin)(2π (u - 1/2)), argument in [-π, π)
-      const float r0 = -sqrtf(-1.3862943611198906f * __log2f(u0)) * sc;
-      const float r2 = -sqrtf(-1.3862943611198906f * __log2f(u2)) * sc;
-      float s1, c1, s3, c3;
-      __sincosf(6.283185307179586f * (u1 - 0.5f), &s1, &c1);
-      __sincosf(6.283185307179586f * (u3 - 0.5f), &s3, &c3);
-      const float4 g = make_float4(r0 * c1, r0 * s1, r2 * c3, r2 * s3);
-      const int64_t j = 4 * q;
-      if (vec && j + 3 < O.cols) {
-        *reinterpret_cast<float4 *>(orow + j) = g;
-      } else {
-        orow[j] = g.x;
-        if (j + 1 < O.cols) orow[j + 1] = g.y;
-        if (j + 2 < O.cols) orow[j + 2] = g.z;
-        if (j + 3 < O.cols) orow[j + 3] = g.w;
+    // two counters per iteration: independent Philox chains interleave (ILP)
+    for (int64_t q0 = lane; q0 < nq; q0 += 64) {
+      U4 w[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t q = q0 + 32 * u;
+        w[u] = philox4x32_10(U4{(uint32_t)q, (uint32_t)(gi & 0xFFFFFFFF), (uint32_t)((uint64_t)gi >> 32), kTagOmega},
+                             k0, k1);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t q = q0 + 32 * u;
+        if (q >= nq) break;
+        // Box–Muller in fp32 (the block is fp32; |error| ~1e-7 relative to the fp64 oracle)
+        const float u0 = ((float)w[u].x + 0.5f) * 2.3283064365386963e-10f;  // 2^-32
+        const float u1 = ((float)w[u].y + 0.5f) * 2.3283064365386963e-10f;
+        const float u2 = ((float)w[u].z + 0.5f) * 2.3283064365386963e-10f;
+        const float u3 = ((float)w[u].w + 0.5f) * 2.3283064365386963e-10f;
+        // MUFU log2 / sin / cos (abs. error ~1e-6 on a N(0,1) draw; the oracle
+        // draws in fp64): (cos, sin)(2π u) = -(cos, sin)(2π (u - 1/2)), argument in [-π, π)
+        const float r0 = -sqrtf(-1.3862943611198906f * __log2f(u0)) * sc;
+        const float r2 = -sqrtf(-1.3862943611198906f * __log2f(u2)) * sc;
+        float s1, c1, s3, c3;
+        __sincosf(6.283185307179586f * (u1 - 0.5f), &s1, &c1);
+        __sincosf(6.283185307179586f * (u3 - 0.5f), &s3, &c3);
+        const float4 g = make_float4(r0 * c1, r0 * s1, r2 * c3, r2 * s3);
+        const int64_t j = 4 * q;
+        if (vec && j + 3 < O.cols) {
+          *reinterpret_cast<float4 *>(orow + j) = g;
+        } else {
+          orow[j] = g.x;
+          if (j + 1 < O.cols) orow[j + 1] = g.y;
+          if (j + 2 < O.cols) orow[j + 2] = g.z;
+          if (j + 3 < O.cols) orow[j + 3] = g.w;
+        }
       }
     }
   }
