@@ -386,6 +386,27 @@ __global__ void __launch_bounds__(256, MINB) k_spmm_fused(SpmmArgs p, FusedGraph
                        fg.nsegs, fg.part, fg.hcnt, gridDim.y, nblk_heavy, fg.nblk_tile);
 }
 
+// 286 = 2·128 + 30 columns in ONE launch: blockIdx.y < mpasses runs the
+// 128-column passes (warp per row), blockIdx.y == mpasses the narrow tail pass
+// (8-lane groups), so the tail's blocks start while the last 128-column
+// blocks drain instead of after them.  The two share the counter array
+// (stride mpasses + 1: the tail's counters are slot mpasses) and use disjoint
+// partial-slot regions.
+template <bool GEN>
+__global__ void __launch_bounds__(256, 8) k_spmm_fused_tail(SpmmArgs pm, SpmmArgs pt, FusedGraph fg, float *part_t,
+                                                            int nblk_heavy_m, int nblk_heavy_t) {
+  grid_dep_enter();
+  const int mpasses = (int)gridDim.y - 1;
+  if ((int)blockIdx.y < mpasses) {
+    fused_body<32, GEN>(pm, blockIdx.y, blockIdx.x, fg.rowptr, fg.col, fg.n, fg.heavy, fg.seg_ptr, fg.seg_e0,
+                        fg.seg_h, fg.nsegs, fg.part, fg.hcnt, gridDim.y, nblk_heavy_m, fg.nblk_tile);
+  } else {
+    if ((int)blockIdx.x >= fg.nblk_tile + nblk_heavy_t) return;
+    fused_body<8, GEN>(pt, 0, blockIdx.x, fg.rowptr, fg.col, fg.n, fg.heavy, fg.seg_ptr, fg.seg_e0, fg.seg_h,
+                       fg.nsegs, part_t, fg.hcnt + mpasses, gridDim.y, nblk_heavy_t, fg.nblk_tile);
+  }
+}
+
 // Warp-per-row path for a column scale s_col (general D^-a A D^-b): heavy
 // rows' partial sums from k_spmm_heavy, then k_spmm_rows with the epilogue.
 template <int LPR, bool SCOL, int MINB>
@@ -433,6 +454,31 @@ static void spmm_fused_impl(Ctx &c, const Graph &g, const SpmmArgs &p) {
     NM_LAUNCH(c, "spmm_fused", launch_pdl(c.stream, k_spmm_fused<LPR, 8, false>, grid, 256, 0, p, fg, nbh));
 }
 
+// main (multiple of 128 columns) + tail (<= 32 columns) in one launch
+static void spmm_fused_tail_impl(Ctx &c, const Graph &g, const SpmmArgs &pm, const SpmmArgs &pt) {
+  const unsigned mpasses = ceil_div(pm.cols, 128);
+  if (g.n_heavy > 0) {
+    const size_t need = (size_t)g.n_heavy_segs * (mpasses * 128 + 32), needc = (size_t)g.n_heavy * (mpasses + 1);
+    if (c.spmm_part.n < need) c.spmm_part.alloc(need, c.stream);
+    if (c.spmm_cnt.n < needc) {
+      c.spmm_cnt.alloc(needc, c.stream);
+      c.spmm_cnt.zero();
+    }
+  }
+  FusedGraph fg{g.rowptr, g.col, g.n, g.heavy, g.heavy_seg_ptr, g.seg_e0, g.seg_h, g.n_heavy_segs,
+                c.spmm_part.p, c.spmm_cnt.p, 0};
+  const int64_t ntiles = ceil_div(g.n, 32);
+  fg.nblk_tile = (int)std::min<int64_t>(ceil_div(ntiles, 8), (int64_t)c.num_sms * 32);
+  const int nbh_m = g.n_heavy > 0 ? (int)ceil_div(g.n_heavy_segs, 256 / 32) : 0;
+  const int nbh_t = g.n_heavy > 0 ? (int)ceil_div(g.n_heavy_segs, 256 / 8) : 0;
+  float *part_t = c.spmm_part.p ? c.spmm_part.p + (size_t)g.n_heavy_segs * mpasses * 128 : nullptr;
+  dim3 grid((unsigned)(fg.nblk_tile + nbh_m), mpasses + 1);
+  if (pm.prev || pm.acc_out || !pm.Y)
+    NM_LAUNCH(c, "spmm_fused", launch_pdl(c.stream, k_spmm_fused_tail<true>, grid, 256, 0, pm, pt, fg, part_t, nbh_m, nbh_t));
+  else
+    NM_LAUNCH(c, "spmm_fused", launch_pdl(c.stream, k_spmm_fused_tail<false>, grid, 256, 0, pm, pt, fg, part_t, nbh_m, nbh_t));
+}
+
 void spmm(Ctx &c, const Graph &g, const SpmmArgs &p_in) {
   SpmmArgs p = p_in;
   p.light_cap = g.light_cap;
@@ -455,6 +501,22 @@ void spmm(Ctx &c, const Graph &g, const SpmmArgs &p_in) {
     return v ? atoi(v) : 128;
   }();
   const int64_t main = p.cols / pass_w * pass_w, tail = p.cols - main;
+  static const bool merge_tail = [] {
+    const char *v = getenv("NETMFP_SPMM_MERGE_TAIL");
+    return !v || atoi(v) != 0;
+  }();
+  if (merge_tail && pass_w == 128 && main > 0 && tail > 0 && tail <= 32) {
+    SpmmArgs pm = p, pt = p;
+    pm.cols = main;
+    pt.cols = tail;
+    pt.X = p.X + main;
+    if (pt.Y) pt.Y = p.Y + main;
+    if (pt.prev) pt.prev = p.prev + main;
+    if (pt.acc_in) pt.acc_in = p.acc_in + main;
+    if (pt.acc_out) pt.acc_out = p.acc_out + main;
+    spmm_fused_tail_impl(c, g, pm, pt);
+    return;
+  }
   if (main > 0) {
     SpmmArgs pm = p;
     pm.cols = main;
