@@ -114,10 +114,11 @@ __global__ void k_gram_reduce(const float *__restrict__ part, int nslab, int64_t
 // tile (tiny graphs) use the CUDA-core kernels below.  There is no switch.
 constexpr int64_t kTcMinRows = 128;
 
-void gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg, bool exact) {
+void gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg, bool exact,
+          bool sym_result) {
   NM_REQUIRE(A.rows == B.rows, "gram: row mismatch");
   if (A.rows >= kTcMinRows) {
-    tc_gram(c, A, B, deg, wexp, G, ldg, exact);
+    tc_gram(c, A, B, deg, wexp, G, ldg, exact, sym_result && A.cols == B.cols);
     return;
   }
   const int64_t n = A.rows;

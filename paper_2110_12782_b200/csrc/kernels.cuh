@@ -61,8 +61,10 @@ void deg_pow(Ctx &c, const Graph &g, float e, float *out);  // out[i] = d_i^-e (
 // upper triangle is computed and mirrored.
 // exact = false: tf32 products only (~1e-3 relative; for CholeskyQR passes
 // whose output only needs to be a well-conditioned basis of the same span)
+// sym_result: AᵀWB is known to be symmetric (e.g. Pᵀ(A P) with A symmetric):
+// only the upper block-triangle is computed and mirrored.
 void gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg,
-          bool exact = true);
+          bool exact = true, bool sym_result = false);
 // C[n×b] = rs_i · (A[n×a] · Bs[a×b]) with Bs fp64 small (converted to fp32),
 // rs_i = d_i^-e (e = rexp, deg != null) else 1.
 void gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcols, const int32_t *deg,
@@ -71,7 +73,7 @@ void gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcol
 void tc_gemm_tall(Ctx &c, const Mat &A, const double *Bs, int64_t ldb, int64_t bcols, const int32_t *deg,
                   float rexp, const Mat &C);
 void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg,
-             bool exact = true);
+             bool exact = true, bool sym_result = false);
 void tc_gemm_tall_tri(Ctx &c, const Mat &A, const double *Rinv, int64_t ldb, int64_t bcols, const int32_t *deg,
                       float rexp, const Mat &C, bool exact = true);
 // C = rs · A · Rinv with Rinv (a×a) upper triangular (CholeskyQR's Y R⁻¹).  exact =

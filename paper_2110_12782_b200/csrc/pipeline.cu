@@ -88,7 +88,7 @@ void freigs(Ctx &c, const Graph &g, double alpha, int k, int s1, int q, uint64_t
   dist_spmm(c, g, P.m, s3, xfull);
   xfull.release();
   DBuf<double> S((size_t)l * l, s), lam(l, s), V((size_t)l * l, s);
-  gram(c, P.m, T.m, nullptr, 0.f, S, l);
+  gram(c, P.m, T.m, nullptr, 0.f, S, l, true, true);  // S = Pᵀ (A P) is symmetric: upper tiles only
   dist_allreduce(c, S, (size_t)l * l, DType::F64);
   symmetrize64(c, S, l, l);
   // step 8: [Û, Λ] = eig(S), ordered by |λ| [R3]

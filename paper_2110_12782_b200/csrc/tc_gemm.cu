@@ -736,7 +736,8 @@ __global__ void k_gram_wrow(const int32_t *__restrict__ deg, int64_t n, float e,
 }
 
 // G[a×b] (fp64, ldg) = Aᵀ diag(d^-wexp) B over the n rows
-void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg, bool exact) {
+void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp, double *G, int64_t ldg, bool exact,
+             bool sym_result) {
   using namespace tc;
   NM_REQUIRE(A.rows == B.rows, "tc_gram: row mismatch");
   const int64_t n = A.rows, a = A.cols, b = B.cols;
@@ -745,12 +746,15 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
     return;
   }
   const bool sym = (A.p == B.p && A.cols == B.cols && A.ld == B.ld);
+  // a symmetric result (same operand, or the caller says so) needs only the
+  // upper block-triangle of output units; the reduction mirrors it
+  const bool upper = sym || (sym_result && a == b);
   const int na_blk = (int)ceil_div(a, 32), nb_blk = (int)ceil_div(b, 32);
   // output units: M tiles of 128 rows (4 blocks of A), N ranges of <= 256 cols
   std::vector<GUnit> all;
   const int mt = (int)ceil_div(a, 128);
   for (int m = 0; m < mt; ++m) {
-    const int n_lo = sym ? 4 * m : 0;  // sym: upper block-triangle only
+    const int n_lo = upper ? 4 * m : 0;  // upper block-triangle only
     const int n_hi = nb_blk;
     int ncols = (n_hi - n_lo) * 32;
     if (ncols <= 0) continue;
@@ -843,7 +847,7 @@ void tc_gram(Ctx &c, const Mat &A, const Mat &B, const int32_t *deg, float wexp,
   for (int i = 0; i < R.nunits; ++i) R.u[i] = all[i];
   R.a = a;
   R.b = b;
-  R.sym = sym;
+  R.sym = upper;
   R.nchain = nchain;
   R.part_stride = total;
   NM_LAUNCH(c, "tc_gram_reduce",
