@@ -12,7 +12,7 @@ int main() {
   cudaMalloc(&A, n * ld * 4); cudaMalloc(&C, n * ld * 4); cudaMalloc(&B, K * K * 8);
   cudaMemset(A, 0, n * ld * 4); cudaMemset(B, 0, K * K * 8);
   Mat Am{A, n, K, ld}, Cm{C, n, K, ld};
-  for (int tri = 0; tri < 2; ++tri)
+  for (int tri = 0; tri < 3; ++tri)
   for (int rep = 0; rep < 2; ++rep) {
 #ifdef TC_PROF
     unsigned long long zero[1024 * 8] = {};
@@ -22,7 +22,7 @@ int main() {
     const int reps = rep ? 10 : 1;
     cudaEventRecord(e0, c.stream);
     for (int r = 0; r < reps; ++r) {
-      if (tri) tc_gemm_tall_tri(c, Am, B, K, K, nullptr, 0.f, Cm); else tc_gemm_tall(c, Am, B, K, K, nullptr, 0.f, Cm);
+      if (tri == 2) tc_gemm_tall_tri(c, Am, B, K, K, nullptr, 0.f, Cm, false); else if (tri) tc_gemm_tall_tri(c, Am, B, K, K, nullptr, 0.f, Cm); else tc_gemm_tall(c, Am, B, K, K, nullptr, 0.f, Cm);
     }
     cudaEventRecord(e1, c.stream);
     cudaStreamSynchronize(c.stream);
