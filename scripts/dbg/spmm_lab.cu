@@ -21,7 +21,7 @@
     }                                                                                  \
   } while (0)
 
-enum : int { H_COL = 1, H_Y = 2, H_X = 4, H_DET = 8, H_NACOL = 16, H_NAX = 32, H_U8 = 64, H_COOP = 128, H_COOP8 = 256, H_YCS = 512, H_PCG = 1024, H_PAIR = 2048 };
+enum : int { H_COL = 1, H_Y = 2, H_X = 4, H_DET = 8, H_NACOL = 16, H_NAX = 32, H_U8 = 64, H_COOP = 128, H_COOP8 = 256, H_YCS = 512, H_PCG = 1024, H_PAIR = 2048, H_V4 = 4096 };
 
 struct G {
   const int64_t *rowptr;
@@ -134,6 +134,20 @@ template <int HINT>
 __device__ __forceinline__ float4 gsum(const int32_t *col, int64_t e0, int64_t e1, const float *Xc, uint32_t ld,
                                        uint64_t pf, uint64_t pl) {
   float4 acc = make_float4(0, 0, 0, 0);
+  if (HINT & H_V4) {
+    // 4 column indices per 16-B load (every lane the same address: one wavefront),
+    // groups aligned to 4 entries, entries outside [e0, e1) predicated off
+    const float4 z = make_float4(0, 0, 0, 0);
+    for (int64_t e = e0 & ~(int64_t)3; e < e1; e += 4) {
+      const int4 q = __ldg(reinterpret_cast<const int4 *>(col + e));
+      const float4 x0 = (e >= e0) ? ldx<HINT>(Xc, (uint32_t)q.x, ld, pf, pl) : z;
+      const float4 x1 = (e + 1 >= e0 && e + 1 < e1) ? ldx<HINT>(Xc, (uint32_t)q.y, ld, pf, pl) : z;
+      const float4 x2 = (e + 2 >= e0 && e + 2 < e1) ? ldx<HINT>(Xc, (uint32_t)q.z, ld, pf, pl) : z;
+      const float4 x3 = (e + 3 < e1) ? ldx<HINT>(Xc, (uint32_t)q.w, ld, pf, pl) : z;
+      acc = add4(add4(add4(x0, x1), add4(x2, x3)), acc);
+    }
+    return acc;
+  }
   const int32_t *cp = col + e0;
   int cnt = (int)(e1 - e0);
   if (HINT & H_U8) {
@@ -192,7 +206,20 @@ __global__ void __launch_bounds__(256, MINB) k_lab(G g, int nblk_heavy) {
       const bool hv = dl > g.light_cap;
       const unsigned hmask = __ballot_sync(0xffffffffu, hv);
       uint32_t k0 = 0, k1 = 0, k2 = 0, k3 = 0;
-      if (!hv) {
+      if ((HINT & H_V4) && !hv && dl > 0) {
+        // the row's first 4 indices from one or two aligned 16-B loads
+        const int64_t a = rp & ~(int64_t)3;
+        const int off = (int)(rp - a);
+        const int4 qa = __ldg(reinterpret_cast<const int4 *>(col + a));
+        int4 qb = make_int4(0, 0, 0, 0);
+        if (off > 0 && dl > 4 - off) qb = __ldg(reinterpret_cast<const int4 *>(col + a + 4));
+        const uint32_t w[7] = {(uint32_t)qa.x, (uint32_t)qa.y, (uint32_t)qa.z, (uint32_t)qa.w,
+                               (uint32_t)qb.x, (uint32_t)qb.y, (uint32_t)qb.z};
+        k0 = off == 0 ? w[0] : off == 1 ? w[1] : off == 2 ? w[2] : w[3];
+        k1 = off == 0 ? w[1] : off == 1 ? w[2] : off == 2 ? w[3] : w[4];
+        k2 = off == 0 ? w[2] : off == 1 ? w[3] : off == 2 ? w[4] : w[5];
+        k3 = off == 0 ? w[3] : off == 1 ? w[4] : off == 2 ? w[5] : w[6];
+      } else if (!hv) {
         if (dl > 0) k0 = ldcol<HINT>(col + rp, pf);
         if (dl > 1) k1 = ldcol<HINT>(col + rp + 1, pf);
         if (dl > 2) k2 = ldcol<HINT>(col + rp + 2, pf);
@@ -888,7 +915,9 @@ int main(int argc, char **argv) {
   };
   G g{};
   g.rowptr = (int64_t *)up(rp.data(), rp.size() * 8);
+  col.resize(col.size() + 8, 0);  // 16-B index loads may read up to 7 entries past nnz
   g.col = (int32_t *)up(col.data(), col.size() * 4);
+  col.resize(nnz);
   int32_t *colt;
   CK(cudaMalloc(&colt, nnz * 4));
   g.colt = colt;
@@ -979,6 +1008,30 @@ int main(int argc, char **argv) {
     k_gather_ceiling<4, 8><<<dim3((unsigned)((nwarps + 7) / 8), 2), 256>>>(g.col, nnz, X, 288u, chunk, sink);
     CK(cudaDeviceSynchronize());
     printf("ncu pair done\n");
+    return 0;
+  }
+  if (getenv("LAB_CARVE")) {  // L1 / shared-memory carveout of the plain kernel (L1 capacity for hub rows)
+    run("ref det 2x128 (default carveout)", k_lab<32, H_DET>, 32, 2, 256, true, 3);
+    CK(cudaMemcpy(hr.data(), Yref, n * 288 * 4, cudaMemcpyDeviceToHost));
+    run("det 2x128 default carveout", k_lab<32, H_DET>, 32, 2, 256, false);
+    for (int cv : {0, 25, 50, 100}) {
+      CK(cudaFuncSetAttribute(k_lab<32, H_DET>, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
+      char nm[64];
+      snprintf(nm, sizeof nm, "det 2x128 carveout %d%% smem", cv);
+      run(nm, k_lab<32, H_DET>, 32, 2, 256, false);
+    }
+    printf("done\n");
+    return 0;
+  }
+  if (getenv("LAB_V4")) {  // 16-B column-index loads (fewer LSU wavefronts per gathered row)
+    run("ref det 2x128", k_lab<32, H_DET>, 32, 2, 256, true, 3);
+    CK(cudaMemcpy(hr.data(), Yref, n * 288 * 4, cudaMemcpyDeviceToHost));
+    run("det 2x128", k_lab<32, H_DET>, 32, 2, 256, false);
+    run("det v4 2x128", k_lab<32, H_DET | H_V4>, 32, 2, 256, false);
+    run("det 2x128 (again)", k_lab<32, H_DET>, 32, 2, 256, false);
+    run("det v4 2x128 (again)", k_lab<32, H_DET | H_V4>, 32, 2, 256, false);
+    run("det v4 2x128 minb6", k_lab<32, H_DET | H_V4, 6>, 32, 2, 256, false);
+    printf("done\n");
     return 0;
   }
   // reference: 2 x 128 plain
