@@ -3,7 +3,8 @@
 //               S = Pᵀ(AP), Eq. 3's K = Uᵀ D^(-1+2α) U
 //   gemm_tall:  C = diag(rs) · A · Bs — Q = Y R⁻¹, U = Q Û, F·C, E = Q Û √Σ
 //   gaussian_block: Ω = randn (Alg. 2 step 2, Philox [R1])
-// Round-1 SIMT fp32 kernels (FFMA); DESIGN.md §6 plans tcgen05 3xTF32.
+// Blocks of >= 128 rows run the tcgen05 kernels of tc_gemm.cu; the CUDA-core
+// kernels here serve only blocks shorter than one tensor-core M tile.
 #include "common.cuh"
 #include "kernels.cuh"
 
