@@ -917,13 +917,25 @@ static void tc_gemm_tall_impl(Ctx &c, const Mat &A, const double *Bs, int64_t ld
   p.astages = ST;
   const size_t smem = 1024 + S * stage + staging + (3 * S + 10) * 8;
   smem_attr(k_gemm_tc, kSmemMax);
-  // triangular B: part-major order and the unneeded K chunks skipped (every
-  // CTA streams the same Bᵀ chunks at the same time; measured 0.311 -> 0.295
-  // ms at n = 406727); full B: parts of a tile side by side (0.351 vs 0.362)
+  // Parts of a tile side by side (order 0: the two CTAs working on a tile's
+  // parts read its A rows once from HBM, the second time from L2), the
+  // unneeded K chunks of triangular B skipped.  Triangular B with an odd grid:
+  // every CTA alternates between the short and the long part, so neighbouring
+  // CTAs stay within a few K chunks of each other; configs[2], tall GEMM per
+  // embedding 2.91-3.06 -> 2.74-2.80 ms against part-major order (every CTA on
+  // the same part: A read twice, 755 MB per n'×286 call instead of ~470).
+  // NETMFP_GEMM_TRI_ORDER=1 restores part-major order for A/B measurements.
   p.bexact = exact ? 1 : 0;
-  p.order = tri ? 1 : 0;
+  static const int tri_order = [] {
+    const char *v = getenv("NETMFP_GEMM_TRI_ORDER");
+    return v ? atoi(v) : 0;
+  }();
+  p.order = tri ? tri_order : 0;
   p.skip = tri ? 1 : 0;
-  const int64_t grid = std::min<int64_t>(p.nitems, c.num_sms);
+  int64_t grid = std::min<int64_t>(p.nitems, c.num_sms);
+  // triangular B, parts side by side: an odd grid alternates every CTA
+  // between the short and the long part (an even one pins each CTA to one)
+  if (tri && p.order == 0 && nh == 2 && grid % 2 == 0 && grid > 1) --grid;
   CUtensorMap mc = make_map(C.p, n, bcols, C.ld, 32, SW128, 32);
   NM_LAUNCH(c, "tc_gemm_tall", launch_pdl(c.stream, k_gemm_tc, (unsigned)grid, NTG, smem, ma, mb, mc, p));
 }
