@@ -21,7 +21,7 @@
     }                                                                                  \
   } while (0)
 
-enum : int { H_COL = 1, H_Y = 2, H_X = 4, H_DET = 8, H_NACOL = 16, H_NAX = 32, H_U8 = 64, H_COOP = 128, H_COOP8 = 256, H_YCS = 512, H_PCG = 1024, H_PAIR = 2048, H_V4 = 4096 };
+enum : int { H_COL = 1, H_Y = 2, H_X = 4, H_DET = 8, H_NACOL = 16, H_NAX = 32, H_U8 = 64, H_COOP = 128, H_COOP8 = 256, H_YCS = 512, H_PCG = 1024, H_PAIR = 2048, H_V4 = 4096, H_PF = 8192 };
 
 struct G {
   const int64_t *rowptr;
@@ -150,6 +150,10 @@ __device__ __forceinline__ float4 gsum(const int32_t *col, int64_t e0, int64_t e
   }
   const int32_t *cp = col + e0;
   int cnt = (int)(e1 - e0);
+  if (HINT & H_PF) {  // the later index lines of this range into L1 ahead of use (no registers)
+    for (int off = 32 - (int)(((uintptr_t)cp >> 2) & 31); off < cnt; off += 32)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(cp + off));
+  }
   if (HINT & H_U8) {
     for (; cnt >= 8; cnt -= 8, cp += 8) {
       uint32_t v[8];
@@ -1020,6 +1024,16 @@ int main(int argc, char **argv) {
       snprintf(nm, sizeof nm, "det 2x128 carveout %d%% smem", cv);
       run(nm, k_lab<32, H_DET>, 32, 2, 256, false);
     }
+    printf("done\n");
+    return 0;
+  }
+  if (getenv("LAB_PF")) {  // L1 prefetch of a segment's later column-index lines
+    run("ref det 2x128", k_lab<32, H_DET>, 32, 2, 256, true, 3);
+    CK(cudaMemcpy(hr.data(), Yref, n * 288 * 4, cudaMemcpyDeviceToHost));
+    run("det 2x128", k_lab<32, H_DET>, 32, 2, 256, false);
+    run("det pf 2x128", k_lab<32, H_DET | H_PF>, 32, 2, 256, false);
+    run("det 2x128 (again)", k_lab<32, H_DET>, 32, 2, 256, false);
+    run("det pf 2x128 (again)", k_lab<32, H_DET | H_PF>, 32, 2, 256, false);
     printf("done\n");
     return 0;
   }
