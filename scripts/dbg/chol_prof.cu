@@ -17,7 +17,7 @@ int main() {
     cudaMemcpy(G, h.data(), l * l * 8, cudaMemcpyHostToDevice);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0, c.stream);
-    chol_inv_df(c, G, l, l, R, flag);
+    chol_inv_df(c, G, l, l, R, flag, 0.0);
     cudaEventRecord(e1, c.stream);
     cudaStreamSynchronize(c.stream);
     float ms; cudaEventElapsedTime(&ms, e0, e1);

@@ -1,9 +1,11 @@
-"""The two A/B switches of the library must not change what is computed:
+"""The A/B switches of the library must not change what is computed:
 programmatic dependent launch (NETMFP_PDL) only changes when a kernel's launch
 is processed, so an embedding is bitwise identical with and without it; the
 fp16-split sketches (NETMFP_SKETCH_F16, default) and the 3xTF32 ones are two
 ~22-bit evaluations of the same Eq. 5 sums, within the sketch tolerance of
-each other (1e-4 relative Frobenius, north_star).  Each setting runs in its
+each other (1e-4 relative Frobenius, north_star); the tall GEMM's item order
+(NETMFP_GEMM_TRI_ORDER: which CTA computes which output tile) cannot change
+any tile's arithmetic, so CholeskyQR output is bitwise identical.  Each setting runs in its
 own process (the switches are read once per process)."""
 import json
 import os
@@ -75,3 +77,39 @@ def test_fp16_split_sketch_matches_3xtf32(tmp_path):
     assert relf(h["Z"], t["Z"]) <= 1e-4, relf(h["Z"], t["Z"])
     # the eigen side (Alg. 2) does not use the sketch: identical
     assert np.array_equal(h["lam"], t["lam"])
+
+
+GEMM_CHILD = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ROOT)
+import __graft_entry__ as ge
+ge.build()
+from paper_2110_12782_b200 import _lib as L
+ctx = L.Context(0)
+n, c = 50001, 286  # two column parts of the triangular R^-1 GEMM, ragged last M tile
+Yh = (np.random.default_rng(7).standard_normal((n, c)) * np.logspace(0, 2, c)[None, :]).astype(np.float32)
+Y = torch.zeros(n, 288, dtype=torch.float32, device="cuda")[:, :c]
+Y.copy_(torch.from_numpy(Yh))
+outs = {}
+for passes in (1, 2):
+    Q = torch.zeros(n, 288, dtype=torch.float32, device="cuda")[:, :c]
+    L.netmfp_orthonormalize(ctx, Y, Q, passes)
+    outs[f"Q{passes}"] = Q.cpu().numpy()
+torch.cuda.synchronize()
+np.savez(OUT, **outs)
+'''
+
+
+def test_gemm_item_order_is_bitwise_neutral(tmp_path):
+    res = {}
+    for order in ("0", "1"):
+        out = str(tmp_path / f"gemm{order}.npz")
+        code = f"ROOT = {ROOT!r}\nOUT = {out!r}\n" + GEMM_CHILD
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, NETMFP_GEMM_TRI_ORDER=order),
+                           capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-3000:]
+        res[order] = dict(np.load(out))
+    for key in res["0"]:
+        assert np.array_equal(res["0"][key], res["1"][key]), key
+    q = res["0"]["Q2"].astype(np.float64)
+    assert np.abs(q.T @ q - np.eye(q.shape[1])).max() <= 1e-4
