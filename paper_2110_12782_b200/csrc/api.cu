@@ -226,6 +226,12 @@ int netmfp_ctx_destroy(netmfp_ctx *ctx) {
       dist_destroy(ctx->c);
     } catch (...) {
     }
+    if (ctx->c.side) {
+      cudaStreamSynchronize(ctx->c.side);
+      cudaStreamDestroy(ctx->c.side);
+      cudaEventDestroy(ctx->c.ev_fork);
+      cudaEventDestroy(ctx->c.ev_join);
+    }
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
     delete ctx;
   });

@@ -130,6 +130,10 @@ struct Ctx {
   int nranks = 1, rank = 0;
   void *comm = nullptr;  // ncclComm_t
   cudaStream_t comm_stream = nullptr;  // NCCL stream (overlaps all-gathers with SpMM passes)
+  // single-GPU side stream for work independent of the main chain (Alg. 4's
+  // Z sketch beside orth(Y)), forked / joined by events; created on first use
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   netmfp_comm_ops ops{};  // host-staged communicator (netmfp_dist_init_ops) when ops_on
   bool ops_on = false;
   int64_t collectives = 0;

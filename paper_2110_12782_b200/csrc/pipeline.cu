@@ -1,5 +1,6 @@
 // pipeline.cu — the NetMF+ stages of Alg. 5 on device blocks.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -194,24 +195,53 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
     tc_sketch_y(c, F, C, k, Psi.rows, Psi.signs, h2, z, fs, logmode, Y.m, row0);
   }
   if (Yout) copy_block(c, Y.m.p, Y.m.ld, Yout->p, Yout->ld, n, h2);
+  // steps 5-6 need F, C and Π only, not Q: on one GPU they run on the side
+  // stream while step 4 (CholeskyQR2 of Y, whose Cholesky factors occupy 37
+  // SMs on a latency-bound chain) runs on the main one; joined before step 7
+  static const bool side_on = [] {  // NETMFP_SIDE_STREAM=0: everything on the main stream (A/B)
+    const char *v = getenv("NETMFP_SIDE_STREAM");
+    return !(v && atoi(v) == 0);
+  }();
+  const bool fork = side_on && c.nranks == 1 && !c.comm && !c.ops_on;
+  DBuf<double> Z((size_t)h3 * h3, s), PtQ((size_t)h3 * h2, s);
+  SparseSign Pi;
+  if (fork) {
+    if (!c.side) {
+      NM_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+      NM_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+      NM_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
+    }
+    NM_CUDA(cudaEventRecord(c.ev_fork, s));
+    NM_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+    c.stream = c.side;
+  }
+  try {
+    // step 5: Π
+    {
+      NM_STAGE(c, "stage_gen_sparse_sign");
+      gen_sparse_sign(c, n_global, h3, z, seed, kTagPi, Pi);
+      if (comp_id) remap_rows(c, Pi.rows, h3 * z, comp_id);
+    }
+    // step 6: Z = Πᵀ f(scale F(p,:) C F(p,:)ᵀ) Π  (both sides restricted to Π's coordinates)
+    NM_STAGE(c, "stage_sketch_z");
+    DBuf<float> Zf((size_t)h3 * h3, c.stream);
+    tc_sketch_z(c, F, C, k, Pi.rows, Pi.signs, h3, z, fs, logmode, Zf, h3, row0);
+    f32_to_f64(c, Zf, h3, Z, h3, h3, h3);
+  } catch (...) {
+    c.stream = s;
+    throw;
+  }
+  if (fork) {
+    NM_CUDA(cudaEventRecord(c.ev_join, c.side));
+    c.stream = s;
+    Pi.rows.s = s;  // freed after their last use on the main stream
+    Pi.signs.s = s;
+  }
   // step 4: Q = orth(Y)   (CholeskyQR2 [R7])
   cholqr(c, Y.m, Qb.m, nullptr, 0.f, 2, &Tb.m);
   check_flag(c, "single-pass SVD orth(Y)");
-  // step 5: Π
-  SparseSign Pi;
-  {
-    NM_STAGE(c, "stage_gen_sparse_sign");
-    gen_sparse_sign(c, n_global, h3, z, seed, kTagPi, Pi);
-    if (comp_id) remap_rows(c, Pi.rows, h3 * z, comp_id);
-  }
-  // step 6: Z = Πᵀ f(scale F(p,:) C F(p,:)ᵀ) Π  (both sides restricted to Π's coordinates)
+  if (fork) NM_CUDA(cudaStreamWaitEvent(s, c.ev_join, 0));
   NM_STAGE(c, "stage_sketch_z_core");
-  DBuf<double> Z((size_t)h3 * h3, s), PtQ((size_t)h3 * h2, s);
-  {
-    DBuf<float> Zf((size_t)h3 * h3, s);
-    tc_sketch_z(c, F, C, k, Pi.rows, Pi.signs, h3, z, fs, logmode, Zf, h3, row0);
-    f32_to_f64(c, Zf, h3, Z, h3, h3, h3);
-  }
   if (Zout) NM_CUDA(cudaMemcpyAsync(Zout, Z.p, (size_t)h3 * h3 * 8, cudaMemcpyDeviceToDevice, s));
   // step 7: S = (ΠᵀQ)† Z (QᵀΠ)†  via the normal equations in fp64
   sign_gather_T(c, Pi, Qb.m, PtQ, h2, row0);
