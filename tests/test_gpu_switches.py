@@ -5,7 +5,9 @@ fp16-split sketches (NETMFP_SKETCH_F16, default) and the 3xTF32 ones are two
 ~22-bit evaluations of the same Eq. 5 sums, within the sketch tolerance of
 each other (1e-4 relative Frobenius, north_star); the tall GEMM's item order
 (NETMFP_GEMM_TRI_ORDER: which CTA computes which output tile) cannot change
-any tile's arithmetic, so CholeskyQR output is bitwise identical.  Each setting runs in its
+any tile's arithmetic, so CholeskyQR output is bitwise identical; running
+Alg. 4's Z sketch on the side stream (NETMFP_SIDE_STREAM) only changes when
+it runs, so the embedding is bitwise identical.  Each setting runs in its
 own process (the switches are read once per process)."""
 import json
 import os
@@ -66,6 +68,13 @@ def relf(a, b):
 def test_pdl_is_bitwise_neutral(tmp_path):
     on = run(tmp_path, "pdl1", {"NETMFP_PDL": "1"})
     off = run(tmp_path, "pdl0", {"NETMFP_PDL": "0"})
+    for key in on:
+        assert np.array_equal(on[key], off[key]), key
+
+
+def test_side_stream_is_bitwise_neutral(tmp_path):
+    on = run(tmp_path, "side1", {"NETMFP_SIDE_STREAM": "1"})
+    off = run(tmp_path, "side0", {"NETMFP_SIDE_STREAM": "0"})
     for key in on:
         assert np.array_equal(on[key], off[key]), key
 
