@@ -176,6 +176,14 @@ int netmfp_spmm(netmfp_ctx *ctx, const netmfp_graph *g, double a, double b, cons
 
 /* ---- dense steps of Alg. 2 / Alg. 4 (exposed for step-wise parity) ---------- */
 
+/* Omega = randn(n, l) of Alg. 2 step 2: entries (i, 4q..4q+3)
+ * from Philox4x32-10 on counter (q, i mod 2^32, i >> 32, tag Omega) with key
+ * (seed mod 2^32, seed >> 32) and Box-Muller on both word pairs [R1] -- the
+ * draw netmfp_eig / netmfp_embed use (before their degree row scale).
+ * Omega: n×l fp32, row-major, ld >= l (device: ld % 4 == 0, 16-B aligned),
+ * caller-owned.  Errors: NETMFP_ERR_ARG for l < 1, n < 0 or ld < l. */
+int netmfp_gaussian(netmfp_ctx *ctx, int64_t n, int64_t l, uint64_t seed, float *Omega, int64_t ld, int mem);
+
 /* G = Aᵀ B over the n rows (fp64 result, row-major a×b).  A: n×a fp32 (lda),
  * B: n×b fp32 (ldb).  The Gram matrix of eigSVD/CholeskyQR. */
 int netmfp_gram(netmfp_ctx *ctx, int64_t n, const float *A, int64_t lda, int64_t a, const float *B,

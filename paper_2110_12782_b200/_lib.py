@@ -54,6 +54,7 @@ _SIGS = {
     "netmfp_graph_free": (C.c_int, [_p]),
     "netmfp_partition_rows": (C.c_int, [_p, _i64, _i32, _p]),
     "netmfp_spmm": (C.c_int, [_p, _p, _d, _d, _p, _i64, _p, _i64, _i64, C.c_int]),
+    "netmfp_gaussian": (C.c_int, [_p, _i64, _i64, C.c_uint64, _p, _i64, C.c_int]),
     "netmfp_gram": (C.c_int, [_p, _i64, _p, _i64, _i64, _p, _i64, _i64, _p, C.c_int]),
     "netmfp_orthonormalize": (C.c_int, [_p, _i64, _i64, _p, _i64, _p, _i64, _i32, C.c_int]),
     "netmfp_sym_eig": (C.c_int, [_p, _p, _i64, _p, _p, _i32, C.c_int]),
@@ -328,6 +329,12 @@ def netmfp_spmm(ctx, g: Graph, a: float, b: float, X, Y, cols=None):
     _check(_L.netmfp_spmm(ctx.h, g.h, a, b, _ptr(X), _ld(X, "float32"), _ptr(Y), _ld(Y, "float32"),
                           cols, mem))
     return Y
+
+
+def netmfp_gaussian(ctx, seed, Omega):
+    mem = _same_mem(Omega)
+    _check(_L.netmfp_gaussian(ctx.h, Omega.shape[0], Omega.shape[1], seed, _ptr(Omega), _ld(Omega, "float32"), mem))
+    return Omega
 
 
 def netmfp_gram(ctx, A, B, G):

@@ -443,6 +443,21 @@ int netmfp_spmm(netmfp_ctx *ctx, const netmfp_graph *gr, double a, double b, con
   });
 }
 
+int netmfp_gaussian(netmfp_ctx *ctx, int64_t n, int64_t l, uint64_t seed, float *Omega, int64_t ld, int mem) {
+  return guarded([&] {
+    NM_REQUIRE(ctx && Omega, "gaussian: NULL argument");
+    NM_REQUIRE(n >= 0 && l >= 1 && ld >= l, "gaussian: need n >= 0, l >= 1, ld >= l");
+    check_mem(mem);
+    Ctx &c = ctx->c;
+    DevScope _dev(c);
+    if (n == 0) return;
+    InMat out(c, Omega, n, l, ld, mem, false);
+    gaussian_block(c, out.m, seed, nullptr, 0.f, 0, nullptr);  // Alg. 2 step 2, no row scale
+    out.copy_out(c, Omega, ld, mem);
+    finish(c);
+  });
+}
+
 int netmfp_gram(netmfp_ctx *ctx, int64_t n, const float *A, int64_t lda, int64_t a, const float *B,
                 int64_t ldb, int64_t b, double *G, int mem) {
   return guarded([&] {
