@@ -683,16 +683,32 @@ static void embed_core(Ctx &c, const Graph &g, const netmfp_params &p, const Mat
     freigs(c, g, p.alpha, p.k, p.s1, p.q, p.seed, F.m, lam, true);    // Alg. 5 step 1 (F = D^(-1+α) U)
   }
   if (lambda_dev) NM_CUDA(cudaMemcpyAsync(lambda_dev, lam.p, p.k * 8, cudaMemcpyDeviceToDevice, s));
+  // the Y sketch's A operand (F split into fp16 planes) needs F only: on one
+  // GPU it is prepared on the side stream while Eq. 3 runs on the main one
+  SketchA preA;
+  bool pre = false;
+  if (sketch_uses_split() && side_fork(c)) {
+    try {
+      sketch_split_a(c, F.m, preA);
+    } catch (...) {
+      c.stream = s;
+      throw;
+    }
+    side_join_point(c, s);
+    preA.set_stream(s);
+    pre = true;
+  }
   {
     NM_STAGE(c, "stage_factor_pair");
     factor_pair(c, g, p.alpha, p.T, F.m, lam, p.k, F.m, C, true);      // steps 2-3
   }
+  if (pre) NM_CUDA(cudaStreamWaitEvent(s, c.ev_join, 0));
   const double scale = (double)g.nnz_global / (p.b * p.T);           // vol(G)/(bT)
   {
     NM_STAGE(c, "stage_sketch_svd");
     sketch_svd(c, F.m, C, p.k, scale, p.d, p.s2, p.s3, p.z, p.seed, p.logmode, nullptr, sigma_dev, &E,
                nullptr, nullptr, g.row0, compacted ? g.n_orig : g.n_global,
-               compacted ? g.comp_id.p : nullptr);                     // steps 4-5
+               compacted ? g.comp_id.p : nullptr, pre ? &preA : nullptr);  // steps 4-5
   }
   F.buf.release();
   {

@@ -134,8 +134,21 @@ void gen_sparse_sign(Ctx &c, int64_t n, int64_t h, int64_t z, uint64_t seed, uin
 // Y[n×h] = f(scale · F C F(rows)ᵀ) Ψ  (Eq. 5 sketch), tensor cores
 // (F holds this rank's rows [row0, row0 + F.rows); the gathered rows are
 // summed over ranks)
+// A operand of the fp16-split Y sketch: F split once into hi / lo fp16 planes
+// with per-row power-of-two scales (depends on F only, so embed prepares it
+// on the side stream while Eq. 3 runs)
+struct SketchA {
+  int64_t n = 0;
+  int k = 0, kp = 0;
+  DBuf<uint16_t> hi, lo;  // n × kp fp16 bit patterns
+  DBuf<float> rinv;       // per-row 2^-e
+  void set_stream(cudaStream_t s) { hi.s = s; lo.s = s; rinv.s = s; }
+};
+bool sketch_uses_split();  // the fp16-split path is on (NETMFP_SKETCH_F16)
+void sketch_split_a(Ctx &c, const Mat &F, SketchA &A);
 void tc_sketch_y(Ctx &c, const Mat &F, const double *C, int64_t ldc, const int32_t *rows, const float *signs,
-                 int64_t h, int z, float scale, int logmode, const Mat &Y, int64_t row0 = 0);
+                 int64_t h, int z, float scale, int logmode, const Mat &Y, int64_t row0 = 0,
+                 const SketchA *pre = nullptr);
 // Zf[h×h] (fp32, ldz) = Πᵀ f(scale · F C Fᵀ restricted to Π's rows) Π  (Alg. 4 step 6)
 void tc_sketch_z(Ctx &c, const Mat &F, const double *C, int64_t ldc, const int32_t *rows, const float *signs,
                  int64_t h, int z, float scale, int logmode, float *Zf, int64_t ldz, int64_t row0 = 0);

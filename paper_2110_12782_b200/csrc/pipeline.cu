@@ -167,10 +167,37 @@ __global__ void k_abs(const double *lam, int d, double *out) {
   if (i < d) out[i] = fabs(lam[i]);
 }
 
+// Side stream (one GPU): side_fork() makes c.stream the side stream, ordered
+// after everything queued so far on the main one; side_join_point() records
+// where it ends and switches back; the main stream waits on c.ev_join where it
+// needs the side's results.  NETMFP_SIDE_STREAM=0 keeps everything on the main
+// stream (A/B measurements).
+bool side_fork(Ctx &c) {
+  static const bool side_on = [] {
+    const char *v = getenv("NETMFP_SIDE_STREAM");
+    return !(v && atoi(v) == 0);
+  }();
+  if (!side_on || c.nranks != 1 || c.comm || c.ops_on) return false;
+  if (!c.side) {
+    NM_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+    NM_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+    NM_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
+  }
+  NM_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+  NM_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+  c.stream = c.side;
+  return true;
+}
+void side_join_point(Ctx &c, cudaStream_t main) {
+  NM_CUDA(cudaEventRecord(c.ev_join, c.side));
+  c.stream = main;
+}
+
 // Alg. 4
 void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int d, int s2, int s3, int z,
                 uint64_t seed, int logmode, const Mat *Uout, double *sigma_dev, const Mat *Eout,
-                const Mat *Yout, double *Zout, int64_t row0, int64_t n_global, const int32_t *comp_id) {
+                const Mat *Yout, double *Zout, int64_t row0, int64_t n_global, const int32_t *comp_id,
+                const SketchA *preA) {
   const int64_t n = F.rows;  // this rank's rows [row0, row0 + n) of n_global
   if (n_global < 0) n_global = n;
   // comp_id (compacted graph): Ψ and Π are drawn over the n_global original
@@ -192,29 +219,15 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
   Block Y(n, h2, s), Qb(n, h2, s), Tb(n, h2, s);
   {
     NM_STAGE(c, "stage_sketch_y");
-    tc_sketch_y(c, F, C, k, Psi.rows, Psi.signs, h2, z, fs, logmode, Y.m, row0);
+    tc_sketch_y(c, F, C, k, Psi.rows, Psi.signs, h2, z, fs, logmode, Y.m, row0, preA);
   }
   if (Yout) copy_block(c, Y.m.p, Y.m.ld, Yout->p, Yout->ld, n, h2);
   // steps 5-6 need F, C and Π only, not Q: on one GPU they run on the side
   // stream while step 4 (CholeskyQR2 of Y, whose Cholesky factors occupy 37
   // SMs on a latency-bound chain) runs on the main one; joined before step 7
-  static const bool side_on = [] {  // NETMFP_SIDE_STREAM=0: everything on the main stream (A/B)
-    const char *v = getenv("NETMFP_SIDE_STREAM");
-    return !(v && atoi(v) == 0);
-  }();
-  const bool fork = side_on && c.nranks == 1 && !c.comm && !c.ops_on;
+  const bool fork = side_fork(c);
   DBuf<double> Z((size_t)h3 * h3, s), PtQ((size_t)h3 * h2, s);
   SparseSign Pi;
-  if (fork) {
-    if (!c.side) {
-      NM_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
-      NM_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
-      NM_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
-    }
-    NM_CUDA(cudaEventRecord(c.ev_fork, s));
-    NM_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
-    c.stream = c.side;
-  }
   try {
     // step 5: Π
     {
@@ -232,8 +245,7 @@ void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int 
     throw;
   }
   if (fork) {
-    NM_CUDA(cudaEventRecord(c.ev_join, c.side));
-    c.stream = s;
+    side_join_point(c, s);
     Pi.rows.s = s;  // freed after their last use on the main stream
     Pi.signs.s = s;
   }

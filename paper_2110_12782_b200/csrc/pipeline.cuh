@@ -14,7 +14,9 @@ void factor_pair(Ctx &c, const Graph &g, double alpha, int T, const Mat &U, cons
 void sketch_svd(Ctx &c, const Mat &F, const double *C, int k, double scale, int d, int s2, int s3, int z,
                 uint64_t seed, int logmode, const Mat *Uout, double *sigma_dev, const Mat *Eout,
                 const Mat *Yout, double *Zout, int64_t row0 = 0, int64_t n_global = -1,
-                const int32_t *comp_id = nullptr);
+                const int32_t *comp_id = nullptr, const SketchA *preA = nullptr);
+bool side_fork(Ctx &c);
+void side_join_point(Ctx &c, cudaStream_t main);
 void cheb_coeffs(int order, double mu, double theta, double *c);
 void propagate(Ctx &c, const Graph &g, const Mat &E, int order, double mu, double theta);
 }  // namespace netmfp

@@ -714,8 +714,25 @@ static void rows_times(Ctx &c, float *G, int64_t nr, int k, int64_t ldb, const d
 // Y[n × h] = f(scale · F C F(rows)ᵀ) Ψ  (Y mode; Ψ = (rows, signs) with z per column).
 // M̂ = (F C) F_rᵀ = F (F_r Cᵀ)ᵀ: the A operand is F itself and the gathered
 // rows F_r are multiplied by Cᵀ (an h·zp × k × k product) — no n × k F·C block.
+bool sketch_uses_split() { return sketch_f16(); }
+
+void sketch_split_a(Ctx &c, const Mat &F, SketchA &A) {
+  using namespace tcs;
+  A.n = F.rows;
+  A.k = (int)F.cols;
+  A.kp = (int)((A.k + HBK - 1) / HBK * HBK);
+  A.hi.alloc((size_t)A.n * A.kp, c.stream);
+  A.lo.alloc((size_t)A.n * A.kp, c.stream);
+  A.rinv.alloc(A.n, c.stream);
+  if (A.n == 0) return;
+  NM_LAUNCH(c, "split_f16", launch_pdl(c.stream, k_split_f16,
+                                       (unsigned)std::min<int64_t>(ceil_div(A.n, 8), (int64_t)c.num_sms * 16), 256, 0,
+                                       F.p, A.n, A.k, F.ld, A.kp, reinterpret_cast<__half *>(A.hi.p),
+                                       reinterpret_cast<__half *>(A.lo.p), A.rinv.p, nullptr));
+}
+
 void tc_sketch_y(Ctx &c, const Mat &F, const double *C, int64_t ldc, const int32_t *rows, const float *signs,
-                 int64_t h, int z, float scale, int logmode, const Mat &Y, int64_t row0) {
+                 int64_t h, int z, float scale, int logmode, const Mat &Y, int64_t row0, const SketchA *pre) {
   using namespace tcs;
   NM_REQUIRE(Y.rows == F.rows && Y.cols == h, "tc_sketch_y: shapes");
   NM_REQUIRE(z >= 2 && z <= 64, "tc_sketch_y: 2 <= z <= 64");
@@ -742,19 +759,20 @@ void tc_sketch_y(Ctx &c, const Mat &F, const double *C, int64_t ldc, const int32
       gemm_tall(c, Gm, Ct.p, k, k, nullptr, 0.f, Om);
     }
     const int kp = (int)((k + HBK - 1) / HBK * HBK);
-    DBuf<__half> ah((size_t)n * kp, c.stream), al((size_t)n * kp, c.stream);
+    SketchA own;
+    if (!pre) sketch_split_a(c, F, own);
+    const SketchA &A = pre ? *pre : own;
+    NM_REQUIRE(A.n == n && A.k == k && A.kp == kp, "tc_sketch_y: pre-split operand does not match F");
+    const __half *ah = reinterpret_cast<const __half *>(A.hi.p), *al = reinterpret_cast<const __half *>(A.lo.p);
+    const float *rinv = A.rinv.p;
     DBuf<__half> bhh((size_t)ncols * kp, c.stream), blh((size_t)ncols * kp, c.stream);
-    DBuf<float> rinv(n, c.stream);
     DBuf<int> bexp(1, c.stream);
     NM_CUDA(cudaMemsetAsync(bexp.p, 0x80, sizeof(int), c.stream));
     NM_LAUNCH(c, "rows_maxexp", launch_pdl(c.stream, k_rows_maxexp, ceil_div(ncols * k, 256), 256, 0, bt.p, ncols, k,
                                            ldb, bexp.p));
     NM_LAUNCH(c, "split_f16", launch_pdl(c.stream, k_split_f16, ceil_div(ncols, 8), 256, 0, bt.p, ncols, k, ldb, kp,
                                          bhh.p, blh.p, nullptr, bexp.p));
-    NM_LAUNCH(c, "split_f16", launch_pdl(c.stream, k_split_f16,
-                                         (unsigned)std::min<int64_t>(ceil_div(n, 8), (int64_t)c.num_sms * 16), 256, 0,
-                                         F.p, n, k, F.ld, kp, ah.p, al.p, rinv.p, nullptr));
-    CUtensorMap mah = make_map_f16(ah.p, n, kp, kp, 128), mal = make_map_f16(al.p, n, kp, kp, 128);
+    CUtensorMap mah = make_map_f16(ah, n, kp, kp, 128), mal = make_map_f16(al, n, kp, kp, 128);
     CUtensorMap mbh = make_map_f16(bhh.p, ncols, kp, kp, NW), mbl = make_map_f16(blh.p, ncols, kp, kp, NW);
     SkP prm{};
     prm.m = n;
@@ -771,7 +789,7 @@ void tc_sketch_y(Ctx &c, const Mat &F, const double *C, int64_t ldc, const int32
     prm.row_sign = nullptr;
     prm.out = Y.p;
     prm.ldo = Y.ld;
-    launch_sketch_h(c, mah, mal, mbh, mbl, prm, sg.p, rinv.p, bexp.p);
+    launch_sketch_h(c, mah, mal, mbh, mbl, prm, sg.p, rinv, bexp.p);
     return;
   }
   rows_times(c, g.p, ncols, k, ldb, Ct.p, bh.p, bl.p);  // B rows = F_r Cᵀ
