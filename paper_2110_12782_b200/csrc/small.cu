@@ -1069,10 +1069,10 @@ __global__ void k_clusters(const double *__restrict__ w, const double *__restric
   *ncl = c;
 }
 
-// eigenvectors of S: x <- H_0 (H_1 (… H_{l-3} z)); one warp per eigenvector
-// one warp per eigenvector, held in registers (lane owns entries ln + 32 i);
-// the next reflector is prefetched while the current one is applied (Hv rows
-// are zero at k <= j, so no masking below the reflector's support)
+// eigenvectors of S: x <- H_0 (H_1 (… H_{l-3} z)); one warp per eigenvector,
+// held in registers (lane owns entries ln + 32 i); the reflectors two steps
+// ahead are in flight while the current one is applied (Hv rows are zero at
+// k <= j, so no masking below the reflector's support)
 constexpr int BT_NR = 15;  // l <= 480
 constexpr int BT_T = 64;  // 2 warps per block: the l eigenvectors spread over every SM
 __global__ void __launch_bounds__(BT_T) k_backtransform(const double *__restrict__ Hv, const double *__restrict__ hbeta,
@@ -1082,27 +1082,21 @@ __global__ void __launch_bounds__(BT_T) k_backtransform(const double *__restrict
   const int ln = threadIdx.x % 32;
   if (m >= l) return;
   double *xg = Zt + (int64_t)m * l;
-  double x[BT_NR], vn[BT_NR];
+  double x[BT_NR];
 #pragma unroll
   for (int i = 0; i < BT_NR; ++i) {
     const int k = ln + 32 * i;
     x[i] = k < l ? xg[k] : 0.0;
   }
-  auto load = [&](int j) {
+  auto load = [&](double *dst, int j) {
     const double *v = Hv + (int64_t)j * l;
 #pragma unroll
     for (int i = 0; i < BT_NR; ++i) {
       const int k = ln + 32 * i;
-      vn[i] = k < l ? __ldg(v + k) : 0.0;
+      dst[i] = k < l ? __ldg(v + k) : 0.0;
     }
   };
-  if (l >= 3) load(l - 3);
-  for (int j = l - 3; j >= 0; --j) {
-    double v[BT_NR];
-#pragma unroll
-    for (int i = 0; i < BT_NR; ++i) v[i] = vn[i];
-    const double b = __ldg(hbeta + j);
-    if (j > 0) load(j - 1);
+  auto apply = [&](const double *v, double b) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;  // three short chains instead of one of BT_NR
 #pragma unroll
     for (int i = 0; i < BT_NR; i += 3) {
@@ -1113,6 +1107,38 @@ __global__ void __launch_bounds__(BT_T) k_backtransform(const double *__restrict
     const double sacc = warp_sum((s0 + s1) + s2) * b;
 #pragma unroll
     for (int i = 0; i < BT_NR; ++i) x[i] = fma(-sacc, v[i], x[i]);
+  };
+  // reflectors j = l-3 .. 0, two in flight: the loads of reflector j-2 are
+  // issued before reflector j is applied (one step of prefetch left each
+  // step waiting on an L2 round trip)
+  double va[BT_NR], vb[BT_NR], v[BT_NR];
+  double ba = 0.0, bb = 0.0;
+  if (l >= 3) {
+    load(va, l - 3);
+    ba = __ldg(hbeta + l - 3);
+  }
+  if (l >= 4) {
+    load(vb, l - 4);
+    bb = __ldg(hbeta + l - 4);
+  }
+  for (int j = l - 3; j >= 0; j -= 2) {
+#pragma unroll
+    for (int i = 0; i < BT_NR; ++i) v[i] = va[i];
+    double b = ba;
+    if (j >= 2) {
+      load(va, j - 2);
+      ba = __ldg(hbeta + j - 2);
+    }
+    apply(v, b);
+    if (j == 0) break;
+#pragma unroll
+    for (int i = 0; i < BT_NR; ++i) v[i] = vb[i];
+    b = bb;
+    if (j >= 3) {
+      load(vb, j - 3);
+      bb = __ldg(hbeta + j - 3);
+    }
+    apply(v, b);
   }
 #pragma unroll
   for (int i = 0; i < BT_NR; ++i) {
