@@ -65,6 +65,9 @@ def gather_roofline(achieved_tbps):
                 out["access_stream_ceiling_TBps"] = gr["access_stream_ceiling_TBps"]
                 out["frac_of_access_stream_ceiling"] = achieved_tbps / gr["access_stream_ceiling_TBps"]
                 out["access_stream_source"] = gr["access_stream_source"]
+        bu = json.load(open(tp)).get("binding_units")
+        if bu:
+            out["binding_units"] = bu  # ncu unit breakdown of the SpMM and of its gather-only ceiling
     return out
 
 
