@@ -364,9 +364,22 @@ __device__ __forceinline__ int64_t item_of(const GemmP &p, int64_t k) {
   const int64_t q = blockIdx.x + k * gridDim.x;
   if (q >= p.nitems) return -1;
   if (p.order == 0) return q;
-  const int64_t nt = p.nitems / p.nh;
-  return (q % nt) * p.nh + q / nt;
+  const int nt = (int)(p.nitems / p.nh);
+  return (int64_t)((int)q % nt) * p.nh + (int)q / nt;
 }
+// position in an S-slot ring: slot and how many times it was used before
+// (advanced incrementally: a 64-bit g % S / g / S per chunk cost each role
+// a software division on its issue path)
+struct RingPos {
+  int s = 0;
+  int use = 0;
+  __device__ __forceinline__ void next(int S) {
+    if (++s == S) {
+      s = 0;
+      ++use;
+    }
+  }
+};
 __device__ __forceinline__ int part_chunks(const GemmP &p, int h) {
   return (p.tri && p.skip) ? min(p.nk, (min(h * p.hr + p.hr, p.c16) + 31) / 32) : p.nk;
 }
@@ -414,14 +427,14 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmBh);
-      int64_t g = 0;
+      RingPos rg;
       for (int64_t kq = 0, it = item_of(p, 0); it >= 0; ++kq, it = item_of(p, kq)) {
-        const int64_t t = it / p.nh;
-        const int h = (int)(it % p.nh);
+        const int64_t t = (int)it / p.nh;  // items < 2^31
+        const int h = (int)it % p.nh;
         const int nkp = part_chunks(p, h);
-        for (int kc = 0; kc < nkp; ++kc, ++g) {
-          const int s = (int)(g % S);
-          const int64_t use = g / S;
+        for (int kc = 0; kc < nkp; ++kc, rg.next(S)) {
+          const int s = rg.s;
+          const int use = rg.use;
           if (use > 0) {
             TCP_T0();
             mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
@@ -436,9 +449,10 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
     }
   } else if (warp == 1) {
     {  // the whole warp runs the loop (uniform addresses); one elected lane issues
-      int64_t g = 0, ic = 0;
+      RingPos rg, ra;
+      int64_t ic = 0;
       for (int64_t kq = 0, it = item_of(p, 0); it >= 0; ++kq, it = item_of(p, kq), ++ic) {
-        const int h = (int)(it % p.nh);
+        const int h = (int)it % p.nh;
         const int buf = (int)(ic & 1);
         const int64_t use_b = ic >> 1;
         if (use_b > 0) {
@@ -449,9 +463,9 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
         tc_fence_after();
         const int pc0 = h * p.hr, pc1 = min(pc0 + p.hr, p.c16);  // this part's output columns
         const int nkp = part_chunks(p, h);
-        for (int kc = 0; kc < nkp; ++kc, ++g) {
-          const int s = (int)(g % S);
-          const int64_t use = g / S;
+        for (int kc = 0; kc < nkp; ++kc, rg.next(S), ra.next(ST)) {
+          const int s = rg.s;
+          const int use = rg.use;
           {
             TCP_T0();
             mbar_wait(&split[s], (uint32_t)(use & 1));
@@ -460,7 +474,7 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
           tc_fence_after();
           TCP_T0();
           const uint32_t bhi = smem_u32(base + s * stage_bytes) + ABYTES, blo = bhi + bbytes;
-          const int sa = (int)(g % ST);
+          const int sa = ra.s;
           const uint32_t ahi = tA + (uint32_t)(64 * sa), alo = ahi + 32;
           int c0 = pc0;
           if (p.tri) c0 = max(c0, (kc * 32) & ~15);
@@ -513,13 +527,13 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
     const int q = warp & 3;
     const int r = 32 * q + lane;
     const int wt = threadIdx.x - 64;
-    int64_t g = 0;
+    RingPos rg, ra;
     for (int64_t kq = 0, it = item_of(p, 0); it >= 0; ++kq, it = item_of(p, kq)) {
-      const int h = (int)(it % p.nh);
+      const int h = (int)it % p.nh;
       const int nkp = part_chunks(p, h);
-      for (int kc = 0; kc < nkp; ++kc, ++g) {
-        const int s = (int)(g % S);
-        const int64_t use = g / S;
+      for (int kc = 0; kc < nkp; ++kc, rg.next(S), ra.next(ST)) {
+        const int s = rg.s;
+        const int use = rg.use;
         {
           TCP_T0();
           mbar_wait(&full[s], (uint32_t)(use & 1));
@@ -534,8 +548,8 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
         }
 #pragma unroll
         for (int i = 0; i < 32; ++i) lo[i] = hi[i] - tf32_trunc(hi[i]);
-        const int sa = (int)(g % ST);
-        const int64_t ua = g / ST;
+        const int sa = ra.s;
+        const int ua = ra.use;
         if (ua > 0) mbar_wait(&aempty[sa], (uint32_t)((ua - 1) & 1));  // MMAs done with this TMEM stage
         tc_fence_after();
         const uint32_t ta = tA + ((uint32_t)(32 * q) << 16) + (uint32_t)(64 * sa);
@@ -556,8 +570,8 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
     int nst = 0;  // stores issued by this warp (staging buffer = nst & 1)
     int64_t ic = 0;
     for (int64_t kq = 0, it = item_of(p, 0); it >= 0; ++kq, it = item_of(p, kq), ++ic) {
-      const int64_t t = it / p.nh;
-      const int h = (int)(it % p.nh);
+      const int64_t t = (int)it / p.nh;  // items < 2^31
+      const int h = (int)it % p.nh;
       const int buf = (int)(ic & 1);
       {
         TCP_T0();
