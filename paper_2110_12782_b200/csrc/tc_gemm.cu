@@ -86,6 +86,19 @@ struct GramP {
   int exact;            // 1: 3xTF32 (A_hi B_hi + A_hi B_lo + A_lo B_hi); 0: A_hi B_hi only (no lo parts)
 };
 
+// position in an S-slot ring: slot and how many times it was used before
+// (advanced incrementally: a 64-bit g % S / g / S per chunk cost each role
+// a software division on its issue path)
+struct RingPos {
+  int s = 0;
+  int use = 0;
+  __device__ __forceinline__ void next(int S) {
+    if (++s == S) {
+      s = 0;
+      ++use;
+    }
+  }
+};
 template <int BK, bool SYM, bool EXACT>
 __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUtensorMap tmA,
                                                    const __grid_constant__ CUtensorMap tmB, const GramP p) {
@@ -128,8 +141,9 @@ __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUten
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       if (!SYM) tma_prefetch_desc(&tmB);
-      for (int kc = 0; kc < nk; ++kc) {
-        const int s = kc % S, use = kc / S;
+      RingPos rg;
+      for (int kc = 0; kc < nk; ++kc, rg.next(S)) {
+        const int s = rg.s, use = rg.use;
         {
           TCP_T0();
           if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
@@ -152,8 +166,9 @@ __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUten
     }
   } else if (warp == 1) {
     {  // whole warp (uniform addresses), one elected lane issues
-      for (int kc = 0; kc < nk; ++kc) {
-        const int s = kc % S, use = kc / S;
+      RingPos rg;
+      for (int kc = 0; kc < nk; ++kc, rg.next(S)) {
+        const int s = rg.s, use = rg.use;
         {
           TCP_T0();
           mbar_wait(direct ? &full[s] : &split[s], (uint32_t)(use & 1));
@@ -196,8 +211,9 @@ __global__ void __launch_bounds__(NT, 1) k_gram_tc(const __grid_constant__ CUten
     // workers: lo split (+ row weights) for every chunk, then the epilogue
     const int wt = threadIdx.x - 64;  // 0..127
     const int q = warp & 3;
-    for (int kc = 0; kc < (direct ? 0 : nk); ++kc) {
-      const int s = kc % S, use = kc / S;
+    RingPos rg;
+    for (int kc = 0; kc < (direct ? 0 : nk); ++kc, rg.next(S)) {
+      const int s = rg.s, use = rg.use;
       {
         TCP_T0();
         mbar_wait(&full[s], (uint32_t)(use & 1));
@@ -367,19 +383,6 @@ __device__ __forceinline__ int64_t item_of(const GemmP &p, int64_t k) {
   const int nt = (int)(p.nitems / p.nh);
   return (int64_t)((int)q % nt) * p.nh + (int)q / nt;
 }
-// position in an S-slot ring: slot and how many times it was used before
-// (advanced incrementally: a 64-bit g % S / g / S per chunk cost each role
-// a software division on its issue path)
-struct RingPos {
-  int s = 0;
-  int use = 0;
-  __device__ __forceinline__ void next(int S) {
-    if (++s == S) {
-      s = 0;
-      ++use;
-    }
-  }
-};
 __device__ __forceinline__ int part_chunks(const GemmP &p, int h) {
   return (p.tri && p.skip) ? min(p.nk, (min(h * p.hr + p.hr, p.c16) + 31) / 32) : p.nk;
 }
