@@ -21,7 +21,7 @@
     }                                                                                  \
   } while (0)
 
-enum : int { H_COL = 1, H_Y = 2, H_X = 4, H_DET = 8, H_NACOL = 16, H_NAX = 32, H_U8 = 64, H_COOP = 128, H_COOP8 = 256, H_YCS = 512, H_PCG = 1024, H_PAIR = 2048, H_V4 = 4096, H_PF = 8192 };
+enum : int { H_COL = 1, H_Y = 2, H_X = 4, H_DET = 8, H_NACOL = 16, H_NAX = 32, H_U8 = 64, H_COOP = 128, H_COOP8 = 256, H_YCS = 512, H_PCG = 1024, H_PAIR = 2048, H_V4 = 4096, H_PF = 8192, H_REL = 16384 };
 
 struct G {
   const int64_t *rowptr;
@@ -334,9 +334,15 @@ __global__ void __launch_bounds__(256, MINB) k_lab(G g, int nblk_heavy) {
   int32_t *cnt = g.hcnt + h * 4 + py;
   int last = 0;
   if (li == 0) {
-    __threadfence();
-    last = atomicAdd(cnt, 1) == (int)(s1 - s0) - 1;
-    if (last) __threadfence();
+    if (HINT & H_REL) {  // release RMW (MEMBAR, no L1 invalidation); .cg reads need no acquire fence
+      int old;
+      asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+      last = old == (int)(s1 - s0) - 1;
+    } else {
+      __threadfence();
+      last = atomicAdd(cnt, 1) == (int)(s1 - s0) - 1;
+      if (last) __threadfence();
+    }
   }
   last = __shfl_sync(gmask, last, lane / LPR * LPR);
   if (!last) return;
@@ -1024,6 +1030,16 @@ int main(int argc, char **argv) {
       snprintf(nm, sizeof nm, "det 2x128 carveout %d%% smem", cv);
       run(nm, k_lab<32, H_DET>, 32, 2, 256, false);
     }
+    printf("done\n");
+    return 0;
+  }
+  if (getenv("LAB_REL")) {  // heavy-row arrival: release atomic instead of two gpu-scope fences (each flushes L1)
+    run("ref det 2x128", k_lab<32, H_DET>, 32, 2, 256, true, 3);
+    CK(cudaMemcpy(hr.data(), Yref, n * 288 * 4, cudaMemcpyDeviceToHost));
+    run("det 2x128", k_lab<32, H_DET>, 32, 2, 256, false);
+    run("det rel 2x128", k_lab<32, H_DET | H_REL>, 32, 2, 256, false);
+    run("det 2x128 (again)", k_lab<32, H_DET>, 32, 2, 256, false);
+    run("det rel 2x128 (again)", k_lab<32, H_DET | H_REL>, 32, 2, 256, false);
     printf("done\n");
     return 0;
   }
