@@ -43,9 +43,9 @@ namespace cdf {
 constexpr int T = 256;
 constexpr int TL = 33;  // smem tile row stride (doubles)
 
-__device__ __forceinline__ int ld_acquire(const int *p) {
+__device__ __forceinline__ int ld_relaxed(const int *p) {
   int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release(int *p, int v) {
@@ -69,14 +69,17 @@ struct DfP {
 __device__ bool wait_flag(const DfP &p, const int *f, int want, int attempt) {
   __shared__ int ok;
   if (threadIdx.x == 0) {
+    // relaxed polls, one acquire fence once the flag is seen (an acquire
+    // load at gpu scope invalidates the SM's L1 on every poll)
     int r = 1;
-    while (ld_acquire(f) < want) {
-      if (ld_acquire(p.fail) == attempt + 1) {
+    while (ld_relaxed(f) < want) {
+      if (ld_relaxed(p.fail) == attempt + 1) {
         r = 0;
         break;
       }
       __nanosleep(64);
     }
+    asm volatile("fence.acquire.gpu;" ::: "memory");
     ok = r;
   }
   __syncthreads();
@@ -87,10 +90,7 @@ __device__ bool wait_flag(const DfP &p, const int *f, int want, int attempt) {
 
 __device__ void publish(int *f, int v) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    st_release(f, v);
-  }
+  if (threadIdx.x == 0) st_release(f, v);  // cumulative: the CTA's writes ordered by the barrier
 }
 
 // load a 32×32 tile (rows r0.., cols c0.., valid ib×jb, zero padded) bypassing L1
