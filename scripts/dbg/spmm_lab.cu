@@ -21,7 +21,7 @@
     }                                                                                  \
   } while (0)
 
-enum : int { H_COL = 1, H_Y = 2, H_X = 4, H_DET = 8, H_NACOL = 16, H_NAX = 32, H_U8 = 64, H_COOP = 128, H_COOP8 = 256, H_YCS = 512, H_PCG = 1024, H_PAIR = 2048, H_V4 = 4096, H_PF = 8192, H_REL = 16384 };
+enum : int { H_COL = 1, H_Y = 2, H_X = 4, H_DET = 8, H_NACOL = 16, H_NAX = 32, H_U8 = 64, H_COOP = 128, H_COOP8 = 256, H_YCS = 512, H_PCG = 1024, H_PAIR = 2048, H_V4 = 4096, H_PF = 8192, H_REL = 16384, H_COLEF = 32768, H_XEL = 65536 };
 
 struct G {
   const int64_t *rowptr;
@@ -65,6 +65,11 @@ __device__ __forceinline__ int32_t ldcol(const int32_t *p, uint64_t pf) {
     asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
   }
+  if (HINT & H_COLEF) {  // allocate (the next indices of the line hit) but evict first
+    int32_t v;
+    asm volatile("ld.global.nc.L1::evict_first.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+  }
   return __ldg(p);
 }
 // gather of one neighbour row slice: hot -> evict_last, cold -> L1 no_allocate + evict_first
@@ -85,6 +90,12 @@ __device__ __forceinline__ float4 ldx(const float *Xc, uint32_t v, uint32_t ld, 
   if (HINT & H_NAX) {
     float4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(Xc + (uint64_t)(v & 0x7fffffffu) * ld));
+    return r;
+  }
+  if (HINT & H_XEL) {  // X rows: L1 evict_last (hub rows are the reused ones)
+    float4 r;
+    asm volatile("ld.global.nc.L1::evict_last.v4.f32 {%0,%1,%2,%3}, [%4];"
                  : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(Xc + (uint64_t)(v & 0x7fffffffu) * ld));
     return r;
   }
@@ -1040,6 +1051,10 @@ int main(int argc, char **argv) {
     run("det rel 2x128", k_lab<32, H_DET | H_REL>, 32, 2, 256, false);
     run("det 2x128 (again)", k_lab<32, H_DET>, 32, 2, 256, false);
     run("det rel 2x128 (again)", k_lab<32, H_DET | H_REL>, 32, 2, 256, false);
+    run("det rel colEF 2x128", k_lab<32, H_DET | H_REL | H_COLEF>, 32, 2, 256, false);
+    run("det rel xEL 2x128", k_lab<32, H_DET | H_REL | H_XEL>, 32, 2, 256, false);
+    run("det rel colEF xEL 2x128", k_lab<32, H_DET | H_REL | H_COLEF | H_XEL>, 32, 2, 256, false);
+    run("det rel 2x128 (third)", k_lab<32, H_DET | H_REL>, 32, 2, 256, false);
     printf("done\n");
     return 0;
   }
