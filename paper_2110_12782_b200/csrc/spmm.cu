@@ -184,9 +184,11 @@ __global__ void __launch_bounds__(256, MINB) k_spmm_rows(SpmmArgs p, const int64
   }
 }
 
+// epilogue traffic is single-use: streamed (.cs: evict-first) so that it does
+// not displace the gathered neighbour rows from L1 / L2
 __device__ __forceinline__ void store_f4(float *dst, float4 v, int nv) {
   if (nv >= 4) {
-    *reinterpret_cast<float4 *>(dst) = v;
+    __stcs(reinterpret_cast<float4 *>(dst), v);
   } else {
     dst[0] = v.x;
     if (nv > 1) dst[1] = v.y;
@@ -200,9 +202,9 @@ template <bool GEN>
 __device__ __forceinline__ void slice_epilogue(const SpmmArgs &p, int64_t u, int c, float sr, float4 acc) {
   const int nv = (int)p.cols - c;
   float4 pv = make_float4(0.f, 0.f, 0.f, 0.f), a0 = pv;
-  if (GEN && p.prev) pv = *reinterpret_cast<const float4 *>(p.prev + u * p.ldp + c);
+  if (GEN && p.prev) pv = __ldcs(reinterpret_cast<const float4 *>(p.prev + u * p.ldp + c));
   if (GEN && p.acc_out && p.acc_in && p.acc_scale != 0.f)
-    a0 = *reinterpret_cast<const float4 *>(p.acc_in + u * p.ldai + c);
+    a0 = __ldcs(reinterpret_cast<const float4 *>(p.acc_in + u * p.ldai + c));
   float4 y = make_float4(sr * acc.x, sr * acc.y, sr * acc.z, sr * acc.w);
   if (GEN && p.prev) y = f4_fma(p.beta, pv, y);
   if (!GEN || p.Y) store_f4(p.Y + u * p.ldy + c, y, nv);
