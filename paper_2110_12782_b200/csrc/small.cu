@@ -633,6 +633,13 @@ __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
   __syncthreads();
   // reflector of step j from row j (entries j+1..l-1; owner CTA only), pushed
   // with beta_j to every CTA's parity buffer
+  // The reflector's global outputs (Hv row j, d_j, e_j, beta_j) are written
+  // AFTER the owner arrives at S1: the barrier's release waits for every
+  // outstanding store of the CTA, and global stores to L2 pending at the
+  // arrive held the owner (and with it the whole cluster) ~1000 cycles per
+  // step (ncu: ERRBAR).  Each thread keeps the one entry it computed (l <= nt).
+  int hk = -1;
+  double hv = 0.0, h_alpha = 0.0, h_beta = 0.0, h_d = 0.0;
   auto reflector = [&](int j) {
     const int par = j & 1;
     double *v = vbuf + par * l;
@@ -648,21 +655,30 @@ __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
       v0 = x0 - alpha;
       beta = 2.0 / (ss + v0 * v0);
     }
+    hk = -1;
     for (int k = j + 1 + tid; k < l; k += nt) {
       const double val = ss > 0.0 ? (k == j + 1 ? v0 : x[k]) : 0.0;
 #pragma unroll
       for (int r = 0; r < TDC; ++r) cl.map_shared_rank(v, r)[k] = val;
-      Hv[(int64_t)j * l + k] = val;
+      hk = k;
+      hv = val;
     }
     if (tid < TDC) cl.map_shared_rank(xchg, tid)[32 * TDC + par] = beta;
+    h_alpha = alpha;
+    h_beta = beta;
+    h_d = x[j];
+  };
+  auto reflector_out = [&](int j) {  // after the arrive
+    if (hk >= 0) Hv[(int64_t)j * l + hk] = hv;
     if (tid == 0) {
-      dd[j] = x[j];
-      ee[j] = alpha;
-      hbeta[j] = beta;
+      dd[j] = h_d;
+      ee[j] = h_alpha;
+      hbeta[j] = h_beta;
     }
   };
   if (l >= 3 && rank == 0) reflector(0);
   cluster_arrive();  // S1(0)
+  if (l >= 3 && rank == 0) reflector_out(0);
   for (int j = 0; j + 2 < l; ++j) {
     const int par = j & 1;
     const double *v = vbuf + par * l;
@@ -705,6 +721,7 @@ __global__ void __cluster_dims__(TDC, 1, 1) __launch_bounds__(TDT)
       __syncthreads();
       reflector(jn);
       cluster_arrive();  // S1(j+1)
+      reflector_out(jn);
     }
     for (int li = wid; li < nloc; li += nt / 32) {
       const int i = li * TDC + rank;
