@@ -384,7 +384,7 @@ struct Block {
 // rows with more neighbours than light_cap are split across warps in segments
 // of heavy_seg entries (spmm.cu); per graph, NETMFP_LIGHT_CAP / NETMFP_HEAVY_SEG
 constexpr int kLightCapDefault = 64;
-constexpr int kHeavySegDefault = 128;  // (fused SpMM sweep on configs[2]: 32 0.72, 64 0.69, 128 0.67, 256 0.68 ms)
+constexpr int kHeavySegDefault = 256;  // configs[2] SpMM family per embedding: 64 11.94, 96 11.46, 128 11.01-11.18, 192 11.05, 256 10.87-10.96, 384 11.01, 512 11.36 ms (scripts/gpu_ab_seg.sh; 128 was best while every segment fenced L1 away)
 
 struct Graph {
   int64_t n = 0, nnz = 0;  // local rows [row0, row0 + n) and their nonzeros
