@@ -576,6 +576,12 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
       const int64_t t = (int)it / p.nh;  // items < 2^31
       const int h = (int)it % p.nh;
       const int buf = (int)(ic & 1);
+      // the row's degree scale is loaded before waiting for the accumulator
+      // (its global load latency sat on the epilogue's path, ncu)
+      const int64_t r0 = t * 128 + 32 * q;
+      const int64_t row = r0 + lane;
+      float sc = 1.f;
+      if (p.deg && row < p.n) sc = deg_pow_dev(p.deg, row, p.rexp);
       {
         TCP_T0();
         mbar_wait(&done[buf], (uint32_t)((ic >> 1) & 1));
@@ -583,10 +589,6 @@ __global__ void __launch_bounds__(NTG, 1) k_gemm_tc(const __grid_constant__ CUte
       }
       TCP_T0();
       tc_fence_after();
-      const int64_t r0 = t * 128 + 32 * q;
-      const int64_t row = r0 + lane;
-      float sc = 1.f;
-      if (p.deg && row < p.n) sc = deg_pow_dev(p.deg, row, p.rexp);
       const int pc0 = h * p.hr;
       const int nblk = (min(p.hr, p.c16 - pc0) + 31) / 32;  // hr is a multiple of 32
       for (int cb = 0; cb < nblk; ++cb) {
