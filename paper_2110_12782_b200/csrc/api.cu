@@ -105,6 +105,7 @@ struct DevScope {
   }
   ~DevScope() {
     if (std::uncaught_exceptions() > unwinding0) {
+      if (c.side) cudaStreamSynchronize(c.side);  // side-stream work may still use freed buffers
       cudaStreamSynchronize(c.stream);
       cudaGetLastError();
       c.flag_checks.clear();
