@@ -122,3 +122,59 @@ def test_two_ranks_on_one_gpu(tmp_path, split):
     assert cols
     assert _cols_up_to_sign(E, ref["E"], cols) <= 1e-3
     assert _cols_up_to_sign(E, E1, cols) <= 1e-4
+
+
+def _nccl_worker(rank, ws, port, bounds, out_dir):
+    """One rank per GPU over the library's own NCCL communicator (netmfp_dist_init):
+    the row-partitioned path exactly as `bench.py --gpus N` runs it."""
+    import torch.distributed as dist
+    import __graft_entry__ as ge
+    ge.build()
+    from paper_2110_12782_b200 import _lib as L
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=ws)
+    try:
+        torch.cuda.set_device(rank)
+        dev = torch.device(f"cuda:{rank}")
+        uid = [L.netmfp_dist_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx = L.Context(rank)
+        L.netmfp_dist_init(ctx, uid[0], ws, rank)
+        n, s, t = _graph()
+        g = L.netmfp_dist_build_csr(ctx, n, torch.from_numpy(s).to(dev), torch.from_numpy(t).to(dev), bounds)
+        nl = int(bounds[rank + 1] - bounds[rank])
+        E = torch.zeros(nl, 32, dtype=torch.float32, device=dev)[:, :PRM["d"]]
+        sig = torch.zeros(PRM["d"], dtype=torch.float64, device=dev)
+        lam = torch.zeros(PRM["k"], dtype=torch.float64, device=dev)
+        L.netmfp_embed(ctx, g, L.make_params(**PRM), E, sig, lam)
+        torch.cuda.synchronize(dev)
+        np.savez(os.path.join(out_dir, f"n{rank}.npz"), E=E.cpu().numpy(), sig=sig.cpu().numpy(),
+                 lam=lam.cpu().numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="the NCCL row-partitioned path needs two GPUs (one rank per GPU)")
+def test_two_ranks_nccl_on_two_gpus(tmp_path):
+    """The library's NCCL communicator with one rank per GPU: oracle parity of
+    Alg. 5 on the row-partitioned graph (replicated λ, σ identical on both
+    ranks; E's separated columns up to sign)."""
+    import torch.multiprocessing as mp
+    n, s, t = _graph()
+    rp, col, deg = O.build_csr(n, s, t)
+    cost = rp + np.arange(n + 1)
+    bounds = np.array([0, int(np.searchsorted(cost, cost[-1] / 2)), n], dtype=np.int64)
+    mp.start_processes(_nccl_worker, args=(2, _free_port(), bounds, str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    parts = [dict(np.load(os.path.join(tmp_path, f"n{r}.npz"))) for r in range(2)]
+    ref = O.netmf_plus(n, s, t, **PRM)
+    so = ref["sigma"]
+    lead = so >= 1e-2 * so[0]
+    for p in parts:
+        assert np.array_equal(p["lam"], parts[0]["lam"]) and np.array_equal(p["sig"], parts[0]["sig"])
+        assert np.abs(p["lam"] - ref["lam"]).max() <= 1e-3 * abs(ref["lam"][0])
+        assert np.abs(p["sig"] - so)[lead].max() <= 1e-3 * so[0]
+    E = np.concatenate([p["E"] for p in parts], axis=0).astype(np.float64)
+    assert np.all(E[deg == 0] == 0.0)
+    cols = [j for j in range(8) if (j == 0 or so[j - 1] - so[j] > 1e-2 * so[j]) and so[j] - so[j + 1] > 1e-2 * so[j]]
+    assert _cols_up_to_sign(E, ref["E"], cols) <= 1e-3
